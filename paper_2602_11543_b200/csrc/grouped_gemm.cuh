@@ -1,0 +1,240 @@
+// Grouped BF16 GEMM on the sm_100a tensor cores (tcgen05 + TMEM + TMA).
+//
+//   D_g[m, n] = sum_k A[a_row0 + m, k0 + k] * B[b_row0 + n, k0 + k]     (both K-major)
+//
+// for every group g of a device-resident group table. This one kernel carries
+// all dense contractions of the SPES local step:
+//   * expert forward  gate||up  (groups = experts, rows = routed tokens),
+//   * expert forward  down,
+//   * expert backward dH and dX (all routed experts, frozen ones included),
+//   * expert backward dW (owned experts only; K = that expert's routed tokens),
+//   * head forward / dX / dW.
+// Group sizes come from routing counts that live on the device, so the tile
+// space is read from device memory and the launch never syncs with the host.
+//
+// Structure (one CTA per SM, persistent):
+//   warp 0  : TMA producer       (one elected lane)
+//   warp 1  : MMA issuer         (one elected lane, tcgen05.mma cta_group::1, M=128)
+//   warp 2  : TMEM allocator
+//   warps 4-7: epilogue (TMEM lanes 0-127 -> registers -> fused epilogue -> global)
+// Pipelines: STAGES-deep smem ring (full/empty mbarriers) and a 2-deep TMEM
+// accumulator ring (tmem_full/tmem_empty) so the epilogue of tile i overlaps
+// the MMAs of tile i+1.
+#pragma once
+
+#include "sm100_primitives.cuh"
+
+namespace spes_dev {
+
+constexpr int GEMM_BM = 128;
+constexpr int GEMM_BK = 64;  // 64 bf16 = 128 B = one swizzle row
+constexpr int GEMM_THREADS = 256;
+
+struct GemmGroup {
+    int32_t a_row0;      // first row of this group's A tile space
+    int32_t b_row0;      // first row of this group's B tile space
+    int32_t k0;          // K offset (elements) in both A and B
+    int32_t k_len;       // K extent (multiple of 64; 0 => result is zero)
+    int32_t m_tiles;     // tiles of 128 rows
+    int32_t n_tiles;     // tiles of BN columns
+    int32_t tile_start;  // exclusive prefix of m_tiles*n_tiles over groups
+    int32_t tag;         // epilogue-defined (expert id, ...)
+    int64_t out_row0;    // epilogue-defined output row offset
+    int64_t ldo;         // epilogue-defined leading dimension
+    void* out0;          // epilogue-defined outputs
+    void* out1;
+};
+
+template <int BN>
+struct GemmCfg {
+    static constexpr int STAGES = (BN == 256) ? 4 : 6;
+    static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
+    static constexpr int B_BYTES = BN * GEMM_BK * 2;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int TMEM_COLS = 2 * BN;  // two accumulator buffers
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ int find_group(const GemmGroup* __restrict__ groups, int num_groups,
+                                          int tile) {
+    int g = 0;
+    while (g + 1 < num_groups && groups[g + 1].tile_start <= tile) ++g;
+    return g;
+}
+
+// Epi must provide:
+//   __device__ void operator()(const GemmGroup& g, int mt, int nt, int r, uint32_t taddr,
+//                              bool empty) const;
+// r = row within the 128-row tile handled by this thread; taddr = TMEM address of
+// (lane r, column 0) of this tile's accumulator; empty => k_len == 0 (result is 0).
+template <int BN, class Epi>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    grouped_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
+                        const __grid_constant__ CUtensorMap mapB,
+                        const GemmGroup* __restrict__ groups, int num_groups,
+                        const int* __restrict__ total_tiles_ptr, int max_tiles, Epi epi) {
+    using C = GemmCfg<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + C::STAGES;
+    uint64_t* tfull = bars + 2 * C::STAGES;
+    uint64_t* tempty = bars + 2 * C::STAGES + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&mapA);
+        tma_prefetch_desc(&mapB);
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    int total = *total_tiles_ptr;
+    if (total > max_tiles) total = max_tiles;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                const int gi = find_group(groups, num_groups, t);
+                const GemmGroup& g = groups[gi];
+                const int local = t - g.tile_start;
+                const int mt = local / g.n_tiles, nt = local % g.n_tiles;
+                const int arow = g.a_row0 + mt * GEMM_BM;
+                const int brow = g.b_row0 + nt * BN;
+                const int nkb = g.k_len / GEMM_BK;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* sa = smem + stage * C::STAGE_BYTES;
+                    uint8_t* sb = sa + C::A_BYTES;
+                    mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+                    const int kc = g.k0 + kb * GEMM_BK;
+                    tma_load_2d(&mapA, &full[stage], sa, kc, arow);
+                    tma_load_2d(&mapB, &full[stage], sb, kc, brow);
+                    if (++stage == C::STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_bf16_f32(GEMM_BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+                const int gi = find_group(groups, num_groups, t);
+                const int nkb = groups[gi].k_len / GEMM_BK;
+                const int acc = it & 1;
+                const uint32_t acc_phase = (it >> 1) & 1;
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t dtmem = tmem_base + acc * BN;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
+                    const uint32_t sb = sa + C::A_BYTES;
+                    const uint64_t adesc = desc_kmajor_sw128(sa);
+                    const uint64_t bdesc = desc_kmajor_sw128(sb);
+#pragma unroll
+                    for (int k = 0; k < GEMM_BK / 16; ++k) {
+                        // advance 16 elements = 32 B inside the 128 B swizzle row
+                        umma_bf16(dtmem, adesc + 2 * k, bdesc + 2 * k, idesc,
+                                  (kb | k) != 0 ? 1u : 0u);
+                    }
+                    umma_commit(&empty[stage]);
+                    if (++stage == C::STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                if (nkb > 0)
+                    umma_commit(&tfull[acc]);
+                else
+                    mbar_arrive(&tfull[acc]);
+            }
+        }
+    } else if (warp >= 4) {
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int r = q * 32 + lane;
+        int it = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+            const int gi = find_group(groups, num_groups, t);
+            const GemmGroup& g = groups[gi];
+            const int local = t - g.tile_start;
+            const int mt = local / g.n_tiles, nt = local % g.n_tiles;
+            const int acc = it & 1;
+            const uint32_t acc_phase = (it >> 1) & 1;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+            epi(g, mt, nt, r, taddr, g.k_len == 0);
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, C::TMEM_COLS);
+    }
+}
+
+// Load 32 accumulator columns (or zeros for an empty K range) as floats.
+__device__ __forceinline__ void acc_load32(uint32_t taddr, bool empty, float (&v)[32]) {
+    if (empty) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        return;
+    }
+    uint32_t u[32];
+    tmem_ld32(taddr, u);
+    tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(u[i]);
+}
+
+// Plain FP32 store: out0[(out_row0 + mt*128 + r) * ldo + nt*BN + c].
+template <int BN>
+struct EpiStoreF32 {
+    __device__ void operator()(const GemmGroup& g, int mt, int nt, int r, uint32_t taddr,
+                               bool empty) const {
+        float* out = static_cast<float*>(g.out0) +
+                     (g.out_row0 + static_cast<int64_t>(mt) * GEMM_BM + r) * g.ldo +
+                     static_cast<int64_t>(nt) * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+            float v[32];
+            acc_load32(taddr + c, empty, v);
+            float4* dst = reinterpret_cast<float4*>(out + c);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+    }
+};
+
+}  // namespace spes_dev
