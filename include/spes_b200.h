@@ -1,0 +1,201 @@
+/*
+ * spes_b200.h -- C ABI of the B200-native SPES hot path.
+ *
+ * SPES (Sparse Expert Synchronization, arXiv 2602.11543): every node trains the
+ * shared parameters psi plus its owned experts Phi_i, keeps the other experts
+ * frozen, and every H steps synchronizes psi over all nodes and each expert over
+ * its owner set; early rounds additionally blend similar experts (merge warm-up).
+ *
+ * One context = one node = one GPU. All parameters live on the device in the
+ * reference's canonical block order (enumerate_blocks, proj/include/spes/model.hpp:95-111),
+ * so spes_load_params / spes_read_params are plain fp32 copies of that layout.
+ *
+ * Every entry point below names the reference interface it replaces.
+ * Errors: a non-zero spes_status whose class mirrors the reference's exception
+ * type (proj/include/spes/*.hpp); spes_last_error() returns the
+ * message (thread-local).
+ */
+#ifndef SPES_B200_H
+#define SPES_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPES_B200_ABI_VERSION 1
+
+typedef enum {
+    SPES_OK = 0,
+    SPES_INVALID_ARGUMENT = 1, /* std::invalid_argument                       */
+    SPES_OUT_OF_RANGE = 2,     /* std::out_of_range (token id, layer)          */
+    SPES_LOGIC_ERROR = 3,      /* std::logic_error (step on frozen block, tied) */
+    SPES_RUNTIME_ERROR = 4,    /* std::runtime_error (non-finite loss)         */
+    SPES_CUDA_ERROR = 5,       /* device / driver failure                      */
+    SPES_NCCL_ERROR = 6,       /* collective failure                           */
+    SPES_PROTOCOL_ERROR = 7    /* ProtocolError (proj/include/spes/wire.hpp:23-47) */
+} spes_status;
+
+/* ModelConfig + LossCoeffs (proj/include/spes/model.hpp:14-41). */
+typedef struct {
+    int64_t vocab;
+    int64_t hidden;       /* d */
+    int64_t intermediate; /* f */
+    int32_t layers;       /* L */
+    int32_t experts_total;  /* M */
+    int32_t experts_active; /* k */
+    int32_t renormalize_after_topk;
+    int32_t tied_head; /* must be 0: the reference throws logic_error (model.hpp:361) */
+    int32_t _pad;
+    double coeff_ce, coeff_lb, coeff_moe_z, coeff_z; /* defaults 1, 0.01, 0.001, 1e-5 */
+    float rms_eps;                                    /* default 1e-5 */
+    float _pad2;
+} spes_model_cfg;
+
+/* AdamWConfig (proj/include/spes/trainer.hpp:45-51). */
+typedef struct {
+    double lr, beta1, beta2, eps, weight_decay;
+} spes_adamw_cfg;
+
+/* MergeSchedule (proj/include/spes/merging.hpp:14-25). source: 0 Gate, 1 Up, 2 Concat. */
+typedef struct {
+    int32_t warmup_rounds;
+    int32_t interval;
+    double alpha0;
+    int32_t peers;
+    int32_t source;
+} spes_merge_sched;
+
+/* LossBundle (proj/include/spes/model.hpp:376-378). */
+typedef struct {
+    double total, ce, lb, moe_z, z;
+} spes_losses;
+
+/* MergeEvent (proj/include/spes/merging.hpp:97-102); peers: experts_total x peers_k. */
+typedef struct {
+    int32_t layer;
+    int32_t peers_k; /* |Q_j| (identical for every j) */
+    double alpha;
+    double displacement_sq;
+} spes_merge_event;
+
+typedef struct {
+    double psi_bytes_in;    /* bytes received for the shared mean               */
+    double expert_bytes_in; /* bytes received for owner-set means + gather       */
+    double ms;              /* device time of the whole sync (CUDA events)       */
+} spes_sync_stats;
+
+typedef struct spes_ctx spes_ctx;
+
+/* ---- configuration helpers (pure host) ---- */
+
+/* ModelConfig::validate (model.hpp:33-40) plus the B200 tiling constraints. */
+spes_status spes_validate_cfg(const spes_model_cfg* cfg);
+/* sum of numel over enumerate_blocks(cfg) (model.hpp:95-111, 138-149). */
+int64_t spes_param_count(const spes_model_cfg* cfg);
+/* offsets (in floats) of every block in enumerate_blocks order; n_blocks_out may be NULL. */
+spes_status spes_block_offsets(const spes_model_cfg* cfg, int64_t* offsets, int32_t* n_blocks_out);
+/* param_partition (model.hpp:466-477): CSR node -> experts (node_offsets has N+1 entries). */
+spes_status spes_param_partition(const spes_model_cfg* cfg, int32_t n_nodes,
+                                 int32_t* node_offsets, int32_t* experts);
+/* LrSchedule::at (proj/src/experiment.cpp:32-41). */
+double spes_lr_at(double peak, double min_frac, int64_t warmup_steps, int64_t total_steps,
+                  int64_t step);
+/* MergeSchedule::merge_at / alpha_at (merging.hpp:21-33). */
+int32_t spes_merge_at(const spes_merge_sched* s, int32_t round);
+spes_status spes_alpha_at(const spes_merge_sched* s, int32_t round, double* alpha);
+
+/* ---- context ---- */
+
+/* One node. nccl_id: 128-byte ncclUniqueId shared by all nodes (NULL iff n_nodes == 1).
+ * Replaces Worker construction + HELLO/ASSIGN (proj/src/protocol.cpp:109-136, 276-292). */
+spes_status spes_create(const spes_model_cfg* cfg, int32_t node, int32_t n_nodes,
+                        int32_t cuda_device, const void* nccl_id, spes_ctx** out);
+void spes_destroy(spes_ctx* ctx);
+/* ncclGetUniqueId, for the launcher to broadcast (128 bytes). */
+spes_status spes_nccl_unique_id(void* out128);
+
+/* Ownership map, CSR node -> sorted expert ids, identical on every node; any
+ * replication r >= 1 (the reference's param_partition is the r = 1 case).
+ * TrainMask (trainer.hpp:15-30) of this node is derived from it. */
+spes_status spes_set_ownership(spes_ctx* ctx, const int32_t* node_offsets,
+                               const int32_t* experts);
+
+/* Full fp32 parameter vector in enumerate_blocks order (host memory). */
+spes_status spes_load_params(spes_ctx* ctx, const float* host, int64_t n);
+spes_status spes_read_params(spes_ctx* ctx, float* host, int64_t n);
+
+/* Start a local round: fresh MaskedAdamW state (trainer.hpp:151-156) unless carry_state. */
+spes_status spes_round_begin(spes_ctx* ctx, int32_t carry_state);
+
+/* One local step (build_loss + backward + MaskedAdamW::step; trainer.hpp:161-206)
+ * on host tokens B x (S+1). losses may be NULL (then the step does not synchronize).
+ * lr is the already-scheduled learning rate for this step. */
+spes_status spes_local_step(spes_ctx* ctx, const int32_t* tokens, int64_t B, int64_t S,
+                            const spes_adamw_cfg* opt, spes_losses* losses);
+/* Same with device-resident tokens (int32, B x (S+1)). */
+spes_status spes_local_step_device(spes_ctx* ctx, const int32_t* d_tokens, int64_t B, int64_t S,
+                                   const spes_adamw_cfg* opt, spes_losses* losses);
+
+/* local_round (trainer.hpp:143-222): H steps over H host batches laid out
+ * contiguously (H x B x (S+1)); lr[h] per step; per_step[h] receives losses.
+ * Throws runtime_error semantics on a non-finite loss (reports the step). */
+spes_status spes_local_round(spes_ctx* ctx, const int32_t* tokens, int64_t B, int64_t S,
+                             int32_t H, const double* lr, const spes_adamw_cfg* opt,
+                             int32_t carry_state, spes_losses* per_step);
+
+/* Sparse synchronization (Server::aggregate, proj/src/protocol.cpp:197-251):
+ * psi <- fp64 node-order mean over all nodes; each expert <- fp64 mean over its
+ * owner set in ascending node order (== verbatim copy when r = 1); every node
+ * ends with the identical global model. Collective: all nodes must call. */
+spes_status spes_sync(spes_ctx* ctx, spes_sync_stats* stats);
+
+/* merge_model (merging.hpp:138-150) on this node's (global) model. events must
+ * hold `layers` entries and peers `layers * experts_total * peers` ints (either may be NULL).
+ * Returns the number of merged layers in *n_events (0 when the schedule is inactive). */
+spes_status spes_merge(spes_ctx* ctx, const spes_merge_sched* sched, int32_t round0,
+                       spes_merge_event* events, int32_t* peers, int32_t* n_events);
+/* similarity_matrix (merging.hpp:55-82) of one layer, M x M doubles. */
+spes_status spes_similarity(spes_ctx* ctx, int32_t layer, int32_t source, double* sim_out);
+
+/* ---- introspection (tests / benchmarks) ---- */
+
+/* Counters: optimizer-state scalars (2(|psi|+|Phi_i|)), gradient scalars, step count. */
+spes_status spes_counts(spes_ctx* ctx, int64_t* opt_state_scalars, int64_t* grad_scalars,
+                        int64_t* adam_step);
+/* Read a named device buffer of the last step (see DESIGN.md §debug names). */
+spes_status spes_debug_read(spes_ctx* ctx, const char* name, int32_t layer, void* host,
+                            int64_t bytes);
+/* Gradient of the last step, full parameter layout (zeros for frozen blocks). */
+spes_status spes_read_grads(spes_ctx* ctx, float* host, int64_t n);
+/* The CUDA stream all work of this context is issued on (cudaStream_t). */
+void* spes_stream(spes_ctx* ctx);
+/* Number of kernels this context launched since creation. */
+int64_t spes_kernel_launches(spes_ctx* ctx);
+const char* spes_last_error(void);
+
+/* ---- kernel-level entry points for bit-exact parity on identical inputs ---- */
+
+/* Router forward (rmsnorm -> logits -> softmax -> top-k) on host arrays. */
+spes_status spes_kernel_router(const spes_model_cfg* cfg, const float* h, const float* gain,
+                               const float* router, int64_t T, float* normed, float* logits,
+                               float* probs, int32_t* topk_idx, float* topk_w, int32_t* counts,
+                               int32_t* perm, int32_t cuda_device);
+/* MaskedAdamW element update on host arrays (trainer.hpp:85-92); step = optimizer step count. */
+spes_status spes_kernel_adamw(float* theta, const float* grad, float* m, float* v, int64_t n,
+                              const spes_adamw_cfg* opt, int64_t step, int32_t cuda_device);
+/* Owner-set fp64 node-order mean: x is n_owners x n (ascending node order). */
+spes_status spes_kernel_owner_mean(const float* x, int32_t n_owners, int64_t n, float* out,
+                                   int32_t cuda_device);
+/* glibc-compatible expf port evaluated on the device / on the host (variant: 0 auto). */
+spes_status spes_kernel_expf(const float* x, float* y, int64_t n, int32_t cuda_device);
+void spes_host_expf_port(const float* x, float* y, int64_t n, int32_t variant);
+int32_t spes_host_expf_variant(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPES_B200_H */

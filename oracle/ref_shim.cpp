@@ -1,0 +1,321 @@
+// ref_shim.cpp -- C ABI over the UNMODIFIED reference (/root/reference/proj), built
+// by oracle/Makefile into oracle/_ref/libspes_ref.so. TEST INFRASTRUCTURE ONLY:
+// it pins the C restatement (spes_oracle.c) bit-for-bit and is the reference arm
+// / cpu_baseline of bench.py. It calls the reference's own public API; nothing
+// of the reference is copied here.
+#include <cstring>
+#include <span>
+#include <vector>
+
+#include "spes/experiment.hpp"
+#include "spes/merging.hpp"
+#include "spes/model.hpp"
+#include "spes/protocol.hpp"
+#include "spes/trainer.hpp"
+#include "spes/wire.hpp"
+
+#include "../include/spes_b200.h"
+
+using namespace spes;
+
+namespace {
+
+ModelConfig to_cfg(const spes_model_cfg* c) {
+    ModelConfig m;
+    m.vocab = c->vocab;
+    m.hidden = c->hidden;
+    m.intermediate = c->intermediate;
+    m.layers = c->layers;
+    m.experts_total = c->experts_total;
+    m.experts_active = c->experts_active;
+    m.renormalize_after_topk = c->renormalize_after_topk != 0;
+    m.tied_head = c->tied_head != 0;
+    m.loss.ce = c->coeff_ce;
+    m.loss.lb = c->coeff_lb;
+    m.loss.moe_z = c->coeff_moe_z;
+    m.loss.z = c->coeff_z;
+    m.rms_eps = c->rms_eps;
+    return m;
+}
+
+ModelParams from_flat(const ModelConfig& c, const float* flat) {
+    ModelParams p = init_model<float>(c, 0, 0.0);
+    size_t off = 0;
+    for (const auto& b : enumerate_blocks(c)) {
+        Tensor& t = block_tensor(p, b);
+        std::memcpy(t.data.data(), flat + off, t.data.size() * sizeof(float));
+        off += t.data.size();
+    }
+    return p;
+}
+
+void to_flat(const ModelParams& p, float* flat) {
+    size_t off = 0;
+    for (const auto& b : enumerate_blocks(p.config)) {
+        const Tensor& t = block_tensor(p, b);
+        std::memcpy(flat + off, t.data.data(), t.data.size() * sizeof(float));
+        off += t.data.size();
+    }
+}
+
+TrainMask mask_from(const ModelConfig& c, const uint8_t* trainable_expert, int node) {
+    TrainMask m;
+    m.node_id = node;
+    for (int j = 0; j < c.experts_total; ++j)
+        if (trainable_expert[j]) m.owned_experts.push_back(j);
+    return m;
+}
+
+Batch batch_from(const int32_t* tokens, int64_t B, int64_t S) {
+    Batch b;
+    b.batch = B;
+    b.seq = S;
+    b.tokens.assign(tokens, tokens + B * (S + 1));
+    return b;
+}
+
+}  // namespace
+
+extern "C" {
+
+void ref_set_parallel(int on) { kernels::set_parallel(on != 0); }
+
+int64_t ref_param_count(const spes_model_cfg* c) {
+    auto pc = param_counts(to_cfg(c));
+    return pc.shared + pc.experts_total;
+}
+
+// init_model<float>(cfg, seed, std) (model.hpp:153-173)
+void ref_init_model(const spes_model_cfg* c, uint64_t seed, double init_std, float* out) {
+    to_flat(init_model<float>(to_cfg(c), seed, init_std), out);
+}
+
+// build_loss + backward (model.hpp:252-374); routing of every layer (model.hpp:185-216)
+int ref_forward_backward(const spes_model_cfg* c, const float* params, const int32_t* tokens,
+                         int64_t B, int64_t S, const uint8_t* trainable_expert, float* grads,
+                         double* losses, float* probs, int32_t* topk_idx, float* topk_w) {
+    try {
+        ModelConfig cfg = to_cfg(c);
+        ModelParams p = from_flat(cfg, params);
+        TrainMask mask = mask_from(cfg, trainable_expert, 0);
+        auto lg = build_loss(p, batch_from(tokens, B, S),
+                             [&mask](const BlockDesc& b) { return mask.trainable(b); });
+        losses[0] = lg.g.value(lg.total).data[0];
+        losses[1] = lg.g.value(lg.ce).data[0];
+        losses[2] = lg.g.value(lg.lb).data[0];
+        losses[3] = lg.g.value(lg.moe_z).data[0];
+        losses[4] = lg.g.value(lg.z).data[0];
+        lg.g.backward(lg.total);
+        auto blocks = enumerate_blocks(cfg);
+        size_t off = 0;
+        for (size_t i = 0; i < blocks.size(); ++i) {
+            Tensor g = lg.g.grad(lg.block_leaves[i]);
+            std::memcpy(grads + off, g.data.data(), g.data.size() * sizeof(float));
+            off += g.data.size();
+        }
+        const int64_t T = B * S;
+        const int M = cfg.experts_total, k = cfg.experts_active;
+        for (size_t l = 0; l < lg.routing.size(); ++l) {
+            const auto& rd = lg.routing[l];
+            if (probs) std::memcpy(probs + l * T * M, rd.probs.data.data(), T * M * sizeof(float));
+            for (int64_t t = 0; t < T; ++t)
+                for (int s = 0; s < k; ++s) {
+                    if (topk_idx) topk_idx[(l * T + t) * k + s] = rd.selected[t][s];
+                    if (topk_w) topk_w[(l * T + t) * k + s] = rd.weights[t][s];
+                }
+        }
+        return 0;
+    } catch (const std::out_of_range&) {
+        return 2;
+    } catch (...) {
+        return 1;
+    }
+}
+
+// local_round (trainer.hpp:143-222) with a fresh MaskedAdamW and per-step lr.
+int ref_local_round(const spes_model_cfg* c, float* params, const int32_t* tokens, int64_t B,
+                    int64_t S, int32_t H, const double* lr, const spes_adamw_cfg* opt,
+                    const uint8_t* trainable_expert, double* losses) {
+    try {
+        ModelConfig cfg = to_cfg(c);
+        ModelParams p = from_flat(cfg, params);
+        TrainMask mask = mask_from(cfg, trainable_expert, 0);
+        int draw = 0;
+        BatchProvider next = [&]() {
+            return batch_from(tokens + static_cast<int64_t>(draw++) * B * (S + 1), B, S);
+        };
+        LocalRoundConfig rc;
+        rc.steps = H;
+        rc.opt.lr = opt->lr;
+        rc.opt.beta1 = opt->beta1;
+        rc.opt.beta2 = opt->beta2;
+        rc.opt.eps = opt->eps;
+        rc.opt.weight_decay = opt->weight_decay;
+        if (lr) rc.lr_at = [lr](int64_t s) { return lr[s]; };
+        rc.first_step = 0;
+        auto res = local_round(p, next, rc, mask);
+        for (size_t h = 0; h < res.step_losses.size(); ++h) {
+            losses[5 * h + 0] = res.step_losses[h].total;
+            losses[5 * h + 1] = res.step_losses[h].ce;
+            losses[5 * h + 2] = res.step_losses[h].lb;
+            losses[5 * h + 3] = res.step_losses[h].moe_z;
+            losses[5 * h + 4] = res.step_losses[h].z;
+        }
+        to_flat(res.params, params);
+        return 0;
+    } catch (const std::out_of_range&) {
+        return 2;
+    } catch (const std::runtime_error&) {
+        return 3;
+    } catch (...) {
+        return 1;
+    }
+}
+
+// Server::aggregate through the reference's public protocol API (protocol.cpp:56-251):
+// HELLO from every node, then each node's LocalUpdate with sparse_update_blocks under
+// param_partition ownership. Result: the server's global model after round 1.
+int ref_aggregate_partition(const spes_model_cfg* c, int32_t N, const float* node_params,
+                            const float* global_in, float* global_out) {
+    try {
+        SyncConfig sc;
+        sc.model = to_cfg(c);
+        sc.nodes = N;
+        sc.rounds = 1;
+        sc.config_hash = 0;
+        sc.merge.warmup_rounds = 0;
+        ModelParams init = from_flat(sc.model, global_in);
+        Server s(sc, init);
+        auto part = param_partition(sc.model, N);
+        auto frame = [](MsgKind kind, uint32_t round, std::vector<uint8_t> payload) {
+            WireMessage m;
+            m.kind = kind;
+            m.round = round;
+            m.payload = std::move(payload);
+            return encode_message(m);
+        };
+        for (int n = 0; n < N; ++n) {
+            HelloPayload h;
+            h.node_id = static_cast<uint32_t>(n);
+            h.config_hash = 0;
+            auto bytes = frame(MsgKind::Hello, 0, encode_hello(h));
+            s.on_bytes(n, bytes);
+        }
+        const int64_t P = ref_param_count(c);
+        for (int n = 0; n < N; ++n) {
+            ModelParams local = from_flat(sc.model, node_params + static_cast<int64_t>(n) * P);
+            TrainMask m;
+            m.node_id = n;
+            m.owned_experts = part[static_cast<size_t>(n)];
+            auto bytes = frame(MsgKind::LocalUpdate, 1, encode_blocks(sparse_update_blocks(local, m)));
+            s.on_bytes(n, bytes);
+        }
+        to_flat(s.global(), global_out);
+        return 0;
+    } catch (...) {
+        return 1;
+    }
+}
+
+void ref_similarity(const spes_model_cfg* c, const float* params, int32_t layer, int32_t source,
+                    double* sim) {
+    ModelConfig cfg = to_cfg(c);
+    ModelParams p = from_flat(cfg, params);
+    auto s = similarity_matrix(p.experts[static_cast<size_t>(layer)],
+                               static_cast<SimilaritySource>(source));
+    std::memcpy(sim, s.a.data(), s.a.size() * sizeof(double));
+}
+
+int32_t ref_select_peers(const double* sim, int32_t M, int32_t j, int32_t K, int32_t* peers) {
+    SimilarityMatrix s;
+    s.experts = M;
+    s.a.assign(sim, sim + static_cast<int64_t>(M) * M);
+    auto v = select_peers(s, j, K);
+    for (size_t i = 0; i < v.size(); ++i) peers[i] = v[i];
+    return static_cast<int32_t>(v.size());
+}
+
+int32_t ref_merge_model(const spes_model_cfg* c, float* params, const spes_merge_sched* sch,
+                        int32_t round, spes_merge_event* events, int32_t* peers) {
+    ModelConfig cfg = to_cfg(c);
+    ModelParams p = from_flat(cfg, params);
+    MergeSchedule s;
+    s.warmup_rounds = sch->warmup_rounds;
+    s.interval = sch->interval;
+    s.alpha0 = sch->alpha0;
+    s.peers = sch->peers;
+    s.source = static_cast<SimilaritySource>(sch->source);
+    auto evs = merge_model(p, s, round);
+    for (size_t l = 0; l < evs.size(); ++l) {
+        if (events) {
+            events[l].layer = evs[l].layer;
+            events[l].alpha = evs[l].alpha;
+            events[l].displacement_sq = evs[l].displacement_sq;
+            events[l].peers_k = evs[l].peer_sets.empty() ? 0 : (int32_t)evs[l].peer_sets[0].size();
+        }
+        if (peers) {
+            int32_t K = evs[l].peer_sets.empty() ? 0 : (int32_t)evs[l].peer_sets[0].size();
+            for (int j = 0; j < cfg.experts_total; ++j)
+                for (int q = 0; q < K; ++q)
+                    peers[(l * cfg.experts_total + j) * K + q] = evs[l].peer_sets[j][q];
+        }
+    }
+    to_flat(p, params);
+    return static_cast<int32_t>(evs.size());
+}
+
+// One MaskedAdamW step from a fresh state (trainer.hpp:56-94).
+int ref_adamw_first_step(const spes_model_cfg* c, float* params, const float* grads,
+                         const uint8_t* trainable_expert, const spes_adamw_cfg* opt) {
+    try {
+        ModelConfig cfg = to_cfg(c);
+        ModelParams p = from_flat(cfg, params);
+        TrainMask mask = mask_from(cfg, trainable_expert, 0);
+        MaskedAdamW o(cfg, mask);
+        AdamWConfig ac;
+        ac.lr = opt->lr;
+        ac.beta1 = opt->beta1;
+        ac.beta2 = opt->beta2;
+        ac.eps = opt->eps;
+        ac.weight_decay = opt->weight_decay;
+        std::vector<GradBlock> gb;
+        auto blocks = enumerate_blocks(cfg);
+        size_t off = 0;
+        for (size_t i = 0; i < blocks.size(); ++i) {
+            int64_t n = Tensor::numel_of(blocks[i].shape);
+            if (mask.trainable(blocks[i]))
+                gb.push_back({i, Tensor(blocks[i].shape,
+                                        std::vector<float>(grads + off, grads + off + n))});
+            off += n;
+        }
+        o.step(p, gb, ac);
+        to_flat(p, params);
+        return 0;
+    } catch (const std::logic_error&) {
+        return 3;
+    } catch (...) {
+        return 1;
+    }
+}
+
+double ref_lr_at(double peak, double min_frac, int64_t warmup, int64_t total, int64_t step) {
+    LrSchedule s;
+    s.peak = peak;
+    s.min_frac = min_frac;
+    s.warmup_steps = warmup;
+    s.total_steps = total;
+    return s.at(step);
+}
+
+void ref_param_partition(const spes_model_cfg* c, int32_t N, int32_t* node_offsets,
+                         int32_t* experts) {
+    auto part = param_partition(to_cfg(c), N);
+    int32_t q = 0;
+    node_offsets[0] = 0;
+    for (int n = 0; n < N; ++n) {
+        for (int e : part[static_cast<size_t>(n)]) experts[q++] = e;
+        node_offsets[n + 1] = q;
+    }
+}
+
+}  // extern "C"
