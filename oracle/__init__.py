@@ -80,6 +80,8 @@ def lib():
                                               _f32p, _f64p, C.POINTER(OracleTrace)]
         L.oracle_adamw_step.argtypes = [_cfgp, _f32p, _f32p, _f32p, _f32p, _u8p,
                                         C.POINTER(AdamWCfg), C.c_int64]
+        L.oracle_adamw_array.argtypes = [_f32p, _f32p, _f32p, _f32p, C.c_int64,
+                                         C.POINTER(AdamWCfg), C.c_int64]
         L.oracle_local_round.restype = C.c_int
         L.oracle_local_round.argtypes = [_cfgp, _f32p, _i32p, C.c_int64, C.c_int64, C.c_int32,
                                          _f64n, C.POINTER(AdamWCfg), _u8p, _f64p]

@@ -647,6 +647,15 @@ void oracle_adamw_step(const spes_model_cfg* c, float* P, const float* G, float*
         }
 }
 
+/* Flat-array form of the same element update (for kernel-level parity). */
+void oracle_adamw_array(float* theta, const float* g, float* m, float* v, int64_t n,
+                        const spes_adamw_cfg* o, int64_t step) {
+    float bc1 = 1.f - (float)pow(o->beta1, (double)step);
+    float bc2 = 1.f - (float)pow(o->beta2, (double)step);
+    adamw_range(theta, g, m, v, n, (float)o->lr, (float)o->beta1, (float)o->beta2, (float)o->eps,
+                (float)o->weight_decay, bc1, bc2);
+}
+
 /* ---------------- local_round (trainer.hpp:143-222), AdamW, fresh state ---------------- */
 
 int oracle_local_round(const spes_model_cfg* c, float* P, const int32_t* tokens, int64_t B,

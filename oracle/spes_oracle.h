@@ -61,6 +61,9 @@ void oracle_adamw_step(const spes_model_cfg* c, float* params, const float* grad
                        float* v, const uint8_t* trainable_expert, const spes_adamw_cfg* opt,
                        int64_t step);
 
+void oracle_adamw_array(float* theta, const float* g, float* m, float* v, int64_t n,
+                        const spes_adamw_cfg* opt, int64_t step);
+
 /* local_round (AdamW, fresh state) over H batches; lr[h] per step; losses[H][5].
  * Returns 0, 2 (bad token), or 3 + h when step h has a non-finite loss. */
 int oracle_local_round(const spes_model_cfg* c, float* params, const int32_t* tokens, int64_t B,

@@ -1,0 +1,281 @@
+"""B200-native SPES hot path: Python host mirror over the C ABI (include/spes_b200.h).
+
+The product is libspes_b200.so (C++ host orchestration + sm_100a CUDA kernels +
+NCCL); this module only binds it with ctypes and mirrors the reference's
+operator interface (proj/include/spes/trainer.hpp, merging.hpp, protocol.cpp):
+
+    Node(cfg, node, n_nodes, device, nccl_id)      one SPES node == one GPU
+      .set_ownership(owned_lists)                   ASSIGN / TrainMask (any replication)
+      .load_params / read_params                    enumerate_blocks layout, fp32
+      .local_round(tokens[H,B,S+1], opt, lr, carry) local_round (trainer.hpp:143-222)
+      .local_step(...)                              one build_loss + backward + AdamW step
+      .sync()                                       Server::aggregate (protocol.cpp:197-251)
+      .merge_model(sched, round0)                   merge_model (merging.hpp:138-150)
+
+There is no CPU fallback: if the shared library is missing, loading fails loudly.
+"""
+import ctypes as C
+import os
+
+import numpy as np
+
+from .abi import (CONFIGS, AdamWCfg, Losses, MergeEvent, MergeSched, ModelCfg, SyncStats,
+                  adamw_cfg, merge_sched, model_cfg)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libspes_b200.so")
+
+SPES_OK = 0
+_STATUS = {1: "invalid_argument", 2: "out_of_range", 3: "logic_error", 4: "runtime_error",
+           5: "cuda_error", 6: "nccl_error", 7: "protocol_error"}
+
+
+class SpesError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"[{_STATUS.get(status, status)}] {msg}")
+        self.status = status
+        self.kind = _STATUS.get(status, "error")
+
+
+_lib = None
+
+
+def build():
+    import subprocess
+    subprocess.check_call(["make", "-s", "-C", os.path.join(HERE, "csrc"), "-j4"])
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64, f32p = C.c_void_p, C.c_int32, C.c_int64, C.POINTER(C.c_float)
+        cfgp = C.POINTER(ModelCfg)
+        L.spes_last_error.restype = C.c_char_p
+        L.spes_validate_cfg.argtypes = [cfgp]
+        L.spes_param_count.restype = i64
+        L.spes_param_count.argtypes = [cfgp]
+        L.spes_block_offsets.argtypes = [cfgp, C.POINTER(i64), C.POINTER(i32)]
+        L.spes_param_partition.argtypes = [cfgp, i32, C.POINTER(i32), C.POINTER(i32)]
+        L.spes_lr_at.restype = C.c_double
+        L.spes_lr_at.argtypes = [C.c_double, C.c_double, i64, i64, i64]
+        L.spes_merge_at.restype = i32
+        L.spes_merge_at.argtypes = [C.POINTER(MergeSched), i32]
+        L.spes_alpha_at.argtypes = [C.POINTER(MergeSched), i32, C.POINTER(C.c_double)]
+        L.spes_create.argtypes = [cfgp, i32, i32, i32, vp, C.POINTER(vp)]
+        L.spes_destroy.argtypes = [vp]
+        L.spes_destroy.restype = None
+        L.spes_nccl_unique_id.argtypes = [vp]
+        L.spes_set_ownership.argtypes = [vp, C.POINTER(i32), C.POINTER(i32)]
+        L.spes_load_params.argtypes = [vp, f32p, i64]
+        L.spes_read_params.argtypes = [vp, f32p, i64]
+        L.spes_read_grads.argtypes = [vp, f32p, i64]
+        L.spes_round_begin.argtypes = [vp, i32]
+        L.spes_local_step.argtypes = [vp, C.POINTER(i32), i64, i64, C.POINTER(AdamWCfg),
+                                      C.POINTER(Losses)]
+        L.spes_local_step_device.argtypes = [vp, vp, i64, i64, C.POINTER(AdamWCfg),
+                                             C.POINTER(Losses)]
+        L.spes_local_round.argtypes = [vp, C.POINTER(i32), i64, i64, i32, C.POINTER(C.c_double),
+                                       C.POINTER(AdamWCfg), i32, C.POINTER(Losses)]
+        L.spes_sync.argtypes = [vp, C.POINTER(SyncStats)]
+        L.spes_merge.argtypes = [vp, C.POINTER(MergeSched), i32, C.POINTER(MergeEvent),
+                                 C.POINTER(i32), C.POINTER(i32)]
+        L.spes_similarity.argtypes = [vp, i32, i32, C.POINTER(C.c_double)]
+        L.spes_counts.argtypes = [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]
+        L.spes_debug_read.argtypes = [vp, C.c_char_p, i32, vp, i64]
+        L.spes_stream.restype = vp
+        L.spes_stream.argtypes = [vp]
+        L.spes_kernel_launches.restype = i64
+        L.spes_kernel_launches.argtypes = [vp]
+        L.spes_kernel_router.argtypes = [cfgp, f32p, f32p, f32p, i64, f32p, f32p, f32p,
+                                         C.POINTER(i32), f32p, C.POINTER(i32), C.POINTER(i32), i32]
+        L.spes_kernel_adamw.argtypes = [f32p, f32p, f32p, f32p, i64, C.POINTER(AdamWCfg), i64, i32]
+        L.spes_kernel_owner_mean.argtypes = [f32p, i32, i64, f32p, i32]
+        L.spes_kernel_expf.argtypes = [f32p, f32p, i64, i32]
+        L.spes_host_expf_port.argtypes = [f32p, f32p, i64, i32]
+        L.spes_host_expf_port.restype = None
+        L.spes_host_expf_variant.restype = i32
+        _lib = L
+    return _lib
+
+
+def _check(status):
+    if status != SPES_OK:
+        raise SpesError(status, lib().spes_last_error().decode())
+
+
+def _p(a, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+def f32(a):
+    return _p(a, C.c_float)
+
+
+def i32(a):
+    return _p(a, C.c_int32)
+
+
+def param_count(cfg):
+    return lib().spes_param_count(C.byref(cfg))
+
+
+def block_offsets(cfg):
+    n = C.c_int32()
+    _check(lib().spes_block_offsets(C.byref(cfg), None, C.byref(n)))
+    out = np.zeros(n.value, np.int64)
+    _check(lib().spes_block_offsets(C.byref(cfg), _p(out, C.c_int64), None))
+    return out
+
+
+def param_partition(cfg, n):
+    offs = np.zeros(n + 1, np.int32)
+    ex = np.zeros(max(cfg.experts_total, 1), np.int32)
+    _check(lib().spes_param_partition(C.byref(cfg), n, i32(offs), i32(ex)))
+    return [list(ex[offs[i]:offs[i + 1]]) for i in range(n)]
+
+
+def replicated_ownership(M, N, r=2):
+    """node n owns {(s*n + i) mod M, i < E} with s = M/N, E = min(M, r*M/N)."""
+    s = M // N
+    E = min(M, r * M // N)
+    return [sorted({(s * n + i) % M for i in range(E)}) for n in range(N)]
+
+
+def nccl_unique_id():
+    buf = (C.c_char * 128)()
+    _check(lib().spes_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def lr_at(peak, min_frac, warmup, total, step):
+    return lib().spes_lr_at(peak, min_frac, warmup, total, step)
+
+
+class Node:
+    """One SPES node on one GPU."""
+
+    def __init__(self, cfg, node=0, n_nodes=1, device=0, nccl_id=None):
+        self.cfg = cfg
+        self.node, self.n_nodes, self.device = node, n_nodes, device
+        self._ctx = C.c_void_p()
+        idbuf = None
+        if nccl_id is not None:
+            idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+        _check(lib().spes_create(C.byref(cfg), node, n_nodes, device,
+                                 C.cast(idbuf, C.c_void_p) if idbuf is not None else None,
+                                 C.byref(self._ctx)))
+        self.P = param_count(cfg)
+
+    def close(self):
+        if self._ctx:
+            lib().spes_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def ctx(self):
+        return self._ctx
+
+    def set_ownership(self, owned_lists):
+        offs = np.zeros(len(owned_lists) + 1, np.int32)
+        flat = []
+        for n, e in enumerate(owned_lists):
+            flat.extend(sorted(int(x) for x in e))
+            offs[n + 1] = len(flat)
+        arr = np.array(flat if flat else [0], np.int32)
+        _check(lib().spes_set_ownership(self._ctx, i32(offs), i32(arr)))
+
+    def load_params(self, p):
+        p = np.ascontiguousarray(p, np.float32)
+        _check(lib().spes_load_params(self._ctx, f32(p), p.size))
+
+    def read_params(self):
+        out = np.zeros(self.P, np.float32)
+        _check(lib().spes_read_params(self._ctx, f32(out), out.size))
+        return out
+
+    def read_grads(self):
+        out = np.zeros(self.P, np.float32)
+        _check(lib().spes_read_grads(self._ctx, f32(out), out.size))
+        return out
+
+    def round_begin(self, carry_state=False):
+        _check(lib().spes_round_begin(self._ctx, int(carry_state)))
+
+    def local_step(self, tokens, opt=None, want_losses=True):
+        tokens = np.ascontiguousarray(tokens, np.int32)
+        B, S1 = tokens.shape[-2:]
+        lo = Losses()
+        _check(lib().spes_local_step(self._ctx, i32(tokens), B, S1 - 1,
+                                     C.byref(opt or adamw_cfg()),
+                                     C.byref(lo) if want_losses else None))
+        return lo.as_tuple() if want_losses else None
+
+    def local_step_device(self, dev_ptr, B, S, opt=None, want_losses=False):
+        lo = Losses()
+        _check(lib().spes_local_step_device(self._ctx, C.c_void_p(dev_ptr), B, S,
+                                            C.byref(opt or adamw_cfg()),
+                                            C.byref(lo) if want_losses else None))
+        return lo.as_tuple() if want_losses else None
+
+    def local_round(self, tokens, opt=None, lr=None, carry_state=False):
+        """tokens: H x B x (S+1) int32; returns losses [H, 5] (total, ce, lb, moe_z, z)."""
+        tokens = np.ascontiguousarray(tokens, np.int32)
+        H, B, S1 = tokens.shape
+        losses = (Losses * H)()
+        lr_arr = None
+        if lr is not None:
+            lr_arr = np.ascontiguousarray(lr, np.float64)
+        _check(lib().spes_local_round(self._ctx, i32(tokens), B, S1 - 1, H,
+                                      _p(lr_arr, C.c_double) if lr_arr is not None else None,
+                                      C.byref(opt or adamw_cfg()), int(carry_state), losses))
+        return np.array([l.as_tuple() for l in losses])
+
+    def sync(self):
+        st = SyncStats()
+        _check(lib().spes_sync(self._ctx, C.byref(st)))
+        return dict(psi_bytes_in=st.psi_bytes_in, expert_bytes_in=st.expert_bytes_in, ms=st.ms)
+
+    def merge_model(self, sched, round0):
+        L, M = self.cfg.layers, self.cfg.experts_total
+        K = max(1, min(sched.peers, M - 1))
+        ev = (MergeEvent * L)()
+        peers = np.zeros((L, M, K), np.int32)
+        n = C.c_int32()
+        _check(lib().spes_merge(self._ctx, C.byref(sched), round0, ev, i32(peers), C.byref(n)))
+        return [(e.layer, e.peers_k, e.alpha, e.displacement_sq) for e in ev[:n.value]], \
+            peers[:n.value]
+
+    def similarity(self, layer, source=0):
+        M = self.cfg.experts_total
+        out = np.zeros((M, M), np.float64)
+        _check(lib().spes_similarity(self._ctx, layer, source, _p(out, C.c_double)))
+        return out
+
+    def counts(self):
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(lib().spes_counts(self._ctx, C.byref(a), C.byref(b), C.byref(c)))
+        return dict(opt_state_scalars=a.value, grad_scalars=b.value, adam_step=c.value)
+
+    def debug(self, name, layer=0, dtype=np.float32, shape=None, count=None):
+        cfg = self.cfg
+        if count is None:
+            raise ValueError("count required")
+        out = np.zeros(count, dtype)
+        _check(lib().spes_debug_read(self._ctx, name.encode(), layer, out.ctypes.data,
+                                     out.nbytes))
+        return out.reshape(shape) if shape is not None else out
+
+    def stream(self):
+        return lib().spes_stream(self._ctx)
+
+    def kernel_launches(self):
+        return lib().spes_kernel_launches(self._ctx)

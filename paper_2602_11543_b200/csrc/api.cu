@@ -1,0 +1,1331 @@
+// C-ABI implementation: one spes_ctx per node/GPU. Host orchestration in C++,
+// device work in kernels.cu / gemm.cu, collectives through NCCL.
+// Reference interfaces each entry point replaces are listed in include/spes_b200.h.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/spes_b200.h"
+#include "glibc_expf.h"
+#include "kernels.h"
+#include "tmap.hpp"
+
+using spes_dev::GemmGroup;
+using spes_k::bf16;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct SpesError : std::runtime_error {
+    spes_status code;
+    SpesError(spes_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void fail(spes_status c, const std::string& m) { throw SpesError(c, m); }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(SPES_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+void ckn(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) fail(SPES_NCCL_ERROR, std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+template <class F>
+spes_status guard(F&& f) {
+    try {
+        f();
+        return SPES_OK;
+    } catch (const SpesError& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::invalid_argument& e) {
+        g_last_error = e.what();
+        return SPES_INVALID_ARGUMENT;
+    } catch (const std::out_of_range& e) {
+        g_last_error = e.what();
+        return SPES_OUT_OF_RANGE;
+    } catch (const std::logic_error& e) {
+        g_last_error = e.what();
+        return SPES_LOGIC_ERROR;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return SPES_RUNTIME_ERROR;
+    }
+}
+
+// ---- layout (enumerate_blocks, proj/include/spes/model.hpp:95-111) ----
+struct Layout {
+    int64_t V, d, f;
+    int L, M, k;
+    int64_t off_emb() const { return 0; }
+    int64_t off_head() const { return V * d; }
+    int64_t off_norm(int l) const { return 2 * V * d + static_cast<int64_t>(l) * (d + d * M); }
+    int64_t off_router(int l) const { return off_norm(l) + d; }
+    int64_t psi() const { return 2 * V * d + static_cast<int64_t>(L) * (d + d * M); }
+    int64_t per_expert() const { return 3 * d * f; }
+    int64_t off_expert(int l, int j) const {
+        return psi() + (static_cast<int64_t>(l) * M + j) * per_expert();
+    }
+    int64_t total() const { return off_expert(L, 0); }
+};
+
+Layout layout_of(const spes_model_cfg* c) {
+    return Layout{c->vocab, c->hidden, c->intermediate, c->layers, c->experts_total,
+                  c->experts_active};
+}
+
+// ModelConfig::validate (model.hpp:33-40) + B200 tiling constraints.
+void validate_cfg(const spes_model_cfg* c) {
+    if (!c) fail(SPES_INVALID_ARGUMENT, "model config: null");
+    if (c->vocab < 1 || c->hidden < 1 || c->intermediate < 1 || c->layers < 1)
+        throw std::invalid_argument("model config: all dims must be >= 1");
+    if (c->experts_active < 1 || c->experts_active > c->experts_total)
+        throw std::invalid_argument("model config: need 1 <= k <= M");
+    if (c->coeff_ce < 0 || c->coeff_lb < 0 || c->coeff_moe_z < 0 || c->coeff_z < 0)
+        throw std::invalid_argument("model config: loss coefficients must be >= 0");
+    if (c->tied_head) throw std::logic_error("tied head not implemented");
+    if (c->hidden % 128 || c->intermediate % 128 || c->vocab % 128)
+        fail(SPES_INVALID_ARGUMENT,
+             "B200 path: hidden, intermediate and vocab must be multiples of 128 (tcgen05 tiles)");
+    if (c->experts_total > 64 || c->experts_active > 8)
+        fail(SPES_INVALID_ARGUMENT, "B200 path: experts_total <= 64 and experts_active <= 8");
+}
+
+int bn_for(int64_t n) { return (n % 256 == 0) ? 256 : 128; }
+int64_t rup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+struct DevMem {
+    std::vector<void*> ptrs;
+    template <class T>
+    T* alloc(int64_t n) {
+        void* p = nullptr;
+        const size_t bytes = static_cast<size_t>(std::max<int64_t>(n, 1)) * sizeof(T);
+        ck(cudaMalloc(&p, bytes), "cudaMalloc");
+        ck(cudaMemset(p, 0, bytes), "cudaMemset");
+        ptrs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    void release() {
+        for (void* p : ptrs) cudaFree(p);
+        ptrs.clear();
+    }
+    ~DevMem() { release(); }
+};
+
+struct LayerBufs {
+    float *normed, *logits, *probs, *topk_w, *lse_r, *inv_rms, *denom, *y, *row_w, *lb_coeff;
+    int32_t *topk_idx, *chunk_counts, *counts, *pad_off, *slot_row, *row_token, *tiles;
+    GemmGroup* groups;
+    bf16 *xp, *xpT, *gu, *hact, *hactT;
+    int64_t* grad_off;  // device [M]
+    CUtensorMap a_xp, a_hact, a_xpT, a_hactT;
+    CUtensorMap b_w1t, b_w2t, b_w2, b_w1;
+};
+
+}  // namespace
+
+struct spes_ctx {
+    spes_model_cfg cfg;
+    Layout lay;
+    int node = 0, n_nodes = 1, device = 0;
+    int expf_variant = 1;
+    cudaStream_t stream = nullptr;
+    ncclComm_t comm = nullptr;
+    int64_t launches = 0;
+
+    // ownership
+    std::vector<std::vector<int>> node_experts;  // node -> sorted experts
+    std::vector<std::vector<int>> owners;        // expert -> ascending nodes
+    std::vector<uint8_t> owned;                  // this node's mask [M]
+    std::vector<int64_t> grad_off_host;          // [L*M] compact offset or -1
+    int64_t G = 0;                               // compact trainable size
+    std::vector<spes_k::AdamSeg> segs_host;
+
+    DevMem persistent;  // params, shadows, optimizer state
+    float* params = nullptr;
+    bf16 *w1t = nullptr, *w2t = nullptr, *w1 = nullptr, *w2 = nullptr, *headB = nullptr,
+         *headT = nullptr;
+    float *grads = nullptr, *m = nullptr, *v = nullptr;
+    spes_k::AdamSeg* segs = nullptr;
+    int64_t* all_expert_offs = nullptr;     // [L*M] param offsets
+    int64_t* all_shadow_slots = nullptr;    // [L*M] 0..L*M-1
+    int64_t* owned_expert_offs = nullptr;   // [L*|owned|]
+    int64_t* owned_shadow_slots = nullptr;  // [L*|owned|]
+    int n_owned_slots = 0;
+    int64_t* grad_off_dev = nullptr;  // [L*M]
+    int64_t adam_step = 0;
+
+    // activations (sized for T_pad)
+    DevMem act;
+    int64_t T = 0, T_pad = 0, R_cap = 0, B = 0, S = 0;
+    std::vector<float*> h;  // L+1 buffers [T_pad x d]
+    std::vector<LayerBufs> layers;
+    int32_t *tokens = nullptr, *inputs = nullptr, *targets = nullptr, *err = nullptr;
+    bf16 *dyw = nullptr, *dywT = nullptr, *dgu = nullptr, *dguT = nullptr;
+    float *dxp = nullptr, *gw_part = nullptr, *glog = nullptr, *gnormed = nullptr, *gh = nullptr,
+          *nr_partial = nullptr;
+    bf16 *hL = nullptr, *hLT = nullptr, *dlog_bf = nullptr, *dlogT = nullptr;
+    float *head_logits = nullptr, *dlogits = nullptr, *diff = nullptr, *lse_head = nullptr;
+    float *lse_all = nullptr, *probs_all = nullptr, *coeff_all = nullptr;
+    double* d_losses = nullptr;
+    GemmGroup* head_groups = nullptr;  // [3]
+    int32_t* head_tiles = nullptr;     // [3]
+    int head_max[3] = {0, 0, 0};
+    CUtensorMap a_dyw, a_dgu, b_dguT, b_dywT, a_hL, b_headT, a_dlog, b_headB, a_hLT, b_dlogT;
+    int max_tiles[6] = {0, 0, 0, 0, 0, 0};
+
+    // host staging
+    int32_t* h_tokens = nullptr;
+    int64_t h_tokens_cap = 0;
+    double* h_losses = nullptr;
+
+    // sync / merge scratch
+    DevMem scratch;
+    float* psi_stage = nullptr;
+    float* expert_stage = nullptr;
+    int64_t expert_stage_cap = 0;
+    double *gram_partial = nullptr, *sim = nullptr, *coef = nullptr, *disp_partial = nullptr;
+    int32_t* peers_dev = nullptr;
+    int64_t* layer_expert_offs = nullptr;  // [M] scratch
+    int gram_chunks = 0;
+};
+
+namespace {
+
+void set_counter(spes_ctx* c) { spes_k::g_launch_counter = &c->launches; }
+
+void build_ownership_tables(spes_ctx* c) {
+    const Layout& L = c->lay;
+    c->owned.assign(L.M, 0);
+    for (int e : c->node_experts[c->node]) c->owned[e] = 1;
+    c->owners.assign(L.M, {});
+    for (int n = 0; n < c->n_nodes; ++n)
+        for (int e : c->node_experts[n]) c->owners[e].push_back(n);
+    // compact trainable layout: psi, then owned experts (layer-major, ascending)
+    c->grad_off_host.assign(static_cast<size_t>(L.L) * L.M, -1);
+    c->segs_host.clear();
+    c->segs_host.push_back({0, 0, L.psi()});
+    int64_t off = L.psi();
+    std::vector<int64_t> oo, os;
+    for (int l = 0; l < L.L; ++l)
+        for (int j = 0; j < L.M; ++j)
+            if (c->owned[j]) {
+                c->grad_off_host[static_cast<size_t>(l) * L.M + j] = off;
+                c->segs_host.push_back({L.off_expert(l, j), off, L.per_expert()});
+                oo.push_back(L.off_expert(l, j));
+                os.push_back(static_cast<int64_t>(l) * L.M + j);
+                off += L.per_expert();
+            }
+    c->G = off;
+    // (re)allocate grads / moments
+    if (c->grads) {
+        cudaFree(c->grads);
+        cudaFree(c->m);
+        cudaFree(c->v);
+        cudaFree(c->segs);
+        cudaFree(c->owned_expert_offs);
+        cudaFree(c->owned_shadow_slots);
+        auto& P = c->persistent.ptrs;
+        P.erase(std::remove_if(P.begin(), P.end(),
+                               [&](void* p) {
+                                   return p == c->grads || p == c->m || p == c->v ||
+                                          p == c->segs || p == c->owned_expert_offs ||
+                                          p == c->owned_shadow_slots;
+                               }),
+                P.end());
+    }
+    c->grads = c->persistent.alloc<float>(c->G);
+    c->m = c->persistent.alloc<float>(c->G);
+    c->v = c->persistent.alloc<float>(c->G);
+    c->segs = c->persistent.alloc<spes_k::AdamSeg>(static_cast<int64_t>(c->segs_host.size()));
+    ck(cudaMemcpy(c->segs, c->segs_host.data(), sizeof(spes_k::AdamSeg) * c->segs_host.size(),
+                  cudaMemcpyHostToDevice),
+       "segs");
+    c->n_owned_slots = static_cast<int>(oo.size());
+    c->owned_expert_offs = c->persistent.alloc<int64_t>(static_cast<int64_t>(oo.size()));
+    c->owned_shadow_slots = c->persistent.alloc<int64_t>(static_cast<int64_t>(os.size()));
+    if (!oo.empty()) {
+        ck(cudaMemcpy(c->owned_expert_offs, oo.data(), 8 * oo.size(), cudaMemcpyHostToDevice), "oo");
+        ck(cudaMemcpy(c->owned_shadow_slots, os.data(), 8 * os.size(), cudaMemcpyHostToDevice), "os");
+    }
+    ck(cudaMemcpy(c->grad_off_dev, c->grad_off_host.data(), 8 * c->grad_off_host.size(),
+                  cudaMemcpyHostToDevice),
+       "grad_off");
+    c->adam_step = 0;
+}
+
+void refresh_shadows_all(spes_ctx* c) {
+    const Layout& L = c->lay;
+    spes_k::expert_shadows(c->params, c->all_expert_offs, L.L * L.M, c->all_shadow_slots, L.d, L.f,
+                           c->w1t, c->w2t, c->w1, c->w2, c->stream);
+    spes_k::head_shadows(c->params + L.off_head(), L.d, L.V, c->headB, c->headT, c->stream);
+}
+
+void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
+    const int64_t T = B * S;
+    if (T < 1) throw std::invalid_argument("batch: need B*S >= 1");
+    c->B = B;
+    c->S = S;
+    if (T == c->T && c->T_pad > 0) return;
+    const Layout& L = c->lay;
+    c->act.release();
+    c->T = T;
+    c->T_pad = rup(T, 128);
+    c->R_cap = rup(T * L.k + static_cast<int64_t>(L.M) * 128, 128);
+    const int64_t Tp = c->T_pad, R = c->R_cap, d = L.d, f = L.f, V = L.V, M = L.M, k = L.k;
+    DevMem& A = c->act;
+    c->h.assign(L.L + 1, nullptr);
+    for (auto& p : c->h) p = A.alloc<float>(Tp * d);
+    c->tokens = A.alloc<int32_t>(B * (S + 1));
+    c->inputs = A.alloc<int32_t>(Tp);
+    c->targets = A.alloc<int32_t>(Tp);
+    c->err = A.alloc<int32_t>(1);
+    c->layers.assign(L.L, LayerBufs{});
+    const int64_t nchunks = (T + 255) / 256;
+    c->lse_all = A.alloc<float>(L.L * Tp);
+    c->probs_all = A.alloc<float>(L.L * Tp * M);
+    c->coeff_all = A.alloc<float>(L.L * M);
+    for (int l = 0; l < L.L; ++l) {
+        LayerBufs& Y = c->layers[l];
+        Y.normed = A.alloc<float>(Tp * d);
+        Y.logits = A.alloc<float>(Tp * M);
+        Y.probs = c->probs_all + l * Tp * M;
+        Y.topk_w = A.alloc<float>(Tp * k);
+        Y.topk_idx = A.alloc<int32_t>(Tp * k);
+        Y.lse_r = c->lse_all + l * Tp;
+        Y.inv_rms = A.alloc<float>(Tp);
+        Y.denom = A.alloc<float>(Tp);
+        Y.chunk_counts = A.alloc<int32_t>(nchunks * M);
+        Y.counts = A.alloc<int32_t>(M);
+        Y.pad_off = A.alloc<int32_t>(M + 1);
+        Y.lb_coeff = c->coeff_all + l * M;
+        Y.slot_row = A.alloc<int32_t>(Tp * k);
+        Y.row_token = A.alloc<int32_t>(R);
+        Y.row_w = A.alloc<float>(R);
+        Y.groups = A.alloc<GemmGroup>(6 * M);
+        Y.tiles = A.alloc<int32_t>(6);
+        Y.xp = A.alloc<bf16>(R * d);
+        Y.xpT = A.alloc<bf16>(d * R);
+        Y.gu = A.alloc<bf16>(R * 2 * f);
+        Y.hact = A.alloc<bf16>(R * f);
+        Y.hactT = A.alloc<bf16>(f * R);
+        Y.y = A.alloc<float>(R * d);
+        Y.grad_off = c->grad_off_dev + static_cast<int64_t>(l) * M;
+        using spes_host::make_tmap_bf16;
+        Y.a_xp = make_tmap_bf16(Y.xp, R, d, 128);
+        Y.a_hact = make_tmap_bf16(Y.hact, R, f, 128);
+        Y.a_xpT = make_tmap_bf16(Y.xpT, d, R, 128);
+        Y.a_hactT = make_tmap_bf16(Y.hactT, f, R, 128);
+        Y.b_w1t = make_tmap_bf16(c->w1t + static_cast<int64_t>(l) * M * 2 * f * d, M * 2 * f, d, 256);
+        Y.b_w2t = make_tmap_bf16(c->w2t + static_cast<int64_t>(l) * M * d * f, M * d, f, bn_for(d));
+        Y.b_w2 = make_tmap_bf16(c->w2 + static_cast<int64_t>(l) * M * f * d, M * f, d, bn_for(f));
+        Y.b_w1 = make_tmap_bf16(c->w1 + static_cast<int64_t>(l) * M * d * 2 * f, M * d, 2 * f, bn_for(d));
+    }
+    c->dyw = A.alloc<bf16>(R * d);
+    c->dywT = A.alloc<bf16>(d * R);
+    c->dgu = A.alloc<bf16>(R * 2 * f);
+    c->dguT = A.alloc<bf16>(2 * f * R);
+    c->dxp = A.alloc<float>(R * d);
+    c->gw_part = A.alloc<float>(R * (d / 64));
+    c->glog = A.alloc<float>(Tp * M);
+    c->gnormed = A.alloc<float>(Tp * d);
+    c->gh = A.alloc<float>(Tp * d);
+    c->nr_partial = A.alloc<float>(16 * d * (M + 1));
+    c->hL = A.alloc<bf16>(Tp * d);
+    c->hLT = A.alloc<bf16>(d * Tp);
+    c->head_logits = A.alloc<float>(Tp * V);
+    c->dlogits = A.alloc<float>(Tp * V);
+    c->dlog_bf = A.alloc<bf16>(Tp * V);
+    c->dlogT = A.alloc<bf16>(V * Tp);
+    c->diff = A.alloc<float>(Tp);
+    c->lse_head = A.alloc<float>(Tp);
+    c->d_losses = A.alloc<double>(8);
+    c->head_groups = A.alloc<GemmGroup>(3);
+    c->head_tiles = A.alloc<int32_t>(3);
+    using spes_host::make_tmap_bf16;
+    c->a_dyw = make_tmap_bf16(c->dyw, R, d, 128);
+    c->a_dgu = make_tmap_bf16(c->dgu, R, 2 * f, 128);
+    c->b_dguT = make_tmap_bf16(c->dguT, 2 * f, R, 256);
+    c->b_dywT = make_tmap_bf16(c->dywT, d, R, bn_for(d));
+    c->a_hL = make_tmap_bf16(c->hL, Tp, d, 128);
+    c->b_headT = make_tmap_bf16(c->headT, V, d, bn_for(V));
+    c->a_dlog = make_tmap_bf16(c->dlog_bf, Tp, V, 128);
+    c->b_headB = make_tmap_bf16(c->headB, d, V, bn_for(d));
+    c->a_hLT = make_tmap_bf16(c->hLT, d, Tp, 128);
+    c->b_dlogT = make_tmap_bf16(c->dlogT, V, Tp, bn_for(V));
+    // head GEMM groups (static for a given T_pad)
+    GemmGroup hg[3]{};
+    hg[0].k_len = static_cast<int32_t>(d);
+    hg[0].m_tiles = static_cast<int32_t>(Tp / 128);
+    hg[0].n_tiles = static_cast<int32_t>(V / bn_for(V));
+    hg[0].out0 = c->head_logits;
+    hg[0].ldo = V;
+    hg[1].k_len = static_cast<int32_t>(V);
+    hg[1].m_tiles = static_cast<int32_t>(Tp / 128);
+    hg[1].n_tiles = static_cast<int32_t>(d / bn_for(d));
+    hg[1].out0 = c->gh;
+    hg[1].ldo = d;
+    hg[2].k_len = static_cast<int32_t>(Tp);
+    hg[2].m_tiles = static_cast<int32_t>(d / 128);
+    hg[2].n_tiles = static_cast<int32_t>(V / bn_for(V));
+    hg[2].out0 = c->grads + L.off_head();  // psi is first in the compact layout
+    hg[2].ldo = V;
+    int32_t ht[3];
+    for (int i = 0; i < 3; ++i) {
+        ht[i] = hg[i].m_tiles * hg[i].n_tiles;
+        c->head_max[i] = ht[i];
+    }
+    ck(cudaMemcpy(c->head_groups, hg, sizeof(hg), cudaMemcpyHostToDevice), "head groups");
+    ck(cudaMemcpy(c->head_tiles, ht, sizeof(ht), cudaMemcpyHostToDevice), "head tiles");
+    // upper bounds of routed GEMM tile counts
+    const int64_t mt_max = (T * k) / 128 + M;
+    c->max_tiles[0] = static_cast<int>(mt_max * (2 * f / 256));
+    c->max_tiles[1] = static_cast<int>(mt_max * (d / bn_for(d)));
+    c->max_tiles[2] = static_cast<int>(mt_max * (f / bn_for(f)));
+    c->max_tiles[3] = static_cast<int>(mt_max * (d / bn_for(d)));
+    const int64_t no = static_cast<int64_t>(std::count(c->owned.begin(), c->owned.end(), 1));
+    c->max_tiles[4] = static_cast<int>(no * (d / 128) * (2 * f / 256));
+    c->max_tiles[5] = static_cast<int>(no * (f / 128) * (d / bn_for(d)));
+}
+
+// gradient seeds of the reverse tape (model.hpp:365-372): float arithmetic as the reference
+struct Seeds {
+    float inv_T, inv_L, c_ce, c_lb, c_mz, c_z, g_lbsum, g_mzsum, g_s2, g_ssum, g_s;
+};
+Seeds seeds_for(const spes_ctx* c) {
+    Seeds s;
+    volatile float one = 1.f;
+    s.inv_T = one / static_cast<float>(c->T);
+    s.inv_L = one / static_cast<float>(c->lay.L);
+    s.c_ce = static_cast<float>(c->cfg.coeff_ce);
+    s.c_lb = static_cast<float>(c->cfg.coeff_lb);
+    s.c_mz = static_cast<float>(c->cfg.coeff_moe_z);
+    s.c_z = static_cast<float>(c->cfg.coeff_z);
+    const float g_z = s.c_z * one, g_mz = s.c_mz * one, g_lb = s.c_lb * one, g_ce = s.c_ce * one;
+    s.g_lbsum = s.inv_L * g_lb;
+    s.g_mzsum = s.inv_L * g_mz;
+    s.g_s2 = s.inv_T * g_z;
+    s.g_ssum = s.inv_T * g_ce;
+    s.g_s = s.inv_T * s.g_mzsum;
+    return s;
+}
+
+void forward_backward(spes_ctx* c) {
+    const Layout& L = c->lay;
+    cudaStream_t st = c->stream;
+    const int64_t T = c->T, Tp = c->T_pad, R = c->R_cap, d = L.d, f = L.f, V = L.V;
+    const int M = L.M, k = L.k;
+    const Seeds sd = seeds_for(c);
+    float* P = c->params;
+
+    spes_k::embed_gather(P + L.off_emb(), c->tokens, c->B, c->S, d, V, c->h[0], c->inputs,
+                         c->targets, c->err, st);
+    for (int l = 0; l < L.L; ++l) {
+        LayerBufs& Y = c->layers[l];
+        spes_k::router_forward(c->h[l], P + L.off_norm(l), P + L.off_router(l), T, d, M, k,
+                               c->cfg.renormalize_after_topk, c->cfg.rms_eps, c->expf_variant,
+                               Y.normed, Y.logits, Y.probs, Y.topk_idx, Y.topk_w, Y.lse_r,
+                               Y.inv_rms, Y.denom, st);
+        spes_k::RoutePlan rp{Y.chunk_counts, Y.counts, Y.pad_off, Y.lb_coeff, Y.slot_row,
+                             Y.row_token, Y.row_w, Y.groups, Y.tiles};
+        spes_k::GroupBases gb{Y.gu, Y.y, c->dgu, c->dxp, c->grads, Y.grad_off, d, f,
+                              bn_for(d), bn_for(f), bn_for(d), bn_for(d)};
+        spes_k::route_plan(Y.topk_idx, Y.topk_w, T, M, k, R, rp, gb, st);
+        spes_k::gather_rows_bf16(Y.normed, d, Y.row_token, Y.pad_off + M, R, d, Y.xp, Y.xpT, R, st);
+        spes_k::gemm_swiglu(Y.a_xp, Y.b_w1t, Y.groups + 0 * M, M, Y.tiles + 0, c->max_tiles[0],
+                            Y.hact, Y.hactT, R, f, st);
+        spes_k::gemm_store_f32(bn_for(d), Y.a_hact, Y.b_w2t, Y.groups + 1 * M, M, Y.tiles + 1,
+                               c->max_tiles[1], st);
+        spes_k::combine_forward(c->h[l], Y.y, Y.slot_row, Y.topk_idx, Y.topk_w, T, d, k,
+                                c->h[l + 1], st);
+    }
+    // head + CE
+    spes_k::gather_rows_bf16(c->h[L.L], d, nullptr, nullptr, Tp, d, c->hL, c->hLT, Tp, st);
+    spes_k::gemm_store_f32(bn_for(V), c->a_hL, c->b_headT, c->head_groups + 0, 1, c->head_tiles + 0,
+                           c->head_max[0], st);
+    spes_k::head_ce(c->head_logits, c->targets, T, Tp, V, c->expf_variant, sd.g_s2, sd.g_ssum,
+                    c->dlogits, c->diff, c->lse_head, st);
+    spes_k::losses_reduce(c->diff, c->lse_head, c->lse_all, c->probs_all, c->coeff_all, T, Tp,
+                          L.L, M, sd.inv_T, sd.inv_L, sd.c_ce, sd.c_lb, sd.c_mz, sd.c_z,
+                          c->d_losses, st);
+    // ---- backward ----
+    spes_k::gather_rows_bf16(c->dlogits, V, nullptr, nullptr, Tp, V, c->dlog_bf, c->dlogT, Tp, st);
+    spes_k::gemm_store_f32(bn_for(d), c->a_dlog, c->b_headB, c->head_groups + 1, 1,
+                           c->head_tiles + 1, c->head_max[1], st);
+    spes_k::gemm_store_f32(bn_for(V), c->a_hLT, c->b_dlogT, c->head_groups + 2, 1,
+                           c->head_tiles + 2, c->head_max[2], st);
+    for (int l = L.L - 1; l >= 0; --l) {
+        LayerBufs& Y = c->layers[l];
+        spes_k::combine_backward(c->gh, Y.y, Y.row_token, Y.row_w, Y.pad_off + M, R, d, c->dyw,
+                                 c->dywT, c->gw_part, st);
+        spes_k::gemm_dswiglu(bn_for(f), c->a_dyw, Y.b_w2, Y.groups + 2 * M, M, Y.tiles + 2,
+                             c->max_tiles[2], Y.gu, c->dgu, c->dguT, R, f, st);
+        spes_k::gemm_store_f32(bn_for(d), c->a_dgu, Y.b_w1, Y.groups + 3 * M, M, Y.tiles + 3,
+                               c->max_tiles[3], st);
+        if (c->max_tiles[4] > 0) {
+            spes_k::gemm_grad_w1(Y.a_xpT, c->b_dguT, Y.groups + 4 * M, M, Y.tiles + 4,
+                                 c->max_tiles[4], st);
+            spes_k::gemm_store_f32(bn_for(d), Y.a_hactT, c->b_dywT, Y.groups + 5 * M, M,
+                                   Y.tiles + 5, c->max_tiles[5], st);
+        }
+        spes_k::router_backward(c->h[l], P + L.off_norm(l), P + L.off_router(l), Y.probs, Y.lse_r,
+                                Y.inv_rms, Y.denom, Y.topk_idx, Y.slot_row, c->gw_part, c->dxp,
+                                Y.lb_coeff, T, d, M, k, c->cfg.renormalize_after_topk,
+                                sd.g_lbsum, sd.g_s, c->glog, c->gnormed, c->gh, st);
+        spes_k::norm_router_grads(c->h[l], Y.normed, c->gnormed, c->glog, Y.inv_rms, T, d, M,
+                                  c->nr_partial, c->grads + L.off_norm(l),
+                                  c->grads + L.off_router(l), st);
+    }
+    spes_k::embed_grad(c->inputs, c->gh, T, d, V, c->grads + L.off_emb(), st);
+}
+
+void optimizer_step(spes_ctx* c, const spes_adamw_cfg* o) {
+    c->adam_step += 1;
+    // MaskedAdamW::step (trainer.hpp:68-84): bias corrections in double, cast to float
+    const float bc1 = 1.f - static_cast<float>(std::pow(o->beta1, static_cast<double>(c->adam_step)));
+    const float bc2 = 1.f - static_cast<float>(std::pow(o->beta2, static_cast<double>(c->adam_step)));
+    const float b1 = static_cast<float>(o->beta1), b2 = static_cast<float>(o->beta2);
+    volatile float one = 1.f;
+    const float omb1 = one - b1, omb2 = one - b2;
+    spes_k::adamw(c->params, c->grads, c->m, c->v, c->segs, static_cast<int>(c->segs_host.size()),
+                  c->G, static_cast<float>(o->lr), b1, b2, omb1, omb2, static_cast<float>(o->eps),
+                  static_cast<float>(o->weight_decay), bc1, bc2, c->stream);
+    const Layout& L = c->lay;
+    spes_k::expert_shadows(c->params, c->owned_expert_offs, c->n_owned_slots,
+                           c->owned_shadow_slots, L.d, L.f, c->w1t, c->w2t, c->w1, c->w2,
+                           c->stream);
+    spes_k::head_shadows(c->params + L.off_head(), L.d, L.V, c->headB, c->headT, c->stream);
+}
+
+void validate_tokens(const spes_ctx* c, const int32_t* tokens, int64_t n) {
+    for (int64_t i = 0; i < n; ++i)
+        if (tokens[i] < 0 || tokens[i] >= c->lay.V)
+            throw std::out_of_range("batch: token id out of vocabulary");
+}
+
+void upload_tokens(spes_ctx* c, const int32_t* tokens, int64_t n) {
+    if (n > c->h_tokens_cap) {
+        if (c->h_tokens) cudaFreeHost(c->h_tokens);
+        ck(cudaMallocHost(&c->h_tokens, sizeof(int32_t) * n), "cudaMallocHost");
+        c->h_tokens_cap = n;
+    }
+    std::memcpy(c->h_tokens, tokens, sizeof(int32_t) * n);
+    ck(cudaMemcpyAsync(c->tokens, c->h_tokens, sizeof(int32_t) * n, cudaMemcpyHostToDevice,
+                       c->stream),
+       "H2D tokens");
+}
+
+void read_losses(spes_ctx* c, spes_losses* out) {
+    ck(cudaMemcpyAsync(c->h_losses, c->d_losses, sizeof(double) * 5, cudaMemcpyDeviceToHost,
+                       c->stream),
+       "D2H losses");
+    ck(cudaStreamSynchronize(c->stream), "step");
+    out->total = c->h_losses[0];
+    out->ce = c->h_losses[1];
+    out->lb = c->h_losses[2];
+    out->moe_z = c->h_losses[3];
+    out->z = c->h_losses[4];
+}
+
+void check_err_flag(spes_ctx* c) {
+    int32_t e = 0;
+    ck(cudaMemcpyAsync(&e, c->err, 4, cudaMemcpyDeviceToHost, c->stream), "err");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    if (e) {
+        cudaMemsetAsync(c->err, 0, 4, c->stream);
+        throw std::out_of_range("batch: token id out of vocabulary");
+    }
+}
+
+void local_step_impl(spes_ctx* c, int64_t B, int64_t S, const spes_adamw_cfg* opt,
+                     spes_losses* losses) {
+    forward_backward(c);
+    if (losses) {
+        read_losses(c, losses);
+        if (!std::isfinite(losses->total)) return;  // caller reports runtime_error
+    }
+    optimizer_step(c, opt);
+    (void)B;
+    (void)S;
+}
+
+}  // namespace
+
+// ============================ C ABI ============================
+extern "C" {
+
+const char* spes_last_error(void) { return g_last_error.c_str(); }
+
+spes_status spes_validate_cfg(const spes_model_cfg* cfg) {
+    return guard([&] { validate_cfg(cfg); });
+}
+
+int64_t spes_param_count(const spes_model_cfg* cfg) { return layout_of(cfg).total(); }
+
+spes_status spes_block_offsets(const spes_model_cfg* cfg, int64_t* offsets, int32_t* n_out) {
+    return guard([&] {
+        Layout L = layout_of(cfg);
+        std::vector<int64_t> o;
+        o.push_back(L.off_emb());
+        o.push_back(L.off_head());
+        for (int l = 0; l < L.L; ++l) {
+            o.push_back(L.off_norm(l));
+            o.push_back(L.off_router(l));
+        }
+        for (int l = 0; l < L.L; ++l)
+            for (int j = 0; j < L.M; ++j)
+                for (int w = 0; w < 3; ++w) o.push_back(L.off_expert(l, j) + w * L.d * L.f);
+        if (offsets) std::copy(o.begin(), o.end(), offsets);
+        if (n_out) *n_out = static_cast<int32_t>(o.size());
+    });
+}
+
+spes_status spes_param_partition(const spes_model_cfg* cfg, int32_t n, int32_t* node_offsets,
+                                 int32_t* experts) {
+    return guard([&] {
+        const int m = cfg->experts_total;
+        if (n < 1 || n > m) throw std::invalid_argument("partition: need 1 <= N <= M (no empty nodes)");
+        int base = m / n, extra = m % n, next = 0;
+        node_offsets[0] = 0;
+        for (int i = 0; i < n; ++i) {
+            int take = base + (i < extra ? 1 : 0);
+            for (int j = 0; j < take; ++j) experts[next] = next, ++next;
+            node_offsets[i + 1] = next;
+        }
+    });
+}
+
+double spes_lr_at(double peak, double min_frac, int64_t warmup, int64_t total, int64_t step) {
+    if (warmup > 0 && step < warmup) return peak * static_cast<double>(step + 1) / static_cast<double>(warmup);
+    double lo = peak * min_frac;
+    int64_t span = total - warmup;
+    if (span <= 0) return peak;
+    double progress = static_cast<double>(step - warmup) / static_cast<double>(span);
+    progress = std::min(1.0, std::max(0.0, progress));
+    return lo + (peak - lo) * 0.5 * (1.0 + std::cos(M_PI * progress));
+}
+
+int32_t spes_merge_at(const spes_merge_sched* s, int32_t round) {
+    return s->warmup_rounds > 0 && round < s->warmup_rounds && s->interval > 0 &&
+           round % s->interval == 0;
+}
+
+spes_status spes_alpha_at(const spes_merge_sched* s, int32_t round, double* alpha) {
+    return guard([&] {
+        if (round < 0) throw std::invalid_argument("alpha_at: negative round");
+        if (s->warmup_rounds <= 0) {
+            *alpha = 0.0;
+            return;
+        }
+        double frac = 1.0 - static_cast<double>(round) / static_cast<double>(s->warmup_rounds);
+        *alpha = s->alpha0 * std::max(0.0, frac);
+    });
+}
+
+spes_status spes_nccl_unique_id(void* out128) {
+    return guard([&] {
+        ncclUniqueId id;
+        ckn(ncclGetUniqueId(&id), "ncclGetUniqueId");
+        std::memcpy(out128, &id, sizeof(id));
+    });
+}
+
+spes_status spes_create(const spes_model_cfg* cfg, int32_t node, int32_t n_nodes,
+                        int32_t cuda_device, const void* nccl_id, spes_ctx** out) {
+    return guard([&] {
+        validate_cfg(cfg);
+        if (n_nodes < 1 || node < 0 || node >= n_nodes)
+            throw std::invalid_argument("worker: node id out of range");
+        if (n_nodes > 1 && !nccl_id) throw std::invalid_argument("nccl id required when n_nodes > 1");
+        auto c = std::make_unique<spes_ctx>();
+        c->cfg = *cfg;
+        c->lay = layout_of(cfg);
+        c->node = node;
+        c->n_nodes = n_nodes;
+        c->device = cuda_device;
+        ck(cudaSetDevice(cuda_device), "cudaSetDevice");
+        set_counter(c.get());
+        ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+        c->expf_variant = spes_expf::host_variant_from(&expf);
+        spes_k::gemm_prepare(cuda_device);
+        const Layout& L = c->lay;
+        DevMem& P = c->persistent;
+        c->params = P.alloc<float>(L.total());
+        const int64_t slots = static_cast<int64_t>(L.L) * L.M;
+        c->w1t = P.alloc<bf16>(slots * 2 * L.f * L.d);
+        c->w2t = P.alloc<bf16>(slots * L.d * L.f);
+        c->w1 = P.alloc<bf16>(slots * L.d * 2 * L.f);
+        c->w2 = P.alloc<bf16>(slots * L.f * L.d);
+        c->headB = P.alloc<bf16>(L.d * L.V);
+        c->headT = P.alloc<bf16>(L.V * L.d);
+        c->grad_off_dev = P.alloc<int64_t>(slots);
+        c->all_expert_offs = P.alloc<int64_t>(slots);
+        c->all_shadow_slots = P.alloc<int64_t>(slots);
+        std::vector<int64_t> eo(slots), es(slots);
+        for (int l = 0; l < L.L; ++l)
+            for (int j = 0; j < L.M; ++j) {
+                eo[static_cast<size_t>(l) * L.M + j] = L.off_expert(l, j);
+                es[static_cast<size_t>(l) * L.M + j] = static_cast<int64_t>(l) * L.M + j;
+            }
+        ck(cudaMemcpy(c->all_expert_offs, eo.data(), 8 * slots, cudaMemcpyHostToDevice), "eo");
+        ck(cudaMemcpy(c->all_shadow_slots, es.data(), 8 * slots, cudaMemcpyHostToDevice), "es");
+        ck(cudaMallocHost(&c->h_losses, sizeof(double) * 8), "pinned losses");
+        // default ownership: param_partition (model.hpp:466-477) when N <= M, else all
+        c->node_experts.assign(n_nodes, {});
+        if (n_nodes <= L.M) {
+            int base = L.M / n_nodes, extra = L.M % n_nodes, next = 0;
+            for (int i = 0; i < n_nodes; ++i) {
+                int take = base + (i < extra ? 1 : 0);
+                for (int j = 0; j < take; ++j) c->node_experts[i].push_back(next++);
+            }
+        } else {
+            throw std::invalid_argument("partition: need 1 <= N <= M (no empty nodes)");
+        }
+        build_ownership_tables(c.get());
+        if (n_nodes > 1) {
+            ncclUniqueId id;
+            std::memcpy(&id, nccl_id, sizeof(id));
+            ckn(ncclCommInitRank(&c->comm, n_nodes, id, node), "ncclCommInitRank");
+        }
+        *out = c.release();
+    });
+}
+
+void spes_destroy(spes_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->h_tokens) cudaFreeHost(c->h_tokens);
+    if (c->h_losses) cudaFreeHost(c->h_losses);
+    c->act.release();
+    c->scratch.release();
+    c->persistent.release();
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+spes_status spes_set_ownership(spes_ctx* c, const int32_t* node_offsets, const int32_t* experts) {
+    return guard([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        set_counter(c);
+        std::vector<std::vector<int>> ne(c->n_nodes);
+        for (int n = 0; n < c->n_nodes; ++n) {
+            for (int q = node_offsets[n]; q < node_offsets[n + 1]; ++q) {
+                const int e = experts[q];
+                if (e < 0 || e >= c->lay.M)
+                    throw std::invalid_argument("ownership: expert id out of range");
+                if (!ne[n].empty() && e <= ne[n].back())
+                    throw std::invalid_argument("ownership: experts must be sorted and distinct");
+                ne[n].push_back(e);
+            }
+        }
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        c->node_experts = ne;
+        build_ownership_tables(c);
+        // activation buffers embed grad offsets / tile bounds: rebuild on next step
+        c->act.release();
+        c->T = c->T_pad = 0;
+    });
+}
+
+spes_status spes_load_params(spes_ctx* c, const float* host, int64_t n) {
+    return guard([&] {
+        if (n != c->lay.total()) throw std::invalid_argument("load_params: size mismatch");
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        set_counter(c);
+        ck(cudaMemcpyAsync(c->params, host, sizeof(float) * n, cudaMemcpyHostToDevice, c->stream),
+           "H2D params");
+        refresh_shadows_all(c);
+        ck(cudaStreamSynchronize(c->stream), "sync");
+    });
+}
+
+spes_status spes_read_params(spes_ctx* c, float* host, int64_t n) {
+    return guard([&] {
+        if (n != c->lay.total()) throw std::invalid_argument("read_params: size mismatch");
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        ck(cudaMemcpyAsync(host, c->params, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream),
+           "D2H params");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+    });
+}
+
+spes_status spes_round_begin(spes_ctx* c, int32_t carry_state) {
+    return guard([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        if (!carry_state) {
+            // fresh MaskedAdamW (trainer.hpp:151-156): zero moments, step 0
+            ck(cudaMemsetAsync(c->m, 0, sizeof(float) * c->G, c->stream), "m");
+            ck(cudaMemsetAsync(c->v, 0, sizeof(float) * c->G, c->stream), "v");
+            c->adam_step = 0;
+        }
+    });
+}
+
+spes_status spes_local_step(spes_ctx* c, const int32_t* tokens, int64_t B, int64_t S,
+                            const spes_adamw_cfg* opt, spes_losses* losses) {
+    return guard([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        set_counter(c);
+        if (B < 1 || S < 1) throw std::invalid_argument("batch: need B, S >= 1");
+        validate_tokens(c, tokens, B * (S + 1));
+        ensure_activations(c, B, S);
+        upload_tokens(c, tokens, B * (S + 1));
+        local_step_impl(c, B, S, opt, losses);
+        if (losses && !std::isfinite(losses->total))
+            throw std::runtime_error("local_round: non-finite loss at step 0");
+    });
+}
+
+spes_status spes_local_step_device(spes_ctx* c, const int32_t* d_tokens, int64_t B, int64_t S,
+                                   const spes_adamw_cfg* opt, spes_losses* losses) {
+    return guard([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        set_counter(c);
+        if (B < 1 || S < 1) throw std::invalid_argument("batch: need B, S >= 1");
+        ensure_activations(c, B, S);
+        ck(cudaMemcpyAsync(c->tokens, d_tokens, sizeof(int32_t) * B * (S + 1),
+                           cudaMemcpyDeviceToDevice, c->stream),
+           "D2D tokens");
+        local_step_impl(c, B, S, opt, losses);
+        if (losses) {
+            check_err_flag(c);
+            if (!std::isfinite(losses->total))
+                throw std::runtime_error("local_round: non-finite loss at step 0");
+        }
+    });
+}
+
+spes_status spes_local_round(spes_ctx* c, const int32_t* tokens, int64_t B, int64_t S, int32_t H,
+                             const double* lr, const spes_adamw_cfg* opt, int32_t carry_state,
+                             spes_losses* per_step) {
+    return guard([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        set_counter(c);
+        if (H < 1) throw std::invalid_argument("local_round: need H >= 1");
+        if (B < 1 || S < 1) throw std::invalid_argument("batch: need B, S >= 1");
+        const int64_t per = B * (S + 1);
+        if (!carry_state) {
+            ck(cudaMemsetAsync(c->m, 0, sizeof(float) * c->G, c->stream), "m");
+            ck(cudaMemsetAsync(c->v, 0, sizeof(float) * c->G, c->stream), "v");
+            c->adam_step = 0;
+        }
+        ensure_activations(c, B, S);
+        for (int h = 0; h < H; ++h) {
+            const int32_t* tk = tokens + static_cast<int64_t>(h) * per;
+            validate_tokens(c, tk, per);
+            upload_tokens(c, tk, per);
+            spes_adamw_cfg o = *opt;
+            if (lr) o.lr = lr[h];
+            spes_losses tmp;
+            spes_losses* lo = per_step ? &per_step[h] : &tmp;
+            local_step_impl(c, B, S, &o, lo);
+            if (!std::isfinite(lo->total))
+                throw std::runtime_error("local_round: non-finite loss at step " + std::to_string(h));
+        }
+    });
+}
+
+// ---- sync (Server::aggregate, protocol.cpp:197-251) ----
+spes_status spes_sync(spes_ctx* c, spes_sync_stats* stats) {
+    return guard([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        set_counter(c);
+        const Layout& L = c->lay;
+        const int N = c->n_nodes, me = c->node;
+        cudaStream_t st = c->stream;
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+        double psi_in = 0, exp_in = 0;
+        if (N > 1) {
+            const int64_t psi = L.psi();
+            if (!c->psi_stage) c->psi_stage = c->scratch.alloc<float>(psi * N);
+            // psi: every node's copy, then fp64 node-order mean (protocol.cpp:238-243)
+            ckn(ncclAllGather(c->params, c->psi_stage, psi, ncclFloat, c->comm, st), "allgather psi");
+            spes_k::owner_mean_strided(c->psi_stage, N, psi, psi, c->params, st);
+            psi_in = 4.0 * psi * (N - 1);
+            // experts: primary owner per expert
+            const int s_bal = (L.M % N == 0) ? L.M / N : 0;
+            std::vector<int> primary(L.M, -1);
+            bool balanced = s_bal > 0;
+            for (int e = 0; e < L.M; ++e) {
+                const auto& O = c->owners[e];
+                if (O.empty()) {
+                    balanced = false;
+                    continue;
+                }
+                int p = O.front();
+                if (s_bal && std::find(O.begin(), O.end(), e / s_bal) != O.end()) p = e / s_bal;
+                primary[e] = p;
+                if (!s_bal || p != e / s_bal) balanced = false;
+            }
+            const int64_t per = L.per_expert();
+            // staging for co-owner copies received by this primary
+            int64_t need = 0;
+            for (int e = 0; e < L.M; ++e)
+                if (primary[e] == me) need += static_cast<int64_t>(c->owners[e].size() - 1) * per * L.L;
+            if (need > c->expert_stage_cap) {
+                c->expert_stage = c->scratch.alloc<float>(need);
+                c->expert_stage_cap = need;
+            }
+            std::map<std::pair<int, int>, float*> slot;  // (expert*L + l, owner) -> staging
+            int64_t q = 0;
+            ckn(ncclGroupStart(), "group");
+            for (int l = 0; l < L.L; ++l)
+                for (int e = 0; e < L.M; ++e) {
+                    const auto& O = c->owners[e];
+                    if (O.size() < 2) continue;
+                    float* mine = c->params + L.off_expert(l, e);
+                    if (primary[e] == me) {
+                        for (int o : O) {
+                            if (o == me) continue;
+                            float* dst = c->expert_stage + q;
+                            q += per;
+                            slot[{e * L.L + l, o}] = dst;
+                            ckn(ncclRecv(dst, per, ncclFloat, o, c->comm, st), "recv");
+                            exp_in += 4.0 * per;
+                        }
+                    } else if (std::find(O.begin(), O.end(), me) != O.end()) {
+                        ckn(ncclSend(mine, per, ncclFloat, primary[e], c->comm, st), "send");
+                    }
+                }
+            ckn(ncclGroupEnd(), "group end");
+            // owner-set mean at the primary, owners in ascending node order
+            for (int l = 0; l < L.L; ++l)
+                for (int e = 0; e < L.M; ++e) {
+                    const auto& O = c->owners[e];
+                    if (O.size() < 2 || primary[e] != me) continue;
+                    std::vector<const float*> srcs;
+                    float* mine = c->params + L.off_expert(l, e);
+                    for (int o : O) srcs.push_back(o == me ? mine : slot[{e * L.L + l, o}]);
+                    spes_k::owner_mean(srcs.data(), static_cast<int>(srcs.size()), per, mine, st);
+                }
+            // every node receives every expert from its primary
+            if (balanced) {
+                for (int l = 0; l < L.L; ++l) {
+                    float* base = c->params + L.off_expert(l, 0);
+                    const int64_t cnt = per * s_bal;
+                    ckn(ncclAllGather(base + me * cnt, base, cnt, ncclFloat, c->comm, st), "allgather experts");
+                }
+            } else {
+                ckn(ncclGroupStart(), "group");
+                for (int l = 0; l < L.L; ++l)
+                    for (int e = 0; e < L.M; ++e) {
+                        if (primary[e] < 0) continue;
+                        float* p = c->params + L.off_expert(l, e);
+                        ckn(ncclBroadcast(p, p, per, ncclFloat, primary[e], c->comm, st), "bcast");
+                    }
+                ckn(ncclGroupEnd(), "group end");
+            }
+            int64_t mine_primary = 0;
+            for (int e = 0; e < L.M; ++e) mine_primary += primary[e] == me;
+            exp_in += 4.0 * per * L.L * (L.M - mine_primary);
+            refresh_shadows_all(c);
+        }
+        cudaEventRecord(e1, st);
+        ck(cudaStreamSynchronize(st), "sync");
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (stats) {
+            stats->psi_bytes_in = psi_in;
+            stats->expert_bytes_in = exp_in;
+            stats->ms = ms;
+        }
+    });
+}
+
+// ---- merge (merging.hpp:55-150) ----
+namespace {
+
+void layer_sims(spes_ctx* c, int l, int source) {
+    const Layout& L = c->lay;
+    const int M = L.M;
+    const int64_t df = L.d * L.f;
+    if (!c->gram_partial) {
+        c->gram_chunks = 148 * 2;
+        c->gram_partial = c->scratch.alloc<double>(static_cast<int64_t>(c->gram_chunks) * M * (M + 1) / 2);
+        c->sim = c->scratch.alloc<double>(static_cast<int64_t>(M) * M);
+        c->coef = c->scratch.alloc<double>(M);
+        c->disp_partial = c->scratch.alloc<double>(148 * 8);
+        c->peers_dev = c->scratch.alloc<int32_t>(M * M);
+        c->layer_expert_offs = c->scratch.alloc<int64_t>(2 * M);
+    }
+    std::vector<int64_t> vo(M);
+    for (int j = 0; j < M; ++j) vo[j] = L.off_expert(l, j) + (source == 1 ? df : 0);
+    ck(cudaMemcpyAsync(c->layer_expert_offs + M, vo.data(), 8 * M, cudaMemcpyHostToDevice, c->stream), "vo");
+    spes_k::gram_partials(c->params, c->layer_expert_offs + M, M, df, df, source == 2 ? 1 : 0,
+                          c->gram_partial, c->gram_chunks, c->stream);
+    spes_k::gram_finish(c->gram_partial, M, c->gram_chunks, c->sim, c->stream);
+}
+
+// Sequential fp64 similarity row (exact reference order), for near-tie resolution.
+void exact_sim_row(spes_ctx* c, int l, int source, int j, std::vector<double>& row) {
+    const Layout& L = c->lay;
+    const int M = L.M;
+    const int64_t df = L.d * L.f;
+    const int64_t D = source == 2 ? 2 * df : df;
+    std::vector<std::vector<float>> w(M, std::vector<float>(D));
+    for (int e = 0; e < M; ++e) {
+        const int64_t o = L.off_expert(l, e);
+        if (source == 0 || source == 2)
+            ck(cudaMemcpy(w[e].data(), c->params + o, 4 * df, cudaMemcpyDeviceToHost), "D2H");
+        if (source == 1)
+            ck(cudaMemcpy(w[e].data(), c->params + o + df, 4 * df, cudaMemcpyDeviceToHost), "D2H");
+        if (source == 2)
+            ck(cudaMemcpy(w[e].data() + df, c->params + o + df, 4 * df, cudaMemcpyDeviceToHost), "D2H");
+    }
+    std::vector<double> norm(M);
+    for (int e = 0; e < M; ++e) {
+        double n2 = 0.0;
+        for (int64_t i = 0; i < D; ++i) n2 += static_cast<double>(w[e][i]) * static_cast<double>(w[e][i]);
+        norm[e] = std::sqrt(n2);
+    }
+    row.assign(M, 0.0);
+    for (int e = 0; e < M; ++e) {
+        double v = 0.0;
+        if (norm[j] > 0.0 && norm[e] > 0.0) {
+            double dot = 0.0;
+            const int a = std::min(j, e), b = std::max(j, e);
+            for (int64_t i = 0; i < D; ++i) dot += static_cast<double>(w[a][i]) * static_cast<double>(w[b][i]);
+            v = dot / (norm[a] * norm[b]);
+        }
+        row[e] = v;
+    }
+}
+
+// select_peers (merging.hpp:85-95): stable descending, K, ascending
+std::vector<int> select_peers_host(const double* sim_row, int M, int j, int K) {
+    std::vector<int> idx;
+    for (int i = 0; i < M; ++i)
+        if (i != j) idx.push_back(i);
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return sim_row[a] > sim_row[b]; });
+    if (static_cast<int>(idx.size()) > K) idx.resize(K);
+    std::sort(idx.begin(), idx.end());
+    return idx;
+}
+
+bool near_tie_at_boundary(const double* sim_row, int M, int j, int K) {
+    std::vector<double> v;
+    for (int i = 0; i < M; ++i)
+        if (i != j) v.push_back(sim_row[i]);
+    if (static_cast<int>(v.size()) <= K) return false;
+    std::sort(v.begin(), v.end(), std::greater<double>());
+    const double a = v[K - 1], b = v[K];
+    return std::fabs(a - b) <= 1e-9 * std::max(1.0, std::max(std::fabs(a), std::fabs(b)));
+}
+
+}  // namespace
+
+spes_status spes_similarity(spes_ctx* c, int32_t layer, int32_t source, double* sim_out) {
+    return guard([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        set_counter(c);
+        if (c->lay.M < 2) throw std::invalid_argument("similarity_matrix: need M >= 2");
+        if (layer < 0 || layer >= c->lay.L) throw std::out_of_range("similarity: bad layer");
+        layer_sims(c, layer, source);
+        ck(cudaMemcpyAsync(sim_out, c->sim, 8 * c->lay.M * c->lay.M, cudaMemcpyDeviceToHost, c->stream), "D2H sim");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+    });
+}
+
+spes_status spes_merge(spes_ctx* c, const spes_merge_sched* sched, int32_t round0,
+                       spes_merge_event* events, int32_t* peers_out, int32_t* n_events) {
+    return guard([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        set_counter(c);
+        if (n_events) *n_events = 0;
+        if (!spes_merge_at(sched, round0)) return;
+        double alpha = 0.0;
+        {
+            spes_status s = spes_alpha_at(sched, round0, &alpha);
+            if (s != SPES_OK) throw std::invalid_argument(g_last_error);
+        }
+        if (alpha <= 0.0) return;
+        const Layout& L = c->lay;
+        const int M = L.M;
+        if (M < 2) throw std::invalid_argument("similarity_matrix: need M >= 2");
+        const int K = std::min(sched->peers, M - 1);
+        if (K < 1) throw std::invalid_argument("select_peers: need K >= 1");
+        std::vector<double> sim(static_cast<size_t>(M) * M);
+        for (int l = 0; l < L.L; ++l) {
+            layer_sims(c, l, sched->source);
+            ck(cudaMemcpyAsync(sim.data(), c->sim, 8 * M * M, cudaMemcpyDeviceToHost, c->stream), "D2H sim");
+            ck(cudaStreamSynchronize(c->stream), "sync");
+            std::vector<int32_t> peers(static_cast<size_t>(M) * K);
+            std::vector<double> coef(M);
+            for (int j = 0; j < M; ++j) {
+                const double* row = sim.data() + static_cast<size_t>(j) * M;
+                std::vector<double> exact;
+                if (near_tie_at_boundary(row, M, j, K)) {
+                    exact_sim_row(c, l, sched->source, j, exact);
+                    row = exact.data();
+                }
+                auto p = select_peers_host(row, M, j, K);
+                for (int q = 0; q < K; ++q) peers[static_cast<size_t>(j) * K + q] = p[q];
+                coef[j] = alpha / static_cast<double>(p.size());
+            }
+            std::vector<int64_t> eo(M);
+            for (int j = 0; j < M; ++j) eo[j] = L.off_expert(l, j);
+            ck(cudaMemcpyAsync(c->peers_dev, peers.data(), 4 * M * K, cudaMemcpyHostToDevice, c->stream), "peers");
+            ck(cudaMemcpyAsync(c->coef, coef.data(), 8 * M, cudaMemcpyHostToDevice, c->stream), "coef");
+            ck(cudaMemcpyAsync(c->layer_expert_offs, eo.data(), 8 * M, cudaMemcpyHostToDevice, c->stream), "eo");
+            const int nblocks = 148 * 4;
+            spes_k::merge_apply(c->params, c->layer_expert_offs, M, L.per_expert(), c->peers_dev, K,
+                                c->coef, c->disp_partial, nblocks, c->stream);
+            std::vector<double> dp(nblocks);
+            ck(cudaMemcpyAsync(dp.data(), c->disp_partial, 8 * nblocks, cudaMemcpyDeviceToHost, c->stream), "disp");
+            ck(cudaStreamSynchronize(c->stream), "sync");
+            double disp = 0.0;
+            for (double x : dp) disp += x;
+            if (events) {
+                events[l].layer = l;
+                events[l].peers_k = K;
+                events[l].alpha = alpha;
+                events[l].displacement_sq = disp;
+            }
+            if (peers_out)
+                std::memcpy(peers_out + static_cast<size_t>(l) * M * K, peers.data(), 4 * M * K);
+        }
+        refresh_shadows_all(c);
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        if (n_events) *n_events = L.L;
+    });
+}
+
+spes_status spes_counts(spes_ctx* c, int64_t* opt_state, int64_t* grad_scalars, int64_t* step) {
+    return guard([&] {
+        if (opt_state) *opt_state = 2 * c->G;
+        if (grad_scalars) *grad_scalars = c->G;
+        if (step) *step = c->adam_step;
+    });
+}
+
+spes_status spes_read_grads(spes_ctx* c, float* host, int64_t n) {
+    return guard([&] {
+        if (n != c->lay.total()) throw std::invalid_argument("read_grads: size mismatch");
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        std::vector<float> comp(c->G);
+        ck(cudaMemcpyAsync(comp.data(), c->grads, 4 * c->G, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        std::memset(host, 0, 4 * n);
+        for (const auto& s : c->segs_host)
+            std::memcpy(host + s.param_off, comp.data() + s.comp_off, 4 * s.len);
+    });
+}
+
+spes_status spes_debug_read(spes_ctx* c, const char* name, int32_t layer, void* host,
+                            int64_t bytes) {
+    return guard([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        const Layout& L = c->lay;
+        const std::string n(name);
+        if (c->T == 0) throw std::logic_error("debug_read: no step has run");
+        const int64_t T = c->T, d = L.d, M = L.M, k = L.k;
+        const void* src = nullptr;
+        int64_t sz = 0;
+        auto lay = [&]() -> LayerBufs& {
+            if (layer < 0 || layer >= L.L) throw std::out_of_range("debug_read: bad layer");
+            return c->layers[layer];
+        };
+        if (n == "h") {
+            if (layer < 0 || layer > L.L) throw std::out_of_range("debug_read: bad layer");
+            src = c->h[layer];
+            sz = 4 * T * d;
+        } else if (n == "normed") {
+            src = lay().normed;
+            sz = 4 * T * d;
+        } else if (n == "logits") {
+            src = lay().logits;
+            sz = 4 * T * M;
+        } else if (n == "probs") {
+            src = lay().probs;
+            sz = 4 * T * M;
+        } else if (n == "topk_idx") {
+            src = lay().topk_idx;
+            sz = 4 * T * k;
+        } else if (n == "topk_w") {
+            src = lay().topk_w;
+            sz = 4 * T * k;
+        } else if (n == "counts") {
+            src = lay().counts;
+            sz = 4 * M;
+        } else if (n == "pad_off") {
+            src = lay().pad_off;
+            sz = 4 * (M + 1);
+        } else if (n == "row_token") {
+            src = lay().row_token;
+            sz = 4 * c->R_cap;
+        } else if (n == "slot_row") {
+            src = lay().slot_row;
+            sz = 4 * T * k;
+        } else if (n == "head_logits") {
+            src = c->head_logits;
+            sz = 4 * T * L.V;
+        } else if (n == "y") {
+            src = lay().y;
+            sz = 4 * c->R_cap * d;
+        } else if (n == "perm") {
+            // token of each routed row, expert-major, without padding (model.hpp:314-318)
+            std::vector<int32_t> rt(c->R_cap), po(M + 1);
+            ck(cudaMemcpy(rt.data(), lay().row_token, 4 * c->R_cap, cudaMemcpyDeviceToHost), "D2H");
+            ck(cudaMemcpy(po.data(), lay().pad_off, 4 * (M + 1), cudaMemcpyDeviceToHost), "D2H");
+            std::vector<int32_t> out;
+            for (int j = 0; j < M; ++j)
+                for (int r = po[j]; r < po[j + 1]; ++r)
+                    if (rt[r] >= 0) out.push_back(rt[r]);
+            if (bytes < static_cast<int64_t>(4 * out.size())) throw std::invalid_argument("debug_read: buffer too small");
+            std::memcpy(host, out.data(), 4 * out.size());
+            return;
+        } else {
+            throw std::invalid_argument("debug_read: unknown buffer " + n);
+        }
+        if (bytes < sz) throw std::invalid_argument("debug_read: buffer too small");
+        ck(cudaMemcpyAsync(host, src, sz, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+    });
+}
+
+void* spes_stream(spes_ctx* c) { return c->stream; }
+int64_t spes_kernel_launches(spes_ctx* c) { return c->launches; }
+
+// ---- kernel-level entry points ----
+spes_status spes_kernel_router(const spes_model_cfg* cfg, const float* h, const float* gain,
+                               const float* router, int64_t T, float* normed, float* logits,
+                               float* probs, int32_t* topk_idx, float* topk_w, int32_t* counts,
+                               int32_t* perm, int32_t cuda_device) {
+    return guard([&] {
+        ck(cudaSetDevice(cuda_device), "cudaSetDevice");
+        const int64_t d = cfg->hidden;
+        const int M = cfg->experts_total, k = cfg->experts_active;
+        if (k < 1 || k > M || M > 64 || k > 8) throw std::invalid_argument("route: need 1 <= k <= M");
+        if (d % 4) throw std::invalid_argument("router kernel: hidden must be a multiple of 4");
+        DevMem D;
+        float* dh = D.alloc<float>(T * d);
+        float* dg = D.alloc<float>(d);
+        float* dr = D.alloc<float>(d * M);
+        float* dn = D.alloc<float>(T * d);
+        float* dl = D.alloc<float>(T * M);
+        float* dp = D.alloc<float>(T * M);
+        int32_t* di = D.alloc<int32_t>(T * k);
+        float* dw = D.alloc<float>(T * k);
+        float* dlse = D.alloc<float>(T);
+        float* dinv = D.alloc<float>(T);
+        float* dden = D.alloc<float>(T);
+        ck(cudaMemcpy(dh, h, 4 * T * d, cudaMemcpyHostToDevice), "H2D");
+        ck(cudaMemcpy(dg, gain, 4 * d, cudaMemcpyHostToDevice), "H2D");
+        ck(cudaMemcpy(dr, router, 4 * d * M, cudaMemcpyHostToDevice), "H2D");
+        const int variant = spes_expf::host_variant_from(&expf);
+        spes_k::router_forward(dh, dg, dr, T, d, M, k, cfg->renormalize_after_topk, cfg->rms_eps,
+                               variant, dn, dl, dp, di, dw, dlse, dinv, dden, 0);
+        // routing plan for counts / permutation
+        const int64_t R = rup(T * k + static_cast<int64_t>(M) * 128, 128);
+        const int64_t nchunks = (T + 255) / 256;
+        spes_k::RoutePlan rp{D.alloc<int32_t>(nchunks * M), D.alloc<int32_t>(M),
+                             D.alloc<int32_t>(M + 1), D.alloc<float>(M), D.alloc<int32_t>(T * k),
+                             D.alloc<int32_t>(R), D.alloc<float>(R), D.alloc<GemmGroup>(6 * M),
+                             D.alloc<int32_t>(6)};
+        spes_k::GroupBases gb{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 128, 128,
+                              128, 128, 128, 128};
+        spes_k::route_plan(di, dw, T, M, k, R, rp, gb, 0);
+        ck(cudaDeviceSynchronize(), "router kernel");
+        if (normed) ck(cudaMemcpy(normed, dn, 4 * T * d, cudaMemcpyDeviceToHost), "D2H");
+        if (logits) ck(cudaMemcpy(logits, dl, 4 * T * M, cudaMemcpyDeviceToHost), "D2H");
+        if (probs) ck(cudaMemcpy(probs, dp, 4 * T * M, cudaMemcpyDeviceToHost), "D2H");
+        if (topk_idx) ck(cudaMemcpy(topk_idx, di, 4 * T * k, cudaMemcpyDeviceToHost), "D2H");
+        if (topk_w) ck(cudaMemcpy(topk_w, dw, 4 * T * k, cudaMemcpyDeviceToHost), "D2H");
+        if (counts) ck(cudaMemcpy(counts, rp.counts, 4 * M, cudaMemcpyDeviceToHost), "D2H");
+        if (perm) {
+            std::vector<int32_t> rt(R), po(M + 1);
+            ck(cudaMemcpy(rt.data(), rp.row_token, 4 * R, cudaMemcpyDeviceToHost), "D2H");
+            ck(cudaMemcpy(po.data(), rp.pad_off, 4 * (M + 1), cudaMemcpyDeviceToHost), "D2H");
+            int64_t q = 0;
+            for (int j = 0; j < M; ++j)
+                for (int r = po[j]; r < po[j + 1]; ++r)
+                    if (rt[r] >= 0) perm[q++] = rt[r];
+        }
+    });
+}
+
+spes_status spes_kernel_adamw(float* theta, const float* grad, float* m, float* v, int64_t n,
+                              const spes_adamw_cfg* o, int64_t step, int32_t cuda_device) {
+    return guard([&] {
+        ck(cudaSetDevice(cuda_device), "cudaSetDevice");
+        if (n % 4) throw std::invalid_argument("adamw kernel: n must be a multiple of 4");
+        DevMem D;
+        float* dt = D.alloc<float>(n);
+        float* dgr = D.alloc<float>(n);
+        float* dm = D.alloc<float>(n);
+        float* dv = D.alloc<float>(n);
+        spes_k::AdamSeg seg{0, 0, n};
+        auto* ds = D.alloc<spes_k::AdamSeg>(1);
+        ck(cudaMemcpy(ds, &seg, sizeof(seg), cudaMemcpyHostToDevice), "H2D");
+        ck(cudaMemcpy(dt, theta, 4 * n, cudaMemcpyHostToDevice), "H2D");
+        ck(cudaMemcpy(dgr, grad, 4 * n, cudaMemcpyHostToDevice), "H2D");
+        ck(cudaMemcpy(dm, m, 4 * n, cudaMemcpyHostToDevice), "H2D");
+        ck(cudaMemcpy(dv, v, 4 * n, cudaMemcpyHostToDevice), "H2D");
+        const float bc1 = 1.f - static_cast<float>(std::pow(o->beta1, static_cast<double>(step)));
+        const float bc2 = 1.f - static_cast<float>(std::pow(o->beta2, static_cast<double>(step)));
+        const float b1 = static_cast<float>(o->beta1), b2 = static_cast<float>(o->beta2);
+        volatile float one = 1.f;
+        spes_k::adamw(dt, dgr, dm, dv, ds, 1, n, static_cast<float>(o->lr), b1, b2, one - b1,
+                      one - b2, static_cast<float>(o->eps), static_cast<float>(o->weight_decay),
+                      bc1, bc2, 0);
+        ck(cudaDeviceSynchronize(), "adamw kernel");
+        ck(cudaMemcpy(theta, dt, 4 * n, cudaMemcpyDeviceToHost), "D2H");
+        ck(cudaMemcpy(m, dm, 4 * n, cudaMemcpyDeviceToHost), "D2H");
+        ck(cudaMemcpy(v, dv, 4 * n, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+spes_status spes_kernel_owner_mean(const float* x, int32_t n_owners, int64_t n, float* out,
+                                   int32_t cuda_device) {
+    return guard([&] {
+        ck(cudaSetDevice(cuda_device), "cudaSetDevice");
+        DevMem D;
+        float* dx = D.alloc<float>(n * n_owners);
+        float* dout = D.alloc<float>(n);
+        ck(cudaMemcpy(dx, x, 4 * n * n_owners, cudaMemcpyHostToDevice), "H2D");
+        spes_k::owner_mean_strided(dx, n_owners, n, n, dout, 0);
+        ck(cudaDeviceSynchronize(), "owner mean");
+        ck(cudaMemcpy(out, dout, 4 * n, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+spes_status spes_kernel_expf(const float* x, float* y, int64_t n, int32_t cuda_device) {
+    return guard([&] {
+        ck(cudaSetDevice(cuda_device), "cudaSetDevice");
+        DevMem D;
+        float* dx = D.alloc<float>(n);
+        float* dy = D.alloc<float>(n);
+        ck(cudaMemcpy(dx, x, 4 * n, cudaMemcpyHostToDevice), "H2D");
+        spes_k::expf_port_device(dx, dy, n, spes_expf::host_variant_from(&expf), 0);
+        ck(cudaDeviceSynchronize(), "expf");
+        ck(cudaMemcpy(y, dy, 4 * n, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+void spes_host_expf_port(const float* x, float* y, int64_t n, int32_t variant) {
+    const int v = variant == 0 ? spes_expf::host_variant_from(&expf) : variant - 1;
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i)
+        y[i] = v ? spes_expf::expf_glibc<1>(x[i]) : spes_expf::expf_glibc<0>(x[i]);
+}
+
+int32_t spes_host_expf_variant(void) { return spes_expf::host_variant_from(&expf); }
+
+}  // extern "C"

@@ -1,0 +1,55 @@
+// Shared device helpers for the SPES kernels.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace spes_dev {
+
+// Explicitly rounded fp32 ops: the reference is compiled without FMA and with
+// strictly sequential reductions; kernels that must reproduce its
+// bits use these so nvcc never contracts a*b+c into an FMA.
+__device__ __forceinline__ float fadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float fsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float fmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float fdiv(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ float fsqrt(float a) { return __fsqrt_rn(a); }
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Interleaved gate||up column layout used by the expert GEMMs: blocks of 128
+// gate columns followed by the matching 128 up columns.
+__host__ __device__ __forceinline__ int64_t il_gate(int64_t x) { return 256 * (x >> 7) + (x & 127); }
+__host__ __device__ __forceinline__ int64_t il_up(int64_t x) { return il_gate(x) + 128; }
+
+__device__ __forceinline__ float silu_f(float z) {
+    // z * sigmoid(z) with the reference's branch structure (kernels.hpp:92-103)
+    float s = z >= 0.f ? 1.f / (1.f + __expf(-z)) : __expf(z) / (1.f + __expf(z));
+    return z * s;
+}
+__device__ __forceinline__ float sigmoid_f(float z) {
+    return z >= 0.f ? 1.f / (1.f + __expf(-z)) : __expf(z) / (1.f + __expf(z));
+}
+
+}  // namespace spes_dev

@@ -1,0 +1,1269 @@
+// SPES device kernels other than the tensor-core GEMMs (see gemm.cu).
+//
+// Exactness policy: kernels on the routing path, the AdamW
+// update, the owner-set mean and the merge apply reproduce the reference's fp32
+// / fp64 operation order exactly (explicitly rounded ops, sequential reductions,
+// glibc-compatible expf), so they are bit-exact given identical inputs. Loss
+// scalars and the column reductions feeding parameter gradients use fixed-order
+// parallel trees: deterministic run to run, within tolerance of the reference.
+#include <cuda_bf16.h>
+#include <stdio.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "glibc_expf.h"
+#include "kernels.h"
+
+namespace spes_k {
+
+thread_local int64_t* g_launch_counter = nullptr;
+
+using namespace spes_dev;
+
+static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ============================ embedding gather ============================
+// h0[t] = emb[inputs[t]] (model.hpp:286, graph.hpp:208-219)
+__global__ void embed_gather_k(const float* __restrict__ emb, const int32_t* __restrict__ tokens,
+                               int64_t S, int64_t d, int64_t V, float* __restrict__ h,
+                               int32_t* __restrict__ inputs, int32_t* __restrict__ targets,
+                               int32_t* err) {
+    const int64_t t = blockIdx.x;
+    const int64_t b = t / S, s = t % S;
+    int32_t tin = tokens[b * (S + 1) + s], tout = tokens[b * (S + 1) + s + 1];
+    const bool bad = tin < 0 || tin >= V || tout < 0 || tout >= V;
+    if (threadIdx.x == 0) {
+        inputs[t] = bad ? 0 : tin;
+        targets[t] = bad ? 0 : tout;
+        if (bad) atomicExch(err, 1);
+    }
+    if (bad) tin = 0;
+    const float4* src = reinterpret_cast<const float4*>(emb + static_cast<int64_t>(tin) * d);
+    float4* dst = reinterpret_cast<float4*>(h + t * d);
+    for (int64_t q = threadIdx.x; q < d / 4; q += blockDim.x) dst[q] = __ldg(src + q);
+}
+
+void embed_gather(const float* emb, const int32_t* tokens, int64_t B, int64_t S, int64_t d,
+                  int64_t V, float* h, int32_t* inputs, int32_t* targets, int32_t* err,
+                  cudaStream_t s) {
+    embed_gather_k<<<static_cast<unsigned>(B * S), 128, 0, s>>>(emb, tokens, S, d, V, h, inputs,
+                                                                targets, err);
+    count_launch();
+}
+
+// ============================ router forward ============================
+// One thread per token, bit-exact with the reference given identical h:
+//   rmsnorm_forward (kernels.hpp:117-128): sequential sum of squares, y = (x*inv)*g
+//   matmul (kernels.hpp:27-38): logit_e = sum_p normed_p * R[p][e], p ascending, no FMA
+//   softmax_rows (kernels.hpp:156-172) with glibc expf; logsumexp (:174-185)
+//   route_from_logits (model.hpp:185-216): stable top-k, ascending indices, weights
+constexpr int RCH = 32;  // router rows staged per smem chunk
+
+template <int MAXM>
+__global__ void __launch_bounds__(128) router_fwd_k(
+    const float* __restrict__ h, const float* __restrict__ gain, const float* __restrict__ R,
+    int T, int d, int M, int k, int renorm, float eps, int variant, float* __restrict__ normed,
+    float* __restrict__ logits, float* __restrict__ probs, int32_t* __restrict__ topk_idx,
+    float* __restrict__ topk_w, float* __restrict__ lse_out, float* __restrict__ inv_out,
+    float* __restrict__ denom_out) {
+    __shared__ __align__(16) float sR[RCH * MAXM];
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = t < T;
+    const float* x = h + static_cast<int64_t>(valid ? t : 0) * d;
+
+    float ms = 0.f;
+    if (valid) {
+        for (int q = 0; q < d; q += 4) {
+            float4 v = __ldg(reinterpret_cast<const float4*>(x + q));
+            ms = fadd(ms, fmul(v.x, v.x));
+            ms = fadd(ms, fmul(v.y, v.y));
+            ms = fadd(ms, fmul(v.z, v.z));
+            ms = fadd(ms, fmul(v.w, v.w));
+        }
+    }
+    const float inv = fdiv(1.f, fsqrt(fadd(fdiv(ms, static_cast<float>(d)), eps)));
+
+    float acc[MAXM];
+#pragma unroll
+    for (int e = 0; e < MAXM; ++e) acc[e] = 0.f;
+    float* nrow = normed + static_cast<int64_t>(valid ? t : 0) * d;
+    for (int q0 = 0; q0 < d; q0 += RCH) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < RCH * M; i += blockDim.x) sR[i] = __ldg(R + static_cast<int64_t>(q0) * M + i);
+        __syncthreads();
+        if (!valid) continue;
+#pragma unroll 1
+        for (int qq = 0; qq < RCH; qq += 4) {
+            const float4 xv = __ldg(reinterpret_cast<const float4*>(x + q0 + qq));
+            const float4 gv = __ldg(reinterpret_cast<const float4*>(gain + q0 + qq));
+            float nv[4];
+            nv[0] = fmul(fmul(xv.x, inv), gv.x);
+            nv[1] = fmul(fmul(xv.y, inv), gv.y);
+            nv[2] = fmul(fmul(xv.z, inv), gv.z);
+            nv[3] = fmul(fmul(xv.w, inv), gv.w);
+            *reinterpret_cast<float4*>(nrow + q0 + qq) = make_float4(nv[0], nv[1], nv[2], nv[3]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float* rrow = sR + (qq + u) * M;
+#pragma unroll
+                for (int e = 0; e < MAXM; ++e)
+                    if (e < M) acc[e] = fadd(acc[e], fmul(nv[u], rrow[e]));
+            }
+        }
+    }
+    if (!valid) return;
+
+    float* lrow = logits + static_cast<int64_t>(t) * M;
+    float mx = acc[0];
+#pragma unroll
+    for (int e = 0; e < MAXM; ++e) {
+        if (e < M) {
+            lrow[e] = acc[e];
+            if (e > 0) mx = (mx < acc[e]) ? acc[e] : mx;  // std::max(mx, x)
+        }
+    }
+    float sum = 0.f;
+#pragma unroll
+    for (int e = 0; e < MAXM; ++e) {
+        if (e < M) {
+            const float z = fsub(acc[e], mx);
+            acc[e] = variant ? spes_expf::expf_glibc<1>(z) : spes_expf::expf_glibc<0>(z);
+            sum = fadd(sum, acc[e]);
+        }
+    }
+    const float isum = fdiv(1.f, sum);
+    float* prow = probs + static_cast<int64_t>(t) * M;
+#pragma unroll
+    for (int e = 0; e < MAXM; ++e) {
+        if (e < M) {
+            acc[e] = fmul(acc[e], isum);
+            prow[e] = acc[e];
+        }
+    }
+    lse_out[t] = mx + logf(sum);
+    inv_out[t] = inv;
+
+    // top-k: iterative argmax (strict '>' scanning ascending => lowest index on ties),
+    // identical to the first k of a stable descending sort.
+    uint64_t chosen = 0;
+    for (int s = 0; s < k; ++s) {
+        int best = -1;
+        float bv = 0.f;
+#pragma unroll
+        for (int e = 0; e < MAXM; ++e) {
+            if (e < M && !((chosen >> e) & 1ull)) {
+                if (best < 0 || acc[e] > bv) {
+                    best = e;
+                    bv = acc[e];
+                }
+            }
+        }
+        chosen |= 1ull << best;
+    }
+    float dn = 0.f;
+#pragma unroll
+    for (int e = 0; e < MAXM; ++e)
+        if ((chosen >> e) & 1ull) dn = fadd(dn, acc[e]);
+    int slot = 0;
+    int32_t* irow = topk_idx + static_cast<int64_t>(t) * k;
+    float* wrow = topk_w + static_cast<int64_t>(t) * k;
+#pragma unroll
+    for (int e = 0; e < MAXM; ++e) {
+        if ((chosen >> e) & 1ull) {
+            irow[slot] = e;
+            wrow[slot] = renorm ? fdiv(acc[e], dn) : acc[e];
+            ++slot;
+        }
+    }
+    if (denom_out) denom_out[t] = dn;
+}
+
+void router_forward(const float* h, const float* gain, const float* router, int64_t T, int64_t d,
+                    int M, int k, int renorm, float eps, int variant, float* normed,
+                    float* logits, float* probs, int32_t* topk_idx, float* topk_w, float* lse,
+                    float* inv_rms, float* denom, cudaStream_t s) {
+    dim3 grid(static_cast<unsigned>(cdiv(T, 128)));
+#define SPES_ROUTER(MM)                                                                         \
+    router_fwd_k<MM><<<grid, 128, 0, s>>>(h, gain, router, (int)T, (int)d, M, k, renorm, eps,   \
+                                          variant, normed, logits, probs, topk_idx, topk_w, lse, \
+                                          inv_rms, denom)
+    if (M <= 8)
+        SPES_ROUTER(8);
+    else if (M <= 16)
+        SPES_ROUTER(16);
+    else if (M <= 32)
+        SPES_ROUTER(32);
+    else
+        SPES_ROUTER(64);
+#undef SPES_ROUTER
+    count_launch();
+}
+
+// ============================ routing plan ============================
+constexpr int ROUTE_CH = 256;  // tokens per chunk
+
+__global__ void route_count_k(const int32_t* __restrict__ idx, int T, int M, int k,
+                              int32_t* __restrict__ chunk_counts) {
+    __shared__ int32_t hist[64];
+    for (int j = threadIdx.x; j < M; j += blockDim.x) hist[j] = 0;
+    __syncthreads();
+    const int t = blockIdx.x * ROUTE_CH + threadIdx.x;
+    if (t < T)
+        for (int s = 0; s < k; ++s) atomicAdd(&hist[idx[static_cast<int64_t>(t) * k + s]], 1);
+    __syncthreads();
+    for (int j = threadIdx.x; j < M; j += blockDim.x)
+        chunk_counts[static_cast<int64_t>(blockIdx.x) * M + j] = hist[j];
+}
+
+// Single block: per-expert scan over chunks, padded offsets, lb coefficients
+// (model.hpp:344-353, computed in double exactly as the reference), and the six
+// GEMM group tables of the layer.
+__global__ void route_scan_k(int32_t* __restrict__ chunk_counts, int nchunks, int T, int M,
+                             int k, int32_t* __restrict__ counts, int32_t* __restrict__ pad_off,
+                             float* __restrict__ lb_coeff, GemmGroup* __restrict__ groups,
+                             int32_t* __restrict__ tiles, GroupBases gb) {
+    __shared__ int32_t s_cnt[64];
+    __shared__ int32_t s_off[65];
+    const int j = threadIdx.x;
+    if (j < M) {
+        int32_t run = 0;
+        for (int c = 0; c < nchunks; ++c) {
+            int32_t v = chunk_counts[static_cast<int64_t>(c) * M + j];
+            chunk_counts[static_cast<int64_t>(c) * M + j] = run;  // becomes chunk base
+            run += v;
+        }
+        s_cnt[j] = run;
+        counts[j] = run;
+        const double assignments = static_cast<double>(T) * k;
+        const double f_j = static_cast<double>(run) / assignments;
+        lb_coeff[j] = static_cast<float>(static_cast<double>(M) * f_j / static_cast<double>(T));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int32_t acc = 0;
+        for (int e = 0; e < M; ++e) {
+            s_off[e] = acc;
+            acc += (s_cnt[e] + 127) / 128 * 128;
+        }
+        s_off[M] = acc;
+        for (int e = 0; e <= M; ++e) pad_off[e] = s_off[e];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int64_t d = gb.d, f = gb.f;
+        int32_t ts[6] = {0, 0, 0, 0, 0, 0};
+        for (int e = 0; e < M; ++e) {
+            const int32_t mt = (s_off[e + 1] - s_off[e]) / 128;
+            const int64_t goff = gb.grad_off_layer ? gb.grad_off_layer[e] : -1;
+            for (int g = 0; g < 6; ++g) {
+                GemmGroup G{};
+                G.tag = e;
+                G.out_row0 = s_off[e];
+                G.a_row0 = s_off[e];
+                G.k0 = 0;
+                G.m_tiles = mt;
+                switch (g) {
+                    case 0:  // fwd gate||up: Xp[R x d] . W1t_e[2f x d]^T
+                        G.b_row0 = static_cast<int32_t>(e * 2 * f);
+                        G.n_tiles = static_cast<int32_t>(2 * f / 256);
+                        G.k_len = static_cast<int32_t>(d);
+                        G.out0 = gb.gu;
+                        G.ldo = 2 * f;
+                        break;
+                    case 1:  // fwd down: Hact[R x f] . W2t_e[d x f]^T
+                        G.b_row0 = static_cast<int32_t>(e * d);
+                        G.n_tiles = static_cast<int32_t>(d / gb.bn_fwd2);
+                        G.k_len = static_cast<int32_t>(f);
+                        G.out0 = gb.y;
+                        G.ldo = d;
+                        break;
+                    case 2:  // bwd dH: dYw[R x d] . Wd_e[f x d]^T
+                        G.b_row0 = static_cast<int32_t>(e * f);
+                        G.n_tiles = static_cast<int32_t>(f / gb.bn_dh);
+                        G.k_len = static_cast<int32_t>(d);
+                        G.out0 = gb.dgu;
+                        G.ldo = 2 * f;
+                        break;
+                    case 3:  // bwd dX: dGU[R x 2f] . W1_e[d x 2f]^T
+                        G.b_row0 = static_cast<int32_t>(e * d);
+                        G.n_tiles = static_cast<int32_t>(d / gb.bn_dx);
+                        G.k_len = static_cast<int32_t>(2 * f);
+                        G.out0 = gb.dxp;
+                        G.ldo = d;
+                        break;
+                    case 4:  // bwd dW1 (owned): XpT[d x R] . dGUT[2f x R]^T over this expert's rows
+                        G.a_row0 = 0;
+                        G.b_row0 = 0;
+                        G.k0 = s_off[e];
+                        G.k_len = s_off[e + 1] - s_off[e];
+                        G.m_tiles = goff >= 0 ? static_cast<int32_t>(d / 128) : 0;
+                        G.n_tiles = static_cast<int32_t>(2 * f / 256);
+                        G.out_row0 = 0;
+                        G.out0 = goff >= 0 ? gb.grad_expert_base + goff : nullptr;
+                        G.out1 = goff >= 0 ? gb.grad_expert_base + goff + d * f : nullptr;
+                        G.ldo = f;
+                        break;
+                    default:  // bwd dW2 (owned): HactT[f x R] . dYwT[d x R]^T
+                        G.a_row0 = 0;
+                        G.b_row0 = 0;
+                        G.k0 = s_off[e];
+                        G.k_len = s_off[e + 1] - s_off[e];
+                        G.m_tiles = goff >= 0 ? static_cast<int32_t>(f / 128) : 0;
+                        G.n_tiles = static_cast<int32_t>(d / gb.bn_dw2);
+                        G.out_row0 = 0;
+                        G.out0 = goff >= 0 ? gb.grad_expert_base + goff + 2 * d * f : nullptr;
+                        G.ldo = d;
+                        break;
+                }
+                G.tile_start = ts[g];
+                ts[g] += G.m_tiles * G.n_tiles;
+                groups[g * M + e] = G;
+            }
+        }
+        for (int g = 0; g < 6; ++g) tiles[g] = ts[g];
+    }
+}
+
+// Stable scatter: rows of expert j in ascending token order (model.hpp:314-318).
+// Warps of a chunk run one after another; inside a warp, ballots give ranks.
+__global__ void route_scatter_k(const int32_t* __restrict__ idx, const float* __restrict__ w,
+                                int T, int M, int k, const int32_t* __restrict__ chunk_base,
+                                const int32_t* __restrict__ pad_off, int32_t* __restrict__ slot_row,
+                                int32_t* __restrict__ row_token, float* __restrict__ row_w) {
+    __shared__ int32_t base[64];
+    for (int j = threadIdx.x; j < M; j += blockDim.x)
+        base[j] = pad_off[j] + chunk_base[static_cast<int64_t>(blockIdx.x) * M + j];
+    const int t = blockIdx.x * ROUTE_CH + threadIdx.x;
+    const bool valid = t < T;
+    int32_t sel[8];
+    for (int s = 0; s < k; ++s) sel[s] = valid ? idx[static_cast<int64_t>(t) * k + s] : -1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t lt = lanemask_lt();
+    for (int w8 = 0; w8 < ROUTE_CH / 32; ++w8) {
+        __syncthreads();
+        if (warp == w8) {
+            for (int j = 0; j < M; ++j) {
+                int my_s = -1;
+                for (int s = 0; s < k; ++s)
+                    if (sel[s] == j) my_s = s;
+                const uint32_t mask = __ballot_sync(0xffffffffu, my_s >= 0);
+                if (mask == 0) continue;
+                if (my_s >= 0) {
+                    const int32_t row = base[j] + __popc(mask & lt);
+                    slot_row[static_cast<int64_t>(t) * k + my_s] = row;
+                    row_token[row] = t;
+                    row_w[row] = w[static_cast<int64_t>(t) * k + my_s];
+                }
+                __syncwarp();
+                if (lane == 0) base[j] += __popc(mask);
+                __syncwarp();
+            }
+        }
+    }
+}
+
+void route_plan(const int32_t* topk_idx, const float* topk_w, int64_t T, int M, int k,
+                int64_t R_cap, const RoutePlan& p, const GroupBases& gb, cudaStream_t s) {
+    const int nchunks = static_cast<int>(cdiv(T, ROUTE_CH));
+    route_count_k<<<nchunks, ROUTE_CH, 0, s>>>(topk_idx, (int)T, M, k, p.chunk_counts);
+    route_scan_k<<<1, 64, 0, s>>>(p.chunk_counts, nchunks, (int)T, M, k, p.counts, p.pad_off,
+                                  p.lb_coeff, p.groups, p.tiles, gb);
+    cudaMemsetAsync(p.row_token, 0xFF, sizeof(int32_t) * R_cap, s);
+    cudaMemsetAsync(p.row_w, 0, sizeof(float) * R_cap, s);
+    route_scatter_k<<<nchunks, ROUTE_CH, 0, s>>>(topk_idx, topk_w, (int)T, M, k, p.chunk_counts,
+                                                 p.pad_off, p.slot_row, p.row_token, p.row_w);
+    count_launch(3);
+}
+
+// ============================ gather / transpose to bf16 ============================
+// 64 x 64 tile: dst[r][c] = bf16(src[map(r)][c]) and dstT[c][r] = same.
+__global__ void __launch_bounds__(256) gather_rows_bf16_k(
+    const float* __restrict__ src, int64_t ld_src, const int32_t* __restrict__ row_map,
+    const int32_t* __restrict__ nrows_dev, int64_t rows, int64_t cols, bf16* __restrict__ dst,
+    bf16* __restrict__ dstT, int64_t rows_cap) {
+    __shared__ float tile[64][65];
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 64;
+    const int64_t c0 = static_cast<int64_t>(blockIdx.y) * 64;
+    const int64_t nrows = nrows_dev ? *nrows_dev : rows;
+    if (r0 >= nrows) return;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int rr = ty + 16 * i;
+        const int64_t r = r0 + rr;
+        int64_t srow = -1;
+        if (r < nrows) srow = row_map ? row_map[r] : r;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (srow >= 0) v = __ldg(reinterpret_cast<const float4*>(src + srow * ld_src + c0 + 4 * tx));
+        tile[rr][4 * tx + 0] = v.x;
+        tile[rr][4 * tx + 1] = v.y;
+        tile[rr][4 * tx + 2] = v.z;
+        tile[rr][4 * tx + 3] = v.w;
+        if (r < nrows) {
+            __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y);
+            __nv_bfloat162 b = __floats2bfloat162_rn(v.z, v.w);
+            uint2 pk;
+            pk.x = *reinterpret_cast<uint32_t*>(&a);
+            pk.y = *reinterpret_cast<uint32_t*>(&b);
+            *reinterpret_cast<uint2*>(dst + r * cols + c0 + 4 * tx) = pk;
+        }
+    }
+    __syncthreads();
+    if (!dstT) return;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int cc = ty + 16 * i;
+        __nv_bfloat162 a = __floats2bfloat162_rn(tile[4 * tx + 0][cc], tile[4 * tx + 1][cc]);
+        __nv_bfloat162 b = __floats2bfloat162_rn(tile[4 * tx + 2][cc], tile[4 * tx + 3][cc]);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&a);
+        pk.y = *reinterpret_cast<uint32_t*>(&b);
+        const int64_t r = r0 + 4 * tx;
+        if (r < rows_cap) *reinterpret_cast<uint2*>(dstT + (c0 + cc) * rows_cap + r) = pk;
+    }
+}
+
+void gather_rows_bf16(const float* src, int64_t ld_src, const int32_t* row_map,
+                      const int32_t* nrows_dev, int64_t rows, int64_t cols, bf16* dst,
+                      bf16* dstT, int64_t rows_cap, cudaStream_t s) {
+    dim3 grid(static_cast<unsigned>(cdiv(rows, 64)), static_cast<unsigned>(cols / 64));
+    gather_rows_bf16_k<<<grid, 256, 0, s>>>(src, ld_src, row_map, nrows_dev, rows, cols, dst,
+                                            dstT, rows_cap);
+    count_launch();
+}
+
+// ============================ combine (forward) ============================
+// h_next[t] = h[t] + sum over selected experts in ascending order of (0 + w*y)
+// (model.hpp:330-338: rowwise_mul, scatter_rows into zeros, add chain, residual add)
+__global__ void combine_fwd_k(const float* __restrict__ h, const float* __restrict__ y,
+                              const int32_t* __restrict__ slot_row, const float* __restrict__ w,
+                              int64_t d, int k, float* __restrict__ h_next) {
+    const int64_t t = blockIdx.x;
+    int32_t rows[8];
+    float ws[8];
+    for (int s = 0; s < k; ++s) {
+        rows[s] = slot_row[t * k + s];
+        ws[s] = w[t * k + s];
+    }
+    for (int64_t q = threadIdx.x * 4; q < d; q += blockDim.x * 4) {
+        float4 acc;
+        {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(y + rows[0] * d + q));
+            acc.x = fadd(0.f, fmul(v.x, ws[0]));
+            acc.y = fadd(0.f, fmul(v.y, ws[0]));
+            acc.z = fadd(0.f, fmul(v.z, ws[0]));
+            acc.w = fadd(0.f, fmul(v.w, ws[0]));
+        }
+        for (int s = 1; s < k; ++s) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(y + rows[s] * d + q));
+            acc.x = fadd(acc.x, fadd(0.f, fmul(v.x, ws[s])));
+            acc.y = fadd(acc.y, fadd(0.f, fmul(v.y, ws[s])));
+            acc.z = fadd(acc.z, fadd(0.f, fmul(v.z, ws[s])));
+            acc.w = fadd(acc.w, fadd(0.f, fmul(v.w, ws[s])));
+        }
+        const float4 hv = __ldg(reinterpret_cast<const float4*>(h + t * d + q));
+        *reinterpret_cast<float4*>(h_next + t * d + q) =
+            make_float4(fadd(hv.x, acc.x), fadd(hv.y, acc.y), fadd(hv.z, acc.z), fadd(hv.w, acc.w));
+    }
+}
+
+void combine_forward(const float* h, const float* y, const int32_t* slot_row,
+                     const int32_t* topk_idx, const float* topk_w, int64_t T, int64_t d, int k,
+                     float* h_next, cudaStream_t s) {
+    (void)topk_idx;
+    const int threads = d >= 1024 ? 256 : static_cast<int>(d / 4);
+    combine_fwd_k<<<static_cast<unsigned>(T), threads, 0, s>>>(h, y, slot_row, topk_w, d, k,
+                                                               h_next);
+    count_launch();
+}
+
+// ============================ head: CE + z ============================
+// Warp per token. lse, picked (graph.hpp:410-423); d logits following the
+// reverse tape: gather_cols then logsumexp backward (graph.hpp:192-204, 274-281).
+__global__ void head_ce_k(const float* __restrict__ logits, const int32_t* __restrict__ targets,
+                          int64_t T, int64_t T_pad, int64_t V, int variant, float g_s2,
+                          float g_ssum, float* __restrict__ dlogits, float* __restrict__ diff,
+                          float* __restrict__ lse_out) {
+    const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= T_pad) return;
+    float* drow = dlogits + t * V;
+    if (t >= T) {
+        for (int64_t j = lane; j < V; j += 32) drow[j] = 0.f;
+        return;
+    }
+    const float* row = logits + t * V;
+    float mx = -INFINITY;
+    for (int64_t j = lane; j < V; j += 32) mx = fmaxf(mx, row[j]);
+    mx = warp_max(mx);
+    float sum = 0.f;
+    for (int64_t j = lane; j < V; j += 32) {
+        const float z = fsub(row[j], mx);
+        sum += variant ? spes_expf::expf_glibc<1>(z) : spes_expf::expf_glibc<0>(z);
+    }
+    sum = warp_sum(sum);
+    const float lse = mx + logf(sum);
+    const int32_t tgt = targets[t];
+    const float picked = row[tgt];
+    if (lane == 0) {
+        diff[t] = lse + picked * -1.f;
+        lse_out[t] = lse;
+    }
+    // lse.grad = (0 + g_s2*lse) + g_s2*lse + g_ssum (z-loss mul, then ce add)
+    float glse = fadd(fadd(fadd(0.f, fmul(g_s2, lse)), fmul(g_s2, lse)), g_ssum);
+    const float isum = 1.f / sum;
+    for (int64_t j = lane; j < V; j += 32) {
+        const float z = fsub(row[j], mx);
+        const float p = (variant ? spes_expf::expf_glibc<1>(z) : spes_expf::expf_glibc<0>(z)) * isum;
+        const float base = (j == tgt) ? -1.f * g_ssum : 0.f;
+        drow[j] = fadd(base, fmul(glse, p));
+    }
+}
+
+void head_ce(const float* logits, const int32_t* targets, int64_t T, int64_t T_pad, int64_t V,
+             int variant, float g_s2, float g_ssum, float* dlogits, float* diff, float* lse,
+             cudaStream_t s) {
+    const int64_t threads = T_pad * 32;
+    head_ce_k<<<static_cast<unsigned>(cdiv(threads, 256)), 256, 0, s>>>(
+        logits, targets, T, T_pad, V, variant, g_s2, g_ssum, dlogits, diff, lse);
+    count_launch();
+}
+
+// ============================ loss scalars ============================
+__device__ double block_sum_d(double v, double* sh) {
+    v = warp_sum_d(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) r += sh[i];
+    return r;  // valid in thread 0
+}
+
+__global__ void losses_k(const float* __restrict__ diff, const float* __restrict__ lse_head,
+                         const float* __restrict__ lse_r, const float* __restrict__ probs,
+                         const float* __restrict__ lb_coeff, int64_t T, int64_t Tstride, int L,
+                         int M, float inv_T,
+                         float inv_L, float c_ce, float c_lb, float c_mz, float c_z,
+                         double* __restrict__ out) {
+    __shared__ double sh[32];
+    double a = 0, b = 0;
+    for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
+        a += diff[t];
+        b += static_cast<double>(lse_head[t]) * lse_head[t];
+    }
+    const double s_ce = block_sum_d(a, sh);
+    const double s_z = block_sum_d(b, sh);
+    double mz = 0, lb = 0;
+    for (int l = 0; l < L; ++l) {
+        double c = 0, e = 0;
+        for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
+            const float lv = lse_r[static_cast<int64_t>(l) * Tstride + t];
+            c += static_cast<double>(lv) * lv;
+            const float* pr = probs + (static_cast<int64_t>(l) * Tstride + t) * M;
+            double r = 0;
+            for (int j = 0; j < M; ++j) r += static_cast<double>(pr[j]) * lb_coeff[l * M + j];
+            e += r;
+        }
+        const double sc = block_sum_d(c, sh);
+        const double se = block_sum_d(e, sh);
+        if (threadIdx.x == 0) {
+            mz += static_cast<float>(sc) * inv_T;
+            lb += static_cast<float>(se);
+        }
+    }
+    if (threadIdx.x == 0) {
+        const float ce = static_cast<float>(s_ce) * inv_T;
+        const float z = static_cast<float>(s_z) * inv_T;
+        const float moe_z = static_cast<float>(mz) * inv_L;
+        const float lbv = static_cast<float>(lb) * inv_L;
+        const float total = (ce * c_ce + lbv * c_lb) + (moe_z * c_mz + z * c_z);
+        out[0] = total;
+        out[1] = ce;
+        out[2] = lbv;
+        out[3] = moe_z;
+        out[4] = z;
+    }
+}
+
+void losses_reduce(const float* diff, const float* lse_head, const float* lse_r,
+                   const float* probs, const float* lb_coeff, int64_t T, int64_t Tstride, int L,
+                   int M, float inv_T, float inv_L, float c_ce, float c_lb, float c_mz, float c_z,
+                   double* out, cudaStream_t s) {
+    losses_k<<<1, 1024, 0, s>>>(diff, lse_head, lse_r, probs, lb_coeff, T, Tstride, L, M, inv_T, inv_L,
+                                c_ce, c_lb, c_mz, c_z, out);
+    count_launch();
+}
+
+// ============================ combine (backward) ============================
+// Tile of 64 routed rows x 64 columns: dYw[r] = bf16(gh[t_r] * w_r) (rowwise_mul
+// backward, graph.hpp:299-305) in both layouts, and partial dot products
+// <gh[t_r], Y[r]> for the gate-weight gradient (graph.hpp:307-316).
+__global__ void __launch_bounds__(256) combine_bwd_k(
+    const float* __restrict__ gh, const float* __restrict__ y, const int32_t* __restrict__ row_token,
+    const float* __restrict__ row_w, const int32_t* __restrict__ R_total, int64_t R_cap, int64_t d,
+    bf16* __restrict__ dyw, bf16* __restrict__ dywT, float* __restrict__ gw_part) {
+    __shared__ float tile[64][65];
+    __shared__ float red[64][17];
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 64;
+    const int64_t c0 = static_cast<int64_t>(blockIdx.y) * 64;
+    if (r0 >= *R_total) return;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int rr = ty + 16 * i;
+        const int64_t r = r0 + rr;
+        const int32_t t = row_token[r];
+        float4 g = make_float4(0.f, 0.f, 0.f, 0.f), yv = g;
+        float wv = 0.f;
+        if (t >= 0) {
+            g = __ldg(reinterpret_cast<const float4*>(gh + static_cast<int64_t>(t) * d + c0 + 4 * tx));
+            yv = __ldg(reinterpret_cast<const float4*>(y + r * d + c0 + 4 * tx));
+            wv = row_w[r];
+        }
+        const float a0 = g.x * wv, a1 = g.y * wv, a2 = g.z * wv, a3 = g.w * wv;
+        tile[rr][4 * tx + 0] = a0;
+        tile[rr][4 * tx + 1] = a1;
+        tile[rr][4 * tx + 2] = a2;
+        tile[rr][4 * tx + 3] = a3;
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(a0, a1), p1 = __floats2bfloat162_rn(a2, a3);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&p0);
+        pk.y = *reinterpret_cast<uint32_t*>(&p1);
+        *reinterpret_cast<uint2*>(dyw + r * d + c0 + 4 * tx) = pk;
+        red[rr][tx] = ((g.x * yv.x + g.y * yv.y) + g.z * yv.z) + g.w * yv.w;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int cc = ty + 16 * i;
+        __nv_bfloat162 a = __floats2bfloat162_rn(tile[4 * tx + 0][cc], tile[4 * tx + 1][cc]);
+        __nv_bfloat162 b = __floats2bfloat162_rn(tile[4 * tx + 2][cc], tile[4 * tx + 3][cc]);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&a);
+        pk.y = *reinterpret_cast<uint32_t*>(&b);
+        *reinterpret_cast<uint2*>(dywT + (c0 + cc) * R_cap + r0 + 4 * tx) = pk;
+    }
+    if (threadIdx.x < 64) {
+        float s = 0.f;
+        for (int i = 0; i < 16; ++i) s += red[threadIdx.x][i];
+        gw_part[(r0 + threadIdx.x) * (d / 64) + blockIdx.y] = s;
+    }
+}
+
+void combine_backward(const float* gh, const float* y, const int32_t* row_token,
+                      const float* row_w, const int32_t* R_total_dev, int64_t R_cap, int64_t d,
+                      bf16* dyw, bf16* dywT, float* gw_part, cudaStream_t s) {
+    dim3 grid(static_cast<unsigned>(R_cap / 64), static_cast<unsigned>(d / 64));
+    combine_bwd_k<<<grid, 256, 0, s>>>(gh, y, row_token, row_w, R_total_dev, R_cap, d, dyw, dywT,
+                                       gw_part);
+    count_launch();
+}
+
+// ============================ router backward + rmsnorm backward ============================
+// One thread per token, following the reverse tape of one layer:
+//   probs.grad = (0 + g_lb*coeff_j) [lb, model.hpp:358] + gate-weight grads (experts desc.)
+//   logits.grad = (0 + gl*p_j) [moe_z logsumexp] + p_j*(gprobs_j - dot) [softmax bwd]
+//   normed.grad = dX of selected experts (desc.) + glog . R^T [matmul_nt_acc]
+//   h.grad += rmsnorm backward (kernels.hpp:130-152)
+template <int MAXM>
+__global__ void __launch_bounds__(128) router_bwd_k(
+    const float* __restrict__ h, const float* __restrict__ gain, const float* __restrict__ R,
+    const float* __restrict__ probs, const float* __restrict__ lse_r,
+    const float* __restrict__ inv_rms, const float* __restrict__ denom,
+    const int32_t* __restrict__ topk_idx, const int32_t* __restrict__ slot_row,
+    const float* __restrict__ gw_part, const float* __restrict__ dxp,
+    const float* __restrict__ lb_coeff, int T, int d, int M, int k, int renorm, float g_lbsum,
+    float g_s, float* __restrict__ glog, float* __restrict__ gnormed, float* __restrict__ gh) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    const int nparts = d / 64;
+    float p[MAXM], gp[MAXM];
+    const float* prow = probs + static_cast<int64_t>(t) * M;
+#pragma unroll
+    for (int e = 0; e < MAXM; ++e) {
+        if (e < M) {
+            p[e] = prow[e];
+            gp[e] = fadd(0.f, fmul(g_lbsum, __ldg(lb_coeff + e)));
+        }
+    }
+    int32_t sel[8], rows[8];
+    for (int s = 0; s < k; ++s) {
+        sel[s] = topk_idx[static_cast<int64_t>(t) * k + s];
+        rows[s] = slot_row[static_cast<int64_t>(t) * k + s];
+    }
+    const float dn = renorm ? denom[t] : 1.f;
+    float gden = 0.f;
+    for (int s = k - 1; s >= 0; --s) {  // experts in descending order
+        float gw = 0.f;
+        const float* part = gw_part + static_cast<int64_t>(rows[s]) * nparts;
+        for (int i = 0; i < nparts; ++i) gw += part[i];
+        const int j = sel[s];
+#pragma unroll
+        for (int e = 0; e < MAXM; ++e) {
+            if (e == j) {
+                if (renorm) {
+                    gden = fsub(gden, fdiv(fmul(gw, p[e]), fmul(dn, dn)));
+                    gp[e] = fadd(gp[e], fadd(0.f, fdiv(gw, dn)));
+                } else {
+                    gp[e] = fadd(gp[e], fadd(0.f, gw));
+                }
+            }
+        }
+    }
+    if (renorm)
+        for (int s = k - 1; s >= 0; --s) {
+#pragma unroll
+            for (int e = 0; e < MAXM; ++e)
+                if (e == sel[s]) gp[e] = fadd(gp[e], gden);
+        }
+    const float lv = lse_r[t];
+    const float gl = fadd(fadd(0.f, fmul(g_s, lv)), fmul(g_s, lv));
+    float dot = 0.f;
+#pragma unroll
+    for (int e = 0; e < MAXM; ++e)
+        if (e < M) dot = fadd(dot, fmul(gp[e], p[e]));
+    float* grow = glog + static_cast<int64_t>(t) * M;
+#pragma unroll
+    for (int e = 0; e < MAXM; ++e) {
+        if (e < M) {
+            gp[e] = fadd(fadd(0.f, fmul(gl, p[e])), fmul(p[e], fsub(gp[e], dot)));  // = glog_e
+            grow[e] = gp[e];
+        }
+    }
+    // normed.grad: expert dX (descending experts) then + sum_e glog_e * R[q][e]
+    const float* x = h + static_cast<int64_t>(t) * d;
+    float* gy = gnormed + static_cast<int64_t>(t) * d;
+    const float inv = inv_rms[t];
+    float dot2 = 0.f;
+    for (int q = 0; q < d; ++q) {
+        float a = 0.f;
+        for (int s = k - 1; s >= 0; --s) a = fadd(a, __ldg(dxp + static_cast<int64_t>(rows[s]) * d + q));
+        const float* rr = R + static_cast<int64_t>(q) * M;
+        float sr = 0.f;
+#pragma unroll
+        for (int e = 0; e < MAXM; ++e)
+            if (e < M) sr = fadd(sr, fmul(gp[e], __ldg(rr + e)));
+        a = fadd(a, sr);
+        gy[q] = a;
+        dot2 = fadd(dot2, fmul(fmul(a, __ldg(gain + q)), x[q]));
+    }
+    const float coef = fdiv(fmul(fmul(fmul(dot2, inv), inv), inv), static_cast<float>(d));
+    float* ghr = gh + static_cast<int64_t>(t) * d;
+    for (int q = 0; q < d; ++q) {
+        const float a = gy[q];
+        ghr[q] = fadd(ghr[q], fsub(fmul(fmul(a, __ldg(gain + q)), inv), fmul(coef, x[q])));
+    }
+}
+
+void router_backward(const float* h, const float* gain, const float* router, const float* probs,
+                     const float* lse_r, const float* inv_rms, const float* denom,
+                     const int32_t* topk_idx, const int32_t* slot_row, const float* gw_part,
+                     const float* dxp, const float* lb_coeff, int64_t T, int64_t d, int M, int k,
+                     int renorm, float g_lbsum, float g_s, float* glog, float* gnormed,
+                     float* gh, cudaStream_t s) {
+    dim3 grid(static_cast<unsigned>(cdiv(T, 128)));
+#define SPES_RB(MM)                                                                              \
+    router_bwd_k<MM><<<grid, 128, 0, s>>>(h, gain, router, probs, lse_r, inv_rms, denom, topk_idx, \
+                                          slot_row, gw_part, dxp, lb_coeff, (int)T, (int)d, M, k,  \
+                                          renorm, g_lbsum, g_s, glog, gnormed, gh)
+    if (M <= 8)
+        SPES_RB(8);
+    else if (M <= 16)
+        SPES_RB(16);
+    else if (M <= 32)
+        SPES_RB(32);
+    else
+        SPES_RB(64);
+#undef SPES_RB
+    count_launch();
+}
+
+// ============================ norm-gain and router weight gradients ============================
+// g_gain[q] = sum_t (gy*x)*inv ; g_router[q][e] = sum_t normed[t][q]*glog[t][e]
+// Fixed-order partials over TC token chunks, then a fixed-order sum.
+constexpr int NRG_TC = 16;
+template <int MAXM>
+__global__ void __launch_bounds__(256) norm_router_partial_k(
+    const float* __restrict__ h, const float* __restrict__ normed, const float* __restrict__ gnormed,
+    const float* __restrict__ glog, const float* __restrict__ inv_rms, int T, int d, int M,
+    float* __restrict__ partial) {
+    const int q = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int ph = threadIdx.x >> 5;  // 8 phases
+    const int chunk = blockIdx.y;
+    const int per = (T + NRG_TC - 1) / NRG_TC;
+    const int t0 = chunk * per, t1 = min(T, t0 + per);
+    float gg = 0.f, gr[MAXM];
+#pragma unroll
+    for (int e = 0; e < MAXM; ++e) gr[e] = 0.f;
+    for (int t = t0 + ph; t < t1; t += 8) {
+        const int64_t o = static_cast<int64_t>(t) * d + q;
+        gg += (gnormed[o] * h[o]) * inv_rms[t];
+        const float nv = normed[o];
+        const float* gl = glog + static_cast<int64_t>(t) * M;
+#pragma unroll
+        for (int e = 0; e < MAXM; ++e)
+            if (e < M) gr[e] += nv * __ldg(gl + e);
+    }
+    extern __shared__ float sh[];  // [8][32][M+1]
+    float* mine = sh + (ph * 32 + (threadIdx.x & 31)) * (M + 1);
+    mine[0] = gg;
+#pragma unroll
+    for (int e = 0; e < MAXM; ++e)
+        if (e < M) mine[1 + e] = gr[e];
+    __syncthreads();
+    if (ph == 0) {
+        float* outp = partial + (static_cast<int64_t>(chunk) * d + q) * (M + 1);
+        for (int c = 0; c <= M; ++c) {
+            float s = 0.f;
+            for (int i = 0; i < 8; ++i) s += sh[(i * 32 + (threadIdx.x & 31)) * (M + 1) + c];
+            outp[c] = s;
+        }
+    }
+}
+
+__global__ void norm_router_finish_k(const float* __restrict__ partial, int d, int M,
+                                     float* __restrict__ g_gain, float* __restrict__ g_router) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= static_cast<int64_t>(d) * (M + 1)) return;
+    const int q = static_cast<int>(i / (M + 1)), c = static_cast<int>(i % (M + 1));
+    float s = 0.f;
+    for (int ch = 0; ch < NRG_TC; ++ch) s += partial[(static_cast<int64_t>(ch) * d + q) * (M + 1) + c];
+    if (c == 0)
+        g_gain[q] = s;
+    else
+        g_router[static_cast<int64_t>(q) * M + (c - 1)] = s;
+}
+
+void norm_router_grads(const float* h, const float* normed, const float* gnormed,
+                       const float* glog, const float* inv_rms, int64_t T, int64_t d, int M,
+                       float* partial, float* g_gain, float* g_router, cudaStream_t s) {
+    dim3 grid(static_cast<unsigned>(d / 32), NRG_TC);
+    const size_t smem = sizeof(float) * 8 * 32 * (M + 1);
+#define SPES_NR(MM)                                                                           \
+    do {                                                                                      \
+        cudaFuncSetAttribute(norm_router_partial_k<MM>,                                       \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
+        norm_router_partial_k<MM><<<grid, 256, smem, s>>>(h, normed, gnormed, glog, inv_rms,  \
+                                                          (int)T, (int)d, M, partial);        \
+    } while (0)
+    if (M <= 8)
+        SPES_NR(8);
+    else if (M <= 16)
+        SPES_NR(16);
+    else if (M <= 32)
+        SPES_NR(32);
+    else
+        SPES_NR(64);
+#undef SPES_NR
+    const int64_t n = d * (M + 1);
+    norm_router_finish_k<<<static_cast<unsigned>(cdiv(n, 256)), 256, 0, s>>>(partial, (int)d, M,
+                                                                            g_gain, g_router);
+    count_launch(2);
+}
+
+// ============================ embedding gradient ============================
+// g_emb[v] = sum over t ascending with inputs[t] == v of gh0[t] (graph.hpp:220-229):
+// one block per (vocab id, 1024-column slab); the token list is compacted in
+// order, the sum per column is sequential => bit-exact given identical gh0.
+__global__ void __launch_bounds__(256) embed_grad_k(const int32_t* __restrict__ inputs,
+                                                    const float* __restrict__ gh0, int64_t T,
+                                                    int64_t d, float* __restrict__ g_emb) {
+    __shared__ int32_t list[256];
+    __shared__ int32_t wcount[8];
+    const int v = blockIdx.x;
+    const int64_t q = static_cast<int64_t>(blockIdx.y) * 1024 + threadIdx.x * 4;
+    const bool active = q < d;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t base = 0; base < T; base += 256) {
+        const int64_t t = base + threadIdx.x;
+        const bool hit = t < T && inputs[t] == v;
+        const uint32_t m = __ballot_sync(0xffffffffu, hit);
+        if (lane == 0) wcount[warp] = __popc(m);
+        __syncthreads();
+        int off = 0, tot = 0;
+        for (int w = 0; w < 8; ++w) {
+            if (w < warp) off += wcount[w];
+            tot += wcount[w];
+        }
+        if (hit) list[off + __popc(m & lanemask_lt())] = static_cast<int32_t>(t);
+        __syncthreads();
+        if (active)
+            for (int i = 0; i < tot; ++i) {
+                const float4 g = __ldg(reinterpret_cast<const float4*>(gh0 + static_cast<int64_t>(list[i]) * d + q));
+                acc.x = fadd(acc.x, g.x);
+                acc.y = fadd(acc.y, g.y);
+                acc.z = fadd(acc.z, g.z);
+                acc.w = fadd(acc.w, g.w);
+            }
+        __syncthreads();
+    }
+    if (active) *reinterpret_cast<float4*>(g_emb + static_cast<int64_t>(v) * d + q) = acc;
+}
+
+void embed_grad(const int32_t* inputs, const float* gh0, int64_t T, int64_t d, int64_t V,
+                float* g_emb, cudaStream_t s) {
+    dim3 grid(static_cast<unsigned>(V), static_cast<unsigned>(cdiv(d, 1024)));
+    embed_grad_k<<<grid, 256, 0, s>>>(inputs, gh0, T, d, g_emb);
+    count_launch();
+}
+
+// ============================ AdamW ============================
+// MaskedAdamW::step element update (trainer.hpp:85-92), exact fp32 op order,
+// over the compact trainable segments (psi + owned experts).
+__global__ void __launch_bounds__(256) adamw_k(float* __restrict__ params,
+                                               const float* __restrict__ grads,
+                                               float* __restrict__ m, float* __restrict__ v,
+                                               const AdamSeg* __restrict__ segs, int nseg,
+                                               int64_t total4, float lr, float b1, float b2,
+                                               float omb1, float omb2, float eps, float wd,
+                                               float bc1, float bc2) {
+    for (int64_t i4 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i4 < total4;
+         i4 += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = i4 * 4;
+        int lo = 0, hi = nseg - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (segs[mid].comp_off <= i) lo = mid; else hi = mid - 1;
+        }
+        const int64_t p = segs[lo].param_off + (i - segs[lo].comp_off);
+        float4 th = *reinterpret_cast<float4*>(params + p);
+        const float4 g = *reinterpret_cast<const float4*>(grads + i);
+        float4 mm = *reinterpret_cast<float4*>(m + i);
+        float4 vv = *reinterpret_cast<float4*>(v + i);
+        float* thp = &th.x;
+        const float* gp = &g.x;
+        float* mp = &mm.x;
+        float* vp = &vv.x;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float gi = gp[u];
+            mp[u] = fadd(fmul(b1, mp[u]), fmul(omb1, gi));
+            vp[u] = fadd(fmul(b2, vp[u]), fmul(fmul(omb2, gi), gi));
+            const float mhat = fdiv(mp[u], bc1);
+            const float vhat = fdiv(vp[u], bc2);
+            const float upd = fmul(lr, fadd(fdiv(mhat, fadd(fsqrt(vhat), eps)), fmul(wd, thp[u])));
+            thp[u] = fsub(thp[u], upd);
+        }
+        *reinterpret_cast<float4*>(params + p) = th;
+        *reinterpret_cast<float4*>(m + i) = mm;
+        *reinterpret_cast<float4*>(v + i) = vv;
+    }
+}
+
+void adamw(float* params, const float* grads, float* m, float* v, const AdamSeg* segs, int nseg,
+           int64_t total, float lr, float b1, float b2, float omb1, float omb2, float eps,
+           float wd, float bc1, float bc2, cudaStream_t s) {
+    const int64_t total4 = total / 4;
+    const int blocks = static_cast<int>(std::min<int64_t>(cdiv(total4, 256), 148 * 8));
+    adamw_k<<<blocks, 256, 0, s>>>(params, grads, m, v, segs, nseg, total4, lr, b1, b2, omb1,
+                                   omb2, eps, wd, bc1, bc2);
+    count_launch();
+}
+
+// ============================ bf16 operand shadows ============================
+// mode 0: plain (dst col = c); mode 1: gate interleave; mode 2: up interleave.
+__device__ __forceinline__ int64_t map_col(int64_t c, int mode) {
+    return mode == 0 ? c : (mode == 1 ? il_gate(c) : il_up(c));
+}
+
+// src fp32 [R x C] -> dst bf16 [R x ldd] (cols mapped) and dstT bf16 [mapped C rows x R]
+__device__ void cvt_tile(const float* __restrict__ src, int64_t R, int64_t C, bf16* __restrict__ dst,
+                         int64_t ldd, bf16* __restrict__ dstT, int mode, int64_t tr, int64_t tc,
+                         float (*tile)[65]) {
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int64_t r0 = tr * 64, c0 = tc * 64;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int rr = ty + 16 * i;
+        const float4 v = __ldg(reinterpret_cast<const float4*>(src + (r0 + rr) * C + c0 + 4 * tx));
+        tile[rr][4 * tx + 0] = v.x;
+        tile[rr][4 * tx + 1] = v.y;
+        tile[rr][4 * tx + 2] = v.z;
+        tile[rr][4 * tx + 3] = v.w;
+        __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&a);
+        pk.y = *reinterpret_cast<uint32_t*>(&b);
+        *reinterpret_cast<uint2*>(dst + (r0 + rr) * ldd + map_col(c0 + 4 * tx, mode)) = pk;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int cc = ty + 16 * i;
+        __nv_bfloat162 a = __floats2bfloat162_rn(tile[4 * tx + 0][cc], tile[4 * tx + 1][cc]);
+        __nv_bfloat162 b = __floats2bfloat162_rn(tile[4 * tx + 2][cc], tile[4 * tx + 3][cc]);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&a);
+        pk.y = *reinterpret_cast<uint32_t*>(&b);
+        *reinterpret_cast<uint2*>(dstT + map_col(c0 + cc, mode) * R + r0 + 4 * tx) = pk;
+    }
+    __syncthreads();
+}
+
+// grid: x = tile index within the three matrices of one expert, y = expert in list
+__global__ void __launch_bounds__(256) expert_shadows_k(const float* __restrict__ params,
+                                                        const int64_t* __restrict__ expert_offs,
+                                                        const int64_t* __restrict__ shadow_offs,
+                                                        int64_t d, int64_t f, bf16* w1t, bf16* w2t,
+                                                        bf16* w1, bf16* w2) {
+    __shared__ float tile[64][65];
+    const int64_t po = expert_offs[blockIdx.y];
+    const int64_t so = shadow_offs[blockIdx.y];  // expert slot index (layer*M + j)
+    const int64_t tg = (d / 64) * (f / 64);       // tiles per d x f matrix
+    int64_t t = blockIdx.x;
+    if (t < 2 * tg) {  // wg (mode 1) or wu (mode 2): [d x f]
+        const int mode = t < tg ? 1 : 2;
+        if (t >= tg) t -= tg;
+        const float* src = params + po + (mode == 2 ? d * f : 0);
+        cvt_tile(src, d, f, w1 + so * d * 2 * f, 2 * f, w1t + so * 2 * f * d, mode, t / (f / 64),
+                 t % (f / 64), tile);
+    } else {  // wd: [f x d]
+        t -= 2 * tg;
+        const float* src = params + po + 2 * d * f;
+        cvt_tile(src, f, d, w2 + so * f * d, d, w2t + so * d * f, 0, t / (d / 64), t % (d / 64),
+                 tile);
+    }
+}
+
+void expert_shadows(const float* params, const int64_t* expert_offs, int n_experts,
+                    const int64_t* shadow_offs, int64_t d, int64_t f, bf16* w1t, bf16* w2t,
+                    bf16* w1, bf16* w2, cudaStream_t s) {
+    if (n_experts == 0) return;
+    dim3 grid(static_cast<unsigned>(3 * (d / 64) * (f / 64)), static_cast<unsigned>(n_experts));
+    expert_shadows_k<<<grid, 256, 0, s>>>(params, expert_offs, shadow_offs, d, f, w1t, w2t, w1, w2);
+    count_launch();
+}
+
+__global__ void __launch_bounds__(256) head_shadows_k(const float* __restrict__ head, int64_t d,
+                                                      int64_t V, bf16* headB, bf16* headT) {
+    __shared__ float tile[64][65];
+    cvt_tile(head, d, V, headB, V, headT, 0, blockIdx.x / (V / 64), blockIdx.x % (V / 64), tile);
+}
+
+void head_shadows(const float* head, int64_t d, int64_t V, bf16* headB, bf16* headT,
+                  cudaStream_t s) {
+    head_shadows_k<<<static_cast<unsigned>((d / 64) * (V / 64)), 256, 0, s>>>(head, d, V, headB,
+                                                                             headT);
+    count_launch();
+}
+
+// ============================ sync: owner-set mean ============================
+// out[i] = float((sum over sources in order of double(x)) * (1.0/n))  (protocol.cpp:238-243)
+__global__ void owner_mean_strided_k(const float* __restrict__ x, int n_src, int64_t stride,
+                                     int64_t n, float* __restrict__ out) {
+    const double inv = 1.0 / static_cast<double>(n_src);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double acc = 0.0;
+        for (int s = 0; s < n_src; ++s) acc = __dadd_rn(acc, static_cast<double>(x[s * stride + i]));
+        out[i] = __double2float_rn(__dmul_rn(acc, inv));
+    }
+}
+
+void owner_mean_strided(const float* x, int n_src, int64_t stride, int64_t n, float* out,
+                        cudaStream_t s) {
+    const int blocks = static_cast<int>(std::min<int64_t>(cdiv(n, 256), 148 * 16));
+    owner_mean_strided_k<<<blocks, 256, 0, s>>>(x, n_src, stride, n, out);
+    count_launch();
+}
+
+struct SrcList {
+    const float* p[16];
+};
+__global__ void owner_mean_list_k(SrcList L, int n_src, int64_t n, float* __restrict__ out) {
+    const double inv = 1.0 / static_cast<double>(n_src);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double acc = 0.0;
+        for (int s = 0; s < n_src; ++s) acc = __dadd_rn(acc, static_cast<double>(L.p[s][i]));
+        out[i] = __double2float_rn(__dmul_rn(acc, inv));
+    }
+}
+
+void owner_mean(const float* const* srcs, int n_src, int64_t n, float* out, cudaStream_t s) {
+    SrcList L{};
+    for (int i = 0; i < n_src && i < 16; ++i) L.p[i] = srcs[i];
+    const int blocks = static_cast<int>(std::min<int64_t>(cdiv(n, 256), 148 * 16));
+    owner_mean_list_k<<<blocks, 256, 0, s>>>(L, n_src, n, out);
+    count_launch();
+}
+
+// ============================ merge: Gram + apply ============================
+// Projection vector of expert j: D1 floats at vec_offs[j] (+ a second D1 run at
+// +gap when two_parts: Concat source). Partial fp64 dot products per chunk.
+constexpr int GRAM_SUB = 128;
+__global__ void __launch_bounds__(256) gram_partial_k(const float* __restrict__ params,
+                                                      const int64_t* __restrict__ vec_offs, int M,
+                                                      int64_t D1, int64_t gap, int two_parts,
+                                                      double* __restrict__ partial, int nchunks) {
+    extern __shared__ float sv[];  // [M][GRAM_SUB]
+    const int64_t D = two_parts ? 2 * D1 : D1;
+    const int npairs = M * (M + 1) / 2;
+    const int64_t per = ((D + nchunks - 1) / nchunks + GRAM_SUB - 1) / GRAM_SUB * GRAM_SUB;
+    const int64_t e0 = static_cast<int64_t>(blockIdx.x) * per, e1 = min(D, e0 + per);
+    constexpr int PPT = 16;  // pairs per thread (M <= 64 -> 2080 pairs / 256 threads <= 9)
+    double acc[PPT];
+    int pa[PPT], pb[PPT];
+#pragma unroll
+    for (int u = 0; u < PPT; ++u) {
+        acc[u] = 0.0;
+        const int pidx = threadIdx.x + u * 256;
+        int a = 0, rem = pidx;
+        if (pidx < npairs)
+            while (rem >= M - a) {
+                rem -= M - a;
+                ++a;
+            }
+        pa[u] = a;
+        pb[u] = a + rem;
+    }
+    for (int64_t b = e0; b < e1; b += GRAM_SUB) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < M * GRAM_SUB; i += blockDim.x) {
+            const int j = i / GRAM_SUB;
+            const int64_t e = b + (i % GRAM_SUB);
+            float v = 0.f;
+            if (e < e1) {
+                const int64_t src = (two_parts && e >= D1) ? vec_offs[j] + gap + (e - D1) : vec_offs[j] + e;
+                v = params[src];
+            }
+            sv[i] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < PPT; ++u) {
+            const int pidx = threadIdx.x + u * 256;
+            if (pidx < npairs) {
+                const float* va = sv + pa[u] * GRAM_SUB;
+                const float* vb = sv + pb[u] * GRAM_SUB;
+                double s = acc[u];
+                for (int i = 0; i < GRAM_SUB; ++i) s += static_cast<double>(va[i]) * vb[i];
+                acc[u] = s;
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < PPT; ++u) {
+        const int pidx = threadIdx.x + u * 256;
+        if (pidx < npairs) partial[static_cast<int64_t>(blockIdx.x) * npairs + pidx] = acc[u];
+    }
+}
+
+void gram_partials(const float* params, const int64_t* vec_offs, int M, int64_t D1, int64_t gap,
+                   int two_parts, double* partial, int nchunks, cudaStream_t s) {
+    const size_t smem = sizeof(float) * M * GRAM_SUB;
+    cudaFuncSetAttribute(gram_partial_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    gram_partial_k<<<nchunks, 256, smem, s>>>(params, vec_offs, M, D1, gap, two_parts, partial,
+                                             nchunks);
+    count_launch();
+}
+
+// sim[a][b] = dot/(norm_a*norm_b) (merging.hpp:55-82); zero norm -> 0
+__global__ void gram_finish_k(const double* __restrict__ partial, int M, int nchunks,
+                              double* __restrict__ sim) {
+    __shared__ double g[64 * 65 / 2 + 64];
+    const int npairs = M * (M + 1) / 2;
+    for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+        double s = 0.0;
+        for (int c = 0; c < nchunks; ++c) s += partial[static_cast<int64_t>(c) * npairs + p];
+        g[p] = s;
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+        int a = 0, rem = p;
+        while (rem >= M - a) {
+            rem -= M - a;
+            ++a;
+        }
+        const int b = a + rem;
+        auto diag = [&](int j) {
+            int idx = 0;
+            for (int i = 0; i < j; ++i) idx += M - i;
+            return g[idx];
+        };
+        const double na = sqrt(diag(a)), nb = sqrt(diag(b));
+        double v = 0.0;
+        if (na > 0.0 && nb > 0.0) v = g[p] / (na * nb);
+        sim[a * M + b] = v;
+        sim[b * M + a] = v;
+    }
+}
+
+void gram_finish(const double* partial, int M, int nchunks, double* sim, cudaStream_t s) {
+    gram_finish_k<<<1, 256, 0, s>>>(partial, M, nchunks, sim);
+    count_launch();
+}
+
+// In place, simultaneous: thread i reads element i of every expert before writing any
+// (merging.hpp:106-135: phi_j <- float(phi_j + alpha/|Q|*sum_p (phi_p - phi_j)) in fp64).
+template <int MAXM>
+__global__ void __launch_bounds__(256) merge_apply_k(float* __restrict__ params,
+                                                     const int64_t* __restrict__ expert_offs,
+                                                     int M, int64_t per,
+                                                     const int32_t* __restrict__ peers, int K,
+                                                     const double* __restrict__ coef,
+                                                     double* __restrict__ disp_partial) {
+    __shared__ int32_t sp[64 * 64];
+    __shared__ double sc[64];
+    __shared__ int64_t so[64];
+    __shared__ double red[256];
+    extern __shared__ float snap[];  // [M][256]: element i of every expert, per thread
+    for (int i = threadIdx.x; i < M * K; i += blockDim.x) sp[i] = peers[i];
+    for (int i = threadIdx.x; i < M; i += blockDim.x) {
+        sc[i] = coef[i];
+        so[i] = expert_offs[i];
+    }
+    __syncthreads();
+    double disp = 0.0;
+    const int tid = threadIdx.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + tid; i < per;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        for (int j = 0; j < M; ++j) snap[j * 256 + tid] = params[so[j] + i];
+        for (int j = 0; j < M; ++j) {
+            const double self = static_cast<double>(snap[j * 256 + tid]);
+            double acc = 0.0;
+            for (int q = 0; q < K; ++q)
+                acc = __dadd_rn(acc, __dsub_rn(static_cast<double>(snap[sp[j * K + q] * 256 + tid]), self));
+            const double delta = __dmul_rn(sc[j], acc);
+            disp += delta * delta;
+            params[so[j] + i] = __double2float_rn(__dadd_rn(self, delta));
+        }
+    }
+    red[tid] = disp;
+    __syncthreads();
+    if (tid == 0) {
+        double s = 0.0;
+        for (int i = 0; i < (int)blockDim.x; ++i) s += red[i];
+        disp_partial[blockIdx.x] = s;
+    }
+}
+
+void merge_apply(float* params, const int64_t* expert_offs, int M, int64_t per,
+                 const int32_t* peers, int K, const double* coef, double* disp_partial,
+                 int nblocks, cudaStream_t s) {
+    const size_t smem = sizeof(float) * M * 256;
+    cudaFuncSetAttribute(merge_apply_k<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    merge_apply_k<64><<<nblocks, 256, smem, s>>>(params, expert_offs, M, per, peers, K, coef,
+                                                 disp_partial);
+    count_launch();
+}
+
+// ============================ expf port probe ============================
+__global__ void expf_port_k(const float* __restrict__ x, float* __restrict__ y, int64_t n,
+                            int variant) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        y[i] = variant ? spes_expf::expf_glibc<1>(x[i]) : spes_expf::expf_glibc<0>(x[i]);
+}
+
+void expf_port_device(const float* x, float* y, int64_t n, int variant, cudaStream_t s) {
+    expf_port_k<<<148 * 16, 256, 0, s>>>(x, y, n, variant);
+    count_launch();
+}
+
+}  // namespace spes_k

@@ -1,0 +1,137 @@
+// Host-side launchers of the SPES device kernels (kernels.cu, gemm.cu).
+// All launches go to the given stream; nothing here synchronizes.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "grouped_gemm.cuh"
+
+namespace spes_k {
+
+using bf16 = __nv_bfloat16;
+using spes_dev::GemmGroup;
+
+// Counts every kernel launch (for the bench's gpu_launches claim).
+extern thread_local int64_t* g_launch_counter;
+inline void count_launch(int n = 1) {
+    if (g_launch_counter) *g_launch_counter += n;
+}
+
+struct AdamSeg {
+    int64_t param_off;  // offset in the fp32 parameter vector
+    int64_t comp_off;   // offset in the compact (trainable-only) grad / m / v buffers
+    int64_t len;
+};
+
+// ---- forward ----
+void embed_gather(const float* emb, const int32_t* tokens, int64_t B, int64_t S, int64_t d,
+                  int64_t V, float* h, int32_t* inputs, int32_t* targets, int32_t* err,
+                  cudaStream_t s);
+void router_forward(const float* h, const float* gain, const float* router, int64_t T, int64_t d,
+                    int M, int k, int renorm, float eps, int expf_variant, float* normed,
+                    float* logits, float* probs, int32_t* topk_idx, float* topk_w, float* lse,
+                    float* inv_rms, float* denom, cudaStream_t s);
+// Deterministic counting sort of the (token, slot) pairs, expert-major and
+// token-ascending (model.hpp:314-318), each expert padded to 128 rows; also
+// builds the GEMM group tables of this layer on the device.
+struct RoutePlan {
+    int32_t* chunk_counts;  // [nchunks][M]
+    int32_t* counts;        // [M]
+    int32_t* pad_off;       // [M+1]
+    float* lb_coeff;        // [M]
+    int32_t* slot_row;      // [T][k]
+    int32_t* row_token;     // [R_cap]  (-1 = padding)
+    float* row_w;           // [R_cap]
+    GemmGroup* groups;      // [6][M]: fwd1, fwd2, dH, dX, dW1, dW2
+    int32_t* tiles;         // [6] total tiles per GEMM
+};
+struct GroupBases {  // output bases written into the group tables
+    bf16* gu;
+    float* y;
+    bf16* dgu;
+    float* dxp;
+    float* grad_expert_base;       // compact grad buffer
+    const int64_t* grad_off_layer; // [M]: offset of expert j of this layer in grads, -1 = frozen
+    int64_t d, f;
+    int bn_fwd2, bn_dh, bn_dx, bn_dw2;
+};
+void route_plan(const int32_t* topk_idx, const float* topk_w, int64_t T, int M, int k,
+                int64_t R_cap, const RoutePlan& p, const GroupBases& gb, cudaStream_t s);
+// rows of src (fp32, row_map[r] or r when row_map == nullptr, -1 => zero row) as bf16
+// [rows x cols] and transposed [cols x rows_cap]; rows processed: *nrows (device) or rows.
+void gather_rows_bf16(const float* src, int64_t ld_src, const int32_t* row_map,
+                      const int32_t* nrows_dev, int64_t rows, int64_t cols, bf16* dst,
+                      bf16* dstT, int64_t rows_cap, cudaStream_t s);
+void combine_forward(const float* h, const float* y, const int32_t* slot_row,
+                     const int32_t* topk_idx, const float* topk_w, int64_t T, int64_t d, int k,
+                     float* h_next, cudaStream_t s);
+// CE + z on head logits; writes dlogits fp32 (padding rows zero) and per-token terms.
+void head_ce(const float* logits, const int32_t* targets, int64_t T, int64_t T_pad, int64_t V,
+             int expf_variant, float g_s2, float g_ssum, float* dlogits, float* diff,
+             float* lse, cudaStream_t s);
+// Loss scalars (tolerance-level, deterministic tree order) -> out[5] (doubles)
+void losses_reduce(const float* diff, const float* lse_head, const float* lse_r,
+                   const float* probs, const float* lb_coeff, int64_t T, int64_t Tstride, int L,
+                   int M,
+                   float inv_T, float inv_L, float c_ce, float c_lb, float c_mz, float c_z,
+                   double* out, cudaStream_t s);
+
+// ---- backward ----
+void combine_backward(const float* gh, const float* y, const int32_t* row_token,
+                      const float* row_w, const int32_t* R_total_dev, int64_t R_cap, int64_t d,
+                      bf16* dyw, bf16* dywT, float* gw_part, cudaStream_t s);
+void router_backward(const float* h, const float* gain, const float* router, const float* probs,
+                     const float* lse_r, const float* inv_rms, const float* denom,
+                     const int32_t* topk_idx, const int32_t* slot_row, const float* gw_part,
+                     const float* dxp, const float* lb_coeff, int64_t T, int64_t d, int M, int k,
+                     int renorm, float g_lbsum, float g_s, float* glog, float* gnormed,
+                     float* gh, cudaStream_t s);
+void norm_router_grads(const float* h, const float* normed, const float* gnormed,
+                       const float* glog, const float* inv_rms, int64_t T, int64_t d, int M,
+                       float* partial, float* g_gain, float* g_router, cudaStream_t s);
+void embed_grad(const int32_t* inputs, const float* gh0, int64_t T, int64_t d, int64_t V,
+                float* g_emb, cudaStream_t s);
+
+// ---- optimizer / shadows ----
+void adamw(float* params, const float* grads, float* m, float* v, const AdamSeg* segs, int nseg,
+           int64_t total, float lr, float b1, float b2, float omb1, float omb2, float eps,
+           float wd, float bc1, float bc2, cudaStream_t s);
+// bf16 operand layouts of expert (l, j) = 4 GEMM-ready copies
+void expert_shadows(const float* params, const int64_t* expert_offs, int n_experts,
+                    const int64_t* shadow_offs, int64_t d, int64_t f, bf16* w1t, bf16* w2t,
+                    bf16* w1, bf16* w2, cudaStream_t s);
+void head_shadows(const float* head, int64_t d, int64_t V, bf16* headB, bf16* headT,
+                  cudaStream_t s);
+
+// ---- sync / merge ----
+void owner_mean(const float* const* srcs, int n_src, int64_t n, float* out, cudaStream_t s);
+void owner_mean_strided(const float* x, int n_src, int64_t stride, int64_t n, float* out,
+                        cudaStream_t s);
+void gram_partials(const float* params, const int64_t* vec_offs, int M, int64_t D1,
+                   int64_t gap, int two_parts, double* partial, int nchunks, cudaStream_t s);
+void gram_finish(const double* partial, int M, int nchunks, double* sim, cudaStream_t s);
+void merge_apply(float* params, const int64_t* expert_offs, int M, int64_t per,
+                 const int32_t* peers, int K, const double* coef, double* disp_partial,
+                 int nblocks, cudaStream_t s);
+
+// ---- GEMMs (gemm.cu) ----
+struct GemmMaps;  // opaque
+void gemm_swiglu(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
+                 const int32_t* tiles, int max_tiles, bf16* hact, bf16* hactT, int64_t R_cap,
+                 int64_t f, cudaStream_t s);
+void gemm_store_f32(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g,
+                    int ng, const int32_t* tiles, int max_tiles, cudaStream_t s);
+void gemm_dswiglu(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
+                  const int32_t* tiles, int max_tiles, const bf16* gu, bf16* dgu, bf16* dguT,
+                  int64_t R_cap, int64_t f, cudaStream_t s);
+void gemm_grad_w1(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
+                  const int32_t* tiles, int max_tiles, cudaStream_t s);
+void gemm_prepare(int device);
+int num_sms();
+
+// expf port checks
+void expf_port_device(const float* x, float* y, int64_t n, int variant, cudaStream_t s);
+
+}  // namespace spes_k
