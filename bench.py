@@ -1,0 +1,438 @@
+#!/usr/bin/env python
+"""SPES hot-path benchmark (BASELINE.json metric) on 1..8 B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+
+One bench step = one SPES round of the configuration: H local training steps
+(forward + backward + masked AdamW over psi and the owned experts) on every node,
+then the sparse synchronization (owner-set means over NCCL), plus the expert merge
+when the configuration has the warm-up active. Metric = training tokens/s
+(all nodes) = N * H * B * S / round time; the sync is therefore amortised over H
+exactly as in the metric's definition. For N > 1 launch with torchrun; one process
+per GPU; timing = CUDA events on the library's stream, max over ranks.
+
+Timed arms:
+  value : tokens already resident in HBM, no host sync inside a round except the sync step;
+  e2e   : the public C-ABI call with HOST tokens (H2D each step) and the losses read back
+          (D2H each step), wall clock, max over ranks.
+--impl reference times the reference's own CPU implementation (oracle/_ref, compiled
+from /root/reference sources) on this host's cores, on a bounded sample.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "training tokens/sec per SPES step (local + amortised sync) at 1/2/4/8 B200"
+UNIT = "tokens/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--H", type=int, default=None, help="override sync interval")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+class Dist:
+    """torch.distributed over gloo (CPU) for the launcher plumbing only: NCCL id
+    exchange, barriers and the max-over-ranks of the measured times."""
+
+    def __init__(self, rank, world):
+        self.rank, self.world = rank, world
+        self.pg = None
+        if world > 1:
+            import torch.distributed as td
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            td.init_process_group("gloo", rank=rank, world_size=world)
+            self.td = td
+
+    def barrier(self):
+        if self.world > 1:
+            self.td.barrier()
+
+    def bcast(self, obj):
+        if self.world == 1:
+            return obj
+        lst = [obj]
+        self.td.broadcast_object_list(lst, src=0)
+        return lst[0]
+
+    def max(self, x):
+        if self.world == 1:
+            return x
+        import torch
+        t = torch.tensor([float(x)], dtype=torch.float64)
+        self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x):
+        if self.world == 1:
+            return x
+        import torch
+        t = torch.tensor([float(x)], dtype=torch.float64)
+        self.td.all_reduce(t, op=self.td.ReduceOp.SUM)
+        return float(t.item())
+
+
+def workload(name, N, H_override=None):
+    from paper_2602_11543_b200.abi import CONFIGS, model_cfg
+    import paper_2602_11543_b200 as spes
+    c = dict(CONFIGS[name])
+    cfg = model_cfg(**c["model"])
+    M = cfg.experts_total
+    if name == "cfg1":
+        owned = spes.param_partition(cfg, N) if N <= M else None
+        repl = 1
+    else:
+        owned = spes.replicated_ownership(M, N, 2)
+        repl = 2
+    H = H_override or c["H"]
+    desc = {
+        "cfg1": "cfg1 tiny MoE: V=256 d=128 f=256 L=2, 8 experts top-2, disjoint ownership",
+        "cfg2": "cfg2 single MoE block d=1024 f=1024, 16 experts top-2, V=256, 2x replicated "
+                "ownership (8 nodes x 4 owned at N=8), seq 2048, sync every 50 steps",
+        "cfg3": "cfg3 = cfg2 shapes with sync + expert-merging warm-up every round (H=1)",
+        "cfg4": "cfg4 2B-class layer d=2048 f=1024, 64 experts top-8, 2x replicated ownership, "
+                "seq 4096",
+        "cfg5": "cfg5 7B-class stack d=4096 f=2048 L=4, 64 experts top-8, 2x replicated, seq 4096",
+    }[name]
+    return cfg, owned, H, c["B"], c["S"], bool(c.get("merge")), repl, desc
+
+
+def expert_flops_per_step(cfg, counts_by_layer, owned):
+    """Algorithmic tensor FLOPs of one local step:
+    6*d*f*(2*sum_j n_j + sum_{owned} n_j) per layer + head 3 * 2*T*d*V."""
+    d, f = cfg.hidden, cfg.intermediate
+    tot = 0.0
+    for cnt in counts_by_layer:
+        cnt = np.asarray(cnt, np.float64)
+        tot += 6.0 * d * f * (2.0 * cnt.sum() + cnt[list(owned)].sum())
+    return tot
+
+
+def clocks_sampler():
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+    q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    try:
+        p = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                              "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                             text=True)
+    except Exception:
+        return None
+    lines = []
+
+    def rd():
+        for ln in p.stdout:
+            lines.append(ln.strip())
+
+    t = threading.Thread(target=rd, daemon=True)
+    t.start()
+    return p, lines
+
+
+def clocks_summary(handle, device):
+    if handle is None:
+        return None
+    p, lines = handle
+    time.sleep(0.3)
+    p.terminate()
+    try:
+        p.wait(timeout=5)
+    except Exception:
+        p.kill()
+    sm, mx, reasons = [], 0, set()
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    for ln in lines:
+        parts = [x.strip() for x in ln.split(",")]
+        if len(parts) < 9 or not parts[0].isdigit() or int(parts[0]) != device:
+            continue
+        try:
+            sm.append(float(parts[1]))
+            mx = max(mx, float(parts[2]))
+        except ValueError:
+            continue
+        for nm, v in zip(names, parts[5:9]):
+            if v.lower() == "active":
+                reasons.add(nm)
+    if not sm:
+        return None
+    loaded = [x for x in sm if x > 0.5 * mx] or sm
+    return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+            "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p["bf16_tflops"], p["bf16_tflops_sustained"], p["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the grouped GEMM from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_gemm_summary.json")) as fh:
+            return json.load(fh).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ CPU reference
+
+def cpu_reference_sample(cfg_name, N, reps=1):
+    """The reference's own CPU path (oracle/_ref = /root/reference compiled from its sources):
+    one local_round step (build_loss + backward + MaskedAdamW) at B=1, S=256 of the config's
+    shapes with node 0's ownership, plus Server::aggregate of the full model amortised over H.
+    Returns (tokens/s, seconds per sample, threads, description)."""
+    import ctypes as C
+    import oracle
+    from paper_2602_11543_b200.abi import adamw_cfg
+    cfg, owned, H, B, S, merge, repl, desc = workload(cfg_name, N)
+    R = oracle.ref()
+    R.ref_set_parallel(1)
+    P = oracle.param_count(cfg)
+    rng = np.random.default_rng(1)
+    params = (rng.standard_normal(P, dtype=np.float32) * np.float32(0.02))
+    Bs, Ss = 1, 256
+    toks = rng.integers(0, cfg.vocab, size=(1, Bs, Ss + 1), dtype=np.int32)
+    mask = oracle.trainable_mask(cfg, owned[0])
+    opt = adamw_cfg()
+    losses = np.zeros(5)
+    best = None
+    for _ in range(reps):
+        p = params.copy()
+        t0 = time.perf_counter()
+        rc = R.ref_local_round(C.byref(cfg), p, toks, Bs, Ss, 1, None, C.byref(opt), mask, losses)
+        t1 = time.perf_counter()
+        assert rc == 0, rc
+        best = t1 - t0 if best is None else min(best, t1 - t0)
+    # sync: the reference server aggregate over the model (one node copy), amortised over H
+    nodes = params[None, :].repeat(1, axis=0)
+    out = np.zeros(P, np.float32)
+    t0 = time.perf_counter()
+    R.ref_aggregate_partition(C.byref(cfg), 1, nodes, params, out)
+    t_sync = time.perf_counter() - t0
+    per_step = best + t_sync / H
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    sample = (f"{cfg_name} shapes, reference local_round H=1 at B=1 S=256 (256 tokens, full "
+              f"parameter size, node 0 owns {len(owned[0])} experts) + Server::aggregate/{H}; "
+              f"OpenMP threads={threads}")
+    return Ss * Bs / per_step, per_step, threads, sample
+
+
+def reference_arm(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, sec, threads, sample = cpu_reference_sample(args.config, args.gpus)
+        if i >= args.warmup:
+            vals.append((v, sec))
+    value = float(np.mean([v for v, _ in vals]))
+    ms = float(np.mean([s for _, s in vals])) * 1e3
+    cfg, owned, H, B, S, merge, repl, desc = workload(args.config, args.gpus)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+        "config": {"workload": desc, "sample": "bounded CPU sample (see cpu_baseline)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+
+def our_arm(args):
+    import torch
+    import paper_2602_11543_b200 as spes
+    from paper_2602_11543_b200.abi import adamw_cfg, merge_sched
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        log(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using {world}")
+    N = world
+    dist = Dist(rank, world)
+    cfg, owned, H, B, S, merge, repl, desc = workload(args.config, N, args.H)
+    torch.cuda.set_device(local)
+    nccl_id = dist.bcast(spes.nccl_unique_id() if rank == 0 else None) if N > 1 else None
+    node = spes.Node(cfg, node=rank, n_nodes=N, device=local, nccl_id=nccl_id)
+    node.set_ownership(owned)
+    P = spes.param_count(cfg)
+    rng = np.random.default_rng(1)  # identical global init on every node
+    params = rng.standard_normal(P, dtype=np.float32) * np.float32(0.02)
+    offs = spes.block_offsets(cfg)
+    for l in range(cfg.layers):
+        o = offs[2 + 2 * l]
+        params[o:o + cfg.hidden] = 1.0
+    node.load_params(params)
+    del params
+    trng = np.random.default_rng(1000 + rank)  # per-node data shard
+    toks_host = trng.integers(0, cfg.vocab, size=(H, B, S + 1), dtype=np.int32)
+    toks_dev = torch.from_numpy(toks_host).to(f"cuda:{local}")
+    ptrs = [toks_dev[h].data_ptr() for h in range(H)]
+    opt = adamw_cfg(lr=1e-4)
+    sched = merge_sched(warmup_rounds=10 ** 6, interval=1, alpha0=0.1, peers=4, source=0)
+    stream = torch.cuda.ExternalStream(node.stream(), device=f"cuda:{local}")
+
+    round_no = [0]
+
+    def spes_round(host=False):
+        node.round_begin()
+        for h in range(H):
+            if host:
+                node.local_step(toks_host[h], opt)  # H2D tokens + D2H losses every step
+            else:
+                node.local_step_device(ptrs[h], B, S, opt)
+        node.sync()
+        if merge:
+            node.merge_model(sched, round_no[0])
+        round_no[0] += 1
+
+    for _ in range(args.warmup):
+        spes_round()
+    torch.cuda.synchronize(local)
+    dist.barrier()
+
+    # ---- timed region: K rounds, device-resident tokens ----
+    clk = clocks_sampler() if rank == 0 else None
+    node.profile(True, reset=True)
+    launches0 = node.kernel_launches()
+    dist.barrier()
+    torch.cuda.synchronize(local)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        spes_round()
+    e1.record(stream)
+    torch.cuda.synchronize(local)
+    dist.barrier()
+    ms = dist.max(e0.elapsed_time(e1))
+    launches = node.kernel_launches() - launches0
+    node.profile(False)
+    fam = node.profile_stats()
+    clocks = clocks_summary(clk, local) if rank == 0 else None
+
+    tokens = N * H * B * S * args.steps
+    value = tokens / (ms / 1e3)
+
+    # ---- e2e: public API with host tokens and losses read back every step ----
+    ke = args.e2e_steps or max(1, min(args.steps, 3))
+    dist.barrier()
+    torch.cuda.synchronize(local)
+    t0 = time.perf_counter()
+    for _ in range(ke):
+        spes_round(host=True)
+    torch.cuda.synchronize(local)
+    t_e2e = dist.max(time.perf_counter() - t0)
+    e2e_value = N * H * B * S * ke / t_e2e
+
+    # ---- roofline of the grouped tcgen05 GEMM (all its launches in the timed region) ----
+    T = B * S
+    counts = [node.debug("counts", l, np.int32, None, cfg.experts_total) for l in range(cfg.layers)]
+    flops_step = expert_flops_per_step(cfg, counts, owned[rank]) + 3 * 2.0 * T * cfg.hidden * cfg.vocab
+    gemm_fams = [k for k in fam if k.startswith("gemm_") or k in ("head_fwd", "head_bwd")]
+    gemm_ms = sum(fam[k][0] for k in gemm_fams if k.startswith("gemm_"))
+    gemm_launches = sum(fam[k][1] for k in gemm_fams if k.startswith("gemm_"))
+    expert_flops = expert_flops_per_step(cfg, counts, owned[rank]) * H * args.steps
+    burst, sustained, hbm, peak_src = peaks()
+    achieved = expert_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else 0.0
+    step_ms_total = sum(v[0] for v in fam.values())
+    if rank == 0:
+        log("kernel family breakdown (device ms over the timed region, share of profiled time):")
+        for k, (t, n) in sorted(fam.items(), key=lambda kv: -kv[1][0]):
+            log(f"  {k:24s} {t:10.3f} ms  {n:6d} launches  {100 * t / max(step_ms_total, 1e-9):5.1f}%")
+        # HBM-bound kernels: algorithmic bytes per launch
+        hb = {}
+        G = node.counts()["grad_scalars"]
+        if "adamw" in fam:
+            bytes_adamw = 28.0 * G  # theta,g,m,v read; theta,m,v written (fp32)
+            hb["adamw"] = bytes_adamw * fam["adamw"][1] / (fam["adamw"][0] / 1e3) / 1e9
+        log("HBM-bound kernels (GB/s, algorithmic bytes): " + json.dumps(hb))
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": desc, "name": args.config, "d": cfg.hidden, "f": cfg.intermediate,
+                   "layers": cfg.layers, "experts": cfg.experts_total, "top_k": cfg.experts_active,
+                   "vocab": cfg.vocab, "B": B, "S": S, "H": H, "global_batch": N * B,
+                   "seq_len": S, "nodes": N, "replication": repl,
+                   "owned_per_node": len(owned[rank]), "merge_every_round": merge,
+                   "parallelism": f"spes-dp{N} (expert ownership, sparse sync)",
+                   "step": f"one SPES round = {H} local steps + sparse sync"
+                           + (" + merge" if merge else ""),
+                   "l2": "inputs larger than L2: per-step activations >> 126 MB, no flush"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(H * B * (S + 1) * 4),
+                "d2h_bytes_per_step": int(H * 5 * 8), "steps": ke},
+        "gpu_launches": int(dist.sum(launches)),
+        "roofline": {"bound": "tensor", "kernel": "grouped_gemm_kernel (tcgen05/TMEM/TMA, "
+                                                   "6 expert contractions)",
+                     "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
+                     "frac": achieved / sustained if sustained else None,
+                     "peak_kind": f"bf16 sustained ({peak_src})",
+                     "frac_of_burst": achieved / burst if burst else None,
+                     "traffic": ncu_traffic(), "launches": int(gemm_launches),
+                     "flops_source": "6*d*f*(2*sum n_j + sum_owned n_j) per layer, last step's "
+                                     "routing counts"},
+        "kernels_ms": {k: round(v[0], 4) for k, v in fam.items()},
+        "clocks": clocks,
+    }
+    if rank == 0 and N == 1 and not args.no_cpu_baseline:
+        try:
+            v, sec, threads, sample = cpu_reference_sample(args.config, N)
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads,
+                                    "kind": "reference", "sample": sample}
+        except Exception as e:  # the reference lib is test infra; report, don't fail
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                                    "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    node.close()
+    return 0
+
+
+def main():
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+    return our_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

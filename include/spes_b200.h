@@ -170,6 +170,13 @@ spes_status spes_debug_read(spes_ctx* ctx, const char* name, int32_t layer, void
                             int64_t bytes);
 /* Gradient of the last step, full parameter layout (zeros for frozen blocks). */
 spes_status spes_read_grads(spes_ctx* ctx, float* host, int64_t n);
+/* Live per-kernel-family timing: CUDA events bracket every launch family on the
+ * context stream while enabled; totals accumulate until spes_profile_reset. */
+spes_status spes_profile(spes_ctx* ctx, int32_t enable);
+spes_status spes_profile_reset(spes_ctx* ctx);
+int32_t spes_profile_count(spes_ctx* ctx);
+spes_status spes_profile_get(spes_ctx* ctx, int32_t index, char* name64, double* total_ms,
+                             int64_t* launches);
 /* The CUDA stream all work of this context is issued on (cudaStream_t). */
 void* spes_stream(spes_ctx* ctx);
 /* Number of kernels this context launched since creation. */

@@ -87,6 +87,12 @@ def lib():
         L.spes_debug_read.argtypes = [vp, C.c_char_p, i32, vp, i64]
         L.spes_stream.restype = vp
         L.spes_stream.argtypes = [vp]
+        L.spes_profile.argtypes = [vp, i32]
+        L.spes_profile_reset.argtypes = [vp]
+        L.spes_profile_count.restype = i32
+        L.spes_profile_count.argtypes = [vp]
+        L.spes_profile_get.argtypes = [vp, i32, C.c_char_p, C.POINTER(C.c_double),
+                                       C.POINTER(i64)]
         L.spes_kernel_launches.restype = i64
         L.spes_kernel_launches.argtypes = [vp]
         L.spes_kernel_router.argtypes = [cfgp, f32p, f32p, f32p, i64, f32p, f32p, f32p,
@@ -273,6 +279,23 @@ class Node:
         _check(lib().spes_debug_read(self._ctx, name.encode(), layer, out.ctypes.data,
                                      out.nbytes))
         return out.reshape(shape) if shape is not None else out
+
+    def profile(self, enable=True, reset=False):
+        if reset:
+            _check(lib().spes_profile_reset(self._ctx))
+        _check(lib().spes_profile(self._ctx, int(enable)))
+
+    def profile_stats(self):
+        """{kernel family: (total device ms, launches)} from live CUDA-event timing."""
+        L = lib()
+        out = {}
+        n = L.spes_profile_count(self._ctx)
+        for i in range(n):
+            name = C.create_string_buffer(64)
+            ms, cnt = C.c_double(), C.c_int64()
+            _check(L.spes_profile_get(self._ctx, i, name, C.byref(ms), C.byref(cnt)))
+            out[name.value.decode()] = (ms.value, cnt.value)
+        return out
 
     def stream(self):
         return lib().spes_stream(self._ctx)

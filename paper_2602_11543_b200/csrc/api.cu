@@ -198,11 +198,65 @@ struct spes_ctx {
     int32_t* peers_dev = nullptr;
     int64_t* layer_expert_offs = nullptr;  // [M] scratch
     int gram_chunks = 0;
+
+    // live per-kernel-family timing with CUDA events on the context's stream
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    std::vector<std::pair<int, size_t>> pending;  // (family, start event index)
+    std::vector<std::string> fam_names;
+    std::vector<double> fam_ms;
+    std::vector<int64_t> fam_n;
 };
 
 namespace {
 
 void set_counter(spes_ctx* c) { spes_k::g_launch_counter = &c->launches; }
+
+// Brackets the launches of one kernel family with CUDA events when profiling is on.
+struct Prof {
+    spes_ctx* c;
+    int fam = -1;
+    size_t i = 0;
+    Prof(spes_ctx* ctx, const char* name) : c(ctx) {
+        if (!c->prof) return;
+        auto it = std::find(c->fam_names.begin(), c->fam_names.end(), name);
+        if (it == c->fam_names.end()) {
+            c->fam_names.push_back(name);
+            c->fam_ms.push_back(0.0);
+            c->fam_n.push_back(0);
+            fam = static_cast<int>(c->fam_names.size()) - 1;
+        } else {
+            fam = static_cast<int>(it - c->fam_names.begin());
+        }
+        while (c->ev_pool.size() < c->ev_used + 2) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            c->ev_pool.push_back(e);
+        }
+        i = c->ev_used;
+        c->ev_used += 2;
+        cudaEventRecord(c->ev_pool[i], c->stream);
+    }
+    ~Prof() {
+        if (fam < 0) return;
+        cudaEventRecord(c->ev_pool[i + 1], c->stream);
+        c->pending.push_back({fam, i});
+    }
+};
+
+void prof_collect(spes_ctx* c) {
+    if (c->pending.empty()) return;
+    cudaStreamSynchronize(c->stream);
+    for (auto& p : c->pending) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c->ev_pool[p.second], c->ev_pool[p.second + 1]);
+        c->fam_ms[p.first] += ms;
+        c->fam_n[p.first] += 1;
+    }
+    c->pending.clear();
+    c->ev_used = 0;
+}
 
 void build_ownership_tables(spes_ctx* c) {
     const Layout& L = c->lay;
@@ -427,66 +481,120 @@ void forward_backward(spes_ctx* c) {
     const int M = L.M, k = L.k;
     const Seeds sd = seeds_for(c);
     float* P = c->params;
-
-    spes_k::embed_gather(P + L.off_emb(), c->tokens, c->B, c->S, d, V, c->h[0], c->inputs,
-                         c->targets, c->err, st);
+#define PROF(name) Prof _prof_##__LINE__(c, name)
+    {
+        PROF("embed_gather");
+        spes_k::embed_gather(P + L.off_emb(), c->tokens, c->B, c->S, d, V, c->h[0], c->inputs,
+                             c->targets, c->err, st);
+    }
     for (int l = 0; l < L.L; ++l) {
         LayerBufs& Y = c->layers[l];
-        spes_k::router_forward(c->h[l], P + L.off_norm(l), P + L.off_router(l), T, d, M, k,
-                               c->cfg.renormalize_after_topk, c->cfg.rms_eps, c->expf_variant,
-                               Y.normed, Y.logits, Y.probs, Y.topk_idx, Y.topk_w, Y.lse_r,
-                               Y.inv_rms, Y.denom, st);
-        spes_k::RoutePlan rp{Y.chunk_counts, Y.counts, Y.pad_off, Y.lb_coeff, Y.slot_row,
-                             Y.row_token, Y.row_w, Y.groups, Y.tiles};
-        spes_k::GroupBases gb{Y.gu, Y.y, c->dgu, c->dxp, c->grads, Y.grad_off, d, f,
-                              bn_for(d), bn_for(f), bn_for(d), bn_for(d)};
-        spes_k::route_plan(Y.topk_idx, Y.topk_w, T, M, k, R, rp, gb, st);
-        spes_k::gather_rows_bf16(Y.normed, d, Y.row_token, Y.pad_off + M, R, d, Y.xp, Y.xpT, R, st);
-        spes_k::gemm_swiglu(Y.a_xp, Y.b_w1t, Y.groups + 0 * M, M, Y.tiles + 0, c->max_tiles[0],
-                            Y.hact, Y.hactT, R, f, st);
-        spes_k::gemm_store_f32(bn_for(d), Y.a_hact, Y.b_w2t, Y.groups + 1 * M, M, Y.tiles + 1,
-                               c->max_tiles[1], st);
-        spes_k::combine_forward(c->h[l], Y.y, Y.slot_row, Y.topk_idx, Y.topk_w, T, d, k,
-                                c->h[l + 1], st);
+        {
+            PROF("router_fwd");
+            spes_k::router_forward(c->h[l], P + L.off_norm(l), P + L.off_router(l), T, d, M, k,
+                                   c->cfg.renormalize_after_topk, c->cfg.rms_eps, c->expf_variant,
+                                   Y.normed, Y.logits, Y.probs, Y.topk_idx, Y.topk_w, Y.lse_r,
+                                   Y.inv_rms, Y.denom, st);
+        }
+        {
+            PROF("route_plan");
+            spes_k::RoutePlan rp{Y.chunk_counts, Y.counts, Y.pad_off, Y.lb_coeff, Y.slot_row,
+                                 Y.row_token, Y.row_w, Y.groups, Y.tiles};
+            spes_k::GroupBases gb{Y.gu, Y.y, c->dgu, c->dxp, c->grads, Y.grad_off, d, f,
+                                  bn_for(d), bn_for(f), bn_for(d), bn_for(d)};
+            spes_k::route_plan(Y.topk_idx, Y.topk_w, T, M, k, R, rp, gb, st);
+        }
+        {
+            PROF("permute");
+            spes_k::gather_rows_bf16(Y.normed, d, Y.row_token, Y.pad_off + M, R, d, Y.xp, Y.xpT, R, st);
+        }
+        {
+            PROF("gemm_fwd_gate_up");
+            spes_k::gemm_swiglu(Y.a_xp, Y.b_w1t, Y.groups + 0 * M, M, Y.tiles + 0, c->max_tiles[0],
+                                Y.hact, Y.hactT, R, f, st);
+        }
+        {
+            PROF("gemm_fwd_down");
+            spes_k::gemm_store_f32(bn_for(d), Y.a_hact, Y.b_w2t, Y.groups + 1 * M, M, Y.tiles + 1,
+                                   c->max_tiles[1], st);
+        }
+        {
+            PROF("combine_fwd");
+            spes_k::combine_forward(c->h[l], Y.y, Y.slot_row, Y.topk_idx, Y.topk_w, T, d, k,
+                                    c->h[l + 1], st);
+        }
     }
-    // head + CE
-    spes_k::gather_rows_bf16(c->h[L.L], d, nullptr, nullptr, Tp, d, c->hL, c->hLT, Tp, st);
-    spes_k::gemm_store_f32(bn_for(V), c->a_hL, c->b_headT, c->head_groups + 0, 1, c->head_tiles + 0,
-                           c->head_max[0], st);
-    spes_k::head_ce(c->head_logits, c->targets, T, Tp, V, c->expf_variant, sd.g_s2, sd.g_ssum,
-                    c->dlogits, c->diff, c->lse_head, st);
-    spes_k::losses_reduce(c->diff, c->lse_head, c->lse_all, c->probs_all, c->coeff_all, T, Tp,
-                          L.L, M, sd.inv_T, sd.inv_L, sd.c_ce, sd.c_lb, sd.c_mz, sd.c_z,
-                          c->d_losses, st);
+    {
+        PROF("head_fwd");
+        spes_k::gather_rows_bf16(c->h[L.L], d, nullptr, nullptr, Tp, d, c->hL, c->hLT, Tp, st);
+        spes_k::gemm_store_f32(bn_for(V), c->a_hL, c->b_headT, c->head_groups + 0, 1,
+                               c->head_tiles + 0, c->head_max[0], st);
+    }
+    {
+        PROF("head_ce_losses");
+        spes_k::head_ce(c->head_logits, c->targets, T, Tp, V, c->expf_variant, sd.g_s2, sd.g_ssum,
+                        c->dlogits, c->diff, c->lse_head, st);
+        spes_k::losses_reduce(c->diff, c->lse_head, c->lse_all, c->probs_all, c->coeff_all, T, Tp,
+                              L.L, M, sd.inv_T, sd.inv_L, sd.c_ce, sd.c_lb, sd.c_mz, sd.c_z,
+                              c->d_losses, st);
+    }
     // ---- backward ----
-    spes_k::gather_rows_bf16(c->dlogits, V, nullptr, nullptr, Tp, V, c->dlog_bf, c->dlogT, Tp, st);
-    spes_k::gemm_store_f32(bn_for(d), c->a_dlog, c->b_headB, c->head_groups + 1, 1,
-                           c->head_tiles + 1, c->head_max[1], st);
-    spes_k::gemm_store_f32(bn_for(V), c->a_hLT, c->b_dlogT, c->head_groups + 2, 1,
-                           c->head_tiles + 2, c->head_max[2], st);
+    {
+        PROF("head_bwd");
+        spes_k::gather_rows_bf16(c->dlogits, V, nullptr, nullptr, Tp, V, c->dlog_bf, c->dlogT, Tp, st);
+        spes_k::gemm_store_f32(bn_for(d), c->a_dlog, c->b_headB, c->head_groups + 1, 1,
+                               c->head_tiles + 1, c->head_max[1], st);
+        spes_k::gemm_store_f32(bn_for(V), c->a_hLT, c->b_dlogT, c->head_groups + 2, 1,
+                               c->head_tiles + 2, c->head_max[2], st);
+    }
     for (int l = L.L - 1; l >= 0; --l) {
         LayerBufs& Y = c->layers[l];
-        spes_k::combine_backward(c->gh, Y.y, Y.row_token, Y.row_w, Y.pad_off + M, R, d, c->dyw,
-                                 c->dywT, c->gw_part, st);
-        spes_k::gemm_dswiglu(bn_for(f), c->a_dyw, Y.b_w2, Y.groups + 2 * M, M, Y.tiles + 2,
-                             c->max_tiles[2], Y.gu, c->dgu, c->dguT, R, f, st);
-        spes_k::gemm_store_f32(bn_for(d), c->a_dgu, Y.b_w1, Y.groups + 3 * M, M, Y.tiles + 3,
-                               c->max_tiles[3], st);
-        if (c->max_tiles[4] > 0) {
-            spes_k::gemm_grad_w1(Y.a_xpT, c->b_dguT, Y.groups + 4 * M, M, Y.tiles + 4,
-                                 c->max_tiles[4], st);
-            spes_k::gemm_store_f32(bn_for(d), Y.a_hactT, c->b_dywT, Y.groups + 5 * M, M,
-                                   Y.tiles + 5, c->max_tiles[5], st);
+        {
+            PROF("combine_bwd");
+            spes_k::combine_backward(c->gh, Y.y, Y.row_token, Y.row_w, Y.pad_off + M, R, d, c->dyw,
+                                     c->dywT, c->gw_part, st);
         }
-        spes_k::router_backward(c->h[l], P + L.off_norm(l), P + L.off_router(l), Y.probs, Y.lse_r,
-                                Y.inv_rms, Y.denom, Y.topk_idx, Y.slot_row, c->gw_part, c->dxp,
-                                Y.lb_coeff, T, d, M, k, c->cfg.renormalize_after_topk,
-                                sd.g_lbsum, sd.g_s, c->glog, c->gnormed, c->gh, st);
-        spes_k::norm_router_grads(c->h[l], Y.normed, c->gnormed, c->glog, Y.inv_rms, T, d, M,
-                                  c->nr_partial, c->grads + L.off_norm(l),
-                                  c->grads + L.off_router(l), st);
+        {
+            PROF("gemm_bwd_dh");
+            spes_k::gemm_dswiglu(bn_for(f), c->a_dyw, Y.b_w2, Y.groups + 2 * M, M, Y.tiles + 2,
+                                 c->max_tiles[2], Y.gu, c->dgu, c->dguT, R, f, st);
+        }
+        {
+            PROF("gemm_bwd_dx");
+            spes_k::gemm_store_f32(bn_for(d), c->a_dgu, Y.b_w1, Y.groups + 3 * M, M, Y.tiles + 3,
+                                   c->max_tiles[3], st);
+        }
+        if (c->max_tiles[4] > 0) {
+            {
+                PROF("gemm_bwd_dw_gate_up");
+                spes_k::gemm_grad_w1(Y.a_xpT, c->b_dguT, Y.groups + 4 * M, M, Y.tiles + 4,
+                                     c->max_tiles[4], st);
+            }
+            {
+                PROF("gemm_bwd_dw_down");
+                spes_k::gemm_store_f32(bn_for(d), Y.a_hactT, c->b_dywT, Y.groups + 5 * M, M,
+                                       Y.tiles + 5, c->max_tiles[5], st);
+            }
+        }
+        {
+            PROF("router_bwd");
+            spes_k::router_backward(c->h[l], P + L.off_norm(l), P + L.off_router(l), Y.probs,
+                                    Y.lse_r, Y.inv_rms, Y.denom, Y.topk_idx, Y.slot_row,
+                                    c->gw_part, c->dxp, Y.lb_coeff, T, d, M, k,
+                                    c->cfg.renormalize_after_topk, sd.g_lbsum, sd.g_s, c->glog,
+                                    c->gnormed, c->gh, st);
+        }
+        {
+            PROF("norm_router_grads");
+            spes_k::norm_router_grads(c->h[l], Y.normed, c->gnormed, c->glog, Y.inv_rms, T, d, M,
+                                      c->nr_partial, c->grads + L.off_norm(l),
+                                      c->grads + L.off_router(l), st);
+        }
     }
-    spes_k::embed_grad(c->inputs, c->gh, T, d, V, c->grads + L.off_emb(), st);
+    {
+        PROF("embed_grad");
+        spes_k::embed_grad(c->inputs, c->gh, T, d, V, c->grads + L.off_emb(), st);
+    }
 }
 
 void optimizer_step(spes_ctx* c, const spes_adamw_cfg* o) {
@@ -497,10 +605,15 @@ void optimizer_step(spes_ctx* c, const spes_adamw_cfg* o) {
     const float b1 = static_cast<float>(o->beta1), b2 = static_cast<float>(o->beta2);
     volatile float one = 1.f;
     const float omb1 = one - b1, omb2 = one - b2;
-    spes_k::adamw(c->params, c->grads, c->m, c->v, c->segs, static_cast<int>(c->segs_host.size()),
-                  c->G, static_cast<float>(o->lr), b1, b2, omb1, omb2, static_cast<float>(o->eps),
-                  static_cast<float>(o->weight_decay), bc1, bc2, c->stream);
+    {
+        PROF("adamw");
+        spes_k::adamw(c->params, c->grads, c->m, c->v, c->segs,
+                      static_cast<int>(c->segs_host.size()), c->G, static_cast<float>(o->lr), b1,
+                      b2, omb1, omb2, static_cast<float>(o->eps),
+                      static_cast<float>(o->weight_decay), bc1, bc2, c->stream);
+    }
     const Layout& L = c->lay;
+    PROF("bf16_shadows");
     spes_k::expert_shadows(c->params, c->owned_expert_offs, c->n_owned_slots,
                            c->owned_shadow_slots, L.d, L.f, c->w1t, c->w2t, c->w1, c->w2,
                            c->stream);
@@ -850,6 +963,7 @@ spes_status spes_sync(spes_ctx* c, spes_sync_stats* stats) {
         cudaEventCreate(&e1);
         cudaEventRecord(e0, st);
         double psi_in = 0, exp_in = 0;
+        Prof prof_sync(c, "sync");
         if (N > 1) {
             const int64_t psi = L.psi();
             if (!c->psi_stage) c->psi_stage = c->scratch.alloc<float>(psi * N);
@@ -1197,6 +1311,40 @@ spes_status spes_debug_read(spes_ctx* c, const char* name, int32_t layer, void* 
         if (bytes < sz) throw std::invalid_argument("debug_read: buffer too small");
         ck(cudaMemcpyAsync(host, src, sz, cudaMemcpyDeviceToHost, c->stream), "D2H");
         ck(cudaStreamSynchronize(c->stream), "sync");
+    });
+}
+
+spes_status spes_profile(spes_ctx* c, int32_t enable) {
+    return guard([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        prof_collect(c);
+        c->prof = enable != 0;
+    });
+}
+
+spes_status spes_profile_reset(spes_ctx* c) {
+    return guard([&] {
+        prof_collect(c);
+        std::fill(c->fam_ms.begin(), c->fam_ms.end(), 0.0);
+        std::fill(c->fam_n.begin(), c->fam_n.end(), 0);
+    });
+}
+
+int32_t spes_profile_count(spes_ctx* c) {
+    prof_collect(c);
+    return static_cast<int32_t>(c->fam_names.size());
+}
+
+spes_status spes_profile_get(spes_ctx* c, int32_t i, char* name64, double* total_ms,
+                             int64_t* launches) {
+    return guard([&] {
+        prof_collect(c);
+        if (i < 0 || i >= static_cast<int32_t>(c->fam_names.size()))
+            throw std::out_of_range("profile: bad index");
+        std::strncpy(name64, c->fam_names[i].c_str(), 63);
+        name64[63] = 0;
+        *total_ms = c->fam_ms[i];
+        *launches = c->fam_n[i];
     });
 }
 
