@@ -126,9 +126,9 @@ struct LayerBufs {
     float *normed, *logits, *probs, *topk_w, *lse_r, *inv_rms, *denom, *y, *row_w, *lb_coeff;
     int32_t *topk_idx, *chunk_counts, *counts, *pad_off, *slot_row, *row_token, *tiles;
     GemmGroup* groups;
-    bf16 *xp, *xpT, *gu, *hact, *hactT;
+    bf16 *xp, *gu, *hact;
     int64_t* grad_off;  // device [M]
-    CUtensorMap a_xp, a_hact, a_xpT, a_hactT;
+    CUtensorMap a_xp, a_hact, a_xp_mn, a_hact_mn;  // *_mn: [tokens x features] as MN-major
     CUtensorMap b_w1t, b_w2t, b_w2, b_w1;
 };
 
@@ -171,17 +171,17 @@ struct spes_ctx {
     std::vector<float*> h;  // L+1 buffers [T_pad x d]
     std::vector<LayerBufs> layers;
     int32_t *tokens = nullptr, *inputs = nullptr, *targets = nullptr, *err = nullptr;
-    bf16 *dyw = nullptr, *dywT = nullptr, *dgu = nullptr, *dguT = nullptr;
+    bf16 *dyw = nullptr, *dgu = nullptr;
     float *dxp = nullptr, *gw_part = nullptr, *glog = nullptr, *gnormed = nullptr, *gh = nullptr,
           *nr_partial = nullptr;
-    bf16 *hL = nullptr, *hLT = nullptr, *dlog_bf = nullptr, *dlogT = nullptr;
+    bf16 *hL = nullptr, *dlog_bf = nullptr;
     float *head_logits = nullptr, *dlogits = nullptr, *diff = nullptr, *lse_head = nullptr;
     float *lse_all = nullptr, *probs_all = nullptr, *coeff_all = nullptr;
     double* d_losses = nullptr;
     GemmGroup* head_groups = nullptr;  // [3]
     int32_t* head_tiles = nullptr;     // [3]
     int head_max[3] = {0, 0, 0};
-    CUtensorMap a_dyw, a_dgu, b_dguT, b_dywT, a_hL, b_headT, a_dlog, b_headB, a_hLT, b_dlogT;
+    CUtensorMap a_dyw, a_dgu, b_dgu_mn, b_dyw_mn, a_hL, b_headT, a_dlog, b_headB, a_hL_mn, b_dlog_mn;
     int max_tiles[6] = {0, 0, 0, 0, 0, 0};
 
     // host staging
@@ -369,38 +369,32 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
         Y.groups = A.alloc<GemmGroup>(6 * M);
         Y.tiles = A.alloc<int32_t>(6);
         Y.xp = A.alloc<bf16>(R * d);
-        Y.xpT = A.alloc<bf16>(d * R);
         Y.gu = A.alloc<bf16>(R * 2 * f);
         Y.hact = A.alloc<bf16>(R * f);
-        Y.hactT = A.alloc<bf16>(f * R);
         Y.y = A.alloc<float>(R * d);
         Y.grad_off = c->grad_off_dev + static_cast<int64_t>(l) * M;
         using spes_host::make_tmap_bf16;
         Y.a_xp = make_tmap_bf16(Y.xp, R, d, 128);
         Y.a_hact = make_tmap_bf16(Y.hact, R, f, 128);
-        Y.a_xpT = make_tmap_bf16(Y.xpT, d, R, 128);
-        Y.a_hactT = make_tmap_bf16(Y.hactT, f, R, 128);
+        Y.a_xp_mn = make_tmap_bf16(Y.xp, R, d, 64);
+        Y.a_hact_mn = make_tmap_bf16(Y.hact, R, f, 64);
         Y.b_w1t = make_tmap_bf16(c->w1t + static_cast<int64_t>(l) * M * 2 * f * d, M * 2 * f, d, 256);
         Y.b_w2t = make_tmap_bf16(c->w2t + static_cast<int64_t>(l) * M * d * f, M * d, f, bn_for(d));
         Y.b_w2 = make_tmap_bf16(c->w2 + static_cast<int64_t>(l) * M * f * d, M * f, d, bn_for(f));
         Y.b_w1 = make_tmap_bf16(c->w1 + static_cast<int64_t>(l) * M * d * 2 * f, M * d, 2 * f, bn_for(d));
     }
     c->dyw = A.alloc<bf16>(R * d);
-    c->dywT = A.alloc<bf16>(d * R);
     c->dgu = A.alloc<bf16>(R * 2 * f);
-    c->dguT = A.alloc<bf16>(2 * f * R);
     c->dxp = A.alloc<float>(R * d);
-    c->gw_part = A.alloc<float>(R * (d / 64));
+    c->gw_part = A.alloc<float>(R);
     c->glog = A.alloc<float>(Tp * M);
     c->gnormed = A.alloc<float>(Tp * d);
     c->gh = A.alloc<float>(Tp * d);
     c->nr_partial = A.alloc<float>(16 * d * (M + 1));
     c->hL = A.alloc<bf16>(Tp * d);
-    c->hLT = A.alloc<bf16>(d * Tp);
     c->head_logits = A.alloc<float>(Tp * V);
     c->dlogits = A.alloc<float>(Tp * V);
     c->dlog_bf = A.alloc<bf16>(Tp * V);
-    c->dlogT = A.alloc<bf16>(V * Tp);
     c->diff = A.alloc<float>(Tp);
     c->lse_head = A.alloc<float>(Tp);
     c->d_losses = A.alloc<double>(8);
@@ -409,14 +403,14 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     using spes_host::make_tmap_bf16;
     c->a_dyw = make_tmap_bf16(c->dyw, R, d, 128);
     c->a_dgu = make_tmap_bf16(c->dgu, R, 2 * f, 128);
-    c->b_dguT = make_tmap_bf16(c->dguT, 2 * f, R, 256);
-    c->b_dywT = make_tmap_bf16(c->dywT, d, R, bn_for(d));
+    c->b_dgu_mn = make_tmap_bf16(c->dgu, R, 2 * f, 64);
+    c->b_dyw_mn = make_tmap_bf16(c->dyw, R, d, 64);
     c->a_hL = make_tmap_bf16(c->hL, Tp, d, 128);
     c->b_headT = make_tmap_bf16(c->headT, V, d, bn_for(V));
     c->a_dlog = make_tmap_bf16(c->dlog_bf, Tp, V, 128);
     c->b_headB = make_tmap_bf16(c->headB, d, V, bn_for(d));
-    c->a_hLT = make_tmap_bf16(c->hLT, d, Tp, 128);
-    c->b_dlogT = make_tmap_bf16(c->dlogT, V, Tp, bn_for(V));
+    c->a_hL_mn = make_tmap_bf16(c->hL, Tp, d, 64);
+    c->b_dlog_mn = make_tmap_bf16(c->dlog_bf, Tp, V, 64);
     // head GEMM groups (static for a given T_pad)
     GemmGroup hg[3]{};
     hg[0].k_len = static_cast<int32_t>(d);
@@ -506,16 +500,16 @@ void forward_backward(spes_ctx* c) {
         }
         {
             PROF("permute");
-            spes_k::gather_rows_bf16(Y.normed, d, Y.row_token, Y.pad_off + M, R, d, Y.xp, Y.xpT, R, st);
+            spes_k::gather_rows_bf16(Y.normed, d, Y.row_token, Y.pad_off + M, R, d, Y.xp, nullptr, R, st);
         }
         {
             PROF("gemm_fwd_gate_up");
             spes_k::gemm_swiglu(Y.a_xp, Y.b_w1t, Y.groups + 0 * M, M, Y.tiles + 0, c->max_tiles[0],
-                                Y.hact, Y.hactT, R, f, st);
+                                Y.hact, f, st);
         }
         {
             PROF("gemm_fwd_down");
-            spes_k::gemm_store_f32(bn_for(d), Y.a_hact, Y.b_w2t, Y.groups + 1 * M, M, Y.tiles + 1,
+            spes_k::gemm_store_f32(bn_for(d), false, Y.a_hact, Y.b_w2t, Y.groups + 1 * M, M, Y.tiles + 1,
                                    c->max_tiles[1], st);
         }
         {
@@ -526,8 +520,8 @@ void forward_backward(spes_ctx* c) {
     }
     {
         PROF("head_fwd");
-        spes_k::gather_rows_bf16(c->h[L.L], d, nullptr, nullptr, Tp, d, c->hL, c->hLT, Tp, st);
-        spes_k::gemm_store_f32(bn_for(V), c->a_hL, c->b_headT, c->head_groups + 0, 1,
+        spes_k::gather_rows_bf16(c->h[L.L], d, nullptr, nullptr, Tp, d, c->hL, nullptr, Tp, st);
+        spes_k::gemm_store_f32(bn_for(V), false, c->a_hL, c->b_headT, c->head_groups + 0, 1,
                                c->head_tiles + 0, c->head_max[0], st);
     }
     {
@@ -541,10 +535,10 @@ void forward_backward(spes_ctx* c) {
     // ---- backward ----
     {
         PROF("head_bwd");
-        spes_k::gather_rows_bf16(c->dlogits, V, nullptr, nullptr, Tp, V, c->dlog_bf, c->dlogT, Tp, st);
-        spes_k::gemm_store_f32(bn_for(d), c->a_dlog, c->b_headB, c->head_groups + 1, 1,
+        spes_k::gather_rows_bf16(c->dlogits, V, nullptr, nullptr, Tp, V, c->dlog_bf, nullptr, Tp, st);
+        spes_k::gemm_store_f32(bn_for(d), false, c->a_dlog, c->b_headB, c->head_groups + 1, 1,
                                c->head_tiles + 1, c->head_max[1], st);
-        spes_k::gemm_store_f32(bn_for(V), c->a_hLT, c->b_dlogT, c->head_groups + 2, 1,
+        spes_k::gemm_store_f32(bn_for(V), true, c->a_hL_mn, c->b_dlog_mn, c->head_groups + 2, 1,
                                c->head_tiles + 2, c->head_max[2], st);
     }
     for (int l = L.L - 1; l >= 0; --l) {
@@ -552,27 +546,27 @@ void forward_backward(spes_ctx* c) {
         {
             PROF("combine_bwd");
             spes_k::combine_backward(c->gh, Y.y, Y.row_token, Y.row_w, Y.pad_off + M, R, d, c->dyw,
-                                     c->dywT, c->gw_part, st);
+                                     c->gw_part, st);
         }
         {
             PROF("gemm_bwd_dh");
             spes_k::gemm_dswiglu(bn_for(f), c->a_dyw, Y.b_w2, Y.groups + 2 * M, M, Y.tiles + 2,
-                                 c->max_tiles[2], Y.gu, c->dgu, c->dguT, R, f, st);
+                                 c->max_tiles[2], Y.gu, f, st);
         }
         {
             PROF("gemm_bwd_dx");
-            spes_k::gemm_store_f32(bn_for(d), c->a_dgu, Y.b_w1, Y.groups + 3 * M, M, Y.tiles + 3,
+            spes_k::gemm_store_f32(bn_for(d), false, c->a_dgu, Y.b_w1, Y.groups + 3 * M, M, Y.tiles + 3,
                                    c->max_tiles[3], st);
         }
         if (c->max_tiles[4] > 0) {
             {
                 PROF("gemm_bwd_dw_gate_up");
-                spes_k::gemm_grad_w1(Y.a_xpT, c->b_dguT, Y.groups + 4 * M, M, Y.tiles + 4,
+                spes_k::gemm_grad_w1(Y.a_xp_mn, c->b_dgu_mn, Y.groups + 4 * M, M, Y.tiles + 4,
                                      c->max_tiles[4], st);
             }
             {
                 PROF("gemm_bwd_dw_down");
-                spes_k::gemm_store_f32(bn_for(d), Y.a_hactT, c->b_dywT, Y.groups + 5 * M, M,
+                spes_k::gemm_store_f32(bn_for(d), true, Y.a_hact_mn, c->b_dyw_mn, Y.groups + 5 * M, M,
                                        Y.tiles + 5, c->max_tiles[5], st);
             }
         }

@@ -48,6 +48,11 @@ __device__ __forceinline__ float silu_f(float z) {
     float s = z >= 0.f ? 1.f / (1.f + __expf(-z)) : __expf(z) / (1.f + __expf(z));
     return z * s;
 }
+// bf16-path activation: 1 / (1 + 2^(-z*log2 e)) with the SFU exp2 / reciprocal
+// (the expert FFN runs on bf16 operands; its tolerance is far above these ulps).
+__device__ __forceinline__ float sigmoid_fast(float z) {
+    return __frcp_rn(1.f + exp2f(-1.4426950408889634f * z));
+}
 __device__ __forceinline__ float sigmoid_f(float z) {
     return z >= 0.f ? 1.f / (1.f + __expf(-z)) : __expf(z) / (1.f + __expf(z));
 }

@@ -2,12 +2,14 @@
 //
 //   EpiSwiGLU   expert forward gate||up: accumulator columns [0,128) are gate,
 //               [128,256) the matching up columns; writes GU (bf16, saved for
-//               backward), Hact = silu(G)*U in row and transposed layouts.
+//               backward) and Hact = silu(G)*U (bf16).
 //   EpiStoreF32 plain fp32 tile store (expert down-proj Y, dX, head logits / dh,
 //               dWd and dHead straight into the gradient buffer).
-//   EpiDSwiGLU  expert backward: dHact -> (dG, dU) using the saved GU, written
-//               as dGU (bf16, row + transposed) for the dX and dW GEMMs.
+//   EpiDSwiGLU  expert backward: dHact -> (dG, dU) using the saved GU, written as
+//               dGU (bf16) for the dX and dW GEMMs.
 //   EpiGradW1   dW of gate||up straight into the fp32 wg / wu gradient blocks.
+// Weight-gradient GEMMs read the row-major activations directly as MN-major
+// operands (grouped_gemm_kernel<..., MN=true>): no transposed copies are made.
 #include "common.cuh"
 #include "grouped_gemm.cuh"
 #include "kernels.h"
@@ -35,10 +37,12 @@ __device__ __forceinline__ void store_bf16x32(bf16* dst, const float (&v)[32]) {
 
 __device__ __forceinline__ void load_bf16x32(const bf16* src, float (&v)[32]) {
     const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4 pk[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) pk[i] = __ldg(s4 + i);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        uint4 pk = __ldg(s4 + i);
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&pk);
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&pk[i]);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             float2 f = __bfloat1622float2(h[j]);
@@ -50,27 +54,22 @@ __device__ __forceinline__ void load_bf16x32(const bf16* src, float (&v)[32]) {
 
 struct EpiSwiGLU {
     bf16* hact;
-    bf16* hactT;
-    int64_t R_cap;
     int64_t f;
     __device__ void operator()(const GemmGroup& g, int mt, int nt, int r, uint32_t taddr,
-                               bool empty) const {
+                               bool empty, int half) const {
         const int64_t row = g.out_row0 + static_cast<int64_t>(mt) * GEMM_BM + r;
         bf16* gu = static_cast<bf16*>(g.out0) + row * g.ldo + static_cast<int64_t>(nt) * 256;
         bf16* ha = hact + row * f + static_cast<int64_t>(nt) * 128;
 #pragma unroll 1
-        for (int c = 0; c < 128; c += 32) {
+        for (int c = half * 64; c < half * 64 + 64; c += 32) {
             float gv[32], uv[32], hv[32];
             acc_load32(taddr + c, empty, gv);
             acc_load32(taddr + 128 + c, empty, uv);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) hv[i] = silu_f(gv[i]) * uv[i];
+            for (int i = 0; i < 32; ++i) hv[i] = gv[i] * sigmoid_fast(gv[i]) * uv[i];
             store_bf16x32(gu + c, gv);
             store_bf16x32(gu + 128 + c, uv);
             store_bf16x32(ha + c, hv);
-            bf16* col = hactT + (static_cast<int64_t>(nt) * 128 + c) * R_cap + row;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) col[i * R_cap] = __float2bfloat16_rn(hv[i]);
         }
     }
 };
@@ -78,47 +77,38 @@ struct EpiSwiGLU {
 template <int BN>
 struct EpiDSwiGLU {
     const bf16* gu;
-    bf16* dguT;
-    int64_t R_cap;
     int64_t f;
     __device__ void operator()(const GemmGroup& g, int mt, int nt, int r, uint32_t taddr,
-                               bool empty) const {
+                               bool empty, int half) const {
         const int64_t row = g.out_row0 + static_cast<int64_t>(mt) * GEMM_BM + r;
         const bf16* gurow = gu + row * 2 * f;
         bf16* dgurow = static_cast<bf16*>(g.out0) + row * g.ldo;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
             const int64_t x0 = static_cast<int64_t>(nt) * BN + c;  // f index of column 0
             const int64_t ig = il_gate(x0), iu = il_up(x0);
             float dh[32], gv[32], uv[32], dg[32], du[32];
-            acc_load32(taddr + c, empty, dh);
             load_bf16x32(gurow + ig, gv);
             load_bf16x32(gurow + iu, uv);
+            acc_load32(taddr + c, empty, dh);
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
-                const float s = sigmoid_f(gv[i]);
+                const float s = sigmoid_fast(gv[i]);
                 dg[i] = dh[i] * uv[i] * (s * (1.f + gv[i] * (1.f - s)));
                 du[i] = dh[i] * (gv[i] * s);
             }
             store_bf16x32(dgurow + ig, dg);
             store_bf16x32(dgurow + iu, du);
-            bf16* cg = dguT + ig * R_cap + row;
-            bf16* cu = dguT + iu * R_cap + row;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                cg[i * R_cap] = __float2bfloat16_rn(dg[i]);
-                cu[i * R_cap] = __float2bfloat16_rn(du[i]);
-            }
         }
     }
 };
 
 struct EpiGradW1 {
     __device__ void operator()(const GemmGroup& g, int mt, int nt, int r, uint32_t taddr,
-                               bool empty) const {
+                               bool empty, int half) const {
         const int64_t row = static_cast<int64_t>(mt) * GEMM_BM + r;  // d index
 #pragma unroll 1
-        for (int c = 0; c < 256; c += 32) {
+        for (int c = half * 128; c < half * 128 + 128; c += 32) {
             float v[32];
             acc_load32(taddr + c, empty, v);
             float* base = static_cast<float*>(c < 128 ? g.out0 : g.out1);
@@ -142,11 +132,11 @@ int num_sms() {
     return g_num_sms;
 }
 
-template <int BN, class Epi>
+template <int BN, bool MN, class Epi>
 static void launch(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
                    const int32_t* tiles, int max_tiles, const Epi& epi, cudaStream_t s) {
     if (max_tiles <= 0) return;
-    auto kern = grouped_gemm_kernel<BN, Epi>;
+    auto kern = grouped_gemm_kernel<BN, Epi, MN>;
     static bool configured = false;  // one per template instantiation
     if (!configured) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -164,32 +154,38 @@ void gemm_prepare(int device) {
 }
 
 void gemm_swiglu(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
-                 const int32_t* tiles, int max_tiles, bf16* hact, bf16* hactT, int64_t R_cap,
-                 int64_t f, cudaStream_t s) {
-    launch<256>(a, b, g, ng, tiles, max_tiles, EpiSwiGLU{hact, hactT, R_cap, f}, s);
+                 const int32_t* tiles, int max_tiles, bf16* hact, int64_t f, cudaStream_t s) {
+    launch<256, false>(a, b, g, ng, tiles, max_tiles, EpiSwiGLU{hact, f}, s);
 }
 
-void gemm_store_f32(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g,
-                    int ng, const int32_t* tiles, int max_tiles, cudaStream_t s) {
-    if (bn == 256)
-        launch<256>(a, b, g, ng, tiles, max_tiles, EpiStoreF32<256>{}, s);
-    else
-        launch<128>(a, b, g, ng, tiles, max_tiles, EpiStoreF32<128>{}, s);
+void gemm_store_f32(int bn, bool mn, const CUtensorMap& a, const CUtensorMap& b,
+                    const GemmGroup* g, int ng, const int32_t* tiles, int max_tiles,
+                    cudaStream_t s) {
+    if (bn == 256) {
+        if (mn)
+            launch<256, true>(a, b, g, ng, tiles, max_tiles, EpiStoreF32<256>{}, s);
+        else
+            launch<256, false>(a, b, g, ng, tiles, max_tiles, EpiStoreF32<256>{}, s);
+    } else {
+        if (mn)
+            launch<128, true>(a, b, g, ng, tiles, max_tiles, EpiStoreF32<128>{}, s);
+        else
+            launch<128, false>(a, b, g, ng, tiles, max_tiles, EpiStoreF32<128>{}, s);
+    }
 }
 
 void gemm_dswiglu(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
-                  const int32_t* tiles, int max_tiles, const bf16* gu, bf16* dgu, bf16* dguT,
-                  int64_t R_cap, int64_t f, cudaStream_t s) {
-    (void)dgu;
+                  const int32_t* tiles, int max_tiles, const bf16* gu, int64_t f,
+                  cudaStream_t s) {
     if (bn == 256)
-        launch<256>(a, b, g, ng, tiles, max_tiles, EpiDSwiGLU<256>{gu, dguT, R_cap, f}, s);
+        launch<256, false>(a, b, g, ng, tiles, max_tiles, EpiDSwiGLU<256>{gu, f}, s);
     else
-        launch<128>(a, b, g, ng, tiles, max_tiles, EpiDSwiGLU<128>{gu, dguT, R_cap, f}, s);
+        launch<128, false>(a, b, g, ng, tiles, max_tiles, EpiDSwiGLU<128>{gu, f}, s);
 }
 
 void gemm_grad_w1(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
                   const int32_t* tiles, int max_tiles, cudaStream_t s) {
-    launch<256>(a, b, g, ng, tiles, max_tiles, EpiGradW1{}, s);
+    launch<256, true>(a, b, g, ng, tiles, max_tiles, EpiGradW1{}, s);
 }
 
 }  // namespace spes_k

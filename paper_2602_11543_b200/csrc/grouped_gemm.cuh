@@ -16,7 +16,8 @@
 //   warp 0  : TMA producer       (one elected lane)
 //   warp 1  : MMA issuer         (one elected lane, tcgen05.mma cta_group::1, M=128)
 //   warp 2  : TMEM allocator
-//   warps 4-7: epilogue (TMEM lanes 0-127 -> registers -> fused epilogue -> global)
+//   warps 4-11: epilogue, two warps per TMEM lane quarter, each on half of the tile's
+//               columns (TMEM -> registers -> fused epilogue -> global)
 // Pipelines: STAGES-deep smem ring (full/empty mbarriers) and a 2-deep TMEM
 // accumulator ring (tmem_full/tmem_empty) so the epilogue of tile i overlaps
 // the MMAs of tile i+1.
@@ -28,7 +29,7 @@ namespace spes_dev {
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;  // 64 bf16 = 128 B = one swizzle row
-constexpr int GEMM_THREADS = 256;
+constexpr int GEMM_THREADS = 384;  // 4 control warps + 8 epilogue warps
 
 struct GemmGroup {
     int32_t a_row0;      // first row of this group's A tile space
@@ -64,10 +65,16 @@ __device__ __forceinline__ int find_group(const GemmGroup* __restrict__ groups, 
 
 // Epi must provide:
 //   __device__ void operator()(const GemmGroup& g, int mt, int nt, int r, uint32_t taddr,
-//                              bool empty) const;
+//                              bool empty, int half) const;
 // r = row within the 128-row tile handled by this thread; taddr = TMEM address of
 // (lane r, column 0) of this tile's accumulator; empty => k_len == 0 (result is 0).
-template <int BN, class Epi>
+//
+// MN == false: A [rows x K] and B [rows x K] row-major (K contiguous), tiles at
+//              (k0 + kb*64, a_row0 + mt*128) / (k0 + kb*64, b_row0 + nt*BN).
+// MN == true : A [K x Mtot] and B [K x Ntot] row-major (M / N contiguous), i.e. the
+//              weight-gradient form D = A^T B over K = tokens; a_row0 / b_row0 are
+//              column offsets and k0 the first K row; boxes of 64 x 64.
+template <int BN, class Epi, bool MN = false>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
                         const __grid_constant__ CUtensorMap mapB,
@@ -96,7 +103,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 128);
+            mbar_init(&tempty[a], 256);
         }
         fence_barrier_init();
     }
@@ -127,8 +134,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     uint8_t* sb = sa + C::A_BYTES;
                     mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
                     const int kc = g.k0 + kb * GEMM_BK;
-                    tma_load_2d(&mapA, &full[stage], sa, kc, arow);
-                    tma_load_2d(&mapB, &full[stage], sb, kc, brow);
+                    if constexpr (!MN) {
+                        tma_load_2d(&mapA, &full[stage], sa, kc, arow);
+                        tma_load_2d(&mapB, &full[stage], sb, kc, brow);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < GEMM_BM / 64; ++i)
+                            tma_load_2d(&mapA, &full[stage], sa + i * 8192, arow + 64 * i, kc);
+#pragma unroll
+                        for (int i = 0; i < BN / 64; ++i)
+                            tma_load_2d(&mapB, &full[stage], sb + i * 8192, brow + 64 * i, kc);
+                    }
                     if (++stage == C::STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -138,7 +154,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            constexpr uint32_t idesc = idesc_bf16_f32(GEMM_BM, BN);
+            constexpr uint32_t idesc = idesc_bf16_f32(GEMM_BM, BN, MN);
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
@@ -155,13 +171,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     tc_fence_after();
                     const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
                     const uint32_t sb = sa + C::A_BYTES;
-                    const uint64_t adesc = desc_kmajor_sw128(sa);
-                    const uint64_t bdesc = desc_kmajor_sw128(sb);
+                    if constexpr (!MN) {
+                        const uint64_t adesc = desc_kmajor_sw128(sa);
+                        const uint64_t bdesc = desc_kmajor_sw128(sb);
 #pragma unroll
-                    for (int k = 0; k < GEMM_BK / 16; ++k) {
-                        // advance 16 elements = 32 B inside the 128 B swizzle row
-                        umma_bf16(dtmem, adesc + 2 * k, bdesc + 2 * k, idesc,
-                                  (kb | k) != 0 ? 1u : 0u);
+                        for (int k = 0; k < GEMM_BK / 16; ++k) {
+                            // advance 16 elements = 32 B inside the 128 B swizzle row
+                            umma_bf16(dtmem, adesc + 2 * k, bdesc + 2 * k, idesc,
+                                      (kb | k) != 0 ? 1u : 0u);
+                        }
+                    } else {
+                        const uint64_t adesc = desc_mnmajor_sw128(sa, 8192);
+                        const uint64_t bdesc = desc_mnmajor_sw128(sb, 8192);
+#pragma unroll
+                        for (int k = 0; k < GEMM_BK / 16; ++k) {
+                            // advance 16 K rows = 2 KiB (two 8-row swizzle atoms)
+                            umma_bf16(dtmem, adesc + 128 * k, bdesc + 128 * k, idesc,
+                                      (kb | k) != 0 ? 1u : 0u);
+                        }
                     }
                     umma_commit(&empty[stage]);
                     if (++stage == C::STAGES) {
@@ -176,7 +203,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
         }
     } else if (warp >= 4) {
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int q = warp & 3;           // TMEM lane quarter this warp may access
+        const int half = (warp - 4) >> 2;  // which half of the tile's columns
         const int r = q * 32 + lane;
         int it = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
@@ -189,7 +217,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
-            epi(g, mt, nt, r, taddr, g.k_len == 0);
+            epi(g, mt, nt, r, taddr, g.k_len == 0, half);
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
         }
@@ -221,12 +249,12 @@ __device__ __forceinline__ void acc_load32(uint32_t taddr, bool empty, float (&v
 template <int BN>
 struct EpiStoreF32 {
     __device__ void operator()(const GemmGroup& g, int mt, int nt, int r, uint32_t taddr,
-                               bool empty) const {
+                               bool empty, int half) const {
         float* out = static_cast<float*>(g.out0) +
                      (g.out_row0 + static_cast<int64_t>(mt) * GEMM_BM + r) * g.ldo +
                      static_cast<int64_t>(nt) * BN;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
             float v[32];
             acc_load32(taddr + c, empty, v);
             float4* dst = reinterpret_cast<float4*>(out + c);

@@ -599,186 +599,42 @@ void losses_reduce(const float* diff, const float* lse_head, const float* lse_r,
 }
 
 // ============================ combine (backward) ============================
-// Tile of 64 routed rows x 64 columns: dYw[r] = bf16(gh[t_r] * w_r) (rowwise_mul
-// backward, graph.hpp:299-305) in both layouts, and partial dot products
-// <gh[t_r], Y[r]> for the gate-weight gradient (graph.hpp:307-316).
+// Warp per routed row r (token t_r, weight w_r): dYw[r] = bf16(gh[t_r] * w_r)
+// (rowwise_mul backward, graph.hpp:299-305) and the gate-weight gradient
+// <gh[t_r], Y[r]> (graph.hpp:307-316). Padding rows get zeros.
 __global__ void __launch_bounds__(256) combine_bwd_k(
     const float* __restrict__ gh, const float* __restrict__ y, const int32_t* __restrict__ row_token,
-    const float* __restrict__ row_w, const int32_t* __restrict__ R_total, int64_t R_cap, int64_t d,
-    bf16* __restrict__ dyw, bf16* __restrict__ dywT, float* __restrict__ gw_part) {
-    __shared__ float tile[64][65];
-    __shared__ float red[64][17];
-    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 64;
-    const int64_t c0 = static_cast<int64_t>(blockIdx.y) * 64;
-    if (r0 >= *R_total) return;
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int rr = ty + 16 * i;
-        const int64_t r = r0 + rr;
-        const int32_t t = row_token[r];
+    const float* __restrict__ row_w, const int32_t* __restrict__ R_total, int64_t d,
+    bf16* __restrict__ dyw, float* __restrict__ gw) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (r >= *R_total) return;
+    const int32_t t = row_token[r];
+    const float wv = t >= 0 ? row_w[r] : 0.f;
+    float dot = 0.f;
+    for (int64_t q = lane * 4; q < d; q += 128) {
         float4 g = make_float4(0.f, 0.f, 0.f, 0.f), yv = g;
-        float wv = 0.f;
         if (t >= 0) {
-            g = __ldg(reinterpret_cast<const float4*>(gh + static_cast<int64_t>(t) * d + c0 + 4 * tx));
-            yv = __ldg(reinterpret_cast<const float4*>(y + r * d + c0 + 4 * tx));
-            wv = row_w[r];
+            g = __ldg(reinterpret_cast<const float4*>(gh + static_cast<int64_t>(t) * d + q));
+            yv = __ldg(reinterpret_cast<const float4*>(y + r * d + q));
         }
-        const float a0 = g.x * wv, a1 = g.y * wv, a2 = g.z * wv, a3 = g.w * wv;
-        tile[rr][4 * tx + 0] = a0;
-        tile[rr][4 * tx + 1] = a1;
-        tile[rr][4 * tx + 2] = a2;
-        tile[rr][4 * tx + 3] = a3;
-        __nv_bfloat162 p0 = __floats2bfloat162_rn(a0, a1), p1 = __floats2bfloat162_rn(a2, a3);
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(g.x * wv, g.y * wv);
+        __nv_bfloat162 p1 = __floats2bfloat162_rn(g.z * wv, g.w * wv);
         uint2 pk;
         pk.x = *reinterpret_cast<uint32_t*>(&p0);
         pk.y = *reinterpret_cast<uint32_t*>(&p1);
-        *reinterpret_cast<uint2*>(dyw + r * d + c0 + 4 * tx) = pk;
-        red[rr][tx] = ((g.x * yv.x + g.y * yv.y) + g.z * yv.z) + g.w * yv.w;
+        *reinterpret_cast<uint2*>(dyw + r * d + q) = pk;
+        dot += ((g.x * yv.x + g.y * yv.y) + g.z * yv.z) + g.w * yv.w;
     }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int cc = ty + 16 * i;
-        __nv_bfloat162 a = __floats2bfloat162_rn(tile[4 * tx + 0][cc], tile[4 * tx + 1][cc]);
-        __nv_bfloat162 b = __floats2bfloat162_rn(tile[4 * tx + 2][cc], tile[4 * tx + 3][cc]);
-        uint2 pk;
-        pk.x = *reinterpret_cast<uint32_t*>(&a);
-        pk.y = *reinterpret_cast<uint32_t*>(&b);
-        *reinterpret_cast<uint2*>(dywT + (c0 + cc) * R_cap + r0 + 4 * tx) = pk;
-    }
-    if (threadIdx.x < 64) {
-        float s = 0.f;
-        for (int i = 0; i < 16; ++i) s += red[threadIdx.x][i];
-        gw_part[(r0 + threadIdx.x) * (d / 64) + blockIdx.y] = s;
-    }
+    dot = warp_sum(dot);
+    if (lane == 0) gw[r] = dot;
 }
 
 void combine_backward(const float* gh, const float* y, const int32_t* row_token,
                       const float* row_w, const int32_t* R_total_dev, int64_t R_cap, int64_t d,
-                      bf16* dyw, bf16* dywT, float* gw_part, cudaStream_t s) {
-    dim3 grid(static_cast<unsigned>(R_cap / 64), static_cast<unsigned>(d / 64));
-    combine_bwd_k<<<grid, 256, 0, s>>>(gh, y, row_token, row_w, R_total_dev, R_cap, d, dyw, dywT,
-                                       gw_part);
-    count_launch();
-}
-
-// ============================ router backward + rmsnorm backward ============================
-// One thread per token, following the reverse tape of one layer:
-//   probs.grad = (0 + g_lb*coeff_j) [lb, model.hpp:358] + gate-weight grads (experts desc.)
-//   logits.grad = (0 + gl*p_j) [moe_z logsumexp] + p_j*(gprobs_j - dot) [softmax bwd]
-//   normed.grad = dX of selected experts (desc.) + glog . R^T [matmul_nt_acc]
-//   h.grad += rmsnorm backward (kernels.hpp:130-152)
-template <int MAXM>
-__global__ void __launch_bounds__(128) router_bwd_k(
-    const float* __restrict__ h, const float* __restrict__ gain, const float* __restrict__ R,
-    const float* __restrict__ probs, const float* __restrict__ lse_r,
-    const float* __restrict__ inv_rms, const float* __restrict__ denom,
-    const int32_t* __restrict__ topk_idx, const int32_t* __restrict__ slot_row,
-    const float* __restrict__ gw_part, const float* __restrict__ dxp,
-    const float* __restrict__ lb_coeff, int T, int d, int M, int k, int renorm, float g_lbsum,
-    float g_s, float* __restrict__ glog, float* __restrict__ gnormed, float* __restrict__ gh) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= T) return;
-    const int nparts = d / 64;
-    float p[MAXM], gp[MAXM];
-    const float* prow = probs + static_cast<int64_t>(t) * M;
-#pragma unroll
-    for (int e = 0; e < MAXM; ++e) {
-        if (e < M) {
-            p[e] = prow[e];
-            gp[e] = fadd(0.f, fmul(g_lbsum, __ldg(lb_coeff + e)));
-        }
-    }
-    int32_t sel[8], rows[8];
-    for (int s = 0; s < k; ++s) {
-        sel[s] = topk_idx[static_cast<int64_t>(t) * k + s];
-        rows[s] = slot_row[static_cast<int64_t>(t) * k + s];
-    }
-    const float dn = renorm ? denom[t] : 1.f;
-    float gden = 0.f;
-    for (int s = k - 1; s >= 0; --s) {  // experts in descending order
-        float gw = 0.f;
-        const float* part = gw_part + static_cast<int64_t>(rows[s]) * nparts;
-        for (int i = 0; i < nparts; ++i) gw += part[i];
-        const int j = sel[s];
-#pragma unroll
-        for (int e = 0; e < MAXM; ++e) {
-            if (e == j) {
-                if (renorm) {
-                    gden = fsub(gden, fdiv(fmul(gw, p[e]), fmul(dn, dn)));
-                    gp[e] = fadd(gp[e], fadd(0.f, fdiv(gw, dn)));
-                } else {
-                    gp[e] = fadd(gp[e], fadd(0.f, gw));
-                }
-            }
-        }
-    }
-    if (renorm)
-        for (int s = k - 1; s >= 0; --s) {
-#pragma unroll
-            for (int e = 0; e < MAXM; ++e)
-                if (e == sel[s]) gp[e] = fadd(gp[e], gden);
-        }
-    const float lv = lse_r[t];
-    const float gl = fadd(fadd(0.f, fmul(g_s, lv)), fmul(g_s, lv));
-    float dot = 0.f;
-#pragma unroll
-    for (int e = 0; e < MAXM; ++e)
-        if (e < M) dot = fadd(dot, fmul(gp[e], p[e]));
-    float* grow = glog + static_cast<int64_t>(t) * M;
-#pragma unroll
-    for (int e = 0; e < MAXM; ++e) {
-        if (e < M) {
-            gp[e] = fadd(fadd(0.f, fmul(gl, p[e])), fmul(p[e], fsub(gp[e], dot)));  // = glog_e
-            grow[e] = gp[e];
-        }
-    }
-    // normed.grad: expert dX (descending experts) then + sum_e glog_e * R[q][e]
-    const float* x = h + static_cast<int64_t>(t) * d;
-    float* gy = gnormed + static_cast<int64_t>(t) * d;
-    const float inv = inv_rms[t];
-    float dot2 = 0.f;
-    for (int q = 0; q < d; ++q) {
-        float a = 0.f;
-        for (int s = k - 1; s >= 0; --s) a = fadd(a, __ldg(dxp + static_cast<int64_t>(rows[s]) * d + q));
-        const float* rr = R + static_cast<int64_t>(q) * M;
-        float sr = 0.f;
-#pragma unroll
-        for (int e = 0; e < MAXM; ++e)
-            if (e < M) sr = fadd(sr, fmul(gp[e], __ldg(rr + e)));
-        a = fadd(a, sr);
-        gy[q] = a;
-        dot2 = fadd(dot2, fmul(fmul(a, __ldg(gain + q)), x[q]));
-    }
-    const float coef = fdiv(fmul(fmul(fmul(dot2, inv), inv), inv), static_cast<float>(d));
-    float* ghr = gh + static_cast<int64_t>(t) * d;
-    for (int q = 0; q < d; ++q) {
-        const float a = gy[q];
-        ghr[q] = fadd(ghr[q], fsub(fmul(fmul(a, __ldg(gain + q)), inv), fmul(coef, x[q])));
-    }
-}
-
-void router_backward(const float* h, const float* gain, const float* router, const float* probs,
-                     const float* lse_r, const float* inv_rms, const float* denom,
-                     const int32_t* topk_idx, const int32_t* slot_row, const float* gw_part,
-                     const float* dxp, const float* lb_coeff, int64_t T, int64_t d, int M, int k,
-                     int renorm, float g_lbsum, float g_s, float* glog, float* gnormed,
-                     float* gh, cudaStream_t s) {
-    dim3 grid(static_cast<unsigned>(cdiv(T, 128)));
-#define SPES_RB(MM)                                                                              \
-    router_bwd_k<MM><<<grid, 128, 0, s>>>(h, gain, router, probs, lse_r, inv_rms, denom, topk_idx, \
-                                          slot_row, gw_part, dxp, lb_coeff, (int)T, (int)d, M, k,  \
-                                          renorm, g_lbsum, g_s, glog, gnormed, gh)
-    if (M <= 8)
-        SPES_RB(8);
-    else if (M <= 16)
-        SPES_RB(16);
-    else if (M <= 32)
-        SPES_RB(32);
-    else
-        SPES_RB(64);
-#undef SPES_RB
+                      bf16* dyw, float* gw, cudaStream_t s) {
+    combine_bwd_k<<<static_cast<unsigned>(cdiv(R_cap, 8)), 256, 0, s>>>(gh, y, row_token, row_w,
+                                                                       R_total_dev, d, dyw, gw);
     count_launch();
 }
 

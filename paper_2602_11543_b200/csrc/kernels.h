@@ -81,7 +81,7 @@ void losses_reduce(const float* diff, const float* lse_head, const float* lse_r,
 // ---- backward ----
 void combine_backward(const float* gh, const float* y, const int32_t* row_token,
                       const float* row_w, const int32_t* R_total_dev, int64_t R_cap, int64_t d,
-                      bf16* dyw, bf16* dywT, float* gw_part, cudaStream_t s);
+                      bf16* dyw, float* gw_part, cudaStream_t s);
 void router_backward(const float* h, const float* gain, const float* router, const float* probs,
                      const float* lse_r, const float* inv_rms, const float* denom,
                      const int32_t* topk_idx, const int32_t* slot_row, const float* gw_part,
@@ -117,15 +117,15 @@ void merge_apply(float* params, const int64_t* expert_offs, int M, int64_t per,
                  int nblocks, cudaStream_t s);
 
 // ---- GEMMs (gemm.cu) ----
-struct GemmMaps;  // opaque
 void gemm_swiglu(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
-                 const int32_t* tiles, int max_tiles, bf16* hact, bf16* hactT, int64_t R_cap,
-                 int64_t f, cudaStream_t s);
-void gemm_store_f32(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g,
-                    int ng, const int32_t* tiles, int max_tiles, cudaStream_t s);
+                 const int32_t* tiles, int max_tiles, bf16* hact, int64_t f, cudaStream_t s);
+// mn: operands are [K x M] / [K x N] row-major (weight-gradient form)
+void gemm_store_f32(int bn, bool mn, const CUtensorMap& a, const CUtensorMap& b,
+                    const GemmGroup* g, int ng, const int32_t* tiles, int max_tiles,
+                    cudaStream_t s);
 void gemm_dswiglu(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
-                  const int32_t* tiles, int max_tiles, const bf16* gu, bf16* dgu, bf16* dguT,
-                  int64_t R_cap, int64_t f, cudaStream_t s);
+                  const int32_t* tiles, int max_tiles, const bf16* gu, int64_t f,
+                  cudaStream_t s);
 void gemm_grad_w1(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
                   const int32_t* tiles, int max_tiles, cudaStream_t s);
 void gemm_prepare(int device);
