@@ -172,15 +172,19 @@ struct spes_ctx {
     std::vector<LayerBufs> layers;
     int32_t *tokens = nullptr, *inputs = nullptr, *targets = nullptr, *err = nullptr;
     bf16 *dyw = nullptr, *dgu = nullptr;
+    float *dot_part = nullptr;
+    double* loss_part = nullptr;
     float *dxp = nullptr, *gw_part = nullptr, *glog = nullptr, *gnormed = nullptr, *gh = nullptr,
           *nr_partial = nullptr;
     bf16 *hL = nullptr, *dlog_bf = nullptr;
     float *head_logits = nullptr, *dlogits = nullptr, *diff = nullptr, *lse_head = nullptr;
     float *lse_all = nullptr, *probs_all = nullptr, *coeff_all = nullptr;
     double* d_losses = nullptr;
-    GemmGroup* head_groups = nullptr;  // [3]
+    GemmGroup* head_groups = nullptr;  // [2 + head_split]: fwd, dX, dW K-splits
     int32_t* head_tiles = nullptr;     // [3]
     int head_max[3] = {0, 0, 0};
+    int head_split = 1;
+    float* head_dw_part = nullptr;
     CUtensorMap a_dyw, a_dgu, b_dgu_mn, b_dyw_mn, a_hL, b_headT, a_dlog, b_headB, a_hL_mn, b_dlog_mn;
     int max_tiles[6] = {0, 0, 0, 0, 0, 0};
 
@@ -387,6 +391,8 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     c->dgu = A.alloc<bf16>(R * 2 * f);
     c->dxp = A.alloc<float>(R * d);
     c->gw_part = A.alloc<float>(R);
+    c->dot_part = A.alloc<float>(Tp * (d / 128));
+    c->loss_part = A.alloc<double>((Tp / 256 + 1) * (2 + 2 * L.L));
     c->glog = A.alloc<float>(Tp * M);
     c->gnormed = A.alloc<float>(Tp * d);
     c->gh = A.alloc<float>(Tp * d);
@@ -398,8 +404,17 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     c->diff = A.alloc<float>(Tp);
     c->lse_head = A.alloc<float>(Tp);
     c->d_losses = A.alloc<double>(8);
-    c->head_groups = A.alloc<GemmGroup>(3);
+    // head dW = hL^T dlogits has only (d/128)*(V/BN) output tiles: split K (tokens)
+    // so the grid covers the SMs; partials are summed in split order (deterministic).
+    {
+        const int64_t tiles = (d / 128) * (V / bn_for(V));
+        int64_t ns = std::max<int64_t>(1, (2 * 148 + tiles - 1) / tiles);
+        while (ns > 1 && (Tp % (64 * ns) != 0 || Tp / ns < 512)) --ns;
+        c->head_split = static_cast<int>(ns);
+    }
+    c->head_groups = A.alloc<GemmGroup>(2 + c->head_split);
     c->head_tiles = A.alloc<int32_t>(3);
+    c->head_dw_part = c->head_split > 1 ? A.alloc<float>(c->head_split * d * V) : nullptr;
     using spes_host::make_tmap_bf16;
     c->a_dyw = make_tmap_bf16(c->dyw, R, d, 128);
     c->a_dgu = make_tmap_bf16(c->dgu, R, 2 * f, 128);
@@ -412,7 +427,7 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     c->a_hL_mn = make_tmap_bf16(c->hL, Tp, d, 64);
     c->b_dlog_mn = make_tmap_bf16(c->dlog_bf, Tp, V, 64);
     // head GEMM groups (static for a given T_pad)
-    GemmGroup hg[3]{};
+    std::vector<GemmGroup> hg(2 + c->head_split);
     hg[0].k_len = static_cast<int32_t>(d);
     hg[0].m_tiles = static_cast<int32_t>(Tp / 128);
     hg[0].n_tiles = static_cast<int32_t>(V / bn_for(V));
@@ -423,17 +438,29 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     hg[1].n_tiles = static_cast<int32_t>(d / bn_for(d));
     hg[1].out0 = c->gh;
     hg[1].ldo = d;
-    hg[2].k_len = static_cast<int32_t>(Tp);
-    hg[2].m_tiles = static_cast<int32_t>(d / 128);
-    hg[2].n_tiles = static_cast<int32_t>(V / bn_for(V));
-    hg[2].out0 = c->grads + L.off_head();  // psi is first in the compact layout
-    hg[2].ldo = V;
+    const int nsplit = c->head_split;
+    int32_t ts = 0;
+    for (int sp = 0; sp < nsplit; ++sp) {
+        GemmGroup& g = hg[2 + sp];
+        g.k0 = static_cast<int32_t>(sp * (Tp / nsplit));
+        g.k_len = static_cast<int32_t>(Tp / nsplit);
+        g.m_tiles = static_cast<int32_t>(d / 128);
+        g.n_tiles = static_cast<int32_t>(V / bn_for(V));
+        g.out0 = nsplit > 1 ? c->head_dw_part + sp * d * V
+                       : c->grads + L.off_head();  // psi is first in the compact layout
+        g.ldo = V;
+        g.tile_start = ts;
+        ts += g.m_tiles * g.n_tiles;
+    }
     int32_t ht[3];
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < 2; ++i) {
         ht[i] = hg[i].m_tiles * hg[i].n_tiles;
         c->head_max[i] = ht[i];
     }
-    ck(cudaMemcpy(c->head_groups, hg, sizeof(hg), cudaMemcpyHostToDevice), "head groups");
+    ht[2] = ts;
+    c->head_max[2] = ts;
+    ck(cudaMemcpy(c->head_groups, hg.data(), sizeof(GemmGroup) * hg.size(), cudaMemcpyHostToDevice),
+       "head groups");
     ck(cudaMemcpy(c->head_tiles, ht, sizeof(ht), cudaMemcpyHostToDevice), "head tiles");
     // upper bounds of routed GEMM tile counts
     const int64_t mt_max = (T * k) / 128 + M;
@@ -530,7 +557,7 @@ void forward_backward(spes_ctx* c) {
                         c->dlogits, c->diff, c->lse_head, st);
         spes_k::losses_reduce(c->diff, c->lse_head, c->lse_all, c->probs_all, c->coeff_all, T, Tp,
                               L.L, M, sd.inv_T, sd.inv_L, sd.c_ce, sd.c_lb, sd.c_mz, sd.c_z,
-                              c->d_losses, st);
+                              c->loss_part, c->d_losses, st);
     }
     // ---- backward ----
     {
@@ -538,8 +565,11 @@ void forward_backward(spes_ctx* c) {
         spes_k::gather_rows_bf16(c->dlogits, V, nullptr, nullptr, Tp, V, c->dlog_bf, nullptr, Tp, st);
         spes_k::gemm_store_f32(bn_for(d), false, c->a_dlog, c->b_headB, c->head_groups + 1, 1,
                                c->head_tiles + 1, c->head_max[1], st);
-        spes_k::gemm_store_f32(bn_for(V), true, c->a_hL_mn, c->b_dlog_mn, c->head_groups + 2, 1,
-                               c->head_tiles + 2, c->head_max[2], st);
+        spes_k::gemm_store_f32(bn_for(V), true, c->a_hL_mn, c->b_dlog_mn, c->head_groups + 2,
+                               c->head_split, c->head_tiles + 2, c->head_max[2], st);
+        if (c->head_split > 1)
+            spes_k::splitk_reduce(c->head_dw_part, c->head_split, d * V,
+                                  c->grads + L.off_head(), st);
     }
     for (int l = L.L - 1; l >= 0; --l) {
         LayerBufs& Y = c->layers[l];
@@ -576,7 +606,7 @@ void forward_backward(spes_ctx* c) {
                                     Y.lse_r, Y.inv_rms, Y.denom, Y.topk_idx, Y.slot_row,
                                     c->gw_part, c->dxp, Y.lb_coeff, T, d, M, k,
                                     c->cfg.renormalize_after_topk, sd.g_lbsum, sd.g_s, c->glog,
-                                    c->gnormed, c->gh, st);
+                                    c->gnormed, c->dot_part, c->gh, st);
         }
         {
             PROF("norm_router_grads");

@@ -52,154 +52,6 @@ void embed_gather(const float* emb, const int32_t* tokens, int64_t B, int64_t S,
     count_launch();
 }
 
-// ============================ router forward ============================
-// One thread per token, bit-exact with the reference given identical h:
-//   rmsnorm_forward (kernels.hpp:117-128): sequential sum of squares, y = (x*inv)*g
-//   matmul (kernels.hpp:27-38): logit_e = sum_p normed_p * R[p][e], p ascending, no FMA
-//   softmax_rows (kernels.hpp:156-172) with glibc expf; logsumexp (:174-185)
-//   route_from_logits (model.hpp:185-216): stable top-k, ascending indices, weights
-constexpr int RCH = 32;  // router rows staged per smem chunk
-
-template <int MAXM>
-__global__ void __launch_bounds__(128) router_fwd_k(
-    const float* __restrict__ h, const float* __restrict__ gain, const float* __restrict__ R,
-    int T, int d, int M, int k, int renorm, float eps, int variant, float* __restrict__ normed,
-    float* __restrict__ logits, float* __restrict__ probs, int32_t* __restrict__ topk_idx,
-    float* __restrict__ topk_w, float* __restrict__ lse_out, float* __restrict__ inv_out,
-    float* __restrict__ denom_out) {
-    __shared__ __align__(16) float sR[RCH * MAXM];
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool valid = t < T;
-    const float* x = h + static_cast<int64_t>(valid ? t : 0) * d;
-
-    float ms = 0.f;
-    if (valid) {
-        for (int q = 0; q < d; q += 4) {
-            float4 v = __ldg(reinterpret_cast<const float4*>(x + q));
-            ms = fadd(ms, fmul(v.x, v.x));
-            ms = fadd(ms, fmul(v.y, v.y));
-            ms = fadd(ms, fmul(v.z, v.z));
-            ms = fadd(ms, fmul(v.w, v.w));
-        }
-    }
-    const float inv = fdiv(1.f, fsqrt(fadd(fdiv(ms, static_cast<float>(d)), eps)));
-
-    float acc[MAXM];
-#pragma unroll
-    for (int e = 0; e < MAXM; ++e) acc[e] = 0.f;
-    float* nrow = normed + static_cast<int64_t>(valid ? t : 0) * d;
-    for (int q0 = 0; q0 < d; q0 += RCH) {
-        __syncthreads();
-        for (int i = threadIdx.x; i < RCH * M; i += blockDim.x) sR[i] = __ldg(R + static_cast<int64_t>(q0) * M + i);
-        __syncthreads();
-        if (!valid) continue;
-#pragma unroll 1
-        for (int qq = 0; qq < RCH; qq += 4) {
-            const float4 xv = __ldg(reinterpret_cast<const float4*>(x + q0 + qq));
-            const float4 gv = __ldg(reinterpret_cast<const float4*>(gain + q0 + qq));
-            float nv[4];
-            nv[0] = fmul(fmul(xv.x, inv), gv.x);
-            nv[1] = fmul(fmul(xv.y, inv), gv.y);
-            nv[2] = fmul(fmul(xv.z, inv), gv.z);
-            nv[3] = fmul(fmul(xv.w, inv), gv.w);
-            *reinterpret_cast<float4*>(nrow + q0 + qq) = make_float4(nv[0], nv[1], nv[2], nv[3]);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const float* rrow = sR + (qq + u) * M;
-#pragma unroll
-                for (int e = 0; e < MAXM; ++e)
-                    if (e < M) acc[e] = fadd(acc[e], fmul(nv[u], rrow[e]));
-            }
-        }
-    }
-    if (!valid) return;
-
-    float* lrow = logits + static_cast<int64_t>(t) * M;
-    float mx = acc[0];
-#pragma unroll
-    for (int e = 0; e < MAXM; ++e) {
-        if (e < M) {
-            lrow[e] = acc[e];
-            if (e > 0) mx = (mx < acc[e]) ? acc[e] : mx;  // std::max(mx, x)
-        }
-    }
-    float sum = 0.f;
-#pragma unroll
-    for (int e = 0; e < MAXM; ++e) {
-        if (e < M) {
-            const float z = fsub(acc[e], mx);
-            acc[e] = variant ? spes_expf::expf_glibc<1>(z) : spes_expf::expf_glibc<0>(z);
-            sum = fadd(sum, acc[e]);
-        }
-    }
-    const float isum = fdiv(1.f, sum);
-    float* prow = probs + static_cast<int64_t>(t) * M;
-#pragma unroll
-    for (int e = 0; e < MAXM; ++e) {
-        if (e < M) {
-            acc[e] = fmul(acc[e], isum);
-            prow[e] = acc[e];
-        }
-    }
-    lse_out[t] = mx + logf(sum);
-    inv_out[t] = inv;
-
-    // top-k: iterative argmax (strict '>' scanning ascending => lowest index on ties),
-    // identical to the first k of a stable descending sort.
-    uint64_t chosen = 0;
-    for (int s = 0; s < k; ++s) {
-        int best = -1;
-        float bv = 0.f;
-#pragma unroll
-        for (int e = 0; e < MAXM; ++e) {
-            if (e < M && !((chosen >> e) & 1ull)) {
-                if (best < 0 || acc[e] > bv) {
-                    best = e;
-                    bv = acc[e];
-                }
-            }
-        }
-        chosen |= 1ull << best;
-    }
-    float dn = 0.f;
-#pragma unroll
-    for (int e = 0; e < MAXM; ++e)
-        if ((chosen >> e) & 1ull) dn = fadd(dn, acc[e]);
-    int slot = 0;
-    int32_t* irow = topk_idx + static_cast<int64_t>(t) * k;
-    float* wrow = topk_w + static_cast<int64_t>(t) * k;
-#pragma unroll
-    for (int e = 0; e < MAXM; ++e) {
-        if ((chosen >> e) & 1ull) {
-            irow[slot] = e;
-            wrow[slot] = renorm ? fdiv(acc[e], dn) : acc[e];
-            ++slot;
-        }
-    }
-    if (denom_out) denom_out[t] = dn;
-}
-
-void router_forward(const float* h, const float* gain, const float* router, int64_t T, int64_t d,
-                    int M, int k, int renorm, float eps, int variant, float* normed,
-                    float* logits, float* probs, int32_t* topk_idx, float* topk_w, float* lse,
-                    float* inv_rms, float* denom, cudaStream_t s) {
-    dim3 grid(static_cast<unsigned>(cdiv(T, 128)));
-#define SPES_ROUTER(MM)                                                                         \
-    router_fwd_k<MM><<<grid, 128, 0, s>>>(h, gain, router, (int)T, (int)d, M, k, renorm, eps,   \
-                                          variant, normed, logits, probs, topk_idx, topk_w, lse, \
-                                          inv_rms, denom)
-    if (M <= 8)
-        SPES_ROUTER(8);
-    else if (M <= 16)
-        SPES_ROUTER(16);
-    else if (M <= 32)
-        SPES_ROUTER(32);
-    else
-        SPES_ROUTER(64);
-#undef SPES_ROUTER
-    count_launch();
-}
-
 // ============================ routing plan ============================
 constexpr int ROUTE_CH = 256;  // tokens per chunk
 
@@ -331,34 +183,48 @@ __global__ void route_scatter_k(const int32_t* __restrict__ idx, const float* __
                                 int T, int M, int k, const int32_t* __restrict__ chunk_base,
                                 const int32_t* __restrict__ pad_off, int32_t* __restrict__ slot_row,
                                 int32_t* __restrict__ row_token, float* __restrict__ row_w) {
-    __shared__ int32_t base[64];
-    for (int j = threadIdx.x; j < M; j += blockDim.x)
-        base[j] = pad_off[j] + chunk_base[static_cast<int64_t>(blockIdx.x) * M + j];
+    __shared__ int32_t wbase[ROUTE_CH / 32][64];  // per-warp counts, then per-warp bases
     const int t = blockIdx.x * ROUTE_CH + threadIdx.x;
     const bool valid = t < T;
-    int32_t sel[8];
-    for (int s = 0; s < k; ++s) sel[s] = valid ? idx[static_cast<int64_t>(t) * k + s] : -1;
+    int32_t sel[8], rank[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        sel[s] = (valid && s < k) ? idx[static_cast<int64_t>(t) * k + s] : -1;
+        rank[s] = 0;
+    }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t lt = lanemask_lt();
-    for (int w8 = 0; w8 < ROUTE_CH / 32; ++w8) {
-        __syncthreads();
-        if (warp == w8) {
-            for (int j = 0; j < M; ++j) {
-                int my_s = -1;
-                for (int s = 0; s < k; ++s)
-                    if (sel[s] == j) my_s = s;
-                const uint32_t mask = __ballot_sync(0xffffffffu, my_s >= 0);
-                if (mask == 0) continue;
-                if (my_s >= 0) {
-                    const int32_t row = base[j] + __popc(mask & lt);
-                    slot_row[static_cast<int64_t>(t) * k + my_s] = row;
-                    row_token[row] = t;
-                    row_w[row] = w[static_cast<int64_t>(t) * k + my_s];
-                }
-                __syncwarp();
-                if (lane == 0) base[j] += __popc(mask);
-                __syncwarp();
-            }
+    // in-warp ranks: all warps in parallel, one ballot per expert
+    for (int j = 0; j < M; ++j) {
+        bool has = false;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) has |= (sel[s] == j);
+        const uint32_t mask = __ballot_sync(0xffffffffu, has);
+        const int32_t r = __popc(mask & lt);
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+            if (sel[s] == j) rank[s] = r;
+        if (lane == 0) wbase[warp][j] = __popc(mask);
+    }
+    __syncthreads();
+    // exclusive scan over warps in token order, seeded with this chunk's base
+    for (int j = threadIdx.x; j < M; j += blockDim.x) {
+        int32_t acc = pad_off[j] + chunk_base[static_cast<int64_t>(blockIdx.x) * M + j];
+        for (int w8 = 0; w8 < ROUTE_CH / 32; ++w8) {
+            const int32_t c = wbase[w8][j];
+            wbase[w8][j] = acc;
+            acc += c;
+        }
+    }
+    __syncthreads();
+    if (!valid) return;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        if (s < k) {
+            const int32_t row = wbase[warp][sel[s]] + rank[s];
+            slot_row[static_cast<int64_t>(t) * k + s] = row;
+            row_token[row] = t;
+            row_w[row] = w[static_cast<int64_t>(t) * k + s];
         }
     }
 }
@@ -543,41 +409,59 @@ __device__ double block_sum_d(double v, double* sh) {
     return r;  // valid in thread 0
 }
 
-__global__ void losses_k(const float* __restrict__ diff, const float* __restrict__ lse_head,
-                         const float* __restrict__ lse_r, const float* __restrict__ probs,
-                         const float* __restrict__ lb_coeff, int64_t T, int64_t Tstride, int L,
-                         int M, float inv_T,
-                         float inv_L, float c_ce, float c_lb, float c_mz, float c_z,
-                         double* __restrict__ out) {
+// Per-block partial sums (thread per token, fixed-order tree), then one block
+// combines the partials in block order: deterministic, tolerance-level vs the
+// reference's sequential fp32 sums. Slots: 0 ce terms, 1 lse_head^2, then per
+// layer (lse_router^2, sum_j p_j*coeff_j).
+__global__ void __launch_bounds__(256) losses_partial_k(
+    const float* __restrict__ diff, const float* __restrict__ lse_head,
+    const float* __restrict__ lse_r, const float* __restrict__ probs,
+    const float* __restrict__ lb_coeff, int64_t T, int64_t Tstride, int L, int M,
+    double* __restrict__ part) {
     __shared__ double sh[32];
-    double a = 0, b = 0;
-    for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
-        a += diff[t];
-        b += static_cast<double>(lse_head[t]) * lse_head[t];
-    }
-    const double s_ce = block_sum_d(a, sh);
-    const double s_z = block_sum_d(b, sh);
-    double mz = 0, lb = 0;
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool v = t < T;
+    const int ns = 2 + 2 * L;
+    double a = v ? static_cast<double>(diff[t]) : 0.0;
+    double b = v ? static_cast<double>(lse_head[t]) * lse_head[t] : 0.0;
+    a = block_sum_d(a, sh);
+    if (threadIdx.x == 0) part[static_cast<int64_t>(blockIdx.x) * ns + 0] = a;
+    b = block_sum_d(b, sh);
+    if (threadIdx.x == 0) part[static_cast<int64_t>(blockIdx.x) * ns + 1] = b;
     for (int l = 0; l < L; ++l) {
         double c = 0, e = 0;
-        for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
+        if (v) {
             const float lv = lse_r[static_cast<int64_t>(l) * Tstride + t];
-            c += static_cast<double>(lv) * lv;
+            c = static_cast<double>(lv) * lv;
             const float* pr = probs + (static_cast<int64_t>(l) * Tstride + t) * M;
-            double r = 0;
-            for (int j = 0; j < M; ++j) r += static_cast<double>(pr[j]) * lb_coeff[l * M + j];
-            e += r;
+            for (int j = 0; j < M; ++j) e += static_cast<double>(pr[j]) * lb_coeff[l * M + j];
         }
-        const double sc = block_sum_d(c, sh);
-        const double se = block_sum_d(e, sh);
-        if (threadIdx.x == 0) {
-            mz += static_cast<float>(sc) * inv_T;
-            lb += static_cast<float>(se);
-        }
+        c = block_sum_d(c, sh);
+        if (threadIdx.x == 0) part[static_cast<int64_t>(blockIdx.x) * ns + 2 + 2 * l] = c;
+        e = block_sum_d(e, sh);
+        if (threadIdx.x == 0) part[static_cast<int64_t>(blockIdx.x) * ns + 3 + 2 * l] = e;
     }
+}
+
+__global__ void losses_finish_k(const double* __restrict__ part, int nb, int L, float inv_T,
+                                float inv_L, float c_ce, float c_lb, float c_mz, float c_z,
+                                double* __restrict__ out) {
+    __shared__ double acc[2 + 2 * 64];
+    const int ns = 2 + 2 * L;
+    for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+        double s = 0.0;
+        for (int b = 0; b < nb; ++b) s += part[static_cast<int64_t>(b) * ns + i];
+        acc[i] = s;
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
-        const float ce = static_cast<float>(s_ce) * inv_T;
-        const float z = static_cast<float>(s_z) * inv_T;
+        double mz = 0, lb = 0;
+        for (int l = 0; l < L; ++l) {
+            mz += static_cast<float>(acc[2 + 2 * l]) * inv_T;
+            lb += static_cast<float>(acc[3 + 2 * l]);
+        }
+        const float ce = static_cast<float>(acc[0]) * inv_T;
+        const float z = static_cast<float>(acc[1]) * inv_T;
         const float moe_z = static_cast<float>(mz) * inv_L;
         const float lbv = static_cast<float>(lb) * inv_L;
         const float total = (ce * c_ce + lbv * c_lb) + (moe_z * c_mz + z * c_z);
@@ -592,10 +476,12 @@ __global__ void losses_k(const float* __restrict__ diff, const float* __restrict
 void losses_reduce(const float* diff, const float* lse_head, const float* lse_r,
                    const float* probs, const float* lb_coeff, int64_t T, int64_t Tstride, int L,
                    int M, float inv_T, float inv_L, float c_ce, float c_lb, float c_mz, float c_z,
-                   double* out, cudaStream_t s) {
-    losses_k<<<1, 1024, 0, s>>>(diff, lse_head, lse_r, probs, lb_coeff, T, Tstride, L, M, inv_T, inv_L,
-                                c_ce, c_lb, c_mz, c_z, out);
-    count_launch();
+                   double* part, double* out, cudaStream_t s) {
+    const int nb = static_cast<int>(cdiv(T, 256));
+    losses_partial_k<<<nb, 256, 0, s>>>(diff, lse_head, lse_r, probs, lb_coeff, T, Tstride, L, M,
+                                        part);
+    losses_finish_k<<<1, 128, 0, s>>>(part, nb, L, inv_T, inv_L, c_ce, c_lb, c_mz, c_z, out);
+    count_launch(2);
 }
 
 // ============================ combine (backward) ============================
@@ -655,7 +541,27 @@ __global__ void __launch_bounds__(256) norm_router_partial_k(
     float gg = 0.f, gr[MAXM];
 #pragma unroll
     for (int e = 0; e < MAXM; ++e) gr[e] = 0.f;
-    for (int t = t0 + ph; t < t1; t += 8) {
+    int t = t0 + ph;
+    for (; t + 24 < t1; t += 32) {  // four tokens in flight per thread
+        float gn[4], hv[4], iv[4], nv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t o = static_cast<int64_t>(t + 8 * u) * d + q;
+            gn[u] = __ldg(gnormed + o);
+            hv[u] = __ldg(h + o);
+            nv[u] = __ldg(normed + o);
+            iv[u] = __ldg(inv_rms + t + 8 * u);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            gg += (gn[u] * hv[u]) * iv[u];
+            const float* gl = glog + static_cast<int64_t>(t + 8 * u) * M;
+#pragma unroll
+            for (int e = 0; e < MAXM; ++e)
+                if (e < M) gr[e] += nv[u] * __ldg(gl + e);
+        }
+    }
+    for (; t < t1; t += 8) {
         const int64_t o = static_cast<int64_t>(t) * d + q;
         gg += (gnormed[o] * h[o]) * inv_rms[t];
         const float nv = normed[o];
@@ -1106,6 +1012,31 @@ void merge_apply(float* params, const int64_t* expert_offs, int M, int64_t per,
     cudaFuncSetAttribute(merge_apply_k<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     merge_apply_k<64><<<nblocks, 256, smem, s>>>(params, expert_offs, M, per, peers, K, coef,
                                                  disp_partial);
+    count_launch();
+}
+
+// ============================ split-K combine ============================
+__global__ void splitk_reduce_k(const float4* __restrict__ part, int nsplit, int64_t n4,
+                                float4* __restrict__ out) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        float4 a = __ldg(part + i);
+        for (int s = 1; s < nsplit; ++s) {
+            const float4 b = __ldg(part + s * n4 + i);
+            a.x += b.x;
+            a.y += b.y;
+            a.z += b.z;
+            a.w += b.w;
+        }
+        out[i] = a;
+    }
+}
+
+void splitk_reduce(const float* part, int nsplit, int64_t n, float* out, cudaStream_t s) {
+    const int64_t n4 = n / 4;
+    const int blocks = static_cast<int>(std::min<int64_t>(cdiv(n4, 256), 148 * 8));
+    splitk_reduce_k<<<blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(part), nsplit, n4,
+                                           reinterpret_cast<float4*>(out));
     count_launch();
 }
 

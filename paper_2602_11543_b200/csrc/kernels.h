@@ -76,7 +76,7 @@ void losses_reduce(const float* diff, const float* lse_head, const float* lse_r,
                    const float* probs, const float* lb_coeff, int64_t T, int64_t Tstride, int L,
                    int M,
                    float inv_T, float inv_L, float c_ce, float c_lb, float c_mz, float c_z,
-                   double* out, cudaStream_t s);
+                   double* part, double* out, cudaStream_t s);
 
 // ---- backward ----
 void combine_backward(const float* gh, const float* y, const int32_t* row_token,
@@ -87,7 +87,7 @@ void router_backward(const float* h, const float* gain, const float* router, con
                      const int32_t* topk_idx, const int32_t* slot_row, const float* gw_part,
                      const float* dxp, const float* lb_coeff, int64_t T, int64_t d, int M, int k,
                      int renorm, float g_lbsum, float g_s, float* glog, float* gnormed,
-                     float* gh, cudaStream_t s);
+                     float* dot_part, float* gh, cudaStream_t s);
 void norm_router_grads(const float* h, const float* normed, const float* gnormed,
                        const float* glog, const float* inv_rms, int64_t T, int64_t d, int M,
                        float* partial, float* g_gain, float* g_router, cudaStream_t s);
@@ -130,6 +130,9 @@ void gemm_grad_w1(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g
                   const int32_t* tiles, int max_tiles, cudaStream_t s);
 void gemm_prepare(int device);
 int num_sms();
+
+// out[i] = sum over splits in order of part[s*n + i]   (deterministic split-K combine)
+void splitk_reduce(const float* part, int nsplit, int64_t n, float* out, cudaStream_t s);
 
 // expf port checks
 void expf_port_device(const float* x, float* y, int64_t n, int variant, cudaStream_t s);

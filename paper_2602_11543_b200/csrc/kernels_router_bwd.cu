@@ -4,11 +4,14 @@
 //   logits.grad = (0 + gl*p_j) [moe_z logsumexp] + p_j*(gprobs_j - dot) [softmax bwd]
 //   normed.grad = dX of selected experts (desc.) + glog . R^T [matmul_nt_acc]
 //   h.grad     += rmsnorm backward (kernels.hpp:130-152)
-// Block = 8 warps x TPW tokens. Lanes < TPW of each warp do the per-token scalar
-// part (M values) in the reference's order; the d-wide part runs across the warp
-// with the router weights staged through shared memory one 128-row chunk at a
-// time (each chunk serves all the block's tokens), keeping every element's own
-// accumulation order.
+// Three kernels, each streaming its operands once:
+//   router_scalar_bwd_k : thread per token, the M-wide scalar chain  -> glog [T x M]
+//   normed_grad_k       : 32-token x 128-column tiles; per element the dX sum (descending
+//                         experts) then the sequential-e router product; per-tile partial
+//                         of sum_q (gy*g)*x for the rmsnorm dot
+//   rmsnorm_bwd_k       : warp per token, h.grad += (gy*g)*inv - coef*x
+// Every element keeps the reference's own accumulation order; only the rmsnorm dot
+// (a sum over d) is a fixed-order tree.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -16,140 +19,164 @@ namespace spes_k {
 
 using namespace spes_dev;
 
-constexpr int RB_TPW = 4;   // tokens per warp
-constexpr int RB_QCH = 128; // router rows per smem chunk
-
 template <int MAXM>
-__global__ void __launch_bounds__(256) router_bwd_k(
-    const float* __restrict__ h, const float* __restrict__ gain, const float* __restrict__ R,
+__global__ void __launch_bounds__(128) router_scalar_bwd_k(
     const float* __restrict__ probs, const float* __restrict__ lse_r,
-    const float* __restrict__ inv_rms, const float* __restrict__ denom,
-    const int32_t* __restrict__ topk_idx, const int32_t* __restrict__ slot_row,
-    const float* __restrict__ gw_row, const float* __restrict__ dxp,
-    const float* __restrict__ lb_coeff, int T, int d, int M, int k, int renorm, float g_lbsum,
-    float g_s, float* __restrict__ glog, float* __restrict__ gnormed, float* __restrict__ gh) {
-    __shared__ float sR[RB_QCH * (MAXM + 1)];
-    __shared__ float sg[8][RB_TPW][MAXM];
-    __shared__ int32_t srow[8][RB_TPW][8];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tbase = (blockIdx.x * 8 + warp) * RB_TPW;
-
-    // ---- per-token scalar part: lane i handles token tbase + i ----
-    if (lane < RB_TPW) {
-        const int t = tbase + lane;
-        if (t < T) {
-            float p[MAXM], gp[MAXM];
-            const float* prow = probs + static_cast<int64_t>(t) * M;
+    const float* __restrict__ denom, const int32_t* __restrict__ topk_idx,
+    const int32_t* __restrict__ slot_row, const float* __restrict__ gw_row,
+    const float* __restrict__ lb_coeff, int T, int M, int k, int renorm, float g_lbsum, float g_s,
+    float* __restrict__ glog) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    float p[MAXM], gp[MAXM];
+    const float* prow = probs + static_cast<int64_t>(t) * M;
 #pragma unroll
-            for (int e = 0; e < MAXM; ++e) {
-                if (e < M) {
-                    p[e] = prow[e];
-                    gp[e] = fadd(0.f, fmul(g_lbsum, __ldg(lb_coeff + e)));
+    for (int e = 0; e < MAXM; ++e) {
+        if (e < M) {
+            p[e] = prow[e];
+            gp[e] = fadd(0.f, fmul(g_lbsum, __ldg(lb_coeff + e)));
+        }
+    }
+    const float dn = renorm ? denom[t] : 1.f;
+    float gden = 0.f;
+    int32_t sel[8];
+    for (int s = k - 1; s >= 0; --s) {  // experts in descending order
+        const int j = topk_idx[static_cast<int64_t>(t) * k + s];
+        sel[s] = j;
+        const float gw = gw_row[slot_row[static_cast<int64_t>(t) * k + s]];
+#pragma unroll
+        for (int e = 0; e < MAXM; ++e) {
+            if (e == j) {
+                if (renorm) {
+                    gden = fsub(gden, fdiv(fmul(gw, p[e]), fmul(dn, dn)));
+                    gp[e] = fadd(gp[e], fadd(0.f, fdiv(gw, dn)));
+                } else {
+                    gp[e] = fadd(gp[e], fadd(0.f, gw));
                 }
             }
-            int32_t sel[8];
-            for (int s = 0; s < k; ++s) {
-                sel[s] = topk_idx[static_cast<int64_t>(t) * k + s];
-                srow[warp][lane][s] = slot_row[static_cast<int64_t>(t) * k + s];
-            }
-            const float dn = renorm ? denom[t] : 1.f;
-            float gden = 0.f;
-            for (int s = k - 1; s >= 0; --s) {  // experts in descending order
-                const float gw = gw_row[srow[warp][lane][s]];
-                const int j = sel[s];
-#pragma unroll
-                for (int e = 0; e < MAXM; ++e) {
-                    if (e == j) {
-                        if (renorm) {
-                            gden = fsub(gden, fdiv(fmul(gw, p[e]), fmul(dn, dn)));
-                            gp[e] = fadd(gp[e], fadd(0.f, fdiv(gw, dn)));
-                        } else {
-                            gp[e] = fadd(gp[e], fadd(0.f, gw));
-                        }
-                    }
-                }
-            }
-            if (renorm)
-                for (int s = k - 1; s >= 0; --s) {
-#pragma unroll
-                    for (int e = 0; e < MAXM; ++e)
-                        if (e == sel[s]) gp[e] = fadd(gp[e], gden);
-                }
-            const float lv = lse_r[t];
-            const float gl = fadd(fadd(0.f, fmul(g_s, lv)), fmul(g_s, lv));
-            float dot = 0.f;
+        }
+    }
+    if (renorm)
+        for (int s = k - 1; s >= 0; --s) {
 #pragma unroll
             for (int e = 0; e < MAXM; ++e)
-                if (e < M) dot = fadd(dot, fmul(gp[e], p[e]));
-            float* grow = glog + static_cast<int64_t>(t) * M;
-#pragma unroll
-            for (int e = 0; e < MAXM; ++e) {
-                if (e < M) {
-                    const float g = fadd(fadd(0.f, fmul(gl, p[e])), fmul(p[e], fsub(gp[e], dot)));
-                    grow[e] = g;
-                    sg[warp][lane][e] = g;
-                }
-            }
+                if (e == sel[s]) gp[e] = fadd(gp[e], gden);
         }
-    }
+    const float lv = lse_r[t];
+    const float gl = fadd(fadd(0.f, fmul(g_s, lv)), fmul(g_s, lv));
+    float dot = 0.f;
+#pragma unroll
+    for (int e = 0; e < MAXM; ++e)
+        if (e < M) dot = fadd(dot, fmul(gp[e], p[e]));
+    float* grow = glog + static_cast<int64_t>(t) * M;
+#pragma unroll
+    for (int e = 0; e < MAXM; ++e)
+        if (e < M) grow[e] = fadd(fadd(0.f, fmul(gl, p[e])), fmul(p[e], fsub(gp[e], dot)));
+}
 
-    // ---- d-wide part ----
-    float dot2[RB_TPW];
+constexpr int NG_TT = 32;   // tokens per tile
+constexpr int NG_QT = 128;  // columns per tile
+
+// grid (T/32, d/128), 256 threads: thread (ty, tx) -> tokens 4ty..4ty+3, columns tx + 32j
+template <int MAXM>
+__global__ void __launch_bounds__(256) normed_grad_k(
+    const float* __restrict__ h, const float* __restrict__ gain, const float* __restrict__ R,
+    const float* __restrict__ glog, const int32_t* __restrict__ slot_row,
+    const float* __restrict__ dxp, int T, int d, int M, int k, float* __restrict__ gnormed,
+    float* __restrict__ dot_part) {
+    __shared__ float sR[NG_QT * (MAXM + 1)];
+    __shared__ float sG[NG_TT][MAXM];
+    __shared__ int32_t sRow[NG_TT][8];
+    const int t0 = blockIdx.x * NG_TT, q0 = blockIdx.y * NG_QT;
+    for (int i = threadIdx.x; i < NG_QT * M; i += blockDim.x) {
+        const int qq = i / M, e = i % M;
+        sR[qq * (MAXM + 1) + e] = __ldg(R + static_cast<int64_t>(q0 + qq) * M + e);
+    }
+    for (int i = threadIdx.x; i < NG_TT * M; i += blockDim.x) {
+        const int tt = i / M, e = i % M;
+        sG[tt][e] = (t0 + tt < T) ? glog[static_cast<int64_t>(t0 + tt) * M + e] : 0.f;
+    }
+    for (int i = threadIdx.x; i < NG_TT * k; i += blockDim.x) {
+        const int tt = i / k, s = i % k;
+        sRow[tt][s] = (t0 + tt < T) ? slot_row[static_cast<int64_t>(t0 + tt) * k + s] : 0;
+    }
+    __syncthreads();
+    const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
+    float gq[4], xq[4];
 #pragma unroll
-    for (int i = 0; i < RB_TPW; ++i) dot2[i] = 0.f;
-    for (int q0 = 0; q0 < d; q0 += RB_QCH) {
-        __syncthreads();  // also publishes sg / srow on the first chunk
-        for (int i = threadIdx.x; i < RB_QCH * M; i += blockDim.x) {
-            const int qq = i / M, e = i % M;
-            sR[qq * (MAXM + 1) + e] = __ldg(R + static_cast<int64_t>(q0 + qq) * M + e);
-        }
-        __syncthreads();
+    for (int i = 0; i < 4; ++i) {
+        const int tt = ty * 4 + i;
+        const int t = t0 + tt;
+        if (t >= T) break;
+        float acc[4];
+        // issue all loads of this token first (memory-level parallelism)
+        float dv[8][4];
 #pragma unroll
-        for (int i = 0; i < RB_TPW; ++i) {
-            const int t = tbase + i;
-            if (t >= T) break;
-            const float* xr = h + static_cast<int64_t>(t) * d;
-            float* gy = gnormed + static_cast<int64_t>(t) * d;
+        for (int s = 0; s < 8; ++s) {
+            if (s < k) {
+                const float* src = dxp + static_cast<int64_t>(sRow[tt][s]) * d + q0 + tx;
 #pragma unroll
-            for (int u = 0; u < RB_QCH / 32; ++u) {
-                const int qq = lane + 32 * u;
-                const int q = q0 + qq;
-                float a = 0.f;
-                for (int s = k - 1; s >= 0; --s)
-                    a = fadd(a, __ldg(dxp + static_cast<int64_t>(srow[warp][i][s]) * d + q));
-                float sr = 0.f;
-                const float* rr = sR + qq * (MAXM + 1);
-#pragma unroll
-                for (int e = 0; e < MAXM; ++e)
-                    if (e < M) sr = fadd(sr, fmul(sg[warp][i][e], rr[e]));
-                a = fadd(a, sr);
-                gy[q] = a;
-                dot2[i] += (a * __ldg(gain + q)) * __ldg(xr + q);
+                for (int j = 0; j < 4; ++j) dv[s][j] = __ldg(src + 32 * j);
             }
         }
-    }
-    // ---- rmsnorm backward into h.grad ----
+        const float* xr = h + static_cast<int64_t>(t) * d + q0 + tx;
 #pragma unroll
-    for (int i = 0; i < RB_TPW; ++i) {
-        const int t = tbase + i;
-        const float tot = warp_sum(dot2[i]);
-        if (t >= T) continue;
-        const float inv = inv_rms[t];
-        const float coef = fdiv(fmul(fmul(fmul(tot, inv), inv), inv), static_cast<float>(d));
-        const float* xr = h + static_cast<int64_t>(t) * d;
-        const float* gy = gnormed + static_cast<int64_t>(t) * d;
-        float* ghr = gh + static_cast<int64_t>(t) * d;
-        for (int q0 = lane * 4; q0 < d; q0 += 128) {
-            const float4 a = *reinterpret_cast<const float4*>(gy + q0);
-            const float4 xv = __ldg(reinterpret_cast<const float4*>(xr + q0));
-            const float4 gv = __ldg(reinterpret_cast<const float4*>(gain + q0));
-            float4 o = *reinterpret_cast<const float4*>(ghr + q0);
-            o.x = fadd(o.x, fsub(fmul(fmul(a.x, gv.x), inv), fmul(coef, xv.x)));
-            o.y = fadd(o.y, fsub(fmul(fmul(a.y, gv.y), inv), fmul(coef, xv.y)));
-            o.z = fadd(o.z, fsub(fmul(fmul(a.z, gv.z), inv), fmul(coef, xv.z)));
-            o.w = fadd(o.w, fsub(fmul(fmul(a.w, gv.w), inv), fmul(coef, xv.w)));
-            *reinterpret_cast<float4*>(ghr + q0) = o;
+        for (int j = 0; j < 4; ++j) {
+            xq[j] = __ldg(xr + 32 * j);
+            gq[j] = __ldg(gain + q0 + tx + 32 * j);
         }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            float a = 0.f;
+#pragma unroll
+            for (int s = 7; s >= 0; --s)
+                if (s < k) a = fadd(a, dv[s][j]);
+            const float* rr = sR + (tx + 32 * j) * (MAXM + 1);
+            float sr = 0.f;
+#pragma unroll
+            for (int e = 0; e < MAXM; ++e)
+                if (e < M) sr = fadd(sr, fmul(sG[tt][e], rr[e]));
+            acc[j] = fadd(a, sr);
+        }
+        float* gy = gnormed + static_cast<int64_t>(t) * d + q0 + tx;
+        float part = 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            gy[32 * j] = acc[j];
+            part += (acc[j] * gq[j]) * xq[j];
+        }
+        part = warp_sum(part);
+        if (tx == 0) dot_part[static_cast<int64_t>(t) * (d / NG_QT) + blockIdx.y] = part;
+    }
+}
+
+__global__ void __launch_bounds__(256) rmsnorm_bwd_k(const float* __restrict__ h,
+                                                     const float* __restrict__ gain,
+                                                     const float* __restrict__ inv_rms,
+                                                     const float* __restrict__ gnormed,
+                                                     const float* __restrict__ dot_part, int T,
+                                                     int d, float* __restrict__ gh) {
+    const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (t >= T) return;
+    const int np = d / NG_QT;
+    float dot2 = 0.f;
+    for (int i = 0; i < np; ++i) dot2 += dot_part[static_cast<int64_t>(t) * np + i];
+    const float inv = inv_rms[t];
+    const float coef = fdiv(fmul(fmul(fmul(dot2, inv), inv), inv), static_cast<float>(d));
+    const float* xr = h + static_cast<int64_t>(t) * d;
+    const float* gy = gnormed + static_cast<int64_t>(t) * d;
+    float* ghr = gh + static_cast<int64_t>(t) * d;
+    for (int q0 = lane * 4; q0 < d; q0 += 128) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(gy + q0));
+        const float4 xv = __ldg(reinterpret_cast<const float4*>(xr + q0));
+        const float4 gv = __ldg(reinterpret_cast<const float4*>(gain + q0));
+        float4 o = *reinterpret_cast<const float4*>(ghr + q0);
+        o.x = fadd(o.x, fsub(fmul(fmul(a.x, gv.x), inv), fmul(coef, xv.x)));
+        o.y = fadd(o.y, fsub(fmul(fmul(a.y, gv.y), inv), fmul(coef, xv.y)));
+        o.z = fadd(o.z, fsub(fmul(fmul(a.z, gv.z), inv), fmul(coef, xv.z)));
+        o.w = fadd(o.w, fsub(fmul(fmul(a.w, gv.w), inv), fmul(coef, xv.w)));
+        *reinterpret_cast<float4*>(ghr + q0) = o;
     }
 }
 
@@ -158,12 +185,18 @@ void router_backward(const float* h, const float* gain, const float* router, con
                      const int32_t* topk_idx, const int32_t* slot_row, const float* gw_row,
                      const float* dxp, const float* lb_coeff, int64_t T, int64_t d, int M, int k,
                      int renorm, float g_lbsum, float g_s, float* glog, float* gnormed,
-                     float* gh, cudaStream_t s) {
-    const unsigned grid = static_cast<unsigned>((T + 8 * RB_TPW - 1) / (8 * RB_TPW));
-#define SPES_RB(MM)                                                                              \
-    router_bwd_k<MM><<<grid, 256, 0, s>>>(h, gain, router, probs, lse_r, inv_rms, denom, topk_idx, \
-                                          slot_row, gw_row, dxp, lb_coeff, (int)T, (int)d, M, k,   \
-                                          renorm, g_lbsum, g_s, glog, gnormed, gh)
+                     float* dot_part, float* gh, cudaStream_t s) {
+    const unsigned g1 = static_cast<unsigned>((T + 127) / 128);
+    const dim3 g2(static_cast<unsigned>((T + NG_TT - 1) / NG_TT), static_cast<unsigned>(d / NG_QT));
+    const unsigned g3 = static_cast<unsigned>((T + 7) / 8);
+#define SPES_RB(MM)                                                                             \
+    do {                                                                                        \
+        router_scalar_bwd_k<MM><<<g1, 128, 0, s>>>(probs, lse_r, denom, topk_idx, slot_row,     \
+                                                   gw_row, lb_coeff, (int)T, M, k, renorm,      \
+                                                   g_lbsum, g_s, glog);                         \
+        normed_grad_k<MM><<<g2, 256, 0, s>>>(h, gain, router, glog, slot_row, dxp, (int)T,      \
+                                             (int)d, M, k, gnormed, dot_part);                  \
+    } while (0)
     if (M <= 8)
         SPES_RB(8);
     else if (M <= 16)
@@ -173,7 +206,8 @@ void router_backward(const float* h, const float* gain, const float* router, con
     else
         SPES_RB(64);
 #undef SPES_RB
-    count_launch();
+    rmsnorm_bwd_k<<<g3, 256, 0, s>>>(h, gain, inv_rms, gnormed, dot_part, (int)T, (int)d, gh);
+    count_launch(3);
 }
 
 }  // namespace spes_k
