@@ -1385,7 +1385,7 @@ spes_status spes_kernel_router(const spes_model_cfg* cfg, const float* h, const 
         const int64_t d = cfg->hidden;
         const int M = cfg->experts_total, k = cfg->experts_active;
         if (k < 1 || k > M || M > 64 || k > 8) throw std::invalid_argument("route: need 1 <= k <= M");
-        if (d % 4) throw std::invalid_argument("router kernel: hidden must be a multiple of 4");
+        if (d % 64) throw std::invalid_argument("router kernel: hidden must be a multiple of 64");
         DevMem D;
         float* dh = D.alloc<float>(T * d);
         float* dg = D.alloc<float>(d);

@@ -102,48 +102,51 @@ __global__ void __launch_bounds__(256) normed_grad_k(
     }
     __syncthreads();
     const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
-    float gq[4], xq[4];
+    // router product for 4 tokens x 4 columns: one broadcast glog load per token and
+    // one router load per column feed 16 independent sequential-e chains
+    float sr[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sr[i][j] = 0.f;
+#pragma unroll 4
+    for (int e = 0; e < M; ++e) {
+        float g[4], r[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) g[i] = sG[ty * 4 + i][e];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) r[j] = sR[(tx + 32 * j) * (MAXM + 1) + e];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) sr[i][j] = fadd(sr[i][j], fmul(g[i], r[j]));
+    }
+    float gq[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) gq[j] = __ldg(gain + q0 + tx + 32 * j);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int tt = ty * 4 + i;
         const int t = t0 + tt;
         if (t >= T) break;
-        float acc[4];
-        // issue all loads of this token first (memory-level parallelism)
-        float dv[8][4];
+        // expert dX rows in descending expert order (select_rows backward, j descending)
+        float a[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int s = 0; s < 8; ++s) {
+        for (int s = 7; s >= 0; --s) {
             if (s < k) {
                 const float* src = dxp + static_cast<int64_t>(sRow[tt][s]) * d + q0 + tx;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) dv[s][j] = __ldg(src + 32 * j);
+                for (int j = 0; j < 4; ++j) a[j] = fadd(a[j], __ldg(src + 32 * j));
             }
         }
         const float* xr = h + static_cast<int64_t>(t) * d + q0 + tx;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            xq[j] = __ldg(xr + 32 * j);
-            gq[j] = __ldg(gain + q0 + tx + 32 * j);
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            float a = 0.f;
-#pragma unroll
-            for (int s = 7; s >= 0; --s)
-                if (s < k) a = fadd(a, dv[s][j]);
-            const float* rr = sR + (tx + 32 * j) * (MAXM + 1);
-            float sr = 0.f;
-#pragma unroll
-            for (int e = 0; e < MAXM; ++e)
-                if (e < M) sr = fadd(sr, fmul(sG[tt][e], rr[e]));
-            acc[j] = fadd(a, sr);
-        }
         float* gy = gnormed + static_cast<int64_t>(t) * d + q0 + tx;
         float part = 0.f;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            gy[32 * j] = acc[j];
-            part += (acc[j] * gq[j]) * xq[j];
+            const float v = fadd(a[j], sr[i][j]);
+            gy[32 * j] = v;
+            part += (v * gq[j]) * __ldg(xr + 32 * j);
         }
         part = warp_sum(part);
         if (tx == 0) dot_part[static_cast<int64_t>(t) * (d / NG_QT) + blockIdx.y] = part;
