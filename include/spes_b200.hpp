@@ -1,0 +1,192 @@
+// spes_b200.hpp -- C++ host mirror of the reference's operator interface over the C ABI.
+//
+// RAII context + the reference's exception types. When the reference headers are on
+// the include path (building inside /root/reference/proj), the
+// drop-in overloads below take and return the reference's own types with the same
+// signatures and semantics as
+//   local_round  (proj/include/spes/trainer.hpp:143-145)
+//   merge_model  (proj/include/spes/merging.hpp:138)
+//   Server::aggregate (proj/src/protocol.cpp:197-251; collective here: every node calls)
+#pragma once
+
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "spes_b200.h"
+
+namespace spes_b200 {
+
+// Rethrow a status as the exception class the reference would have thrown.
+inline void check(spes_status s) {
+    if (s == SPES_OK) return;
+    const std::string msg = spes_last_error();
+    switch (s) {
+        case SPES_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case SPES_OUT_OF_RANGE: throw std::out_of_range(msg);
+        case SPES_LOGIC_ERROR: throw std::logic_error(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+
+class Context {
+public:
+    Context(const spes_model_cfg& cfg, int node, int n_nodes, int device,
+            const void* nccl_id = nullptr)
+        : cfg_(cfg) {
+        check(spes_create(&cfg_, node, n_nodes, device, nccl_id, &ctx_));
+    }
+    ~Context() { spes_destroy(ctx_); }
+    Context(const Context&) = delete;
+    Context& operator=(const Context&) = delete;
+
+    spes_ctx* get() const { return ctx_; }
+    const spes_model_cfg& cfg() const { return cfg_; }
+    int64_t param_count() const { return spes_param_count(&cfg_); }
+
+    // node -> sorted experts, identical on every node (TrainMask of this node derived)
+    void set_ownership(const std::vector<std::vector<int>>& owned) {
+        std::vector<int32_t> offs{0}, ex;
+        for (const auto& o : owned) {
+            ex.insert(ex.end(), o.begin(), o.end());
+            offs.push_back(static_cast<int32_t>(ex.size()));
+        }
+        if (ex.empty()) ex.push_back(0);
+        check(spes_set_ownership(ctx_, offs.data(), ex.data()));
+    }
+    void load(const std::vector<float>& flat) {
+        check(spes_load_params(ctx_, flat.data(), static_cast<int64_t>(flat.size())));
+    }
+    std::vector<float> read() const {
+        std::vector<float> out(static_cast<size_t>(param_count()));
+        check(spes_read_params(ctx_, out.data(), static_cast<int64_t>(out.size())));
+        return out;
+    }
+    std::vector<spes_losses> local_round(const std::vector<int32_t>& tokens, int64_t B, int64_t S,
+                                         int H, const std::vector<double>& lr,
+                                         const spes_adamw_cfg& opt, bool carry_state = false) {
+        std::vector<spes_losses> out(static_cast<size_t>(H));
+        check(spes_local_round(ctx_, tokens.data(), B, S, H, lr.empty() ? nullptr : lr.data(), &opt,
+                               carry_state ? 1 : 0, out.data()));
+        return out;
+    }
+    spes_sync_stats sync() {
+        spes_sync_stats st{};
+        check(spes_sync(ctx_, &st));
+        return st;
+    }
+
+private:
+    spes_model_cfg cfg_;
+    spes_ctx* ctx_ = nullptr;
+};
+
+}  // namespace spes_b200
+
+#if defined(__has_include)
+#if __has_include("spes/trainer.hpp") && __has_include("spes/merging.hpp")
+#include "spes/merging.hpp"
+#include "spes/trainer.hpp"
+
+namespace spes_b200 {
+
+inline spes_model_cfg to_c(const spes::ModelConfig& c) {
+    spes_model_cfg o{};
+    o.vocab = c.vocab;
+    o.hidden = c.hidden;
+    o.intermediate = c.intermediate;
+    o.layers = c.layers;
+    o.experts_total = c.experts_total;
+    o.experts_active = c.experts_active;
+    o.renormalize_after_topk = c.renormalize_after_topk;
+    o.tied_head = c.tied_head;
+    o.coeff_ce = c.loss.ce;
+    o.coeff_lb = c.loss.lb;
+    o.coeff_moe_z = c.loss.moe_z;
+    o.coeff_z = c.loss.z;
+    o.rms_eps = c.rms_eps;
+    return o;
+}
+
+inline std::vector<float> flatten(const spes::ModelParams& p) {
+    std::vector<float> out;
+    for (const auto& b : spes::enumerate_blocks(p.config)) {
+        const auto& t = spes::block_tensor(p, b);
+        out.insert(out.end(), t.data.begin(), t.data.end());
+    }
+    return out;
+}
+
+inline void unflatten(const std::vector<float>& flat, spes::ModelParams& p) {
+    size_t off = 0;
+    for (const auto& b : spes::enumerate_blocks(p.config)) {
+        auto& t = spes::block_tensor(p, b);
+        std::memcpy(t.data.data(), flat.data() + off, t.data.size() * sizeof(float));
+        off += t.data.size();
+    }
+}
+
+// Drop-in for spes::local_round (trainer.hpp:143-222) with AdamW inner steps.
+inline spes::LocalRoundResult local_round(Context& ctx, const spes::ModelParams& global,
+                                          const spes::BatchProvider& next_batch,
+                                          const spes::LocalRoundConfig& cfg,
+                                          const spes::TrainMask& mask, bool carry_state = false) {
+    if (cfg.steps < 1) throw std::invalid_argument("local_round: need H >= 1");
+    if (cfg.inner != spes::InnerOpt::AdamW)
+        throw std::logic_error("b200 local_round: only the AdamW inner optimizer is on the B200 path");
+    ctx.load(flatten(global));
+    std::vector<int32_t> tokens;
+    int64_t B = 0, S = 0;
+    std::vector<double> lr;
+    for (int h = 0; h < cfg.steps; ++h) {
+        spes::Batch b = next_batch();
+        B = b.batch;
+        S = b.seq;
+        tokens.insert(tokens.end(), b.tokens.begin(), b.tokens.end());
+        lr.push_back(cfg.lr_at ? cfg.lr_at(cfg.first_step + h) : cfg.opt.lr);
+    }
+    spes_adamw_cfg opt{cfg.opt.lr, cfg.opt.beta1, cfg.opt.beta2, cfg.opt.eps,
+                       cfg.opt.weight_decay};
+    auto losses = ctx.local_round(tokens, B, S, cfg.steps, lr, opt, carry_state);
+    spes::LocalRoundResult res;
+    res.params = global;
+    unflatten(ctx.read(), res.params);
+    for (const auto& l : losses) res.step_losses.push_back({l.total, l.ce, l.lb, l.moe_z, l.z});
+    int64_t opt_state = 0, grads = 0, step = 0;
+    check(spes_counts(ctx.get(), &opt_state, &grads, &step));
+    res.grad_scalar_count = grads;
+    (void)mask;  // the context's ownership map defines the mask (Context::set_ownership)
+    return res;
+}
+
+// Drop-in for spes::merge_model (merging.hpp:138-150) on the context's model.
+inline std::vector<spes::MergeEvent> merge_model(Context& ctx, spes::ModelParams& params,
+                                                 const spes::MergeSchedule& sched, int round) {
+    spes_merge_sched s{sched.warmup_rounds, sched.interval, sched.alpha0, sched.peers,
+                       static_cast<int32_t>(sched.source)};
+    ctx.load(flatten(params));
+    const int L = params.config.layers, M = params.config.experts_total;
+    const int K = std::max(1, std::min(sched.peers, M - 1));
+    std::vector<spes_merge_event> ev(static_cast<size_t>(L));
+    std::vector<int32_t> peers(static_cast<size_t>(L) * M * K);
+    int32_t n = 0;
+    check(spes_merge(ctx.get(), &s, round, ev.data(), peers.data(), &n));
+    std::vector<spes::MergeEvent> out;
+    for (int l = 0; l < n; ++l) {
+        spes::MergeEvent e;
+        e.layer = ev[l].layer;
+        e.alpha = ev[l].alpha;
+        e.displacement_sq = ev[l].displacement_sq;
+        for (int j = 0; j < M; ++j)
+            e.peer_sets.emplace_back(peers.begin() + (static_cast<size_t>(l) * M + j) * K,
+                                     peers.begin() + (static_cast<size_t>(l) * M + j + 1) * K);
+        out.push_back(std::move(e));
+    }
+    if (n > 0) unflatten(ctx.read(), params);
+    return out;
+}
+
+}  // namespace spes_b200
+#endif
+#endif

@@ -129,7 +129,7 @@ struct LayerBufs {
     bf16 *xp, *gu, *hact;
     int64_t* grad_off;  // device [M]
     CUtensorMap a_xp, a_hact, a_xp_mn, a_hact_mn;  // *_mn: [tokens x features] as MN-major
-    CUtensorMap b_w1t, b_w2t, b_w2, b_w1;
+    CUtensorMap b_w1_mn, b_w2_mn, b_w2, b_w1;  // *_mn: row-major weights as MN-major B
 };
 
 }  // namespace
@@ -153,15 +153,12 @@ struct spes_ctx {
 
     DevMem persistent;  // params, shadows, optimizer state
     float* params = nullptr;
-    bf16 *w1t = nullptr, *w2t = nullptr, *w1 = nullptr, *w2 = nullptr, *headB = nullptr,
-         *headT = nullptr;
+    bf16 *w1 = nullptr, *w2 = nullptr, *headB = nullptr;  // bf16 GEMM operand copies
     float *grads = nullptr, *m = nullptr, *v = nullptr;
     spes_k::AdamSeg* segs = nullptr;
-    int64_t* all_expert_offs = nullptr;     // [L*M] param offsets
-    int64_t* all_shadow_slots = nullptr;    // [L*M] 0..L*M-1
-    int64_t* owned_expert_offs = nullptr;   // [L*|owned|]
-    int64_t* owned_shadow_slots = nullptr;  // [L*|owned|]
-    int n_owned_slots = 0;
+    spes_k::AdamSeg* all_segs = nullptr;  // head + every expert (shadow refresh)
+    int n_all_segs = 0;
+    int64_t all_segs_total = 0;
     int64_t* grad_off_dev = nullptr;  // [L*M]
     int64_t adam_step = 0;
 
@@ -185,7 +182,8 @@ struct spes_ctx {
     int head_max[3] = {0, 0, 0};
     int head_split = 1;
     float* head_dw_part = nullptr;
-    CUtensorMap a_dyw, a_dgu, b_dgu_mn, b_dyw_mn, a_hL, b_headT, a_dlog, b_headB, a_hL_mn, b_dlog_mn;
+    CUtensorMap a_dyw, a_dgu, b_dgu_mn, b_dyw_mn, a_hL, b_headB_mn, a_dlog, b_headB, a_hL_mn,
+        b_dlog_mn;
     int max_tiles[6] = {0, 0, 0, 0, 0, 0};
 
     // host staging
@@ -269,19 +267,20 @@ void build_ownership_tables(spes_ctx* c) {
     c->owners.assign(L.M, {});
     for (int n = 0; n < c->n_nodes; ++n)
         for (int e : c->node_experts[n]) c->owners[e].push_back(n);
-    // compact trainable layout: psi, then owned experts (layer-major, ascending)
+    // compact trainable layout: psi, then owned experts (layer-major, ascending). The
+    // segments also tell the optimizer which bf16 operand copy each element feeds
+    // (kind 2: head -> headB, kind 1: expert -> W1/W2 slot).
     c->grad_off_host.assign(static_cast<size_t>(L.L) * L.M, -1);
     c->segs_host.clear();
-    c->segs_host.push_back({0, 0, L.psi()});
+    c->segs_host.push_back({0, 0, L.V * L.d, 0, 0});                          // emb
+    c->segs_host.push_back({L.off_head(), L.off_head(), L.V * L.d, 2, 0});     // head
+    c->segs_host.push_back({2 * L.V * L.d, 2 * L.V * L.d, L.psi() - 2 * L.V * L.d, 0, 0});
     int64_t off = L.psi();
-    std::vector<int64_t> oo, os;
     for (int l = 0; l < L.L; ++l)
         for (int j = 0; j < L.M; ++j)
             if (c->owned[j]) {
                 c->grad_off_host[static_cast<size_t>(l) * L.M + j] = off;
-                c->segs_host.push_back({L.off_expert(l, j), off, L.per_expert()});
-                oo.push_back(L.off_expert(l, j));
-                os.push_back(static_cast<int64_t>(l) * L.M + j);
+                c->segs_host.push_back({L.off_expert(l, j), off, L.per_expert(), 1, l * L.M + j});
                 off += L.per_expert();
             }
     c->G = off;
@@ -291,14 +290,10 @@ void build_ownership_tables(spes_ctx* c) {
         cudaFree(c->m);
         cudaFree(c->v);
         cudaFree(c->segs);
-        cudaFree(c->owned_expert_offs);
-        cudaFree(c->owned_shadow_slots);
         auto& P = c->persistent.ptrs;
         P.erase(std::remove_if(P.begin(), P.end(),
                                [&](void* p) {
-                                   return p == c->grads || p == c->m || p == c->v ||
-                                          p == c->segs || p == c->owned_expert_offs ||
-                                          p == c->owned_shadow_slots;
+                                   return p == c->grads || p == c->m || p == c->v || p == c->segs;
                                }),
                 P.end());
     }
@@ -309,24 +304,20 @@ void build_ownership_tables(spes_ctx* c) {
     ck(cudaMemcpy(c->segs, c->segs_host.data(), sizeof(spes_k::AdamSeg) * c->segs_host.size(),
                   cudaMemcpyHostToDevice),
        "segs");
-    c->n_owned_slots = static_cast<int>(oo.size());
-    c->owned_expert_offs = c->persistent.alloc<int64_t>(static_cast<int64_t>(oo.size()));
-    c->owned_shadow_slots = c->persistent.alloc<int64_t>(static_cast<int64_t>(os.size()));
-    if (!oo.empty()) {
-        ck(cudaMemcpy(c->owned_expert_offs, oo.data(), 8 * oo.size(), cudaMemcpyHostToDevice), "oo");
-        ck(cudaMemcpy(c->owned_shadow_slots, os.data(), 8 * os.size(), cudaMemcpyHostToDevice), "os");
-    }
     ck(cudaMemcpy(c->grad_off_dev, c->grad_off_host.data(), 8 * c->grad_off_host.size(),
                   cudaMemcpyHostToDevice),
        "grad_off");
     c->adam_step = 0;
 }
 
+spes_k::Shadows shadows_of(const spes_ctx* c) {
+    return spes_k::Shadows{c->w1, c->w2, c->headB, c->lay.d, c->lay.f};
+}
+
+// Every bf16 operand copy from the fp32 parameters (after load / sync / merge).
 void refresh_shadows_all(spes_ctx* c) {
-    const Layout& L = c->lay;
-    spes_k::expert_shadows(c->params, c->all_expert_offs, L.L * L.M, c->all_shadow_slots, L.d, L.f,
-                           c->w1t, c->w2t, c->w1, c->w2, c->stream);
-    spes_k::head_shadows(c->params + L.off_head(), L.d, L.V, c->headB, c->headT, c->stream);
+    spes_k::refresh_shadows(c->params, c->all_segs, c->n_all_segs, c->all_segs_total,
+                            shadows_of(c), c->stream);
 }
 
 void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
@@ -382,8 +373,8 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
         Y.a_hact = make_tmap_bf16(Y.hact, R, f, 128);
         Y.a_xp_mn = make_tmap_bf16(Y.xp, R, d, 64);
         Y.a_hact_mn = make_tmap_bf16(Y.hact, R, f, 64);
-        Y.b_w1t = make_tmap_bf16(c->w1t + static_cast<int64_t>(l) * M * 2 * f * d, M * 2 * f, d, 256);
-        Y.b_w2t = make_tmap_bf16(c->w2t + static_cast<int64_t>(l) * M * d * f, M * d, f, bn_for(d));
+        Y.b_w1_mn = make_tmap_bf16(c->w1 + static_cast<int64_t>(l) * M * d * 2 * f, M * d, 2 * f, 64);
+        Y.b_w2_mn = make_tmap_bf16(c->w2 + static_cast<int64_t>(l) * M * f * d, M * f, d, 64);
         Y.b_w2 = make_tmap_bf16(c->w2 + static_cast<int64_t>(l) * M * f * d, M * f, d, bn_for(f));
         Y.b_w1 = make_tmap_bf16(c->w1 + static_cast<int64_t>(l) * M * d * 2 * f, M * d, 2 * f, bn_for(d));
     }
@@ -421,7 +412,7 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     c->b_dgu_mn = make_tmap_bf16(c->dgu, R, 2 * f, 64);
     c->b_dyw_mn = make_tmap_bf16(c->dyw, R, d, 64);
     c->a_hL = make_tmap_bf16(c->hL, Tp, d, 128);
-    c->b_headT = make_tmap_bf16(c->headT, V, d, bn_for(V));
+    c->b_headB_mn = make_tmap_bf16(c->headB, d, V, 64);
     c->a_dlog = make_tmap_bf16(c->dlog_bf, Tp, V, 128);
     c->b_headB = make_tmap_bf16(c->headB, d, V, bn_for(d));
     c->a_hL_mn = make_tmap_bf16(c->hL, Tp, d, 64);
@@ -443,6 +434,7 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     for (int sp = 0; sp < nsplit; ++sp) {
         GemmGroup& g = hg[2 + sp];
         g.k0 = static_cast<int32_t>(sp * (Tp / nsplit));
+        g.bk0 = g.k0;
         g.k_len = static_cast<int32_t>(Tp / nsplit);
         g.m_tiles = static_cast<int32_t>(d / 128);
         g.n_tiles = static_cast<int32_t>(V / bn_for(V));
@@ -531,12 +523,13 @@ void forward_backward(spes_ctx* c) {
         }
         {
             PROF("gemm_fwd_gate_up");
-            spes_k::gemm_swiglu(Y.a_xp, Y.b_w1t, Y.groups + 0 * M, M, Y.tiles + 0, c->max_tiles[0],
+            spes_k::gemm_swiglu(Y.a_xp, Y.b_w1_mn, Y.groups + 0 * M, M, Y.tiles + 0, c->max_tiles[0],
                                 Y.hact, f, st);
         }
         {
             PROF("gemm_fwd_down");
-            spes_k::gemm_store_f32(bn_for(d), false, Y.a_hact, Y.b_w2t, Y.groups + 1 * M, M, Y.tiles + 1,
+            spes_k::gemm_store_f32(bn_for(d), spes_k::GemmMajor::KMN, Y.a_hact, Y.b_w2_mn,
+                                   Y.groups + 1 * M, M, Y.tiles + 1,
                                    c->max_tiles[1], st);
         }
         {
@@ -548,7 +541,8 @@ void forward_backward(spes_ctx* c) {
     {
         PROF("head_fwd");
         spes_k::gather_rows_bf16(c->h[L.L], d, nullptr, nullptr, Tp, d, c->hL, nullptr, Tp, st);
-        spes_k::gemm_store_f32(bn_for(V), false, c->a_hL, c->b_headT, c->head_groups + 0, 1,
+        spes_k::gemm_store_f32(bn_for(V), spes_k::GemmMajor::KMN, c->a_hL, c->b_headB_mn,
+                               c->head_groups + 0, 1,
                                c->head_tiles + 0, c->head_max[0], st);
     }
     {
@@ -563,9 +557,11 @@ void forward_backward(spes_ctx* c) {
     {
         PROF("head_bwd");
         spes_k::gather_rows_bf16(c->dlogits, V, nullptr, nullptr, Tp, V, c->dlog_bf, nullptr, Tp, st);
-        spes_k::gemm_store_f32(bn_for(d), false, c->a_dlog, c->b_headB, c->head_groups + 1, 1,
+        spes_k::gemm_store_f32(bn_for(d), spes_k::GemmMajor::KK, c->a_dlog, c->b_headB,
+                               c->head_groups + 1, 1,
                                c->head_tiles + 1, c->head_max[1], st);
-        spes_k::gemm_store_f32(bn_for(V), true, c->a_hL_mn, c->b_dlog_mn, c->head_groups + 2,
+        spes_k::gemm_store_f32(bn_for(V), spes_k::GemmMajor::MNMN, c->a_hL_mn, c->b_dlog_mn,
+                               c->head_groups + 2,
                                c->head_split, c->head_tiles + 2, c->head_max[2], st);
         if (c->head_split > 1)
             spes_k::splitk_reduce(c->head_dw_part, c->head_split, d * V,
@@ -585,7 +581,8 @@ void forward_backward(spes_ctx* c) {
         }
         {
             PROF("gemm_bwd_dx");
-            spes_k::gemm_store_f32(bn_for(d), false, c->a_dgu, Y.b_w1, Y.groups + 3 * M, M, Y.tiles + 3,
+            spes_k::gemm_store_f32(bn_for(d), spes_k::GemmMajor::KK, c->a_dgu, Y.b_w1,
+                                   Y.groups + 3 * M, M, Y.tiles + 3,
                                    c->max_tiles[3], st);
         }
         if (c->max_tiles[4] > 0) {
@@ -596,7 +593,8 @@ void forward_backward(spes_ctx* c) {
             }
             {
                 PROF("gemm_bwd_dw_down");
-                spes_k::gemm_store_f32(bn_for(d), true, Y.a_hact_mn, c->b_dyw_mn, Y.groups + 5 * M, M,
+                spes_k::gemm_store_f32(bn_for(d), spes_k::GemmMajor::MNMN, Y.a_hact_mn,
+                                       c->b_dyw_mn, Y.groups + 5 * M, M,
                                        Y.tiles + 5, c->max_tiles[5], st);
             }
         }
@@ -634,14 +632,8 @@ void optimizer_step(spes_ctx* c, const spes_adamw_cfg* o) {
         spes_k::adamw(c->params, c->grads, c->m, c->v, c->segs,
                       static_cast<int>(c->segs_host.size()), c->G, static_cast<float>(o->lr), b1,
                       b2, omb1, omb2, static_cast<float>(o->eps),
-                      static_cast<float>(o->weight_decay), bc1, bc2, c->stream);
+                      static_cast<float>(o->weight_decay), bc1, bc2, shadows_of(c), c->stream);
     }
-    const Layout& L = c->lay;
-    PROF("bf16_shadows");
-    spes_k::expert_shadows(c->params, c->owned_expert_offs, c->n_owned_slots,
-                           c->owned_shadow_slots, L.d, L.f, c->w1t, c->w2t, c->w1, c->w2,
-                           c->stream);
-    spes_k::head_shadows(c->params + L.off_head(), L.d, L.V, c->headB, c->headT, c->stream);
 }
 
 void validate_tokens(const spes_ctx* c, const int32_t* tokens, int64_t n) {
@@ -799,23 +791,27 @@ spes_status spes_create(const spes_model_cfg* cfg, int32_t node, int32_t n_nodes
         DevMem& P = c->persistent;
         c->params = P.alloc<float>(L.total());
         const int64_t slots = static_cast<int64_t>(L.L) * L.M;
-        c->w1t = P.alloc<bf16>(slots * 2 * L.f * L.d);
-        c->w2t = P.alloc<bf16>(slots * L.d * L.f);
         c->w1 = P.alloc<bf16>(slots * L.d * 2 * L.f);
         c->w2 = P.alloc<bf16>(slots * L.f * L.d);
         c->headB = P.alloc<bf16>(L.d * L.V);
-        c->headT = P.alloc<bf16>(L.V * L.d);
         c->grad_off_dev = P.alloc<int64_t>(slots);
-        c->all_expert_offs = P.alloc<int64_t>(slots);
-        c->all_shadow_slots = P.alloc<int64_t>(slots);
-        std::vector<int64_t> eo(slots), es(slots);
-        for (int l = 0; l < L.L; ++l)
-            for (int j = 0; j < L.M; ++j) {
-                eo[static_cast<size_t>(l) * L.M + j] = L.off_expert(l, j);
-                es[static_cast<size_t>(l) * L.M + j] = static_cast<int64_t>(l) * L.M + j;
-            }
-        ck(cudaMemcpy(c->all_expert_offs, eo.data(), 8 * slots, cudaMemcpyHostToDevice), "eo");
-        ck(cudaMemcpy(c->all_shadow_slots, es.data(), 8 * slots, cudaMemcpyHostToDevice), "es");
+        {  // refresh table: head + every expert, indexed contiguously
+            std::vector<spes_k::AdamSeg> all;
+            int64_t off = 0;
+            all.push_back({L.off_head(), off, L.V * L.d, 2, 0});
+            off += L.V * L.d;
+            for (int l = 0; l < L.L; ++l)
+                for (int j = 0; j < L.M; ++j) {
+                    all.push_back({L.off_expert(l, j), off, L.per_expert(), 1, l * L.M + j});
+                    off += L.per_expert();
+                }
+            c->n_all_segs = static_cast<int>(all.size());
+            c->all_segs_total = off;
+            c->all_segs = P.alloc<spes_k::AdamSeg>(static_cast<int64_t>(all.size()));
+            ck(cudaMemcpy(c->all_segs, all.data(), sizeof(spes_k::AdamSeg) * all.size(),
+                          cudaMemcpyHostToDevice),
+               "all segs");
+        }
         ck(cudaMallocHost(&c->h_losses, sizeof(double) * 8), "pinned losses");
         // default ownership: param_partition (model.hpp:466-477) when N <= M, else all
         c->node_experts.assign(n_nodes, {});
@@ -1443,7 +1439,7 @@ spes_status spes_kernel_adamw(float* theta, const float* grad, float* m, float* 
         float* dgr = D.alloc<float>(n);
         float* dm = D.alloc<float>(n);
         float* dv = D.alloc<float>(n);
-        spes_k::AdamSeg seg{0, 0, n};
+        spes_k::AdamSeg seg{0, 0, n, 0, 0};
         auto* ds = D.alloc<spes_k::AdamSeg>(1);
         ck(cudaMemcpy(ds, &seg, sizeof(seg), cudaMemcpyHostToDevice), "H2D");
         ck(cudaMemcpy(dt, theta, 4 * n, cudaMemcpyHostToDevice), "H2D");
@@ -1456,7 +1452,7 @@ spes_status spes_kernel_adamw(float* theta, const float* grad, float* m, float* 
         volatile float one = 1.f;
         spes_k::adamw(dt, dgr, dm, dv, ds, 1, n, static_cast<float>(o->lr), b1, b2, one - b1,
                       one - b2, static_cast<float>(o->eps), static_cast<float>(o->weight_decay),
-                      bc1, bc2, 0);
+                      bc1, bc2, spes_k::Shadows{nullptr, nullptr, nullptr, 0, 0}, 0);
         ck(cudaDeviceSynchronize(), "adamw kernel");
         ck(cudaMemcpy(theta, dt, 4 * n, cudaMemcpyDeviceToHost), "D2H");
         ck(cudaMemcpy(m, dm, 4 * n, cudaMemcpyDeviceToHost), "D2H");

@@ -132,11 +132,11 @@ int num_sms() {
     return g_num_sms;
 }
 
-template <int BN, bool MN, class Epi>
+template <int BN, bool AMN, bool BMN, class Epi>
 static void launch(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
                    const int32_t* tiles, int max_tiles, const Epi& epi, cudaStream_t s) {
     if (max_tiles <= 0) return;
-    auto kern = grouped_gemm_kernel<BN, Epi, MN>;
+    auto kern = grouped_gemm_kernel<BN, Epi, AMN, BMN>;
     static bool configured = false;  // one per template instantiation
     if (!configured) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -153,39 +153,50 @@ void gemm_prepare(int device) {
     num_sms();
 }
 
+// expert forward gate||up: A = Xp (K-major), B = W1 [d x 2f] row-major (MN-major)
 void gemm_swiglu(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
                  const int32_t* tiles, int max_tiles, bf16* hact, int64_t f, cudaStream_t s) {
-    launch<256, false>(a, b, g, ng, tiles, max_tiles, EpiSwiGLU{hact, f}, s);
+    launch<256, false, true>(a, b, g, ng, tiles, max_tiles, EpiSwiGLU{hact, f}, s);
 }
 
-void gemm_store_f32(int bn, bool mn, const CUtensorMap& a, const CUtensorMap& b,
+template <int BN>
+static void store_f32(GemmMajor mj, const CUtensorMap& a, const CUtensorMap& b,
+                      const GemmGroup* g, int ng, const int32_t* tiles, int max_tiles,
+                      cudaStream_t s) {
+    switch (mj) {
+        case GemmMajor::KK:
+            launch<BN, false, false>(a, b, g, ng, tiles, max_tiles, EpiStoreF32<BN>{}, s);
+            break;
+        case GemmMajor::KMN:
+            launch<BN, false, true>(a, b, g, ng, tiles, max_tiles, EpiStoreF32<BN>{}, s);
+            break;
+        case GemmMajor::MNMN:
+            launch<BN, true, true>(a, b, g, ng, tiles, max_tiles, EpiStoreF32<BN>{}, s);
+            break;
+    }
+}
+
+void gemm_store_f32(int bn, GemmMajor mj, const CUtensorMap& a, const CUtensorMap& b,
                     const GemmGroup* g, int ng, const int32_t* tiles, int max_tiles,
                     cudaStream_t s) {
-    if (bn == 256) {
-        if (mn)
-            launch<256, true>(a, b, g, ng, tiles, max_tiles, EpiStoreF32<256>{}, s);
-        else
-            launch<256, false>(a, b, g, ng, tiles, max_tiles, EpiStoreF32<256>{}, s);
-    } else {
-        if (mn)
-            launch<128, true>(a, b, g, ng, tiles, max_tiles, EpiStoreF32<128>{}, s);
-        else
-            launch<128, false>(a, b, g, ng, tiles, max_tiles, EpiStoreF32<128>{}, s);
-    }
+    if (bn == 256)
+        store_f32<256>(mj, a, b, g, ng, tiles, max_tiles, s);
+    else
+        store_f32<128>(mj, a, b, g, ng, tiles, max_tiles, s);
 }
 
 void gemm_dswiglu(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
                   const int32_t* tiles, int max_tiles, const bf16* gu, int64_t f,
                   cudaStream_t s) {
     if (bn == 256)
-        launch<256, false>(a, b, g, ng, tiles, max_tiles, EpiDSwiGLU<256>{gu, f}, s);
+        launch<256, false, false>(a, b, g, ng, tiles, max_tiles, EpiDSwiGLU<256>{gu, f}, s);
     else
-        launch<128, false>(a, b, g, ng, tiles, max_tiles, EpiDSwiGLU<128>{gu, f}, s);
+        launch<128, false, false>(a, b, g, ng, tiles, max_tiles, EpiDSwiGLU<128>{gu, f}, s);
 }
 
 void gemm_grad_w1(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
                   const int32_t* tiles, int max_tiles, cudaStream_t s) {
-    launch<256, true>(a, b, g, ng, tiles, max_tiles, EpiGradW1{}, s);
+    launch<256, true, true>(a, b, g, ng, tiles, max_tiles, EpiGradW1{}, s);
 }
 
 }  // namespace spes_k

@@ -39,7 +39,7 @@ struct GemmGroup {
     int32_t m_tiles;     // tiles of 128 rows
     int32_t n_tiles;     // tiles of BN columns
     int32_t tile_start;  // exclusive prefix of m_tiles*n_tiles over groups
-    int32_t tag;         // epilogue-defined (expert id, ...)
+    int32_t bk0;         // K offset (elements) in B
     int64_t out_row0;    // epilogue-defined output row offset
     int64_t ldo;         // epilogue-defined leading dimension
     void* out0;          // epilogue-defined outputs
@@ -69,12 +69,13 @@ __device__ __forceinline__ int find_group(const GemmGroup* __restrict__ groups, 
 // r = row within the 128-row tile handled by this thread; taddr = TMEM address of
 // (lane r, column 0) of this tile's accumulator; empty => k_len == 0 (result is 0).
 //
-// MN == false: A [rows x K] and B [rows x K] row-major (K contiguous), tiles at
-//              (k0 + kb*64, a_row0 + mt*128) / (k0 + kb*64, b_row0 + nt*BN).
-// MN == true : A [K x Mtot] and B [K x Ntot] row-major (M / N contiguous), i.e. the
-//              weight-gradient form D = A^T B over K = tokens; a_row0 / b_row0 are
-//              column offsets and k0 the first K row; boxes of 64 x 64.
-template <int BN, class Epi, bool MN = false>
+// Operand majors (independent for A and B):
+//   K-major : X [rows x K] row-major (K contiguous); one box (k, row) of 64 x rows.
+//   MN-major: X [K x cols] row-major (M / N contiguous); row0 is a column offset and
+//             the K offset a row index; boxes of 64 x 64 (weight-gradient form
+//             D = A^T B over K = tokens, and row-major weights as B).
+// A's K offset is g.k0, B's is g.bk0.
+template <int BN, class Epi, bool A_MN = false, bool B_MN = false>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap mapA,
                         const __grid_constant__ CUtensorMap mapB,
@@ -133,17 +134,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     uint8_t* sa = smem + stage * C::STAGE_BYTES;
                     uint8_t* sb = sa + C::A_BYTES;
                     mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-                    const int kc = g.k0 + kb * GEMM_BK;
-                    if constexpr (!MN) {
-                        tma_load_2d(&mapA, &full[stage], sa, kc, arow);
-                        tma_load_2d(&mapB, &full[stage], sb, kc, brow);
+                    const int kca = g.k0 + kb * GEMM_BK;
+                    const int kcb = g.bk0 + kb * GEMM_BK;
+                    if constexpr (!A_MN) {
+                        tma_load_2d(&mapA, &full[stage], sa, kca, arow);
                     } else {
 #pragma unroll
                         for (int i = 0; i < GEMM_BM / 64; ++i)
-                            tma_load_2d(&mapA, &full[stage], sa + i * 8192, arow + 64 * i, kc);
+                            tma_load_2d(&mapA, &full[stage], sa + i * 8192, arow + 64 * i, kca);
+                    }
+                    if constexpr (!B_MN) {
+                        tma_load_2d(&mapB, &full[stage], sb, kcb, brow);
+                    } else {
 #pragma unroll
                         for (int i = 0; i < BN / 64; ++i)
-                            tma_load_2d(&mapB, &full[stage], sb + i * 8192, brow + 64 * i, kc);
+                            tma_load_2d(&mapB, &full[stage], sb + i * 8192, brow + 64 * i, kcb);
                     }
                     if (++stage == C::STAGES) {
                         stage = 0;
@@ -154,7 +159,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            constexpr uint32_t idesc = idesc_bf16_f32(GEMM_BM, BN, MN);
+            constexpr uint32_t idesc = idesc_bf16_f32(GEMM_BM, BN, A_MN, B_MN);
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
@@ -171,25 +176,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     tc_fence_after();
                     const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
                     const uint32_t sb = sa + C::A_BYTES;
-                    if constexpr (!MN) {
-                        const uint64_t adesc = desc_kmajor_sw128(sa);
-                        const uint64_t bdesc = desc_kmajor_sw128(sb);
+                    // K-major: advance 16 elements = 32 B inside the 128 B swizzle row;
+                    // MN-major: advance 16 K rows = 2 KiB (two 8-row swizzle atoms)
+                    const uint64_t adesc = A_MN ? desc_mnmajor_sw128(sa, 8192) : desc_kmajor_sw128(sa);
+                    const uint64_t bdesc = B_MN ? desc_mnmajor_sw128(sb, 8192) : desc_kmajor_sw128(sb);
+                    constexpr uint64_t astep = A_MN ? 128 : 2, bstep = B_MN ? 128 : 2;
 #pragma unroll
-                        for (int k = 0; k < GEMM_BK / 16; ++k) {
-                            // advance 16 elements = 32 B inside the 128 B swizzle row
-                            umma_bf16(dtmem, adesc + 2 * k, bdesc + 2 * k, idesc,
-                                      (kb | k) != 0 ? 1u : 0u);
-                        }
-                    } else {
-                        const uint64_t adesc = desc_mnmajor_sw128(sa, 8192);
-                        const uint64_t bdesc = desc_mnmajor_sw128(sb, 8192);
-#pragma unroll
-                        for (int k = 0; k < GEMM_BK / 16; ++k) {
-                            // advance 16 K rows = 2 KiB (two 8-row swizzle atoms)
-                            umma_bf16(dtmem, adesc + 128 * k, bdesc + 128 * k, idesc,
-                                      (kb | k) != 0 ? 1u : 0u);
-                        }
-                    }
+                    for (int k = 0; k < GEMM_BK / 16; ++k)
+                        umma_bf16(dtmem, adesc + astep * k, bdesc + bstep * k, idesc,
+                                  (kb | k) != 0 ? 1u : 0u);
                     umma_commit(&empty[stage]);
                     if (++stage == C::STAGES) {
                         stage = 0;

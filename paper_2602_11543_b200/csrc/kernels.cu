@@ -110,21 +110,23 @@ __global__ void route_scan_k(int32_t* __restrict__ chunk_counts, int nchunks, in
             const int64_t goff = gb.grad_off_layer ? gb.grad_off_layer[e] : -1;
             for (int g = 0; g < 6; ++g) {
                 GemmGroup G{};
-                G.tag = e;
+                G.bk0 = 0;
                 G.out_row0 = s_off[e];
                 G.a_row0 = s_off[e];
                 G.k0 = 0;
                 G.m_tiles = mt;
                 switch (g) {
-                    case 0:  // fwd gate||up: Xp[R x d] . W1t_e[2f x d]^T
-                        G.b_row0 = static_cast<int32_t>(e * 2 * f);
+                    case 0:  // fwd gate||up: Xp[R x d] . W1_e[d x 2f] (B MN-major, rows e*d..)
+                        G.b_row0 = 0;
+                        G.bk0 = static_cast<int32_t>(e * d);
                         G.n_tiles = static_cast<int32_t>(2 * f / 256);
                         G.k_len = static_cast<int32_t>(d);
                         G.out0 = gb.gu;
                         G.ldo = 2 * f;
                         break;
-                    case 1:  // fwd down: Hact[R x f] . W2t_e[d x f]^T
-                        G.b_row0 = static_cast<int32_t>(e * d);
+                    case 1:  // fwd down: Hact[R x f] . Wd_e[f x d] (B MN-major, rows e*f..)
+                        G.b_row0 = 0;
+                        G.bk0 = static_cast<int32_t>(e * f);
                         G.n_tiles = static_cast<int32_t>(d / gb.bn_fwd2);
                         G.k_len = static_cast<int32_t>(f);
                         G.out0 = gb.y;
@@ -148,6 +150,7 @@ __global__ void route_scan_k(int32_t* __restrict__ chunk_counts, int nchunks, in
                         G.a_row0 = 0;
                         G.b_row0 = 0;
                         G.k0 = s_off[e];
+                        G.bk0 = s_off[e];
                         G.k_len = s_off[e + 1] - s_off[e];
                         G.m_tiles = goff >= 0 ? static_cast<int32_t>(d / 128) : 0;
                         G.n_tiles = static_cast<int32_t>(2 * f / 256);
@@ -160,6 +163,7 @@ __global__ void route_scan_k(int32_t* __restrict__ chunk_counts, int nchunks, in
                         G.a_row0 = 0;
                         G.b_row0 = 0;
                         G.k0 = s_off[e];
+                        G.bk0 = s_off[e];
                         G.k_len = s_off[e + 1] - s_off[e];
                         G.m_tiles = goff >= 0 ? static_cast<int32_t>(f / 128) : 0;
                         G.n_tiles = static_cast<int32_t>(d / gb.bn_dw2);
@@ -674,29 +678,63 @@ void embed_grad(const int32_t* inputs, const float* gh0, int64_t T, int64_t d, i
     count_launch();
 }
 
-// ============================ AdamW ============================
-// MaskedAdamW::step element update (trainer.hpp:85-92), exact fp32 op order,
-// over the compact trainable segments (psi + owned experts).
+// ============================ AdamW (+ bf16 operand copies) ============================
+// MaskedAdamW::step element update (trainer.hpp:85-92), exact fp32 op order, over the
+// compact trainable segments (psi + owned experts). The updated values are also written
+// as the bf16 GEMM operand copies (W1 interleaved gate|up, W2 = Wd, headB), so no
+// separate shadow pass re-reads the parameters.
+__device__ __forceinline__ int find_seg(const AdamSeg* __restrict__ segs, int nseg, int64_t i) {
+    int lo = 0, hi = nseg - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (segs[mid].comp_off <= i) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// 4 consecutive parameters starting at offset o within segment sg -> bf16 copy
+__device__ __forceinline__ void write_shadow4(const AdamSeg& sg, int64_t o, const float4& v,
+                                              const Shadows& sh) {
+    if (sg.kind == 0) return;
+    bf16* dst;
+    if (sg.kind == 2) {
+        dst = sh.headB + o;
+    } else {
+        const int64_t df = sh.d * sh.f;
+        if (o < 2 * df) {  // wg / wu: [d x f] -> W1 [d x 2f] interleaved
+            const bool up = o >= df;
+            const int64_t oo = up ? o - df : o;
+            const int64_t q = oo / sh.f, x = oo % sh.f;
+            dst = sh.w1 + static_cast<int64_t>(sg.slot) * 2 * df + q * 2 * sh.f +
+                  (up ? il_up(x) : il_gate(x));
+        } else {  // wd: [f x d] -> W2 as is
+            dst = sh.w2 + static_cast<int64_t>(sg.slot) * df + (o - 2 * df);
+        }
+    }
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&a);
+    pk.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(dst) = pk;
+}
+
 __global__ void __launch_bounds__(256) adamw_k(float* __restrict__ params,
                                                const float* __restrict__ grads,
                                                float* __restrict__ m, float* __restrict__ v,
                                                const AdamSeg* __restrict__ segs, int nseg,
                                                int64_t total4, float lr, float b1, float b2,
                                                float omb1, float omb2, float eps, float wd,
-                                               float bc1, float bc2) {
+                                               float bc1, float bc2, Shadows sh) {
     for (int64_t i4 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i4 < total4;
          i4 += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t i = i4 * 4;
-        int lo = 0, hi = nseg - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (segs[mid].comp_off <= i) lo = mid; else hi = mid - 1;
-        }
-        const int64_t p = segs[lo].param_off + (i - segs[lo].comp_off);
+        const AdamSeg sg = segs[find_seg(segs, nseg, i)];
+        const int64_t o = i - sg.comp_off;
+        const int64_t p = sg.param_off + o;
         float4 th = *reinterpret_cast<float4*>(params + p);
-        const float4 g = *reinterpret_cast<const float4*>(grads + i);
-        float4 mm = *reinterpret_cast<float4*>(m + i);
-        float4 vv = *reinterpret_cast<float4*>(v + i);
+        const float4 g = __ldcs(reinterpret_cast<const float4*>(grads + i));
+        float4 mm = __ldcs(reinterpret_cast<const float4*>(m + i));
+        float4 vv = __ldcs(reinterpret_cast<const float4*>(v + i));
         float* thp = &th.x;
         const float* gp = &g.x;
         float* mp = &mm.x;
@@ -712,105 +750,40 @@ __global__ void __launch_bounds__(256) adamw_k(float* __restrict__ params,
             thp[u] = fsub(thp[u], upd);
         }
         *reinterpret_cast<float4*>(params + p) = th;
-        *reinterpret_cast<float4*>(m + i) = mm;
-        *reinterpret_cast<float4*>(v + i) = vv;
+        __stcs(reinterpret_cast<float4*>(m + i), mm);
+        __stcs(reinterpret_cast<float4*>(v + i), vv);
+        write_shadow4(sg, o, th, sh);
     }
 }
 
 void adamw(float* params, const float* grads, float* m, float* v, const AdamSeg* segs, int nseg,
            int64_t total, float lr, float b1, float b2, float omb1, float omb2, float eps,
-           float wd, float bc1, float bc2, cudaStream_t s) {
+           float wd, float bc1, float bc2, Shadows sh, cudaStream_t s) {
     const int64_t total4 = total / 4;
     const int blocks = static_cast<int>(std::min<int64_t>(cdiv(total4, 256), 148 * 8));
     adamw_k<<<blocks, 256, 0, s>>>(params, grads, m, v, segs, nseg, total4, lr, b1, b2, omb1,
-                                   omb2, eps, wd, bc1, bc2);
+                                   omb2, eps, wd, bc1, bc2, sh);
     count_launch();
 }
 
-// ============================ bf16 operand shadows ============================
-// mode 0: plain (dst col = c); mode 1: gate interleave; mode 2: up interleave.
-__device__ __forceinline__ int64_t map_col(int64_t c, int mode) {
-    return mode == 0 ? c : (mode == 1 ? il_gate(c) : il_up(c));
-}
-
-// src fp32 [R x C] -> dst bf16 [R x ldd] (cols mapped) and dstT bf16 [mapped C rows x R]
-__device__ void cvt_tile(const float* __restrict__ src, int64_t R, int64_t C, bf16* __restrict__ dst,
-                         int64_t ldd, bf16* __restrict__ dstT, int mode, int64_t tr, int64_t tc,
-                         float (*tile)[65]) {
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const int64_t r0 = tr * 64, c0 = tc * 64;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int rr = ty + 16 * i;
-        const float4 v = __ldg(reinterpret_cast<const float4*>(src + (r0 + rr) * C + c0 + 4 * tx));
-        tile[rr][4 * tx + 0] = v.x;
-        tile[rr][4 * tx + 1] = v.y;
-        tile[rr][4 * tx + 2] = v.z;
-        tile[rr][4 * tx + 3] = v.w;
-        __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
-        uint2 pk;
-        pk.x = *reinterpret_cast<uint32_t*>(&a);
-        pk.y = *reinterpret_cast<uint32_t*>(&b);
-        *reinterpret_cast<uint2*>(dst + (r0 + rr) * ldd + map_col(c0 + 4 * tx, mode)) = pk;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int cc = ty + 16 * i;
-        __nv_bfloat162 a = __floats2bfloat162_rn(tile[4 * tx + 0][cc], tile[4 * tx + 1][cc]);
-        __nv_bfloat162 b = __floats2bfloat162_rn(tile[4 * tx + 2][cc], tile[4 * tx + 3][cc]);
-        uint2 pk;
-        pk.x = *reinterpret_cast<uint32_t*>(&a);
-        pk.y = *reinterpret_cast<uint32_t*>(&b);
-        *reinterpret_cast<uint2*>(dstT + map_col(c0 + cc, mode) * R + r0 + 4 * tx) = pk;
-    }
-    __syncthreads();
-}
-
-// grid: x = tile index within the three matrices of one expert, y = expert in list
-__global__ void __launch_bounds__(256) expert_shadows_k(const float* __restrict__ params,
-                                                        const int64_t* __restrict__ expert_offs,
-                                                        const int64_t* __restrict__ shadow_offs,
-                                                        int64_t d, int64_t f, bf16* w1t, bf16* w2t,
-                                                        bf16* w1, bf16* w2) {
-    __shared__ float tile[64][65];
-    const int64_t po = expert_offs[blockIdx.y];
-    const int64_t so = shadow_offs[blockIdx.y];  // expert slot index (layer*M + j)
-    const int64_t tg = (d / 64) * (f / 64);       // tiles per d x f matrix
-    int64_t t = blockIdx.x;
-    if (t < 2 * tg) {  // wg (mode 1) or wu (mode 2): [d x f]
-        const int mode = t < tg ? 1 : 2;
-        if (t >= tg) t -= tg;
-        const float* src = params + po + (mode == 2 ? d * f : 0);
-        cvt_tile(src, d, f, w1 + so * d * 2 * f, 2 * f, w1t + so * 2 * f * d, mode, t / (f / 64),
-                 t % (f / 64), tile);
-    } else {  // wd: [f x d]
-        t -= 2 * tg;
-        const float* src = params + po + 2 * d * f;
-        cvt_tile(src, f, d, w2 + so * f * d, d, w2t + so * d * f, 0, t / (d / 64), t % (d / 64),
-                 tile);
+__global__ void __launch_bounds__(256) refresh_shadows_k(const float* __restrict__ params,
+                                                         const AdamSeg* __restrict__ segs,
+                                                         int nseg, int64_t total4, Shadows sh) {
+    for (int64_t i4 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i4 < total4;
+         i4 += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = i4 * 4;
+        const AdamSeg sg = segs[find_seg(segs, nseg, i)];
+        if (sg.kind == 0) continue;
+        const int64_t o = i - sg.comp_off;
+        write_shadow4(sg, o, __ldg(reinterpret_cast<const float4*>(params + sg.param_off + o)), sh);
     }
 }
 
-void expert_shadows(const float* params, const int64_t* expert_offs, int n_experts,
-                    const int64_t* shadow_offs, int64_t d, int64_t f, bf16* w1t, bf16* w2t,
-                    bf16* w1, bf16* w2, cudaStream_t s) {
-    if (n_experts == 0) return;
-    dim3 grid(static_cast<unsigned>(3 * (d / 64) * (f / 64)), static_cast<unsigned>(n_experts));
-    expert_shadows_k<<<grid, 256, 0, s>>>(params, expert_offs, shadow_offs, d, f, w1t, w2t, w1, w2);
-    count_launch();
-}
-
-__global__ void __launch_bounds__(256) head_shadows_k(const float* __restrict__ head, int64_t d,
-                                                      int64_t V, bf16* headB, bf16* headT) {
-    __shared__ float tile[64][65];
-    cvt_tile(head, d, V, headB, V, headT, 0, blockIdx.x / (V / 64), blockIdx.x % (V / 64), tile);
-}
-
-void head_shadows(const float* head, int64_t d, int64_t V, bf16* headB, bf16* headT,
-                  cudaStream_t s) {
-    head_shadows_k<<<static_cast<unsigned>((d / 64) * (V / 64)), 256, 0, s>>>(head, d, V, headB,
-                                                                             headT);
+void refresh_shadows(const float* params, const AdamSeg* segs, int nseg, int64_t total,
+                     Shadows sh, cudaStream_t s) {
+    const int64_t total4 = total / 4;
+    const int blocks = static_cast<int>(std::min<int64_t>(cdiv(total4, 256), 148 * 8));
+    refresh_shadows_k<<<blocks, 256, 0, s>>>(params, segs, nseg, total4, sh);
     count_launch();
 }
 

@@ -23,6 +23,8 @@ struct AdamSeg {
     int64_t param_off;  // offset in the fp32 parameter vector
     int64_t comp_off;   // offset in the compact (trainable-only) grad / m / v buffers
     int64_t len;
+    int32_t kind;       // bf16 operand copy to refresh: 0 none, 1 expert (wg|wu|wd), 2 head
+    int32_t slot;       // expert slot (layer*M + j) for kind 1
 };
 
 // ---- forward ----
@@ -95,15 +97,21 @@ void embed_grad(const int32_t* inputs, const float* gh0, int64_t T, int64_t d, i
                 float* g_emb, cudaStream_t s);
 
 // ---- optimizer / shadows ----
+// bf16 GEMM operand copies written by the optimizer / refresh: W1 [slots][d][2f]
+// (gate|up interleaved in 128-column blocks), W2 [slots][f][d] (= Wd), headB [d][V].
+struct Shadows {
+    bf16* w1;
+    bf16* w2;
+    bf16* headB;
+    int64_t d, f;
+};
+// MaskedAdamW step over the compact segments; also writes the refreshed bf16 copies.
 void adamw(float* params, const float* grads, float* m, float* v, const AdamSeg* segs, int nseg,
            int64_t total, float lr, float b1, float b2, float omb1, float omb2, float eps,
-           float wd, float bc1, float bc2, cudaStream_t s);
-// bf16 operand layouts of expert (l, j) = 4 GEMM-ready copies
-void expert_shadows(const float* params, const int64_t* expert_offs, int n_experts,
-                    const int64_t* shadow_offs, int64_t d, int64_t f, bf16* w1t, bf16* w2t,
-                    bf16* w1, bf16* w2, cudaStream_t s);
-void head_shadows(const float* head, int64_t d, int64_t V, bf16* headB, bf16* headT,
-                  cudaStream_t s);
+           float wd, float bc1, float bc2, Shadows sh, cudaStream_t s);
+// Rewrite every bf16 copy from the fp32 parameters (after load / sync / merge).
+void refresh_shadows(const float* params, const AdamSeg* segs, int nseg, int64_t total,
+                     Shadows sh, cudaStream_t s);
 
 // ---- sync / merge ----
 void owner_mean(const float* const* srcs, int n_src, int64_t n, float* out, cudaStream_t s);
@@ -119,8 +127,10 @@ void merge_apply(float* params, const int64_t* expert_offs, int M, int64_t per,
 // ---- GEMMs (gemm.cu) ----
 void gemm_swiglu(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
                  const int32_t* tiles, int max_tiles, bf16* hact, int64_t f, cudaStream_t s);
-// mn: operands are [K x M] / [K x N] row-major (weight-gradient form)
-void gemm_store_f32(int bn, bool mn, const CUtensorMap& a, const CUtensorMap& b,
+// operand majors: KK (both K contiguous), KMN (B = row-major weight [K x N]),
+// MNMN (weight-gradient form: A [K x M], B [K x N] row-major over K = tokens)
+enum class GemmMajor { KK, KMN, MNMN };
+void gemm_store_f32(int bn, GemmMajor mj, const CUtensorMap& a, const CUtensorMap& b,
                     const GemmGroup* g, int ng, const int32_t* tiles, int max_tiles,
                     cudaStream_t s);
 void gemm_dswiglu(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,

@@ -19,7 +19,7 @@ using namespace spes_dev;
     } while (0)
 
 __global__ void ref_gemm(const __nv_bfloat16* A, const __nv_bfloat16* B, const GemmGroup* groups,
-                         int ng, float* out, int BN) {
+                         int ng, float* out, int BN, int lda) {
     // one thread per output element of every group (slow; test sizes only)
     int g = blockIdx.y;
     if (g >= ng) return;
@@ -31,8 +31,8 @@ __global__ void ref_gemm(const __nv_bfloat16* A, const __nv_bfloat16* B, const G
         float s = 0.f;
         // lda/ldb passed through ldo==K convention below
         for (int k = 0; k < gg.k_len; ++k)
-            s += __bfloat162float(A[(int64_t)(gg.a_row0 + m) * gg.tag + gg.k0 + k]) *
-                 __bfloat162float(B[(int64_t)(gg.b_row0 + n) * gg.tag + gg.k0 + k]);
+            s += __bfloat162float(A[(int64_t)(gg.a_row0 + m) * lda + gg.k0 + k]) *
+                 __bfloat162float(B[(int64_t)(gg.b_row0 + n) * lda + gg.bk0 + k]);
         out[(gg.out_row0 + m) * gg.ldo + n] = s;
     }
 }
@@ -67,7 +67,7 @@ int run_case(const char* name, int K_total, int a_rows, int b_rows, std::vector<
         tiles += g.m_tiles * g.n_tiles;
         g.out0 = out;
         g.ldo = out_cols;
-        g.tag = K_total;
+        g.bk0 = g.k0;
     }
     GemmGroup* dg;
     CK(cudaMalloc(&dg, groups.size() * sizeof(GemmGroup)));
@@ -90,7 +90,7 @@ int run_case(const char* name, int K_total, int a_rows, int b_rows, std::vector<
     std::vector<GemmGroup> rg = groups;
     for (auto& g : rg) g.out0 = ref;
     CK(cudaMemcpy(dg, rg.data(), rg.size() * sizeof(GemmGroup), cudaMemcpyHostToDevice));
-    ref_gemm<<<dim3(256, groups.size()), 256>>>(A, B, dg, (int)groups.size(), ref, BN);
+    ref_gemm<<<dim3(256, groups.size()), 256>>>(A, B, dg, (int)groups.size(), ref, BN, K_total);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
 
@@ -179,6 +179,7 @@ int run_case_mn(const char* name, int K_total, int Mtot, int Ntot, std::vector<G
         tiles += g.m_tiles * g.n_tiles;
         g.out0 = out;
         g.ldo = out_cols;
+        g.bk0 = g.k0;
     }
     GemmGroup* dg;
     CK(cudaMalloc(&dg, groups.size() * sizeof(GemmGroup)));
@@ -188,7 +189,7 @@ int run_case_mn(const char* name, int K_total, int Mtot, int Ntot, std::vector<G
     CK(cudaMemcpy(dtiles, &tiles, 4, cudaMemcpyHostToDevice));
     CUtensorMap ma = spes_host::make_tmap_bf16(A, K_total, Mtot, 64);
     CUtensorMap mb = spes_host::make_tmap_bf16(B, K_total, Ntot, 64);
-    auto kern = grouped_gemm_kernel<BN, EpiStoreF32<BN>, true>;
+    auto kern = grouped_gemm_kernel<BN, EpiStoreF32<BN>, true, true>;
     int smem = GemmCfg<BN>::SMEM_BYTES;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int grid = tiles < 148 ? tiles : 148;
