@@ -100,6 +100,10 @@ spes_status spes_block_offsets(const spes_model_cfg* cfg, int64_t* offsets, int3
 /* param_partition (model.hpp:466-477): CSR node -> experts (node_offsets has N+1 entries). */
 spes_status spes_param_partition(const spes_model_cfg* cfg, int32_t n_nodes,
                                  int32_t* node_offsets, int32_t* experts);
+/* Sync plan of spes_sync for an ownership map: primary owner per expert (-1: unowned)
+ * and whether the primaries form contiguous balanced slices (in-place all-gather). */
+spes_status spes_sync_plan(int32_t experts_total, int32_t n_nodes, const int32_t* node_offsets,
+                           const int32_t* experts, int32_t* primary_out, int32_t* balanced_out);
 /* LrSchedule::at (proj/src/experiment.cpp:32-41). */
 double spes_lr_at(double peak, double min_frac, int64_t warmup_steps, int64_t total_steps,
                   int64_t step);

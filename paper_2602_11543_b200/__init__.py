@@ -59,6 +59,8 @@ def lib():
         L.spes_param_count.argtypes = [cfgp]
         L.spes_block_offsets.argtypes = [cfgp, C.POINTER(i64), C.POINTER(i32)]
         L.spes_param_partition.argtypes = [cfgp, i32, C.POINTER(i32), C.POINTER(i32)]
+        L.spes_sync_plan.argtypes = [i32, i32, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32),
+                                     C.POINTER(i32)]
         L.spes_lr_at.restype = C.c_double
         L.spes_lr_at.argtypes = [C.c_double, C.c_double, i64, i64, i64]
         L.spes_merge_at.restype = i32
@@ -148,6 +150,21 @@ def replicated_ownership(M, N, r=2):
     s = M // N
     E = min(M, r * M // N)
     return [sorted({(s * n + i) % M for i in range(E)}) for n in range(N)]
+
+
+def sync_plan(M, owned_lists):
+    """(primary owner per expert, balanced?) exactly as spes_sync uses them."""
+    N = len(owned_lists)
+    offs = np.zeros(N + 1, np.int32)
+    flat = []
+    for n, e in enumerate(owned_lists):
+        flat.extend(sorted(int(x) for x in e))
+        offs[n + 1] = len(flat)
+    arr = np.array(flat if flat else [0], np.int32)
+    prim = np.zeros(M, np.int32)
+    bal = C.c_int32()
+    _check(lib().spes_sync_plan(M, N, i32(offs), i32(arr), i32(prim), C.byref(bal)))
+    return prim, bool(bal.value)
 
 
 def nccl_unique_id():

@@ -215,6 +215,28 @@ namespace {
 
 void set_counter(spes_ctx* c) { spes_k::g_launch_counter = &c->launches; }
 
+// Sync plan: the primary owner of expert e computes its owner-set
+// mean and distributes it. Primary = e / (M/N) when N | M and that node owns e (the
+// contiguous balanced layout -> one in-place all-gather per layer), else the lowest
+// owner (-> grouped broadcasts). Experts without owners keep their global value.
+void sync_plan(int M, int N, const std::vector<std::vector<int>>& owners,
+               std::vector<int>& primary, bool& balanced) {
+    const int s_bal = (M % N == 0) ? M / N : 0;
+    primary.assign(M, -1);
+    balanced = s_bal > 0;
+    for (int e = 0; e < M; ++e) {
+        const auto& O = owners[e];
+        if (O.empty()) {
+            balanced = false;
+            continue;
+        }
+        int p = O.front();
+        if (s_bal && std::find(O.begin(), O.end(), e / s_bal) != O.end()) p = e / s_bal;
+        primary[e] = p;
+        if (!s_bal || p != e / s_bal) balanced = false;
+    }
+}
+
 // Brackets the launches of one kernel family with CUDA events when profiling is on.
 struct Prof {
     spes_ctx* c;
@@ -744,6 +766,25 @@ double spes_lr_at(double peak, double min_frac, int64_t warmup, int64_t total, i
     return lo + (peak - lo) * 0.5 * (1.0 + std::cos(M_PI * progress));
 }
 
+spes_status spes_sync_plan(int32_t experts_total, int32_t n_nodes, const int32_t* node_offsets,
+                           const int32_t* experts, int32_t* primary_out, int32_t* balanced_out) {
+    return guard([&] {
+        if (n_nodes < 1 || experts_total < 1) throw std::invalid_argument("sync_plan: bad sizes");
+        std::vector<std::vector<int>> owners(experts_total);
+        for (int n = 0; n < n_nodes; ++n)
+            for (int q = node_offsets[n]; q < node_offsets[n + 1]; ++q) {
+                if (experts[q] < 0 || experts[q] >= experts_total)
+                    throw std::invalid_argument("ownership: expert id out of range");
+                owners[experts[q]].push_back(n);
+            }
+        std::vector<int> primary;
+        bool balanced = false;
+        sync_plan(experts_total, n_nodes, owners, primary, balanced);
+        std::copy(primary.begin(), primary.end(), primary_out);
+        *balanced_out = balanced ? 1 : 0;
+    });
+}
+
 int32_t spes_merge_at(const spes_merge_sched* s, int32_t round) {
     return s->warmup_rounds > 0 && round < s->warmup_rounds && s->interval > 0 &&
            round % s->interval == 0;
@@ -992,20 +1033,10 @@ spes_status spes_sync(spes_ctx* c, spes_sync_stats* stats) {
             spes_k::owner_mean_strided(c->psi_stage, N, psi, psi, c->params, st);
             psi_in = 4.0 * psi * (N - 1);
             // experts: primary owner per expert
-            const int s_bal = (L.M % N == 0) ? L.M / N : 0;
-            std::vector<int> primary(L.M, -1);
-            bool balanced = s_bal > 0;
-            for (int e = 0; e < L.M; ++e) {
-                const auto& O = c->owners[e];
-                if (O.empty()) {
-                    balanced = false;
-                    continue;
-                }
-                int p = O.front();
-                if (s_bal && std::find(O.begin(), O.end(), e / s_bal) != O.end()) p = e / s_bal;
-                primary[e] = p;
-                if (!s_bal || p != e / s_bal) balanced = false;
-            }
+            std::vector<int> primary;
+            bool balanced = false;
+            sync_plan(L.M, N, c->owners, primary, balanced);
+            const int s_bal = balanced ? L.M / N : 0;
             const int64_t per = L.per_expert();
             // staging for co-owner copies received by this primary
             int64_t need = 0;

@@ -1,0 +1,81 @@
+"""Multi-GPU sparse sync over NCCL (one process per GPU, one SPES node each).
+
+Every rank trains its own shard for a short local round, then spes_sync runs the
+owner-set means over NCCL. The synced model must equal the oracle's
+Server::aggregate restatement on the gathered pre-sync node models bit-for-bit,
+on every rank; the merge warm-up afterwards must be identical on every rank and
+equal to the oracle's merge_model. Skipped when fewer GPUs are visible.
+"""
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+import oracle
+import paper_2602_11543_b200 as spes
+from paper_2602_11543_b200.abi import adamw_cfg, merge_sched, model_cfg
+
+pytestmark = pytest.mark.gpu
+
+CFG = dict(vocab=256, hidden=128, intermediate=256, layers=2, experts_total=8, experts_active=2)
+SCHED = dict(warmup_rounds=4, interval=1, alpha0=0.1, peers=3, source=0)
+
+
+def _n_gpus():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+def _rank(rank, world, nccl_id, owned, params, tokens, q):
+    try:
+        cfg = model_cfg(**CFG)
+        node = spes.Node(cfg, rank, world, rank, nccl_id)
+        node.set_ownership(owned)
+        node.load_params(params)
+        node.local_round(tokens[rank], adamw_cfg(lr=1e-3))
+        pre = node.read_params()
+        st = node.sync()
+        post = node.read_params()
+        ev, peers = node.merge_model(merge_sched(**SCHED), 0)
+        merged = node.read_params()
+        node.close()
+        q.put((rank, pre, post, merged, st, None))
+    except Exception as e:  # pragma: no cover - surfaced by the parent
+        q.put((rank, None, None, None, None, repr(e)))
+
+
+@pytest.mark.parametrize("world,layout", [(2, "replicated"), (2, "partition"), (4, "replicated"),
+                                          (4, "partition")])
+def test_nccl_sync_matches_oracle(world, layout):
+    if _n_gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cfg = model_cfg(**CFG)
+    M = cfg.experts_total
+    owned = (spes.replicated_ownership(M, world, 2) if layout == "replicated"
+             else spes.param_partition(cfg, world))
+    params = oracle.random_params(cfg, 5)
+    tokens = [oracle.random_tokens(cfg, 2, 64, 100 + r, H=2) for r in range(world)]
+    nccl_id = spes.nccl_unique_id()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank, args=(r, world, nccl_id, owned, params, tokens, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+    errs = [r[5] for r in res if r[5]]
+    assert not errs, errs
+    pre = np.stack([r[1] for r in res])
+    expect = oracle.aggregate(cfg, pre, owned, params)
+    for rank, _, post, merged, st, _ in res:
+        assert np.array_equal(post.view(np.uint32), expect.view(np.uint32)), f"rank {rank}"
+        assert st["psi_bytes_in"] > 0
+    merged0 = res[0][3]
+    for r in res[1:]:
+        assert np.array_equal(r[3].view(np.uint32), merged0.view(np.uint32))
+    m_ref, _, _ = oracle.merge_model(cfg, expect, merge_sched(**SCHED), 0)
+    assert np.array_equal(merged0.view(np.uint32), m_ref.view(np.uint32))
