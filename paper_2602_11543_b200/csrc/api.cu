@@ -409,7 +409,7 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     c->glog = A.alloc<float>(Tp * M);
     c->gnormed = A.alloc<float>(Tp * d);
     c->gh = A.alloc<float>(Tp * d);
-    c->nr_partial = A.alloc<float>(16 * d * (M + 1));
+    c->nr_partial = A.alloc<float>(64 * d * (M + 1));  // NRG_TC token chunks
     c->hL = A.alloc<bf16>(Tp * d);
     c->head_logits = A.alloc<float>(Tp * V);
     c->dlogits = A.alloc<float>(Tp * V);

@@ -531,62 +531,82 @@ void combine_backward(const float* gh, const float* y, const int32_t* row_token,
 // ============================ norm-gain and router weight gradients ============================
 // g_gain[q] = sum_t (gy*x)*inv ; g_router[q][e] = sum_t normed[t][q]*glog[t][e]
 // Fixed-order partials over TC token chunks, then a fixed-order sum.
-constexpr int NRG_TC = 16;
-template <int MAXM>
+// grid (d/128, NRG_TC, ceil(M/16)), 256 threads: warp ph takes tokens t = ph (mod 8) of
+// the chunk, lane tx the columns 4tx..4tx+3 of the 128-column slab (float4 streams);
+// each thread keeps 4 columns x 16 experts of router-gradient partials in registers.
+constexpr int NRG_TC = 64;
+constexpr int NRG_EG = 16;
 __global__ void __launch_bounds__(256) norm_router_partial_k(
     const float* __restrict__ h, const float* __restrict__ normed, const float* __restrict__ gnormed,
     const float* __restrict__ glog, const float* __restrict__ inv_rms, int T, int d, int M,
     float* __restrict__ partial) {
-    const int q = blockIdx.x * 32 + (threadIdx.x & 31);
-    const int ph = threadIdx.x >> 5;  // 8 phases
+    __shared__ __align__(16) float sgl[64][NRG_EG];
+    __shared__ float red[32][4][NRG_EG + 1];
+    const int ph = threadIdx.x >> 5, tx = threadIdx.x & 31;
+    const int q = blockIdx.x * 128 + 4 * tx;
     const int chunk = blockIdx.y;
+    const int e0 = blockIdx.z * NRG_EG;
+    const int ne = min(NRG_EG, M - e0);
+    const bool do_gain = blockIdx.z == 0;
     const int per = (T + NRG_TC - 1) / NRG_TC;
     const int t0 = chunk * per, t1 = min(T, t0 + per);
-    float gg = 0.f, gr[MAXM];
+    float gg[4] = {0.f, 0.f, 0.f, 0.f};
+    float gr[4][NRG_EG];
 #pragma unroll
-    for (int e = 0; e < MAXM; ++e) gr[e] = 0.f;
-    int t = t0 + ph;
-    for (; t + 24 < t1; t += 32) {  // four tokens in flight per thread
-        float gn[4], hv[4], iv[4], nv[4];
+    for (int j = 0; j < 4; ++j)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int64_t o = static_cast<int64_t>(t + 8 * u) * d + q;
-            gn[u] = __ldg(gnormed + o);
-            hv[u] = __ldg(h + o);
-            nv[u] = __ldg(normed + o);
-            iv[u] = __ldg(inv_rms + t + 8 * u);
+        for (int e = 0; e < NRG_EG; ++e) gr[j][e] = 0.f;
+    for (int tb = t0; tb < t1; tb += 64) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < 64 * NRG_EG; i += blockDim.x) {
+            const int tt = i / NRG_EG, e = i % NRG_EG;
+            sgl[tt][e] = (tb + tt < t1 && e < ne) ? glog[static_cast<int64_t>(tb + tt) * M + e0 + e] : 0.f;
         }
+        __syncthreads();
+        for (int tt = ph; tt < 64 && tb + tt < t1; tt += 8) {
+            const int64_t o = static_cast<int64_t>(tb + tt) * d + q;
+            const float4 nv = __ldg(reinterpret_cast<const float4*>(normed + o));
+            if (do_gain) {
+                const float4 gv = __ldg(reinterpret_cast<const float4*>(gnormed + o));
+                const float4 xv = __ldg(reinterpret_cast<const float4*>(h + o));
+                const float iv = __ldg(inv_rms + tb + tt);
+                gg[0] += (gv.x * xv.x) * iv;
+                gg[1] += (gv.y * xv.y) * iv;
+                gg[2] += (gv.z * xv.z) * iv;
+                gg[3] += (gv.w * xv.w) * iv;
+            }
+            const float n[4] = {nv.x, nv.y, nv.z, nv.w};
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            gg += (gn[u] * hv[u]) * iv[u];
-            const float* gl = glog + static_cast<int64_t>(t + 8 * u) * M;
+            for (int e4 = 0; e4 < NRG_EG; e4 += 4) {
+                const float4 g4 = *reinterpret_cast<const float4*>(&sgl[tt][e4]);
+                const float g[4] = {g4.x, g4.y, g4.z, g4.w};
 #pragma unroll
-            for (int e = 0; e < MAXM; ++e)
-                if (e < M) gr[e] += nv[u] * __ldg(gl + e);
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) gr[j][e4 + u] += n[j] * g[u];
+            }
         }
     }
-    for (; t < t1; t += 8) {
-        const int64_t o = static_cast<int64_t>(t) * d + q;
-        gg += (gnormed[o] * h[o]) * inv_rms[t];
-        const float nv = normed[o];
-        const float* gl = glog + static_cast<int64_t>(t) * M;
+    // combine the 8 warps in warp order (fixed), then write this chunk's partial
+    for (int w = 0; w < 8; ++w) {
+        __syncthreads();
+        if (ph == w) {
 #pragma unroll
-        for (int e = 0; e < MAXM; ++e)
-            if (e < M) gr[e] += nv * __ldg(gl + e);
+            for (int j = 0; j < 4; ++j) {
+                red[tx][j][0] = (w == 0 ? 0.f : red[tx][j][0]) + gg[j];
+#pragma unroll
+                for (int e = 0; e < NRG_EG; ++e)
+                    red[tx][j][1 + e] = (w == 0 ? 0.f : red[tx][j][1 + e]) + gr[j][e];
+            }
+        }
     }
-    extern __shared__ float sh[];  // [8][32][M+1]
-    float* mine = sh + (ph * 32 + (threadIdx.x & 31)) * (M + 1);
-    mine[0] = gg;
-#pragma unroll
-    for (int e = 0; e < MAXM; ++e)
-        if (e < M) mine[1 + e] = gr[e];
     __syncthreads();
     if (ph == 0) {
-        float* outp = partial + (static_cast<int64_t>(chunk) * d + q) * (M + 1);
-        for (int c = 0; c <= M; ++c) {
-            float s = 0.f;
-            for (int i = 0; i < 8; ++i) s += sh[(i * 32 + (threadIdx.x & 31)) * (M + 1) + c];
-            outp[c] = s;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            float* outp = partial + (static_cast<int64_t>(chunk) * d + q + j) * (M + 1);
+            if (do_gain) outp[0] = red[tx][j][0];
+            for (int e = 0; e < ne; ++e) outp[1 + e0 + e] = red[tx][j][1 + e];
         }
     }
 }
@@ -607,24 +627,9 @@ __global__ void norm_router_finish_k(const float* __restrict__ partial, int d, i
 void norm_router_grads(const float* h, const float* normed, const float* gnormed,
                        const float* glog, const float* inv_rms, int64_t T, int64_t d, int M,
                        float* partial, float* g_gain, float* g_router, cudaStream_t s) {
-    dim3 grid(static_cast<unsigned>(d / 32), NRG_TC);
-    const size_t smem = sizeof(float) * 8 * 32 * (M + 1);
-#define SPES_NR(MM)                                                                           \
-    do {                                                                                      \
-        cudaFuncSetAttribute(norm_router_partial_k<MM>,                                       \
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
-        norm_router_partial_k<MM><<<grid, 256, smem, s>>>(h, normed, gnormed, glog, inv_rms,  \
-                                                          (int)T, (int)d, M, partial);        \
-    } while (0)
-    if (M <= 8)
-        SPES_NR(8);
-    else if (M <= 16)
-        SPES_NR(16);
-    else if (M <= 32)
-        SPES_NR(32);
-    else
-        SPES_NR(64);
-#undef SPES_NR
+    dim3 grid(static_cast<unsigned>(d / 128), NRG_TC, static_cast<unsigned>((M + NRG_EG - 1) / NRG_EG));
+    norm_router_partial_k<<<grid, 256, 0, s>>>(h, normed, gnormed, glog, inv_rms, (int)T, (int)d, M,
+                                               partial);
     const int64_t n = d * (M + 1);
     norm_router_finish_k<<<static_cast<unsigned>(cdiv(n, 256)), 256, 0, s>>>(partial, (int)d, M,
                                                                             g_gain, g_router);

@@ -77,20 +77,20 @@ __global__ void __launch_bounds__(128) router_scalar_bwd_k(
 constexpr int NG_TT = 32;   // tokens per tile
 constexpr int NG_QT = 128;  // columns per tile
 
-// grid (T/32, d/128), 256 threads: thread (ty, tx) -> tokens 4ty..4ty+3, columns tx + 32j
+// grid (T/32, d/128), 256 threads: thread (ty, tx) -> tokens 4ty..4ty+3, columns 4tx..4tx+3
 template <int MAXM>
 __global__ void __launch_bounds__(256) normed_grad_k(
     const float* __restrict__ h, const float* __restrict__ gain, const float* __restrict__ R,
     const float* __restrict__ glog, const int32_t* __restrict__ slot_row,
     const float* __restrict__ dxp, int T, int d, int M, int k, float* __restrict__ gnormed,
     float* __restrict__ dot_part) {
-    __shared__ float sR[NG_QT * (MAXM + 1)];
+    __shared__ __align__(16) float sRT[MAXM][NG_QT];  // router tile, transposed: [e][q]
     __shared__ float sG[NG_TT][MAXM];
     __shared__ int32_t sRow[NG_TT][8];
     const int t0 = blockIdx.x * NG_TT, q0 = blockIdx.y * NG_QT;
     for (int i = threadIdx.x; i < NG_QT * M; i += blockDim.x) {
         const int qq = i / M, e = i % M;
-        sR[qq * (MAXM + 1) + e] = __ldg(R + static_cast<int64_t>(q0 + qq) * M + e);
+        sRT[e][qq] = __ldg(R + static_cast<int64_t>(q0 + qq) * M + e);
     }
     for (int i = threadIdx.x; i < NG_TT * M; i += blockDim.x) {
         const int tt = i / M, e = i % M;
@@ -109,21 +109,20 @@ __global__ void __launch_bounds__(256) normed_grad_k(
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) sr[i][j] = 0.f;
+    // this thread's columns: q0 + 4tx .. q0 + 4tx + 3 (float4 everywhere)
 #pragma unroll 4
     for (int e = 0; e < M; ++e) {
-        float g[4], r[4];
+        float g[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) g[i] = sG[ty * 4 + i][e];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) r[j] = sR[(tx + 32 * j) * (MAXM + 1) + e];
+        const float4 r4 = *reinterpret_cast<const float4*>(&sRT[e][4 * tx]);
+        const float r[4] = {r4.x, r4.y, r4.z, r4.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j) sr[i][j] = fadd(sr[i][j], fmul(g[i], r[j]));
     }
-    float gq[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) gq[j] = __ldg(gain + q0 + tx + 32 * j);
+    const float4 gq = __ldg(reinterpret_cast<const float4*>(gain + q0 + 4 * tx));
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int tt = ty * 4 + i;
@@ -134,20 +133,23 @@ __global__ void __launch_bounds__(256) normed_grad_k(
 #pragma unroll
         for (int s = 7; s >= 0; --s) {
             if (s < k) {
-                const float* src = dxp + static_cast<int64_t>(sRow[tt][s]) * d + q0 + tx;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) a[j] = fadd(a[j], __ldg(src + 32 * j));
+                const float4 v = __ldg(reinterpret_cast<const float4*>(
+                    dxp + static_cast<int64_t>(sRow[tt][s]) * d + q0 + 4 * tx));
+                a[0] = fadd(a[0], v.x);
+                a[1] = fadd(a[1], v.y);
+                a[2] = fadd(a[2], v.z);
+                a[3] = fadd(a[3], v.w);
             }
         }
-        const float* xr = h + static_cast<int64_t>(t) * d + q0 + tx;
-        float* gy = gnormed + static_cast<int64_t>(t) * d + q0 + tx;
-        float part = 0.f;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const float v = fadd(a[j], sr[i][j]);
-            gy[32 * j] = v;
-            part += (v * gq[j]) * __ldg(xr + 32 * j);
-        }
+        const float4 xv = __ldg(reinterpret_cast<const float4*>(h + static_cast<int64_t>(t) * d + q0 + 4 * tx));
+        float4 o;
+        o.x = fadd(a[0], sr[i][0]);
+        o.y = fadd(a[1], sr[i][1]);
+        o.z = fadd(a[2], sr[i][2]);
+        o.w = fadd(a[3], sr[i][3]);
+        *reinterpret_cast<float4*>(gnormed + static_cast<int64_t>(t) * d + q0 + 4 * tx) = o;
+        float part = (o.x * gq.x) * xv.x + (o.y * gq.y) * xv.y + (o.z * gq.z) * xv.z +
+                     (o.w * gq.w) * xv.w;
         part = warp_sum(part);
         if (tx == 0) dot_part[static_cast<int64_t>(t) * (d / NG_QT) + blockIdx.y] = part;
     }
