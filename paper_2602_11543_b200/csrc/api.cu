@@ -165,6 +165,8 @@ struct spes_ctx {
     // activations (sized for T_pad)
     DevMem act;
     int64_t T = 0, T_pad = 0, R_cap = 0, B = 0, S = 0;
+    bool use_pairs = false;  // cta_group::2 GEMMs (256-row tiles)
+    int tr = 128;            // GEMM tile rows == expert row padding
     std::vector<float*> h;  // L+1 buffers [T_pad x d]
     std::vector<LayerBufs> layers;
     int32_t *tokens = nullptr, *inputs = nullptr, *targets = nullptr, *err = nullptr;
@@ -351,8 +353,13 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     const Layout& L = c->lay;
     c->act.release();
     c->T = T;
-    c->T_pad = rup(T, 128);
-    c->R_cap = rup(T * L.k + static_cast<int64_t>(L.M) * 128, 128);
+    // cta_group::2 pair tiles (256 rows) whenever every GEMM M dimension allows it
+    c->use_pairs = (L.d % 256 == 0) && (L.f % 256 == 0);
+    c->tr = c->use_pairs ? 256 : 128;
+    const int64_t tr = c->tr;
+    const int bdiv = c->use_pairs ? 2 : 1;  // K-major B box rows per CTA = BN / bdiv
+    c->T_pad = rup(T, tr);
+    c->R_cap = rup(T * L.k + static_cast<int64_t>(L.M) * tr, tr);
     const int64_t Tp = c->T_pad, R = c->R_cap, d = L.d, f = L.f, V = L.V, M = L.M, k = L.k;
     DevMem& A = c->act;
     c->h.assign(L.L + 1, nullptr);
@@ -397,8 +404,10 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
         Y.a_hact_mn = make_tmap_bf16(Y.hact, R, f, 64);
         Y.b_w1_mn = make_tmap_bf16(c->w1 + static_cast<int64_t>(l) * M * d * 2 * f, M * d, 2 * f, 64);
         Y.b_w2_mn = make_tmap_bf16(c->w2 + static_cast<int64_t>(l) * M * f * d, M * f, d, 64);
-        Y.b_w2 = make_tmap_bf16(c->w2 + static_cast<int64_t>(l) * M * f * d, M * f, d, bn_for(f));
-        Y.b_w1 = make_tmap_bf16(c->w1 + static_cast<int64_t>(l) * M * d * 2 * f, M * d, 2 * f, bn_for(d));
+        Y.b_w2 = make_tmap_bf16(c->w2 + static_cast<int64_t>(l) * M * f * d, M * f, d,
+                                bn_for(f) / bdiv);
+        Y.b_w1 = make_tmap_bf16(c->w1 + static_cast<int64_t>(l) * M * d * 2 * f, M * d, 2 * f,
+                                bn_for(d) / bdiv);
     }
     c->dyw = A.alloc<bf16>(R * d);
     c->dgu = A.alloc<bf16>(R * 2 * f);
@@ -420,8 +429,8 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     // head dW = hL^T dlogits has only (d/128)*(V/BN) output tiles: split K (tokens)
     // so the grid covers the SMs; partials are summed in split order (deterministic).
     {
-        const int64_t tiles = (d / 128) * (V / bn_for(V));
-        int64_t ns = std::max<int64_t>(1, (2 * 148 + tiles - 1) / tiles);
+        const int64_t tiles = (d / tr) * (V / bn_for(V));
+        int64_t ns = std::max<int64_t>(1, (2 * 148 / bdiv + tiles - 1) / tiles);
         while (ns > 1 && (Tp % (64 * ns) != 0 || Tp / ns < 512)) --ns;
         c->head_split = static_cast<int>(ns);
     }
@@ -436,18 +445,18 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     c->a_hL = make_tmap_bf16(c->hL, Tp, d, 128);
     c->b_headB_mn = make_tmap_bf16(c->headB, d, V, 64);
     c->a_dlog = make_tmap_bf16(c->dlog_bf, Tp, V, 128);
-    c->b_headB = make_tmap_bf16(c->headB, d, V, bn_for(d));
+    c->b_headB = make_tmap_bf16(c->headB, d, V, bn_for(d) / bdiv);
     c->a_hL_mn = make_tmap_bf16(c->hL, Tp, d, 64);
     c->b_dlog_mn = make_tmap_bf16(c->dlog_bf, Tp, V, 64);
     // head GEMM groups (static for a given T_pad)
     std::vector<GemmGroup> hg(2 + c->head_split);
     hg[0].k_len = static_cast<int32_t>(d);
-    hg[0].m_tiles = static_cast<int32_t>(Tp / 128);
+    hg[0].m_tiles = static_cast<int32_t>(Tp / tr);
     hg[0].n_tiles = static_cast<int32_t>(V / bn_for(V));
     hg[0].out0 = c->head_logits;
     hg[0].ldo = V;
     hg[1].k_len = static_cast<int32_t>(V);
-    hg[1].m_tiles = static_cast<int32_t>(Tp / 128);
+    hg[1].m_tiles = static_cast<int32_t>(Tp / tr);
     hg[1].n_tiles = static_cast<int32_t>(d / bn_for(d));
     hg[1].out0 = c->gh;
     hg[1].ldo = d;
@@ -458,7 +467,7 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
         g.k0 = static_cast<int32_t>(sp * (Tp / nsplit));
         g.bk0 = g.k0;
         g.k_len = static_cast<int32_t>(Tp / nsplit);
-        g.m_tiles = static_cast<int32_t>(d / 128);
+        g.m_tiles = static_cast<int32_t>(d / tr);
         g.n_tiles = static_cast<int32_t>(V / bn_for(V));
         g.out0 = nsplit > 1 ? c->head_dw_part + sp * d * V
                        : c->grads + L.off_head();  // psi is first in the compact layout
@@ -477,14 +486,14 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
        "head groups");
     ck(cudaMemcpy(c->head_tiles, ht, sizeof(ht), cudaMemcpyHostToDevice), "head tiles");
     // upper bounds of routed GEMM tile counts
-    const int64_t mt_max = (T * k) / 128 + M;
+    const int64_t mt_max = (T * k) / tr + M;
     c->max_tiles[0] = static_cast<int>(mt_max * (2 * f / 256));
     c->max_tiles[1] = static_cast<int>(mt_max * (d / bn_for(d)));
     c->max_tiles[2] = static_cast<int>(mt_max * (f / bn_for(f)));
     c->max_tiles[3] = static_cast<int>(mt_max * (d / bn_for(d)));
     const int64_t no = static_cast<int64_t>(std::count(c->owned.begin(), c->owned.end(), 1));
-    c->max_tiles[4] = static_cast<int>(no * (d / 128) * (2 * f / 256));
-    c->max_tiles[5] = static_cast<int>(no * (f / 128) * (d / bn_for(d)));
+    c->max_tiles[4] = static_cast<int>(no * (d / tr) * (2 * f / 256));
+    c->max_tiles[5] = static_cast<int>(no * (f / tr) * (d / bn_for(d)));
 }
 
 // gradient seeds of the reverse tape (model.hpp:365-372): float arithmetic as the reference
@@ -516,6 +525,7 @@ void forward_backward(spes_ctx* c) {
     const int M = L.M, k = L.k;
     const Seeds sd = seeds_for(c);
     float* P = c->params;
+    spes_k::gemm_set_pair_mode(c->use_pairs);
 #define PROF(name) Prof _prof_##__LINE__(c, name)
     {
         PROF("embed_gather");
@@ -536,7 +546,7 @@ void forward_backward(spes_ctx* c) {
             spes_k::RoutePlan rp{Y.chunk_counts, Y.counts, Y.pad_off, Y.lb_coeff, Y.slot_row,
                                  Y.row_token, Y.row_w, Y.groups, Y.tiles};
             spes_k::GroupBases gb{Y.gu, Y.y, c->dgu, c->dxp, c->grads, Y.grad_off, d, f,
-                                  bn_for(d), bn_for(f), bn_for(d), bn_for(d)};
+                                  bn_for(d), bn_for(f), bn_for(d), bn_for(d), c->tr};
             spes_k::route_plan(Y.topk_idx, Y.topk_w, T, M, k, R, rp, gb, st);
         }
         {
@@ -1439,7 +1449,7 @@ spes_status spes_kernel_router(const spes_model_cfg* cfg, const float* h, const 
                              D.alloc<int32_t>(R), D.alloc<float>(R), D.alloc<GemmGroup>(6 * M),
                              D.alloc<int32_t>(6)};
         spes_k::GroupBases gb{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 128, 128,
-                              128, 128, 128, 128};
+                              128, 128, 128, 128, 128};
         spes_k::route_plan(di, dw, T, M, k, R, rp, gb, 0);
         ck(cudaDeviceSynchronize(), "router kernel");
         if (normed) ck(cudaMemcpy(normed, dn, 4 * T * d, cudaMemcpyDeviceToHost), "D2H");

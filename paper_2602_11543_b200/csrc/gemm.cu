@@ -12,6 +12,7 @@
 // operands (grouped_gemm_kernel<..., MN=true>): no transposed copies are made.
 #include "common.cuh"
 #include "grouped_gemm.cuh"
+#include "grouped_gemm_2cta.cuh"
 #include "kernels.h"
 
 namespace spes_k {
@@ -132,10 +133,40 @@ int num_sms() {
     return g_num_sms;
 }
 
+thread_local bool g_gemm_pairs = false;
+void gemm_set_pair_mode(bool on) { g_gemm_pairs = on; }
+
+// Pair mode: cta_group::2 kernel on cluster pairs (tiles of 256 rows); otherwise the
+// 1-CTA kernel (tiles of 128 rows). The group tables must match the mode.
 template <int BN, bool AMN, bool BMN, class Epi>
 static void launch(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
                    const int32_t* tiles, int max_tiles, const Epi& epi, cudaStream_t s) {
     if (max_tiles <= 0) return;
+    if (g_gemm_pairs) {
+        auto kern = grouped_gemm_2cta_kernel<BN, Epi, AMN, BMN>;
+        static bool configured2 = false;
+        if (!configured2) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Gemm2Cfg<BN>::SMEM_BYTES);
+            configured2 = true;
+        }
+        const int pairs = max_tiles < num_sms() / 2 ? max_tiles : num_sms() / 2;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(2 * pairs);
+        cfg.blockDim = dim3(GEMM_THREADS);
+        cfg.dynamicSmemBytes = Gemm2Cfg<BN>::SMEM_BYTES;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, kern, a, b, g, ng, tiles, max_tiles, epi);
+        count_launch();
+        return;
+    }
     auto kern = grouped_gemm_kernel<BN, Epi, AMN, BMN>;
     static bool configured = false;  // one per template instantiation
     if (!configured) {

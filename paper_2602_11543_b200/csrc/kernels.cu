@@ -96,7 +96,7 @@ __global__ void route_scan_k(int32_t* __restrict__ chunk_counts, int nchunks, in
         int32_t acc = 0;
         for (int e = 0; e < M; ++e) {
             s_off[e] = acc;
-            acc += (s_cnt[e] + 127) / 128 * 128;
+            acc += (s_cnt[e] + gb.tile_rows - 1) / gb.tile_rows * gb.tile_rows;
         }
         s_off[M] = acc;
         for (int e = 0; e <= M; ++e) pad_off[e] = s_off[e];
@@ -106,7 +106,7 @@ __global__ void route_scan_k(int32_t* __restrict__ chunk_counts, int nchunks, in
         const int64_t d = gb.d, f = gb.f;
         int32_t ts[6] = {0, 0, 0, 0, 0, 0};
         for (int e = 0; e < M; ++e) {
-            const int32_t mt = (s_off[e + 1] - s_off[e]) / 128;
+            const int32_t mt = (s_off[e + 1] - s_off[e]) / gb.tile_rows;
             const int64_t goff = gb.grad_off_layer ? gb.grad_off_layer[e] : -1;
             for (int g = 0; g < 6; ++g) {
                 GemmGroup G{};
@@ -152,7 +152,7 @@ __global__ void route_scan_k(int32_t* __restrict__ chunk_counts, int nchunks, in
                         G.k0 = s_off[e];
                         G.bk0 = s_off[e];
                         G.k_len = s_off[e + 1] - s_off[e];
-                        G.m_tiles = goff >= 0 ? static_cast<int32_t>(d / 128) : 0;
+                        G.m_tiles = goff >= 0 ? static_cast<int32_t>(d / gb.tile_rows) : 0;
                         G.n_tiles = static_cast<int32_t>(2 * f / 256);
                         G.out_row0 = 0;
                         G.out0 = goff >= 0 ? gb.grad_expert_base + goff : nullptr;
@@ -165,7 +165,7 @@ __global__ void route_scan_k(int32_t* __restrict__ chunk_counts, int nchunks, in
                         G.k0 = s_off[e];
                         G.bk0 = s_off[e];
                         G.k_len = s_off[e + 1] - s_off[e];
-                        G.m_tiles = goff >= 0 ? static_cast<int32_t>(f / 128) : 0;
+                        G.m_tiles = goff >= 0 ? static_cast<int32_t>(f / gb.tile_rows) : 0;
                         G.n_tiles = static_cast<int32_t>(d / gb.bn_dw2);
                         G.out_row0 = 0;
                         G.out0 = goff >= 0 ? gb.grad_expert_base + goff + 2 * d * f : nullptr;

@@ -58,6 +58,7 @@ struct GroupBases {  // output bases written into the group tables
     const int64_t* grad_off_layer; // [M]: offset of expert j of this layer in grads, -1 = frozen
     int64_t d, f;
     int bn_fwd2, bn_dh, bn_dx, bn_dw2;
+    int tile_rows;  // 128 (1-CTA tiles) or 256 (cta_group::2 pair tiles); also the row padding
 };
 void route_plan(const int32_t* topk_idx, const float* topk_w, int64_t T, int M, int k,
                 int64_t R_cap, const RoutePlan& p, const GroupBases& gb, cudaStream_t s);
@@ -139,6 +140,8 @@ void gemm_dswiglu(int bn, const CUtensorMap& a, const CUtensorMap& b, const Gemm
 void gemm_grad_w1(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
                   const int32_t* tiles, int max_tiles, cudaStream_t s);
 void gemm_prepare(int device);
+// cta_group::2 cluster-pair GEMMs (256-row tiles) for the following launches on this thread
+void gemm_set_pair_mode(bool on);
 int num_sms();
 
 // out[i] = sum over splits in order of part[s*n + i]   (deterministic split-K combine)
