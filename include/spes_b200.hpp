@@ -34,7 +34,7 @@ class Context {
 public:
     Context(const spes_model_cfg& cfg, int node, int n_nodes, int device,
             const void* nccl_id = nullptr)
-        : cfg_(cfg) {
+        : cfg_(cfg), node_(node), n_nodes_(n_nodes) {
         check(spes_create(&cfg_, node, n_nodes, device, nccl_id, &ctx_));
     }
     ~Context() { spes_destroy(ctx_); }
@@ -54,7 +54,12 @@ public:
         }
         if (ex.empty()) ex.push_back(0);
         check(spes_set_ownership(ctx_, offs.data(), ex.data()));
+        owned_ = owned;
     }
+    int node() const { return node_; }
+    int n_nodes() const { return n_nodes_; }
+    // empty until set_ownership
+    const std::vector<std::vector<int>>& ownership() const { return owned_; }
     void load(const std::vector<float>& flat) {
         check(spes_load_params(ctx_, flat.data(), static_cast<int64_t>(flat.size())));
     }
@@ -79,6 +84,8 @@ public:
 
 private:
     spes_model_cfg cfg_;
+    int node_ = 0, n_nodes_ = 1;
+    std::vector<std::vector<int>> owned_;
     spes_ctx* ctx_ = nullptr;
 };
 
@@ -135,6 +142,18 @@ inline spes::LocalRoundResult local_round(Context& ctx, const spes::ModelParams&
     if (cfg.steps < 1) throw std::invalid_argument("local_round: need H >= 1");
     if (cfg.inner != spes::InnerOpt::AdamW)
         throw std::logic_error("b200 local_round: only the AdamW inner optimizer is on the B200 path");
+    if (cfg.record_trace)
+        throw std::logic_error("b200 local_round: record_trace is not on the B200 path");
+    // The TrainMask must be this node's row of the context's ownership map (the map is
+    // global because the sparse sync needs every node's owner set). A single-node
+    // context adopts the mask as its map.
+    if (mask.node_id != ctx.node())
+        throw std::invalid_argument("b200 local_round: mask.node_id differs from the context's node");
+    if (ctx.n_nodes() == 1 && (ctx.ownership().empty() || ctx.ownership()[0] != mask.owned_experts))
+        ctx.set_ownership({mask.owned_experts});
+    else if (ctx.ownership().empty() ||
+             ctx.ownership()[static_cast<size_t>(ctx.node())] != mask.owned_experts)
+        throw std::invalid_argument("b200 local_round: mask differs from the context's ownership map");
     ctx.load(flatten(global));
     std::vector<int32_t> tokens;
     int64_t B = 0, S = 0;
@@ -156,7 +175,6 @@ inline spes::LocalRoundResult local_round(Context& ctx, const spes::ModelParams&
     int64_t opt_state = 0, grads = 0, step = 0;
     check(spes_counts(ctx.get(), &opt_state, &grads, &step));
     res.grad_scalar_count = grads;
-    (void)mask;  // the context's ownership map defines the mask (Context::set_ownership)
     return res;
 }
 

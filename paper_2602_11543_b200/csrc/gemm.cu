@@ -15,6 +15,8 @@
 #include "grouped_gemm_2cta.cuh"
 #include "kernels.h"
 
+#include <stdexcept>
+
 namespace spes_k {
 
 using namespace spes_dev;
@@ -142,6 +144,7 @@ template <int BN, bool AMN, bool BMN, class Epi>
 static void launch(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
                    const int32_t* tiles, int max_tiles, const Epi& epi, cudaStream_t s) {
     if (max_tiles <= 0) return;
+    if (ng > GEMM_MAX_GROUPS) throw std::invalid_argument("grouped GEMM: too many groups");
     if (g_gemm_pairs) {
         auto kern = grouped_gemm_2cta_kernel<BN, Epi, AMN, BMN>;
         static bool configured2 = false;

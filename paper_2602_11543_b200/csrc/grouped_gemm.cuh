@@ -31,6 +31,9 @@ constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;  // 64 bf16 = 128 B = one swizzle row
 constexpr int GEMM_THREADS = 384;  // 4 control warps + 8 epilogue warps
 
+constexpr int GEMM_MAX_GROUPS = 512;
+constexpr int GEMM_TABLE_BYTES = 8 * GEMM_MAX_GROUPS;
+
 struct GemmGroup {
     int32_t a_row0;      // first row of this group's A tile space
     int32_t b_row0;      // first row of this group's B tile space
@@ -53,14 +56,31 @@ struct GemmCfg {
     static constexpr int B_BYTES = BN * GEMM_BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int TMEM_COLS = 2 * BN;  // two accumulator buffers
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int SMEM_BYTES =
+        STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + GEMM_TABLE_BYTES;
 };
 
-__device__ __forceinline__ int find_group(const GemmGroup* __restrict__ groups, int num_groups,
-                                          int tile) {
-    int g = 0;
-    while (g + 1 < num_groups && groups[g + 1].tile_start <= tile) ++g;
-    return g;
+// Per-CTA copy of the group table's tile_start / k-block counts in shared memory: the
+// tile -> group lookup is a binary search over smem instead of a chain of dependent
+// global loads in the single MMA-issuing thread (which starved the tensor pipe).
+__device__ __forceinline__ void load_group_table(const GemmGroup* __restrict__ groups, int n,
+                                                 int* ts, int* nkb) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        ts[i] = groups[i].tile_start;
+        nkb[i] = groups[i].k_len / GEMM_BK;
+    }
+}
+// largest g with ts[g] <= tile (zero-tile groups share their successor's tile_start)
+__device__ __forceinline__ int find_group(const int* ts, int n, int tile) {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (ts[mid] <= tile)
+            lo = mid;
+        else
+            hi = mid - 1;
+    }
+    return lo;
 }
 
 // Epi must provide:
@@ -91,10 +111,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint64_t* tfull = bars + 2 * C::STAGES;
     uint64_t* tempty = bars + 2 * C::STAGES + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
+    int* s_ts = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(bars) + 256);
+    int* s_nkb = s_ts + GEMM_MAX_GROUPS;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
 
+    load_group_table(groups, num_groups, s_ts, s_nkb);
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&mapA);
         tma_prefetch_desc(&mapB);
@@ -122,7 +145,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
-                const int gi = find_group(groups, num_groups, t);
+                const int gi = find_group(s_ts, num_groups, t);
                 const GemmGroup& g = groups[gi];
                 const int local = t - g.tile_start;
                 const int mt = local / g.n_tiles, nt = local % g.n_tiles;
@@ -164,8 +187,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             uint32_t phase = 0;
             int it = 0;
             for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
-                const int gi = find_group(groups, num_groups, t);
-                const int nkb = groups[gi].k_len / GEMM_BK;
+                const int gi = find_group(s_ts, num_groups, t);
+                const int nkb = s_nkb[gi];
                 const int acc = it & 1;
                 const uint32_t acc_phase = (it >> 1) & 1;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -203,7 +226,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int r = q * 32 + lane;
         int it = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
-            const int gi = find_group(groups, num_groups, t);
+            const int gi = find_group(s_ts, num_groups, t);
             const GemmGroup& g = groups[gi];
             const int local = t - g.tile_start;
             const int mt = local / g.n_tiles, nt = local % g.n_tiles;

@@ -24,7 +24,7 @@ struct Gemm2Cfg {
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int STAGES = (192 * 1024) / STAGE_BYTES;
     static constexpr int TMEM_COLS = 2 * BN;
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + GEMM_TABLE_BYTES;
 };
 
 template <int BN, class Epi, bool A_MN = false, bool B_MN = false, int DBG_NO_TMA = 0>
@@ -43,6 +43,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint64_t* tfull = bars + 2 * C::STAGES;
     uint64_t* tempty = bars + 2 * C::STAGES + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
+    int* s_ts = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(bars) + 256);
+    int* s_nkb = s_ts + GEMM_MAX_GROUPS;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -51,6 +53,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int pair = blockIdx.x >> 1;
     const int npairs = gridDim.x >> 1;
 
+    load_group_table(groups, num_groups, s_ts, s_nkb);
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&mapA);
         tma_prefetch_desc(&mapB);
@@ -79,7 +82,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int t = pair; t < total; t += npairs) {
-                const int gi = find_group(groups, num_groups, t);
+                const int gi = find_group(s_ts, num_groups, t);
                 const GemmGroup& g = groups[gi];
                 const int local = t - g.tile_start;
                 const int mt = local / g.n_tiles, nt = local % g.n_tiles;
@@ -133,8 +136,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             uint32_t phase = 0;
             int it = 0;
             for (int t = pair; t < total; t += npairs, ++it) {
-                const int gi = find_group(groups, num_groups, t);
-                const int nkb = groups[gi].k_len / GEMM_BK;
+                const int gi = find_group(s_ts, num_groups, t);
+                const int nkb = s_nkb[gi];
                 const int acc = it & 1;
                 const uint32_t acc_phase = (it >> 1) & 1;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -174,7 +177,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int r = q * 32 + lane;
         int it = 0;
         for (int t = pair; t < total; t += npairs, ++it) {
-            const int gi = find_group(groups, num_groups, t);
+            const int gi = find_group(s_ts, num_groups, t);
             const GemmGroup& g = groups[gi];
             const int local = t - g.tile_start;
             const int mt = local / g.n_tiles, nt = local % g.n_tiles;
@@ -186,7 +189,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             epi(g, 2 * mt + static_cast<int>(rank), nt, r, taddr, g.k_len == 0, half);
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+            // relaxed remote arrive: only the (already waited) TMEM reads need ordering
+            if (lane == 0) mbar_arrive_remote(mapa_shared(smem_u32(&tempty[acc]), 0));
         }
     }
 

@@ -269,7 +269,6 @@ int main() {
         for (int j = 0; j < 16; ++j) gs.push_back(G(j * 2048, 0, 0, j * 1024, 1024, 8, 8, j * 2048));
         probe<256, false, true, EpiNull>("fwd1_nullepi", 16 * 2048, 1024, 16 * 1024, 2048, gs, 74);
         probe<256, false, true, EpiNull>("fwd1_nullepi_p37", 16 * 2048, 1024, 16 * 1024, 2048, gs, 37);
-        probe<256, false, true, EpiStoreF32<256>>("fwd1_store_p37", 16 * 2048, 1024, 16 * 1024, 2048, gs, 37);
     }
     printf(fails ? "SELFTEST2 FAILED\n" : "SELFTEST2 OK\n");
     return fails;
