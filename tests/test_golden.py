@@ -73,8 +73,13 @@ def test_oracle_local_round_aggregate_merge_match_golden(name):
     assert sha(pm) == m["params_sha"]
 
 
+# the B200 path tiles d, f and V by 128 (spes_validate_cfg); the tiny cases pin the oracle
+GPU_CASES = [n for n in CASES if all(GOLDEN["cases"][n]["shape"][k] % 128 == 0
+                                     for k in ("vocab", "hidden", "intermediate"))]
+
+
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("name", GPU_CASES)
 def test_b200_matches_golden(name):
     """Layer-0 routing of the first step and merge_model on the reference's trained
     parameters are bit-exact against the reference; step losses within tolerance."""
