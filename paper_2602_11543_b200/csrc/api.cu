@@ -123,7 +123,7 @@ struct DevMem {
 };
 
 struct LayerBufs {
-    float *normed, *logits, *probs, *topk_w, *lse_r, *inv_rms, *denom, *y, *row_w, *lb_coeff;
+    float *logits, *probs, *topk_w, *lse_r, *inv_rms, *denom, *y, *row_w, *lb_coeff;
     int32_t *topk_idx, *chunk_counts, *counts, *pad_off, *slot_row, *row_token, *tiles;
     GemmGroup* groups;
     bf16 *xp, *gu, *hact;
@@ -173,6 +173,7 @@ struct spes_ctx {
     bf16 *dyw = nullptr, *dgu = nullptr;
     float *dot_part = nullptr;
     double* loss_part = nullptr;
+    bf16* normed_bf = nullptr;  // router-normalized h of the current layer (expert GEMM input)
     float *dxp = nullptr, *gw_part = nullptr, *glog = nullptr, *gnormed = nullptr, *gh = nullptr,
           *nr_partial = nullptr;
     bf16 *hL = nullptr, *dlog_bf = nullptr;
@@ -375,7 +376,6 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     c->coeff_all = A.alloc<float>(L.L * M);
     for (int l = 0; l < L.L; ++l) {
         LayerBufs& Y = c->layers[l];
-        Y.normed = A.alloc<float>(Tp * d);
         Y.logits = A.alloc<float>(Tp * M);
         Y.probs = c->probs_all + l * Tp * M;
         Y.topk_w = A.alloc<float>(Tp * k);
@@ -417,6 +417,7 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     c->loss_part = A.alloc<double>((Tp / 256 + 1) * (2 + 2 * L.L));
     c->glog = A.alloc<float>(Tp * M);
     c->gnormed = A.alloc<float>(Tp * d);
+    c->normed_bf = A.alloc<bf16>(Tp * d);
     c->gh = A.alloc<float>(Tp * d);
     c->nr_partial = A.alloc<float>(64 * d * (M + 1));  // NRG_TC token chunks
     c->hL = A.alloc<bf16>(Tp * d);
@@ -538,8 +539,8 @@ void forward_backward(spes_ctx* c) {
             PROF("router_fwd");
             spes_k::router_forward(c->h[l], P + L.off_norm(l), P + L.off_router(l), T, d, M, k,
                                    c->cfg.renormalize_after_topk, c->cfg.rms_eps, c->expf_variant,
-                                   Y.normed, Y.logits, Y.probs, Y.topk_idx, Y.topk_w, Y.lse_r,
-                                   Y.inv_rms, Y.denom, st);
+                                   nullptr, c->normed_bf, Y.logits, Y.probs, Y.topk_idx,
+                                   Y.topk_w, Y.lse_r, Y.inv_rms, Y.denom, st);
         }
         {
             PROF("route_plan");
@@ -551,7 +552,7 @@ void forward_backward(spes_ctx* c) {
         }
         {
             PROF("permute");
-            spes_k::gather_rows_bf16(Y.normed, d, Y.row_token, Y.pad_off + M, R, d, Y.xp, nullptr, R, st);
+            spes_k::permute_rows_bf16(c->normed_bf, d, Y.row_token, Y.pad_off + M, R, Y.xp, st);
         }
         {
             PROF("gemm_fwd_gate_up");
@@ -640,7 +641,7 @@ void forward_backward(spes_ctx* c) {
         }
         {
             PROF("norm_router_grads");
-            spes_k::norm_router_grads(c->h[l], Y.normed, c->gnormed, c->glog, Y.inv_rms, T, d, M,
+            spes_k::norm_router_grads(c->h[l], P + L.off_norm(l), c->gnormed, c->glog, Y.inv_rms, T, d, M,
                                       c->nr_partial, c->grads + L.off_norm(l),
                                       c->grads + L.off_router(l), st);
         }
@@ -1322,8 +1323,9 @@ spes_status spes_debug_read(spes_ctx* c, const char* name, int32_t layer, void* 
             src = c->h[layer];
             sz = 4 * T * d;
         } else if (n == "normed") {
-            src = lay().normed;
-            sz = 4 * T * d;
+            throw std::invalid_argument(
+                "debug_read: normed is not stored on the training path (recomputed in "
+                "backward); spes_kernel_router returns it");
         } else if (n == "logits") {
             src = lay().logits;
             sz = 4 * T * M;
@@ -1440,7 +1442,7 @@ spes_status spes_kernel_router(const spes_model_cfg* cfg, const float* h, const 
         ck(cudaMemcpy(dr, router, 4 * d * M, cudaMemcpyHostToDevice), "H2D");
         const int variant = spes_expf::host_variant_from(&expf);
         spes_k::router_forward(dh, dg, dr, T, d, M, k, cfg->renormalize_after_topk, cfg->rms_eps,
-                               variant, dn, dl, dp, di, dw, dlse, dinv, dden, 0);
+                               variant, dn, nullptr, dl, dp, di, dw, dlse, dinv, dden, 0);
         // routing plan for counts / permutation
         const int64_t R = rup(T * k + static_cast<int64_t>(M) * 128, 128);
         const int64_t nchunks = (T + 255) / 256;

@@ -303,6 +303,35 @@ void gather_rows_bf16(const float* src, int64_t ld_src, const int32_t* row_map,
     count_launch();
 }
 
+// ============================ permute (bf16 rows) ============================
+// One warp per destination row, 16-byte vectors; padding rows (row_map < 0) are zeroed.
+__global__ void __launch_bounds__(256) permute_rows_bf16_k(const bf16* __restrict__ src,
+                                                           int64_t cols,
+                                                           const int32_t* __restrict__ row_map,
+                                                           const int32_t* __restrict__ nrows_dev,
+                                                           bf16* __restrict__ dst) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    if (r >= *nrows_dev) return;
+    const int lane = threadIdx.x & 31;
+    const int32_t sr = row_map[r];
+    const int64_t n16 = cols / 8;
+    uint4* d4 = reinterpret_cast<uint4*>(dst + r * cols);
+    if (sr < 0) {
+        for (int64_t i = lane; i < n16; i += 32) d4[i] = make_uint4(0, 0, 0, 0);
+        return;
+    }
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + static_cast<int64_t>(sr) * cols);
+#pragma unroll 4
+    for (int64_t i = lane; i < n16; i += 32) d4[i] = __ldg(s4 + i);
+}
+
+void permute_rows_bf16(const bf16* src, int64_t cols, const int32_t* row_map,
+                       const int32_t* nrows_dev, int64_t rows_cap, bf16* dst, cudaStream_t s) {
+    permute_rows_bf16_k<<<static_cast<unsigned>(cdiv(rows_cap, 8)), 256, 0, s>>>(
+        src, cols, row_map, nrows_dev, dst);
+    count_launch();
+}
+
 // ============================ combine (forward) ============================
 // h_next[t] = h[t] + sum over selected experts in ascending order of (0 + w*y)
 // (model.hpp:330-338: rowwise_mul, scatter_rows into zeros, add chain, residual add)
@@ -537,7 +566,7 @@ void combine_backward(const float* gh, const float* y, const int32_t* row_token,
 constexpr int NRG_TC = 64;
 constexpr int NRG_EG = 16;
 __global__ void __launch_bounds__(256) norm_router_partial_k(
-    const float* __restrict__ h, const float* __restrict__ normed, const float* __restrict__ gnormed,
+    const float* __restrict__ h, const float* __restrict__ gain, const float* __restrict__ gnormed,
     const float* __restrict__ glog, const float* __restrict__ inv_rms, int T, int d, int M,
     float* __restrict__ partial) {
     __shared__ __align__(16) float sgl[64][NRG_EG];
@@ -556,6 +585,7 @@ __global__ void __launch_bounds__(256) norm_router_partial_k(
     for (int j = 0; j < 4; ++j)
 #pragma unroll
         for (int e = 0; e < NRG_EG; ++e) gr[j][e] = 0.f;
+    const float4 gq = __ldg(reinterpret_cast<const float4*>(gain + q));
     for (int tb = t0; tb < t1; tb += 64) {
         __syncthreads();
         for (int i = threadIdx.x; i < 64 * NRG_EG; i += blockDim.x) {
@@ -565,11 +595,16 @@ __global__ void __launch_bounds__(256) norm_router_partial_k(
         __syncthreads();
         for (int tt = ph; tt < 64 && tb + tt < t1; tt += 8) {
             const int64_t o = static_cast<int64_t>(tb + tt) * d + q;
-            const float4 nv = __ldg(reinterpret_cast<const float4*>(normed + o));
+            const float4 xv = __ldg(reinterpret_cast<const float4*>(h + o));
+            const float iv = __ldg(inv_rms + tb + tt);
+            // normed exactly as the forward formed it: (x * inv) * g
+            float4 nv;
+            nv.x = fmul(fmul(xv.x, iv), gq.x);
+            nv.y = fmul(fmul(xv.y, iv), gq.y);
+            nv.z = fmul(fmul(xv.z, iv), gq.z);
+            nv.w = fmul(fmul(xv.w, iv), gq.w);
             if (do_gain) {
                 const float4 gv = __ldg(reinterpret_cast<const float4*>(gnormed + o));
-                const float4 xv = __ldg(reinterpret_cast<const float4*>(h + o));
-                const float iv = __ldg(inv_rms + tb + tt);
                 gg[0] += (gv.x * xv.x) * iv;
                 gg[1] += (gv.y * xv.y) * iv;
                 gg[2] += (gv.z * xv.z) * iv;
@@ -624,11 +659,11 @@ __global__ void norm_router_finish_k(const float* __restrict__ partial, int d, i
         g_router[static_cast<int64_t>(q) * M + (c - 1)] = s;
 }
 
-void norm_router_grads(const float* h, const float* normed, const float* gnormed,
+void norm_router_grads(const float* h, const float* gain, const float* gnormed,
                        const float* glog, const float* inv_rms, int64_t T, int64_t d, int M,
                        float* partial, float* g_gain, float* g_router, cudaStream_t s) {
     dim3 grid(static_cast<unsigned>(d / 128), NRG_TC, static_cast<unsigned>((M + NRG_EG - 1) / NRG_EG));
-    norm_router_partial_k<<<grid, 256, 0, s>>>(h, normed, gnormed, glog, inv_rms, (int)T, (int)d, M,
+    norm_router_partial_k<<<grid, 256, 0, s>>>(h, gain, gnormed, glog, inv_rms, (int)T, (int)d, M,
                                                partial);
     const int64_t n = d * (M + 1);
     norm_router_finish_k<<<static_cast<unsigned>(cdiv(n, 256)), 256, 0, s>>>(partial, (int)d, M,

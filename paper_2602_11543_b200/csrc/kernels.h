@@ -31,10 +31,11 @@ struct AdamSeg {
 void embed_gather(const float* emb, const int32_t* tokens, int64_t B, int64_t S, int64_t d,
                   int64_t V, float* h, int32_t* inputs, int32_t* targets, int32_t* err,
                   cudaStream_t s);
+// normed (fp32) and normed_bf (bf16, the expert GEMM operand) are each optional.
 void router_forward(const float* h, const float* gain, const float* router, int64_t T, int64_t d,
                     int M, int k, int renorm, float eps, int expf_variant, float* normed,
-                    float* logits, float* probs, int32_t* topk_idx, float* topk_w, float* lse,
-                    float* inv_rms, float* denom, cudaStream_t s);
+                    bf16* normed_bf, float* logits, float* probs, int32_t* topk_idx,
+                    float* topk_w, float* lse, float* inv_rms, float* denom, cudaStream_t s);
 // Deterministic counting sort of the (token, slot) pairs, expert-major and
 // token-ascending (model.hpp:314-318), each expert padded to 128 rows; also
 // builds the GEMM group tables of this layer on the device.
@@ -67,6 +68,10 @@ void route_plan(const int32_t* topk_idx, const float* topk_w, int64_t T, int M, 
 void gather_rows_bf16(const float* src, int64_t ld_src, const int32_t* row_map,
                       const int32_t* nrows_dev, int64_t rows, int64_t cols, bf16* dst,
                       bf16* dstT, int64_t rows_cap, cudaStream_t s);
+// dst[r] = src[row_map[r]] (bf16 rows of `cols`), zero rows where row_map[r] < 0;
+// rows processed: *nrows_dev.
+void permute_rows_bf16(const bf16* src, int64_t cols, const int32_t* row_map,
+                       const int32_t* nrows_dev, int64_t rows_cap, bf16* dst, cudaStream_t s);
 void combine_forward(const float* h, const float* y, const int32_t* slot_row,
                      const int32_t* topk_idx, const float* topk_w, int64_t T, int64_t d, int k,
                      float* h_next, cudaStream_t s);
@@ -91,7 +96,8 @@ void router_backward(const float* h, const float* gain, const float* router, con
                      const float* dxp, const float* lb_coeff, int64_t T, int64_t d, int M, int k,
                      int renorm, float g_lbsum, float g_s, float* glog, float* gnormed,
                      float* dot_part, float* gh, cudaStream_t s);
-void norm_router_grads(const float* h, const float* normed, const float* gnormed,
+// normed is recomputed exactly from h, inv_rms and the gain (not stored in forward)
+void norm_router_grads(const float* h, const float* gain, const float* gnormed,
                        const float* glog, const float* inv_rms, int64_t T, int64_t d, int M,
                        float* partial, float* g_gain, float* g_router, cudaStream_t s);
 void embed_grad(const int32_t* inputs, const float* gh0, int64_t T, int64_t d, int64_t V,

@@ -4,12 +4,14 @@
 //   softmax_rows (kernels.hpp:156-172) with the glibc-compatible expf; logsumexp (:174-185)
 //   route_from_logits (model.hpp:185-216): stable top-k, ascending indices, weights
 //
-// Block = NT tokens x (MAXM/4) expert quads = 256 threads. Token rows stream through
-// shared memory in 64-column chunks twice: pass 1 accumulates the sequential sum of
-// squares (one thread per token), pass 2 forms normed = (x*inv)*g and advances every
-// logit chain over the chunk. Each thread owns one token x four experts, so one
-// broadcast load of normed and one 16-byte load of router weights feed four
-// independent exact-order chains.
+// Layout: a token's (padded) experts are split over LPT lanes, 8 experts per lane
+// (lane = token * LPT + part). A warp stages its TPW = 32/LPT token rows
+// through a per-warp cp.async ring (64-column chunks, padded pitch => conflict-free
+// LDS.128), the block stages the matching router rows and gain chunk, so every lane runs
+// its token's sequential sum-of-squares chain and then 8 independent exact-order logit
+// chains fed by broadcast LDS.128 of router rows. Softmax / top-k run on the token's
+// first lane over the logits gathered in smem. normed is emitted as bf16 (the expert
+// GEMM operand, permuted by route_plan) and, for the kernel-level API only, as fp32.
 #include "common.cuh"
 #include "glibc_expf.h"
 #include "kernels.h"
@@ -18,188 +20,277 @@ namespace spes_k {
 
 using namespace spes_dev;
 
-constexpr int RF_QC = 64;  // columns per chunk
+constexpr int RF_WARPS = 4;  // warps per block (march through p together)
+constexpr int RF_RCH = 64;   // router rows per smem chunk
+constexpr int RF_XS = 3;     // ring depth (chunks of RF_RCH columns of x and rows of R)
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+
+__device__ __forceinline__ uint2 pack_bf16x4(float a, float b, float c, float d) {
+    __nv_bfloat162 x = __floats2bfloat162_rn(a, b);
+    __nv_bfloat162 y = __floats2bfloat162_rn(c, d);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&x);
+    u.y = *reinterpret_cast<uint32_t*>(&y);
+    return u;
+}
 
 template <int MAXM>
-__global__ void __launch_bounds__(256) router_fwd_k(
+struct RfSmem {
+    static constexpr int EPL = MAXM < 8 ? MAXM : 8;  // experts per lane
+    static constexpr int LPT = MAXM / EPL;           // lanes per token
+    static constexpr int TPW = 32 / LPT;             // tokens per warp
+    static constexpr int PITCH = RF_RCH + 4;  // padded row pitch (floats): conflict-free LDS.128
+    static constexpr int R_FLOATS = RF_XS * RF_RCH * MAXM;   // router row ring
+    static constexpr int G_FLOATS = RF_XS * RF_RCH;          // gain ring
+    static constexpr int X_FLOATS = RF_WARPS * RF_XS * TPW * PITCH;  // per-warp token-row rings
+    static constexpr int BYTES = 4 * (R_FLOATS + G_FLOATS + X_FLOATS);
+};
+
+template <int MAXM>
+__global__ void __launch_bounds__(32 * RF_WARPS) router_fwd_k(
     const float* __restrict__ h, const float* __restrict__ gain, const float* __restrict__ R,
     int T, int d, int M, int k, int renorm, float eps, int variant, float* __restrict__ normed,
-    float* __restrict__ logits, float* __restrict__ probs, int32_t* __restrict__ topk_idx,
-    float* __restrict__ topk_w, float* __restrict__ lse_out, float* __restrict__ inv_out,
-    float* __restrict__ denom_out) {
-    constexpr int EG = MAXM / 4;      // expert quads
-    constexpr int NT = 256 / EG;      // tokens per block
-    __shared__ float sx[NT][RF_QC + 1];
-    __shared__ __align__(16) float sR[RF_QC][MAXM];
-    __shared__ float sv[NT][MAXM + 1];
-    __shared__ float sinv[NT], smx[NT];
-    const int t0 = blockIdx.x * NT;
-    const int nt = min(NT, T - t0);
-    const int tq = threadIdx.x / EG, eg = threadIdx.x % EG;
+    bf16* __restrict__ normed_bf, float* __restrict__ logits, float* __restrict__ probs,
+    int32_t* __restrict__ topk_idx, float* __restrict__ topk_w, float* __restrict__ lse_out,
+    float* __restrict__ inv_out, float* __restrict__ denom_out) {
+    using SM = RfSmem<MAXM>;
+    constexpr int EPL = SM::EPL, LPT = SM::LPT, TPW = SM::TPW;
+    constexpr int QC = RF_RCH / 4;  // float4 per row chunk
+    constexpr int PITCH = SM::PITCH;
+    extern __shared__ __align__(16) float rf_smem[];
+    float(*sR)[RF_RCH][MAXM] = reinterpret_cast<float(*)[RF_RCH][MAXM]>(rf_smem);  // [RF_XS]
+    float(*sG)[RF_RCH] = reinterpret_cast<float(*)[RF_RCH]>(rf_smem + SM::R_FLOATS);
+    float(*sxw)[TPW][PITCH] = reinterpret_cast<float(*)[TPW][PITCH]>(
+        rf_smem + SM::R_FLOATS + SM::G_FLOATS);  // [warp * RF_XS + slot]
+    __shared__ float sv_all[RF_WARPS][TPW][MAXM + 1];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float(*sv)[MAXM + 1] = sv_all[warp];
+    const int tok = lane / LPT, part = lane % LPT, e0 = part * EPL;
+    const int tw0 = (blockIdx.x * RF_WARPS + warp) * TPW;  // first token of this warp
+    const int t = tw0 + tok;
+    const bool valid = t < T;
+    const int nrc = d / RF_RCH;  // row chunks (= router / gain chunks)
 
-    auto load_chunk = [&](int q0) {
-        for (int i = threadIdx.x; i < NT * (RF_QC / 4); i += blockDim.x) {
-            const int tt = i / (RF_QC / 4), c = (i % (RF_QC / 4)) * 4;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (tt < nt) v = __ldg(reinterpret_cast<const float4*>(h + static_cast<int64_t>(t0 + tt) * d + q0 + c));
-            sx[tt][c] = v.x;
-            sx[tt][c + 1] = v.y;
-            sx[tt][c + 2] = v.z;
-            sx[tt][c + 3] = v.w;
+    // chunk c of the warp's TPW rows (RF_RCH floats each) -> ring slot c % RF_XS;
+    // 16 lanes per row => 256-byte contiguous cp.async runs; rows past T are clamped.
+    auto issue_x = [&](int c) {
+        float(*dst)[PITCH] = sxw[warp * RF_XS + c % RF_XS];
+#pragma unroll 4
+        for (int i = lane; i < TPW * QC; i += 32) {
+            const int row = i / QC, q = i % QC;
+            const int tr = min(tw0 + row, T - 1);
+            cp_async16(&dst[row][4 * q], h + static_cast<int64_t>(tr) * d + c * RF_RCH + 4 * q);
         }
     };
+    // router rows [c*RF_RCH, +RF_RCH) -> sR[c % RF_XS] and gain -> sG (block-cooperative);
+    // experts M..MAXM-1 are zero columns
+    auto issue_rg = [&](int c) {
+        float* dst = &sR[c % RF_XS][0][0];
+        const float* src = R + static_cast<int64_t>(c) * RF_RCH * M;
+        if ((M & 3) == 0 && M == MAXM) {
+            for (int i = threadIdx.x; i < RF_RCH * MAXM / 4; i += blockDim.x)
+                cp_async16(dst + 4 * i, src + 4 * i);
+        } else {
+            for (int i = threadIdx.x; i < RF_RCH * MAXM; i += blockDim.x) {
+                const int rr = i / MAXM, e = i % MAXM;
+                dst[i] = e < M ? __ldg(src + static_cast<int64_t>(rr) * M + e) : 0.f;
+            }
+        }
+        if (threadIdx.x < QC)
+            cp_async16(&sG[c % RF_XS][4 * threadIdx.x], gain + c * RF_RCH + 4 * threadIdx.x);
+    };
+    auto wait_oldest = [&]() {  // group of the oldest in-flight chunk complete
+        asm volatile("cp.async.wait_group %0;" ::"n"(RF_XS - 2) : "memory");
+    };
 
-    // pass 1: sum of squares, sequential per token
+    // ---- pass 1: rmsnorm_forward sum of squares, sequential over p (kernels.hpp:117-128);
+    // the LPT lanes of a token run the same chain
     float ms = 0.f;
-    for (int q0 = 0; q0 < d; q0 += RF_QC) {
-        __syncthreads();
-        load_chunk(q0);
-        __syncthreads();
-        if (threadIdx.x < nt) {
-            const float* xr = sx[threadIdx.x];
-#pragma unroll 16
-            for (int c = 0; c < RF_QC; ++c) ms = fadd(ms, fmul(xr[c], xr[c]));
+#pragma unroll
+    for (int c = 0; c < RF_XS - 1; ++c) {
+        if (c < nrc) issue_x(c);
+        cp_async_commit();
+    }
+    for (int c = 0; c < nrc; ++c) {
+        wait_oldest();
+        __syncwarp();  // every lane's copies of chunk c visible; slot (c-1) % XS free
+        if (c + RF_XS - 1 < nrc) issue_x(c + RF_XS - 1);
+        cp_async_commit();
+        const float* xrow = sxw[warp * RF_XS + c % RF_XS][tok];
+#pragma unroll
+        for (int i = 0; i < QC; ++i) {
+            const float4 x = *reinterpret_cast<const float4*>(xrow + 4 * i);
+            ms = fadd(ms, fmul(x.x, x.x));
+            ms = fadd(ms, fmul(x.y, x.y));
+            ms = fadd(ms, fmul(x.z, x.z));
+            ms = fadd(ms, fmul(x.w, x.w));
         }
     }
-    if (threadIdx.x < nt) {
-        const float inv = fdiv(1.f, fsqrt(fadd(fdiv(ms, static_cast<float>(d)), eps)));
-        sinv[threadIdx.x] = inv;
-        inv_out[t0 + threadIdx.x] = inv;
-    }
+    const float inv = fdiv(1.f, fsqrt(fadd(fdiv(ms, static_cast<float>(d)), eps)));
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();  // all warps done with pass 1 before the rings are reused
 
-    // pass 2: normed chunk + logits
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    const bool active = tq < nt;
-    for (int q0 = 0; q0 < d; q0 += RF_QC) {
-        __syncthreads();
-        load_chunk(q0);
-        for (int i = threadIdx.x; i < RF_QC * MAXM; i += blockDim.x) {
-            const int c = i / MAXM, e = i % MAXM;
-            sR[c][e] = e < M ? __ldg(R + static_cast<int64_t>(q0 + c) * M + e) : 0.f;
-        }
-        __syncthreads();
-        for (int i = threadIdx.x; i < nt * RF_QC; i += blockDim.x) {
-            const int tt = i / RF_QC, c = i % RF_QC;
-            const float nv = fmul(fmul(sx[tt][c], sinv[tt]), __ldg(gain + q0 + c));
-            sx[tt][c] = nv;
-            normed[static_cast<int64_t>(t0 + tt) * d + q0 + c] = nv;
-        }
-        __syncthreads();
-        if (active) {
-            const float* xr = sx[tq];
-#pragma unroll 8
-            for (int c = 0; c < RF_QC; ++c) {
-                const float nv = xr[c];
-                const float4 r = *reinterpret_cast<const float4*>(&sR[c][4 * eg]);
-                acc[0] = fadd(acc[0], fmul(nv, r.x));
-                acc[1] = fadd(acc[1], fmul(nv, r.y));
-                acc[2] = fadd(acc[2], fmul(nv, r.z));
-                acc[3] = fadd(acc[3], fmul(nv, r.w));
-            }
-        }
-    }
-    if (active) {
+    // ---- pass 2: normed = (x * inv) * g; logit_e = sum_p normed_p * R[p][e], p ascending,
+    // no FMA; this lane owns experts [e0, e0 + EPL). Each cp.async group carries {x chunk c
+    // of this warp, this thread's share of R / gain chunk c}; the block barrier after the
+    // wait makes chunk c visible to all and guarantees slot (c-1) % XS is no longer read.
+    float acc[EPL];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int e = 4 * eg + u;
-            if (e < M) {
-                sv[tq][e] = acc[u];
-                logits[static_cast<int64_t>(t0 + tq) * M + e] = acc[u];
-            }
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x < nt) {  // std::max scan (kernels.hpp:160)
-        const float* lr = sv[threadIdx.x];
-        float mx = lr[0];
-        for (int j = 1; j < M; ++j) mx = (mx < lr[j]) ? lr[j] : mx;
-        smx[threadIdx.x] = mx;
-    }
-    __syncthreads();
-    if (active) {
+    for (int e = 0; e < EPL; ++e) acc[e] = 0.f;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int e = 4 * eg + u;
-            if (e < M) {
-                const float z = fsub(acc[u], smx[tq]);
-                sv[tq][e] = variant ? spes_expf::expf_glibc<1>(z) : spes_expf::expf_glibc<0>(z);
-            }
+    for (int c = 0; c < RF_XS - 1; ++c) {
+        if (c < nrc) {
+            issue_x(c);
+            issue_rg(c);
         }
+        cp_async_commit();
     }
-    __syncthreads();
-    if (threadIdx.x < nt) {  // sequential sum, 1/sum, lse
-        const float* ex = sv[threadIdx.x];
-        float sum = 0.f;
-        for (int j = 0; j < M; ++j) sum = fadd(sum, ex[j]);
-        sinv[threadIdx.x] = fdiv(1.f, sum);
-        lse_out[t0 + threadIdx.x] = smx[threadIdx.x] + logf(sum);
-    }
-    __syncthreads();
-    if (active) {
+    // normed stores: the token's LPT lanes take turns per 8-column group
+    bf16* nb_row = normed_bf ? normed_bf + static_cast<int64_t>(t) * d : nullptr;
+    float* nf_row = normed ? normed + static_cast<int64_t>(t) * d : nullptr;
+    for (int c = 0; c < nrc; ++c) {
+        wait_oldest();
+        __syncthreads();
+        if (c + RF_XS - 1 < nrc) {
+            issue_x(c + RF_XS - 1);
+            issue_rg(c + RF_XS - 1);
+        }
+        cp_async_commit();
+        const float* xrow = sxw[warp * RF_XS + c % RF_XS][tok];
+        const float(*rr)[MAXM] = sR[c % RF_XS];
+        const float* gg = sG[c % RF_XS];
+#pragma unroll 2
+        for (int i = 0; i < QC; i += 2) {  // 8 p per iteration => one 16-byte bf16 store
+            float nv[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int e = 4 * eg + u;
-            if (e < M) {
-                const float p = fmul(sv[tq][e], sinv[tq]);
-                sv[tq][e] = p;
-                probs[static_cast<int64_t>(t0 + tq) * M + e] = p;
+            for (int u = 0; u < 2; ++u) {
+                const float4 x = *reinterpret_cast<const float4*>(xrow + 4 * (i + u));
+                const float4 g = *reinterpret_cast<const float4*>(gg + 4 * (i + u));
+                nv[4 * u + 0] = fmul(fmul(x.x, inv), g.x);
+                nv[4 * u + 1] = fmul(fmul(x.y, inv), g.y);
+                nv[4 * u + 2] = fmul(fmul(x.z, inv), g.z);
+                nv[4 * u + 3] = fmul(fmul(x.w, inv), g.w);
             }
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x < nt) {
-        // iterative argmax (strict '>' scanning ascending => lowest index on ties) ==
-        // the first k of a stable descending sort; then ascending order
-        const int t = t0 + threadIdx.x;
-        const float* p = sv[threadIdx.x];
-        uint64_t chosen = 0;
-        for (int s = 0; s < k; ++s) {
-            int best = -1;
-            float bv = 0.f;
-            for (int j = 0; j < M; ++j) {
-                if ((chosen >> j) & 1ull) continue;
-                if (best < 0 || p[j] > bv) {
-                    best = j;
-                    bv = p[j];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float* rrow = rr[4 * i + j] + e0;
+#pragma unroll
+                for (int e4 = 0; e4 < EPL; e4 += 4) {
+                    const float4 r = *reinterpret_cast<const float4*>(rrow + e4);
+                    acc[e4 + 0] = fadd(acc[e4 + 0], fmul(nv[j], r.x));
+                    acc[e4 + 1] = fadd(acc[e4 + 1], fmul(nv[j], r.y));
+                    acc[e4 + 2] = fadd(acc[e4 + 2], fmul(nv[j], r.z));
+                    acc[e4 + 3] = fadd(acc[e4 + 3], fmul(nv[j], r.w));
                 }
             }
-            chosen |= 1ull << best;
-        }
-        float dn = 0.f;
-        for (int j = 0; j < M; ++j)
-            if ((chosen >> j) & 1ull) dn = fadd(dn, p[j]);
-        int slot = 0;
-        for (int j = 0; j < M; ++j) {
-            if ((chosen >> j) & 1ull) {
-                topk_idx[static_cast<int64_t>(t) * k + slot] = j;
-                topk_w[static_cast<int64_t>(t) * k + slot] = renorm ? fdiv(p[j], dn) : p[j];
-                ++slot;
+            if (valid && ((i >> 1) % LPT) == part) {
+                const int p0 = c * RF_RCH + 4 * i;
+                if (nb_row) {
+                    uint4 pk;
+                    const uint2 lo = pack_bf16x4(nv[0], nv[1], nv[2], nv[3]);
+                    const uint2 hi = pack_bf16x4(nv[4], nv[5], nv[6], nv[7]);
+                    pk.x = lo.x; pk.y = lo.y; pk.z = hi.x; pk.w = hi.y;
+                    *reinterpret_cast<uint4*>(nb_row + p0) = pk;
+                }
+                if (nf_row) {
+                    *reinterpret_cast<float4*>(nf_row + p0) = make_float4(nv[0], nv[1], nv[2], nv[3]);
+                    *reinterpret_cast<float4*>(nf_row + p0 + 4) = make_float4(nv[4], nv[5], nv[6], nv[7]);
+                }
             }
         }
-        if (denom_out) denom_out[t] = dn;
     }
+
+    // ---- softmax_rows (kernels.hpp:156-172) and route_from_logits (model.hpp:185-216):
+    // logits gathered per token in smem, the scans run on the token's part-0 lane
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) sv[tok][e0 + e] = acc[e];
+    __syncwarp();
+    if (part != 0 || !valid) return;
+    float* lrow = logits + static_cast<int64_t>(t) * M;
+    float* prow = probs + static_cast<int64_t>(t) * M;
+    float* pv = sv[tok];
+    float mx = pv[0];
+    for (int e = 0; e < M; ++e) {
+        lrow[e] = pv[e];
+        if (e > 0) mx = (mx < pv[e]) ? pv[e] : mx;  // std::max scan (kernels.hpp:160)
+    }
+    float sum = 0.f;
+    for (int e = 0; e < M; ++e) {
+        const float z = fsub(pv[e], mx);
+        const float ex = variant ? spes_expf::expf_glibc<1>(z) : spes_expf::expf_glibc<0>(z);
+        pv[e] = ex;
+        sum = fadd(sum, ex);
+    }
+    const float rs = fdiv(1.f, sum);
+    lse_out[t] = mx + logf(sum);
+    inv_out[t] = inv;
+    for (int e = 0; e < M; ++e) {
+        pv[e] = fmul(pv[e], rs);  // probabilities
+        prow[e] = pv[e];
+    }
+    // iterative argmax (strict '>' scanning ascending => lowest index on ties) == the
+    // first k of a stable descending sort; then ascending order
+    uint64_t chosen = 0;
+    for (int s2 = 0; s2 < k; ++s2) {
+        int best = -1;
+        float bv = 0.f;
+        for (int j = 0; j < M; ++j) {
+            if (!((chosen >> j) & 1ull) && (best < 0 || pv[j] > bv)) {
+                best = j;
+                bv = pv[j];
+            }
+        }
+        chosen |= 1ull << best;
+    }
+    float dn = 0.f;
+    for (int j = 0; j < M; ++j)
+        if ((chosen >> j) & 1ull) dn = fadd(dn, pv[j]);
+    int slot = 0;
+    for (int j = 0; j < M; ++j) {
+        if ((chosen >> j) & 1ull) {
+            topk_idx[static_cast<int64_t>(t) * k + slot] = j;
+            topk_w[static_cast<int64_t>(t) * k + slot] = renorm ? fdiv(pv[j], dn) : pv[j];
+            ++slot;
+        }
+    }
+    if (denom_out) denom_out[t] = dn;
+}
+
+template <int MM>
+static void launch_rf(unsigned grid, cudaStream_t s, const float* h, const float* gain,
+                      const float* router, int64_t T, int64_t d, int M, int k, int renorm,
+                      float eps, int variant, float* normed, bf16* normed_bf, float* logits,
+                      float* probs, int32_t* topk_idx, float* topk_w, float* lse, float* inv_rms,
+                      float* denom) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(router_fwd_k<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             RfSmem<MM>::BYTES);
+        configured = true;
+    }
+    router_fwd_k<MM><<<grid, 32 * RF_WARPS, RfSmem<MM>::BYTES, s>>>(
+        h, gain, router, (int)T, (int)d, M, k, renorm, eps, variant, normed, normed_bf, logits,
+        probs, topk_idx, topk_w, lse, inv_rms, denom);
 }
 
 void router_forward(const float* h, const float* gain, const float* router, int64_t T, int64_t d,
                     int M, int k, int renorm, float eps, int variant, float* normed,
-                    float* logits, float* probs, int32_t* topk_idx, float* topk_w, float* lse,
-                    float* inv_rms, float* denom, cudaStream_t s) {
+                    bf16* normed_bf, float* logits, float* probs, int32_t* topk_idx,
+                    float* topk_w, float* lse, float* inv_rms, float* denom, cudaStream_t s) {
     const int maxm = M <= 8 ? 8 : (M <= 16 ? 16 : (M <= 32 ? 32 : 64));
-    const int NT = 256 / (maxm / 4);
-    const unsigned grid = static_cast<unsigned>((T + NT - 1) / NT);
-#define SPES_RF(MM)                                                                              \
-    router_fwd_k<MM><<<grid, 256, 0, s>>>(h, gain, router, (int)T, (int)d, M, k, renorm, eps,    \
-                                          variant, normed, logits, probs, topk_idx, topk_w, lse, \
-                                          inv_rms, denom)
-    if (maxm == 8)
-        SPES_RF(8);
-    else if (maxm == 16)
-        SPES_RF(16);
-    else if (maxm == 32)
-        SPES_RF(32);
-    else
-        SPES_RF(64);
-#undef SPES_RF
+    const int per_block = RF_WARPS * (32 / (maxm / (maxm < 8 ? maxm : 8)));
+    const unsigned grid = static_cast<unsigned>((T + per_block - 1) / per_block);
+    auto* f = maxm == 8 ? launch_rf<8> : maxm == 16 ? launch_rf<16> : maxm == 32 ? launch_rf<32>
+                                                                                  : launch_rf<64>;
+    f(grid, s, h, gain, router, T, d, M, k, renorm, eps, variant, normed, normed_bf, logits, probs,
+      topk_idx, topk_w, lse, inv_rms, denom);
     count_launch();
 }
 
