@@ -172,8 +172,14 @@ spes_status spes_counts(spes_ctx* ctx, int64_t* opt_state_scalars, int64_t* grad
 /* Read a named device buffer of the last step (see DESIGN.md §debug names). */
 spes_status spes_debug_read(spes_ctx* ctx, const char* name, int32_t layer, void* host,
                             int64_t bytes);
-/* Gradient of the last step, full parameter layout (zeros for frozen blocks). */
+/* Gradient of the last step, full parameter layout (zeros for frozen blocks). Needs the
+ * unfused optimizer for owned experts (logic_error otherwise, see below). */
 spes_status spes_read_grads(spes_ctx* ctx, float* host, int64_t n);
+/* Optimizer placement. 1: the owned experts' MaskedAdamW runs inside the dW GEMM
+ * epilogue and their gradients are never materialized (read_grads then throws
+ * logic_error). 0 (default): gradients are materialized and one standalone optimizer
+ * pass runs after the backward. Both give identical bits. */
+spes_status spes_set_fused_optimizer(spes_ctx* ctx, int32_t on);
 /* Live per-kernel-family timing: CUDA events bracket every launch family on the
  * context stream while enabled; totals accumulate until spes_profile_reset. */
 spes_status spes_profile(spes_ctx* ctx, int32_t enable);

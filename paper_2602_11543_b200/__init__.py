@@ -74,6 +74,7 @@ def lib():
         L.spes_load_params.argtypes = [vp, f32p, i64]
         L.spes_read_params.argtypes = [vp, f32p, i64]
         L.spes_read_grads.argtypes = [vp, f32p, i64]
+        L.spes_set_fused_optimizer.argtypes = [vp, C.c_int32]
         L.spes_round_begin.argtypes = [vp, i32]
         L.spes_local_step.argtypes = [vp, C.POINTER(i32), i64, i64, C.POINTER(AdamWCfg),
                                       C.POINTER(Losses)]
@@ -224,6 +225,11 @@ class Node:
         out = np.zeros(self.P, np.float32)
         _check(lib().spes_read_params(self._ctx, f32(out), out.size))
         return out
+
+    def set_fused_optimizer(self, on):
+        """Owned experts' AdamW inside the dW GEMM epilogue (default) or as a separate pass
+        with materialized gradients (needed by read_grads); identical bits either way."""
+        _check(lib().spes_set_fused_optimizer(self._ctx, 1 if on else 0))
 
     def read_grads(self):
         out = np.zeros(self.P, np.float32)

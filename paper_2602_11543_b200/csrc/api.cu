@@ -149,6 +149,13 @@ struct spes_ctx {
     std::vector<uint8_t> owned;                  // this node's mask [M]
     std::vector<int64_t> grad_off_host;          // [L*M] compact offset or -1
     int64_t G = 0;                               // compact trainable size
+    // fused optimizer: owned experts' AdamW runs in the dW GEMM epilogues (their gradients
+    // are never materialized); the standalone pass covers psi only. Off (default): the
+    // gradients are materialized and one standalone pass updates everything. Both give
+    // identical bits; the fused epilogue is issue/latency-bound at ~3.7 TB/s with the 8
+    // epilogue warps that fit next to the MMA ring, so it does not beat the separate pass yet.
+    bool fused_opt = false;
+    spes_k::AdamScalars cur_adam{};  // this step's AdamW scalars (set before backward)
     std::vector<spes_k::AdamSeg> segs_host;
 
     DevMem persistent;  // params, shadows, optimizer state
@@ -547,7 +554,8 @@ void forward_backward(spes_ctx* c) {
             spes_k::RoutePlan rp{Y.chunk_counts, Y.counts, Y.pad_off, Y.lb_coeff, Y.slot_row,
                                  Y.row_token, Y.row_w, Y.groups, Y.tiles};
             spes_k::GroupBases gb{Y.gu, Y.y, c->dgu, c->dxp, c->grads, Y.grad_off, d, f,
-                                  bn_for(d), bn_for(f), bn_for(d), bn_for(d), c->tr};
+                                  bn_for(d), bn_for(f), bn_for(d), bn_for(d), c->tr,
+                                  P + L.off_expert(l, 0), l * M, c->fused_opt ? 1 : 0};
             spes_k::route_plan(Y.topk_idx, Y.topk_w, T, M, k, R, rp, gb, st);
         }
         {
@@ -618,7 +626,21 @@ void forward_backward(spes_ctx* c) {
                                    Y.groups + 3 * M, M, Y.tiles + 3,
                                    c->max_tiles[3], st);
         }
-        if (c->max_tiles[4] > 0) {
+        if (c->max_tiles[4] > 0 && c->fused_opt) {
+            // owned experts: dW and MaskedAdamW in one pass (no gradient materialized)
+            const spes_k::Shadows sh = shadows_of(c);
+            const spes_k::AdamEpi ae{c->cur_adam, c->m, c->v, sh.w1, sh.w2, d, f, c->d_losses};
+            {
+                PROF("gemm_bwd_dw_gate_up+adamw");
+                spes_k::gemm_adamw_w1(Y.a_xp_mn, c->b_dgu_mn, Y.groups + 4 * M, M, Y.tiles + 4,
+                                      c->max_tiles[4], ae, st);
+            }
+            {
+                PROF("gemm_bwd_dw_down+adamw");
+                spes_k::gemm_adamw_w2(bn_for(d), Y.a_hact_mn, c->b_dyw_mn, Y.groups + 5 * M, M,
+                                      Y.tiles + 5, c->max_tiles[5], ae, st);
+            }
+        } else if (c->max_tiles[4] > 0) {
             {
                 PROF("gemm_bwd_dw_gate_up");
                 spes_k::gemm_grad_w1(Y.a_xp_mn, c->b_dgu_mn, Y.groups + 4 * M, M, Y.tiles + 4,
@@ -652,21 +674,27 @@ void forward_backward(spes_ctx* c) {
     }
 }
 
-void optimizer_step(spes_ctx* c, const spes_adamw_cfg* o) {
+// MaskedAdamW::step scalars (trainer.hpp:68-84): bias corrections in double, cast to float.
+// Called before the backward so the fused dW epilogues can apply the step.
+void optimizer_begin(spes_ctx* c, const spes_adamw_cfg* o) {
     c->adam_step += 1;
-    // MaskedAdamW::step (trainer.hpp:68-84): bias corrections in double, cast to float
     const float bc1 = 1.f - static_cast<float>(std::pow(o->beta1, static_cast<double>(c->adam_step)));
     const float bc2 = 1.f - static_cast<float>(std::pow(o->beta2, static_cast<double>(c->adam_step)));
     const float b1 = static_cast<float>(o->beta1), b2 = static_cast<float>(o->beta2);
     volatile float one = 1.f;
     const float omb1 = one - b1, omb2 = one - b2;
-    {
-        PROF("adamw");
-        spes_k::adamw(c->params, c->grads, c->m, c->v, c->segs,
-                      static_cast<int>(c->segs_host.size()), c->G, static_cast<float>(o->lr), b1,
-                      b2, omb1, omb2, static_cast<float>(o->eps),
-                      static_cast<float>(o->weight_decay), bc1, bc2, shadows_of(c), c->stream);
-    }
+    c->cur_adam = spes_k::AdamScalars{static_cast<float>(o->lr), b1, b2, omb1, omb2,
+                                      static_cast<float>(o->eps),
+                                      static_cast<float>(o->weight_decay), bc1, bc2};
+}
+
+// The rest of the step: psi (and, unfused, the owned experts) after the backward.
+void optimizer_finish(spes_ctx* c) {
+    PROF("adamw");
+    const int64_t n = c->fused_opt ? c->lay.psi() : c->G;  // psi is the compact prefix
+    spes_k::adamw(c->params, c->grads, c->m, c->v, c->segs,
+                  static_cast<int>(c->segs_host.size()), n, c->cur_adam, shadows_of(c),
+                  c->d_losses, c->stream);
 }
 
 void validate_tokens(const spes_ctx* c, const int32_t* tokens, int64_t n) {
@@ -711,12 +739,16 @@ void check_err_flag(spes_ctx* c) {
 
 void local_step_impl(spes_ctx* c, int64_t B, int64_t S, const spes_adamw_cfg* opt,
                      spes_losses* losses) {
-    forward_backward(c);
+    optimizer_begin(c, opt);
+    forward_backward(c);  // fused: owned experts updated here unless the loss is non-finite
+    optimizer_finish(c);  // psi; a device-side check skips it after a non-finite loss
     if (losses) {
         read_losses(c, losses);
-        if (!std::isfinite(losses->total)) return;  // caller reports runtime_error
+        if (!std::isfinite(losses->total)) {  // no update was applied; caller reports it
+            c->adam_step -= 1;
+            return;
+        }
     }
-    optimizer_step(c, opt);
     (void)B;
     (void)S;
 }
@@ -1291,9 +1323,20 @@ spes_status spes_counts(spes_ctx* c, int64_t* opt_state, int64_t* grad_scalars, 
     });
 }
 
+spes_status spes_set_fused_optimizer(spes_ctx* c, int32_t on) {
+    return guard([&] {
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        c->fused_opt = on != 0;  // group tables are rebuilt every step with the mode
+    });
+}
+
 spes_status spes_read_grads(spes_ctx* c, float* host, int64_t n) {
     return guard([&] {
         if (n != c->lay.total()) throw std::invalid_argument("read_grads: size mismatch");
+        if (c->fused_opt && c->G > c->lay.psi())
+            throw std::logic_error(
+                "read_grads: owned-expert gradients are fused into the optimizer; call "
+                "spes_set_fused_optimizer(ctx, 0) before the step to materialize them");
         ck(cudaSetDevice(c->device), "cudaSetDevice");
         std::vector<float> comp(c->G);
         ck(cudaMemcpyAsync(comp.data(), c->grads, 4 * c->G, cudaMemcpyDeviceToHost, c->stream), "D2H");
@@ -1493,9 +1536,11 @@ spes_status spes_kernel_adamw(float* theta, const float* grad, float* m, float* 
         const float bc2 = 1.f - static_cast<float>(std::pow(o->beta2, static_cast<double>(step)));
         const float b1 = static_cast<float>(o->beta1), b2 = static_cast<float>(o->beta2);
         volatile float one = 1.f;
-        spes_k::adamw(dt, dgr, dm, dv, ds, 1, n, static_cast<float>(o->lr), b1, b2, one - b1,
-                      one - b2, static_cast<float>(o->eps), static_cast<float>(o->weight_decay),
-                      bc1, bc2, spes_k::Shadows{nullptr, nullptr, nullptr, 0, 0}, 0);
+        const spes_k::AdamScalars a{static_cast<float>(o->lr), b1, b2, one - b1, one - b2,
+                                    static_cast<float>(o->eps),
+                                    static_cast<float>(o->weight_decay), bc1, bc2};
+        spes_k::adamw(dt, dgr, dm, dv, ds, 1, n, a, spes_k::Shadows{nullptr, nullptr, nullptr, 0, 0},
+                      nullptr, 0);
         ck(cudaDeviceSynchronize(), "adamw kernel");
         ck(cudaMemcpy(theta, dt, 4 * n, cudaMemcpyDeviceToHost), "D2H");
         ck(cudaMemcpy(m, dm, 4 * n, cudaMemcpyDeviceToHost), "D2H");

@@ -57,4 +57,25 @@ __device__ __forceinline__ float sigmoid_f(float z) {
     return z >= 0.f ? 1.f / (1.f + __expf(-z)) : __expf(z) / (1.f + __expf(z));
 }
 
+// MaskedAdamW::step scalars (trainer.hpp:68-84; bias corrections computed on the host)
+struct AdamScalars {
+    float lr, b1, b2, omb1, omb2, eps, wd, bc1, bc2;
+};
+// One MaskedAdamW element update (trainer.hpp:85-92), exact fp32 op order. Shared by the
+// standalone optimizer pass and the dW-GEMM epilogues so both produce identical bits.
+__device__ __forceinline__ float adam_elem(float th, float g, float& m, float& v,
+                                           const AdamScalars& a) {
+    m = fadd(fmul(a.b1, m), fmul(a.omb1, g));
+    v = fadd(fmul(a.b2, v), fmul(fmul(a.omb2, g), g));
+    const float mhat = fdiv(m, a.bc1);
+    const float vhat = fdiv(v, a.bc2);
+    const float upd = fmul(a.lr, fadd(fdiv(mhat, fadd(fsqrt(vhat), a.eps)), fmul(a.wd, th)));
+    return fsub(th, upd);
+}
+// device-side guard: the reference applies no update after a non-finite loss
+// (trainer.hpp:166-167); the step's total loss lives on the device
+__device__ __forceinline__ bool loss_ok(const double* total) {
+    return total == nullptr || isfinite(*total);
+}
+
 }  // namespace spes_dev

@@ -7,6 +7,8 @@
 //               dWd and dHead straight into the gradient buffer).
 //   EpiDSwiGLU  expert backward: dHact -> (dG, dU) using the saved GU, written as
 //               dGU (bf16) for the dX and dW GEMMs.
+// All epilogues hand their row pieces to EpiOut (grouped_gemm.cuh): an smem transpose so
+// that each warp store instruction writes whole 128-byte rows.
 //   EpiGradW1   dW of gate||up straight into the fp32 wg / wu gradient blocks.
 // Weight-gradient GEMMs read the row-major activations directly as MN-major
 // operands (grouped_gemm_kernel<..., MN=true>): no transposed copies are made.
@@ -21,28 +23,21 @@ namespace spes_k {
 
 using namespace spes_dev;
 
-__device__ __forceinline__ void store_bf16x32(bf16* dst, const float (&v)[32]) {
-    uint4* d4 = reinterpret_cast<uint4*>(dst);
+__device__ __forceinline__ void pack_bf16x32(const float (&v)[32], uint4 (&pk)[4]) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        uint4 pk;
         __nv_bfloat162 a = __floats2bfloat162_rn(v[8 * i + 0], v[8 * i + 1]);
         __nv_bfloat162 b = __floats2bfloat162_rn(v[8 * i + 2], v[8 * i + 3]);
         __nv_bfloat162 c = __floats2bfloat162_rn(v[8 * i + 4], v[8 * i + 5]);
         __nv_bfloat162 d = __floats2bfloat162_rn(v[8 * i + 6], v[8 * i + 7]);
-        pk.x = *reinterpret_cast<uint32_t*>(&a);
-        pk.y = *reinterpret_cast<uint32_t*>(&b);
-        pk.z = *reinterpret_cast<uint32_t*>(&c);
-        pk.w = *reinterpret_cast<uint32_t*>(&d);
-        d4[i] = pk;
+        pk[i].x = *reinterpret_cast<uint32_t*>(&a);
+        pk[i].y = *reinterpret_cast<uint32_t*>(&b);
+        pk[i].z = *reinterpret_cast<uint32_t*>(&c);
+        pk[i].w = *reinterpret_cast<uint32_t*>(&d);
     }
 }
 
-__device__ __forceinline__ void load_bf16x32(const bf16* src, float (&v)[32]) {
-    const uint4* s4 = reinterpret_cast<const uint4*>(src);
-    uint4 pk[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) pk[i] = __ldg(s4 + i);
+__device__ __forceinline__ void unpack_bf16x32(const uint4* pk, float (&v)[32]) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&pk[i]);
@@ -56,70 +51,196 @@ __device__ __forceinline__ void load_bf16x32(const bf16* src, float (&v)[32]) {
 }
 
 struct EpiSwiGLU {
+    static constexpr int SLOTS = 1;
     bf16* hact;
     int64_t f;
+    __device__ void prefetch(const GemmGroup&, int, int, int, int) const {}
+    // 64 columns per pass so every output piece (gate, up, hact) is a full 128-byte row
     __device__ void operator()(const GemmGroup& g, int mt, int nt, int r, uint32_t taddr,
-                               bool empty, int half) const {
+                               bool empty, int half, EpiOut& out) const {
         const int64_t row = g.out_row0 + static_cast<int64_t>(mt) * GEMM_BM + r;
         bf16* gu = static_cast<bf16*>(g.out0) + row * g.ldo + static_cast<int64_t>(nt) * 256;
         bf16* ha = hact + row * f + static_cast<int64_t>(nt) * 128;
-#pragma unroll 1
-        for (int c = half * 64; c < half * 64 + 64; c += 32) {
+        const int c = half * 64;
+        uint4 pg[8], pu[8], ph[8];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
             float gv[32], uv[32], hv[32];
-            acc_load32(taddr + c, empty, gv);
-            acc_load32(taddr + 128 + c, empty, uv);
+            acc_load32(taddr + c + 32 * s, empty, gv);
+            acc_load32(taddr + 128 + c + 32 * s, empty, uv);
 #pragma unroll
             for (int i = 0; i < 32; ++i) hv[i] = gv[i] * sigmoid_fast(gv[i]) * uv[i];
-            store_bf16x32(gu + c, gv);
-            store_bf16x32(gu + 128 + c, uv);
-            store_bf16x32(ha + c, hv);
+            pack_bf16x32(gv, *reinterpret_cast<uint4(*)[4]>(&pg[4 * s]));
+            pack_bf16x32(uv, *reinterpret_cast<uint4(*)[4]>(&pu[4 * s]));
+            pack_bf16x32(hv, *reinterpret_cast<uint4(*)[4]>(&ph[4 * s]));
         }
+        out.put<8>(gu + c, pg);
+        out.put<8>(gu + 128 + c, pu);
+        out.put<8>(ha + c, ph);
     }
 };
 
 template <int BN>
 struct EpiDSwiGLU {
+    static constexpr int SLOTS = 1;
     const bf16* gu;
     int64_t f;
+    // the saved gate / up rows this thread reads for (mt, nt): 2 x BN/2 bf16 of its row
+    __device__ void prefetch(const GemmGroup& g, int mt, int nt, int r, int half) const {
+        const int64_t row = g.out_row0 + static_cast<int64_t>(mt) * GEMM_BM + r;
+        const bf16* gurow = gu + row * 2 * f;
+#pragma unroll
+        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 64) {
+            const int64_t x0 = static_cast<int64_t>(nt) * BN + c;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(gurow + il_gate(x0)));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(gurow + il_up(x0)));
+        }
+    }
     __device__ void operator()(const GemmGroup& g, int mt, int nt, int r, uint32_t taddr,
-                               bool empty, int half) const {
+                               bool empty, int half, EpiOut& out) const {
         const int64_t row = g.out_row0 + static_cast<int64_t>(mt) * GEMM_BM + r;
         const bf16* gurow = gu + row * 2 * f;
         bf16* dgurow = static_cast<bf16*>(g.out0) + row * g.ldo;
 #pragma unroll 1
-        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
+        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 64) {
             const int64_t x0 = static_cast<int64_t>(nt) * BN + c;  // f index of column 0
-            const int64_t ig = il_gate(x0), iu = il_up(x0);
-            float dh[32], gv[32], uv[32], dg[32], du[32];
-            load_bf16x32(gurow + ig, gv);
-            load_bf16x32(gurow + iu, uv);
-            acc_load32(taddr + c, empty, dh);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const float s = sigmoid_fast(gv[i]);
-                dg[i] = dh[i] * uv[i] * (s * (1.f + gv[i] * (1.f - s)));
-                du[i] = dh[i] * (gv[i] * s);
+            const int64_t ig = il_gate(x0), iu = il_up(x0);         // 64-column runs
+            uint4 pg[8], pu[8], lg[8], lu[8];
+            {  // saved gate / up pre-activations (64 columns each): both loads in flight
+                uint4 tg[8], tu[8];
+                out.load_rows<8>(gurow + ig, tg);
+                out.load_rows<8>(gurow + iu, tu);
+                out.land_rows<8>(tg, lg);
+                out.land_rows<8>(tu, lu);
             }
-            store_bf16x32(dgurow + ig, dg);
-            store_bf16x32(dgurow + iu, du);
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                float dh[32], gv[32], uv[32], dg[32], du[32];
+                unpack_bf16x32(&lg[4 * s], gv);
+                unpack_bf16x32(&lu[4 * s], uv);
+                acc_load32(taddr + c + 32 * s, empty, dh);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const float sg = sigmoid_fast(gv[i]);
+                    dg[i] = dh[i] * uv[i] * (sg * (1.f + gv[i] * (1.f - sg)));
+                    du[i] = dh[i] * (gv[i] * sg);
+                }
+                pack_bf16x32(dg, *reinterpret_cast<uint4(*)[4]>(&pg[4 * s]));
+                pack_bf16x32(du, *reinterpret_cast<uint4(*)[4]>(&pu[4 * s]));
+            }
+            out.put<8>(dgurow + ig, pg);
+            out.put<8>(dgurow + iu, pu);
         }
     }
 };
 
 struct EpiGradW1 {
+    static constexpr int SLOTS = 1;
+    __device__ void prefetch(const GemmGroup&, int, int, int, int) const {}
     __device__ void operator()(const GemmGroup& g, int mt, int nt, int r, uint32_t taddr,
-                               bool empty, int half) const {
+                               bool empty, int half, EpiOut& out) const {
         const int64_t row = static_cast<int64_t>(mt) * GEMM_BM + r;  // d index
 #pragma unroll 1
         for (int c = half * 128; c < half * 128 + 128; c += 32) {
             float v[32];
             acc_load32(taddr + c, empty, v);
             float* base = static_cast<float*>(c < 128 ? g.out0 : g.out1);
-            float* dst = base + row * g.ldo + static_cast<int64_t>(nt) * 128 + (c & 127);
-            float4* d4 = reinterpret_cast<float4*>(dst);
+            out.put_f32x32(base + row * g.ldo + static_cast<int64_t>(nt) * 128 + (c & 127), v);
+        }
+    }
+};
+
+// ---- MaskedAdamW fused into the dW epilogue ----------------------------------------
+// The accumulator tile IS the owned expert's gradient (full K reduction in one tile),
+// so the optimizer step runs right here: theta, m and v rows are fetched row-major into
+// three smem slots with cp.async, each lane updates its row in place with the same
+// adam_elem as the standalone pass (bit-identical), the slots are written back
+// row-major, and the bf16 GEMM operand copy is refreshed. No gradient is materialized.
+// Group fields: out0 = parameters of the block at (row 0, col 0), out_row0 = compact
+// (m / v) offset of the same element, aux = shadow slot, ldo = row length.
+__device__ __forceinline__ void adam_rows32(const EpiOut& out, const float (&gr)[32],
+                                            const AdamScalars& a, float (&th_out)[32]) {
+    float* th = reinterpret_cast<float*>(out.my_row(0));
+    float* mm = reinterpret_cast<float*>(out.my_row(1));
+    float* vv = reinterpret_cast<float*>(out.my_row(2));
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-                d4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    for (int i = 0; i < 32; i += 4) {
+        float4 t4 = *reinterpret_cast<float4*>(th + i);
+        float4 m4 = *reinterpret_cast<float4*>(mm + i);
+        float4 v4 = *reinterpret_cast<float4*>(vv + i);
+        t4.x = adam_elem(t4.x, gr[i + 0], m4.x, v4.x, a);
+        t4.y = adam_elem(t4.y, gr[i + 1], m4.y, v4.y, a);
+        t4.z = adam_elem(t4.z, gr[i + 2], m4.z, v4.z, a);
+        t4.w = adam_elem(t4.w, gr[i + 3], m4.w, v4.w, a);
+        *reinterpret_cast<float4*>(th + i) = t4;
+        *reinterpret_cast<float4*>(mm + i) = m4;
+        *reinterpret_cast<float4*>(vv + i) = v4;
+        th_out[i + 0] = t4.x;
+        th_out[i + 1] = t4.y;
+        th_out[i + 2] = t4.z;
+        th_out[i + 3] = t4.w;
+    }
+}
+
+// one 32-column piece: fetch theta / m / v rows, update, write back, refresh the shadow
+__device__ __forceinline__ void adam_piece(const EpiOut& out, const AdamEpi& p, uint32_t taddr,
+                                           bool empty, float* th_g, int64_t comp, bf16* sh_g) {
+    float gr[32];
+    acc_load32(taddr, empty, gr);
+    out.rows_load_async<8>(0, th_g);
+    out.rows_load_async<8>(1, p.m + comp);
+    out.rows_load_async<8>(2, p.v + comp);
+    out.rows_wait();
+    float th[32];
+    adam_rows32(out, gr, p.a, th);
+    out.rows_store<8>(0, th_g);
+    out.rows_store<8>(1, p.m + comp);
+    out.rows_store<8>(2, p.v + comp);
+    uint4 pk[4];
+    pack_bf16x32(th, pk);
+    out.put<4>(sh_g, pk, 0);
+}
+
+// dW of gate||up (MN-MN, BN = 256): tile rows = d index, columns [0,128) -> wg, [128,256)
+// -> wu at f-columns nt*128 + c; shadow W1 [slot][d][2f] interleaved gate|up.
+struct EpiAdamW1 {
+    static constexpr int SLOTS = 3;
+    AdamEpi p;
+    __device__ void prefetch(const GemmGroup&, int, int, int, int) const {}
+    __device__ void operator()(const GemmGroup& g, int mt, int nt, int r, uint32_t taddr,
+                               bool empty, int half, EpiOut& out) const {
+        if (!loss_ok(p.loss_total)) return;  // uniform: no update after a non-finite loss
+        const int64_t row = static_cast<int64_t>(mt) * GEMM_BM + r;  // d index
+        const int64_t df = p.d * p.f;
+        bf16* sh_row = p.w1 + static_cast<int64_t>(g.aux) * 2 * df + row * 2 * p.f;
+#pragma unroll 1
+        for (int c = half * 128; c < half * 128 + 128; c += 32) {
+            const bool up = c >= 128;
+            const int64_t x0 = static_cast<int64_t>(nt) * 128 + (c & 127);
+            const int64_t off = (up ? df : 0) + row * g.ldo + x0;
+            adam_piece(out, p, taddr + c, empty, static_cast<float*>(g.out0) + off, g.out_row0 + off,
+                       sh_row + (up ? il_up(x0) : il_gate(x0)));
+        }
+    }
+};
+
+// dW of down (MN-MN): tile rows = f index, columns = d index nt*BN + c; shadow W2 = Wd.
+template <int BN>
+struct EpiAdamW2 {
+    static constexpr int SLOTS = 3;
+    AdamEpi p;
+    __device__ void prefetch(const GemmGroup&, int, int, int, int) const {}
+    __device__ void operator()(const GemmGroup& g, int mt, int nt, int r, uint32_t taddr,
+                               bool empty, int half, EpiOut& out) const {
+        if (!loss_ok(p.loss_total)) return;
+        const int64_t row = static_cast<int64_t>(mt) * GEMM_BM + r;  // f index
+        bf16* sh_row = p.w2 + static_cast<int64_t>(g.aux) * p.d * p.f + row * p.d;
+#pragma unroll 1
+        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
+            const int64_t x0 = static_cast<int64_t>(nt) * BN + c;
+            const int64_t off = row * g.ldo + x0;
+            adam_piece(out, p, taddr + c, empty, static_cast<float*>(g.out0) + off, g.out_row0 + off,
+                       sh_row + x0);
         }
     }
 };
@@ -150,14 +271,14 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* 
         static bool configured2 = false;
         if (!configured2) {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Gemm2Cfg<BN>::SMEM_BYTES);
+                                 Gemm2Cfg<BN, Epi::SLOTS>::SMEM_BYTES);
             configured2 = true;
         }
         const int pairs = max_tiles < num_sms() / 2 ? max_tiles : num_sms() / 2;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(2 * pairs);
         cfg.blockDim = dim3(GEMM_THREADS);
-        cfg.dynamicSmemBytes = Gemm2Cfg<BN>::SMEM_BYTES;
+        cfg.dynamicSmemBytes = Gemm2Cfg<BN, Epi::SLOTS>::SMEM_BYTES;
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -174,11 +295,12 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* 
     static bool configured = false;  // one per template instantiation
     if (!configured) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             GemmCfg<BN>::SMEM_BYTES);
+                             GemmCfg<BN, Epi::SLOTS>::SMEM_BYTES);
         configured = true;
     }
     const int grid = max_tiles < num_sms() ? max_tiles : num_sms();
-    kern<<<grid, GEMM_THREADS, GemmCfg<BN>::SMEM_BYTES, s>>>(a, b, g, ng, tiles, max_tiles, epi);
+    kern<<<grid, GEMM_THREADS, GemmCfg<BN, Epi::SLOTS>::SMEM_BYTES, s>>>(a, b, g, ng, tiles,
+                                                                       max_tiles, epi);
     count_launch();
 }
 
@@ -231,6 +353,19 @@ void gemm_dswiglu(int bn, const CUtensorMap& a, const CUtensorMap& b, const Gemm
 void gemm_grad_w1(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
                   const int32_t* tiles, int max_tiles, cudaStream_t s) {
     launch<256, true, true>(a, b, g, ng, tiles, max_tiles, EpiGradW1{}, s);
+}
+
+void gemm_adamw_w1(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
+                   const int32_t* tiles, int max_tiles, const AdamEpi& p, cudaStream_t s) {
+    launch<256, true, true>(a, b, g, ng, tiles, max_tiles, EpiAdamW1{p}, s);
+}
+
+void gemm_adamw_w2(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
+                   const int32_t* tiles, int max_tiles, const AdamEpi& p, cudaStream_t s) {
+    if (bn == 256)
+        launch<256, true, true>(a, b, g, ng, tiles, max_tiles, EpiAdamW2<256>{p}, s);
+    else
+        launch<128, true, true>(a, b, g, ng, tiles, max_tiles, EpiAdamW2<128>{p}, s);
 }
 
 }  // namespace spes_k

@@ -17,7 +17,8 @@
 //   warp 1  : MMA issuer         (one elected lane, tcgen05.mma cta_group::1, M=128)
 //   warp 2  : TMEM allocator
 //   warps 4-11: epilogue, two warps per TMEM lane quarter, each on half of the tile's
-//               columns (TMEM -> registers -> fused epilogue -> global)
+//               columns (TMEM -> registers -> fused epilogue -> smem transpose ->
+//               full-line global stores, EpiOut)
 // Pipelines: STAGES-deep smem ring (full/empty mbarriers) and a 2-deep TMEM
 // accumulator ring (tmem_full/tmem_empty) so the epilogue of tile i overlaps
 // the MMAs of tile i+1.
@@ -30,6 +31,106 @@ namespace spes_dev {
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;  // 64 bf16 = 128 B = one swizzle row
 constexpr int GEMM_THREADS = 384;  // 4 control warps + 8 epilogue warps
+
+// ---- epilogue output staging --------------------------------------------------------
+// Direct 16-byte stores from a row-per-lane layout send 32 half-sector requests to L2 per
+// warp instruction, which capped the epilogue at ~11 GB/s per SM. Instead each lane
+// writes its row piece (<= 128 B) into its smem row, and the warp copies the 32 pieces
+// out row-major: one STG.128 instruction then covers 4 whole 128-byte rows (8 lanes per
+// row, row addresses exchanged by shuffles), i.e. full-line writes.
+constexpr int EPI_SLOT_PITCH = 144;  // 128 B + 16 B pad: STS.128 across rows conflict-free
+constexpr int EPI_SLOT_BYTES = 32 * EPI_SLOT_PITCH;  // one 32-row slot of a warp
+constexpr int EPI_WARPS = 8;
+// staging bytes of a CTA when every epilogue warp owns `slots` slots
+constexpr int epi_stage_bytes(int slots) { return EPI_WARPS * slots * EPI_SLOT_BYTES; }
+constexpr int GEMM_SMEM_MAX = 232448;  // 227 KiB opt-in per CTA
+
+struct EpiOut {
+    uint8_t* base;  // this warp's slots: slot s, lane r at base + s * SLOT_BYTES + r * PITCH
+    int lane;
+    __device__ __forceinline__ uint8_t* row_of(int s, int r) const {
+        return base + s * EPI_SLOT_BYTES + r * EPI_SLOT_PITCH;
+    }
+    __device__ __forceinline__ uint4* my_row(int s) const {
+        return reinterpret_cast<uint4*>(row_of(s, lane));
+    }
+    // warp-collective: slot s (rows = lanes) -> the 32 destinations (each lane passes its
+    // own, 16-byte aligned), row-major so one STG.128 covers 4 whole 128-byte rows
+    template <int N16>
+    __device__ __forceinline__ void rows_store(int s, void* gdst) const {
+        static_assert(N16 == 4 || N16 == 8, "row pieces of 64 or 128 bytes");
+        __syncwarp();
+        constexpr int RPI = 32 / N16;
+        const int sub = lane % N16, r0 = lane / N16;
+        const unsigned long long ga = reinterpret_cast<unsigned long long>(gdst);
+#pragma unroll
+        for (int i = 0; i < N16; ++i) {
+            const int rr = i * RPI + r0;
+            const unsigned long long a = __shfl_sync(0xffffffffu, ga, rr);
+            reinterpret_cast<uint4*>(a)[sub] = reinterpret_cast<const uint4*>(row_of(s, rr))[sub];
+        }
+        __syncwarp();
+    }
+    // warp-collective: each lane's row piece (registers) -> its destination, via slot s
+    template <int N16>
+    __device__ __forceinline__ void put(void* gdst, const uint4* v, int s = 0) const {
+        uint4* row = my_row(s);
+#pragma unroll
+        for (int i = 0; i < N16; ++i) row[i] = v[i];
+        rows_store<N16>(s, gdst);
+    }
+    __device__ __forceinline__ void put_f32x32(float* gdst, const float (&v)[32]) const {
+        put<8>(gdst, reinterpret_cast<const uint4*>(v));
+    }
+    // warp-collective: the 32 sources -> slot s rows, row-major 16-byte cp.async (whole
+    // 128-byte rows per instruction); complete with rows_wait()
+    template <int N16>
+    __device__ __forceinline__ void rows_load_async(int s, const void* gsrc) const {
+        constexpr int RPI = 32 / N16;
+        const int sub = lane % N16, r0 = lane / N16;
+        const unsigned long long ga = reinterpret_cast<unsigned long long>(gsrc);
+#pragma unroll
+        for (int i = 0; i < N16; ++i) {
+            const int rr = i * RPI + r0;
+            const unsigned long long a = __shfl_sync(0xffffffffu, ga, rr);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                             smem_u32(row_of(s, rr) + 16 * sub)),
+                         "l"(a + 16 * sub)
+                         : "memory");
+        }
+    }
+    __device__ __forceinline__ void rows_wait() const {
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+    }
+    // synchronous variant in two halves so several pieces can be in flight: load_rows
+    // issues the row-major loads into registers, land_rows transposes them through slot 0
+    template <int N16>
+    __device__ __forceinline__ void load_rows(const void* gsrc, uint4 (&tmp)[N16]) const {
+        constexpr int RPI = 32 / N16;
+        const int sub = lane % N16, r0 = lane / N16;
+        const unsigned long long ga = reinterpret_cast<unsigned long long>(gsrc);
+#pragma unroll
+        for (int i = 0; i < N16; ++i) {
+            const unsigned long long a = __shfl_sync(0xffffffffu, ga, i * RPI + r0);
+            tmp[i] = __ldg(reinterpret_cast<const uint4*>(a) + sub);
+        }
+    }
+    template <int N16>
+    __device__ __forceinline__ void land_rows(const uint4 (&tmp)[N16], uint4* v) const {
+        constexpr int RPI = 32 / N16;
+        const int sub = lane % N16, r0 = lane / N16;
+#pragma unroll
+        for (int i = 0; i < N16; ++i)
+            reinterpret_cast<uint4*>(row_of(0, i * RPI + r0))[sub] = tmp[i];
+        __syncwarp();
+        const uint4* row = my_row(0);
+#pragma unroll
+        for (int i = 0; i < N16; ++i) v[i] = row[i];
+        __syncwarp();
+    }
+    __device__ __forceinline__ void drain() const {}
+};
 
 constexpr int GEMM_MAX_GROUPS = 512;
 constexpr int GEMM_TABLE_BYTES = 8 * GEMM_MAX_GROUPS;
@@ -47,17 +148,22 @@ struct GemmGroup {
     int64_t ldo;         // epilogue-defined leading dimension
     void* out0;          // epilogue-defined outputs
     void* out1;
+    int32_t aux;         // epilogue-defined (fused optimizer: shadow slot)
+    int32_t _pad;
 };
 
-template <int BN>
+template <int BN, int SLOTS = 1>
 struct GemmCfg {
-    static constexpr int STAGES = (BN == 256) ? 4 : 6;
     static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
     static constexpr int B_BYTES = BN * GEMM_BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int FIXED = 1024 /*align*/ + 256 /*barriers*/ + GEMM_TABLE_BYTES;
+    static constexpr int EPI_BYTES = epi_stage_bytes(SLOTS);
+    static constexpr int FIT = (GEMM_SMEM_MAX - FIXED - EPI_BYTES) / STAGE_BYTES;
+    static constexpr int STAGES = FIT > 6 ? 6 : FIT;
+    static_assert(STAGES >= 2, "smem ring too shallow");
     static constexpr int TMEM_COLS = 2 * BN;  // two accumulator buffers
-    static constexpr int SMEM_BYTES =
-        STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + GEMM_TABLE_BYTES;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + FIXED + EPI_BYTES;
 };
 
 // Per-CTA copy of the group table's tile_start / k-block counts in shared memory: the
@@ -85,7 +191,10 @@ __device__ __forceinline__ int find_group(const int* ts, int n, int tile) {
 
 // Epi must provide:
 //   __device__ void operator()(const GemmGroup& g, int mt, int nt, int r, uint32_t taddr,
-//                              bool empty, int half) const;
+//                              bool empty, int half, EpiOut& out) const;
+//   __device__ void prefetch(const GemmGroup& g, int mt, int nt, int r, int half) const;
+//   static constexpr int SLOTS;  (32-row smem staging slots per epilogue warp)
+//     (L2 warm-up of epilogue inputs of the tile this thread handles next; may be empty)
 // r = row within the 128-row tile handled by this thread; taddr = TMEM address of
 // (lane r, column 0) of this tile's accumulator; empty => k_len == 0 (result is 0).
 //
@@ -101,7 +210,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                         const __grid_constant__ CUtensorMap mapB,
                         const GemmGroup* __restrict__ groups, int num_groups,
                         const int* __restrict__ total_tiles_ptr, int max_tiles, Epi epi) {
-    using C = GemmCfg<BN>;
+    using C = GemmCfg<BN, Epi::SLOTS>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -113,6 +222,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
     int* s_ts = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(bars) + 256);
     int* s_nkb = s_ts + GEMM_MAX_GROUPS;
+    uint8_t* s_epi = reinterpret_cast<uint8_t*>(bars) + 256 + GEMM_TABLE_BYTES;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -224,6 +334,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int q = warp & 3;           // TMEM lane quarter this warp may access
         const int half = (warp - 4) >> 2;  // which half of the tile's columns
         const int r = q * 32 + lane;
+        EpiOut out{s_epi + (warp - 4) * Epi::SLOTS * EPI_SLOT_BYTES, lane};
         int it = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
             const int gi = find_group(s_ts, num_groups, t);
@@ -232,13 +343,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const int mt = local / g.n_tiles, nt = local % g.n_tiles;
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
+            if (t + static_cast<int>(gridDim.x) < total) {  // warm L2 for the next tile's inputs
+                const int tn = t + gridDim.x;
+                const GemmGroup& gn = groups[find_group(s_ts, num_groups, tn)];
+                const int ln = tn - gn.tile_start;
+                epi.prefetch(gn, ln / gn.n_tiles, ln % gn.n_tiles, r, half);
+            }
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
-            epi(g, mt, nt, r, taddr, g.k_len == 0, half);
+            epi(g, mt, nt, r, taddr, g.k_len == 0, half, out);
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
         }
+        out.drain();
     }
 
     tc_fence_before();
@@ -266,19 +384,18 @@ __device__ __forceinline__ void acc_load32(uint32_t taddr, bool empty, float (&v
 // Plain FP32 store: out0[(out_row0 + mt*128 + r) * ldo + nt*BN + c].
 template <int BN>
 struct EpiStoreF32 {
+    static constexpr int SLOTS = 1;
+    __device__ void prefetch(const GemmGroup&, int, int, int, int) const {}
     __device__ void operator()(const GemmGroup& g, int mt, int nt, int r, uint32_t taddr,
-                               bool empty, int half) const {
-        float* out = static_cast<float*>(g.out0) +
+                               bool empty, int half, EpiOut& out) const {
+        float* dst = static_cast<float*>(g.out0) +
                      (g.out_row0 + static_cast<int64_t>(mt) * GEMM_BM + r) * g.ldo +
                      static_cast<int64_t>(nt) * BN;
 #pragma unroll 1
         for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
             float v[32];
             acc_load32(taddr + c, empty, v);
-            float4* dst = reinterpret_cast<float4*>(out + c);
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-                dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            out.put_f32x32(dst + c, v);
         }
     }
 };

@@ -2,7 +2,7 @@
 // computes a 256 x BN tile with one tcgen05.mma.cta_group::2 stream (M = 256).
 //   * each CTA stages its 128 rows of A and its BN/2 rows (K-major) / columns
 //     (MN-major) of B, so per-SM operand traffic drops by a quarter vs the 1-CTA tile
-//     and the smem ring is deeper (6 stages of 32 KiB at BN = 256);
+//     (up to 6 stages of 32 KiB at BN = 256, whatever fits next to the epilogue staging);
 //   * both producers count their TMA bytes on the LEADER's full barrier;
 //   * the leader's single MMA thread issues for the pair and commits with a
 //     cluster multicast to both CTAs' empty / tmem-full barriers;
@@ -16,15 +16,19 @@
 
 namespace spes_dev {
 
-template <int BN>
+template <int BN, int SLOTS = 1>
 struct Gemm2Cfg {
     static constexpr int BNH = BN / 2;
     static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
     static constexpr int B_BYTES = BNH * GEMM_BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int STAGES = (192 * 1024) / STAGE_BYTES;
+    static constexpr int FIXED = 1024 + 256 + GEMM_TABLE_BYTES;
+    static constexpr int EPI_BYTES = epi_stage_bytes(SLOTS);
+    static constexpr int FIT = (GEMM_SMEM_MAX - FIXED - EPI_BYTES) / STAGE_BYTES;
+    static constexpr int STAGES = FIT > 6 ? 6 : FIT;
+    static_assert(STAGES >= 2, "smem ring too shallow");
     static constexpr int TMEM_COLS = 2 * BN;
-    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + GEMM_TABLE_BYTES;
+    static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + FIXED + EPI_BYTES;
 };
 
 template <int BN, class Epi, bool A_MN = false, bool B_MN = false, int DBG_NO_TMA = 0>
@@ -33,7 +37,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                              const __grid_constant__ CUtensorMap mapB,
                              const GemmGroup* __restrict__ groups, int num_groups,
                              const int* __restrict__ total_tiles_ptr, int max_tiles, Epi epi) {
-    using C = Gemm2Cfg<BN>;
+    using C = Gemm2Cfg<BN, Epi::SLOTS>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -45,6 +49,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
     int* s_ts = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(bars) + 256);
     int* s_nkb = s_ts + GEMM_MAX_GROUPS;
+    uint8_t* s_epi = reinterpret_cast<uint8_t*>(bars) + 256 + GEMM_TABLE_BYTES;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -175,6 +180,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int q = warp & 3;
         const int half = (warp - 4) >> 2;
         const int r = q * 32 + lane;
+        EpiOut out{s_epi + (warp - 4) * Epi::SLOTS * EPI_SLOT_BYTES, lane};
         int it = 0;
         for (int t = pair; t < total; t += npairs, ++it) {
             const int gi = find_group(s_ts, num_groups, t);
@@ -183,15 +189,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const int mt = local / g.n_tiles, nt = local % g.n_tiles;
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
+            if (t + npairs < total) {  // warm L2 for the next tile's epilogue inputs
+                const int tn = t + npairs;
+                const GemmGroup& gn = groups[find_group(s_ts, num_groups, tn)];
+                const int ln = tn - gn.tile_start;
+                epi.prefetch(gn, 2 * (ln / gn.n_tiles) + static_cast<int>(rank), ln % gn.n_tiles, r,
+                             half);
+            }
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
-            epi(g, 2 * mt + static_cast<int>(rank), nt, r, taddr, g.k_len == 0, half);
+            epi(g, 2 * mt + static_cast<int>(rank), nt, r, taddr, g.k_len == 0, half, out);
             tc_fence_before();
             __syncwarp();
             // relaxed remote arrive: only the (already waited) TMEM reads need ordering
             if (lane == 0) mbar_arrive_remote(mapa_shared(smem_u32(&tempty[acc]), 0));
         }
+        out.drain();
     }
 
     tc_fence_before();

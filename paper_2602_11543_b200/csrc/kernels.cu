@@ -78,11 +78,15 @@ __global__ void route_scan_k(int32_t* __restrict__ chunk_counts, int nchunks, in
     __shared__ int32_t s_cnt[64];
     __shared__ int32_t s_off[65];
     const int j = threadIdx.x;
+    // stage the per-chunk counts (loads in parallel, not one dependent chain per expert)
+    extern __shared__ int32_t s_cc[];  // [nchunks][M]
+    for (int i = threadIdx.x; i < nchunks * M; i += blockDim.x) s_cc[i] = chunk_counts[i];
+    __syncthreads();
     if (j < M) {
         int32_t run = 0;
         for (int c = 0; c < nchunks; ++c) {
-            int32_t v = chunk_counts[static_cast<int64_t>(c) * M + j];
-            chunk_counts[static_cast<int64_t>(c) * M + j] = run;  // becomes chunk base
+            const int32_t v = s_cc[c * M + j];
+            s_cc[c * M + j] = run;  // becomes chunk base
             run += v;
         }
         s_cnt[j] = run;
@@ -102,6 +106,7 @@ __global__ void route_scan_k(int32_t* __restrict__ chunk_counts, int nchunks, in
         for (int e = 0; e <= M; ++e) pad_off[e] = s_off[e];
     }
     __syncthreads();
+    for (int i = threadIdx.x; i < nchunks * M; i += blockDim.x) chunk_counts[i] = s_cc[i];
     if (threadIdx.x == 0) {
         const int64_t d = gb.d, f = gb.f;
         int32_t ts[6] = {0, 0, 0, 0, 0, 0};
@@ -158,6 +163,12 @@ __global__ void route_scan_k(int32_t* __restrict__ chunk_counts, int nchunks, in
                         G.out0 = goff >= 0 ? gb.grad_expert_base + goff : nullptr;
                         G.out1 = goff >= 0 ? gb.grad_expert_base + goff + d * f : nullptr;
                         G.ldo = f;
+                        if (gb.fused_adam && goff >= 0) {  // params / Adam state of wg (wu = +df)
+                            G.out0 = gb.param_expert_base + e * 3 * d * f;
+                            G.out1 = nullptr;
+                            G.out_row0 = goff;
+                            G.aux = gb.slot0 + e;
+                        }
                         break;
                     default:  // bwd dW2 (owned): HactT[f x R] . dYwT[d x R]^T
                         G.a_row0 = 0;
@@ -170,6 +181,11 @@ __global__ void route_scan_k(int32_t* __restrict__ chunk_counts, int nchunks, in
                         G.out_row0 = 0;
                         G.out0 = goff >= 0 ? gb.grad_expert_base + goff + 2 * d * f : nullptr;
                         G.ldo = d;
+                        if (gb.fused_adam && goff >= 0) {  // params / Adam state of wd
+                            G.out0 = gb.param_expert_base + e * 3 * d * f + 2 * d * f;
+                            G.out_row0 = goff + 2 * d * f;
+                            G.aux = gb.slot0 + e;
+                        }
                         break;
                 }
                 G.tile_start = ts[g];
@@ -237,7 +253,8 @@ void route_plan(const int32_t* topk_idx, const float* topk_w, int64_t T, int M, 
                 int64_t R_cap, const RoutePlan& p, const GroupBases& gb, cudaStream_t s) {
     const int nchunks = static_cast<int>(cdiv(T, ROUTE_CH));
     route_count_k<<<nchunks, ROUTE_CH, 0, s>>>(topk_idx, (int)T, M, k, p.chunk_counts);
-    route_scan_k<<<1, 64, 0, s>>>(p.chunk_counts, nchunks, (int)T, M, k, p.counts, p.pad_off,
+    route_scan_k<<<1, 64, static_cast<size_t>(nchunks) * M * sizeof(int32_t), s>>>(
+        p.chunk_counts, nchunks, (int)T, M, k, p.counts, p.pad_off,
                                   p.lb_coeff, p.groups, p.tiles, gb);
     cudaMemsetAsync(p.row_token, 0xFF, sizeof(int32_t) * R_cap, s);
     cudaMemsetAsync(p.row_w, 0, sizeof(float) * R_cap, s);
@@ -762,9 +779,9 @@ __global__ void __launch_bounds__(256) adamw_k(float* __restrict__ params,
                                                const float* __restrict__ grads,
                                                float* __restrict__ m, float* __restrict__ v,
                                                const AdamSeg* __restrict__ segs, int nseg,
-                                               int64_t total4, float lr, float b1, float b2,
-                                               float omb1, float omb2, float eps, float wd,
-                                               float bc1, float bc2, Shadows sh) {
+                                               int64_t total4, AdamScalars a, Shadows sh,
+                                               const double* __restrict__ loss_total) {
+    if (!loss_ok(loss_total)) return;
     for (int64_t i4 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i4 < total4;
          i4 += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t i = i4 * 4;
@@ -780,15 +797,7 @@ __global__ void __launch_bounds__(256) adamw_k(float* __restrict__ params,
         float* mp = &mm.x;
         float* vp = &vv.x;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const float gi = gp[u];
-            mp[u] = fadd(fmul(b1, mp[u]), fmul(omb1, gi));
-            vp[u] = fadd(fmul(b2, vp[u]), fmul(fmul(omb2, gi), gi));
-            const float mhat = fdiv(mp[u], bc1);
-            const float vhat = fdiv(vp[u], bc2);
-            const float upd = fmul(lr, fadd(fdiv(mhat, fadd(fsqrt(vhat), eps)), fmul(wd, thp[u])));
-            thp[u] = fsub(thp[u], upd);
-        }
+        for (int u = 0; u < 4; ++u) thp[u] = adam_elem(thp[u], gp[u], mp[u], vp[u], a);
         *reinterpret_cast<float4*>(params + p) = th;
         __stcs(reinterpret_cast<float4*>(m + i), mm);
         __stcs(reinterpret_cast<float4*>(v + i), vv);
@@ -797,12 +806,12 @@ __global__ void __launch_bounds__(256) adamw_k(float* __restrict__ params,
 }
 
 void adamw(float* params, const float* grads, float* m, float* v, const AdamSeg* segs, int nseg,
-           int64_t total, float lr, float b1, float b2, float omb1, float omb2, float eps,
-           float wd, float bc1, float bc2, Shadows sh, cudaStream_t s) {
+           int64_t total, const AdamScalars& a, Shadows sh, const double* loss_total,
+           cudaStream_t s) {
     const int64_t total4 = total / 4;
+    if (total4 == 0) return;
     const int blocks = static_cast<int>(std::min<int64_t>(cdiv(total4, 256), 148 * 8));
-    adamw_k<<<blocks, 256, 0, s>>>(params, grads, m, v, segs, nseg, total4, lr, b1, b2, omb1,
-                                   omb2, eps, wd, bc1, bc2, sh);
+    adamw_k<<<blocks, 256, 0, s>>>(params, grads, m, v, segs, nseg, total4, a, sh, loss_total);
     count_launch();
 }
 

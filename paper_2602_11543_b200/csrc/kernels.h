@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "common.cuh"
 #include "grouped_gemm.cuh"
 
 namespace spes_k {
@@ -60,6 +61,11 @@ struct GroupBases {  // output bases written into the group tables
     int64_t d, f;
     int bn_fwd2, bn_dh, bn_dx, bn_dw2;
     int tile_rows;  // 128 (1-CTA tiles) or 256 (cta_group::2 pair tiles); also the row padding
+    // fused optimizer: dW groups address the parameters (param_expert_base + e*3df),
+    // the compact Adam state (grad_off_layer[e]) and shadow slot slot0 + e
+    float* param_expert_base;
+    int32_t slot0;
+    int32_t fused_adam;
 };
 void route_plan(const int32_t* topk_idx, const float* topk_w, int64_t T, int M, int k,
                 int64_t R_cap, const RoutePlan& p, const GroupBases& gb, cudaStream_t s);
@@ -112,10 +118,12 @@ struct Shadows {
     bf16* headB;
     int64_t d, f;
 };
-// MaskedAdamW step over the compact segments; also writes the refreshed bf16 copies.
+// MaskedAdamW step over the first `total` compact scalars; also writes the refreshed
+// bf16 copies. No update when *loss_total is non-finite (loss_total may be null).
+using spes_dev::AdamScalars;
 void adamw(float* params, const float* grads, float* m, float* v, const AdamSeg* segs, int nseg,
-           int64_t total, float lr, float b1, float b2, float omb1, float omb2, float eps,
-           float wd, float bc1, float bc2, Shadows sh, cudaStream_t s);
+           int64_t total, const AdamScalars& a, Shadows sh, const double* loss_total,
+           cudaStream_t s);
 // Rewrite every bf16 copy from the fp32 parameters (after load / sync / merge).
 void refresh_shadows(const float* params, const AdamSeg* segs, int nseg, int64_t total,
                      Shadows sh, cudaStream_t s);
@@ -145,6 +153,21 @@ void gemm_dswiglu(int bn, const CUtensorMap& a, const CUtensorMap& b, const Gemm
                   cudaStream_t s);
 void gemm_grad_w1(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
                   const int32_t* tiles, int max_tiles, cudaStream_t s);
+// dW GEMMs with MaskedAdamW fused into the epilogue (params, m, v and bf16 shadows are
+// updated in place; no gradient is materialized)
+struct AdamEpi {
+    AdamScalars a;
+    float* m;
+    float* v;
+    bf16* w1;
+    bf16* w2;
+    int64_t d, f;
+    const double* loss_total;
+};
+void gemm_adamw_w1(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
+                   const int32_t* tiles, int max_tiles, const AdamEpi& p, cudaStream_t s);
+void gemm_adamw_w2(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
+                   const int32_t* tiles, int max_tiles, const AdamEpi& p, cudaStream_t s);
 void gemm_prepare(int device);
 // cta_group::2 cluster-pair GEMMs (256-row tiles) for the following launches on this thread
 void gemm_set_pair_mode(bool on);

@@ -152,7 +152,9 @@ int run(const char* name, int a_rows, int a_cols, int b_rows, int b_cols,
 }
 
 struct EpiNull {
-    __device__ void operator()(const GemmGroup&, int, int, int, uint32_t, bool, int) const {}
+    static constexpr int SLOTS = 1;
+    __device__ void prefetch(const GemmGroup&, int, int, int, int) const {}
+    __device__ void operator()(const GemmGroup&, int, int, int, uint32_t, bool, int, EpiOut&) const {}
 };
 
 template <int BN, bool AMN, bool BMN, class Epi>

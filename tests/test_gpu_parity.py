@@ -124,11 +124,24 @@ def _check_step(cfg, B, S, owned, seed, renorm=False):
     node = spes.Node(cfg, 0, 1, 0)
     node.set_ownership([owned])
     node.load_params(params)
+    node.set_fused_optimizer(False)  # materialize the gradients for the comparison below
     node.round_begin()
     opt = adamw_cfg(lr=1e-3)
     losses = np.array(node.local_step(tokens, opt))
     g_gpu = node.read_grads()
     p_gpu = node.read_params()
+    # AdamW fused into the dW GEMM epilogues -> identical bits, same losses
+    fused = spes.Node(cfg, 0, 1, 0)
+    fused.set_ownership([owned])
+    fused.load_params(params)
+    fused.set_fused_optimizer(True)
+    fused.round_begin()
+    assert np.array_equal(np.array(fused.local_step(tokens, opt)), losses)
+    assert bitexact(fused.read_params(), p_gpu), "fused optimizer differs from the standalone pass"
+    with pytest.raises(spes.SpesError) as e:
+        fused.read_grads()
+    assert e.value.kind == "logic_error"
+    fused.close()
     T = B * S
     l_ref, g_ref, tr = oracle.forward_backward(cfg, params, tokens, owned, trace=True)
     L, M, k, d = cfg.layers, cfg.experts_total, cfg.experts_active, cfg.hidden
@@ -180,6 +193,26 @@ def _check_step(cfg, B, S, owned, seed, renorm=False):
     psi = oracle.expert_offset(cfg, 0, 0)
     assert c["grad_scalars"] == psi + L * len(owned) * per
     assert c["opt_state_scalars"] == 2 * c["grad_scalars"]
+    node.close()
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_nonfinite_loss_applies_no_update(gpu, fused):
+    """trainer.hpp:166-167: a non-finite loss aborts the round before the optimizer step;
+    with the fused optimizer the device-side guard skips the in-epilogue update too."""
+    cfg = model_cfg(**CFG1)
+    params = oracle.random_params(cfg, 3)
+    tokens = oracle.random_tokens(cfg, 2, 64, 4)
+    params[: cfg.vocab * cfg.hidden] = np.inf  # embedding rows -> non-finite loss
+    node = spes.Node(cfg, 0, 1, 0)
+    node.set_ownership([[0, 1, 2, 3]])
+    node.load_params(params)
+    node.set_fused_optimizer(fused)
+    with pytest.raises(spes.SpesError) as e:
+        node.local_round(tokens, adamw_cfg())
+    assert e.value.kind == "runtime_error"
+    assert bitexact(node.read_params(), params)
+    assert node.counts()["adam_step"] == 0
     node.close()
 
 
