@@ -180,6 +180,7 @@ struct spes_ctx {
     bf16 *dyw = nullptr, *dgu = nullptr;
     float *dot_part = nullptr;
     double* loss_part = nullptr;
+    int32_t* eg_scratch = nullptr;  // embedding-gradient bucketing (2V + 1 + T)
     bf16* normed_bf = nullptr;  // router-normalized h of the current layer (expert GEMM input)
     float *dxp = nullptr, *gw_part = nullptr, *glog = nullptr, *gnormed = nullptr, *gh = nullptr,
           *nr_partial = nullptr;
@@ -374,6 +375,7 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     for (auto& p : c->h) p = A.alloc<float>(Tp * d);
     c->tokens = A.alloc<int32_t>(B * (S + 1));
     c->inputs = A.alloc<int32_t>(Tp);
+    c->eg_scratch = A.alloc<int32_t>(2 * L.V + 1 + Tp);
     c->targets = A.alloc<int32_t>(Tp);
     c->err = A.alloc<int32_t>(1);
     c->layers.assign(L.L, LayerBufs{});
@@ -659,18 +661,18 @@ void forward_backward(spes_ctx* c) {
                                     Y.lse_r, Y.inv_rms, Y.denom, Y.topk_idx, Y.slot_row,
                                     c->gw_part, c->dxp, Y.lb_coeff, T, d, M, k,
                                     c->cfg.renormalize_after_topk, sd.g_lbsum, sd.g_s, c->glog,
-                                    c->gnormed, c->dot_part, c->gh, st);
+                                    c->gnormed, c->dot_part, nullptr, st);
         }
         {
-            PROF("norm_router_grads");
+            PROF("norm_router_grads");  // + rmsnorm backward into gh
             spes_k::norm_router_grads(c->h[l], P + L.off_norm(l), c->gnormed, c->glog, Y.inv_rms, T, d, M,
                                       c->nr_partial, c->grads + L.off_norm(l),
-                                      c->grads + L.off_router(l), st);
+                                      c->grads + L.off_router(l), c->dot_part, c->gh, st);
         }
     }
     {
         PROF("embed_grad");
-        spes_k::embed_grad(c->inputs, c->gh, T, d, V, c->grads + L.off_emb(), st);
+        spes_k::embed_grad(c->inputs, c->gh, T, d, V, c->grads + L.off_emb(), c->eg_scratch, st);
     }
 }
 
@@ -1393,6 +1395,9 @@ spes_status spes_debug_read(spes_ctx* c, const char* name, int32_t layer, void* 
         } else if (n == "slot_row") {
             src = lay().slot_row;
             sz = 4 * T * k;
+        } else if (n == "grad_h0") {  // gradient w.r.t. the embedding output (last step)
+            src = c->gh;
+            sz = 4 * T * d;
         } else if (n == "head_logits") {
             src = c->head_logits;
             sz = 4 * T * L.V;

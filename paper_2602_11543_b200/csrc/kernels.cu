@@ -107,94 +107,110 @@ __global__ void route_scan_k(int32_t* __restrict__ chunk_counts, int nchunks, in
     }
     __syncthreads();
     for (int i = threadIdx.x; i < nchunks * M; i += blockDim.x) chunk_counts[i] = s_cc[i];
-    if (threadIdx.x == 0) {
-        const int64_t d = gb.d, f = gb.f;
-        int32_t ts[6] = {0, 0, 0, 0, 0, 0};
-        for (int e = 0; e < M; ++e) {
-            const int32_t mt = (s_off[e + 1] - s_off[e]) / gb.tile_rows;
-            const int64_t goff = gb.grad_off_layer ? gb.grad_off_layer[e] : -1;
-            for (int g = 0; g < 6; ++g) {
-                GemmGroup G{};
-                G.bk0 = 0;
-                G.out_row0 = s_off[e];
-                G.a_row0 = s_off[e];
-                G.k0 = 0;
-                G.m_tiles = mt;
-                switch (g) {
-                    case 0:  // fwd gate||up: Xp[R x d] . W1_e[d x 2f] (B MN-major, rows e*d..)
-                        G.b_row0 = 0;
-                        G.bk0 = static_cast<int32_t>(e * d);
-                        G.n_tiles = static_cast<int32_t>(2 * f / 256);
-                        G.k_len = static_cast<int32_t>(d);
-                        G.out0 = gb.gu;
-                        G.ldo = 2 * f;
-                        break;
-                    case 1:  // fwd down: Hact[R x f] . Wd_e[f x d] (B MN-major, rows e*f..)
-                        G.b_row0 = 0;
-                        G.bk0 = static_cast<int32_t>(e * f);
-                        G.n_tiles = static_cast<int32_t>(d / gb.bn_fwd2);
-                        G.k_len = static_cast<int32_t>(f);
-                        G.out0 = gb.y;
-                        G.ldo = d;
-                        break;
-                    case 2:  // bwd dH: dYw[R x d] . Wd_e[f x d]^T
-                        G.b_row0 = static_cast<int32_t>(e * f);
-                        G.n_tiles = static_cast<int32_t>(f / gb.bn_dh);
-                        G.k_len = static_cast<int32_t>(d);
-                        G.out0 = gb.dgu;
-                        G.ldo = 2 * f;
-                        break;
-                    case 3:  // bwd dX: dGU[R x 2f] . W1_e[d x 2f]^T
-                        G.b_row0 = static_cast<int32_t>(e * d);
-                        G.n_tiles = static_cast<int32_t>(d / gb.bn_dx);
-                        G.k_len = static_cast<int32_t>(2 * f);
-                        G.out0 = gb.dxp;
-                        G.ldo = d;
-                        break;
-                    case 4:  // bwd dW1 (owned): XpT[d x R] . dGUT[2f x R]^T over this expert's rows
-                        G.a_row0 = 0;
-                        G.b_row0 = 0;
-                        G.k0 = s_off[e];
-                        G.bk0 = s_off[e];
-                        G.k_len = s_off[e + 1] - s_off[e];
-                        G.m_tiles = goff >= 0 ? static_cast<int32_t>(d / gb.tile_rows) : 0;
-                        G.n_tiles = static_cast<int32_t>(2 * f / 256);
-                        G.out_row0 = 0;
-                        G.out0 = goff >= 0 ? gb.grad_expert_base + goff : nullptr;
-                        G.out1 = goff >= 0 ? gb.grad_expert_base + goff + d * f : nullptr;
-                        G.ldo = f;
-                        if (gb.fused_adam && goff >= 0) {  // params / Adam state of wg (wu = +df)
-                            G.out0 = gb.param_expert_base + e * 3 * d * f;
-                            G.out1 = nullptr;
-                            G.out_row0 = goff;
-                            G.aux = gb.slot0 + e;
-                        }
-                        break;
-                    default:  // bwd dW2 (owned): HactT[f x R] . dYwT[d x R]^T
-                        G.a_row0 = 0;
-                        G.b_row0 = 0;
-                        G.k0 = s_off[e];
-                        G.bk0 = s_off[e];
-                        G.k_len = s_off[e + 1] - s_off[e];
-                        G.m_tiles = goff >= 0 ? static_cast<int32_t>(f / gb.tile_rows) : 0;
-                        G.n_tiles = static_cast<int32_t>(d / gb.bn_dw2);
-                        G.out_row0 = 0;
-                        G.out0 = goff >= 0 ? gb.grad_expert_base + goff + 2 * d * f : nullptr;
-                        G.ldo = d;
-                        if (gb.fused_adam && goff >= 0) {  // params / Adam state of wd
-                            G.out0 = gb.param_expert_base + e * 3 * d * f + 2 * d * f;
-                            G.out_row0 = goff + 2 * d * f;
-                            G.aux = gb.slot0 + e;
-                        }
-                        break;
-                }
-                G.tile_start = ts[g];
-                ts[g] += G.m_tiles * G.n_tiles;
-                groups[g * M + e] = G;
+    // groups: thread e builds expert e's six groups; tile_start is a prefix over experts
+    __shared__ int32_t s_nt[6][64];
+    __shared__ GemmGroup s_g[6][64];
+    const int64_t d = gb.d, f = gb.f;
+    if (j < M) {
+        const int e = j;
+        const int32_t mt = (s_off[e + 1] - s_off[e]) / gb.tile_rows;
+        const int64_t goff = gb.grad_off_layer ? gb.grad_off_layer[e] : -1;
+        for (int g = 0; g < 6; ++g) {
+            GemmGroup G{};
+            G.bk0 = 0;
+            G.out_row0 = s_off[e];
+            G.a_row0 = s_off[e];
+            G.k0 = 0;
+            G.m_tiles = mt;
+            switch (g) {
+                case 0:  // fwd gate||up: Xp[R x d] . W1_e[d x 2f] (B MN-major, rows e*d..)
+                    G.b_row0 = 0;
+                    G.bk0 = static_cast<int32_t>(e * d);
+                    G.n_tiles = static_cast<int32_t>(2 * f / 256);
+                    G.k_len = static_cast<int32_t>(d);
+                    G.out0 = gb.gu;
+                    G.ldo = 2 * f;
+                    break;
+                case 1:  // fwd down: Hact[R x f] . Wd_e[f x d] (B MN-major, rows e*f..)
+                    G.b_row0 = 0;
+                    G.bk0 = static_cast<int32_t>(e * f);
+                    G.n_tiles = static_cast<int32_t>(d / gb.bn_fwd2);
+                    G.k_len = static_cast<int32_t>(f);
+                    G.out0 = gb.y;
+                    G.ldo = d;
+                    break;
+                case 2:  // bwd dH: dYw[R x d] . Wd_e[f x d]^T
+                    G.b_row0 = static_cast<int32_t>(e * f);
+                    G.n_tiles = static_cast<int32_t>(f / gb.bn_dh);
+                    G.k_len = static_cast<int32_t>(d);
+                    G.out0 = gb.dgu;
+                    G.ldo = 2 * f;
+                    break;
+                case 3:  // bwd dX: dGU[R x 2f] . W1_e[d x 2f]^T
+                    G.b_row0 = static_cast<int32_t>(e * d);
+                    G.n_tiles = static_cast<int32_t>(d / gb.bn_dx);
+                    G.k_len = static_cast<int32_t>(2 * f);
+                    G.out0 = gb.dxp;
+                    G.ldo = d;
+                    break;
+                case 4:  // bwd dW1 (owned): XpT[d x R] . dGUT[2f x R]^T over this expert's rows
+                    G.a_row0 = 0;
+                    G.b_row0 = 0;
+                    G.k0 = s_off[e];
+                    G.bk0 = s_off[e];
+                    G.k_len = s_off[e + 1] - s_off[e];
+                    G.m_tiles = goff >= 0 ? static_cast<int32_t>(d / gb.tile_rows) : 0;
+                    G.n_tiles = static_cast<int32_t>(2 * f / 256);
+                    G.out_row0 = 0;
+                    G.out0 = goff >= 0 ? gb.grad_expert_base + goff : nullptr;
+                    G.out1 = goff >= 0 ? gb.grad_expert_base + goff + d * f : nullptr;
+                    G.ldo = f;
+                    if (gb.fused_adam && goff >= 0) {  // params / Adam state of wg (wu = +df)
+                        G.out0 = gb.param_expert_base + e * 3 * d * f;
+                        G.out1 = nullptr;
+                        G.out_row0 = goff;
+                        G.aux = gb.slot0 + e;
+                    }
+                    break;
+                default:  // bwd dW2 (owned): HactT[f x R] . dYwT[d x R]^T
+                    G.a_row0 = 0;
+                    G.b_row0 = 0;
+                    G.k0 = s_off[e];
+                    G.bk0 = s_off[e];
+                    G.k_len = s_off[e + 1] - s_off[e];
+                    G.m_tiles = goff >= 0 ? static_cast<int32_t>(f / gb.tile_rows) : 0;
+                    G.n_tiles = static_cast<int32_t>(d / gb.bn_dw2);
+                    G.out_row0 = 0;
+                    G.out0 = goff >= 0 ? gb.grad_expert_base + goff + 2 * d * f : nullptr;
+                    G.ldo = d;
+                    if (gb.fused_adam && goff >= 0) {  // params / Adam state of wd
+                        G.out0 = gb.param_expert_base + e * 3 * d * f + 2 * d * f;
+                        G.out_row0 = goff + 2 * d * f;
+                        G.aux = gb.slot0 + e;
+                    }
+                    break;
             }
+            s_g[g][e] = G;
+            s_nt[g][e] = G.m_tiles * G.n_tiles;
         }
-        for (int g = 0; g < 6; ++g) tiles[g] = ts[g];
     }
+    __syncthreads();
+    if (j < 6) {
+        int32_t acc = 0;
+        for (int e = 0; e < M; ++e) {
+            const int32_t n = s_nt[j][e];
+            s_nt[j][e] = acc;
+            acc += n;
+        }
+        tiles[j] = acc;
+    }
+    __syncthreads();
+    if (j < M)
+        for (int g = 0; g < 6; ++g) {
+            GemmGroup G = s_g[g][j];
+            G.tile_start = s_nt[g][j];
+            groups[g * M + j] = G;
+        }
 }
 
 // Stable scatter: rows of expert j in ascending token order (model.hpp:314-318).
@@ -253,7 +269,11 @@ void route_plan(const int32_t* topk_idx, const float* topk_w, int64_t T, int M, 
                 int64_t R_cap, const RoutePlan& p, const GroupBases& gb, cudaStream_t s) {
     const int nchunks = static_cast<int>(cdiv(T, ROUTE_CH));
     route_count_k<<<nchunks, ROUTE_CH, 0, s>>>(topk_idx, (int)T, M, k, p.chunk_counts);
-    route_scan_k<<<1, 64, static_cast<size_t>(nchunks) * M * sizeof(int32_t), s>>>(
+    const size_t scan_smem = static_cast<size_t>(nchunks) * M * sizeof(int32_t);
+    if (scan_smem > 16 * 1024)
+        cudaFuncSetAttribute(route_scan_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(scan_smem));
+    route_scan_k<<<1, 64, scan_smem, s>>>(
         p.chunk_counts, nchunks, (int)T, M, k, p.counts, p.pad_off,
                                   p.lb_coeff, p.groups, p.tiles, gb);
     cudaMemsetAsync(p.row_token, 0xFF, sizeof(int32_t) * R_cap, s);
@@ -500,7 +520,15 @@ __global__ void losses_finish_k(const double* __restrict__ part, int nb, int L, 
     const int ns = 2 + 2 * L;
     for (int i = threadIdx.x; i < ns; i += blockDim.x) {
         double s = 0.0;
-        for (int b = 0; b < nb; ++b) s += part[static_cast<int64_t>(b) * ns + i];
+        int b = 0;
+        for (; b + 16 <= nb; b += 16) {  // 16 loads in flight, summed in order
+            double v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) v[u] = part[static_cast<int64_t>(b + u) * ns + i];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) s += v[u];
+        }
+        for (; b < nb; ++b) s += part[static_cast<int64_t>(b) * ns + i];
         acc[i] = s;
     }
     __syncthreads();
@@ -581,12 +609,17 @@ void combine_backward(const float* gh, const float* y, const int32_t* row_token,
 // the chunk, lane tx the columns 4tx..4tx+3 of the 128-column slab (float4 streams);
 // each thread keeps 4 columns x 16 experts of router-gradient partials in registers.
 constexpr int NRG_TC = 64;
+constexpr int NG_QT_RMS = 128;  // columns per normed_grad tile = dot partials per token (d / 128)
 constexpr int NRG_EG = 16;
+// With `gh` non-null the z = 0 blocks also apply the rmsnorm backward to their columns
+// (rmsnorm_bwd_k's formula and dot order): h.grad += (gy*g)*inv - coef*x, so h and gnormed
+// are streamed once for both.
 __global__ void __launch_bounds__(256) norm_router_partial_k(
     const float* __restrict__ h, const float* __restrict__ gain, const float* __restrict__ gnormed,
     const float* __restrict__ glog, const float* __restrict__ inv_rms, int T, int d, int M,
-    float* __restrict__ partial) {
+    float* __restrict__ partial, const float* __restrict__ dot_part, float* __restrict__ gh) {
     __shared__ __align__(16) float sgl[64][NRG_EG];
+    __shared__ float scoef[64];
     __shared__ float red[32][4][NRG_EG + 1];
     const int ph = threadIdx.x >> 5, tx = threadIdx.x & 31;
     const int q = blockIdx.x * 128 + 4 * tx;
@@ -609,11 +642,17 @@ __global__ void __launch_bounds__(256) norm_router_partial_k(
             const int tt = i / NRG_EG, e = i % NRG_EG;
             sgl[tt][e] = (tb + tt < t1 && e < ne) ? glog[static_cast<int64_t>(tb + tt) * M + e0 + e] : 0.f;
         }
+        if (gh && do_gain && threadIdx.x < 64 && tb + threadIdx.x < t1) {
+            const int t = tb + threadIdx.x;
+            const int np = d / NG_QT_RMS;
+            float dot2 = 0.f;
+            for (int i = 0; i < np; ++i) dot2 += dot_part[static_cast<int64_t>(t) * np + i];
+            const float inv = inv_rms[t];
+            scoef[threadIdx.x] = fdiv(fmul(fmul(fmul(dot2, inv), inv), inv), static_cast<float>(d));
+        }
         __syncthreads();
-        for (int tt = ph; tt < 64 && tb + tt < t1; tt += 8) {
-            const int64_t o = static_cast<int64_t>(tb + tt) * d + q;
-            const float4 xv = __ldg(reinterpret_cast<const float4*>(h + o));
-            const float iv = __ldg(inv_rms + tb + tt);
+        // two tokens per iteration (tt, tt + 8): both tokens' loads are in flight together
+        auto process = [&](int tt, const float4& xv, const float4& gv, float4 ov, float iv) {
             // normed exactly as the forward formed it: (x * inv) * g
             float4 nv;
             nv.x = fmul(fmul(xv.x, iv), gq.x);
@@ -621,7 +660,14 @@ __global__ void __launch_bounds__(256) norm_router_partial_k(
             nv.z = fmul(fmul(xv.z, iv), gq.z);
             nv.w = fmul(fmul(xv.w, iv), gq.w);
             if (do_gain) {
-                const float4 gv = __ldg(reinterpret_cast<const float4*>(gnormed + o));
+                if (gh) {  // rmsnorm backward (kernels.hpp:130-152)
+                    const float coef = scoef[tt];
+                    ov.x = fadd(ov.x, fsub(fmul(fmul(gv.x, gq.x), iv), fmul(coef, xv.x)));
+                    ov.y = fadd(ov.y, fsub(fmul(fmul(gv.y, gq.y), iv), fmul(coef, xv.y)));
+                    ov.z = fadd(ov.z, fsub(fmul(fmul(gv.z, gq.z), iv), fmul(coef, xv.z)));
+                    ov.w = fadd(ov.w, fsub(fmul(fmul(gv.w, gq.w), iv), fmul(coef, xv.w)));
+                    *reinterpret_cast<float4*>(gh + static_cast<int64_t>(tb + tt) * d + q) = ov;
+                }
                 gg[0] += (gv.x * xv.x) * iv;
                 gg[1] += (gv.y * xv.y) * iv;
                 gg[2] += (gv.z * xv.z) * iv;
@@ -637,6 +683,28 @@ __global__ void __launch_bounds__(256) norm_router_partial_k(
 #pragma unroll
                     for (int u = 0; u < 4; ++u) gr[j][e4 + u] += n[j] * g[u];
             }
+        };
+        const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int tt = ph; tt < 64 && tb + tt < t1; tt += 16) {
+            const int tt2 = tt + 8;
+            const bool v2 = tt2 < 64 && tb + tt2 < t1;
+            const int64_t o1 = static_cast<int64_t>(tb + tt) * d + q;
+            const int64_t o2 = static_cast<int64_t>(tb + (v2 ? tt2 : tt)) * d + q;
+            const float4 x1 = __ldg(reinterpret_cast<const float4*>(h + o1));
+            const float4 x2 = __ldg(reinterpret_cast<const float4*>(h + o2));
+            const float i1 = __ldg(inv_rms + tb + tt);
+            const float i2 = __ldg(inv_rms + tb + (v2 ? tt2 : tt));
+            float4 g1 = z4, g2 = z4, h1 = z4, h2 = z4;
+            if (do_gain) {
+                g1 = __ldg(reinterpret_cast<const float4*>(gnormed + o1));
+                g2 = __ldg(reinterpret_cast<const float4*>(gnormed + o2));
+                if (gh) {
+                    h1 = *reinterpret_cast<const float4*>(gh + o1);
+                    h2 = *reinterpret_cast<const float4*>(gh + o2);
+                }
+            }
+            process(tt, x1, g1, h1, i1);
+            if (v2) process(tt2, x2, g2, h2, i2);
         }
     }
     // combine the 8 warps in warp order (fixed), then write this chunk's partial
@@ -668,8 +736,12 @@ __global__ void norm_router_finish_k(const float* __restrict__ partial, int d, i
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= static_cast<int64_t>(d) * (M + 1)) return;
     const int q = static_cast<int>(i / (M + 1)), c = static_cast<int>(i % (M + 1));
+    float v[NRG_TC];  // all chunk partials in flight, then summed in chunk order
+#pragma unroll
+    for (int ch = 0; ch < NRG_TC; ++ch) v[ch] = partial[(static_cast<int64_t>(ch) * d + q) * (M + 1) + c];
     float s = 0.f;
-    for (int ch = 0; ch < NRG_TC; ++ch) s += partial[(static_cast<int64_t>(ch) * d + q) * (M + 1) + c];
+#pragma unroll
+    for (int ch = 0; ch < NRG_TC; ++ch) s += v[ch];
     if (c == 0)
         g_gain[q] = s;
     else
@@ -678,10 +750,11 @@ __global__ void norm_router_finish_k(const float* __restrict__ partial, int d, i
 
 void norm_router_grads(const float* h, const float* gain, const float* gnormed,
                        const float* glog, const float* inv_rms, int64_t T, int64_t d, int M,
-                       float* partial, float* g_gain, float* g_router, cudaStream_t s) {
+                       float* partial, float* g_gain, float* g_router, const float* dot_part,
+                       float* gh, cudaStream_t s) {
     dim3 grid(static_cast<unsigned>(d / 128), NRG_TC, static_cast<unsigned>((M + NRG_EG - 1) / NRG_EG));
     norm_router_partial_k<<<grid, 256, 0, s>>>(h, gain, gnormed, glog, inv_rms, (int)T, (int)d, M,
-                                               partial);
+                                               partial, dot_part, gh);
     const int64_t n = d * (M + 1);
     norm_router_finish_k<<<static_cast<unsigned>(cdiv(n, 256)), 256, 0, s>>>(partial, (int)d, M,
                                                                             g_gain, g_router);
@@ -728,8 +801,129 @@ __global__ void __launch_bounds__(256) embed_grad_k(const int32_t* __restrict__ 
     if (active) *reinterpret_cast<float4*>(g_emb + static_cast<int64_t>(v) * d + q) = acc;
 }
 
+// Fast path (V <= EG_MAXV): stable bucketing of the token positions by vocabulary id
+// (histogram -> exclusive scan -> per-id ballot compaction in token order), then one
+// thread per (id, 4 columns) sums its bucket's rows in ascending token order with the
+// row loads batched in flight. Same per-column sequential order as embed_grad_k.
+constexpr int EG_MAXV = 1024;
+
+__global__ void vocab_hist_k(const int32_t* __restrict__ inputs, int64_t T,
+                             int32_t* __restrict__ cnt) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t < T) atomicAdd(&cnt[inputs[t]], 1);
+}
+
+__global__ void __launch_bounds__(EG_MAXV) vocab_scan_k(const int32_t* __restrict__ cnt, int V,
+                                                        int32_t* __restrict__ off) {
+    __shared__ int32_t sc[EG_MAXV];
+    const int v = threadIdx.x;
+    sc[v] = v < V ? cnt[v] : 0;
+    __syncthreads();
+    for (int o = 1; o < EG_MAXV; o <<= 1) {  // Hillis-Steele inclusive scan
+        const int32_t x = v >= o ? sc[v - o] : 0;
+        __syncthreads();
+        sc[v] += x;
+        __syncthreads();
+    }
+    if (v < V) off[v + 1] = sc[v];
+    if (v == 0) off[0] = 0;
+}
+
+// block per vocabulary id; each pass covers 2048 tokens (8 contiguous per thread, so the
+// per-thread order and the thread order are both ascending => stable)
+__global__ void __launch_bounds__(256) vocab_bucket_k(const int32_t* __restrict__ inputs,
+                                                      int64_t T, const int32_t* __restrict__ off,
+                                                      int32_t* __restrict__ list) {
+    __shared__ int32_t wsum[8];
+    const int v = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int32_t base = off[v];
+    for (int64_t b0 = 0; b0 < T; b0 += 2048) {
+        const int64_t t0 = b0 + 8 * threadIdx.x;
+        int32_t tok[8];
+        if (t0 + 8 <= T) {
+            const int4 x = __ldg(reinterpret_cast<const int4*>(inputs + t0));
+            const int4 y = __ldg(reinterpret_cast<const int4*>(inputs + t0 + 4));
+            tok[0] = x.x; tok[1] = x.y; tok[2] = x.z; tok[3] = x.w;
+            tok[4] = y.x; tok[5] = y.y; tok[6] = y.z; tok[7] = y.w;
+        } else {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) tok[u] = t0 + u < T ? __ldg(inputs + t0 + u) : -1;
+        }
+        int h = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) h += tok[u] == v;
+        int incl = h;  // inclusive warp scan of the hit counts
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        int pre = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            pre += w < warp ? wsum[w] : 0;
+            tot += wsum[w];
+        }
+        int pos = base + pre + incl - h;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (tok[u] == v) list[pos++] = static_cast<int32_t>(t0 + u);
+        base += tot;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(64) embed_grad_sum_k(const int32_t* __restrict__ off,
+                                                       const int32_t* __restrict__ list,
+                                                       const float* __restrict__ gh0, int64_t d,
+                                                       float* __restrict__ g_emb) {
+    const int v = blockIdx.x;
+    const int64_t q = (static_cast<int64_t>(blockIdx.y) * 64 + threadIdx.x) * 4;
+    if (q >= d) return;
+    const int32_t i0 = off[v], i1 = off[v + 1];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int32_t i = i0;
+    for (; i + 8 <= i1; i += 8) {
+        float4 g[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            g[u] = __ldg(reinterpret_cast<const float4*>(gh0 + static_cast<int64_t>(list[i + u]) * d + q));
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            acc.x = fadd(acc.x, g[u].x);
+            acc.y = fadd(acc.y, g[u].y);
+            acc.z = fadd(acc.z, g[u].z);
+            acc.w = fadd(acc.w, g[u].w);
+        }
+    }
+    for (; i < i1; ++i) {
+        const float4 g = __ldg(reinterpret_cast<const float4*>(gh0 + static_cast<int64_t>(list[i]) * d + q));
+        acc.x = fadd(acc.x, g.x);
+        acc.y = fadd(acc.y, g.y);
+        acc.z = fadd(acc.z, g.z);
+        acc.w = fadd(acc.w, g.w);
+    }
+    *reinterpret_cast<float4*>(g_emb + static_cast<int64_t>(v) * d + q) = acc;
+}
+
 void embed_grad(const int32_t* inputs, const float* gh0, int64_t T, int64_t d, int64_t V,
-                float* g_emb, cudaStream_t s) {
+                float* g_emb, int32_t* scratch, cudaStream_t s) {
+    if (V <= EG_MAXV && scratch) {
+        int32_t* cnt = scratch;           // [V]
+        int32_t* off = scratch + V;       // [V + 1]
+        int32_t* list = scratch + 2 * V + 1;  // [T]
+        cudaMemsetAsync(cnt, 0, sizeof(int32_t) * V, s);
+        vocab_hist_k<<<static_cast<unsigned>(cdiv(T, 256)), 256, 0, s>>>(inputs, T, cnt);
+        vocab_scan_k<<<1, EG_MAXV, 0, s>>>(cnt, static_cast<int>(V), off);
+        vocab_bucket_k<<<static_cast<unsigned>(V), 256, 0, s>>>(inputs, T, off, list);
+        dim3 grid(static_cast<unsigned>(V), static_cast<unsigned>(cdiv(d, 256)));
+        embed_grad_sum_k<<<grid, 64, 0, s>>>(off, list, gh0, d, g_emb);
+        count_launch(4);
+        return;
+    }
     dim3 grid(static_cast<unsigned>(V), static_cast<unsigned>(cdiv(d, 1024)));
     embed_grad_k<<<grid, 256, 0, s>>>(inputs, gh0, T, d, g_emb);
     count_launch();

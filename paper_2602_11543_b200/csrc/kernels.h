@@ -101,13 +101,16 @@ void router_backward(const float* h, const float* gain, const float* router, con
                      const int32_t* topk_idx, const int32_t* slot_row, const float* gw_part,
                      const float* dxp, const float* lb_coeff, int64_t T, int64_t d, int M, int k,
                      int renorm, float g_lbsum, float g_s, float* glog, float* gnormed,
-                     float* dot_part, float* gh, cudaStream_t s);
+                     float* dot_part, float* gh, cudaStream_t s);  // gh null: rmsnorm bwd deferred
 // normed is recomputed exactly from h, inv_rms and the gain (not stored in forward)
+// gh non-null: also applies the rmsnorm backward (router_backward then skips it)
 void norm_router_grads(const float* h, const float* gain, const float* gnormed,
                        const float* glog, const float* inv_rms, int64_t T, int64_t d, int M,
-                       float* partial, float* g_gain, float* g_router, cudaStream_t s);
+                       float* partial, float* g_gain, float* g_router, const float* dot_part,
+                       float* gh, cudaStream_t s);
+// scratch: 2V + 1 + T int32 (fast path for V <= 1024; nullptr => generic kernel)
 void embed_grad(const int32_t* inputs, const float* gh0, int64_t T, int64_t d, int64_t V,
-                float* g_emb, cudaStream_t s);
+                float* g_emb, int32_t* scratch, cudaStream_t s);
 
 // ---- optimizer / shadows ----
 // bf16 GEMM operand copies written by the optimizer / refresh: W1 [slots][d][2f]

@@ -211,8 +211,11 @@ void router_backward(const float* h, const float* gain, const float* router, con
     else
         SPES_RB(64);
 #undef SPES_RB
-    rmsnorm_bwd_k<<<g3, 256, 0, s>>>(h, gain, inv_rms, gnormed, dot_part, (int)T, (int)d, gh);
-    count_launch(3);
+    if (gh) {
+        rmsnorm_bwd_k<<<g3, 256, 0, s>>>(h, gain, inv_rms, gnormed, dot_part, (int)T, (int)d, gh);
+        count_launch();
+    }
+    count_launch(2);
 }
 
 }  // namespace spes_k

@@ -172,7 +172,14 @@ def _check_step(cfg, B, S, owned, seed, renorm=False):
             assert not gg.any(), f"frozen block {b0} got a gradient"
             continue
         assert rel_err(gg, gr) < GRAD_RTOL, f"block at {b0}: rel err {rel_err(gg, gr):.3e}"
-    # embedding gradient given identical upstream: exercised in test_embed_grad_exact
+    # embedding gradient == sequential scatter-add of the device's own grad_h0 rows in
+    # token order (graph.hpp:220-229): bit-exact given identical upstream
+    gh0 = node.debug("grad_h0", 0, np.float32, (T, d), T * d)
+    inputs = tokens[:, :-1].reshape(-1)
+    g_emb = np.zeros((cfg.vocab, d), np.float32)
+    for t in range(T):
+        g_emb[inputs[t]] += gh0[t]  # float32 adds, ascending t
+    assert bitexact(g_gpu[: cfg.vocab * d].reshape(cfg.vocab, d), g_emb), "embedding gradient"
     # optimizer: GPU params == oracle AdamW applied to the GPU's own gradients (bit-exact)
     mask = oracle.trainable_mask(cfg, owned)
     p_chk = params.copy()
