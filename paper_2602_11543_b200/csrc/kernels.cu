@@ -969,6 +969,10 @@ __device__ __forceinline__ void write_shadow4(const AdamSeg& sg, int64_t o, cons
     *reinterpret_cast<uint2*>(dst) = pk;
 }
 
+// Each thread owns ADAM_U consecutive float4 groups per pass (all loads in flight
+// before any update); segments are never split inside a group because every segment
+// length is a multiple of 4.
+constexpr int ADAM_U = 2;
 __global__ void __launch_bounds__(256) adamw_k(float* __restrict__ params,
                                                const float* __restrict__ grads,
                                                float* __restrict__ m, float* __restrict__ v,
@@ -976,26 +980,38 @@ __global__ void __launch_bounds__(256) adamw_k(float* __restrict__ params,
                                                int64_t total4, AdamScalars a, Shadows sh,
                                                const double* __restrict__ loss_total) {
     if (!loss_ok(loss_total)) return;
-    for (int64_t i4 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i4 < total4;
-         i4 += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t i = i4 * 4;
-        const AdamSeg sg = segs[find_seg(segs, nseg, i)];
-        const int64_t o = i - sg.comp_off;
-        const int64_t p = sg.param_off + o;
-        float4 th = *reinterpret_cast<float4*>(params + p);
-        const float4 g = __ldcs(reinterpret_cast<const float4*>(grads + i));
-        float4 mm = __ldcs(reinterpret_cast<const float4*>(m + i));
-        float4 vv = __ldcs(reinterpret_cast<const float4*>(v + i));
-        float* thp = &th.x;
-        const float* gp = &g.x;
-        float* mp = &mm.x;
-        float* vp = &vv.x;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * ADAM_U;
+    for (int64_t base = (static_cast<int64_t>(blockIdx.x) * blockDim.x) * ADAM_U + threadIdx.x;
+         base < total4; base += stride) {
+        float4 th[ADAM_U], g[ADAM_U], mm[ADAM_U], vv[ADAM_U];
+        AdamSeg sg[ADAM_U];
+        int64_t idx[ADAM_U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) thp[u] = adam_elem(thp[u], gp[u], mp[u], vp[u], a);
-        *reinterpret_cast<float4*>(params + p) = th;
-        __stcs(reinterpret_cast<float4*>(m + i), mm);
-        __stcs(reinterpret_cast<float4*>(v + i), vv);
-        write_shadow4(sg, o, th, sh);
+        for (int u = 0; u < ADAM_U; ++u) {
+            idx[u] = base + static_cast<int64_t>(u) * blockDim.x;  // coalesced per u
+            if (idx[u] < total4) {
+                const int64_t i = idx[u] * 4;
+                sg[u] = segs[find_seg(segs, nseg, i)];
+                th[u] = *reinterpret_cast<const float4*>(params + sg[u].param_off + (i - sg[u].comp_off));
+                g[u] = __ldcs(reinterpret_cast<const float4*>(grads + i));
+                mm[u] = __ldcs(reinterpret_cast<const float4*>(m + i));
+                vv[u] = __ldcs(reinterpret_cast<const float4*>(v + i));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < ADAM_U; ++u) {
+            if (idx[u] >= total4) continue;
+            const int64_t i = idx[u] * 4;
+            const int64_t o = i - sg[u].comp_off;
+            th[u].x = adam_elem(th[u].x, g[u].x, mm[u].x, vv[u].x, a);
+            th[u].y = adam_elem(th[u].y, g[u].y, mm[u].y, vv[u].y, a);
+            th[u].z = adam_elem(th[u].z, g[u].z, mm[u].z, vv[u].z, a);
+            th[u].w = adam_elem(th[u].w, g[u].w, mm[u].w, vv[u].w, a);
+            *reinterpret_cast<float4*>(params + sg[u].param_off + o) = th[u];
+            __stcs(reinterpret_cast<float4*>(m + i), mm[u]);
+            __stcs(reinterpret_cast<float4*>(v + i), vv[u]);
+            write_shadow4(sg[u], o, th[u], sh);
+        }
     }
 }
 
@@ -1004,7 +1020,7 @@ void adamw(float* params, const float* grads, float* m, float* v, const AdamSeg*
            cudaStream_t s) {
     const int64_t total4 = total / 4;
     if (total4 == 0) return;
-    const int blocks = static_cast<int>(std::min<int64_t>(cdiv(total4, 256), 148 * 8));
+    const int blocks = static_cast<int>(std::min<int64_t>(cdiv(total4, 256 * ADAM_U), 148 * 8));
     adamw_k<<<blocks, 256, 0, s>>>(params, grads, m, v, segs, nseg, total4, a, sh, loss_total);
     count_launch();
 }
