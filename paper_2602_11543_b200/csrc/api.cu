@@ -156,6 +156,15 @@ struct spes_ctx {
     // epilogue warps that fit next to the MMA ring, so it does not beat the separate pass yet.
     bool fused_opt = false;
     spes_k::AdamScalars cur_adam{};  // this step's AdamW scalars (set before backward)
+    spes_k::AdamScalars* d_adam = nullptr;  // device copy read by the optimizer kernels
+    // the local step as one CUDA graph per (T, optimizer placement): the launch sequence
+    // is host-static (group tables and tile counts live on the device), so it is captured
+    // on the second step of a shape and replayed; profiling runs eagerly
+    bool use_graph = true;
+    cudaGraphExec_t step_graph = nullptr;
+    int64_t graph_T = -1, graph_seen_T = -1;
+    int graph_fused = -1;
+    int64_t graph_launches = 0;
     std::vector<spes_k::AdamSeg> segs_host;
 
     DevMem persistent;  // params, shadows, optimizer state
@@ -225,6 +234,12 @@ struct spes_ctx {
 namespace {
 
 void set_counter(spes_ctx* c) { spes_k::g_launch_counter = &c->launches; }
+
+void drop_graph(spes_ctx* c) {
+    if (c->step_graph) cudaGraphExecDestroy(c->step_graph);
+    c->step_graph = nullptr;
+    c->graph_T = c->graph_seen_T = -1;
+}
 
 // Sync plan: the primary owner of expert e computes its owner-set
 // mean and distributes it. Primary = e / (M/N) when N | M and that node owns e (the
@@ -360,6 +375,7 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     c->S = S;
     if (T == c->T && c->T_pad > 0) return;
     const Layout& L = c->lay;
+    drop_graph(c);  // buffers move
     c->act.release();
     c->T = T;
     // cta_group::2 pair tiles (256 rows) whenever every GEMM M dimension allows it
@@ -436,6 +452,7 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     c->diff = A.alloc<float>(Tp);
     c->lse_head = A.alloc<float>(Tp);
     c->d_losses = A.alloc<double>(8);
+    c->d_adam = A.alloc<spes_k::AdamScalars>(1);
     // head dW = hL^T dlogits has only (d/128)*(V/BN) output tiles: split K (tokens)
     // so the grid covers the SMs; partials are summed in split order (deterministic).
     {
@@ -631,7 +648,7 @@ void forward_backward(spes_ctx* c) {
         if (c->max_tiles[4] > 0 && c->fused_opt) {
             // owned experts: dW and MaskedAdamW in one pass (no gradient materialized)
             const spes_k::Shadows sh = shadows_of(c);
-            const spes_k::AdamEpi ae{c->cur_adam, c->m, c->v, sh.w1, sh.w2, d, f, c->d_losses};
+            const spes_k::AdamEpi ae{c->d_adam, c->m, c->v, sh.w1, sh.w2, d, f, c->d_losses};
             {
                 PROF("gemm_bwd_dw_gate_up+adamw");
                 spes_k::gemm_adamw_w1(Y.a_xp_mn, c->b_dgu_mn, Y.groups + 4 * M, M, Y.tiles + 4,
@@ -688,6 +705,9 @@ void optimizer_begin(spes_ctx* c, const spes_adamw_cfg* o) {
     c->cur_adam = spes_k::AdamScalars{static_cast<float>(o->lr), b1, b2, omb1, omb2,
                                       static_cast<float>(o->eps),
                                       static_cast<float>(o->weight_decay), bc1, bc2};
+    ck(cudaMemcpyAsync(c->d_adam, &c->cur_adam, sizeof(c->cur_adam), cudaMemcpyHostToDevice,
+                       c->stream),
+       "adam scalars");
 }
 
 // The rest of the step: psi (and, unfused, the owned experts) after the backward.
@@ -695,7 +715,7 @@ void optimizer_finish(spes_ctx* c) {
     PROF("adamw");
     const int64_t n = c->fused_opt ? c->lay.psi() : c->G;  // psi is the compact prefix
     spes_k::adamw(c->params, c->grads, c->m, c->v, c->segs,
-                  static_cast<int>(c->segs_host.size()), n, c->cur_adam, shadows_of(c),
+                  static_cast<int>(c->segs_host.size()), n, c->d_adam, shadows_of(c),
                   c->d_losses, c->stream);
 }
 
@@ -742,8 +762,32 @@ void check_err_flag(spes_ctx* c) {
 void local_step_impl(spes_ctx* c, int64_t B, int64_t S, const spes_adamw_cfg* opt,
                      spes_losses* losses) {
     optimizer_begin(c, opt);
-    forward_backward(c);  // fused: owned experts updated here unless the loss is non-finite
-    optimizer_finish(c);  // psi; a device-side check skips it after a non-finite loss
+    // forward + backward (fused: owned experts updated unless the loss is non-finite) and
+    // the optimizer pass (device-side non-finite check), eagerly or as a replayed graph
+    const bool graph = c->use_graph && !c->prof;
+    if (graph && c->step_graph && c->graph_T == c->T && c->graph_fused == (c->fused_opt ? 1 : 0)) {
+        ck(cudaGraphLaunch(c->step_graph, c->stream), "graph launch");
+        c->launches += c->graph_launches;
+    } else if (graph && c->graph_seen_T == c->T) {  // second step of this shape: capture
+        drop_graph(c);
+        const int64_t before = c->launches;
+        ck(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "capture");
+        forward_backward(c);
+        optimizer_finish(c);
+        cudaGraph_t g = nullptr;
+        ck(cudaStreamEndCapture(c->stream, &g), "end capture");
+        ck(cudaGraphInstantiate(&c->step_graph, g, 0), "graph instantiate");
+        cudaGraphDestroy(g);
+        c->graph_launches = c->launches - before;
+        c->launches = before + c->graph_launches;
+        c->graph_T = c->T;
+        c->graph_fused = c->fused_opt ? 1 : 0;
+        ck(cudaGraphLaunch(c->step_graph, c->stream), "graph launch");
+    } else {
+        forward_backward(c);
+        optimizer_finish(c);
+        c->graph_seen_T = c->T;
+    }
     if (losses) {
         read_losses(c, losses);
         if (!std::isfinite(losses->total)) {  // no update was applied; caller reports it
@@ -921,6 +965,7 @@ spes_status spes_create(const spes_model_cfg* cfg, int32_t node, int32_t n_nodes
 }
 
 void spes_destroy(spes_ctx* c) {
+    if (c) drop_graph(c);
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
@@ -1544,7 +1589,9 @@ spes_status spes_kernel_adamw(float* theta, const float* grad, float* m, float* 
         const spes_k::AdamScalars a{static_cast<float>(o->lr), b1, b2, one - b1, one - b2,
                                     static_cast<float>(o->eps),
                                     static_cast<float>(o->weight_decay), bc1, bc2};
-        spes_k::adamw(dt, dgr, dm, dv, ds, 1, n, a, spes_k::Shadows{nullptr, nullptr, nullptr, 0, 0},
+        auto* da = D.alloc<spes_k::AdamScalars>(1);
+        ck(cudaMemcpy(da, &a, sizeof(a), cudaMemcpyHostToDevice), "H2D");
+        spes_k::adamw(dt, dgr, dm, dv, ds, 1, n, da, spes_k::Shadows{nullptr, nullptr, nullptr, 0, 0},
                       nullptr, 0);
         ck(cudaDeviceSynchronize(), "adamw kernel");
         ck(cudaMemcpy(theta, dt, 4 * n, cudaMemcpyDeviceToHost), "D2H");

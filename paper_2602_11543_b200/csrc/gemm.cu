@@ -192,7 +192,7 @@ __device__ __forceinline__ void adam_piece(const EpiOut& out, const AdamEpi& p, 
     out.rows_load_async<8>(2, p.v + comp);
     out.rows_wait();
     float th[32];
-    adam_rows32(out, gr, p.a, th);
+    adam_rows32(out, gr, *p.a, th);
     out.rows_store<8>(0, th_g);
     out.rows_store<8>(1, p.m + comp);
     out.rows_store<8>(2, p.v + comp);

@@ -417,6 +417,9 @@ void combine_forward(const float* h, const float* y, const int32_t* slot_row,
 // ============================ head: CE + z ============================
 // Warp per token. lse, picked (graph.hpp:410-423); d logits following the
 // reverse tape: gather_cols then logsumexp backward (graph.hpp:192-204, 274-281).
+// Warp per token; the row is read once into registers (HC_MAXJ values per lane) and each
+// exponential is evaluated once (V <= 32 * HC_MAXJ; larger V takes the streaming path).
+constexpr int HC_MAXJ = 16;
 __global__ void head_ce_k(const float* __restrict__ logits, const int32_t* __restrict__ targets,
                           int64_t T, int64_t T_pad, int64_t V, int variant, float g_s2,
                           float g_ssum, float* __restrict__ dlogits, float* __restrict__ diff,
@@ -430,28 +433,62 @@ __global__ void head_ce_k(const float* __restrict__ logits, const int32_t* __res
         return;
     }
     const float* row = logits + t * V;
+    auto ex = [&](float z) {
+        return variant ? spes_expf::expf_glibc<1>(z) : spes_expf::expf_glibc<0>(z);
+    };
+    const int32_t tgt = targets[t];
+    if (V <= 32 * HC_MAXJ) {
+        float x[HC_MAXJ];
+        float mx = -INFINITY;
+#pragma unroll
+        for (int u = 0; u < HC_MAXJ; ++u) {
+            const int64_t j = lane + 32 * u;
+            x[u] = j < V ? row[j] : -INFINITY;
+            mx = fmaxf(mx, x[u]);
+        }
+        mx = warp_max(mx);
+        float sum = 0.f;
+#pragma unroll
+        for (int u = 0; u < HC_MAXJ; ++u) {
+            const int64_t j = lane + 32 * u;
+            x[u] = j < V ? ex(fsub(x[u], mx)) : 0.f;
+            sum += x[u];
+        }
+        sum = warp_sum(sum);
+        const float lse = mx + logf(sum);
+        if (lane == 0) {
+            diff[t] = lse + row[tgt] * -1.f;
+            lse_out[t] = lse;
+        }
+        // lse.grad = (0 + g_s2*lse) + g_s2*lse + g_ssum (z-loss mul, then ce add)
+        const float glse = fadd(fadd(fadd(0.f, fmul(g_s2, lse)), fmul(g_s2, lse)), g_ssum);
+        const float isum = 1.f / sum;
+#pragma unroll
+        for (int u = 0; u < HC_MAXJ; ++u) {
+            const int64_t j = lane + 32 * u;
+            if (j < V) {
+                const float base = (j == tgt) ? -1.f * g_ssum : 0.f;
+                drow[j] = fadd(base, fmul(glse, x[u] * isum));
+            }
+        }
+        return;
+    }
     float mx = -INFINITY;
     for (int64_t j = lane; j < V; j += 32) mx = fmaxf(mx, row[j]);
     mx = warp_max(mx);
     float sum = 0.f;
-    for (int64_t j = lane; j < V; j += 32) {
-        const float z = fsub(row[j], mx);
-        sum += variant ? spes_expf::expf_glibc<1>(z) : spes_expf::expf_glibc<0>(z);
-    }
+    for (int64_t j = lane; j < V; j += 32) sum += ex(fsub(row[j], mx));
     sum = warp_sum(sum);
     const float lse = mx + logf(sum);
-    const int32_t tgt = targets[t];
     const float picked = row[tgt];
     if (lane == 0) {
         diff[t] = lse + picked * -1.f;
         lse_out[t] = lse;
     }
-    // lse.grad = (0 + g_s2*lse) + g_s2*lse + g_ssum (z-loss mul, then ce add)
-    float glse = fadd(fadd(fadd(0.f, fmul(g_s2, lse)), fmul(g_s2, lse)), g_ssum);
+    const float glse = fadd(fadd(fadd(0.f, fmul(g_s2, lse)), fmul(g_s2, lse)), g_ssum);
     const float isum = 1.f / sum;
     for (int64_t j = lane; j < V; j += 32) {
-        const float z = fsub(row[j], mx);
-        const float p = (variant ? spes_expf::expf_glibc<1>(z) : spes_expf::expf_glibc<0>(z)) * isum;
+        const float p = ex(fsub(row[j], mx)) * isum;
         const float base = (j == tgt) ? -1.f * g_ssum : 0.f;
         drow[j] = fadd(base, fmul(glse, p));
     }
@@ -977,9 +1014,10 @@ __global__ void __launch_bounds__(256) adamw_k(float* __restrict__ params,
                                                const float* __restrict__ grads,
                                                float* __restrict__ m, float* __restrict__ v,
                                                const AdamSeg* __restrict__ segs, int nseg,
-                                               int64_t total4, AdamScalars a, Shadows sh,
-                                               const double* __restrict__ loss_total) {
+                                               int64_t total4, const AdamScalars* __restrict__ ap,
+                                               Shadows sh, const double* __restrict__ loss_total) {
     if (!loss_ok(loss_total)) return;
+    const AdamScalars a = *ap;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * ADAM_U;
     for (int64_t base = (static_cast<int64_t>(blockIdx.x) * blockDim.x) * ADAM_U + threadIdx.x;
          base < total4; base += stride) {
@@ -1016,7 +1054,7 @@ __global__ void __launch_bounds__(256) adamw_k(float* __restrict__ params,
 }
 
 void adamw(float* params, const float* grads, float* m, float* v, const AdamSeg* segs, int nseg,
-           int64_t total, const AdamScalars& a, Shadows sh, const double* loss_total,
+           int64_t total, const AdamScalars* a, Shadows sh, const double* loss_total,
            cudaStream_t s) {
     const int64_t total4 = total / 4;
     if (total4 == 0) return;

@@ -125,8 +125,8 @@ struct Shadows {
 // bf16 copies. No update when *loss_total is non-finite (loss_total may be null).
 using spes_dev::AdamScalars;
 void adamw(float* params, const float* grads, float* m, float* v, const AdamSeg* segs, int nseg,
-           int64_t total, const AdamScalars& a, Shadows sh, const double* loss_total,
-           cudaStream_t s);
+           int64_t total, const AdamScalars* a, Shadows sh, const double* loss_total,
+           cudaStream_t s);  // a: device memory (graph-replayable)
 // Rewrite every bf16 copy from the fp32 parameters (after load / sync / merge).
 void refresh_shadows(const float* params, const AdamSeg* segs, int nseg, int64_t total,
                      Shadows sh, cudaStream_t s);
@@ -159,7 +159,7 @@ void gemm_grad_w1(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g
 // dW GEMMs with MaskedAdamW fused into the epilogue (params, m, v and bf16 shadows are
 // updated in place; no gradient is materialized)
 struct AdamEpi {
-    AdamScalars a;
+    const AdamScalars* a;  // device memory
     float* m;
     float* v;
     bf16* w1;
