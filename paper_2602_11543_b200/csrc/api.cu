@@ -446,8 +446,8 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     c->gh = A.alloc<float>(Tp * d);
     c->nr_partial = A.alloc<float>(64 * d * (M + 1));  // NRG_TC token chunks
     c->hL = A.alloc<bf16>(Tp * d);
+    ck(cudaMemsetAsync(c->hL, 0, sizeof(bf16) * Tp * d, c->stream), "hL");  // padding rows
     c->head_logits = A.alloc<float>(Tp * V);
-    c->dlogits = A.alloc<float>(Tp * V);
     c->dlog_bf = A.alloc<bf16>(Tp * V);
     c->diff = A.alloc<float>(Tp);
     c->lse_head = A.alloc<float>(Tp);
@@ -595,12 +595,11 @@ void forward_backward(spes_ctx* c) {
         {
             PROF("combine_fwd");
             spes_k::combine_forward(c->h[l], Y.y, Y.slot_row, Y.topk_idx, Y.topk_w, T, d, k,
-                                    c->h[l + 1], st);
+                                    c->h[l + 1], l + 1 == L.L ? c->hL : nullptr, st);
         }
     }
     {
         PROF("head_fwd");
-        spes_k::gather_rows_bf16(c->h[L.L], d, nullptr, nullptr, Tp, d, c->hL, nullptr, Tp, st);
         spes_k::gemm_store_f32(bn_for(V), spes_k::GemmMajor::KMN, c->a_hL, c->b_headB_mn,
                                c->head_groups + 0, 1,
                                c->head_tiles + 0, c->head_max[0], st);
@@ -608,7 +607,7 @@ void forward_backward(spes_ctx* c) {
     {
         PROF("head_ce_losses");
         spes_k::head_ce(c->head_logits, c->targets, T, Tp, V, c->expf_variant, sd.g_s2, sd.g_ssum,
-                        c->dlogits, c->diff, c->lse_head, st);
+                        c->dlog_bf, c->diff, c->lse_head, st);
         spes_k::losses_reduce(c->diff, c->lse_head, c->lse_all, c->probs_all, c->coeff_all, T, Tp,
                               L.L, M, sd.inv_T, sd.inv_L, sd.c_ce, sd.c_lb, sd.c_mz, sd.c_z,
                               c->loss_part, c->d_losses, st);
@@ -616,7 +615,6 @@ void forward_backward(spes_ctx* c) {
     // ---- backward ----
     {
         PROF("head_bwd");
-        spes_k::gather_rows_bf16(c->dlogits, V, nullptr, nullptr, Tp, V, c->dlog_bf, nullptr, Tp, st);
         spes_k::gemm_store_f32(bn_for(d), spes_k::GemmMajor::KK, c->a_dlog, c->b_headB,
                                c->head_groups + 1, 1,
                                c->head_tiles + 1, c->head_max[1], st);

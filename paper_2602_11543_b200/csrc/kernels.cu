@@ -374,7 +374,8 @@ void permute_rows_bf16(const bf16* src, int64_t cols, const int32_t* row_map,
 // (model.hpp:330-338: rowwise_mul, scatter_rows into zeros, add chain, residual add)
 __global__ void combine_fwd_k(const float* __restrict__ h, const float* __restrict__ y,
                               const int32_t* __restrict__ slot_row, const float* __restrict__ w,
-                              int64_t d, int k, float* __restrict__ h_next) {
+                              int64_t d, int k, float* __restrict__ h_next,
+                              bf16* __restrict__ h_next_bf) {
     const int64_t t = blockIdx.x;
     int32_t rows[8];
     float ws[8];
@@ -399,18 +400,26 @@ __global__ void combine_fwd_k(const float* __restrict__ h, const float* __restri
             acc.w = fadd(acc.w, fadd(0.f, fmul(v.w, ws[s])));
         }
         const float4 hv = __ldg(reinterpret_cast<const float4*>(h + t * d + q));
-        *reinterpret_cast<float4*>(h_next + t * d + q) =
-            make_float4(fadd(hv.x, acc.x), fadd(hv.y, acc.y), fadd(hv.z, acc.z), fadd(hv.w, acc.w));
+        const float4 o = make_float4(fadd(hv.x, acc.x), fadd(hv.y, acc.y), fadd(hv.z, acc.z),
+                                     fadd(hv.w, acc.w));
+        *reinterpret_cast<float4*>(h_next + t * d + q) = o;
+        if (h_next_bf) {  // last layer: the head GEMM's bf16 operand, no separate pass
+            __nv_bfloat162 a = __floats2bfloat162_rn(o.x, o.y), b = __floats2bfloat162_rn(o.z, o.w);
+            uint2 pk;
+            pk.x = *reinterpret_cast<uint32_t*>(&a);
+            pk.y = *reinterpret_cast<uint32_t*>(&b);
+            *reinterpret_cast<uint2*>(h_next_bf + t * d + q) = pk;
+        }
     }
 }
 
 void combine_forward(const float* h, const float* y, const int32_t* slot_row,
                      const int32_t* topk_idx, const float* topk_w, int64_t T, int64_t d, int k,
-                     float* h_next, cudaStream_t s) {
+                     float* h_next, bf16* h_next_bf, cudaStream_t s) {
     (void)topk_idx;
     const int threads = d >= 1024 ? 256 : static_cast<int>(d / 4);
     combine_fwd_k<<<static_cast<unsigned>(T), threads, 0, s>>>(h, y, slot_row, topk_w, d, k,
-                                                               h_next);
+                                                               h_next, h_next_bf);
     count_launch();
 }
 
@@ -422,14 +431,14 @@ void combine_forward(const float* h, const float* y, const int32_t* slot_row,
 constexpr int HC_MAXJ = 16;
 __global__ void head_ce_k(const float* __restrict__ logits, const int32_t* __restrict__ targets,
                           int64_t T, int64_t T_pad, int64_t V, int variant, float g_s2,
-                          float g_ssum, float* __restrict__ dlogits, float* __restrict__ diff,
+                          float g_ssum, bf16* __restrict__ dlogits, float* __restrict__ diff,
                           float* __restrict__ lse_out) {
     const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (t >= T_pad) return;
-    float* drow = dlogits + t * V;
+    bf16* drow = dlogits + t * V;  // the head backward GEMMs' bf16 operand, written directly
     if (t >= T) {
-        for (int64_t j = lane; j < V; j += 32) drow[j] = 0.f;
+        for (int64_t j = lane; j < V; j += 32) drow[j] = __float2bfloat16_rn(0.f);
         return;
     }
     const float* row = logits + t * V;
@@ -468,7 +477,7 @@ __global__ void head_ce_k(const float* __restrict__ logits, const int32_t* __res
             const int64_t j = lane + 32 * u;
             if (j < V) {
                 const float base = (j == tgt) ? -1.f * g_ssum : 0.f;
-                drow[j] = fadd(base, fmul(glse, x[u] * isum));
+                drow[j] = __float2bfloat16_rn(fadd(base, fmul(glse, x[u] * isum)));
             }
         }
         return;
@@ -490,12 +499,12 @@ __global__ void head_ce_k(const float* __restrict__ logits, const int32_t* __res
     for (int64_t j = lane; j < V; j += 32) {
         const float p = ex(fsub(row[j], mx)) * isum;
         const float base = (j == tgt) ? -1.f * g_ssum : 0.f;
-        drow[j] = fadd(base, fmul(glse, p));
+        drow[j] = __float2bfloat16_rn(fadd(base, fmul(glse, p)));
     }
 }
 
 void head_ce(const float* logits, const int32_t* targets, int64_t T, int64_t T_pad, int64_t V,
-             int variant, float g_s2, float g_ssum, float* dlogits, float* diff, float* lse,
+             int variant, float g_s2, float g_ssum, bf16* dlogits, float* diff, float* lse,
              cudaStream_t s) {
     const int64_t threads = T_pad * 32;
     head_ce_k<<<static_cast<unsigned>(cdiv(threads, 256)), 256, 0, s>>>(
@@ -988,15 +997,17 @@ __device__ __forceinline__ void write_shadow4(const AdamSeg& sg, int64_t o, cons
     if (sg.kind == 2) {
         dst = sh.headB + o;
     } else {
-        const int64_t df = sh.d * sh.f;
-        if (o < 2 * df) {  // wg / wu: [d x f] -> W1 [d x 2f] interleaved
-            const bool up = o >= df;
-            const int64_t oo = up ? o - df : o;
-            const int64_t q = oo / sh.f, x = oo % sh.f;
-            dst = sh.w1 + static_cast<int64_t>(sg.slot) * 2 * df + q * 2 * sh.f +
+        // per-expert offsets fit in 32 bits (d*f < 2^31): 32-bit index math
+        const uint32_t df = static_cast<uint32_t>(sh.d * sh.f), f = static_cast<uint32_t>(sh.f);
+        const uint32_t o32 = static_cast<uint32_t>(o);
+        if (o32 < 2 * df) {  // wg / wu: [d x f] -> W1 [d x 2f] interleaved
+            const bool up = o32 >= df;
+            const uint32_t oo = up ? o32 - df : o32;
+            const uint32_t q = oo / f, x = oo - q * f;
+            dst = sh.w1 + static_cast<int64_t>(sg.slot) * 2 * df + static_cast<int64_t>(q) * 2 * f +
                   (up ? il_up(x) : il_gate(x));
         } else {  // wd: [f x d] -> W2 as is
-            dst = sh.w2 + static_cast<int64_t>(sg.slot) * df + (o - 2 * df);
+            dst = sh.w2 + static_cast<int64_t>(sg.slot) * df + (o32 - 2 * df);
         }
     }
     __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
@@ -1010,14 +1021,22 @@ __device__ __forceinline__ void write_shadow4(const AdamSeg& sg, int64_t o, cons
 // before any update); segments are never split inside a group because every segment
 // length is a multiple of 4.
 constexpr int ADAM_U = 2;
+constexpr int ADAM_MAX_SEGS = 256;  // segment table in smem up to this size
 __global__ void __launch_bounds__(256) adamw_k(float* __restrict__ params,
                                                const float* __restrict__ grads,
                                                float* __restrict__ m, float* __restrict__ v,
-                                               const AdamSeg* __restrict__ segs, int nseg,
+                                               const AdamSeg* segs, int nseg,
                                                int64_t total4, const AdamScalars* __restrict__ ap,
                                                Shadows sh, const double* __restrict__ loss_total) {
     if (!loss_ok(loss_total)) return;
     const AdamScalars a = *ap;
+    __shared__ AdamSeg s_segs[ADAM_MAX_SEGS];
+    const bool seg_smem = nseg <= ADAM_MAX_SEGS;
+    if (seg_smem) {
+        for (int i = threadIdx.x; i < nseg; i += blockDim.x) s_segs[i] = segs[i];
+        __syncthreads();
+        segs = s_segs;
+    }
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * ADAM_U;
     for (int64_t base = (static_cast<int64_t>(blockIdx.x) * blockDim.x) * ADAM_U + threadIdx.x;
          base < total4; base += stride) {

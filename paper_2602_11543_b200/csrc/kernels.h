@@ -78,12 +78,14 @@ void gather_rows_bf16(const float* src, int64_t ld_src, const int32_t* row_map,
 // rows processed: *nrows_dev.
 void permute_rows_bf16(const bf16* src, int64_t cols, const int32_t* row_map,
                        const int32_t* nrows_dev, int64_t rows_cap, bf16* dst, cudaStream_t s);
+// h_next_bf (optional): bf16 copy of h_next (the head GEMM operand after the last layer)
 void combine_forward(const float* h, const float* y, const int32_t* slot_row,
                      const int32_t* topk_idx, const float* topk_w, int64_t T, int64_t d, int k,
-                     float* h_next, cudaStream_t s);
-// CE + z on head logits; writes dlogits fp32 (padding rows zero) and per-token terms.
+                     float* h_next, bf16* h_next_bf, cudaStream_t s);
+// CE + z on head logits; writes dlogits as bf16 (the head backward GEMM operand; padding
+// rows zero) and the per-token terms.
 void head_ce(const float* logits, const int32_t* targets, int64_t T, int64_t T_pad, int64_t V,
-             int expf_variant, float g_s2, float g_ssum, float* dlogits, float* diff,
+             int expf_variant, float g_s2, float g_ssum, bf16* dlogits, float* diff,
              float* lse, cudaStream_t s);
 // Loss scalars (tolerance-level, deterministic tree order) -> out[5] (doubles)
 void losses_reduce(const float* diff, const float* lse_head, const float* lse_r,
