@@ -1,12 +1,13 @@
 // Fused epilogues of the grouped tcgen05 GEMM (grouped_gemm.cuh) and their launchers.
 //
 //   EpiSwiGLU   expert forward gate||up: accumulator columns [0,128) are gate,
-//               [128,256) the matching up columns; writes GU (bf16, saved for
-//               backward) and Hact = silu(G)*U (bf16).
+//               [128,256) the matching up columns; writes Hact = silu(G)*U (bf16) and,
+//               in the GU buffer, the backward factors A = U*silu'(G) (gate slots) and
+//               B = silu(G) (up slots) as bf16.
 //   EpiStoreF32 plain fp32 tile store (expert down-proj Y, dX, head logits / dh,
 //               dWd and dHead straight into the gradient buffer).
-//   EpiDSwiGLU  expert backward: dHact -> (dG, dU) using the saved GU, written as
-//               dGU (bf16) for the dX and dW GEMMs.
+//   EpiDSwiGLU  expert backward: dHact -> (dG, dU) = (dH*A, dH*B) from the saved
+//               factors, written as dGU (bf16) for the dX and dW GEMMs.
 // All epilogues hand their row pieces to EpiOut (grouped_gemm.cuh): an smem transpose so
 // that each warp store instruction writes whole 128-byte rows.
 //   EpiGradW1   dW of gate||up straight into the fp32 wg / wu gradient blocks.
@@ -69,7 +70,16 @@ struct EpiSwiGLU {
             acc_load32(taddr + c + 32 * s, empty, gv);
             acc_load32(taddr + 128 + c + 32 * s, empty, uv);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) hv[i] = gv[i] * sigmoid_fast(gv[i]) * uv[i];
+            for (int i = 0; i < 32; ++i) {
+                // Hact = silu(G) * U; saved for backward instead of (G, U): the factors
+                // A = U * silu'(G) and B = silu(G), so dG = dH * A and dU = dH * B there
+                const float sg = sigmoid_fast(gv[i]);
+                const float silu = gv[i] * sg;
+                hv[i] = silu * uv[i];
+                const float a = uv[i] * (sg * (1.f + gv[i] * (1.f - sg)));
+                gv[i] = a;
+                uv[i] = silu;
+            }
             pack_bf16x32(gv, *reinterpret_cast<uint4(*)[4]>(&pg[4 * s]));
             pack_bf16x32(uv, *reinterpret_cast<uint4(*)[4]>(&pu[4 * s]));
             pack_bf16x32(hv, *reinterpret_cast<uint4(*)[4]>(&ph[4 * s]));
@@ -115,15 +125,14 @@ struct EpiDSwiGLU {
             }
 #pragma unroll
             for (int s = 0; s < 2; ++s) {
-                float dh[32], gv[32], uv[32], dg[32], du[32];
-                unpack_bf16x32(&lg[4 * s], gv);
-                unpack_bf16x32(&lu[4 * s], uv);
+                float dh[32], fa[32], fb[32], dg[32], du[32];
+                unpack_bf16x32(&lg[4 * s], fa);  // A = U * silu'(G)
+                unpack_bf16x32(&lu[4 * s], fb);  // B = silu(G)
                 acc_load32(taddr + c + 32 * s, empty, dh);
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
-                    const float sg = sigmoid_fast(gv[i]);
-                    dg[i] = dh[i] * uv[i] * (sg * (1.f + gv[i] * (1.f - sg)));
-                    du[i] = dh[i] * (gv[i] * sg);
+                    dg[i] = dh[i] * fa[i];
+                    du[i] = dh[i] * fb[i];
                 }
                 pack_bf16x32(dg, *reinterpret_cast<uint4(*)[4]>(&pg[4 * s]));
                 pack_bf16x32(du, *reinterpret_cast<uint4(*)[4]>(&pu[4 * s]));
