@@ -129,7 +129,10 @@ struct EpiOut {
         for (int i = 0; i < N16; ++i) v[i] = row[i];
         __syncwarp();
     }
-    __device__ __forceinline__ void drain() const {}
+    // outstanding bulk (TMA) stores of this lane complete before the CTA's smem goes away
+    __device__ __forceinline__ void drain() const {
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
 };
 
 constexpr int GEMM_MAX_GROUPS = 512;

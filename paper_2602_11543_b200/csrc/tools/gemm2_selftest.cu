@@ -157,6 +157,77 @@ struct EpiNull {
     __device__ void operator()(const GemmGroup&, int, int, int, uint32_t, bool, int, EpiOut&) const {}
 };
 
+// epilogue cost decomposition probes (fp32 tile of 128 x 256 per CTA)
+struct EpiTmemOnly {  // TMEM -> registers only (results kept alive via an impossible store)
+    static constexpr int SLOTS = 1;
+    __device__ void prefetch(const GemmGroup&, int, int, int, int) const {}
+    __device__ void operator()(const GemmGroup& g, int, int, int r, uint32_t taddr, bool empty,
+                               int half, EpiOut&) const {
+        float acc = 0.f;
+        for (int c = half * 128; c < half * 128 + 128; c += 32) {
+            float v[32];
+            acc_load32(taddr + c, empty, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) acc += v[i];
+        }
+        if (acc == 1234.5f && r == 999) static_cast<float*>(g.out0)[0] = acc;
+    }
+};
+struct EpiTmemSmem {  // TMEM -> registers -> smem slot (no global stores)
+    static constexpr int SLOTS = 1;
+    __device__ void prefetch(const GemmGroup&, int, int, int, int) const {}
+    __device__ void operator()(const GemmGroup&, int, int, int, uint32_t taddr, bool empty,
+                               int half, EpiOut& out) const {
+        for (int c = half * 128; c < half * 128 + 128; c += 32) {
+            float v[32];
+            acc_load32(taddr + c, empty, v);
+            uint4* row = out.my_row(0);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) row[i] = reinterpret_cast<const uint4*>(v)[i];
+            __syncwarp();
+        }
+    }
+};
+
+// TMA-store epilogue probe: each warp writes its 32 x 32 fp32 piece into a 128B-swizzled
+// 4 KiB box and one lane issues cp.async.bulk.tensor.2d (global <- shared), double-buffered
+__device__ CUtensorMap g_out_map;
+__device__ float* g_out_ptr;
+struct EpiTmaF32 {
+    static constexpr int SLOTS = 2;
+    __device__ void prefetch(const GemmGroup&, int, int, int, int) const {}
+    __device__ void operator()(const GemmGroup& g, int mt, int nt, int r, uint32_t taddr, bool empty,
+                               int half, EpiOut& out) const {
+        const int lane = out.lane;
+        uint8_t* base = reinterpret_cast<uint8_t*>(
+            (reinterpret_cast<uintptr_t>(out.base) + 1023) & ~static_cast<uintptr_t>(1023));
+        const int row0 = static_cast<int>(g.out_row0) + mt * 128 + (r - lane);
+        int slot = 0;
+        for (int c = half * 128; c < half * 128 + 128; c += 32) {
+            float v[32];
+            acc_load32(taddr + c, empty, v);
+            uint8_t* box = base + slot * 4096;
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncwarp();
+            const uint4* src = reinterpret_cast<const uint4*>(v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                reinterpret_cast<uint4*>(box + lane * 128)[j ^ (lane & 7)] = src[j];
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                        reinterpret_cast<uint64_t>(&g_out_map)),
+                    "r"(nt * 256 + c), "r"(row0), "r"(smem_u32(box))
+                    : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            slot ^= 1;
+        }
+    }
+};
+
 template <int BN, bool AMN, bool BMN, class Epi>
 void probe(const char* name, int a_rows, int a_cols, int b_rows, int b_cols,
            std::vector<GemmGroup> groups, int grid_pairs) {
@@ -179,8 +250,25 @@ void probe(const char* name, int a_rows, int a_cols, int b_rows, int b_cols,
     CUtensorMap ma = spes_host::make_tmap_bf16(A, a_rows, a_cols, AMN ? 64 : 128);
     CUtensorMap mb = spes_host::make_tmap_bf16(B, b_rows, b_cols, BMN ? 64 : BN / 2);
     auto kern = grouped_gemm_2cta_kernel<BN, Epi, AMN, BMN>;
-    const int smem = Gemm2Cfg<BN>::SMEM_BYTES;
+    const int smem = Gemm2Cfg<BN, Epi::SLOTS>::SMEM_BYTES;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    {  // output for the store probes: [a_rows x b_cols] fp32 (groups write their own rows)
+        float* outp;
+        CK(cudaMalloc(&outp, (size_t)a_rows * b_cols * 4));
+        for (auto& gg : groups) { gg.out0 = outp; gg.ldo = b_cols; }
+        CK(cudaMemcpy(dg, groups.data(), groups.size() * sizeof(GemmGroup), cudaMemcpyHostToDevice));
+        CUtensorMap om;
+        cuuint64_t dims[2] = {(cuuint64_t)b_cols, (cuuint64_t)a_rows};
+        cuuint64_t strides[1] = {(cuuint64_t)b_cols * 4};
+        cuuint32_t box[2] = {32, 32};
+        cuuint32_t es[2] = {1, 1};
+        if (spes_host::tmap_encoder()(&om, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, outp, dims, strides, box,
+                                      es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            printf("out map failed\n");
+        CK(cudaMemcpyToSymbol(g_out_map, &om, sizeof(om)));
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * grid_pairs);
     cfg.blockDim = dim3(GEMM_THREADS);
@@ -270,6 +358,10 @@ int main() {
         std::vector<GemmGroup> gs;
         for (int j = 0; j < 16; ++j) gs.push_back(G(j * 2048, 0, 0, j * 1024, 1024, 8, 8, j * 2048));
         probe<256, false, true, EpiNull>("fwd1_nullepi", 16 * 2048, 1024, 16 * 1024, 2048, gs, 74);
+        probe<256, false, true, EpiTmemOnly>("fwd1_tmem_only", 16 * 2048, 1024, 16 * 1024, 2048, gs, 74);
+        probe<256, false, true, EpiTmemSmem>("fwd1_tmem_smem", 16 * 2048, 1024, 16 * 1024, 2048, gs, 74);
+        probe<256, false, true, EpiStoreF32<256>>("fwd1_put_f32", 16 * 2048, 1024, 16 * 1024, 2048, gs, 74);
+        probe<256, false, true, EpiTmaF32>("fwd1_tma_f32", 16 * 2048, 1024, 16 * 1024, 2048, gs, 74);
         probe<256, false, true, EpiNull>("fwd1_nullepi_p37", 16 * 2048, 1024, 16 * 1024, 2048, gs, 37);
     }
     printf(fails ? "SELFTEST2 FAILED\n" : "SELFTEST2 OK\n");
