@@ -164,6 +164,26 @@ spes_status spes_merge(spes_ctx* ctx, const spes_merge_sched* sched, int32_t rou
 /* similarity_matrix (merging.hpp:55-82) of one layer, M x M doubles. */
 spes_status spes_similarity(spes_ctx* ctx, int32_t layer, int32_t source, double* sim_out);
 
+/* ---- wire / checkpoint format (proj/src/wire.cpp) ----
+ * Byte-identical to the reference: encode_blocks(model_to_blocks(params)) is the
+ * GLOBAL_MODEL payload (wire.cpp:96-115,154-159); a checkpoint is that payload followed by
+ * the u64 round (write_checkpoint / read_checkpoint, wire.cpp:212-236). Decoding validates
+ * exactly like decode_blocks + blocks_into_model (wire.cpp:117-176): SPES_PROTOCOL_ERROR
+ * with the reference's ProtoError name as message prefix ("[Truncated] ..."). */
+/* payload bytes of a model (-1 on an invalid config) */
+int64_t spes_model_payload_bytes(const spes_model_cfg* cfg);
+/* host-only codec over a flat fp32 parameter vector (enumerate_blocks order) */
+spes_status spes_encode_model_host(const spes_model_cfg* cfg, const float* params, uint8_t* out,
+                                   int64_t cap);
+spes_status spes_decode_model_host(const spes_model_cfg* cfg, const uint8_t* payload, int64_t len,
+                                   float* params);
+/* the context's device parameters (device -> host export / host -> device import; the
+ * bf16 GEMM operand copies are refreshed on import) */
+spes_status spes_encode_model(spes_ctx* ctx, uint8_t* out, int64_t cap);
+spes_status spes_decode_model(spes_ctx* ctx, const uint8_t* payload, int64_t len);
+spes_status spes_write_checkpoint(spes_ctx* ctx, const char* path, uint64_t round);
+spes_status spes_read_checkpoint(spes_ctx* ctx, const char* path, uint64_t* round);
+
 /* ---- introspection (tests / benchmarks) ---- */
 
 /* Counters: optimizer-state scalars (2(|psi|+|Phi_i|)), gradient scalars, step count. */

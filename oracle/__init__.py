@@ -137,6 +137,16 @@ def ref():
         R.ref_lr_at.restype = C.c_double
         R.ref_lr_at.argtypes = [C.c_double, C.c_double, C.c_int64, C.c_int64, C.c_int64]
         R.ref_param_partition.argtypes = [_cfgp, C.c_int32, _i32p, _i32p]
+        _u8 = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+        R.ref_encode_model.restype = C.c_int64
+        R.ref_encode_model.argtypes = [_cfgp, _f32p, C.c_void_p, C.c_int64]
+        R.ref_decode_model.restype = C.c_int
+        R.ref_decode_model.argtypes = [_cfgp, _u8, C.c_int64, _f32p, C.c_char_p, C.c_int]
+        R.ref_write_checkpoint.restype = C.c_int
+        R.ref_write_checkpoint.argtypes = [_cfgp, _f32p, C.c_char_p, C.c_uint64]
+        R.ref_read_checkpoint.restype = C.c_int
+        R.ref_read_checkpoint.argtypes = [_cfgp, C.c_char_p, _f32p, C.POINTER(C.c_uint64),
+                                          C.c_char_p, C.c_int]
         R.ref_set_parallel.argtypes = [C.c_int]
         _ref = R
     return _ref

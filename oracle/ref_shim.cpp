@@ -3,6 +3,7 @@
 // it pins the C restatement (spes_oracle.c) bit-for-bit and is the reference arm
 // / cpu_baseline of bench.py. It calls the reference's own public API; nothing
 // of the reference is copied here.
+#include <cstdio>
 #include <cstring>
 #include <span>
 #include <vector>
@@ -318,4 +319,83 @@ void ref_param_partition(const spes_model_cfg* c, int32_t N, int32_t* node_offse
     }
 }
 
+}  // extern "C"
+
+// ---- wire / checkpoint format (proj/src/wire.cpp) ----
+namespace {
+const char* proto_name(ProtoError e) {
+    switch (e) {
+        case ProtoError::BadMagic: return "BadMagic";
+        case ProtoError::BadVersion: return "BadVersion";
+        case ProtoError::UnknownKind: return "UnknownKind";
+        case ProtoError::Truncated: return "Truncated";
+        case ProtoError::LengthMismatch: return "LengthMismatch";
+        case ProtoError::MalformedPayload: return "MalformedPayload";
+        case ProtoError::ConfigMismatch: return "ConfigMismatch";
+        case ProtoError::RoundMismatch: return "RoundMismatch";
+        case ProtoError::DuplicatePush: return "DuplicatePush";
+        case ProtoError::NotOwnedBlock: return "NotOwnedBlock";
+        case ProtoError::UnexpectedMessage: return "UnexpectedMessage";
+        case ProtoError::BarrierViolation: return "BarrierViolation";
+        case ProtoError::Timeout: return "Timeout";
+    }
+    return "?";
+}
+void put_err(char* err, int cap, const std::string& m) {
+    if (err && cap > 0) std::snprintf(err, static_cast<size_t>(cap), "%s", m.c_str());
+}
+}  // namespace
+
+extern "C" {
+// encode_blocks(model_to_blocks(params)) -> out; returns the byte count (or needed size)
+int64_t ref_encode_model(const spes_model_cfg* c, const float* params, uint8_t* out, int64_t cap) {
+    ModelConfig cfg = to_cfg(c);
+    auto bytes = encode_blocks(model_to_blocks(from_flat(cfg, params)));
+    if (out && cap >= static_cast<int64_t>(bytes.size())) std::memcpy(out, bytes.data(), bytes.size());
+    return static_cast<int64_t>(bytes.size());
+}
+// blocks_into_model(decode_blocks(payload)); 0 ok, 1 ProtocolError ("[Code] msg"), 2 other
+int ref_decode_model(const spes_model_cfg* c, const uint8_t* payload, int64_t len, float* params,
+                     char* err, int errcap) {
+    try {
+        ModelConfig cfg = to_cfg(c);
+        ModelParams p = init_model<float>(cfg, 0, 0.0);
+        blocks_into_model(p, decode_blocks(std::span<const uint8_t>(payload, static_cast<size_t>(len))));
+        to_flat(p, params);
+        return 0;
+    } catch (const ProtocolError& e) {
+        put_err(err, errcap, std::string("[") + proto_name(e.code()) + "] " + e.what());
+        return 1;
+    } catch (const std::exception& e) {
+        put_err(err, errcap, e.what());
+        return 2;
+    }
+}
+int ref_write_checkpoint(const spes_model_cfg* c, const float* params, const char* path,
+                         uint64_t round) {
+    try {
+        write_checkpoint(path, from_flat(to_cfg(c), params), round);
+        return 0;
+    } catch (...) {
+        return 2;
+    }
+}
+int ref_read_checkpoint(const spes_model_cfg* c, const char* path, float* params, uint64_t* round,
+                        char* err, int errcap) {
+    try {
+        ModelConfig cfg = to_cfg(c);
+        auto [blocks, r] = read_checkpoint(path);
+        ModelParams p = init_model<float>(cfg, 0, 0.0);
+        blocks_into_model(p, blocks);
+        to_flat(p, params);
+        *round = r;
+        return 0;
+    } catch (const ProtocolError& e) {
+        put_err(err, errcap, std::string("[") + proto_name(e.code()) + "] " + e.what());
+        return 1;
+    } catch (const std::exception& e) {
+        put_err(err, errcap, e.what());
+        return 2;
+    }
+}
 }  // extern "C"

@@ -75,6 +75,15 @@ def lib():
         L.spes_read_params.argtypes = [vp, f32p, i64]
         L.spes_read_grads.argtypes = [vp, f32p, i64]
         L.spes_set_fused_optimizer.argtypes = [vp, C.c_int32]
+        u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+        L.spes_model_payload_bytes.restype = i64
+        L.spes_model_payload_bytes.argtypes = [C.POINTER(ModelCfg)]
+        L.spes_encode_model_host.argtypes = [C.POINTER(ModelCfg), f32p, u8p, i64]
+        L.spes_decode_model_host.argtypes = [C.POINTER(ModelCfg), u8p, i64, f32p]
+        L.spes_encode_model.argtypes = [vp, u8p, i64]
+        L.spes_decode_model.argtypes = [vp, u8p, i64]
+        L.spes_write_checkpoint.argtypes = [vp, C.c_char_p, C.c_uint64]
+        L.spes_read_checkpoint.argtypes = [vp, C.c_char_p, C.POINTER(C.c_uint64)]
         L.spes_round_begin.argtypes = [vp, i32]
         L.spes_local_step.argtypes = [vp, C.POINTER(i32), i64, i64, C.POINTER(AdamWCfg),
                                       C.POINTER(Losses)]
@@ -178,6 +187,29 @@ def lr_at(peak, min_frac, warmup, total, step):
     return lib().spes_lr_at(peak, min_frac, warmup, total, step)
 
 
+# ---- wire / checkpoint format (proj/src/wire.cpp), byte-identical to the reference ----
+
+def model_payload_bytes(cfg):
+    return lib().spes_model_payload_bytes(C.byref(cfg))
+
+
+def encode_model(cfg, params):
+    """encode_blocks(model_to_blocks(params)): the GLOBAL_MODEL payload as bytes (uint8)."""
+    out = np.zeros(model_payload_bytes(cfg), np.uint8)
+    params = np.ascontiguousarray(params, np.float32)
+    _check(lib().spes_encode_model_host(C.byref(cfg), f32(params), out, out.size))
+    return out
+
+
+def decode_model(cfg, payload):
+    """blocks_into_model(decode_blocks(payload)) -> flat fp32 parameters."""
+    payload = np.ascontiguousarray(np.frombuffer(bytes(payload), np.uint8) if not
+                                   isinstance(payload, np.ndarray) else payload, np.uint8)
+    out = np.zeros(param_count(cfg), np.float32)
+    _check(lib().spes_decode_model_host(C.byref(cfg), payload, payload.size, f32(out)))
+    return out
+
+
 class Node:
     """One SPES node on one GPU."""
 
@@ -230,6 +262,23 @@ class Node:
         """Owned experts' AdamW inside the dW GEMM epilogue (default) or as a separate pass
         with materialized gradients (needed by read_grads); identical bits either way."""
         _check(lib().spes_set_fused_optimizer(self._ctx, 1 if on else 0))
+
+    def encode_model(self):
+        out = np.zeros(model_payload_bytes(self.cfg), np.uint8)
+        _check(lib().spes_encode_model(self._ctx, out, out.size))
+        return out
+
+    def decode_model(self, payload):
+        payload = np.ascontiguousarray(payload, np.uint8)
+        _check(lib().spes_decode_model(self._ctx, payload, payload.size))
+
+    def write_checkpoint(self, path, round_no):
+        _check(lib().spes_write_checkpoint(self._ctx, str(path).encode(), round_no))
+
+    def read_checkpoint(self, path):
+        r = C.c_uint64()
+        _check(lib().spes_read_checkpoint(self._ctx, str(path).encode(), C.byref(r)))
+        return r.value
 
     def read_grads(self):
         out = np.zeros(self.P, np.float32)

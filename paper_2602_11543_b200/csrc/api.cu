@@ -17,6 +17,7 @@
 #include "../../include/spes_b200.h"
 #include "glibc_expf.h"
 #include "kernels.h"
+#include "wire.hpp"
 #include "tmap.hpp"
 
 using spes_dev::GemmGroup;
@@ -48,6 +49,9 @@ spes_status guard(F&& f) {
     } catch (const SpesError& e) {
         g_last_error = e.what();
         return e.code;
+    } catch (const spes_wire::ProtocolError& e) {  // "[Code] message"
+        g_last_error = e.what();
+        return SPES_PROTOCOL_ERROR;
     } catch (const std::invalid_argument& e) {
         g_last_error = e.what();
         return SPES_INVALID_ARGUMENT;
@@ -1010,6 +1014,105 @@ spes_status spes_load_params(spes_ctx* c, const float* host, int64_t n) {
            "H2D params");
         refresh_shadows_all(c);
         ck(cudaStreamSynchronize(c->stream), "sync");
+    });
+}
+
+// ---- wire / checkpoint format (proj/src/wire.cpp:96-176, 212-236) ----
+namespace {
+std::vector<spes_wire::Block> wire_blocks(const spes_model_cfg* cfg) {
+    // ModelConfig::validate (model.hpp:33-40) only: the codec has no tiling constraints
+    if (cfg->vocab < 1 || cfg->hidden < 1 || cfg->intermediate < 1 || cfg->layers < 1)
+        throw std::invalid_argument("model config: all dims must be >= 1");
+    if (cfg->experts_active < 1 || cfg->experts_active > cfg->experts_total)
+        throw std::invalid_argument("model config: need 1 <= k <= M");
+    if (cfg->tied_head) throw std::logic_error("tied head not implemented");
+    return spes_wire::model_blocks(cfg->vocab, cfg->hidden, cfg->intermediate, cfg->layers,
+                                   cfg->experts_total);
+}
+// device parameters <-> a host copy (pinned staging would not pay off for a one-shot export)
+std::vector<float> params_to_host(spes_ctx* c) {
+    std::vector<float> h(static_cast<size_t>(c->lay.total()));
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    ck(cudaMemcpyAsync(h.data(), c->params, sizeof(float) * h.size(), cudaMemcpyDeviceToHost,
+                       c->stream),
+       "D2H params");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    return h;
+}
+void params_from_host(spes_ctx* c, const std::vector<float>& h) {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    set_counter(c);
+    ck(cudaMemcpyAsync(c->params, h.data(), sizeof(float) * h.size(), cudaMemcpyHostToDevice,
+                       c->stream),
+       "H2D params");
+    refresh_shadows_all(c);
+    ck(cudaStreamSynchronize(c->stream), "sync");
+}
+}  // namespace
+
+int64_t spes_model_payload_bytes(const spes_model_cfg* cfg) {
+    try {
+        return spes_wire::payload_bytes(wire_blocks(cfg));
+    } catch (...) {
+        return -1;
+    }
+}
+
+spes_status spes_encode_model_host(const spes_model_cfg* cfg, const float* params, uint8_t* out,
+                                   int64_t cap) {
+    return guard([&] {
+        const auto blocks = wire_blocks(cfg);
+        if (cap < spes_wire::payload_bytes(blocks))
+            throw std::invalid_argument("encode_model: output buffer too small");
+        spes_wire::encode_model(blocks, params, out);
+    });
+}
+
+spes_status spes_decode_model_host(const spes_model_cfg* cfg, const uint8_t* payload, int64_t len,
+                                   float* params) {
+    return guard([&] {
+        const auto blocks = wire_blocks(cfg);
+        const auto& last = blocks.back();
+        std::vector<float> tmp(static_cast<size_t>(last.offset + last.numel));
+        spes_wire::decode_model(blocks, payload, len, tmp.data());  // all-or-nothing
+        std::memcpy(params, tmp.data(), sizeof(float) * tmp.size());
+    });
+}
+
+spes_status spes_encode_model(spes_ctx* c, uint8_t* out, int64_t cap) {
+    return guard([&] {
+        const auto blocks = wire_blocks(&c->cfg);
+        if (cap < spes_wire::payload_bytes(blocks))
+            throw std::invalid_argument("encode_model: output buffer too small");
+        const auto h = params_to_host(c);
+        spes_wire::encode_model(blocks, h.data(), out);
+    });
+}
+
+spes_status spes_decode_model(spes_ctx* c, const uint8_t* payload, int64_t len) {
+    return guard([&] {
+        const auto blocks = wire_blocks(&c->cfg);
+        std::vector<float> h(static_cast<size_t>(c->lay.total()));
+        spes_wire::decode_model(blocks, payload, len, h.data());
+        params_from_host(c, h);
+    });
+}
+
+spes_status spes_write_checkpoint(spes_ctx* c, const char* path, uint64_t round) {
+    return guard([&] {
+        const auto blocks = wire_blocks(&c->cfg);
+        const auto h = params_to_host(c);
+        spes_wire::write_checkpoint(path, blocks, h.data(), round);
+    });
+}
+
+spes_status spes_read_checkpoint(spes_ctx* c, const char* path, uint64_t* round) {
+    return guard([&] {
+        const auto blocks = wire_blocks(&c->cfg);
+        std::vector<float> h(static_cast<size_t>(c->lay.total()));
+        const uint64_t r = spes_wire::read_checkpoint(path, blocks, h.data());
+        params_from_host(c, h);
+        if (round) *round = r;
     });
 }
 
