@@ -156,6 +156,17 @@ spes_status spes_local_round(spes_ctx* ctx, const int32_t* tokens, int64_t B, in
  * ends with the identical global model. Collective: all nodes must call. */
 spes_status spes_sync(spes_ctx* ctx, spes_sync_stats* stats);
 
+/* DiLoCo baseline: full-model outer synchronization, Server::aggregate's
+ * diloco branch (protocol.cpp:199-213) with OuterOptimizer::step (trainer.hpp:228-271):
+ * theta <- OuterOpt(theta, mean_i(local_i - theta)) in fp64 with the nodes in order, kind
+ * 0 = SGD, 1 = Nesterov (state persists across calls). spes_outer_begin snapshots the
+ * round-start global model (call it once after loading the initial parameters); each
+ * spes_outer_sync then replaces every node's parameters with the new global model and keeps
+ * it as the next round's theta. Collective: all nodes call it. Bit-exact with the reference. */
+spes_status spes_outer_begin(spes_ctx* ctx);
+spes_status spes_outer_sync(spes_ctx* ctx, int32_t kind, double lr, double momentum,
+                            spes_sync_stats* stats);
+
 /* merge_model (merging.hpp:138-150) on this node's (global) model. events must
  * hold `layers` entries and peers `layers * experts_total * peers` ints (either may be NULL).
  * Returns the number of merged layers in *n_events (0 when the schedule is inactive). */

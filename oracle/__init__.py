@@ -86,6 +86,8 @@ def lib():
         L.oracle_local_round.argtypes = [_cfgp, _f32p, _i32p, C.c_int64, C.c_int64, C.c_int32,
                                          _f64n, C.POINTER(AdamWCfg), _u8p, _f64p]
         L.oracle_aggregate.argtypes = [_cfgp, C.c_int32, _f32p, _i32p, _i32p, _f32p, _f32p]
+        L.oracle_outer_step.argtypes = [C.c_int32, C.c_double, C.c_double, _f32p, _f32p,
+                                        C.c_int32, C.c_int64, _f64p]
         L.oracle_similarity.argtypes = [_cfgp, _f32p, C.c_int32, C.c_int32, _f64p]
         L.oracle_select_peers.restype = C.c_int32
         L.oracle_select_peers.argtypes = [_f64p, C.c_int32, C.c_int32, C.c_int32, _i32p]
@@ -138,6 +140,11 @@ def ref():
         R.ref_lr_at.argtypes = [C.c_double, C.c_double, C.c_int64, C.c_int64, C.c_int64]
         R.ref_param_partition.argtypes = [_cfgp, C.c_int32, _i32p, _i32p]
         _u8 = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+        R.ref_outer_create.restype = C.c_void_p
+        R.ref_outer_create.argtypes = [C.c_int32, C.c_double, C.c_double]
+        R.ref_outer_destroy.argtypes = [C.c_void_p]
+        R.ref_outer_step.restype = C.c_int
+        R.ref_outer_step.argtypes = [C.c_void_p, _cfgp, _f32p, _f32p, C.c_int32]
         R.ref_encode_model.restype = C.c_int64
         R.ref_encode_model.argtypes = [_cfgp, _f32p, C.c_void_p, C.c_int64]
         R.ref_decode_model.restype = C.c_int
@@ -256,6 +263,14 @@ def aggregate(cfg, node_params, owned_lists, global_in):
     lib().oracle_aggregate(C.byref(cfg), N, np.ascontiguousarray(node_params, np.float32), offs,
                            flat, np.ascontiguousarray(global_in, np.float32), out)
     return out
+
+
+def outer_step(kind, lr, momentum, theta, locals_, buf):
+    """OuterOptimizer::step (trainer.hpp:228-266) restated: theta (in place), locals N x n,
+    buf (n doubles, Nesterov state, in place)."""
+    N = locals_.shape[0]
+    lib().oracle_outer_step(kind, lr, momentum, theta, np.ascontiguousarray(locals_, np.float32),
+                            N, theta.size, buf)
 
 
 def similarity(cfg, params, layer, source=0):

@@ -399,3 +399,28 @@ int ref_read_checkpoint(const spes_model_cfg* c, const char* path, float* params
     }
 }
 }  // extern "C"
+
+// ---- OuterOptimizer (trainer.hpp:228-271): persistent handle (Nesterov state) ----
+extern "C" {
+void* ref_outer_create(int32_t kind, double lr, double momentum) {
+    return new OuterOptimizer(kind == 0 ? OuterKind::SGD : OuterKind::Nesterov, lr, momentum);
+}
+void ref_outer_destroy(void* h) { delete static_cast<OuterOptimizer*>(h); }
+// theta (in/out, flat), locals N x P flat
+int ref_outer_step(void* h, const spes_model_cfg* c, float* theta, const float* locals, int32_t N) {
+    try {
+        ModelConfig cfg = to_cfg(c);
+        ModelParams t = from_flat(cfg, theta);
+        const int64_t P = ref_param_count(c);
+        std::vector<ModelParams> ls;
+        for (int32_t i = 0; i < N; ++i) ls.push_back(from_flat(cfg, locals + i * P));
+        std::vector<const ModelParams*> ptrs;
+        for (auto& l : ls) ptrs.push_back(&l);
+        static_cast<OuterOptimizer*>(h)->step(t, ptrs);
+        to_flat(t, theta);
+        return 0;
+    } catch (...) {
+        return 2;
+    }
+}
+}  // extern "C"

@@ -684,6 +684,28 @@ int oracle_local_round(const spes_model_cfg* c, float* P, const int32_t* tokens,
     return rc;
 }
 
+/* ---------------- OuterOptimizer::step (trainer.hpp:228-266), DiLoCo baseline ----------------
+ * theta <- OuterOpt(theta, mean_i(local_i - theta)) per element in fp64: delta accumulates
+ * (local_i - theta) * (1/N) over the locals in order; SGD: theta = float(theta + lr*delta);
+ * Nesterov: g = -delta, b = momentum*b + g, theta = float(theta - lr*(g + momentum*b)).
+ * buf (n doubles, zero before the first step) is the Nesterov state; locals is N x n. */
+void oracle_outer_step(int32_t kind, double lr, double momentum, float* theta,
+                       const float* locals, int32_t N, int64_t n, double* buf) {
+    const double inv_n = 1.0 / (double)N;
+    for (int64_t j = 0; j < n; ++j) {
+        double delta = 0.0;
+        for (int32_t i = 0; i < N; ++i)
+            delta += ((double)locals[(int64_t)i * n + j] - (double)theta[j]) * inv_n;
+        if (kind == 0) {
+            theta[j] = (float)((double)theta[j] + lr * delta);
+        } else {
+            const double g = -delta;
+            buf[j] = momentum * buf[j] + g;
+            theta[j] = (float)((double)theta[j] - lr * (g + momentum * buf[j]));
+        }
+    }
+}
+
 /* ---------------- Server::aggregate (protocol.cpp:197-251), owner-set form ---------------- */
 
 void oracle_aggregate(const spes_model_cfg* c, int32_t N, const float* node_params,

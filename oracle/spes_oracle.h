@@ -73,6 +73,8 @@ int oracle_local_round(const spes_model_cfg* c, float* params, const int32_t* to
 /* Server::aggregate generalized to owner sets: psi <- fp64 node-order mean over all
  * N node copies; expert e <- fp64 mean over owners (ascending node id); experts
  * without owners keep global_in. node_params: N x P. owners via CSR node -> experts. */
+void oracle_outer_step(int32_t kind, double lr, double momentum, float* theta,
+                       const float* locals, int32_t N, int64_t n, double* buf);
 void oracle_aggregate(const spes_model_cfg* c, int32_t n_nodes, const float* node_params,
                       const int32_t* node_offsets, const int32_t* experts,
                       const float* global_in, float* global_out);

@@ -75,6 +75,8 @@ def lib():
         L.spes_read_params.argtypes = [vp, f32p, i64]
         L.spes_read_grads.argtypes = [vp, f32p, i64]
         L.spes_set_fused_optimizer.argtypes = [vp, C.c_int32]
+        L.spes_outer_begin.argtypes = [vp]
+        L.spes_outer_sync.argtypes = [vp, C.c_int32, C.c_double, C.c_double, C.POINTER(SyncStats)]
         u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
         L.spes_model_payload_bytes.restype = i64
         L.spes_model_payload_bytes.argtypes = [C.POINTER(ModelCfg)]
@@ -262,6 +264,17 @@ class Node:
         """Owned experts' AdamW inside the dW GEMM epilogue (default) or as a separate pass
         with materialized gradients (needed by read_grads); identical bits either way."""
         _check(lib().spes_set_fused_optimizer(self._ctx, 1 if on else 0))
+
+    def outer_begin(self):
+        """DiLoCo baseline: snapshot the round-start global model (this rank's slice)."""
+        _check(lib().spes_outer_begin(self._ctx))
+
+    def outer_sync(self, kind="nesterov", lr=0.7, momentum=0.9):
+        """DiLoCo outer step over the full model (collective; protocol.cpp:199-213)."""
+        st = SyncStats()
+        k = {"sgd": 0, "nesterov": 1}[kind] if isinstance(kind, str) else int(kind)
+        _check(lib().spes_outer_sync(self._ctx, k, lr, momentum, C.byref(st)))
+        return dict(bytes_in=st.expert_bytes_in, ms=st.ms)
 
     def encode_model(self):
         out = np.zeros(model_payload_bytes(self.cfg), np.uint8)

@@ -160,6 +160,12 @@ struct spes_ctx {
     // epilogue warps that fit next to the MMA ring, so it does not beat the separate pass yet.
     bool fused_opt = false;
     spes_k::AdamScalars cur_adam{};  // this step's AdamW scalars (set before backward)
+    // DiLoCo baseline: this rank's slice of the round-start global model,
+    // its fp64 Nesterov buffer, and the exchange buffers (N x slice each)
+    float *outer_theta = nullptr, *outer_recv = nullptr, *outer_gather = nullptr;
+    double* outer_buf = nullptr;
+    int64_t outer_slice = 0;
+    bool outer_ready = false;
     spes_k::AdamScalars* d_adam = nullptr;  // device copy read by the optimizer kernels
     // the local step as one CUDA graph per (T, optimizer placement): the launch sequence
     // is host-static (group tables and tile counts live on the device), so it is captured
@@ -1198,6 +1204,92 @@ spes_status spes_local_round(spes_ctx* c, const int32_t* tokens, int64_t B, int6
             local_step_impl(c, B, S, &o, lo);
             if (!std::isfinite(lo->total))
                 throw std::runtime_error("local_round: non-finite loss at step " + std::to_string(h));
+        }
+    });
+}
+
+// ---- DiLoCo baseline: full-model outer sync (protocol.cpp:199-213, trainer.hpp:228-271) ----
+// Slicing: the flat parameter vector in N equal slices of outer_slice floats (the last one
+// padded); rank r owns slice r. Exchange = grouped send/recv (each rank receives its slice
+// from every node, node order), fp64 outer step on the slice, then all-gather.
+spes_status spes_outer_begin(spes_ctx* c) {
+    return guard([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        const int64_t P = c->lay.total(), N = c->n_nodes;
+        const int64_t sl = rup((P + N - 1) / N, 4);
+        if (sl != c->outer_slice) {
+            c->outer_theta = c->persistent.alloc<float>(sl);
+            c->outer_buf = c->persistent.alloc<double>(sl);
+            c->outer_recv = c->persistent.alloc<float>(sl * N);
+            c->outer_gather = c->persistent.alloc<float>(sl * N);
+            c->outer_slice = sl;
+        }
+        const int64_t lo = std::min<int64_t>(P, sl * c->node), n = std::min<int64_t>(P, lo + sl) - lo;
+        ck(cudaMemsetAsync(c->outer_theta, 0, sizeof(float) * sl, c->stream), "theta");
+        ck(cudaMemcpyAsync(c->outer_theta, c->params + lo, sizeof(float) * n, cudaMemcpyDeviceToDevice,
+                           c->stream),
+           "theta snapshot");
+        ck(cudaMemsetAsync(c->outer_buf, 0, sizeof(double) * sl, c->stream), "nesterov");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        c->outer_ready = true;
+    });
+}
+
+spes_status spes_outer_sync(spes_ctx* c, int32_t kind, double lr, double momentum,
+                            spes_sync_stats* stats) {
+    return guard([&] {
+        if (!c->outer_ready)
+            throw std::logic_error("outer_sync: call spes_outer_begin on the round-start model first");
+        if (kind != 0 && kind != 1) throw std::invalid_argument("outer_sync: kind is 0 (SGD) or 1 (Nesterov)");
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        set_counter(c);
+        cudaStream_t st = c->stream;
+        const int64_t P = c->lay.total(), sl = c->outer_slice;
+        const int N = c->n_nodes, me = c->node;
+        auto range = [&](int r) {
+            const int64_t lo = std::min<int64_t>(P, sl * r);
+            return std::make_pair(lo, std::min<int64_t>(P, lo + sl) - lo);
+        };
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+        const auto [mlo, mn] = range(me);
+        // recv[i] = node i's local values of my slice (node order)
+        ck(cudaMemcpyAsync(c->outer_recv + static_cast<int64_t>(me) * sl, c->params + mlo,
+                           sizeof(float) * mn, cudaMemcpyDeviceToDevice, st),
+           "own slice");
+        if (N > 1) {
+            ckn(ncclGroupStart(), "group");
+            for (int p = 0; p < N; ++p) {
+                if (p == me) continue;
+                const auto [plo, pn] = range(p);
+                if (pn > 0) ckn(ncclSend(c->params + plo, pn, ncclFloat, p, c->comm, st), "send");
+                if (mn > 0)
+                    ckn(ncclRecv(c->outer_recv + static_cast<int64_t>(p) * sl, mn, ncclFloat, p, c->comm, st),
+                        "recv");
+            }
+            ckn(ncclGroupEnd(), "group end");
+        }
+        spes_k::outer_step(c->outer_theta, c->outer_recv, N, mn, sl, kind, lr, momentum, c->outer_buf,
+                           c->outer_gather + static_cast<int64_t>(me) * sl, st);
+        if (N > 1)
+            ckn(ncclAllGather(c->outer_gather + static_cast<int64_t>(me) * sl, c->outer_gather, sl,
+                              ncclFloat, c->comm, st),
+                "allgather model");
+        ck(cudaMemcpyAsync(c->params, c->outer_gather, sizeof(float) * P, cudaMemcpyDeviceToDevice, st),
+           "new global");
+        refresh_shadows_all(c);
+        cudaEventRecord(e1, st);
+        ck(cudaStreamSynchronize(st), "outer sync");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (stats) {
+            stats->psi_bytes_in = 0;
+            stats->expert_bytes_in = 4.0 * (static_cast<double>(mn) * (N - 1) + static_cast<double>(P - mn));
+            stats->ms = ms;
         }
     });
 }

@@ -975,6 +975,44 @@ void embed_grad(const int32_t* inputs, const float* gh0, int64_t T, int64_t d, i
     count_launch();
 }
 
+// ============================ DiLoCo outer step (trainer.hpp:228-266) ============================
+// This rank's slice of the global model: theta <- OuterOpt(theta, mean_i(local_i - theta)),
+// per element in fp64 with the locals in node order (recv holds N x n, node-major); the
+// Nesterov buffer of the slice persists in fp64. Bit-exact with OuterOptimizer::step.
+__global__ void __launch_bounds__(256) outer_step_k(float* __restrict__ theta,
+                                                    const float* __restrict__ recv, int N,
+                                                    int64_t n, int64_t ld, int kind, double lr,
+                                                    double momentum, double* __restrict__ buf,
+                                                    float* __restrict__ out) {
+    const double inv_n = 1.0 / static_cast<double>(N);
+    for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double t = static_cast<double>(theta[j]);
+        double delta = 0.0;
+        for (int i = 0; i < N; ++i)
+            delta = __dadd_rn(delta, __dmul_rn(__dsub_rn(static_cast<double>(recv[i * ld + j]), t), inv_n));
+        float nt;
+        if (kind == 0) {
+            nt = static_cast<float>(__dadd_rn(t, __dmul_rn(lr, delta)));
+        } else {
+            const double g = -delta;
+            const double b = __dadd_rn(__dmul_rn(momentum, buf[j]), g);
+            buf[j] = b;
+            nt = static_cast<float>(__dsub_rn(t, __dmul_rn(lr, __dadd_rn(g, __dmul_rn(momentum, b)))));
+        }
+        theta[j] = nt;
+        out[j] = nt;
+    }
+}
+
+void outer_step(float* theta, const float* recv, int N, int64_t n, int64_t ld, int kind, double lr,
+                double momentum, double* buf, float* out, cudaStream_t s) {
+    if (n <= 0) return;
+    const int blocks = static_cast<int>(std::min<int64_t>(cdiv(n, 256), 148 * 8));
+    outer_step_k<<<blocks, 256, 0, s>>>(theta, recv, N, n, ld, kind, lr, momentum, buf, out);
+    count_launch();
+}
+
 // ============================ AdamW (+ bf16 operand copies) ============================
 // MaskedAdamW::step element update (trainer.hpp:85-92), exact fp32 op order, over the
 // compact trainable segments (psi + owned experts). The updated values are also written

@@ -134,6 +134,11 @@ void refresh_shadows(const float* params, const AdamSeg* segs, int nseg, int64_t
                      Shadows sh, cudaStream_t s);
 
 // ---- sync / merge ----
+// DiLoCo outer step over this rank's slice (theta, n scalars): recv = the N nodes' local
+// slices (stride ld, node order); kind 0 SGD, 1 Nesterov (buf: fp64 state); the new values
+// go to theta and out
+void outer_step(float* theta, const float* recv, int N, int64_t n, int64_t ld, int kind, double lr,
+                double momentum, double* buf, float* out, cudaStream_t s);
 void owner_mean(const float* const* srcs, int n_src, int64_t n, float* out, cudaStream_t s);
 void owner_mean_strided(const float* x, int n_src, int64_t stride, int64_t n, float* out,
                         cudaStream_t s);

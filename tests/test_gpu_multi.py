@@ -79,3 +79,54 @@ def test_nccl_sync_matches_oracle(world, layout):
         assert np.array_equal(r[3].view(np.uint32), merged0.view(np.uint32))
     m_ref, _, _ = oracle.merge_model(cfg, expect, merge_sched(**SCHED), 0)
     assert np.array_equal(merged0.view(np.uint32), m_ref.view(np.uint32))
+
+
+def _rank_outer(rank, world, nccl_id, params, tokens, q):
+    try:
+        cfg = model_cfg(**CFG)
+        node = spes.Node(cfg, rank, world, rank, nccl_id)
+        node.set_ownership([list(range(cfg.experts_total))] * world)  # TrainMask::all
+        node.load_params(params)
+        node.outer_begin()
+        out = []
+        for rnd in range(2):
+            node.local_round(tokens[rank][rnd], adamw_cfg(lr=1e-3))
+            pre = node.read_params()
+            node.outer_sync("nesterov", lr=0.7, momentum=0.9)
+            out.append((pre, node.read_params()))
+        node.close()
+        q.put((rank, out, None))
+    except Exception as e:  # pragma: no cover
+        q.put((rank, None, repr(e)))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_nccl_outer_sync_matches_oracle(world):
+    """DiLoCo outer sync over NCCL (slice exchange + fp64 node-order step + all-gather)
+    equals OuterOptimizer::step on the gathered local models, every rank, two rounds."""
+    if _n_gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cfg = model_cfg(**CFG)
+    params = oracle.random_params(cfg, 6)
+    tokens = [[oracle.random_tokens(cfg, 2, 64, 200 + 10 * r + h, H=2) for h in range(2)]
+              for r in range(world)]
+    nccl_id = spes.nccl_unique_id()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank_outer, args=(r, world, nccl_id, params, tokens, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+    errs = [r[2] for r in res if r[2]]
+    assert not errs, errs
+    theta = params.copy()
+    buf = np.zeros(theta.size)
+    for rnd in range(2):
+        locals_ = np.stack([res[r][1][rnd][0] for r in range(world)])
+        oracle.outer_step(1, 0.7, 0.9, theta, locals_, buf)
+        for r in range(world):
+            assert np.array_equal(res[r][1][rnd][1].view(np.uint32), theta.view(np.uint32)), \
+                f"round {rnd} rank {r}"

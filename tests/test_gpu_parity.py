@@ -312,3 +312,25 @@ def test_merge_concat_source_and_cfg2(gpu):
     assert (peers_gpu == peers_ref).all()
     assert bitexact(node.read_params(), p_ref)
     node.close()
+
+
+@pytest.mark.parametrize("kind", ["sgd", "nesterov"])
+def test_outer_sync_single_node_matches_oracle(gpu, kind):
+    """DiLoCo baseline (protocol.cpp:199-213): two rounds of local training + outer step on
+    one node, bit-exact with OuterOptimizer::step restated (Nesterov state carried)."""
+    cfg = model_cfg(**CFG1)
+    params = oracle.random_params(cfg, 41)
+    node = spes.Node(cfg, 0, 1, 0)
+    node.set_ownership([list(range(cfg.experts_total))])
+    node.load_params(params)
+    node.outer_begin()
+    theta = params.copy()
+    buf = np.zeros(theta.size)
+    k = 0 if kind == "sgd" else 1
+    for rnd in range(2):
+        node.local_round(oracle.random_tokens(cfg, 2, 64, 42 + rnd, H=2), adamw_cfg(lr=1e-3))
+        local = node.read_params()
+        node.outer_sync(kind, lr=0.7, momentum=0.9)
+        oracle.outer_step(k, 0.7, 0.9, theta, local[None], buf)
+        assert bitexact(node.read_params(), theta), f"round {rnd}"
+    node.close()

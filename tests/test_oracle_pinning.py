@@ -257,3 +257,33 @@ def test_kat_cosine():
     s = oracle.similarity(cfg, p, 0)
     assert abs(s[0, 1] - 1) < 1e-12 and abs(s[0, 2]) < 1e-12
     assert abs(s[0, 3] - 1 / np.sqrt(2)) < 1e-12 and s[0, 4] == 0 and s[4, 4] == 0
+
+
+@pytest.mark.parametrize("kind,N", [(0, 1), (0, 3), (1, 1), (1, 3)])
+def test_outer_optimizer_bitexact(kind, N):
+    """OuterOptimizer::step (trainer.hpp:228-266) over 3 rounds, state carried."""
+    R = oracle.ref()
+    cfg = model_cfg(**TINY)
+    theta_ref = oracle.random_params(cfg, 31)
+    theta_or = theta_ref.copy()
+    buf = np.zeros(theta_or.size)
+    h = R.ref_outer_create(kind, 0.7, 0.9)
+    try:
+        rng = np.random.default_rng(32)
+        for _ in range(3):
+            locals_ = np.stack([theta_ref + (rng.standard_normal(theta_ref.size) * 1e-2)
+                                .astype(np.float32) for _ in range(N)])
+            assert R.ref_outer_step(h, C.byref(cfg), theta_ref, np.ascontiguousarray(locals_), N) == 0
+            oracle.outer_step(kind, 0.7, 0.9, theta_or, locals_, buf)
+            assert_bitexact(theta_or, theta_ref, f"outer kind={kind} N={N}")
+    finally:
+        R.ref_outer_destroy(h)
+
+
+def test_outer_sgd_lr1_single_node_reproduces_local():
+    """trainer.hpp:232-234: SGD with lr = 1 and N = 1 reproduces the local params exactly."""
+    cfg = model_cfg(**TINY)
+    theta = oracle.random_params(cfg, 33)
+    local = theta + np.float32(0.01)
+    oracle.outer_step(0, 1.0, 0.9, theta, local[None], np.zeros(theta.size))
+    assert_bitexact(theta, local, "sgd lr=1")
