@@ -175,6 +175,17 @@ spes_status spes_merge(spes_ctx* ctx, const spes_merge_sched* sched, int32_t rou
 /* similarity_matrix (merging.hpp:55-82) of one layer, M x M doubles. */
 spes_status spes_similarity(spes_ctx* ctx, int32_t layer, int32_t source, double* sim_out);
 
+/* ---- upcycling ----
+ * upcycle_from_dense (model.hpp:415-460): a dense model (experts_total == 1) -> an m-expert
+ * model: embedding / norms / head copied, routers widened by replicating their column,
+ * every expert a copy of the dense FFN with a noise_frac subset of its elements perturbed
+ * by N(0, noise_std) draws (std::mt19937_64(seed), libstdc++ distributions, the reference's
+ * draw order => bit-identical), renormalize_after_topk = 1. out_cfg may be NULL; out_params
+ * holds spes_param_count(out_cfg) floats. invalid_argument: dense M != 1, m < 2. */
+spes_status spes_upcycle_from_dense(const spes_model_cfg* dense_cfg, const float* dense_params,
+                                    int32_t m, double noise_frac, double noise_std, uint64_t seed,
+                                    spes_model_cfg* out_cfg, float* out_params);
+
 /* ---- wire / checkpoint format (proj/src/wire.cpp) ----
  * Byte-identical to the reference: encode_blocks(model_to_blocks(params)) is the
  * GLOBAL_MODEL payload (wire.cpp:96-115,154-159); a checkpoint is that payload followed by

@@ -140,6 +140,8 @@ def ref():
         R.ref_lr_at.argtypes = [C.c_double, C.c_double, C.c_int64, C.c_int64, C.c_int64]
         R.ref_param_partition.argtypes = [_cfgp, C.c_int32, _i32p, _i32p]
         _u8 = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+        R.ref_upcycle.restype = C.c_int
+        R.ref_upcycle.argtypes = [_cfgp, _f32p, C.c_int32, C.c_double, C.c_double, C.c_uint64, _f32p]
         R.ref_outer_create.restype = C.c_void_p
         R.ref_outer_create.argtypes = [C.c_int32, C.c_double, C.c_double]
         R.ref_outer_destroy.argtypes = [C.c_void_p]

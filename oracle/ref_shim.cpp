@@ -424,3 +424,18 @@ int ref_outer_step(void* h, const spes_model_cfg* c, float* theta, const float* 
     }
 }
 }  // extern "C"
+
+// ---- upcycle_from_dense (model.hpp:415-460) ----
+extern "C" int ref_upcycle(const spes_model_cfg* dense_cfg, const float* dense, int32_t m,
+                           double noise_frac, double noise_std, uint64_t seed, float* out) {
+    try {
+        ModelConfig cfg = to_cfg(dense_cfg);
+        ModelParams up = upcycle_from_dense(from_flat(cfg, dense), m, noise_frac, noise_std, seed);
+        to_flat(up, out);
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return 1;
+    } catch (...) {
+        return 2;
+    }
+}

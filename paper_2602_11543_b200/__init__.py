@@ -76,6 +76,8 @@ def lib():
         L.spes_read_grads.argtypes = [vp, f32p, i64]
         L.spes_set_fused_optimizer.argtypes = [vp, C.c_int32]
         L.spes_outer_begin.argtypes = [vp]
+        L.spes_upcycle_from_dense.argtypes = [C.POINTER(ModelCfg), f32p, C.c_int32, C.c_double,
+                                              C.c_double, C.c_uint64, C.POINTER(ModelCfg), f32p]
         L.spes_outer_sync.argtypes = [vp, C.c_int32, C.c_double, C.c_double, C.POINTER(SyncStats)]
         u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
         L.spes_model_payload_bytes.restype = i64
@@ -210,6 +212,18 @@ def decode_model(cfg, payload):
     out = np.zeros(param_count(cfg), np.float32)
     _check(lib().spes_decode_model_host(C.byref(cfg), payload, payload.size, f32(out)))
     return out
+
+
+def upcycle_from_dense(dense_cfg, dense_params, m, noise_frac=0.5, noise_std=0.02, seed=1):
+    """upcycle_from_dense (model.hpp:415-460) -> (cfg with m experts and renorm, params)."""
+    out_cfg = ModelCfg()
+    probe = ModelCfg.from_buffer_copy(dense_cfg)
+    probe.experts_total = m
+    out = np.zeros(param_count(probe), np.float32)
+    dense_params = np.ascontiguousarray(dense_params, np.float32)
+    _check(lib().spes_upcycle_from_dense(C.byref(dense_cfg), f32(dense_params), m, noise_frac,
+                                         noise_std, seed, C.byref(out_cfg), f32(out)))
+    return out_cfg, out
 
 
 class Node:

@@ -1023,6 +1023,32 @@ spes_status spes_load_params(spes_ctx* c, const float* host, int64_t n) {
     });
 }
 
+// ---- upcycling (model.hpp:415-460), host side: upcycle.cpp ----
+extern "C++" {
+namespace spes_upcycle {
+void upcycle(int64_t V, int64_t d, int64_t f, int L, const float* dense, int m, double noise_frac,
+             double noise_std, uint64_t seed, float* out);
+}
+}
+
+spes_status spes_upcycle_from_dense(const spes_model_cfg* dense_cfg, const float* dense_params,
+                                    int32_t m, double noise_frac, double noise_std, uint64_t seed,
+                                    spes_model_cfg* out_cfg, float* out_params) {
+    return guard([&] {
+        if (dense_cfg->experts_total != 1)
+            throw std::invalid_argument("upcycle: source must have a single expert");
+        if (m < 2) throw std::invalid_argument("upcycle: need M >= 2");
+        if (dense_cfg->tied_head) throw std::logic_error("tied head not implemented");
+        spes_model_cfg oc = *dense_cfg;
+        oc.experts_total = m;
+        oc.renormalize_after_topk = 1;
+        spes_upcycle::upcycle(dense_cfg->vocab, dense_cfg->hidden, dense_cfg->intermediate,
+                              dense_cfg->layers, dense_params, m, noise_frac, noise_std, seed,
+                              out_params);
+        if (out_cfg) *out_cfg = oc;
+    });
+}
+
 // ---- wire / checkpoint format (proj/src/wire.cpp:96-176, 212-236) ----
 namespace {
 std::vector<spes_wire::Block> wire_blocks(const spes_model_cfg* cfg) {

@@ -334,3 +334,28 @@ def test_outer_sync_single_node_matches_oracle(gpu, kind):
         oracle.outer_step(k, 0.7, 0.9, theta, local[None], buf)
         assert bitexact(node.read_params(), theta), f"round {rnd}"
     node.close()
+
+
+def test_upcycled_model_local_step(gpu):
+    """An upcycled model (model.hpp:415-460; renorm on, identical router columns => every
+    token's expert probabilities tie exactly) trains on B200 with the oracle's routing
+    (stable ties -> lowest indices) bit-exact and losses within tolerance."""
+    dense_cfg = model_cfg(vocab=256, hidden=128, intermediate=256, layers=2, experts_total=1,
+                          experts_active=1)
+    dense = oracle.random_params(dense_cfg, 51)
+    ucfg, up = spes.upcycle_from_dense(dense_cfg, dense, 8, 0.5, 0.02, 52)
+    ucfg.experts_active = 2
+    tokens = oracle.random_tokens(ucfg, 2, 64, 53)[0]
+    owned = [0, 1, 2, 3]
+    node = spes.Node(ucfg, 0, 1, 0)
+    node.set_ownership([owned])
+    node.load_params(up)
+    node.round_begin()
+    losses = node.local_step(tokens, adamw_cfg())
+    l_ref, _, tr = oracle.forward_backward(ucfg, up, tokens, owned, trace=True)
+    T = 2 * 64
+    idx0 = node.debug("topk_idx", 0, np.int32, (T, 2), T * 2)
+    assert bitexact(idx0, tr["topk_idx"][0])
+    assert (idx0 == np.array([0, 1])).all()  # exact ties -> lowest indices
+    assert abs(losses[0] - l_ref[0]) <= LOSS_RTOL * abs(l_ref[0])
+    node.close()
