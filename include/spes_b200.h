@@ -175,6 +175,31 @@ spes_status spes_merge(spes_ctx* ctx, const spes_merge_sched* sched, int32_t rou
 /* similarity_matrix (merging.hpp:55-82) of one layer, M x M doubles. */
 spes_status spes_similarity(spes_ctx* ctx, int32_t layer, int32_t source, double* sim_out);
 
+/* ---- synthetic corpus and batch streams (proj/src/corpus.cpp) ----
+ * Host generators bit-identical with the reference (same std::mt19937_64 / libstdc++
+ * distributions and draw order): gen_corpus (corpus.cpp:49-79; tokens: sequences x (S+1),
+ * source_id may be NULL), shard_corpus (:107-128; order + N+1 node offsets), and the index
+ * stream of make_batch_provider (:130-149). The corpus is uploaded to HBM once; a step then
+ * transfers only its B row indices and gathers the batch on the device. */
+typedef struct spes_batch_stream spes_batch_stream;
+spes_status spes_gen_corpus(int64_t vocab, int64_t seq, int32_t sources, int64_t sequences,
+                            uint64_t seed, double skew, int32_t* tokens, int32_t* source_id);
+spes_status spes_shard_corpus(const int32_t* source_id, int64_t sequences, int32_t nodes,
+                              int32_t by_source, uint64_t seed, int64_t* order,
+                              int64_t* node_offsets);
+spes_status spes_batch_stream_create(const int64_t* shard, int64_t n, int64_t batch, uint64_t seed,
+                                     spes_batch_stream** out);
+spes_status spes_batch_stream_next(spes_batch_stream* s, int64_t* rows);
+void spes_batch_stream_destroy(spes_batch_stream* s);
+/* corpus -> HBM (token ids validated once) */
+spes_status spes_corpus_load(spes_ctx* ctx, const int32_t* tokens, int64_t sequences, int64_t seq);
+/* local step / round over corpus rows (rows: B, resp. H x B indices) */
+spes_status spes_local_step_rows(spes_ctx* ctx, const int64_t* rows, int64_t B,
+                                 const spes_adamw_cfg* opt, spes_losses* losses);
+spes_status spes_local_round_rows(spes_ctx* ctx, const int64_t* rows, int64_t B, int32_t H,
+                                  const double* lr, const spes_adamw_cfg* opt, int32_t carry_state,
+                                  spes_losses* per_step);
+
 /* ---- upcycling ----
  * upcycle_from_dense (model.hpp:415-460): a dense model (experts_total == 1) -> an m-expert
  * model: embedding / norms / head copied, routers widened by replicating their column,

@@ -140,6 +140,14 @@ def ref():
         R.ref_lr_at.argtypes = [C.c_double, C.c_double, C.c_int64, C.c_int64, C.c_int64]
         R.ref_param_partition.argtypes = [_cfgp, C.c_int32, _i32p, _i32p]
         _u8 = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+        _i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+        R.ref_gen_corpus.restype = C.c_int
+        R.ref_gen_corpus.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.c_int64, C.c_uint64,
+                                     C.c_double, _i32p, _i32p]
+        R.ref_shard_corpus.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.c_int64, C.c_uint64,
+                                       C.c_int32, C.c_int32, C.c_uint64, _i64p, _i64p]
+        R.ref_batches.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.c_int64, C.c_uint64, _i64p,
+                                  C.c_int64, C.c_int64, C.c_uint64, C.c_int32, _i32p]
         R.ref_upcycle.restype = C.c_int
         R.ref_upcycle.argtypes = [_cfgp, _f32p, C.c_int32, C.c_double, C.c_double, C.c_uint64, _f32p]
         R.ref_outer_create.restype = C.c_void_p

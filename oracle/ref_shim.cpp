@@ -8,6 +8,7 @@
 #include <span>
 #include <vector>
 
+#include "spes/corpus.hpp"
 #include "spes/experiment.hpp"
 #include "spes/merging.hpp"
 #include "spes/model.hpp"
@@ -439,3 +440,45 @@ extern "C" int ref_upcycle(const spes_model_cfg* dense_cfg, const float* dense, 
         return 2;
     }
 }
+
+// ---- corpus.cpp: gen_corpus / shard_corpus / make_batch_provider ----
+extern "C" {
+int ref_gen_corpus(int64_t vocab, int64_t seq, int32_t sources, int64_t sequences, uint64_t seed,
+                   double skew, int32_t* tokens, int32_t* source_id) {
+    try {
+        SyntheticCorpus c = gen_corpus(vocab, seq, sources, sequences, seed, skew);
+        std::memcpy(tokens, c.tokens.data(), sizeof(int32_t) * c.tokens.size());
+        for (size_t i = 0; i < c.source_id.size(); ++i) source_id[i] = c.source_id[i];
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return 1;
+    }
+}
+// shards flattened: order + node offsets (N + 1)
+int ref_shard_corpus(int64_t vocab, int64_t seq, int32_t sources, int64_t sequences,
+                     uint64_t cseed, int32_t nodes, int32_t by_source, uint64_t seed,
+                     int64_t* order, int64_t* offsets) {
+    SyntheticCorpus c = gen_corpus(vocab, seq, sources, sequences, cseed, 0.0);
+    auto sh = shard_corpus(c, nodes, by_source ? ShardPolicy::BySource : ShardPolicy::Random, seed);
+    int64_t k = 0;
+    offsets[0] = 0;
+    for (size_t i = 0; i < sh.size(); ++i) {
+        for (int64_t r : sh[i]) order[k++] = r;
+        offsets[i + 1] = k;
+    }
+    return 0;
+}
+// H batches of the provider over a shard -> tokens H x B x (S+1)
+int ref_batches(int64_t vocab, int64_t seq, int32_t sources, int64_t sequences, uint64_t cseed,
+                const int64_t* shard, int64_t n, int64_t batch, uint64_t seed, int32_t H,
+                int32_t* out) {
+    SyntheticCorpus c = gen_corpus(vocab, seq, sources, sequences, cseed, 0.0);
+    BatchProvider p = make_batch_provider(c, std::vector<int64_t>(shard, shard + n), batch, seed);
+    for (int32_t h = 0; h < H; ++h) {
+        Batch b = p();
+        std::memcpy(out + static_cast<int64_t>(h) * batch * (seq + 1), b.tokens.data(),
+                    sizeof(int32_t) * b.tokens.size());
+    }
+    return 0;
+}
+}  // extern "C"

@@ -76,6 +76,19 @@ def lib():
         L.spes_read_grads.argtypes = [vp, f32p, i64]
         L.spes_set_fused_optimizer.argtypes = [vp, C.c_int32]
         L.spes_outer_begin.argtypes = [vp]
+        i64p = C.POINTER(C.c_int64)
+        L.spes_gen_corpus.argtypes = [i64, i64, C.c_int32, i64, C.c_uint64, C.c_double,
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+        L.spes_shard_corpus.argtypes = [C.POINTER(C.c_int32), i64, C.c_int32, C.c_int32,
+                                        C.c_uint64, i64p, i64p]
+        L.spes_batch_stream_create.argtypes = [i64p, i64, i64, C.c_uint64, C.POINTER(vp)]
+        L.spes_batch_stream_next.argtypes = [vp, i64p]
+        L.spes_batch_stream_destroy.argtypes = [vp]
+        L.spes_batch_stream_destroy.restype = None
+        L.spes_corpus_load.argtypes = [vp, C.POINTER(C.c_int32), i64, i64]
+        L.spes_local_step_rows.argtypes = [vp, i64p, i64, C.POINTER(AdamWCfg), C.POINTER(Losses)]
+        L.spes_local_round_rows.argtypes = [vp, i64p, i64, C.c_int32, C.POINTER(C.c_double),
+                                            C.POINTER(AdamWCfg), C.c_int32, C.POINTER(Losses)]
         L.spes_upcycle_from_dense.argtypes = [C.POINTER(ModelCfg), f32p, C.c_int32, C.c_double,
                                               C.c_double, C.c_uint64, C.POINTER(ModelCfg), f32p]
         L.spes_outer_sync.argtypes = [vp, C.c_int32, C.c_double, C.c_double, C.POINTER(SyncStats)]
@@ -214,6 +227,51 @@ def decode_model(cfg, payload):
     return out
 
 
+# ---- synthetic corpus / batch streams (proj/src/corpus.cpp), bit-identical ----
+
+def _i64(a):
+    return _p(a, C.c_int64)
+
+
+def gen_corpus(vocab, seq, sources, sequences, seed, skew=0.0):
+    """gen_corpus (corpus.cpp:49-79) -> (tokens [sequences, seq+1] int32, source_id int32)."""
+    tok = np.zeros((sequences, seq + 1), np.int32)
+    sid = np.zeros(sequences, np.int32)
+    _check(lib().spes_gen_corpus(vocab, seq, sources, sequences, seed, skew, i32(tok), i32(sid)))
+    return tok, sid
+
+
+def shard_corpus(source_id, nodes, by_source, seed):
+    """shard_corpus (corpus.cpp:107-128) -> list of per-node row index arrays."""
+    source_id = np.ascontiguousarray(source_id, np.int32)
+    order = np.zeros(source_id.size, np.int64)
+    offs = np.zeros(nodes + 1, np.int64)
+    _check(lib().spes_shard_corpus(i32(source_id), source_id.size, nodes, 1 if by_source else 0,
+                                   seed, _i64(order), _i64(offs)))
+    return [order[offs[i]:offs[i + 1]] for i in range(nodes)]
+
+
+class BatchStream:
+    """make_batch_provider's row stream (corpus.cpp:130-149): shuffled epochs, wrap-around."""
+
+    def __init__(self, shard, batch, seed):
+        shard = np.ascontiguousarray(shard, np.int64)
+        self.batch = batch
+        self._s = C.c_void_p()
+        _check(lib().spes_batch_stream_create(_i64(shard), shard.size, batch, seed,
+                                              C.byref(self._s)))
+
+    def next(self):
+        rows = np.zeros(self.batch, np.int64)
+        _check(lib().spes_batch_stream_next(self._s, _i64(rows)))
+        return rows
+
+    def __del__(self):
+        if getattr(self, "_s", None):
+            lib().spes_batch_stream_destroy(self._s)
+            self._s = None
+
+
 def upcycle_from_dense(dense_cfg, dense_params, m, noise_frac=0.5, noise_std=0.02, seed=1):
     """upcycle_from_dense (model.hpp:415-460) -> (cfg with m experts and renorm, params)."""
     out_cfg = ModelCfg()
@@ -278,6 +336,32 @@ class Node:
         """Owned experts' AdamW inside the dW GEMM epilogue (default) or as a separate pass
         with materialized gradients (needed by read_grads); identical bits either way."""
         _check(lib().spes_set_fused_optimizer(self._ctx, 1 if on else 0))
+
+    def corpus_load(self, tokens):
+        """Upload a corpus [sequences, S+1] to HBM once (token ids validated here)."""
+        tokens = np.ascontiguousarray(tokens, np.int32)
+        _check(lib().spes_corpus_load(self._ctx, i32(tokens), tokens.shape[0], tokens.shape[1] - 1))
+
+    def local_step_rows(self, rows, opt=None):
+        rows = np.ascontiguousarray(rows, np.int64)
+        lo = Losses()
+        _check(lib().spes_local_step_rows(self._ctx, _i64(rows), rows.size,
+                                          C.byref(opt or adamw_cfg()), C.byref(lo)))
+        return (lo.total, lo.ce, lo.lb, lo.moe_z, lo.z)
+
+    def local_round_rows(self, rows, opt=None, lr=None, carry_state=False):
+        """rows: H x B corpus row indices; returns losses [H, 5]."""
+        rows = np.ascontiguousarray(rows, np.int64)
+        H, B = rows.shape
+        out = (Losses * H)()
+        lr_p = None
+        if lr is not None:
+            lr_arr = (C.c_double * H)(*lr)
+            lr_p = C.cast(lr_arr, C.POINTER(C.c_double))
+        _check(lib().spes_local_round_rows(self._ctx, _i64(rows), B, H, lr_p,
+                                           C.byref(opt or adamw_cfg()), 1 if carry_state else 0,
+                                           out))
+        return np.array([(o.total, o.ce, o.lb, o.moe_z, o.z) for o in out])
 
     def outer_begin(self):
         """DiLoCo baseline: snapshot the round-start global model (this rank's slice)."""

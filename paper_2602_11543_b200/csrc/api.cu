@@ -162,6 +162,11 @@ struct spes_ctx {
     spes_k::AdamScalars cur_adam{};  // this step's AdamW scalars (set before backward)
     // DiLoCo baseline: this rank's slice of the round-start global model,
     // its fp64 Nesterov buffer, and the exchange buffers (N x slice each)
+    // device corpus: sequences x (S+1) tokens resident in HBM
+    int32_t* corpus = nullptr;
+    int64_t corpus_rows = 0, corpus_seq = 0;
+    int64_t* d_rows = nullptr;
+    int64_t d_rows_cap = 0;
     float *outer_theta = nullptr, *outer_recv = nullptr, *outer_gather = nullptr;
     double* outer_buf = nullptr;
     int64_t outer_slice = 0;
@@ -984,6 +989,8 @@ void spes_destroy(spes_ctx* c) {
     c->scratch.release();
     c->persistent.release();
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->corpus) cudaFree(c->corpus);
+    if (c->d_rows) cudaFree(c->d_rows);
     delete c;
 }
 
@@ -1228,6 +1235,130 @@ spes_status spes_local_round(spes_ctx* c, const int32_t* tokens, int64_t B, int6
             spes_losses tmp;
             spes_losses* lo = per_step ? &per_step[h] : &tmp;
             local_step_impl(c, B, S, &o, lo);
+            if (!std::isfinite(lo->total))
+                throw std::runtime_error("local_round: non-finite loss at step " + std::to_string(h));
+        }
+    });
+}
+
+// ---- device corpus and batch streams (corpus.cpp) ----
+extern "C++" {
+namespace spes_corpus {
+struct BatchStream;
+void gen_corpus(int64_t vocab, int64_t seq, int sources, int64_t sequences, uint64_t seed,
+                double skew, int32_t* tokens, int32_t* source_id);
+void shard_corpus(const int32_t* source_id, int64_t n, int nodes, int by_source, uint64_t seed,
+                  int64_t* order, int64_t* offsets);
+BatchStream* stream_create(const int64_t* shard, int64_t n, int64_t batch, uint64_t seed);
+void stream_next(BatchStream* s, int64_t* rows);
+void stream_destroy(BatchStream* s);
+}
+}
+struct spes_batch_stream {
+    spes_corpus::BatchStream* s;
+};
+
+spes_status spes_gen_corpus(int64_t vocab, int64_t seq, int32_t sources, int64_t sequences,
+                            uint64_t seed, double skew, int32_t* tokens, int32_t* source_id) {
+    return guard([&] {
+        spes_corpus::gen_corpus(vocab, seq, sources, sequences, seed, skew, tokens, source_id);
+    });
+}
+
+spes_status spes_shard_corpus(const int32_t* source_id, int64_t sequences, int32_t nodes,
+                              int32_t by_source, uint64_t seed, int64_t* order,
+                              int64_t* node_offsets) {
+    return guard([&] {
+        spes_corpus::shard_corpus(source_id, sequences, nodes, by_source, seed, order, node_offsets);
+    });
+}
+
+spes_status spes_batch_stream_create(const int64_t* shard, int64_t n, int64_t batch, uint64_t seed,
+                                     spes_batch_stream** out) {
+    return guard([&] {
+        *out = new spes_batch_stream{spes_corpus::stream_create(shard, n, batch, seed)};
+    });
+}
+
+spes_status spes_batch_stream_next(spes_batch_stream* s, int64_t* rows) {
+    return guard([&] { spes_corpus::stream_next(s->s, rows); });
+}
+
+void spes_batch_stream_destroy(spes_batch_stream* s) {
+    if (!s) return;
+    spes_corpus::stream_destroy(s->s);
+    delete s;
+}
+
+spes_status spes_corpus_load(spes_ctx* c, const int32_t* tokens, int64_t sequences, int64_t seq) {
+    return guard([&] {
+        if (sequences < 1 || seq < 1) throw std::invalid_argument("corpus: need sequences, S >= 1");
+        validate_tokens(c, tokens, sequences * (seq + 1));  // once, not per step
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        if (c->corpus) cudaFree(c->corpus);
+        c->corpus = nullptr;
+        ck(cudaMalloc(&c->corpus, sizeof(int32_t) * sequences * (seq + 1)), "corpus alloc");
+        ck(cudaMemcpy(c->corpus, tokens, sizeof(int32_t) * sequences * (seq + 1),
+                      cudaMemcpyHostToDevice),
+           "corpus H2D");
+        c->corpus_rows = sequences;
+        c->corpus_seq = seq;
+    });
+}
+
+namespace {
+void gather_corpus_rows(spes_ctx* c, const int64_t* rows, int64_t B) {
+    if (!c->corpus) throw std::logic_error("local_step_rows: no corpus loaded (spes_corpus_load)");
+    for (int64_t b = 0; b < B; ++b)
+        if (rows[b] < 0 || rows[b] >= c->corpus_rows)
+            throw std::out_of_range("batch: corpus row out of range");
+    if (B > c->d_rows_cap) {
+        if (c->d_rows) cudaFree(c->d_rows);
+        ck(cudaMalloc(&c->d_rows, sizeof(int64_t) * B), "rows alloc");
+        c->d_rows_cap = B;
+    }
+    // pageable source: staged by the driver, safe to reuse right after the call
+    ck(cudaMemcpyAsync(c->d_rows, rows, sizeof(int64_t) * B, cudaMemcpyHostToDevice, c->stream),
+       "H2D rows");
+    spes_k::corpus_gather(c->corpus, c->d_rows, B, c->corpus_seq + 1, c->tokens, c->stream);
+}
+}  // namespace
+
+spes_status spes_local_step_rows(spes_ctx* c, const int64_t* rows, int64_t B,
+                                 const spes_adamw_cfg* opt, spes_losses* losses) {
+    return guard([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        set_counter(c);
+        if (B < 1) throw std::invalid_argument("batch: need B >= 1");
+        ensure_activations(c, B, c->corpus_seq);
+        gather_corpus_rows(c, rows, B);
+        local_step_impl(c, B, c->corpus_seq, opt, losses);
+        if (losses && !std::isfinite(losses->total))
+            throw std::runtime_error("local_round: non-finite loss at step 0");
+    });
+}
+
+spes_status spes_local_round_rows(spes_ctx* c, const int64_t* rows, int64_t B, int32_t H,
+                                  const double* lr, const spes_adamw_cfg* opt, int32_t carry_state,
+                                  spes_losses* per_step) {
+    return guard([&] {
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        set_counter(c);
+        if (H < 1) throw std::invalid_argument("local_round: need H >= 1");
+        if (B < 1) throw std::invalid_argument("batch: need B >= 1");
+        if (!carry_state) {
+            ck(cudaMemsetAsync(c->m, 0, sizeof(float) * c->G, c->stream), "m");
+            ck(cudaMemsetAsync(c->v, 0, sizeof(float) * c->G, c->stream), "v");
+            c->adam_step = 0;
+        }
+        ensure_activations(c, B, c->corpus_seq);
+        for (int h = 0; h < H; ++h) {
+            gather_corpus_rows(c, rows + static_cast<int64_t>(h) * B, B);
+            spes_adamw_cfg o = *opt;
+            if (lr) o.lr = lr[h];
+            spes_losses tmp;
+            spes_losses* lo = per_step ? &per_step[h] : &tmp;
+            local_step_impl(c, B, c->corpus_seq, &o, lo);
             if (!std::isfinite(lo->total))
                 throw std::runtime_error("local_round: non-finite loss at step " + std::to_string(h));
         }

@@ -975,6 +975,22 @@ void embed_grad(const int32_t* inputs, const float* gh0, int64_t T, int64_t d, i
     count_launch();
 }
 
+// ============================ device corpus batches ============================
+// batch row b = corpus row rows[b] (S+1 tokens), make_batch (corpus.cpp:81-87)
+__global__ void corpus_gather_k(const int32_t* __restrict__ corpus, const int64_t* __restrict__ rows,
+                                int64_t S1, int32_t* __restrict__ tokens) {
+    const int64_t b = blockIdx.x;
+    const int32_t* src = corpus + rows[b] * S1;
+    int32_t* dst = tokens + b * S1;
+    for (int64_t p = threadIdx.x; p < S1; p += blockDim.x) dst[p] = __ldg(src + p);
+}
+
+void corpus_gather(const int32_t* corpus, const int64_t* rows, int64_t B, int64_t S1,
+                   int32_t* tokens, cudaStream_t s) {
+    corpus_gather_k<<<static_cast<unsigned>(B), 256, 0, s>>>(corpus, rows, S1, tokens);
+    count_launch();
+}
+
 // ============================ DiLoCo outer step (trainer.hpp:228-266) ============================
 // This rank's slice of the global model: theta <- OuterOpt(theta, mean_i(local_i - theta)),
 // per element in fp64 with the locals in node order (recv holds N x n, node-major); the

@@ -133,6 +133,10 @@ void adamw(float* params, const float* grads, float* m, float* v, const AdamSeg*
 void refresh_shadows(const float* params, const AdamSeg* segs, int nseg, int64_t total,
                      Shadows sh, cudaStream_t s);
 
+// batch tokens B x (S+1) from the HBM-resident corpus rows
+void corpus_gather(const int32_t* corpus, const int64_t* rows, int64_t B, int64_t S1,
+                   int32_t* tokens, cudaStream_t s);
+
 // ---- sync / merge ----
 // DiLoCo outer step over this rank's slice (theta, n scalars): recv = the N nodes' local
 // slices (stride ld, node order); kind 0 SGD, 1 Nesterov (buf: fp64 state); the new values
