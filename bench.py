@@ -410,7 +410,7 @@ def our_arm(args):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(H * B * (S + 1) * 4),
                 "d2h_bytes_per_step": int(H * 5 * 8), "steps": ke},
         "gpu_launches": int(dist.sum(launches)),
-        "roofline": {"bound": "tensor", "kernel": "grouped_gemm_kernel (tcgen05/TMEM/TMA, "
+        "roofline": {"bound": "tensor", "kernel": "grouped_gemm_2cta_kernel (tcgen05 cta_group::2/TMEM/TMA, "
                                                    "6 expert contractions)",
                      "achieved": achieved, "peak": sustained, "unit": "TFLOP/s",
                      "frac": achieved / sustained if sustained else None,
