@@ -372,43 +372,61 @@ void permute_rows_bf16(const bf16* src, int64_t cols, const int32_t* row_map,
 // ============================ combine (forward) ============================
 // h_next[t] = h[t] + sum over selected experts in ascending order of (0 + w*y)
 // (model.hpp:330-338: rowwise_mul, scatter_rows into zeros, add chain, residual add)
+// Block per token; each thread owns CF_U float4 columns (all their loads in flight first).
+constexpr int CF_U = 2;
+template <int KMAX>
 __global__ void combine_fwd_k(const float* __restrict__ h, const float* __restrict__ y,
                               const int32_t* __restrict__ slot_row, const float* __restrict__ w,
                               int64_t d, int k, float* __restrict__ h_next,
                               bf16* __restrict__ h_next_bf) {
     const int64_t t = blockIdx.x;
-    int32_t rows[8];
-    float ws[8];
-    for (int s = 0; s < k; ++s) {
-        rows[s] = slot_row[t * k + s];
-        ws[s] = w[t * k + s];
+    int32_t rows[KMAX];
+    float ws[KMAX];
+#pragma unroll
+    for (int s = 0; s < KMAX; ++s) {
+        rows[s] = s < k ? slot_row[t * k + s] : 0;
+        ws[s] = s < k ? w[t * k + s] : 0.f;
     }
-    for (int64_t q = threadIdx.x * 4; q < d; q += blockDim.x * 4) {
-        float4 acc;
-        {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(y + rows[0] * d + q));
-            acc.x = fadd(0.f, fmul(v.x, ws[0]));
-            acc.y = fadd(0.f, fmul(v.y, ws[0]));
-            acc.z = fadd(0.f, fmul(v.z, ws[0]));
-            acc.w = fadd(0.f, fmul(v.w, ws[0]));
+    const int64_t step = static_cast<int64_t>(blockDim.x) * 4;
+    for (int64_t q0 = threadIdx.x * 4; q0 < d; q0 += step * CF_U) {
+        float4 yv[CF_U][KMAX], hv[CF_U];
+#pragma unroll
+        for (int u = 0; u < CF_U; ++u) {
+            const int64_t q = q0 + u * step;
+            if (q < d) {
+#pragma unroll
+                for (int s = 0; s < KMAX; ++s)
+                    if (s < k) yv[u][s] = __ldg(reinterpret_cast<const float4*>(y + rows[s] * d + q));
+                hv[u] = __ldg(reinterpret_cast<const float4*>(h + t * d + q));
+            }
         }
-        for (int s = 1; s < k; ++s) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(y + rows[s] * d + q));
-            acc.x = fadd(acc.x, fadd(0.f, fmul(v.x, ws[s])));
-            acc.y = fadd(acc.y, fadd(0.f, fmul(v.y, ws[s])));
-            acc.z = fadd(acc.z, fadd(0.f, fmul(v.z, ws[s])));
-            acc.w = fadd(acc.w, fadd(0.f, fmul(v.w, ws[s])));
-        }
-        const float4 hv = __ldg(reinterpret_cast<const float4*>(h + t * d + q));
-        const float4 o = make_float4(fadd(hv.x, acc.x), fadd(hv.y, acc.y), fadd(hv.z, acc.z),
-                                     fadd(hv.w, acc.w));
-        *reinterpret_cast<float4*>(h_next + t * d + q) = o;
-        if (h_next_bf) {  // last layer: the head GEMM's bf16 operand, no separate pass
-            __nv_bfloat162 a = __floats2bfloat162_rn(o.x, o.y), b = __floats2bfloat162_rn(o.z, o.w);
-            uint2 pk;
-            pk.x = *reinterpret_cast<uint32_t*>(&a);
-            pk.y = *reinterpret_cast<uint32_t*>(&b);
-            *reinterpret_cast<uint2*>(h_next_bf + t * d + q) = pk;
+#pragma unroll
+        for (int u = 0; u < CF_U; ++u) {
+            const int64_t q = q0 + u * step;
+            if (q >= d) continue;
+            float4 acc;
+            acc.x = fadd(0.f, fmul(yv[u][0].x, ws[0]));
+            acc.y = fadd(0.f, fmul(yv[u][0].y, ws[0]));
+            acc.z = fadd(0.f, fmul(yv[u][0].z, ws[0]));
+            acc.w = fadd(0.f, fmul(yv[u][0].w, ws[0]));
+#pragma unroll
+            for (int s = 1; s < KMAX; ++s) {
+                if (s >= k) break;
+                acc.x = fadd(acc.x, fadd(0.f, fmul(yv[u][s].x, ws[s])));
+                acc.y = fadd(acc.y, fadd(0.f, fmul(yv[u][s].y, ws[s])));
+                acc.z = fadd(acc.z, fadd(0.f, fmul(yv[u][s].z, ws[s])));
+                acc.w = fadd(acc.w, fadd(0.f, fmul(yv[u][s].w, ws[s])));
+            }
+            const float4 o = make_float4(fadd(hv[u].x, acc.x), fadd(hv[u].y, acc.y),
+                                         fadd(hv[u].z, acc.z), fadd(hv[u].w, acc.w));
+            *reinterpret_cast<float4*>(h_next + t * d + q) = o;
+            if (h_next_bf) {  // last layer: the head GEMM's bf16 operand, no separate pass
+                __nv_bfloat162 a = __floats2bfloat162_rn(o.x, o.y), b = __floats2bfloat162_rn(o.z, o.w);
+                uint2 pk;
+                pk.x = *reinterpret_cast<uint32_t*>(&a);
+                pk.y = *reinterpret_cast<uint32_t*>(&b);
+                *reinterpret_cast<uint2*>(h_next_bf + t * d + q) = pk;
+            }
         }
     }
 }
@@ -417,9 +435,13 @@ void combine_forward(const float* h, const float* y, const int32_t* slot_row,
                      const int32_t* topk_idx, const float* topk_w, int64_t T, int64_t d, int k,
                      float* h_next, bf16* h_next_bf, cudaStream_t s) {
     (void)topk_idx;
-    const int threads = d >= 1024 ? 256 : static_cast<int>(d / 4);
-    combine_fwd_k<<<static_cast<unsigned>(T), threads, 0, s>>>(h, y, slot_row, topk_w, d, k,
-                                                               h_next, h_next_bf);
+    const int threads = d >= 4 * 128 * CF_U ? 128 : static_cast<int>(cdiv(d / 4, CF_U));
+    if (k <= 2)
+        combine_fwd_k<2><<<static_cast<unsigned>(T), threads, 0, s>>>(h, y, slot_row, topk_w, d, k,
+                                                                      h_next, h_next_bf);
+    else
+        combine_fwd_k<8><<<static_cast<unsigned>(T), threads, 0, s>>>(h, y, slot_row, topk_w, d, k,
+                                                                      h_next, h_next_bf);
     count_launch();
 }
 
@@ -622,19 +644,31 @@ __global__ void __launch_bounds__(256) combine_bwd_k(
     const int32_t t = row_token[r];
     const float wv = t >= 0 ? row_w[r] : 0.f;
     float dot = 0.f;
-    for (int64_t q = lane * 4; q < d; q += 128) {
-        float4 g = make_float4(0.f, 0.f, 0.f, 0.f), yv = g;
-        if (t >= 0) {
-            g = __ldg(reinterpret_cast<const float4*>(gh + static_cast<int64_t>(t) * d + q));
-            yv = __ldg(reinterpret_cast<const float4*>(y + r * d + q));
+    constexpr int CB_U = 4;  // column groups per pass, loads first
+    for (int64_t q0 = lane * 4; q0 < d; q0 += 128 * CB_U) {
+        float4 g[CB_U], yv[CB_U];
+#pragma unroll
+        for (int u = 0; u < CB_U; ++u) {
+            const int64_t q = q0 + 128 * u;
+            g[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            yv[u] = g[u];
+            if (t >= 0 && q < d) {
+                g[u] = __ldg(reinterpret_cast<const float4*>(gh + static_cast<int64_t>(t) * d + q));
+                yv[u] = __ldg(reinterpret_cast<const float4*>(y + r * d + q));
+            }
         }
-        __nv_bfloat162 p0 = __floats2bfloat162_rn(g.x * wv, g.y * wv);
-        __nv_bfloat162 p1 = __floats2bfloat162_rn(g.z * wv, g.w * wv);
-        uint2 pk;
-        pk.x = *reinterpret_cast<uint32_t*>(&p0);
-        pk.y = *reinterpret_cast<uint32_t*>(&p1);
-        *reinterpret_cast<uint2*>(dyw + r * d + q) = pk;
-        dot += ((g.x * yv.x + g.y * yv.y) + g.z * yv.z) + g.w * yv.w;
+#pragma unroll
+        for (int u = 0; u < CB_U; ++u) {
+            const int64_t q = q0 + 128 * u;
+            if (q >= d) break;
+            __nv_bfloat162 p0 = __floats2bfloat162_rn(g[u].x * wv, g[u].y * wv);
+            __nv_bfloat162 p1 = __floats2bfloat162_rn(g[u].z * wv, g[u].w * wv);
+            uint2 pk;
+            pk.x = *reinterpret_cast<uint32_t*>(&p0);
+            pk.y = *reinterpret_cast<uint32_t*>(&p1);
+            *reinterpret_cast<uint2*>(dyw + r * d + q) = pk;
+            dot += ((g[u].x * yv[u].x + g[u].y * yv[u].y) + g[u].z * yv[u].z) + g[u].w * yv[u].w;
+        }
     }
     dot = warp_sum(dot);
     if (lane == 0) gw[r] = dot;
