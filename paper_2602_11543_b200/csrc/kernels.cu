@@ -966,13 +966,14 @@ __global__ void __launch_bounds__(64) embed_grad_sum_k(const int32_t* __restrict
     const int32_t i0 = off[v], i1 = off[v + 1];
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     int32_t i = i0;
-    for (; i + 8 <= i1; i += 8) {
-        float4 g[8];
+    constexpr int EU = 16;  // rows in flight
+    for (; i + EU <= i1; i += EU) {
+        float4 g[EU];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < EU; ++u)
             g[u] = __ldg(reinterpret_cast<const float4*>(gh0 + static_cast<int64_t>(list[i + u]) * d + q));
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < EU; ++u) {
             acc.x = fadd(acc.x, g[u].x);
             acc.y = fadd(acc.y, g[u].y);
             acc.z = fadd(acc.z, g[u].z);
