@@ -41,14 +41,19 @@ __device__ __forceinline__ uint2 pack_bf16x4(float a, float b, float c, float d)
     return u;
 }
 
+// TT = tokens per lane: 1 for M <= 16; 4 for M = 32 / 64, where each router value read
+// from shared memory then feeds 4 tokens' chains (the M = 64 kernel was bound by
+// shared-memory wavefronts at TT = 1)
 template <int MAXM>
 struct RfSmem {
     static constexpr int EPL = MAXM < 8 ? MAXM : 8;  // experts per lane
-    static constexpr int LPT = MAXM / EPL;           // lanes per token
-    static constexpr int TPW = 32 / LPT;             // tokens per warp
-    static constexpr int PITCH = RF_RCH + 4;  // padded row pitch (floats): conflict-free LDS.128
-    static constexpr int R_FLOATS = RF_XS * RF_RCH * MAXM;   // router row ring
-    static constexpr int G_FLOATS = RF_XS * RF_RCH;          // gain ring
+    static constexpr int LPT = MAXM / EPL;           // lanes per token group
+    static constexpr int TT = MAXM >= 32 ? 4 : 1;    // tokens per lane (per group)
+    static constexpr int TPW = TT * (32 / LPT);      // tokens per warp
+    static constexpr int RCH = MAXM >= 32 ? 32 : RF_RCH;  // columns (router rows) per chunk
+    static constexpr int PITCH = RCH + 4;  // padded row pitch (floats): conflict-free LDS.128
+    static constexpr int R_FLOATS = RF_XS * RCH * MAXM;   // router row ring
+    static constexpr int G_FLOATS = RF_XS * RCH;          // gain ring
     static constexpr int X_FLOATS = RF_WARPS * RF_XS * TPW * PITCH;  // per-warp token-row rings
     static constexpr int BYTES = 4 * (R_FLOATS + G_FLOATS + X_FLOATS);
 };
@@ -61,24 +66,24 @@ __global__ void __launch_bounds__(32 * RF_WARPS) router_fwd_k(
     int32_t* __restrict__ topk_idx, float* __restrict__ topk_w, float* __restrict__ lse_out,
     float* __restrict__ inv_out, float* __restrict__ denom_out) {
     using SM = RfSmem<MAXM>;
-    constexpr int EPL = SM::EPL, LPT = SM::LPT, TPW = SM::TPW;
-    constexpr int QC = RF_RCH / 4;  // float4 per row chunk
+    constexpr int EPL = SM::EPL, LPT = SM::LPT, TPW = SM::TPW, TT = SM::TT;
+    constexpr int RCH = SM::RCH;
+    constexpr int QC = RCH / 4;  // float4 per row chunk
     constexpr int PITCH = SM::PITCH;
     extern __shared__ __align__(16) float rf_smem[];
-    float(*sR)[RF_RCH][MAXM] = reinterpret_cast<float(*)[RF_RCH][MAXM]>(rf_smem);  // [RF_XS]
-    float(*sG)[RF_RCH] = reinterpret_cast<float(*)[RF_RCH]>(rf_smem + SM::R_FLOATS);
+    float(*sR)[RCH][MAXM] = reinterpret_cast<float(*)[RCH][MAXM]>(rf_smem);  // [RF_XS]
+    float(*sG)[RCH] = reinterpret_cast<float(*)[RCH]>(rf_smem + SM::R_FLOATS);
     float(*sxw)[TPW][PITCH] = reinterpret_cast<float(*)[TPW][PITCH]>(
         rf_smem + SM::R_FLOATS + SM::G_FLOATS);  // [warp * RF_XS + slot]
     __shared__ float sv_all[RF_WARPS][TPW][MAXM + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float(*sv)[MAXM + 1] = sv_all[warp];
-    const int tok = lane / LPT, part = lane % LPT, e0 = part * EPL;
+    const int grp = lane / LPT, part = lane % LPT, e0 = part * EPL;
     const int tw0 = (blockIdx.x * RF_WARPS + warp) * TPW;  // first token of this warp
-    const int t = tw0 + tok;
-    const bool valid = t < T;
-    const int nrc = d / RF_RCH;  // row chunks (= router / gain chunks)
+    const int r0 = grp * TT;                                // this lane's first row in the warp
+    const int nrc = d / RCH;  // row chunks (= router / gain chunks)
 
-    // chunk c of the warp's TPW rows (RF_RCH floats each) -> ring slot c % RF_XS;
+    // chunk c of the warp's TPW rows (RCH floats each) -> ring slot c % RF_XS;
     // 16 lanes per row => 256-byte contiguous cp.async runs; rows past T are clamped.
     auto issue_x = [&](int c) {
         float(*dst)[PITCH] = sxw[warp * RF_XS + c % RF_XS];
@@ -86,33 +91,35 @@ __global__ void __launch_bounds__(32 * RF_WARPS) router_fwd_k(
         for (int i = lane; i < TPW * QC; i += 32) {
             const int row = i / QC, q = i % QC;
             const int tr = min(tw0 + row, T - 1);
-            cp_async16(&dst[row][4 * q], h + static_cast<int64_t>(tr) * d + c * RF_RCH + 4 * q);
+            cp_async16(&dst[row][4 * q], h + static_cast<int64_t>(tr) * d + c * RCH + 4 * q);
         }
     };
-    // router rows [c*RF_RCH, +RF_RCH) -> sR[c % RF_XS] and gain -> sG (block-cooperative);
+    // router rows [c*RCH, +RCH) -> sR[c % RF_XS] and gain -> sG (block-cooperative);
     // experts M..MAXM-1 are zero columns
     auto issue_rg = [&](int c) {
         float* dst = &sR[c % RF_XS][0][0];
-        const float* src = R + static_cast<int64_t>(c) * RF_RCH * M;
+        const float* src = R + static_cast<int64_t>(c) * RCH * M;
         if ((M & 3) == 0 && M == MAXM) {
-            for (int i = threadIdx.x; i < RF_RCH * MAXM / 4; i += blockDim.x)
+            for (int i = threadIdx.x; i < RCH * MAXM / 4; i += blockDim.x)
                 cp_async16(dst + 4 * i, src + 4 * i);
         } else {
-            for (int i = threadIdx.x; i < RF_RCH * MAXM; i += blockDim.x) {
+            for (int i = threadIdx.x; i < RCH * MAXM; i += blockDim.x) {
                 const int rr = i / MAXM, e = i % MAXM;
                 dst[i] = e < M ? __ldg(src + static_cast<int64_t>(rr) * M + e) : 0.f;
             }
         }
         if (threadIdx.x < QC)
-            cp_async16(&sG[c % RF_XS][4 * threadIdx.x], gain + c * RF_RCH + 4 * threadIdx.x);
+            cp_async16(&sG[c % RF_XS][4 * threadIdx.x], gain + c * RCH + 4 * threadIdx.x);
     };
     auto wait_oldest = [&]() {  // group of the oldest in-flight chunk complete
         asm volatile("cp.async.wait_group %0;" ::"n"(RF_XS - 2) : "memory");
     };
 
     // ---- pass 1: rmsnorm_forward sum of squares, sequential over p (kernels.hpp:117-128);
-    // the LPT lanes of a token run the same chain
-    float ms = 0.f;
+    // the LPT lanes of a group run the same TT chains
+    float ms[TT];
+#pragma unroll
+    for (int j = 0; j < TT; ++j) ms[j] = 0.f;
 #pragma unroll
     for (int c = 0; c < RF_XS - 1; ++c) {
         if (c < nrc) issue_x(c);
@@ -123,27 +130,34 @@ __global__ void __launch_bounds__(32 * RF_WARPS) router_fwd_k(
         __syncwarp();  // every lane's copies of chunk c visible; slot (c-1) % XS free
         if (c + RF_XS - 1 < nrc) issue_x(c + RF_XS - 1);
         cp_async_commit();
-        const float* xrow = sxw[warp * RF_XS + c % RF_XS][tok];
 #pragma unroll
-        for (int i = 0; i < QC; ++i) {
-            const float4 x = *reinterpret_cast<const float4*>(xrow + 4 * i);
-            ms = fadd(ms, fmul(x.x, x.x));
-            ms = fadd(ms, fmul(x.y, x.y));
-            ms = fadd(ms, fmul(x.z, x.z));
-            ms = fadd(ms, fmul(x.w, x.w));
+        for (int j = 0; j < TT; ++j) {
+            const float* xrow = sxw[warp * RF_XS + c % RF_XS][r0 + j];
+#pragma unroll
+            for (int i = 0; i < QC; ++i) {
+                const float4 x = *reinterpret_cast<const float4*>(xrow + 4 * i);
+                ms[j] = fadd(ms[j], fmul(x.x, x.x));
+                ms[j] = fadd(ms[j], fmul(x.y, x.y));
+                ms[j] = fadd(ms[j], fmul(x.z, x.z));
+                ms[j] = fadd(ms[j], fmul(x.w, x.w));
+            }
         }
     }
-    const float inv = fdiv(1.f, fsqrt(fadd(fdiv(ms, static_cast<float>(d)), eps)));
+    float inv[TT];
+#pragma unroll
+    for (int j = 0; j < TT; ++j) inv[j] = fdiv(1.f, fsqrt(fadd(fdiv(ms[j], static_cast<float>(d)), eps)));
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();  // all warps done with pass 1 before the rings are reused
 
     // ---- pass 2: normed = (x * inv) * g; logit_e = sum_p normed_p * R[p][e], p ascending,
-    // no FMA; this lane owns experts [e0, e0 + EPL). Each cp.async group carries {x chunk c
-    // of this warp, this thread's share of R / gain chunk c}; the block barrier after the
-    // wait makes chunk c visible to all and guarantees slot (c-1) % XS is no longer read.
-    float acc[EPL];
+    // no FMA; this lane owns experts [e0, e0 + EPL) of its TT tokens. Each cp.async group
+    // carries {x chunk c of this warp, this thread's share of R / gain chunk c}; the block
+    // barrier after the wait makes chunk c visible to all and frees slot (c-1) % XS.
+    float acc[TT][EPL];
 #pragma unroll
-    for (int e = 0; e < EPL; ++e) acc[e] = 0.f;
+    for (int j = 0; j < TT; ++j)
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) acc[j][e] = 0.f;
 #pragma unroll
     for (int c = 0; c < RF_XS - 1; ++c) {
         if (c < nrc) {
@@ -152,9 +166,6 @@ __global__ void __launch_bounds__(32 * RF_WARPS) router_fwd_k(
         }
         cp_async_commit();
     }
-    // normed stores: the token's LPT lanes take turns per 8-column group
-    bf16* nb_row = normed_bf ? normed_bf + static_cast<int64_t>(t) * d : nullptr;
-    float* nf_row = normed ? normed + static_cast<int64_t>(t) * d : nullptr;
     for (int c = 0; c < nrc; ++c) {
         wait_oldest();
         __syncthreads();
@@ -163,59 +174,77 @@ __global__ void __launch_bounds__(32 * RF_WARPS) router_fwd_k(
             issue_rg(c + RF_XS - 1);
         }
         cp_async_commit();
-        const float* xrow = sxw[warp * RF_XS + c % RF_XS][tok];
         const float(*rr)[MAXM] = sR[c % RF_XS];
         const float* gg = sG[c % RF_XS];
 #pragma unroll 2
         for (int i = 0; i < QC; i += 2) {  // 8 p per iteration => one 16-byte bf16 store
-            float nv[8];
+            float nv[TT][8];
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const float4 x = *reinterpret_cast<const float4*>(xrow + 4 * (i + u));
-                const float4 g = *reinterpret_cast<const float4*>(gg + 4 * (i + u));
-                nv[4 * u + 0] = fmul(fmul(x.x, inv), g.x);
-                nv[4 * u + 1] = fmul(fmul(x.y, inv), g.y);
-                nv[4 * u + 2] = fmul(fmul(x.z, inv), g.z);
-                nv[4 * u + 3] = fmul(fmul(x.w, inv), g.w);
+            for (int j = 0; j < TT; ++j) {
+                const float* xrow = sxw[warp * RF_XS + c % RF_XS][r0 + j];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const float4 x = *reinterpret_cast<const float4*>(xrow + 4 * (i + u));
+                    const float4 g = *reinterpret_cast<const float4*>(gg + 4 * (i + u));
+                    nv[j][4 * u + 0] = fmul(fmul(x.x, inv[j]), g.x);
+                    nv[j][4 * u + 1] = fmul(fmul(x.y, inv[j]), g.y);
+                    nv[j][4 * u + 2] = fmul(fmul(x.z, inv[j]), g.z);
+                    nv[j][4 * u + 3] = fmul(fmul(x.w, inv[j]), g.w);
+                }
             }
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const float* rrow = rr[4 * i + j] + e0;
+            for (int jp = 0; jp < 8; ++jp) {
+                const float* rrow = rr[4 * i + jp] + e0;
 #pragma unroll
                 for (int e4 = 0; e4 < EPL; e4 += 4) {
                     const float4 r = *reinterpret_cast<const float4*>(rrow + e4);
-                    acc[e4 + 0] = fadd(acc[e4 + 0], fmul(nv[j], r.x));
-                    acc[e4 + 1] = fadd(acc[e4 + 1], fmul(nv[j], r.y));
-                    acc[e4 + 2] = fadd(acc[e4 + 2], fmul(nv[j], r.z));
-                    acc[e4 + 3] = fadd(acc[e4 + 3], fmul(nv[j], r.w));
+#pragma unroll
+                    for (int j = 0; j < TT; ++j) {
+                        acc[j][e4 + 0] = fadd(acc[j][e4 + 0], fmul(nv[j][jp], r.x));
+                        acc[j][e4 + 1] = fadd(acc[j][e4 + 1], fmul(nv[j][jp], r.y));
+                        acc[j][e4 + 2] = fadd(acc[j][e4 + 2], fmul(nv[j][jp], r.z));
+                        acc[j][e4 + 3] = fadd(acc[j][e4 + 3], fmul(nv[j][jp], r.w));
+                    }
                 }
             }
-            if (valid && ((i >> 1) % LPT) == part) {
-                const int p0 = c * RF_RCH + 4 * i;
-                if (nb_row) {
-                    uint4 pk;
-                    const uint2 lo = pack_bf16x4(nv[0], nv[1], nv[2], nv[3]);
-                    const uint2 hi = pack_bf16x4(nv[4], nv[5], nv[6], nv[7]);
-                    pk.x = lo.x; pk.y = lo.y; pk.z = hi.x; pk.w = hi.y;
-                    *reinterpret_cast<uint4*>(nb_row + p0) = pk;
-                }
-                if (nf_row) {
-                    *reinterpret_cast<float4*>(nf_row + p0) = make_float4(nv[0], nv[1], nv[2], nv[3]);
-                    *reinterpret_cast<float4*>(nf_row + p0 + 4) = make_float4(nv[4], nv[5], nv[6], nv[7]);
+            // normed stores: each (token, 8-column group) written once, spread over the group
+#pragma unroll
+            for (int j = 0; j < TT; ++j) {
+                const int t = tw0 + r0 + j;
+                if (t < T && ((i >> 1) % LPT) == part) {
+                    const int p0 = c * RCH + 4 * i;
+                    if (normed_bf) {
+                        uint4 pk;
+                        const uint2 lo = pack_bf16x4(nv[j][0], nv[j][1], nv[j][2], nv[j][3]);
+                        const uint2 hi = pack_bf16x4(nv[j][4], nv[j][5], nv[j][6], nv[j][7]);
+                        pk.x = lo.x; pk.y = lo.y; pk.z = hi.x; pk.w = hi.y;
+                        *reinterpret_cast<uint4*>(normed_bf + static_cast<int64_t>(t) * d + p0) = pk;
+                    }
+                    if (normed) {
+                        float* nf = normed + static_cast<int64_t>(t) * d + p0;
+                        *reinterpret_cast<float4*>(nf) = make_float4(nv[j][0], nv[j][1], nv[j][2], nv[j][3]);
+                        *reinterpret_cast<float4*>(nf + 4) = make_float4(nv[j][4], nv[j][5], nv[j][6], nv[j][7]);
+                    }
                 }
             }
         }
     }
 
     // ---- softmax_rows (kernels.hpp:156-172) and route_from_logits (model.hpp:185-216):
-    // logits gathered per token in smem, the scans run on the token's part-0 lane
+    // logits gathered per token in smem; the scans of token r0 + j run on the group's lane
+    // part == j
 #pragma unroll
-    for (int e = 0; e < EPL; ++e) sv[tok][e0 + e] = acc[e];
+    for (int j = 0; j < TT; ++j)
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) sv[r0 + j][e0 + e] = acc[j][e];
     __syncwarp();
-    if (part != 0 || !valid) return;
+    if (part >= TT) return;
+    const int j = part;
+    const int t = tw0 + r0 + j;
+    if (t >= T) return;
     float* lrow = logits + static_cast<int64_t>(t) * M;
     float* prow = probs + static_cast<int64_t>(t) * M;
-    float* pv = sv[tok];
+    float* pv = sv[r0 + j];
     float mx = pv[0];
     for (int e = 0; e < M; ++e) {
         lrow[e] = pv[e];
@@ -230,7 +259,11 @@ __global__ void __launch_bounds__(32 * RF_WARPS) router_fwd_k(
     }
     const float rs = fdiv(1.f, sum);
     lse_out[t] = mx + logf(sum);
-    inv_out[t] = inv;
+    float invj = inv[0];
+#pragma unroll
+    for (int jj = 1; jj < TT; ++jj)
+        if (jj == j) invj = inv[jj];
+    inv_out[t] = invj;
     for (int e = 0; e < M; ++e) {
         pv[e] = fmul(pv[e], rs);  // probabilities
         prow[e] = pv[e];
@@ -241,22 +274,22 @@ __global__ void __launch_bounds__(32 * RF_WARPS) router_fwd_k(
     for (int s2 = 0; s2 < k; ++s2) {
         int best = -1;
         float bv = 0.f;
-        for (int j = 0; j < M; ++j) {
-            if (!((chosen >> j) & 1ull) && (best < 0 || pv[j] > bv)) {
-                best = j;
-                bv = pv[j];
+        for (int jj = 0; jj < M; ++jj) {
+            if (!((chosen >> jj) & 1ull) && (best < 0 || pv[jj] > bv)) {
+                best = jj;
+                bv = pv[jj];
             }
         }
         chosen |= 1ull << best;
     }
     float dn = 0.f;
-    for (int j = 0; j < M; ++j)
-        if ((chosen >> j) & 1ull) dn = fadd(dn, pv[j]);
+    for (int jj = 0; jj < M; ++jj)
+        if ((chosen >> jj) & 1ull) dn = fadd(dn, pv[jj]);
     int slot = 0;
-    for (int j = 0; j < M; ++j) {
-        if ((chosen >> j) & 1ull) {
-            topk_idx[static_cast<int64_t>(t) * k + slot] = j;
-            topk_w[static_cast<int64_t>(t) * k + slot] = renorm ? fdiv(pv[j], dn) : pv[j];
+    for (int jj = 0; jj < M; ++jj) {
+        if ((chosen >> jj) & 1ull) {
+            topk_idx[static_cast<int64_t>(t) * k + slot] = jj;
+            topk_w[static_cast<int64_t>(t) * k + slot] = renorm ? fdiv(pv[jj], dn) : pv[jj];
             ++slot;
         }
     }
@@ -285,7 +318,10 @@ void router_forward(const float* h, const float* gain, const float* router, int6
                     bf16* normed_bf, float* logits, float* probs, int32_t* topk_idx,
                     float* topk_w, float* lse, float* inv_rms, float* denom, cudaStream_t s) {
     const int maxm = M <= 8 ? 8 : (M <= 16 ? 16 : (M <= 32 ? 32 : 64));
-    const int per_block = RF_WARPS * (32 / (maxm / (maxm < 8 ? maxm : 8)));
+    const int per_block = RF_WARPS * (maxm == 8    ? RfSmem<8>::TPW
+                                      : maxm == 16 ? RfSmem<16>::TPW
+                                      : maxm == 32 ? RfSmem<32>::TPW
+                                                   : RfSmem<64>::TPW);
     const unsigned grid = static_cast<unsigned>((T + per_block - 1) / per_block);
     auto* f = maxm == 8 ? launch_rf<8> : maxm == 16 ? launch_rf<16> : maxm == 32 ? launch_rf<32>
                                                                                   : launch_rf<64>;
