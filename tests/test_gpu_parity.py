@@ -236,6 +236,12 @@ def test_local_step_cfg2_shapes(gpu):
     _check_step(model_cfg(**CFG2), B=1, S=384, owned=[0, 1, 2, 3], seed=30)
 
 
+def test_local_step_cfg4_shapes(gpu):
+    # M = 64, k = 8, d = 2048: the large-M router (4 tokens per lane), k = 8 combine and
+    # backward paths, cta_group::2 GEMMs at d = 2048
+    _check_step(model_cfg(**CFG4), B=1, S=256, owned=list(range(16)), seed=35)
+
+
 def test_local_step_ragged_T(gpu):
     # T not a multiple of 128, an owned expert that may receive no tokens
     _check_step(model_cfg(**CFG1), B=3, S=37, owned=[0, 7], seed=40)
