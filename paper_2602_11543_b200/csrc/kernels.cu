@@ -1399,7 +1399,20 @@ __global__ void splitk_reduce_k(const float4* __restrict__ part, int nsplit, int
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         float4 a = __ldg(part + i);
-        for (int s = 1; s < nsplit; ++s) {
+        int s = 1;
+        for (; s + 8 <= nsplit; s += 8) {  // 8 loads in flight, added in split order
+            float4 b[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) b[u] = __ldg(part + (s + u) * n4 + i);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                a.x += b[u].x;
+                a.y += b[u].y;
+                a.z += b[u].z;
+                a.w += b[u].w;
+            }
+        }
+        for (; s < nsplit; ++s) {
             const float4 b = __ldg(part + s * n4 + i);
             a.x += b.x;
             a.y += b.y;
