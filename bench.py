@@ -200,6 +200,21 @@ def peaks():
         return 1590.0, 1400.0, 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def adamw_roofline(fam, node, hbm_peak):
+    """The largest single kernel by time at N=1: MaskedAdamW, HBM-bound. Algorithmic bytes
+    per launch = 28 B per trainable scalar (theta, g, m, v read; theta, m, v written) + 2 B
+    per expert / head scalar for the bf16 operand copy; measured CUDA-event time per launch."""
+    if "adamw" not in fam or not hbm_peak:
+        return None
+    G = node.counts()["grad_scalars"]
+    ms, launches = fam["adamw"]
+    achieved = 30.0 * G / (ms / launches / 1e3) / 1e9
+    return {"bound": "hbm", "kernel": "adamw_k", "achieved": achieved, "peak": hbm_peak,
+            "unit": "GB/s", "frac": achieved / hbm_peak, "bytes_per_launch": 30.0 * G,
+            "note": "a no-math kernel with the same 4-read / 3-write fp32 + bf16 pattern "
+                    "reaches ~6.1 TB/s on this GPU (tools/stream_bench.cu)"}
+
+
 def ncu_traffic():
     """dram bytes per launch of the grouped GEMM from the committed ncu --set full summary."""
     try:
@@ -422,6 +437,7 @@ def our_arm(args):
                      "timing": "CUDA events around every GEMM launch on the context stream, "
                                f"{args.prof_rounds} profiled round(s) right after the timed "
                                "region (the timed region itself runs unprofiled)"},
+        "roofline_hbm": adamw_roofline(fam, node, hbm),
         "kernels_ms": {k: round(v[0], 4) for k, v in fam.items()},
         "clocks": clocks,
     }

@@ -197,6 +197,9 @@ struct spes_ctx {
     DevMem act;
     int64_t T = 0, T_pad = 0, R_cap = 0, B = 0, S = 0;
     bool use_pairs = false;  // cta_group::2 GEMMs (256-row tiles)
+    // layer 0's input h0 = emb[inputs] is never materialized: its consumers read the
+    // (L2-resident) embedding rows through the token index
+    bool virtual_h0 = true;
     int tr = 128;            // GEMM tile rows == expert row padding
     std::vector<float*> h;  // L+1 buffers [T_pad x d]
     std::vector<LayerBufs> layers;
@@ -568,17 +571,23 @@ void forward_backward(spes_ctx* c) {
     const Seeds sd = seeds_for(c);
     float* P = c->params;
     spes_k::gemm_set_pair_mode(c->use_pairs);
+    // input rows of layer l: layer 0 reads emb[inputs[t]] in place (virtual_h0)
+    auto hsrc = [&](int l) -> const float* {
+        return (l == 0 && c->virtual_h0) ? P + L.off_emb() : c->h[l];
+    };
+    auto hmap = [&](int l) -> const int32_t* { return (l == 0 && c->virtual_h0) ? c->inputs : nullptr; };
 #define PROF(name) Prof _prof_##__LINE__(c, name)
     {
         PROF("embed_gather");
-        spes_k::embed_gather(P + L.off_emb(), c->tokens, c->B, c->S, d, V, c->h[0], c->inputs,
+        spes_k::embed_gather(P + L.off_emb(), c->tokens, c->B, c->S, d, V,
+                             c->virtual_h0 ? nullptr : c->h[0], c->inputs,
                              c->targets, c->err, st);
     }
     for (int l = 0; l < L.L; ++l) {
         LayerBufs& Y = c->layers[l];
         {
             PROF("router_fwd");
-            spes_k::router_forward(c->h[l], P + L.off_norm(l), P + L.off_router(l), T, d, M, k,
+            spes_k::router_forward(hsrc(l), hmap(l), P + L.off_norm(l), P + L.off_router(l), T, d, M, k,
                                    c->cfg.renormalize_after_topk, c->cfg.rms_eps, c->expf_variant,
                                    nullptr, c->normed_bf, Y.logits, Y.probs, Y.topk_idx,
                                    Y.topk_w, Y.lse_r, Y.inv_rms, Y.denom, st);
@@ -609,7 +618,7 @@ void forward_backward(spes_ctx* c) {
         }
         {
             PROF("combine_fwd");
-            spes_k::combine_forward(c->h[l], Y.y, Y.slot_row, Y.topk_idx, Y.topk_w, T, d, k,
+            spes_k::combine_forward(hsrc(l), hmap(l), Y.y, Y.slot_row, Y.topk_idx, Y.topk_w, T, d, k,
                                     c->h[l + 1], l + 1 == L.L ? c->hL : nullptr, st);
         }
     }
@@ -687,7 +696,7 @@ void forward_backward(spes_ctx* c) {
         }
         {
             PROF("router_bwd");
-            spes_k::router_backward(c->h[l], P + L.off_norm(l), P + L.off_router(l), Y.probs,
+            spes_k::router_backward(hsrc(l), hmap(l), P + L.off_norm(l), P + L.off_router(l), Y.probs,
                                     Y.lse_r, Y.inv_rms, Y.denom, Y.topk_idx, Y.slot_row,
                                     c->gw_part, c->dxp, Y.lb_coeff, T, d, M, k,
                                     c->cfg.renormalize_after_topk, sd.g_lbsum, sd.g_s, c->glog,
@@ -695,7 +704,7 @@ void forward_backward(spes_ctx* c) {
         }
         {
             PROF("norm_router_grads");  // + rmsnorm backward into gh
-            spes_k::norm_router_grads(c->h[l], P + L.off_norm(l), c->gnormed, c->glog, Y.inv_rms, T, d, M,
+            spes_k::norm_router_grads(hsrc(l), hmap(l), P + L.off_norm(l), c->gnormed, c->glog, Y.inv_rms, T, d, M,
                                       c->nr_partial, c->grads + L.off_norm(l),
                                       c->grads + L.off_router(l), c->dot_part, c->gh, st);
         }
@@ -1760,6 +1769,17 @@ spes_status spes_debug_read(spes_ctx* c, const char* name, int32_t layer, void* 
         };
         if (n == "h") {
             if (layer < 0 || layer > L.L) throw std::out_of_range("debug_read: bad layer");
+            if (layer == 0 && c->virtual_h0) {  // emb[inputs] (never materialized on device)
+                if (bytes < 4 * T * d) throw std::invalid_argument("debug_read: buffer too small");
+                std::vector<int32_t> in(static_cast<size_t>(T));
+                ck(cudaMemcpy(in.data(), c->inputs, 4 * T, cudaMemcpyDeviceToHost), "D2H");
+                float* out = static_cast<float*>(host);
+                for (int64_t t = 0; t < T; ++t)
+                    ck(cudaMemcpy(out + t * d, c->params + L.off_emb() + static_cast<int64_t>(in[t]) * d,
+                                  4 * d, cudaMemcpyDeviceToHost),
+                       "D2H emb row");
+                return;
+            }
             src = c->h[layer];
             sz = 4 * T * d;
         } else if (n == "normed") {
@@ -1884,7 +1904,7 @@ spes_status spes_kernel_router(const spes_model_cfg* cfg, const float* h, const 
         ck(cudaMemcpy(dg, gain, 4 * d, cudaMemcpyHostToDevice), "H2D");
         ck(cudaMemcpy(dr, router, 4 * d * M, cudaMemcpyHostToDevice), "H2D");
         const int variant = spes_expf::host_variant_from(&expf);
-        spes_k::router_forward(dh, dg, dr, T, d, M, k, cfg->renormalize_after_topk, cfg->rms_eps,
+        spes_k::router_forward(dh, nullptr, dg, dr, T, d, M, k, cfg->renormalize_after_topk, cfg->rms_eps,
                                variant, dn, nullptr, dl, dp, di, dw, dlse, dinv, dden, 0);
         // routing plan for counts / permutation
         const int64_t R = rup(T * k + static_cast<int64_t>(M) * 128, 128);

@@ -39,6 +39,7 @@ __global__ void embed_gather_k(const float* __restrict__ emb, const int32_t* __r
         if (bad) atomicExch(err, 1);
     }
     if (bad) tin = 0;
+    if (!h) return;  // layer-0 input read in place as emb[inputs[t]] by its consumers
     const float4* src = reinterpret_cast<const float4*>(emb + static_cast<int64_t>(tin) * d);
     float4* dst = reinterpret_cast<float4*>(h + t * d);
     for (int64_t q = threadIdx.x; q < d / 4; q += blockDim.x) dst[q] = __ldg(src + q);
@@ -375,11 +376,13 @@ void permute_rows_bf16(const bf16* src, int64_t cols, const int32_t* row_map,
 // Block per token; each thread owns CF_U float4 columns (all their loads in flight first).
 constexpr int CF_U = 2;
 template <int KMAX>
-__global__ void combine_fwd_k(const float* __restrict__ h, const float* __restrict__ y,
+__global__ void combine_fwd_k(const float* __restrict__ h, const int32_t* __restrict__ hrow,
+                              const float* __restrict__ y,
                               const int32_t* __restrict__ slot_row, const float* __restrict__ w,
                               int64_t d, int k, float* __restrict__ h_next,
                               bf16* __restrict__ h_next_bf) {
     const int64_t t = blockIdx.x;
+    const float* hr = h + (hrow ? static_cast<int64_t>(hrow[t]) : t) * d;
     int32_t rows[KMAX];
     float ws[KMAX];
 #pragma unroll
@@ -397,7 +400,7 @@ __global__ void combine_fwd_k(const float* __restrict__ h, const float* __restri
 #pragma unroll
                 for (int s = 0; s < KMAX; ++s)
                     if (s < k) yv[u][s] = __ldg(reinterpret_cast<const float4*>(y + rows[s] * d + q));
-                hv[u] = __ldg(reinterpret_cast<const float4*>(h + t * d + q));
+                hv[u] = __ldg(reinterpret_cast<const float4*>(hr + q));
             }
         }
 #pragma unroll
@@ -431,16 +434,16 @@ __global__ void combine_fwd_k(const float* __restrict__ h, const float* __restri
     }
 }
 
-void combine_forward(const float* h, const float* y, const int32_t* slot_row,
+void combine_forward(const float* h, const int32_t* hrow, const float* y, const int32_t* slot_row,
                      const int32_t* topk_idx, const float* topk_w, int64_t T, int64_t d, int k,
                      float* h_next, bf16* h_next_bf, cudaStream_t s) {
     (void)topk_idx;
     const int threads = d >= 4 * 128 * CF_U ? 128 : static_cast<int>(cdiv(d / 4, CF_U));
     if (k <= 2)
-        combine_fwd_k<2><<<static_cast<unsigned>(T), threads, 0, s>>>(h, y, slot_row, topk_w, d, k,
+        combine_fwd_k<2><<<static_cast<unsigned>(T), threads, 0, s>>>(h, hrow, y, slot_row, topk_w, d, k,
                                                                       h_next, h_next_bf);
     else
-        combine_fwd_k<8><<<static_cast<unsigned>(T), threads, 0, s>>>(h, y, slot_row, topk_w, d, k,
+        combine_fwd_k<8><<<static_cast<unsigned>(T), threads, 0, s>>>(h, hrow, y, slot_row, topk_w, d, k,
                                                                       h_next, h_next_bf);
     count_launch();
 }
@@ -695,7 +698,8 @@ constexpr int NRG_EG = 16;
 // (rmsnorm_bwd_k's formula and dot order): h.grad += (gy*g)*inv - coef*x, so h and gnormed
 // are streamed once for both.
 __global__ void __launch_bounds__(256) norm_router_partial_k(
-    const float* __restrict__ h, const float* __restrict__ gain, const float* __restrict__ gnormed,
+    const float* __restrict__ h, const int32_t* __restrict__ hrow,
+    const float* __restrict__ gain, const float* __restrict__ gnormed,
     const float* __restrict__ glog, const float* __restrict__ inv_rms, int T, int d, int M,
     float* __restrict__ partial, const float* __restrict__ dot_part, float* __restrict__ gh) {
     __shared__ __align__(16) float sgl[64][NRG_EG];
@@ -770,8 +774,10 @@ __global__ void __launch_bounds__(256) norm_router_partial_k(
             const bool v2 = tt2 < 64 && tb + tt2 < t1;
             const int64_t o1 = static_cast<int64_t>(tb + tt) * d + q;
             const int64_t o2 = static_cast<int64_t>(tb + (v2 ? tt2 : tt)) * d + q;
-            const float4 x1 = __ldg(reinterpret_cast<const float4*>(h + o1));
-            const float4 x2 = __ldg(reinterpret_cast<const float4*>(h + o2));
+            const int64_t xo1 = hrow ? static_cast<int64_t>(hrow[tb + tt]) * d + q : o1;
+            const int64_t xo2 = hrow ? static_cast<int64_t>(hrow[tb + (v2 ? tt2 : tt)]) * d + q : o2;
+            const float4 x1 = __ldg(reinterpret_cast<const float4*>(h + xo1));
+            const float4 x2 = __ldg(reinterpret_cast<const float4*>(h + xo2));
             const float i1 = __ldg(inv_rms + tb + tt);
             const float i2 = __ldg(inv_rms + tb + (v2 ? tt2 : tt));
             float4 g1 = z4, g2 = z4, h1 = z4, h2 = z4;
@@ -828,12 +834,12 @@ __global__ void norm_router_finish_k(const float* __restrict__ partial, int d, i
         g_router[static_cast<int64_t>(q) * M + (c - 1)] = s;
 }
 
-void norm_router_grads(const float* h, const float* gain, const float* gnormed,
+void norm_router_grads(const float* h, const int32_t* hrow, const float* gain, const float* gnormed,
                        const float* glog, const float* inv_rms, int64_t T, int64_t d, int M,
                        float* partial, float* g_gain, float* g_router, const float* dot_part,
                        float* gh, cudaStream_t s) {
     dim3 grid(static_cast<unsigned>(d / 128), NRG_TC, static_cast<unsigned>((M + NRG_EG - 1) / NRG_EG));
-    norm_router_partial_k<<<grid, 256, 0, s>>>(h, gain, gnormed, glog, inv_rms, (int)T, (int)d, M,
+    norm_router_partial_k<<<grid, 256, 0, s>>>(h, hrow, gain, gnormed, glog, inv_rms, (int)T, (int)d, M,
                                                partial, dot_part, gh);
     const int64_t n = d * (M + 1);
     norm_router_finish_k<<<static_cast<unsigned>(cdiv(n, 256)), 256, 0, s>>>(partial, (int)d, M,

@@ -33,7 +33,9 @@ void embed_gather(const float* emb, const int32_t* tokens, int64_t B, int64_t S,
                   int64_t V, float* h, int32_t* inputs, int32_t* targets, int32_t* err,
                   cudaStream_t s);
 // normed (fp32) and normed_bf (bf16, the expert GEMM operand) are each optional.
-void router_forward(const float* h, const float* gain, const float* router, int64_t T, int64_t d,
+// hrow (optional): row t of h is h + hrow[t] * d (layer 0 reads emb[inputs] in place)
+void router_forward(const float* h, const int32_t* hrow, const float* gain, const float* router,
+                    int64_t T, int64_t d,
                     int M, int k, int renorm, float eps, int expf_variant, float* normed,
                     bf16* normed_bf, float* logits, float* probs, int32_t* topk_idx,
                     float* topk_w, float* lse, float* inv_rms, float* denom, cudaStream_t s);
@@ -79,7 +81,7 @@ void gather_rows_bf16(const float* src, int64_t ld_src, const int32_t* row_map,
 void permute_rows_bf16(const bf16* src, int64_t cols, const int32_t* row_map,
                        const int32_t* nrows_dev, int64_t rows_cap, bf16* dst, cudaStream_t s);
 // h_next_bf (optional): bf16 copy of h_next (the head GEMM operand after the last layer)
-void combine_forward(const float* h, const float* y, const int32_t* slot_row,
+void combine_forward(const float* h, const int32_t* hrow, const float* y, const int32_t* slot_row,
                      const int32_t* topk_idx, const float* topk_w, int64_t T, int64_t d, int k,
                      float* h_next, bf16* h_next_bf, cudaStream_t s);
 // CE + z on head logits; writes dlogits as bf16 (the head backward GEMM operand; padding
@@ -98,7 +100,8 @@ void losses_reduce(const float* diff, const float* lse_head, const float* lse_r,
 void combine_backward(const float* gh, const float* y, const int32_t* row_token,
                       const float* row_w, const int32_t* R_total_dev, int64_t R_cap, int64_t d,
                       bf16* dyw, float* gw_part, cudaStream_t s);
-void router_backward(const float* h, const float* gain, const float* router, const float* probs,
+void router_backward(const float* h, const int32_t* hrow, const float* gain, const float* router,
+                     const float* probs,
                      const float* lse_r, const float* inv_rms, const float* denom,
                      const int32_t* topk_idx, const int32_t* slot_row, const float* gw_part,
                      const float* dxp, const float* lb_coeff, int64_t T, int64_t d, int M, int k,
@@ -106,7 +109,7 @@ void router_backward(const float* h, const float* gain, const float* router, con
                      float* dot_part, float* gh, cudaStream_t s);  // gh null: rmsnorm bwd deferred
 // normed is recomputed exactly from h, inv_rms and the gain (not stored in forward)
 // gh non-null: also applies the rmsnorm backward (router_backward then skips it)
-void norm_router_grads(const float* h, const float* gain, const float* gnormed,
+void norm_router_grads(const float* h, const int32_t* hrow, const float* gain, const float* gnormed,
                        const float* glog, const float* inv_rms, int64_t T, int64_t d, int M,
                        float* partial, float* g_gain, float* g_router, const float* dot_part,
                        float* gh, cudaStream_t s);

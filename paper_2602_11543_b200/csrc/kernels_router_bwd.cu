@@ -80,7 +80,8 @@ constexpr int NG_QT = 128;  // columns per tile
 // grid (T/32, d/128), 256 threads: thread (ty, tx) -> tokens 4ty..4ty+3, columns 4tx..4tx+3
 template <int MAXM>
 __global__ void __launch_bounds__(256) normed_grad_k(
-    const float* __restrict__ h, const float* __restrict__ gain, const float* __restrict__ R,
+    const float* __restrict__ h, const int32_t* __restrict__ hrow, const float* __restrict__ gain,
+    const float* __restrict__ R,
     const float* __restrict__ glog, const int32_t* __restrict__ slot_row,
     const float* __restrict__ dxp, int T, int d, int M, int k, float* __restrict__ gnormed,
     float* __restrict__ dot_part) {
@@ -141,7 +142,8 @@ __global__ void __launch_bounds__(256) normed_grad_k(
                 a[3] = fadd(a[3], v.w);
             }
         }
-        const float4 xv = __ldg(reinterpret_cast<const float4*>(h + static_cast<int64_t>(t) * d + q0 + 4 * tx));
+        const int64_t xr_t = hrow ? static_cast<int64_t>(hrow[t]) : t;
+        const float4 xv = __ldg(reinterpret_cast<const float4*>(h + xr_t * d + q0 + 4 * tx));
         float4 o;
         o.x = fadd(a[0], sr[i][0]);
         o.y = fadd(a[1], sr[i][1]);
@@ -156,6 +158,7 @@ __global__ void __launch_bounds__(256) normed_grad_k(
 }
 
 __global__ void __launch_bounds__(256) rmsnorm_bwd_k(const float* __restrict__ h,
+                                                     const int32_t* __restrict__ hrow,
                                                      const float* __restrict__ gain,
                                                      const float* __restrict__ inv_rms,
                                                      const float* __restrict__ gnormed,
@@ -169,7 +172,7 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_k(const float* __restrict__ h
     for (int i = 0; i < np; ++i) dot2 += dot_part[static_cast<int64_t>(t) * np + i];
     const float inv = inv_rms[t];
     const float coef = fdiv(fmul(fmul(fmul(dot2, inv), inv), inv), static_cast<float>(d));
-    const float* xr = h + static_cast<int64_t>(t) * d;
+    const float* xr = h + (hrow ? static_cast<int64_t>(hrow[t]) : static_cast<int64_t>(t)) * d;
     const float* gy = gnormed + static_cast<int64_t>(t) * d;
     float* ghr = gh + static_cast<int64_t>(t) * d;
     for (int q0 = lane * 4; q0 < d; q0 += 128) {
@@ -185,7 +188,8 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_k(const float* __restrict__ h
     }
 }
 
-void router_backward(const float* h, const float* gain, const float* router, const float* probs,
+void router_backward(const float* h, const int32_t* hrow, const float* gain, const float* router,
+                     const float* probs,
                      const float* lse_r, const float* inv_rms, const float* denom,
                      const int32_t* topk_idx, const int32_t* slot_row, const float* gw_row,
                      const float* dxp, const float* lb_coeff, int64_t T, int64_t d, int M, int k,
@@ -199,7 +203,7 @@ void router_backward(const float* h, const float* gain, const float* router, con
         router_scalar_bwd_k<MM><<<g1, 128, 0, s>>>(probs, lse_r, denom, topk_idx, slot_row,     \
                                                    gw_row, lb_coeff, (int)T, M, k, renorm,      \
                                                    g_lbsum, g_s, glog);                         \
-        normed_grad_k<MM><<<g2, 256, 0, s>>>(h, gain, router, glog, slot_row, dxp, (int)T,      \
+        normed_grad_k<MM><<<g2, 256, 0, s>>>(h, hrow, gain, router, glog, slot_row, dxp, (int)T, \
                                              (int)d, M, k, gnormed, dot_part);                  \
     } while (0)
     if (M <= 8)
@@ -212,7 +216,7 @@ void router_backward(const float* h, const float* gain, const float* router, con
         SPES_RB(64);
 #undef SPES_RB
     if (gh) {
-        rmsnorm_bwd_k<<<g3, 256, 0, s>>>(h, gain, inv_rms, gnormed, dot_part, (int)T, (int)d, gh);
+        rmsnorm_bwd_k<<<g3, 256, 0, s>>>(h, hrow, gain, inv_rms, gnormed, dot_part, (int)T, (int)d, gh);
         count_launch();
     }
     count_launch(2);

@@ -60,7 +60,8 @@ struct RfSmem {
 
 template <int MAXM>
 __global__ void __launch_bounds__(32 * RF_WARPS) router_fwd_k(
-    const float* __restrict__ h, const float* __restrict__ gain, const float* __restrict__ R,
+    const float* __restrict__ h, const int32_t* __restrict__ hrow, const float* __restrict__ gain,
+    const float* __restrict__ R,
     int T, int d, int M, int k, int renorm, float eps, int variant, float* __restrict__ normed,
     bf16* __restrict__ normed_bf, float* __restrict__ logits, float* __restrict__ probs,
     int32_t* __restrict__ topk_idx, float* __restrict__ topk_w, float* __restrict__ lse_out,
@@ -90,8 +91,9 @@ __global__ void __launch_bounds__(32 * RF_WARPS) router_fwd_k(
 #pragma unroll 4
         for (int i = lane; i < TPW * QC; i += 32) {
             const int row = i / QC, q = i % QC;
-            const int tr = min(tw0 + row, T - 1);
-            cp_async16(&dst[row][4 * q], h + static_cast<int64_t>(tr) * d + c * RCH + 4 * q);
+            const int tc = min(tw0 + row, T - 1);
+            const int64_t tr = hrow ? static_cast<int64_t>(__ldg(hrow + tc)) : tc;
+            cp_async16(&dst[row][4 * q], h + tr * d + c * RCH + 4 * q);
         }
     };
     // router rows [c*RCH, +RCH) -> sR[c % RF_XS] and gain -> sG (block-cooperative);
@@ -297,7 +299,8 @@ __global__ void __launch_bounds__(32 * RF_WARPS) router_fwd_k(
 }
 
 template <int MM>
-static void launch_rf(unsigned grid, cudaStream_t s, const float* h, const float* gain,
+static void launch_rf(unsigned grid, cudaStream_t s, const float* h, const int32_t* hrow,
+                      const float* gain,
                       const float* router, int64_t T, int64_t d, int M, int k, int renorm,
                       float eps, int variant, float* normed, bf16* normed_bf, float* logits,
                       float* probs, int32_t* topk_idx, float* topk_w, float* lse, float* inv_rms,
@@ -309,11 +312,12 @@ static void launch_rf(unsigned grid, cudaStream_t s, const float* h, const float
         configured = true;
     }
     router_fwd_k<MM><<<grid, 32 * RF_WARPS, RfSmem<MM>::BYTES, s>>>(
-        h, gain, router, (int)T, (int)d, M, k, renorm, eps, variant, normed, normed_bf, logits,
+        h, hrow, gain, router, (int)T, (int)d, M, k, renorm, eps, variant, normed, normed_bf, logits,
         probs, topk_idx, topk_w, lse, inv_rms, denom);
 }
 
-void router_forward(const float* h, const float* gain, const float* router, int64_t T, int64_t d,
+void router_forward(const float* h, const int32_t* hrow, const float* gain, const float* router,
+                    int64_t T, int64_t d,
                     int M, int k, int renorm, float eps, int variant, float* normed,
                     bf16* normed_bf, float* logits, float* probs, int32_t* topk_idx,
                     float* topk_w, float* lse, float* inv_rms, float* denom, cudaStream_t s) {
@@ -325,7 +329,7 @@ void router_forward(const float* h, const float* gain, const float* router, int6
     const unsigned grid = static_cast<unsigned>((T + per_block - 1) / per_block);
     auto* f = maxm == 8 ? launch_rf<8> : maxm == 16 ? launch_rf<16> : maxm == 32 ? launch_rf<32>
                                                                                   : launch_rf<64>;
-    f(grid, s, h, gain, router, T, d, M, k, renorm, eps, variant, normed, normed_bf, logits, probs,
+    f(grid, s, h, hrow, gain, router, T, d, M, k, renorm, eps, variant, normed, normed_bf, logits, probs,
       topk_idx, topk_w, lse, inv_rms, denom);
     count_launch();
 }

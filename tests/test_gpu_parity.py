@@ -151,7 +151,11 @@ def _check_step(cfg, B, S, owned, seed, renorm=False):
     assert bitexact(node.debug("probs", 0, np.float32, (T, M), T * M), tr["probs"][0])
     assert bitexact(node.debug("counts", 0, np.int32, None, M), tr["counts"][0])
     assert bitexact(node.debug("perm", 0, np.int32, None, T * k), tr["perm"][0])
-    assert bitexact(node.debug("h", 0, np.float32, (T, d), T * d), tr["h"][0])
+    # layer-0 input h0 = emb[inputs] is read in place (never materialized): the bit-exact
+    # layer-0 routing above covers it; debug("h", 0) rebuilds it from the CURRENT embedding
+    emb_now = node.read_params()[: cfg.vocab * d].reshape(cfg.vocab, d)
+    assert bitexact(node.debug("h", 0, np.float32, (T, d), T * d),
+                    emb_now[tokens[:, :-1].reshape(-1)])
     # deeper layers: agreement rate, disagreements only at near-ties of the oracle probs
     for l in range(1, L):
         idx = node.debug("topk_idx", l, np.int32, (T, k), T * k)
