@@ -619,7 +619,8 @@ void forward_backward(spes_ctx* c) {
         {
             PROF("combine_fwd");
             spes_k::combine_forward(hsrc(l), hmap(l), Y.y, Y.slot_row, Y.topk_idx, Y.topk_w, T, d, k,
-                                    c->h[l + 1], l + 1 == L.L ? c->hL : nullptr, st);
+                                    l + 1 == L.L ? nullptr : c->h[l + 1],
+                                    l + 1 == L.L ? c->hL : nullptr, st);
         }
     }
     {
@@ -1780,6 +1781,9 @@ spes_status spes_debug_read(spes_ctx* c, const char* name, int32_t layer, void* 
                        "D2H emb row");
                 return;
             }
+            if (layer == L.L)
+                throw std::invalid_argument(
+                    "debug_read: the final hidden state is kept only as the bf16 head operand");
             src = c->h[layer];
             sz = 4 * T * d;
         } else if (n == "normed") {

@@ -422,7 +422,7 @@ __global__ void combine_fwd_k(const float* __restrict__ h, const int32_t* __rest
             }
             const float4 o = make_float4(fadd(hv[u].x, acc.x), fadd(hv[u].y, acc.y),
                                          fadd(hv[u].z, acc.z), fadd(hv[u].w, acc.w));
-            *reinterpret_cast<float4*>(h_next + t * d + q) = o;
+            if (h_next) *reinterpret_cast<float4*>(h_next + t * d + q) = o;
             if (h_next_bf) {  // last layer: the head GEMM's bf16 operand, no separate pass
                 __nv_bfloat162 a = __floats2bfloat162_rn(o.x, o.y), b = __floats2bfloat162_rn(o.z, o.w);
                 uint2 pk;

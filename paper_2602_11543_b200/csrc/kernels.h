@@ -80,7 +80,8 @@ void gather_rows_bf16(const float* src, int64_t ld_src, const int32_t* row_map,
 // rows processed: *nrows_dev.
 void permute_rows_bf16(const bf16* src, int64_t cols, const int32_t* row_map,
                        const int32_t* nrows_dev, int64_t rows_cap, bf16* dst, cudaStream_t s);
-// h_next_bf (optional): bf16 copy of h_next (the head GEMM operand after the last layer)
+// h_next_bf (optional): bf16 copy of h_next (the head GEMM operand after the last layer);
+// h_next may then be null (the final fp32 hidden state has no other consumer)
 void combine_forward(const float* h, const int32_t* hrow, const float* y, const int32_t* slot_row,
                      const int32_t* topk_idx, const float* topk_w, int64_t T, int64_t d, int k,
                      float* h_next, bf16* h_next_bf, cudaStream_t s);
