@@ -625,14 +625,19 @@ void forward_backward(spes_ctx* c) {
     }
     {
         PROF("head_fwd");
-        spes_k::gemm_store_f32(bn_for(V), spes_k::GemmMajor::KMN, c->a_hL, c->b_headB_mn,
-                               c->head_groups + 0, 1,
-                               c->head_tiles + 0, c->head_max[0], st);
+        if (V == 256) {  // softmax-CE in the GEMM epilogue: no fp32 logits round trip
+            spes_k::gemm_head_ce(c->a_hL, c->b_headB_mn, c->head_groups + 0, 1, c->head_tiles + 0,
+                                 c->head_max[0], c->targets, T, sd.g_s2, sd.g_ssum, c->dlog_bf, c->diff, c->lse_head, st);
+        } else {
+            spes_k::gemm_store_f32(bn_for(V), spes_k::GemmMajor::KMN, c->a_hL, c->b_headB_mn,
+                                   c->head_groups + 0, 1, c->head_tiles + 0, c->head_max[0], st);
+        }
     }
     {
         PROF("head_ce_losses");
-        spes_k::head_ce(c->head_logits, c->targets, T, Tp, V, c->expf_variant, sd.g_s2, sd.g_ssum,
-                        c->dlog_bf, c->diff, c->lse_head, st);
+        if (V != 256)
+            spes_k::head_ce(c->head_logits, c->targets, T, Tp, V, sd.g_s2,
+                            sd.g_ssum, c->dlog_bf, c->diff, c->lse_head, st);
         spes_k::losses_reduce(c->diff, c->lse_head, c->lse_all, c->probs_all, c->coeff_all, T, Tp,
                               L.L, M, sd.inv_T, sd.inv_L, sd.c_ce, sd.c_lb, sd.c_mz, sd.c_z,
                               c->loss_part, c->d_losses, st);
@@ -1818,6 +1823,8 @@ spes_status spes_debug_read(spes_ctx* c, const char* name, int32_t layer, void* 
             src = c->gh;
             sz = 4 * T * d;
         } else if (n == "head_logits") {
+            if (L.V == 256)  // the fused head-CE epilogue never writes fp32 logits
+                throw std::logic_error("debug_read: head_logits are not materialised for V == 256");
             src = c->head_logits;
             sz = 4 * T * L.V;
         } else if (n == "y") {

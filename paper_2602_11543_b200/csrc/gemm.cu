@@ -254,6 +254,96 @@ struct EpiAdamW2 {
     }
 };
 
+// ---- head forward with the softmax-CE fused into the epilogue (V == BN == 256) ----------
+// The accumulator tile holds the full logits row of each of its 128 tokens; the two warps
+// of a TMEM lane quarter (column halves) combine their row max and exp sums through smem
+// under a 64-thread named barrier, then each writes its half of the bf16 dlogits (the head
+// backward GEMMs' operand), and the half-0 lane the per-token CE term and lse. Same math as
+// head_ce_k (graph.hpp:410-423 + logsumexp backward), tolerance-level sums.
+struct EpiHeadCE {
+    static constexpr int SLOTS = 1;
+    const int32_t* targets;
+    int64_t T;
+    float g_s2, g_ssum;
+    bf16* dlog;
+    float* diff;
+    float* lse;
+    __device__ void prefetch(const GemmGroup&, int, int, int, int) const {}
+    // CUDA's full-precision expf (not the glibc-exact one): the logits come out of a bf16
+    // tensor-core GEMM, so the loss is a tolerance quantity here and exact exp buys nothing
+    __device__ static float ex(float z) { return expf(z); }
+    __device__ void operator()(const GemmGroup& g, int mt, int nt, int r, uint32_t taddr,
+                               bool empty, int half, EpiOut& out) const {
+        const int64_t t = g.out_row0 + static_cast<int64_t>(mt) * GEMM_BM + r;
+        const bool valid = t < T;
+        const int lane = out.lane;
+        // this lane's exchange words in its own warp's staging; the partner warp (other
+        // column half of the same rows) is 4 warps away
+        float* mine = reinterpret_cast<float*>(out.base);
+        float* theirs = reinterpret_cast<float*>(out.base + (half ? -4 : 4) * SLOTS * EPI_SLOT_BYTES);
+        const int bar = 1 + ((r >> 5) & 3);  // per lane-quarter pair of warps
+        auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar) : "memory"); };
+        const int32_t tgt = valid ? __ldg(targets + t) : -1;
+        const int c0 = half * 128;
+        float mx = -INFINITY, picked = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < 128; c += 32) {
+            float v[32];
+            acc_load32(taddr + c0 + c, empty, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                mx = fmaxf(mx, v[i]);
+                if (c0 + c + i == tgt) picked = v[i];
+            }
+        }
+        mine[2 * lane] = mx;
+        mine[2 * lane + 1] = picked;
+        pair_sync();
+        mx = fmaxf(mx, theirs[2 * lane]);
+        const bool tgt_here = tgt >= c0 && tgt < c0 + 128;
+        if (!tgt_here) picked = theirs[2 * lane + 1];
+        pair_sync();  // exchange words reused below
+        float sum = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < 128; c += 32) {
+            float v[32];
+            acc_load32(taddr + c0 + c, empty, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) sum += ex(fsub(v[i], mx));
+        }
+        mine[2 * lane] = sum;
+        pair_sync();
+        const float total = half ? theirs[2 * lane] + sum : sum + theirs[2 * lane];
+        pair_sync();
+        const float lse_v = mx + logf(total);
+        if (valid && half == 0) {
+            diff[t] = lse_v + picked * -1.f;
+            lse[t] = lse_v;
+        }
+        // lse.grad = (0 + g_s2*lse) + g_s2*lse + g_ssum (z-loss mul, then ce add)
+        const float glse = fadd(fadd(fadd(0.f, fmul(g_s2, lse_v)), fmul(g_s2, lse_v)), g_ssum);
+        const float isum = 1.f / total;
+        bf16* drow = dlog + t * 256 + c0;
+#pragma unroll 1
+        for (int c = 0; c < 128; c += 64) {
+            uint4 pk[8];
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+                float v[32], o[32];
+                acc_load32(taddr + c0 + c + 32 * s2, empty, v);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const int j = c0 + c + 32 * s2 + i;
+                    const float base = (j == tgt) ? -1.f * g_ssum : 0.f;
+                    o[i] = valid ? fadd(base, fmul(glse, ex(fsub(v[i], mx)) * isum)) : 0.f;
+                }
+                pack_bf16x32(o, *reinterpret_cast<uint4(*)[4]>(&pk[4 * s2]));
+            }
+            out.put<8>(drow + c, pk);
+        }
+    }
+};
+
 static int g_num_sms = 0;
 int num_sms() {
     if (!g_num_sms) {
@@ -348,6 +438,14 @@ void gemm_store_f32(int bn, GemmMajor mj, const CUtensorMap& a, const CUtensorMa
         store_f32<256>(mj, a, b, g, ng, tiles, max_tiles, s);
     else
         store_f32<128>(mj, a, b, g, ng, tiles, max_tiles, s);
+}
+
+void gemm_head_ce(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
+                  const int32_t* tiles, int max_tiles, const int32_t* targets, int64_t T,
+                  float g_s2, float g_ssum, bf16* dlog, float* diff, float* lse,
+                  cudaStream_t s) {
+    launch<256, false, true>(a, b, g, ng, tiles, max_tiles,
+                             EpiHeadCE{targets, T, g_s2, g_ssum, dlog, diff, lse}, s);
 }
 
 void gemm_dswiglu(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,

@@ -88,7 +88,7 @@ void combine_forward(const float* h, const int32_t* hrow, const float* y, const 
 // CE + z on head logits; writes dlogits as bf16 (the head backward GEMM operand; padding
 // rows zero) and the per-token terms.
 void head_ce(const float* logits, const int32_t* targets, int64_t T, int64_t T_pad, int64_t V,
-             int expf_variant, float g_s2, float g_ssum, bf16* dlogits, float* diff,
+             float g_s2, float g_ssum, bf16* dlogits, float* diff,
              float* lse, cudaStream_t s);
 // Loss scalars (tolerance-level, deterministic tree order) -> out[5] (doubles)
 void losses_reduce(const float* diff, const float* lse_head, const float* lse_r,
@@ -169,6 +169,11 @@ void gemm_store_f32(int bn, GemmMajor mj, const CUtensorMap& a, const CUtensorMa
 void gemm_dswiglu(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
                   const int32_t* tiles, int max_tiles, const bf16* gu, int64_t f,
                   cudaStream_t s);
+// head forward (V == 256) with softmax-CE fused into the epilogue: writes bf16 dlogits
+// ([T_pad x 256], padding rows zero), the per-token CE term and lse (head_ce semantics)
+void gemm_head_ce(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
+                  const int32_t* tiles, int max_tiles, const int32_t* targets, int64_t T,
+                  float g_s2, float g_ssum, bf16* dlog, float* diff, float* lse, cudaStream_t s);
 void gemm_grad_w1(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
                   const int32_t* tiles, int max_tiles, cudaStream_t s);
 // dW GEMMs with MaskedAdamW fused into the epilogue (params, m, v and bf16 shadows are
