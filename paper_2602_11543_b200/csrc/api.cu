@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -144,6 +145,13 @@ struct spes_ctx {
     int node = 0, n_nodes = 1, device = 0;
     int expf_variant = 1;
     cudaStream_t stream = nullptr;
+    // low-priority side stream: the owned experts' AdamW runs there as soon as their dW
+    // GEMMs finish, under the router / norm / embedding backward on the main stream
+    cudaStream_t side = nullptr;
+    bool overlap_opt = true;
+    std::vector<cudaEvent_t> ev_dw;  // per layer
+    cudaEvent_t ev_join = nullptr;
+    std::vector<int64_t> layer_lo, layer_hi;  // owned experts' compact range per layer
     ncclComm_t comm = nullptr;
     int64_t launches = 0;
 
@@ -342,13 +350,18 @@ void build_ownership_tables(spes_ctx* c) {
     c->segs_host.push_back({L.off_head(), L.off_head(), L.V * L.d, 2, 0});     // head
     c->segs_host.push_back({2 * L.V * L.d, 2 * L.V * L.d, L.psi() - 2 * L.V * L.d, 0, 0});
     int64_t off = L.psi();
-    for (int l = 0; l < L.L; ++l)
+    c->layer_lo.assign(L.L, 0);
+    c->layer_hi.assign(L.L, 0);
+    for (int l = 0; l < L.L; ++l) {
+        c->layer_lo[l] = off;
         for (int j = 0; j < L.M; ++j)
             if (c->owned[j]) {
                 c->grad_off_host[static_cast<size_t>(l) * L.M + j] = off;
                 c->segs_host.push_back({L.off_expert(l, j), off, L.per_expert(), 1, l * L.M + j});
                 off += L.per_expert();
             }
+        c->layer_hi[l] = off;
+    }
     c->G = off;
     // (re)allocate grads / moments
     if (c->grads) {
@@ -563,6 +576,12 @@ Seeds seeds_for(const spes_ctx* c) {
     return s;
 }
 
+// Owned experts' AdamW on the side stream (not while profiling: the per-family event
+// timings need one serial stream).
+bool split_opt(const spes_ctx* c) {
+    return c->overlap_opt && !c->prof && !c->fused_opt && c->G > c->lay.psi();
+}
+
 void forward_backward(spes_ctx* c) {
     const Layout& L = c->lay;
     cudaStream_t st = c->stream;
@@ -700,6 +719,13 @@ void forward_backward(spes_ctx* c) {
                                        Y.tiles + 5, c->max_tiles[5], st);
             }
         }
+        if (split_opt(c)) {  // this layer's gradients are final and its operand copies read
+            ck(cudaEventRecord(c->ev_dw[l], st), "event");
+            ck(cudaStreamWaitEvent(c->side, c->ev_dw[l], 0), "wait");
+            spes_k::adamw(c->params, c->grads, c->m, c->v, c->segs,
+                          static_cast<int>(c->segs_host.size()), c->layer_lo[l], c->layer_hi[l],
+                          c->d_adam, shadows_of(c), c->d_losses, c->side, true);
+        }
         {
             PROF("router_bwd");
             spes_k::router_backward(hsrc(l), hmap(l), P + L.off_norm(l), P + L.off_router(l), Y.probs,
@@ -738,13 +764,19 @@ void optimizer_begin(spes_ctx* c, const spes_adamw_cfg* o) {
        "adam scalars");
 }
 
-// The rest of the step: psi (and, unfused, the owned experts) after the backward.
+// The rest of the step: psi (and, unfused and not split off, the owned experts) after
+// the backward; then the side stream joins.
 void optimizer_finish(spes_ctx* c) {
     PROF("adamw");
-    const int64_t n = c->fused_opt ? c->lay.psi() : c->G;  // psi is the compact prefix
+    const bool split = split_opt(c);
+    const int64_t n = c->fused_opt || split ? c->lay.psi() : c->G;  // psi is the compact prefix
     spes_k::adamw(c->params, c->grads, c->m, c->v, c->segs,
-                  static_cast<int>(c->segs_host.size()), n, c->d_adam, shadows_of(c),
+                  static_cast<int>(c->segs_host.size()), 0, n, c->d_adam, shadows_of(c),
                   c->d_losses, c->stream);
+    if (split) {
+        ck(cudaEventRecord(c->ev_join, c->side), "event");
+        ck(cudaStreamWaitEvent(c->stream, c->ev_join, 0), "wait");
+    }
 }
 
 void validate_tokens(const spes_ctx* c, const int32_t* tokens, int64_t n) {
@@ -942,7 +974,15 @@ spes_status spes_create(const spes_model_cfg* cfg, int32_t node, int32_t n_nodes
         c->device = cuda_device;
         ck(cudaSetDevice(cuda_device), "cudaSetDevice");
         set_counter(c.get());
-        ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+        int prio_lo = 0, prio_hi = 0;
+        ck(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi), "priorities");
+        ck(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi), "stream");
+        ck(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_lo), "stream");
+        ck(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming), "event");
+        c->ev_dw.resize(c->lay.L);
+        for (auto& e : c->ev_dw) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        if (const char* e = std::getenv("SPES_OPT_OVERLAP")) c->overlap_opt = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SPES_FUSED_OPT")) c->fused_opt = std::atoi(e) != 0;
         c->expf_variant = spes_expf::host_variant_from(&expf);
         spes_k::gemm_prepare(cuda_device);
         const Layout& L = c->lay;
@@ -1004,6 +1044,9 @@ void spes_destroy(spes_ctx* c) {
     c->scratch.release();
     c->persistent.release();
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->side) cudaStreamDestroy(c->side);
+    for (auto e : c->ev_dw) cudaEventDestroy(e);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->corpus) cudaFree(c->corpus);
     if (c->d_rows) cudaFree(c->d_rows);
     delete c;
@@ -1972,7 +2015,7 @@ spes_status spes_kernel_adamw(float* theta, const float* grad, float* m, float* 
                                     static_cast<float>(o->weight_decay), bc1, bc2};
         auto* da = D.alloc<spes_k::AdamScalars>(1);
         ck(cudaMemcpy(da, &a, sizeof(a), cudaMemcpyHostToDevice), "H2D");
-        spes_k::adamw(dt, dgr, dm, dv, ds, 1, n, da, spes_k::Shadows{nullptr, nullptr, nullptr, 0, 0},
+        spes_k::adamw(dt, dgr, dm, dv, ds, 1, 0, n, da, spes_k::Shadows{nullptr, nullptr, nullptr, 0, 0},
                       nullptr, 0);
         ck(cudaDeviceSynchronize(), "adamw kernel");
         ck(cudaMemcpy(theta, dt, 4 * n, cudaMemcpyDeviceToHost), "D2H");

@@ -1120,7 +1120,8 @@ __global__ void __launch_bounds__(256) adamw_k(float* __restrict__ params,
                                                const float* __restrict__ grads,
                                                float* __restrict__ m, float* __restrict__ v,
                                                const AdamSeg* segs, int nseg,
-                                               int64_t total4, const AdamScalars* __restrict__ ap,
+                                               int64_t lo4, int64_t total4,
+                                               const AdamScalars* __restrict__ ap,
                                                Shadows sh, const double* __restrict__ loss_total) {
     if (!loss_ok(loss_total)) return;
     const AdamScalars a = *ap;
@@ -1132,7 +1133,7 @@ __global__ void __launch_bounds__(256) adamw_k(float* __restrict__ params,
         segs = s_segs;
     }
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * ADAM_U;
-    for (int64_t base = (static_cast<int64_t>(blockIdx.x) * blockDim.x) * ADAM_U + threadIdx.x;
+    for (int64_t base = lo4 + (static_cast<int64_t>(blockIdx.x) * blockDim.x) * ADAM_U + threadIdx.x;
          base < total4; base += stride) {
         float4 th[ADAM_U], g[ADAM_U], mm[ADAM_U], vv[ADAM_U];
         AdamSeg sg[ADAM_U];
@@ -1167,12 +1168,17 @@ __global__ void __launch_bounds__(256) adamw_k(float* __restrict__ params,
 }
 
 void adamw(float* params, const float* grads, float* m, float* v, const AdamSeg* segs, int nseg,
-           int64_t total, const AdamScalars* a, Shadows sh, const double* loss_total,
-           cudaStream_t s) {
-    const int64_t total4 = total / 4;
-    if (total4 == 0) return;
-    const int blocks = static_cast<int>(std::min<int64_t>(cdiv(total4, 256 * ADAM_U), 148 * 8));
-    adamw_k<<<blocks, 256, 0, s>>>(params, grads, m, v, segs, nseg, total4, a, sh, loss_total);
+           int64_t lo, int64_t hi, const AdamScalars* a, Shadows sh, const double* loss_total,
+           cudaStream_t s, bool short_blocks) {
+    const int64_t lo4 = lo / 4, total4 = hi / 4;  // segment lengths are multiples of 4
+    if (total4 <= lo4) return;
+    // persistent grid, or (background launches) short blocks of 4 strides each, so that a
+    // higher-priority stream's blocks get SMs as these retire
+    const int blocks = static_cast<int>(
+        short_blocks ? cdiv(total4 - lo4, 256 * ADAM_U * 4)
+                     : std::min<int64_t>(cdiv(total4 - lo4, 256 * ADAM_U), 148 * 8));
+    adamw_k<<<blocks, 256, 0, s>>>(params, grads, m, v, segs, nseg, lo4, total4, a, sh,
+                                   loss_total);
     count_launch();
 }
 

@@ -130,9 +130,10 @@ struct Shadows {
 // MaskedAdamW step over the first `total` compact scalars; also writes the refreshed
 // bf16 copies. No update when *loss_total is non-finite (loss_total may be null).
 using spes_dev::AdamScalars;
+// compact elements [lo, hi) (multiples of 4)
 void adamw(float* params, const float* grads, float* m, float* v, const AdamSeg* segs, int nseg,
-           int64_t total, const AdamScalars* a, Shadows sh, const double* loss_total,
-           cudaStream_t s);  // a: device memory (graph-replayable)
+           int64_t lo, int64_t hi, const AdamScalars* a, Shadows sh, const double* loss_total,
+           cudaStream_t s, bool short_blocks = false);  // a: device memory (graph-replayable)
 // Rewrite every bf16 copy from the fp32 parameters (after load / sync / merge).
 void refresh_shadows(const float* params, const AdamSeg* segs, int nseg, int64_t total,
                      Shadows sh, cudaStream_t s);
