@@ -475,7 +475,7 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     c->gnormed = A.alloc<float>(Tp * d);
     c->normed_bf = A.alloc<bf16>(Tp * d);
     c->gh = A.alloc<float>(Tp * d);
-    c->nr_partial = A.alloc<float>(64 * d * (M + 1));  // NRG_TC token chunks
+    c->nr_partial = A.alloc<float>(spes_k::kNormRouterChunks * d * (M + 1));
     c->hL = A.alloc<bf16>(Tp * d);
     ck(cudaMemsetAsync(c->hL, 0, sizeof(bf16) * Tp * d, c->stream), "hL");  // padding rows
     c->head_logits = A.alloc<float>(Tp * V);

@@ -690,7 +690,7 @@ void combine_backward(const float* gh, const float* y, const int32_t* row_token,
 // grid (d/128, NRG_TC, ceil(M/16)), 256 threads: warp ph takes tokens t = ph (mod 8) of
 // the chunk, lane tx the columns 4tx..4tx+3 of the 128-column slab (float4 streams);
 // each thread keeps 4 columns x 16 experts of router-gradient partials in registers.
-constexpr int NRG_TC = 64;
+constexpr int NRG_TC = kNormRouterChunks;
 constexpr int NG_QT_RMS = 128;  // columns per normed_grad tile = dot partials per token (d / 128)
 constexpr int NRG_EG = 16;
 // With `gh` non-null the z = 0 blocks also apply the rmsnorm backward to their columns

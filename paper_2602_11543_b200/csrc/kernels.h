@@ -110,6 +110,9 @@ void router_backward(const float* h, const int32_t* hrow, const float* gain, con
                      float* dot_part, float* gh, cudaStream_t s);  // gh null: rmsnorm bwd deferred
 // normed is recomputed exactly from h, inv_rms and the gain (not stored in forward)
 // gh non-null: also applies the rmsnorm backward (router_backward then skips it)
+// token chunks of norm_router_grads ((d/128) x 37 blocks = whole waves of 2 per SM); its
+// partial buffer holds kNormRouterChunks * d * (M + 1) floats
+constexpr int kNormRouterChunks = 37;
 void norm_router_grads(const float* h, const int32_t* hrow, const float* gain, const float* gnormed,
                        const float* glog, const float* inv_rms, int64_t T, int64_t d, int M,
                        float* partial, float* g_gain, float* g_router, const float* dot_part,
