@@ -15,6 +15,16 @@ __device__ __forceinline__ float fsub(float a, float b) { return __fsub_rn(a, b)
 __device__ __forceinline__ float fmul(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ float fdiv(float a, float b) { return __fdiv_rn(a, b); }
 __device__ __forceinline__ float fsqrt(float a) { return __fsqrt_rn(a); }
+// Two exactly rounded products in one instruction (FMUL2, sm_100). Sum the halves with
+// the scalar fadd only: ptxas contracts mul.rn.f32x2 followed by add.rn.f32x2 into FFMA2.
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<const unsigned long long*>(&a)),
+          "l"(*reinterpret_cast<const unsigned long long*>(&b)));
+    return *reinterpret_cast<const float2*>(&r);
+}
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;

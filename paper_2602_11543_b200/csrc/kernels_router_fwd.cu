@@ -185,13 +185,16 @@ __global__ void __launch_bounds__(32 * RF_WARPS) router_fwd_k(
             for (int j = 0; j < TT; ++j) {
                 const float* xrow = sxw[warp * RF_XS + c % RF_XS][r0 + j];
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
+                for (int u = 0; u < 2; ++u) {  // (x * inv) * g, two lanes per FMUL2
                     const float4 x = *reinterpret_cast<const float4*>(xrow + 4 * (i + u));
                     const float4 g = *reinterpret_cast<const float4*>(gg + 4 * (i + u));
-                    nv[j][4 * u + 0] = fmul(fmul(x.x, inv[j]), g.x);
-                    nv[j][4 * u + 1] = fmul(fmul(x.y, inv[j]), g.y);
-                    nv[j][4 * u + 2] = fmul(fmul(x.z, inv[j]), g.z);
-                    nv[j][4 * u + 3] = fmul(fmul(x.w, inv[j]), g.w);
+                    const float2 iv = make_float2(inv[j], inv[j]);
+                    const float2 lo = fmul2(fmul2(make_float2(x.x, x.y), iv), make_float2(g.x, g.y));
+                    const float2 hi = fmul2(fmul2(make_float2(x.z, x.w), iv), make_float2(g.z, g.w));
+                    nv[j][4 * u + 0] = lo.x;
+                    nv[j][4 * u + 1] = lo.y;
+                    nv[j][4 * u + 2] = hi.x;
+                    nv[j][4 * u + 3] = hi.y;
                 }
             }
 #pragma unroll
@@ -202,10 +205,13 @@ __global__ void __launch_bounds__(32 * RF_WARPS) router_fwd_k(
                     const float4 r = *reinterpret_cast<const float4*>(rrow + e4);
 #pragma unroll
                     for (int j = 0; j < TT; ++j) {
-                        acc[j][e4 + 0] = fadd(acc[j][e4 + 0], fmul(nv[j][jp], r.x));
-                        acc[j][e4 + 1] = fadd(acc[j][e4 + 1], fmul(nv[j][jp], r.y));
-                        acc[j][e4 + 2] = fadd(acc[j][e4 + 2], fmul(nv[j][jp], r.z));
-                        acc[j][e4 + 3] = fadd(acc[j][e4 + 3], fmul(nv[j][jp], r.w));
+                        const float2 nn = make_float2(nv[j][jp], nv[j][jp]);
+                        const float2 p01 = fmul2(nn, make_float2(r.x, r.y));
+                        const float2 p23 = fmul2(nn, make_float2(r.z, r.w));
+                        acc[j][e4 + 0] = fadd(acc[j][e4 + 0], p01.x);
+                        acc[j][e4 + 1] = fadd(acc[j][e4 + 1], p01.y);
+                        acc[j][e4 + 2] = fadd(acc[j][e4 + 2], p23.x);
+                        acc[j][e4 + 3] = fadd(acc[j][e4 + 3], p23.y);
                     }
                 }
             }
