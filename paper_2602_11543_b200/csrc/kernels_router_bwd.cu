@@ -117,11 +117,16 @@ __global__ void __launch_bounds__(256) normed_grad_k(
 #pragma unroll
         for (int i = 0; i < 4; ++i) g[i] = sG[ty * 4 + i][e];
         const float4 r4 = *reinterpret_cast<const float4*>(&sRT[e][4 * tx]);
-        const float r[4] = {r4.x, r4.y, r4.z, r4.w};
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) sr[i][j] = fadd(sr[i][j], fmul(g[i], r[j]));
+        for (int i = 0; i < 4; ++i) {
+            const float2 gi = make_float2(g[i], g[i]);
+            const float2 p01 = fmul2(gi, make_float2(r4.x, r4.y));
+            const float2 p23 = fmul2(gi, make_float2(r4.z, r4.w));
+            sr[i][0] = fadd(sr[i][0], p01.x);
+            sr[i][1] = fadd(sr[i][1], p01.y);
+            sr[i][2] = fadd(sr[i][2], p23.x);
+            sr[i][3] = fadd(sr[i][3], p23.y);
+        }
     }
     const float4 gq = __ldg(reinterpret_cast<const float4*>(gain + q0 + 4 * tx));
 #pragma unroll

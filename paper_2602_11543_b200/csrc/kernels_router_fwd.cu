@@ -138,10 +138,12 @@ __global__ void __launch_bounds__(32 * RF_WARPS) router_fwd_k(
 #pragma unroll
             for (int i = 0; i < QC; ++i) {
                 const float4 x = *reinterpret_cast<const float4*>(xrow + 4 * i);
-                ms[j] = fadd(ms[j], fmul(x.x, x.x));
-                ms[j] = fadd(ms[j], fmul(x.y, x.y));
-                ms[j] = fadd(ms[j], fmul(x.z, x.z));
-                ms[j] = fadd(ms[j], fmul(x.w, x.w));
+                const float2 lo = fmul2(make_float2(x.x, x.y), make_float2(x.x, x.y));
+                const float2 hi = fmul2(make_float2(x.z, x.w), make_float2(x.z, x.w));
+                ms[j] = fadd(ms[j], lo.x);
+                ms[j] = fadd(ms[j], lo.y);
+                ms[j] = fadd(ms[j], hi.x);
+                ms[j] = fadd(ms[j], hi.y);
             }
         }
     }
