@@ -151,6 +151,7 @@ struct spes_ctx {
     bool overlap_opt = true;
     std::vector<cudaEvent_t> ev_dw;  // per layer
     cudaEvent_t ev_join = nullptr;
+    cudaEvent_t ev_fork[3] = {}, ev_ready[3] = {};  // side-stream hand-offs within a step
     std::vector<int64_t> layer_lo, layer_hi;  // owned experts' compact range per layer
     ncclComm_t comm = nullptr;
     int64_t launches = 0;
@@ -576,10 +577,12 @@ Seeds seeds_for(const spes_ctx* c) {
     return s;
 }
 
-// Owned experts' AdamW on the side stream (not while profiling: the per-family event
-// timings need one serial stream).
+// Off-critical-path work on the low-priority side stream (not while profiling: the
+// per-family event timings need one serial stream).
+bool use_side(const spes_ctx* c) { return c->overlap_opt && !c->prof; }
+// owned experts' AdamW there, right after their dW GEMMs
 bool split_opt(const spes_ctx* c) {
-    return c->overlap_opt && !c->prof && !c->fused_opt && c->G > c->lay.psi();
+    return use_side(c) && !c->fused_opt && c->G > c->lay.psi();
 }
 
 void forward_backward(spes_ctx* c) {
@@ -595,12 +598,34 @@ void forward_backward(spes_ctx* c) {
         return (l == 0 && c->virtual_h0) ? P + L.off_emb() : c->h[l];
     };
     auto hmap = [&](int l) -> const int32_t* { return (l == 0 && c->virtual_h0) ? c->inputs : nullptr; };
+    // side-stream hand-offs: fork(i) starts side work after everything enqueued on st so
+    // far; ready(i) marks it done; need(i) makes st wait for it. Serial when profiling.
+    const bool side = use_side(c);
+    cudaStream_t ss = side ? c->side : st;
+    auto fork = [&](int i) {
+        if (!side) return;
+        ck(cudaEventRecord(c->ev_fork[i], st), "event");
+        ck(cudaStreamWaitEvent(ss, c->ev_fork[i], 0), "wait");
+    };
+    auto ready = [&](int i) {
+        if (side) ck(cudaEventRecord(c->ev_ready[i], ss), "event");
+    };
+    auto need = [&](int i) {
+        if (side) ck(cudaStreamWaitEvent(st, c->ev_ready[i], 0), "wait");
+    };
 #define PROF(name) Prof _prof_##__LINE__(c, name)
     {
         PROF("embed_gather");
         spes_k::embed_gather(P + L.off_emb(), c->tokens, c->B, c->S, d, V,
                              c->virtual_h0 ? nullptr : c->h[0], c->inputs,
                              c->targets, c->err, st);
+    }
+    bool eg_planned = false;
+    {  // token bucketing for the embedding gradient: only needs the inputs
+        PROF("embed_grad");
+        fork(0);
+        eg_planned = spes_k::embed_grad_plan(c->inputs, T, V, c->eg_scratch, ss);
+        ready(0);
     }
     for (int l = 0; l < L.L; ++l) {
         LayerBufs& Y = c->layers[l];
@@ -657,9 +682,11 @@ void forward_backward(spes_ctx* c) {
         if (V != 256)
             spes_k::head_ce(c->head_logits, c->targets, T, Tp, V, sd.g_s2,
                             sd.g_ssum, c->dlog_bf, c->diff, c->lse_head, st);
+        fork(1);  // loss scalars: read by the host and by the optimizer's finite-loss guard
         spes_k::losses_reduce(c->diff, c->lse_head, c->lse_all, c->probs_all, c->coeff_all, T, Tp,
                               L.L, M, sd.inv_T, sd.inv_L, sd.c_ce, sd.c_lb, sd.c_mz, sd.c_z,
-                              c->loss_part, c->d_losses, st);
+                              c->loss_part, c->d_losses, ss);
+        ready(1);
     }
     // ---- backward ----
     {
@@ -681,6 +708,16 @@ void forward_backward(spes_ctx* c) {
             spes_k::combine_backward(c->gh, Y.y, Y.row_token, Y.row_w, Y.pad_off + M, R, d, c->dyw,
                                      c->gw_part, st);
         }
+        {  // the router's per-token scalar chain only needs the gate-weight gradients: it
+           // runs beside the expert GEMMs
+            PROF("router_bwd");
+            fork(2);
+            spes_k::router_scalar_backward(Y.probs, Y.lse_r, Y.denom, Y.topk_idx, Y.slot_row,
+                                           c->gw_part, Y.lb_coeff, T, M, k,
+                                           c->cfg.renormalize_after_topk, sd.g_lbsum, sd.g_s,
+                                           c->glog, ss);
+            ready(2);
+        }
         {
             PROF("gemm_bwd_dh");
             spes_k::gemm_dswiglu(bn_for(f), c->a_dyw, Y.b_w2, Y.groups + 2 * M, M, Y.tiles + 2,
@@ -693,6 +730,7 @@ void forward_backward(spes_ctx* c) {
                                    c->max_tiles[3], st);
         }
         if (c->max_tiles[4] > 0 && c->fused_opt) {
+            need(1);  // the epilogues' finite-loss guard reads the loss scalars
             // owned experts: dW and MaskedAdamW in one pass (no gradient materialized)
             const spes_k::Shadows sh = shadows_of(c);
             const spes_k::AdamEpi ae{c->d_adam, c->m, c->v, sh.w1, sh.w2, d, f, c->d_losses};
@@ -728,11 +766,10 @@ void forward_backward(spes_ctx* c) {
         }
         {
             PROF("router_bwd");
-            spes_k::router_backward(hsrc(l), hmap(l), P + L.off_norm(l), P + L.off_router(l), Y.probs,
-                                    Y.lse_r, Y.inv_rms, Y.denom, Y.topk_idx, Y.slot_row,
-                                    c->gw_part, c->dxp, Y.lb_coeff, T, d, M, k,
-                                    c->cfg.renormalize_after_topk, sd.g_lbsum, sd.g_s, c->glog,
-                                    c->gnormed, c->dot_part, nullptr, st);
+            need(2);  // glog (and, earlier on the side stream, the loss scalars)
+            spes_k::normed_grad(hsrc(l), hmap(l), P + L.off_norm(l), P + L.off_router(l), Y.inv_rms,
+                                Y.slot_row, c->dxp, T, d, M, k, c->glog, c->gnormed, c->dot_part,
+                                nullptr, st);
         }
         {
             PROF("norm_router_grads");  // + rmsnorm backward into gh
@@ -743,7 +780,9 @@ void forward_backward(spes_ctx* c) {
     }
     {
         PROF("embed_grad");
-        spes_k::embed_grad(c->inputs, c->gh, T, d, V, c->grads + L.off_emb(), c->eg_scratch, st);
+        if (eg_planned) need(0);
+        spes_k::embed_grad_apply(c->inputs, c->gh, T, d, V, c->grads + L.off_emb(), c->eg_scratch,
+                                 st);
     }
 }
 
@@ -773,7 +812,7 @@ void optimizer_finish(spes_ctx* c) {
     spes_k::adamw(c->params, c->grads, c->m, c->v, c->segs,
                   static_cast<int>(c->segs_host.size()), 0, n, c->d_adam, shadows_of(c),
                   c->d_losses, c->stream);
-    if (split) {
+    if (use_side(c)) {  // everything enqueued on the side stream this step
         ck(cudaEventRecord(c->ev_join, c->side), "event");
         ck(cudaStreamWaitEvent(c->stream, c->ev_join, 0), "wait");
     }
@@ -979,6 +1018,10 @@ spes_status spes_create(const spes_model_cfg* cfg, int32_t node, int32_t n_nodes
         ck(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi), "stream");
         ck(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_lo), "stream");
         ck(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming), "event");
+        for (int i = 0; i < 3; ++i) {
+            ck(cudaEventCreateWithFlags(&c->ev_fork[i], cudaEventDisableTiming), "event");
+            ck(cudaEventCreateWithFlags(&c->ev_ready[i], cudaEventDisableTiming), "event");
+        }
         c->ev_dw.resize(c->lay.L);
         for (auto& e : c->ev_dw) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
         if (const char* e = std::getenv("SPES_OPT_OVERLAP")) c->overlap_opt = std::atoi(e) != 0;
@@ -1047,6 +1090,10 @@ void spes_destroy(spes_ctx* c) {
     if (c->side) cudaStreamDestroy(c->side);
     for (auto e : c->ev_dw) cudaEventDestroy(e);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
+    for (int i = 0; i < 3; ++i) {
+        if (c->ev_fork[i]) cudaEventDestroy(c->ev_fork[i]);
+        if (c->ev_ready[i]) cudaEventDestroy(c->ev_ready[i]);
+    }
     if (c->corpus) cudaFree(c->corpus);
     if (c->d_rows) cudaFree(c->d_rows);
     delete c;

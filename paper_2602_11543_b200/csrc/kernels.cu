@@ -995,24 +995,37 @@ __global__ void __launch_bounds__(64) embed_grad_sum_k(const int32_t* __restrict
     *reinterpret_cast<float4*>(g_emb + static_cast<int64_t>(v) * d + q) = acc;
 }
 
-void embed_grad(const int32_t* inputs, const float* gh0, int64_t T, int64_t d, int64_t V,
-                float* g_emb, int32_t* scratch, cudaStream_t s) {
-    if (V <= EG_MAXV && scratch) {
-        int32_t* cnt = scratch;           // [V]
-        int32_t* off = scratch + V;       // [V + 1]
-        int32_t* list = scratch + 2 * V + 1;  // [T]
-        cudaMemsetAsync(cnt, 0, sizeof(int32_t) * V, s);
-        vocab_hist_k<<<static_cast<unsigned>(cdiv(T, 256)), 256, 0, s>>>(inputs, T, cnt);
-        vocab_scan_k<<<1, EG_MAXV, 0, s>>>(cnt, static_cast<int>(V), off);
-        vocab_bucket_k<<<static_cast<unsigned>(V), 256, 0, s>>>(inputs, T, off, list);
+bool embed_grad_plan(const int32_t* inputs, int64_t T, int64_t V, int32_t* scratch,
+                     cudaStream_t s) {
+    if (!(V <= EG_MAXV && scratch)) return false;
+    int32_t* cnt = scratch;               // [V]
+    int32_t* off = scratch + V;           // [V + 1]
+    int32_t* list = scratch + 2 * V + 1;  // [T]
+    cudaMemsetAsync(cnt, 0, sizeof(int32_t) * V, s);
+    vocab_hist_k<<<static_cast<unsigned>(cdiv(T, 256)), 256, 0, s>>>(inputs, T, cnt);
+    vocab_scan_k<<<1, EG_MAXV, 0, s>>>(cnt, static_cast<int>(V), off);
+    vocab_bucket_k<<<static_cast<unsigned>(V), 256, 0, s>>>(inputs, T, off, list);
+    count_launch(3);
+    return true;
+}
+
+void embed_grad_apply(const int32_t* inputs, const float* gh0, int64_t T, int64_t d, int64_t V,
+                      float* g_emb, int32_t* scratch, cudaStream_t s) {
+    if (V <= EG_MAXV && scratch) {  // planned by embed_grad_plan
         dim3 grid(static_cast<unsigned>(V), static_cast<unsigned>(cdiv(d, 256)));
-        embed_grad_sum_k<<<grid, 64, 0, s>>>(off, list, gh0, d, g_emb);
-        count_launch(4);
+        embed_grad_sum_k<<<grid, 64, 0, s>>>(scratch + V, scratch + 2 * V + 1, gh0, d, g_emb);
+        count_launch();
         return;
     }
     dim3 grid(static_cast<unsigned>(V), static_cast<unsigned>(cdiv(d, 1024)));
     embed_grad_k<<<grid, 256, 0, s>>>(inputs, gh0, T, d, g_emb);
     count_launch();
+}
+
+void embed_grad(const int32_t* inputs, const float* gh0, int64_t T, int64_t d, int64_t V,
+                float* g_emb, int32_t* scratch, cudaStream_t s) {
+    embed_grad_plan(inputs, T, V, scratch, s);
+    embed_grad_apply(inputs, gh0, T, d, V, g_emb, scratch, s);
 }
 
 // ============================ device corpus batches ============================

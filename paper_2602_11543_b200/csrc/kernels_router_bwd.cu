@@ -193,6 +193,39 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_k(const float* __restrict__ h
     }
 }
 
+void router_scalar_backward(const float* probs, const float* lse_r, const float* denom,
+                            const int32_t* topk_idx, const int32_t* slot_row, const float* gw_row,
+                            const float* lb_coeff, int64_t T, int M, int k, int renorm,
+                            float g_lbsum, float g_s, float* glog, cudaStream_t s) {
+    const unsigned g1 = static_cast<unsigned>((T + 127) / 128);
+    auto f = M <= 8    ? router_scalar_bwd_k<8>
+             : M <= 16 ? router_scalar_bwd_k<16>
+             : M <= 32 ? router_scalar_bwd_k<32>
+                       : router_scalar_bwd_k<64>;
+    f<<<g1, 128, 0, s>>>(probs, lse_r, denom, topk_idx, slot_row, gw_row, lb_coeff, (int)T, M, k,
+                         renorm, g_lbsum, g_s, glog);
+    count_launch();
+}
+
+void normed_grad(const float* h, const int32_t* hrow, const float* gain, const float* router,
+                 const float* inv_rms, const int32_t* slot_row, const float* dxp, int64_t T,
+                 int64_t d, int M, int k, const float* glog, float* gnormed, float* dot_part,
+                 float* gh, cudaStream_t s) {
+    const dim3 g2(static_cast<unsigned>((T + NG_TT - 1) / NG_TT), static_cast<unsigned>(d / NG_QT));
+    auto f = M <= 8    ? normed_grad_k<8>
+             : M <= 16 ? normed_grad_k<16>
+             : M <= 32 ? normed_grad_k<32>
+                       : normed_grad_k<64>;
+    f<<<g2, 256, 0, s>>>(h, hrow, gain, router, glog, slot_row, dxp, (int)T, (int)d, M, k, gnormed,
+                         dot_part);
+    count_launch();
+    if (gh) {
+        const unsigned g3 = static_cast<unsigned>((T + 7) / 8);
+        rmsnorm_bwd_k<<<g3, 256, 0, s>>>(h, hrow, gain, inv_rms, gnormed, dot_part, (int)T, (int)d, gh);
+        count_launch();
+    }
+}
+
 void router_backward(const float* h, const int32_t* hrow, const float* gain, const float* router,
                      const float* probs,
                      const float* lse_r, const float* inv_rms, const float* denom,
@@ -200,31 +233,10 @@ void router_backward(const float* h, const int32_t* hrow, const float* gain, con
                      const float* dxp, const float* lb_coeff, int64_t T, int64_t d, int M, int k,
                      int renorm, float g_lbsum, float g_s, float* glog, float* gnormed,
                      float* dot_part, float* gh, cudaStream_t s) {
-    const unsigned g1 = static_cast<unsigned>((T + 127) / 128);
-    const dim3 g2(static_cast<unsigned>((T + NG_TT - 1) / NG_TT), static_cast<unsigned>(d / NG_QT));
-    const unsigned g3 = static_cast<unsigned>((T + 7) / 8);
-#define SPES_RB(MM)                                                                             \
-    do {                                                                                        \
-        router_scalar_bwd_k<MM><<<g1, 128, 0, s>>>(probs, lse_r, denom, topk_idx, slot_row,     \
-                                                   gw_row, lb_coeff, (int)T, M, k, renorm,      \
-                                                   g_lbsum, g_s, glog);                         \
-        normed_grad_k<MM><<<g2, 256, 0, s>>>(h, hrow, gain, router, glog, slot_row, dxp, (int)T, \
-                                             (int)d, M, k, gnormed, dot_part);                  \
-    } while (0)
-    if (M <= 8)
-        SPES_RB(8);
-    else if (M <= 16)
-        SPES_RB(16);
-    else if (M <= 32)
-        SPES_RB(32);
-    else
-        SPES_RB(64);
-#undef SPES_RB
-    if (gh) {
-        rmsnorm_bwd_k<<<g3, 256, 0, s>>>(h, hrow, gain, inv_rms, gnormed, dot_part, (int)T, (int)d, gh);
-        count_launch();
-    }
-    count_launch(2);
+    router_scalar_backward(probs, lse_r, denom, topk_idx, slot_row, gw_row, lb_coeff, T, M, k,
+                           renorm, g_lbsum, g_s, glog, s);
+    normed_grad(h, hrow, gain, router, inv_rms, slot_row, dxp, T, d, M, k, glog, gnormed, dot_part,
+                gh, s);
 }
 
 }  // namespace spes_k
