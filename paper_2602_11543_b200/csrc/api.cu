@@ -149,9 +149,9 @@ struct spes_ctx {
     // GEMMs finish, under the router / norm / embedding backward on the main stream
     cudaStream_t side = nullptr;
     bool overlap_opt = true;
-    std::vector<cudaEvent_t> ev_dw;  // per layer
+    bool early_wd = true;  // wd's AdamW starts right after dW_down (else with wg|wu)
     cudaEvent_t ev_join = nullptr;
-    cudaEvent_t ev_fork[3] = {}, ev_ready[3] = {};  // side-stream hand-offs within a step
+    cudaEvent_t ev_fork[5] = {}, ev_ready[5] = {};  // side-stream hand-offs within a step
     std::vector<int64_t> layer_lo, layer_hi;  // owned experts' compact range per layer
     ncclComm_t comm = nullptr;
     int64_t launches = 0;
@@ -718,10 +718,35 @@ void forward_backward(spes_ctx* c) {
                                            c->glog, ss);
             ready(2);
         }
+        const bool unfused_dw = c->max_tiles[4] > 0 && !c->fused_opt;
+        // owned experts' AdamW for the weights of this layer whose gradients are final and
+        // whose bf16 operand copies the remaining GEMMs no longer read: wd (sub = 2) after
+        // dW_down (dH read W2 before), wg|wu (sub = 0) after dW_gu (dX read W1 before)
+        auto expert_adamw = [&](int sub, int ev) {
+            if (!split_opt(c)) return;
+            const int64_t df = d * f, per = 3 * df;
+            const int nown = static_cast<int>((c->layer_hi[l] - c->layer_lo[l]) / per);
+            if (!c->early_wd && sub == 2) return;
+            const int64_t off = sub == 2 ? 2 * df : 0;
+            const int64_t len = sub == 2 ? df : (c->early_wd ? 2 * df : per);
+            fork(ev);
+            spes_k::adamw_strided(c->params, c->grads, c->m, c->v, c->segs,
+                                  static_cast<int>(c->segs_host.size()), c->layer_lo[l] + off,
+                                  per, len, nown, c->d_adam, shadows_of(c), c->d_losses, ss);
+        };
         {
             PROF("gemm_bwd_dh");
             spes_k::gemm_dswiglu(bn_for(f), c->a_dyw, Y.b_w2, Y.groups + 2 * M, M, Y.tiles + 2,
                                  c->max_tiles[2], Y.gu, f, st);
+        }
+        if (unfused_dw) {
+            {
+                PROF("gemm_bwd_dw_down");
+                spes_k::gemm_store_f32(bn_for(d), spes_k::GemmMajor::MNMN, Y.a_hact_mn,
+                                       c->b_dyw_mn, Y.groups + 5 * M, M,
+                                       Y.tiles + 5, c->max_tiles[5], st);
+            }
+            expert_adamw(2, 3);
         }
         {
             PROF("gemm_bwd_dx");
@@ -744,25 +769,13 @@ void forward_backward(spes_ctx* c) {
                 spes_k::gemm_adamw_w2(bn_for(d), Y.a_hact_mn, c->b_dyw_mn, Y.groups + 5 * M, M,
                                       Y.tiles + 5, c->max_tiles[5], ae, st);
             }
-        } else if (c->max_tiles[4] > 0) {
+        } else if (unfused_dw) {
             {
                 PROF("gemm_bwd_dw_gate_up");
                 spes_k::gemm_grad_w1(Y.a_xp_mn, c->b_dgu_mn, Y.groups + 4 * M, M, Y.tiles + 4,
                                      c->max_tiles[4], st);
             }
-            {
-                PROF("gemm_bwd_dw_down");
-                spes_k::gemm_store_f32(bn_for(d), spes_k::GemmMajor::MNMN, Y.a_hact_mn,
-                                       c->b_dyw_mn, Y.groups + 5 * M, M,
-                                       Y.tiles + 5, c->max_tiles[5], st);
-            }
-        }
-        if (split_opt(c)) {  // this layer's gradients are final and its operand copies read
-            ck(cudaEventRecord(c->ev_dw[l], st), "event");
-            ck(cudaStreamWaitEvent(c->side, c->ev_dw[l], 0), "wait");
-            spes_k::adamw(c->params, c->grads, c->m, c->v, c->segs,
-                          static_cast<int>(c->segs_host.size()), c->layer_lo[l], c->layer_hi[l],
-                          c->d_adam, shadows_of(c), c->d_losses, c->side, true);
+            expert_adamw(0, 4);
         }
         {
             PROF("router_bwd");
@@ -1018,14 +1031,13 @@ spes_status spes_create(const spes_model_cfg* cfg, int32_t node, int32_t n_nodes
         ck(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi), "stream");
         ck(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_lo), "stream");
         ck(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming), "event");
-        for (int i = 0; i < 3; ++i) {
+        for (int i = 0; i < 5; ++i) {
             ck(cudaEventCreateWithFlags(&c->ev_fork[i], cudaEventDisableTiming), "event");
             ck(cudaEventCreateWithFlags(&c->ev_ready[i], cudaEventDisableTiming), "event");
         }
-        c->ev_dw.resize(c->lay.L);
-        for (auto& e : c->ev_dw) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
         if (const char* e = std::getenv("SPES_OPT_OVERLAP")) c->overlap_opt = std::atoi(e) != 0;
         if (const char* e = std::getenv("SPES_FUSED_OPT")) c->fused_opt = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SPES_EARLY_WD")) c->early_wd = std::atoi(e) != 0;
         c->expf_variant = spes_expf::host_variant_from(&expf);
         spes_k::gemm_prepare(cuda_device);
         const Layout& L = c->lay;
@@ -1088,9 +1100,8 @@ void spes_destroy(spes_ctx* c) {
     c->persistent.release();
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->side) cudaStreamDestroy(c->side);
-    for (auto e : c->ev_dw) cudaEventDestroy(e);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < 5; ++i) {
         if (c->ev_fork[i]) cudaEventDestroy(c->ev_fork[i]);
         if (c->ev_ready[i]) cudaEventDestroy(c->ev_ready[i]);
     }

@@ -1128,25 +1128,29 @@ __device__ __forceinline__ void write_shadow4(const AdamSeg& sg, int64_t o, cons
 // before any update); segments are never split inside a group because every segment
 // length is a multiple of 4.
 constexpr int ADAM_U = 2;
-constexpr int ADAM_MAX_SEGS = 256;  // segment table in smem up to this size
+constexpr int ADAM_MAX_SEGS = 256;  // segment table in (dynamic) smem up to this size
+// Elements: blockIdx.y picks the piece [lo4 + y*blk4, + n4) (float4 units) of a strided
+// set (one piece = one contiguous range in the common case; a weight of every owned
+// expert for the background launches); blockIdx.x / threadIdx walk the piece.
 __global__ void __launch_bounds__(256) adamw_k(float* __restrict__ params,
                                                const float* __restrict__ grads,
                                                float* __restrict__ m, float* __restrict__ v,
-                                               const AdamSeg* segs, int nseg,
-                                               int64_t lo4, int64_t total4,
+                                               const AdamSeg* segs, int nseg, int seg_smem,
+                                               int64_t lo4, int64_t blk4, int64_t n4,
                                                const AdamScalars* __restrict__ ap,
                                                Shadows sh, const double* __restrict__ loss_total) {
     if (!loss_ok(loss_total)) return;
     const AdamScalars a = *ap;
-    __shared__ AdamSeg s_segs[ADAM_MAX_SEGS];
-    const bool seg_smem = nseg <= ADAM_MAX_SEGS;
+    extern __shared__ AdamSeg s_segs[];
     if (seg_smem) {
         for (int i = threadIdx.x; i < nseg; i += blockDim.x) s_segs[i] = segs[i];
         __syncthreads();
         segs = s_segs;
     }
+    const int64_t first = lo4 + static_cast<int64_t>(blockIdx.y) * blk4;
+    const int64_t total4 = first + n4;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * ADAM_U;
-    for (int64_t base = lo4 + (static_cast<int64_t>(blockIdx.x) * blockDim.x) * ADAM_U + threadIdx.x;
+    for (int64_t base = first + (static_cast<int64_t>(blockIdx.x) * blockDim.x) * ADAM_U + threadIdx.x;
          base < total4; base += stride) {
         float4 th[ADAM_U], g[ADAM_U], mm[ADAM_U], vv[ADAM_U];
         AdamSeg sg[ADAM_U];
@@ -1180,19 +1184,37 @@ __global__ void __launch_bounds__(256) adamw_k(float* __restrict__ params,
     }
 }
 
+static void adamw_launch(float* params, const float* grads, float* m, float* v,
+                         const AdamSeg* segs, int nseg, int64_t lo4, int64_t blk4, int64_t n4,
+                         int nblk, const AdamScalars* a, Shadows sh, const double* loss_total,
+                         cudaStream_t s, bool background) {
+    if (n4 <= 0 || nblk <= 0) return;
+    // persistent grid with the segment table in smem; or (background launches, beside the
+    // GEMMs) short blocks of 4 strides with no smem, so that they fit next to a GEMM CTA
+    // and a higher-priority stream's blocks get SMs as they retire
+    const int seg_smem = !background && nseg <= ADAM_MAX_SEGS;
+    const int64_t bx = background ? cdiv(n4, 256 * ADAM_U * 4)
+                                  : std::max<int64_t>(1, std::min<int64_t>(cdiv(n4, 256 * ADAM_U),
+                                                                           148 * 8 / nblk));
+    const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(nblk));
+    adamw_k<<<grid, 256, seg_smem ? sizeof(AdamSeg) * nseg : 0, s>>>(
+        params, grads, m, v, segs, nseg, seg_smem, lo4, blk4, n4, a, sh, loss_total);
+    count_launch();
+}
+
 void adamw(float* params, const float* grads, float* m, float* v, const AdamSeg* segs, int nseg,
            int64_t lo, int64_t hi, const AdamScalars* a, Shadows sh, const double* loss_total,
            cudaStream_t s, bool short_blocks) {
-    const int64_t lo4 = lo / 4, total4 = hi / 4;  // segment lengths are multiples of 4
-    if (total4 <= lo4) return;
-    // persistent grid, or (background launches) short blocks of 4 strides each, so that a
-    // higher-priority stream's blocks get SMs as these retire
-    const int blocks = static_cast<int>(
-        short_blocks ? cdiv(total4 - lo4, 256 * ADAM_U * 4)
-                     : std::min<int64_t>(cdiv(total4 - lo4, 256 * ADAM_U), 148 * 8));
-    adamw_k<<<blocks, 256, 0, s>>>(params, grads, m, v, segs, nseg, lo4, total4, a, sh,
-                                   loss_total);
-    count_launch();
+    // segment lengths are multiples of 4
+    adamw_launch(params, grads, m, v, segs, nseg, lo / 4, 0, hi / 4 - lo / 4, 1, a, sh, loss_total,
+                 s, short_blocks);
+}
+
+void adamw_strided(float* params, const float* grads, float* m, float* v, const AdamSeg* segs,
+                   int nseg, int64_t lo, int64_t blk, int64_t len, int nblk, const AdamScalars* a,
+                   Shadows sh, const double* loss_total, cudaStream_t s) {
+    adamw_launch(params, grads, m, v, segs, nseg, lo / 4, blk / 4, len / 4, nblk, a, sh,
+                 loss_total, s, true);
 }
 
 __global__ void __launch_bounds__(256) refresh_shadows_k(const float* __restrict__ params,

@@ -151,7 +151,12 @@ using spes_dev::AdamScalars;
 // compact elements [lo, hi) (multiples of 4)
 void adamw(float* params, const float* grads, float* m, float* v, const AdamSeg* segs, int nseg,
            int64_t lo, int64_t hi, const AdamScalars* a, Shadows sh, const double* loss_total,
-           cudaStream_t s, bool short_blocks = false);  // a: device memory (graph-replayable)
+           cudaStream_t s, bool short_blocks = false);
+// compact elements lo + b*blk + [0, len) for b < nblk (multiples of 4), as a background
+// launch (short blocks, no smem: fits beside a GEMM CTA)
+void adamw_strided(float* params, const float* grads, float* m, float* v, const AdamSeg* segs,
+                   int nseg, int64_t lo, int64_t blk, int64_t len, int nblk, const AdamScalars* a,
+                   Shadows sh, const double* loss_total, cudaStream_t s);  // a: device memory (graph-replayable)
 // Rewrite every bf16 copy from the fp32 parameters (after load / sync / merge).
 void refresh_shadows(const float* params, const AdamSeg* segs, int nseg, int64_t total,
                      Shadows sh, cudaStream_t s);
