@@ -200,6 +200,37 @@ spes_status spes_local_round_rows(spes_ctx* ctx, const int64_t* rows, int64_t B,
                                   const double* lr, const spes_adamw_cfg* opt, int32_t carry_state,
                                   spes_losses* per_step);
 
+/* ---- CommLedger (protocol.hpp:29-52) ----
+ * The reference's transport-agnostic byte accounting for a run of `rounds` SPES rounds
+ * over n_nodes, as its Server records it (protocol.cpp:56-175): every frame is its payload
+ * plus an 18-byte header; HELLO is counted under node -1 (the connection has no node yet),
+ * then ASSIGN, the GLOBAL_MODEL broadcasts of rounds 1..rounds+1, each node's LOCAL_UPDATE
+ * (shared blocks + owned experts; the whole model with diloco) and ROUND_DONE, and the BYE
+ * exchange at round rounds+1. The B200 nodes move these parameters over NCCL instead; this
+ * keeps the reference's accounting (and its metrics.csv bytes_up / bytes_down columns).
+ * Ownership: CSR map as spes_set_ownership, or NULL for param_partition (the reference's
+ * server assignment). Entries in (node, round) order; up to cap are written, *n_entries
+ * is the total; totals = {total_up, total_down, pushes, broadcasts}. */
+typedef struct {
+    int32_t node, round;
+    uint64_t up, down;
+} spes_ledger_entry;
+spes_status spes_comm_ledger(const spes_model_cfg* cfg, int32_t n_nodes,
+                             const int32_t* node_offsets, const int32_t* experts, int32_t rounds,
+                             int32_t diloco, spes_ledger_entry* entries, int32_t cap,
+                             int32_t* n_entries, uint64_t* totals);
+/* RoundMetrics (protocol.hpp:132-137) -> the text of an experiment's metrics.csv
+ * (experiment.cpp:376-385: same header, columns and number formatting). tokens_seen =
+ * tokens_per_round * round (nodes * H * batch * seq_len per round in the reference);
+ * wall_ms may be NULL (0.0). *len = the text's length; up to cap bytes are written. */
+typedef struct {
+    int32_t round;
+    double mean_total, mean_ce, mean_lb, mean_moe_z, mean_z, merge_displacement_sq;
+    uint64_t bytes_up, bytes_down;
+} spes_round_metrics;
+spes_status spes_metrics_csv(const spes_round_metrics* rows, int32_t n, int64_t tokens_per_round,
+                             const double* wall_ms, char* out, int64_t cap, int64_t* len);
+
 /* ---- upcycling ----
  * upcycle_from_dense (model.hpp:415-460): a dense model (experts_total == 1) -> an m-expert
  * model: embedding / norms / head copied, routers widened by replicating their column,

@@ -165,6 +165,17 @@ def ref():
         R.ref_read_checkpoint.argtypes = [_cfgp, C.c_char_p, _f32p, C.POINTER(C.c_uint64),
                                           C.c_char_p, C.c_int]
         R.ref_set_parallel.argtypes = [C.c_int]
+        R.ref_run_experiment.restype = C.c_int
+        R.ref_run_experiment.argtypes = [_cfgp, C.c_int32, C.c_int32, C.c_int32, C.c_int64,
+                                         C.c_int64, C.c_char_p, C.c_char_p, C.c_void_p, C.c_int32,
+                                         C.POINTER(C.c_int32), C.POINTER(C.c_int64)]
+        R.ref_run_inproc_ledger.restype = C.c_int
+        R.ref_run_inproc_ledger.argtypes = [_cfgp, C.c_int32, C.c_int32, C.c_int32, C.c_int64,
+                                            C.c_int64, C.c_int32, C.c_uint64, _i32p, _i32p,
+                                            np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS"),
+                                            np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS"),
+                                            C.c_int32, C.POINTER(C.c_int32),
+                                            np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")]
         _ref = R
     return _ref
 

@@ -482,3 +482,90 @@ int ref_batches(int64_t vocab, int64_t seq, int32_t sources, int64_t sequences, 
     return 0;
 }
 }  // extern "C"
+
+// ---- CommLedger of an in-process protocol run (protocol.hpp:29-52, protocol.cpp:56-175,
+// run_inproc :368-405), SURVEY §8(f) f3 -------------------------------------------------
+extern "C" int ref_run_inproc_ledger(const spes_model_cfg* c, int32_t N, int32_t rounds,
+                                     int32_t H, int64_t B, int64_t S, int32_t diloco,
+                                     uint64_t seed, int32_t* nodes_out, int32_t* rounds_out,
+                                     uint64_t* up_out, uint64_t* down_out, int32_t cap,
+                                     int32_t* n_out, uint64_t* totals) {
+    try {
+        SyncConfig sc;
+        sc.model = to_cfg(c);
+        sc.nodes = N;
+        sc.rounds = rounds;
+        sc.diloco = diloco != 0;
+        sc.config_hash = 7;
+        sc.merge.warmup_rounds = 0;
+        std::vector<float> flat(static_cast<size_t>(ref_param_count(c)));
+        ref_init_model(c, seed, 0.02, flat.data());
+        ModelParams init = from_flat(sc.model, flat.data());
+        Worker::Options wo;
+        wo.round.steps = H;
+        std::vector<int32_t> toks(static_cast<size_t>(B * (S + 1)));
+        for (size_t i = 0; i < toks.size(); ++i)
+            toks[i] = static_cast<int32_t>((i * 2654435761ull + seed) % static_cast<uint64_t>(c->vocab));
+        auto provider = [&](int) -> BatchProvider {
+            return [&]() { return batch_from(toks.data(), B, S); };
+        };
+        RunResult r = run_inproc(sc, init, wo, provider);
+        int32_t n = 0;
+        for (const auto& [key, e] : r.ledger.per_node_round) {
+            if (n < cap) {
+                nodes_out[n] = key.first;
+                rounds_out[n] = key.second;
+                up_out[n] = e.up;
+                down_out[n] = e.down;
+            }
+            ++n;
+        }
+        *n_out = n;
+        totals[0] = r.ledger.total_up;
+        totals[1] = r.ledger.total_down;
+        totals[2] = r.ledger.pushes;
+        totals[3] = r.ledger.broadcasts;
+        return 0;
+    } catch (...) {
+        return 1;
+    }
+}
+
+// ---- metrics.csv of run_experiment (experiment.cpp:270-420), SURVEY §8(f) f3 ----
+struct RefRoundRow {
+    int32_t round;
+    double mean_total, mean_ce, mean_lb, mean_moe_z, mean_z, merge_displacement_sq;
+    uint64_t bytes_up, bytes_down;
+};
+
+extern "C" int ref_run_experiment(const spes_model_cfg* c, int32_t nodes, int32_t H,
+                                  int32_t rounds, int64_t batch, int64_t seq_len,
+                                  const char* out_root, const char* name, RefRoundRow* rows,
+                                  int32_t cap, int32_t* n_out, int64_t* tokens_per_round) {
+    try {
+        ExperimentConfig ec;
+        ec.name = name;
+        ec.model = to_cfg(c);
+        ec.paradigm = Paradigm::Spes;
+        ec.nodes = nodes;
+        ec.local_steps = H;
+        ec.rounds = rounds;
+        ec.batch = batch;
+        ec.seq_len = seq_len;
+        ec.corpus_sequences = 64;
+        ec.lr.total_steps = static_cast<int64_t>(H) * rounds;
+        ExperimentResult r = run_experiment(ec, out_root);
+        int32_t n = 0;
+        for (const RoundMetrics& m : r.rounds) {
+            if (n < cap)
+                rows[n] = {m.round, m.mean_total, m.mean_ce, m.mean_lb, m.mean_moe_z, m.mean_z,
+                           m.merge_displacement_sq, m.bytes_up, m.bytes_down};
+            ++n;
+        }
+        *n_out = n;
+        *tokens_per_round = static_cast<int64_t>(nodes) * H * batch * seq_len;
+        return 0;
+    } catch (...) {
+        return 1;
+    }
+}

@@ -92,6 +92,11 @@ def lib():
         L.spes_upcycle_from_dense.argtypes = [C.POINTER(ModelCfg), f32p, C.c_int32, C.c_double,
                                               C.c_double, C.c_uint64, C.POINTER(ModelCfg), f32p]
         L.spes_outer_sync.argtypes = [vp, C.c_int32, C.c_double, C.c_double, C.POINTER(SyncStats)]
+        L.spes_metrics_csv.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p, C.c_char_p,
+                                       C.c_int64, C.POINTER(C.c_int64)]
+        L.spes_comm_ledger.argtypes = [C.POINTER(ModelCfg), C.c_int32, C.c_void_p, C.c_void_p,
+                                       C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
+                                       C.POINTER(C.c_int32), C.POINTER(C.c_uint64)]
         u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
         L.spes_model_payload_bytes.restype = i64
         L.spes_model_payload_bytes.argtypes = [C.POINTER(ModelCfg)]
@@ -225,6 +230,69 @@ def decode_model(cfg, payload):
     out = np.zeros(param_count(cfg), np.float32)
     _check(lib().spes_decode_model_host(C.byref(cfg), payload, payload.size, f32(out)))
     return out
+
+
+# ---- CommLedger (protocol.hpp:29-52): the reference protocol's byte accounting ----
+
+_LEDGER_DT = np.dtype([("node", np.int32), ("round", np.int32), ("up", np.uint64),
+                       ("down", np.uint64)])
+
+
+def comm_ledger(cfg, n_nodes, rounds, diloco=False, ownership=None):
+    """CommLedger of a SPES run under the reference's protocol (spes_comm_ledger).
+
+    Returns (entries, totals): entries a structured array (node, round, up, down) in
+    (node, round) order, node -1 holding the HELLOs; totals a dict with total_up,
+    total_down, pushes and broadcasts. ownership: list of per-node expert lists, or None
+    for param_partition."""
+    offs = exps = None
+    if ownership is not None:
+        offs = np.zeros(len(ownership) + 1, np.int32)
+        for i, o in enumerate(ownership):
+            offs[i + 1] = offs[i] + len(o)
+        exps = np.ascontiguousarray(np.concatenate([np.asarray(o, np.int32) for o in ownership]),
+                                    np.int32)
+    n = C.c_int32(0)
+    tot = (C.c_uint64 * 4)()
+    cap = n_nodes * (rounds + 2) + 1
+    ent = np.zeros(cap, _LEDGER_DT)
+    _check(lib().spes_comm_ledger(C.byref(cfg), n_nodes,
+                                  None if offs is None else offs.ctypes.data_as(C.c_void_p),
+                                  None if exps is None else exps.ctypes.data_as(C.c_void_p),
+                                  rounds, 1 if diloco else 0, ent.ctypes.data_as(C.c_void_p), cap,
+                                  C.byref(n), tot))
+    return ent[:n.value], dict(total_up=tot[0], total_down=tot[1], pushes=tot[2],
+                               broadcasts=tot[3])
+
+
+class RoundMetrics(C.Structure):
+    """spes_round_metrics == RoundMetrics (protocol.hpp:132-137)."""
+    _fields_ = [("round", C.c_int32), ("mean_total", C.c_double), ("mean_ce", C.c_double),
+                ("mean_lb", C.c_double), ("mean_moe_z", C.c_double), ("mean_z", C.c_double),
+                ("merge_displacement_sq", C.c_double), ("bytes_up", C.c_uint64),
+                ("bytes_down", C.c_uint64)]
+
+
+def metrics_csv(rows, tokens_per_round, wall_ms=None):
+    """metrics.csv text of an experiment (experiment.cpp:376-385) from RoundMetrics rows."""
+    arr = (RoundMetrics * max(1, len(rows)))(*rows)
+    wall = None
+    if wall_ms is not None:
+        wall = np.ascontiguousarray(wall_ms, np.float64)
+    n = C.c_int64(0)
+    L = lib()
+    wp = None if wall is None else wall.ctypes.data_as(C.c_void_p)
+    _check(L.spes_metrics_csv(arr, len(rows), tokens_per_round, wp, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(L.spes_metrics_csv(arr, len(rows), tokens_per_round, wp, buf, n.value, C.byref(n)))
+    return buf.raw[:n.value].decode()
+
+
+def round_bytes(entries, rnd):
+    """RoundMetrics.bytes_up / bytes_down of round rnd (assemble_run_result,
+    protocol.cpp:357-362): the ledger entries of that round summed over nodes."""
+    sel = entries[entries["round"] == rnd]
+    return int(sel["up"].sum()), int(sel["down"].sum())
 
 
 # ---- synthetic corpus / batch streams (proj/src/corpus.cpp), bit-identical ----

@@ -1357,6 +1357,72 @@ spes_status spes_local_round(spes_ctx* c, const int32_t* tokens, int64_t B, int6
     });
 }
 
+// ---- CommLedger (protocol.hpp:29-52) ----
+extern "C++" {
+namespace spes_ledger {
+struct Entry {
+    int32_t node, round;
+    uint64_t up, down;
+};
+std::vector<Entry> expected(int64_t V, int64_t d, int64_t f, int L, int M, int nodes,
+                            const std::vector<std::vector<int>>& owned, int rounds, bool diloco,
+                            uint64_t totals[4]);
+struct RoundRow {
+    int32_t round;
+    double mean_total, mean_ce, mean_lb, mean_moe_z, mean_z, merge_displacement_sq;
+    uint64_t bytes_up, bytes_down;
+};
+std::string metrics_csv(const RoundRow* rows, int n, int64_t tokens_per_round,
+                        const double* wall_ms, int n_wall);
+}
+}
+
+spes_status spes_metrics_csv(const spes_round_metrics* rows, int32_t n, int64_t tokens_per_round,
+                             const double* wall_ms, char* out, int64_t cap, int64_t* len) {
+    return guard([&] {
+        if (n < 0) throw std::invalid_argument("metrics: negative row count");
+        std::vector<spes_ledger::RoundRow> r(static_cast<size_t>(n));
+        for (int i = 0; i < n; ++i)
+            r[i] = {rows[i].round, rows[i].mean_total, rows[i].mean_ce, rows[i].mean_lb,
+                    rows[i].mean_moe_z, rows[i].mean_z, rows[i].merge_displacement_sq,
+                    rows[i].bytes_up, rows[i].bytes_down};
+        const std::string t = spes_ledger::metrics_csv(r.data(), n, tokens_per_round, wall_ms,
+                                                       wall_ms ? n : 0);
+        *len = static_cast<int64_t>(t.size());
+        if (out && cap > 0) std::memcpy(out, t.data(), std::min<size_t>(t.size(), static_cast<size_t>(cap)));
+    });
+}
+
+spes_status spes_comm_ledger(const spes_model_cfg* cfg, int32_t n_nodes,
+                             const int32_t* node_offsets, const int32_t* experts, int32_t rounds,
+                             int32_t diloco, spes_ledger_entry* entries, int32_t cap,
+                             int32_t* n_entries, uint64_t* totals) {
+    return guard([&] {  // host bookkeeping: the model's shape only, no tcgen05 tiling limits
+        if (cfg->vocab < 1 || cfg->hidden < 1 || cfg->intermediate < 1 || cfg->layers < 1 ||
+            cfg->experts_total < 1)
+            throw std::invalid_argument("config: all dimensions must be positive");
+        const int M = cfg->experts_total;
+        if (n_nodes < 1 || n_nodes > M)
+            throw std::invalid_argument("partition: need 1 <= N <= M (no empty nodes)");
+        std::vector<std::vector<int>> owned(static_cast<size_t>(n_nodes));
+        if (node_offsets) {
+            for (int n = 0; n < n_nodes; ++n)
+                for (int q = node_offsets[n]; q < node_offsets[n + 1]; ++q) owned[n].push_back(experts[q]);
+        } else {  // param_partition (model.hpp:466-477)
+            const int base = M / n_nodes, extra = M % n_nodes;
+            int next = 0;
+            for (int n = 0; n < n_nodes; ++n)
+                for (int j = 0; j < base + (n < extra ? 1 : 0); ++j) owned[n].push_back(next++);
+        }
+        const auto e = spes_ledger::expected(cfg->vocab, cfg->hidden, cfg->intermediate,
+                                             cfg->layers, M, n_nodes, owned, rounds, diloco != 0,
+                                             totals);
+        for (size_t i = 0; i < e.size() && static_cast<int32_t>(i) < cap; ++i)
+            entries[i] = spes_ledger_entry{e[i].node, e[i].round, e[i].up, e[i].down};
+        *n_entries = static_cast<int32_t>(e.size());
+    });
+}
+
 // ---- device corpus and batch streams (corpus.cpp) ----
 extern "C++" {
 namespace spes_corpus {
