@@ -278,6 +278,10 @@ spes_status spes_read_grads(spes_ctx* ctx, float* host, int64_t n);
  * logic_error). 0 (default): gradients are materialized and one standalone optimizer
  * pass runs after the backward. Both give identical bits. */
 spes_status spes_set_fused_optimizer(spes_ctx* ctx, int32_t on);
+/* Stream layout of the local step. 1 (default): off-critical-path work (embedding-gradient
+ * bucketing, loss scalars, the router's scalar backward, the owned experts' AdamW) runs on
+ * a low-priority second stream beside the GEMMs; 0: one stream. Identical bits either way. */
+spes_status spes_set_stream_overlap(spes_ctx* ctx, int32_t on);
 /* Live per-kernel-family timing: CUDA events bracket every launch family on the
  * context stream while enabled; totals accumulate until spes_profile_reset. */
 spes_status spes_profile(spes_ctx* ctx, int32_t enable);

@@ -75,6 +75,7 @@ def lib():
         L.spes_read_params.argtypes = [vp, f32p, i64]
         L.spes_read_grads.argtypes = [vp, f32p, i64]
         L.spes_set_fused_optimizer.argtypes = [vp, C.c_int32]
+        L.spes_set_stream_overlap.argtypes = [vp, C.c_int32]
         L.spes_outer_begin.argtypes = [vp]
         i64p = C.POINTER(C.c_int64)
         L.spes_gen_corpus.argtypes = [i64, i64, C.c_int32, i64, C.c_uint64, C.c_double,
@@ -401,9 +402,14 @@ class Node:
         return out
 
     def set_fused_optimizer(self, on):
-        """Owned experts' AdamW inside the dW GEMM epilogue (default) or as a separate pass
+        """Owned experts' AdamW inside the dW GEMM epilogue, or (default) as a separate pass
         with materialized gradients (needed by read_grads); identical bits either way."""
         _check(lib().spes_set_fused_optimizer(self._ctx, 1 if on else 0))
+
+    def set_stream_overlap(self, on):
+        """Second low-priority stream for the step's off-critical-path work (default on);
+        identical bits either way."""
+        _check(lib().spes_set_stream_overlap(self._ctx, 1 if on else 0))
 
     def corpus_load(self, tokens):
         """Upload a corpus [sequences, S+1] to HBM once (token ids validated here)."""

@@ -1909,6 +1909,14 @@ spes_status spes_set_fused_optimizer(spes_ctx* c, int32_t on) {
     });
 }
 
+spes_status spes_set_stream_overlap(spes_ctx* c, int32_t on) {
+    return guard([&] {
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        c->overlap_opt = on != 0;
+        drop_graph(c);  // the captured step holds the other stream layout
+    });
+}
+
 spes_status spes_read_grads(spes_ctx* c, float* host, int64_t n) {
     return guard([&] {
         if (n != c->lay.total()) throw std::invalid_argument("read_grads: size mismatch");

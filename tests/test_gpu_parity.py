@@ -287,6 +287,27 @@ def test_local_round_matches_oracle_losses(gpu):
     node.close()
 
 
+@pytest.mark.parametrize("shape,owned,B,S", [(CFG1, [2, 3, 4, 5], 2, 64),
+                                             (CFG2, list(range(16)), 1, 512)])
+def test_stream_overlap_identical_bits(gpu, shape, owned, B, S):
+    """The two-stream step (side-stream bucketing, losses, router scalar backward and the
+    experts' AdamW) gives the same bits as the one-stream step, eager and graph-replayed."""
+    cfg = model_cfg(**shape)
+    params = oracle.random_params(cfg, 21)
+    toks = oracle.random_tokens(cfg, B, S, 22, H=4)
+    out = []
+    for overlap in (True, False):
+        node = spes.Node(cfg)
+        node.set_ownership([owned])
+        node.load_params(params)
+        node.set_stream_overlap(overlap)
+        losses = node.local_round(toks, adamw_cfg(lr=1e-3))  # step 2 captures, 3-4 replay
+        out.append((losses, node.read_params()))
+        node.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert bitexact(out[0][1], out[1][1])
+
+
 # ---------------------------------------------------------------- merge warm-up
 
 def test_merge_bitexact_vs_oracle(gpu):
