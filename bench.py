@@ -226,17 +226,18 @@ def ncu_traffic():
 
 # ------------------------------------------------------------------ CPU reference
 
-def cpu_reference_sample(cfg_name, N, reps=1):
+def cpu_reference_sample(cfg_name, N, reps=1, parallel=True):
     """The reference's own CPU path (oracle/_ref = /root/reference compiled from its sources):
     one local_round step (build_loss + backward + MaskedAdamW) at B=1, S=256 of the config's
     shapes with node 0's ownership, plus Server::aggregate of the full model amortised over H.
+    parallel=False runs the reference's kernels single-threaded (its set_parallel(false)).
     Returns (tokens/s, seconds per sample, threads, description)."""
     import ctypes as C
     import oracle
     from paper_2602_11543_b200.abi import adamw_cfg
     cfg, owned, H, B, S, merge, repl, desc = workload(cfg_name, N)
     R = oracle.ref()
-    R.ref_set_parallel(1)
+    R.ref_set_parallel(1 if parallel else 0)
     P = oracle.param_count(cfg)
     rng = np.random.default_rng(1)
     params = (rng.standard_normal(P, dtype=np.float32) * np.float32(0.02))
@@ -260,7 +261,8 @@ def cpu_reference_sample(cfg_name, N, reps=1):
     R.ref_aggregate_partition(C.byref(cfg), 1, nodes, params, out)
     t_sync = time.perf_counter() - t0
     per_step = best + t_sync / H
-    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)) if parallel else 1
+    R.ref_set_parallel(1)
     sample = (f"{cfg_name} shapes, reference local_round H=1 at B=1 S=256 (256 tokens, full "
               f"parameter size, node 0 owns {len(owned[0])} experts) + Server::aggregate/{H}; "
               f"OpenMP threads={threads}")
@@ -411,6 +413,7 @@ def our_arm(args):
         log("HBM-bound kernels (GB/s, algorithmic bytes): " + json.dumps(hb))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
+        "value_per_gpu": value / N,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": desc, "name": args.config, "d": cfg.hidden, "f": cfg.intermediate,
@@ -446,6 +449,9 @@ def our_arm(args):
             v, sec, threads, sample = cpu_reference_sample(args.config, N)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads,
                                     "kind": "reference", "sample": sample}
+            # also the reference single-threaded (OpenMP off), same sample
+            v1, _, _, _ = cpu_reference_sample(args.config, N, parallel=False)
+            line["cpu_baseline"]["single_thread"] = {"value": v1, "unit": UNIT, "cores": 1}
         except Exception as e:  # the reference lib is test infra; report, don't fail
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {e}"}
@@ -457,6 +463,8 @@ def our_arm(args):
 
 def main():
     os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+    # NCCL's own log lines ("NCCL version ...") go to stderr: stdout carries only the JSON line
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     args = parse()
     if args.impl == "reference":
         return reference_arm(args)

@@ -237,6 +237,15 @@ struct spes_ctx {
     int32_t* h_tokens = nullptr;
     int64_t h_tokens_cap = 0;
     double* h_losses = nullptr;
+    // pinned staging of the merge's small host<->device transfers (async, no bounce copies)
+    struct MergePin {
+        double sim[64 * 64];
+        int32_t peers[64 * 64];
+        double coef[64];
+        int64_t eo[64], vo[64];
+        double disp[148 * 8];
+    };
+    MergePin* h_merge = nullptr;
 
     // sync / merge scratch
     DevMem scratch;
@@ -1095,6 +1104,7 @@ void spes_destroy(spes_ctx* c) {
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->h_tokens) cudaFreeHost(c->h_tokens);
     if (c->h_losses) cudaFreeHost(c->h_losses);
+    if (c->h_merge) cudaFreeHost(c->h_merge);
     c->act.release();
     c->scratch.release();
     c->persistent.release();
@@ -1641,6 +1651,10 @@ spes_status spes_sync(spes_ctx* c, spes_sync_stats* stats) {
         const Layout& L = c->lay;
         const int N = c->n_nodes, me = c->node;
         cudaStream_t st = c->stream;
+        if (N == 1) {  // one node: the owner-set means are the node's own values
+            if (stats) *stats = spes_sync_stats{};
+            return;
+        }
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
@@ -1752,9 +1766,10 @@ void layer_sims(spes_ctx* c, int l, int source) {
         c->peers_dev = c->scratch.alloc<int32_t>(M * M);
         c->layer_expert_offs = c->scratch.alloc<int64_t>(2 * M);
     }
-    std::vector<int64_t> vo(M);
+    if (!c->h_merge) ck(cudaMallocHost(&c->h_merge, sizeof(spes_ctx::MergePin)), "pinned merge");
+    int64_t* vo = c->h_merge->vo;
     for (int j = 0; j < M; ++j) vo[j] = L.off_expert(l, j) + (source == 1 ? df : 0);
-    ck(cudaMemcpyAsync(c->layer_expert_offs + M, vo.data(), 8 * M, cudaMemcpyHostToDevice, c->stream), "vo");
+    ck(cudaMemcpyAsync(c->layer_expert_offs + M, vo, 8 * M, cudaMemcpyHostToDevice, c->stream), "vo");
     spes_k::gram_partials(c->params, c->layer_expert_offs + M, M, df, df, source == 2 ? 1 : 0,
                           c->gram_partial, c->gram_chunks, c->stream);
     spes_k::gram_finish(c->gram_partial, M, c->gram_chunks, c->sim, c->stream);
@@ -1850,9 +1865,15 @@ spes_status spes_merge(spes_ctx* c, const spes_merge_sched* sched, int32_t round
         if (K < 1) throw std::invalid_argument("select_peers: need K >= 1");
         std::vector<double> sim(static_cast<size_t>(M) * M);
         for (int l = 0; l < L.L; ++l) {
-            layer_sims(c, l, sched->source);
-            ck(cudaMemcpyAsync(sim.data(), c->sim, 8 * M * M, cudaMemcpyDeviceToHost, c->stream), "D2H sim");
+            {
+                Prof prof(c, "merge_similarity");
+                layer_sims(c, l, sched->source);
+                ck(cudaMemcpyAsync(c->h_merge->sim, c->sim, 8 * M * M, cudaMemcpyDeviceToHost,
+                                   c->stream),
+                   "D2H sim");
+            }
             ck(cudaStreamSynchronize(c->stream), "sync");
+            std::memcpy(sim.data(), c->h_merge->sim, 8 * M * M);
             std::vector<int32_t> peers(static_cast<size_t>(M) * K);
             std::vector<double> coef(M);
             for (int j = 0; j < M; ++j) {
@@ -1866,19 +1887,29 @@ spes_status spes_merge(spes_ctx* c, const spes_merge_sched* sched, int32_t round
                 for (int q = 0; q < K; ++q) peers[static_cast<size_t>(j) * K + q] = p[q];
                 coef[j] = alpha / static_cast<double>(p.size());
             }
-            std::vector<int64_t> eo(M);
-            for (int j = 0; j < M; ++j) eo[j] = L.off_expert(l, j);
-            ck(cudaMemcpyAsync(c->peers_dev, peers.data(), 4 * M * K, cudaMemcpyHostToDevice, c->stream), "peers");
-            ck(cudaMemcpyAsync(c->coef, coef.data(), 8 * M, cudaMemcpyHostToDevice, c->stream), "coef");
-            ck(cudaMemcpyAsync(c->layer_expert_offs, eo.data(), 8 * M, cudaMemcpyHostToDevice, c->stream), "eo");
+            auto* hp = c->h_merge;
+            for (int j = 0; j < M; ++j) hp->eo[j] = L.off_expert(l, j);
+            std::memcpy(hp->peers, peers.data(), 4 * M * K);
+            std::memcpy(hp->coef, coef.data(), 8 * M);
             const int nblocks = 148 * 4;
-            spes_k::merge_apply(c->params, c->layer_expert_offs, M, L.per_expert(), c->peers_dev, K,
-                                c->coef, c->disp_partial, nblocks, c->stream);
-            std::vector<double> dp(nblocks);
-            ck(cudaMemcpyAsync(dp.data(), c->disp_partial, 8 * nblocks, cudaMemcpyDeviceToHost, c->stream), "disp");
+            {
+                Prof prof(c, "merge_apply");
+                ck(cudaMemcpyAsync(c->peers_dev, hp->peers, 4 * M * K, cudaMemcpyHostToDevice,
+                                   c->stream),
+                   "peers");
+                ck(cudaMemcpyAsync(c->coef, hp->coef, 8 * M, cudaMemcpyHostToDevice, c->stream), "coef");
+                ck(cudaMemcpyAsync(c->layer_expert_offs, hp->eo, 8 * M, cudaMemcpyHostToDevice,
+                                   c->stream),
+                   "eo");
+                spes_k::merge_apply(c->params, c->layer_expert_offs, M, L.per_expert(), c->peers_dev,
+                                    K, c->coef, c->disp_partial, nblocks, c->stream);
+                ck(cudaMemcpyAsync(hp->disp, c->disp_partial, 8 * nblocks, cudaMemcpyDeviceToHost,
+                                   c->stream),
+                   "disp");
+            }
             ck(cudaStreamSynchronize(c->stream), "sync");
             double disp = 0.0;
-            for (double x : dp) disp += x;
+            for (int i = 0; i < nblocks; ++i) disp += hp->disp[i];
             if (events) {
                 events[l].layer = l;
                 events[l].peers_k = K;
@@ -1888,7 +1919,10 @@ spes_status spes_merge(spes_ctx* c, const spes_merge_sched* sched, int32_t round
             if (peers_out)
                 std::memcpy(peers_out + static_cast<size_t>(l) * M * K, peers.data(), 4 * M * K);
         }
-        refresh_shadows_all(c);
+        {
+            Prof prof(c, "merge_refresh_shadows");
+            refresh_shadows_all(c);
+        }
         ck(cudaStreamSynchronize(c->stream), "sync");
         if (n_events) *n_events = L.L;
     });

@@ -11,6 +11,8 @@
 
 #include <algorithm>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "glibc_expf.h"
 #include "kernels.h"
@@ -1282,123 +1284,254 @@ void owner_mean(const float* const* srcs, int n_src, int64_t n, float* out, cuda
 // ============================ merge: Gram + apply ============================
 // Projection vector of expert j: D1 floats at vec_offs[j] (+ a second D1 run at
 // +gap when two_parts: Concat source). Partial fp64 dot products per chunk.
-constexpr int GRAM_SUB = 128;
+// Gram partials: block = a contiguous element range; per tile of SUB elements the M
+// vectors are staged in smem by float4 loads, then work items (pair, part) accumulate
+// their share in fp64, several items per thread (independent chains). A block's partial of
+// a pair = its parts summed in part order. Fixed grouping -> deterministic; vs the
+// reference's sequential sum ~1e-12 relative (select_peers re-checks near-ties exactly).
+constexpr int GRAM_ITEMS = 9;  // work items per thread (2080 pairs at M = 64)
+__host__ __device__ inline int gram_sub(int M) { return 16384 / M; }  // tile: <= 64 KB smem
+__host__ __device__ inline int gram_parts(int npairs) {
+    int P = 1;
+    while (npairs * P * 2 <= 768 && P < 16) P *= 2;
+    return P;
+}
+
 __global__ void __launch_bounds__(256) gram_partial_k(const float* __restrict__ params,
                                                       const int64_t* __restrict__ vec_offs, int M,
                                                       int64_t D1, int64_t gap, int two_parts,
                                                       double* __restrict__ partial, int nchunks) {
-    extern __shared__ float sv[];  // [M][GRAM_SUB]
+    extern __shared__ __align__(16) float sv[];  // [M][sub], then [npairs * P] doubles
+    const int sub = gram_sub(M), q4 = sub / 4;
+    const int npairs = M * (M + 1) / 2, P = gram_parts(npairs), seg = sub / P;
+    double* sitem = reinterpret_cast<double*>(sv + static_cast<int64_t>(M) * sub);
     const int64_t D = two_parts ? 2 * D1 : D1;
-    const int npairs = M * (M + 1) / 2;
-    const int64_t per = ((D + nchunks - 1) / nchunks + GRAM_SUB - 1) / GRAM_SUB * GRAM_SUB;
+    const int64_t per = ((D + nchunks - 1) / nchunks + sub - 1) / sub * sub;
     const int64_t e0 = static_cast<int64_t>(blockIdx.x) * per, e1 = min(D, e0 + per);
-    constexpr int PPT = 16;  // pairs per thread (M <= 64 -> 2080 pairs / 256 threads <= 9)
-    double acc[PPT];
-    int pa[PPT], pb[PPT];
+    const int nitems = npairs * P;
+    double acc[GRAM_ITEMS];
+    int pa[GRAM_ITEMS], pb[GRAM_ITEMS], pp[GRAM_ITEMS];
 #pragma unroll
-    for (int u = 0; u < PPT; ++u) {
+    for (int u = 0; u < GRAM_ITEMS; ++u) {
         acc[u] = 0.0;
-        const int pidx = threadIdx.x + u * 256;
+        const int item = threadIdx.x + u * 256;
+        const int pidx = item / P;
         int a = 0, rem = pidx;
-        if (pidx < npairs)
+        if (item < nitems)
             while (rem >= M - a) {
                 rem -= M - a;
                 ++a;
             }
         pa[u] = a;
         pb[u] = a + rem;
+        pp[u] = item % P;
     }
-    for (int64_t b = e0; b < e1; b += GRAM_SUB) {
+    for (int64_t b = e0; b < e1; b += sub) {
         __syncthreads();
-        for (int i = threadIdx.x; i < M * GRAM_SUB; i += blockDim.x) {
-            const int j = i / GRAM_SUB;
-            const int64_t e = b + (i % GRAM_SUB);
-            float v = 0.f;
+        for (int i = threadIdx.x; i < M * q4; i += blockDim.x) {
+            const int j = i / q4;
+            const int64_t e = b + 4 * (i % q4);  // D1 and every bound are multiples of 4
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
             if (e < e1) {
                 const int64_t src = (two_parts && e >= D1) ? vec_offs[j] + gap + (e - D1) : vec_offs[j] + e;
-                v = params[src];
+                v = __ldg(reinterpret_cast<const float4*>(params + src));
             }
-            sv[i] = v;
+            reinterpret_cast<float4*>(sv + static_cast<int64_t>(j) * sub)[i % q4] = v;
         }
         __syncthreads();
 #pragma unroll
-        for (int u = 0; u < PPT; ++u) {
-            const int pidx = threadIdx.x + u * 256;
-            if (pidx < npairs) {
-                const float* va = sv + pa[u] * GRAM_SUB;
-                const float* vb = sv + pb[u] * GRAM_SUB;
-                double s = acc[u];
-                for (int i = 0; i < GRAM_SUB; ++i) s += static_cast<double>(va[i]) * vb[i];
-                acc[u] = s;
+        for (int u = 0; u < GRAM_ITEMS; ++u) {
+            if (threadIdx.x + u * 256 < nitems) {
+                const float* va = sv + pa[u] * sub + pp[u] * seg;
+                const float* vb = sv + pb[u] * sub + pp[u] * seg;
+                double s2 = acc[u];
+                for (int i = 0; i < seg; ++i) s2 += static_cast<double>(va[i]) * vb[i];
+                acc[u] = s2;
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < GRAM_ITEMS; ++u)
+        if (threadIdx.x + u * 256 < nitems) sitem[threadIdx.x + u * 256] = acc[u];
+    __syncthreads();
+    for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+        double t = 0.0;
+        for (int q = 0; q < P; ++q) t += sitem[p * P + q];
+        partial[static_cast<int64_t>(blockIdx.x) * npairs + p] = t;
+    }
+}
+
+// M <= 16 (rows padded to 16 with zeros): the 16 x 16 Gram as ten upper-triangle 4 x 4
+// register tiles, warp w owning tiles w and w + 8; lane l takes elements l, l+32, ... of each
+// staged tile (conflict-free LDS: all lanes on the same rows), 8 loads feed 16 fp64 FMAs;
+// the lanes' sums meet in a fixed butterfly at the end. Deterministic.
+constexpr int GRAM_SMALL_SUB = 1024;
+__device__ __forceinline__ int gram_pair_index(int M, int a, int b) {  // a <= b
+    int idx = 0;
+    for (int i = 0; i < a; ++i) idx += M - i;
+    return idx + (b - a);
+}
+__global__ void __launch_bounds__(256) gram_small_k(const float* __restrict__ params,
+                                                    const int64_t* __restrict__ vec_offs, int M,
+                                                    int64_t D1, int64_t gap, int two_parts,
+                                                    double* __restrict__ partial, int nchunks) {
+    extern __shared__ __align__(16) float sv[];  // [16][GRAM_SMALL_SUB]
+    constexpr int SUB = GRAM_SMALL_SUB, Q4 = SUB / 4;
+    const int npairs = M * (M + 1) / 2;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t D = two_parts ? 2 * D1 : D1;
+    const int64_t per = ((D + nchunks - 1) / nchunks + SUB - 1) / SUB * SUB;
+    const int64_t e0 = static_cast<int64_t>(blockIdx.x) * per, e1 = min(D, e0 + per);
+    int bi[2] = {0, 0}, bj[2] = {0, 0}, nt = 0;
+    for (int k = 0; k < 2; ++k) {
+        int t = warp + 8 * k;
+        if (t >= 10) break;
+        int r = 0;
+        while (t >= 4 - r) {
+            t -= 4 - r;
+            ++r;
+        }
+        bi[nt] = r;
+        bj[nt] = r + t;
+        ++nt;
+    }
+    double acc[2][4][4];
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[k][r][c] = 0.0;
+    for (int64_t b = e0; b < e1; b += SUB) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < 16 * Q4; i += blockDim.x) {
+            const int j = i / Q4;
+            const int64_t e = b + 4 * (i % Q4);
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (j < M && e < e1) {
+                const int64_t src = (two_parts && e >= D1) ? vec_offs[j] + gap + (e - D1) : vec_offs[j] + e;
+                v = __ldg(reinterpret_cast<const float4*>(params + src));
+            }
+            reinterpret_cast<float4*>(sv + j * SUB)[i % Q4] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            if (k >= nt) break;
+            const float* ra = sv + 4 * bi[k] * SUB;
+            const float* rb = sv + 4 * bj[k] * SUB;
+            for (int i = lane; i < SUB; i += 32) {
+                float xa[4], xb[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    xa[r] = ra[r * SUB + i];
+                    xb[r] = rb[r * SUB + i];
+                }
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        acc[k][r][c] += static_cast<double>(xa[r]) * static_cast<double>(xb[c]);
             }
         }
     }
 #pragma unroll
-    for (int u = 0; u < PPT; ++u) {
-        const int pidx = threadIdx.x + u * 256;
-        if (pidx < npairs) partial[static_cast<int64_t>(blockIdx.x) * npairs + pidx] = acc[u];
+    for (int k = 0; k < 2; ++k) {
+        if (k >= nt) break;
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const double t = warp_sum_d(acc[k][r][c]);
+                const int a = 4 * bi[k] + r, bb = 4 * bj[k] + c;
+                if (lane == 0 && a <= bb && bb < M)
+                    partial[static_cast<int64_t>(blockIdx.x) * npairs + gram_pair_index(M, a, bb)] = t;
+            }
     }
 }
 
 void gram_partials(const float* params, const int64_t* vec_offs, int M, int64_t D1, int64_t gap,
                    int two_parts, double* partial, int nchunks, cudaStream_t s) {
-    const size_t smem = sizeof(float) * M * GRAM_SUB;
+    const int npairs = M * (M + 1) / 2;
+    if (M <= 16) {
+        const size_t smem = sizeof(float) * 16 * GRAM_SMALL_SUB;
+        cudaFuncSetAttribute(gram_small_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        gram_small_k<<<nchunks, 256, smem, s>>>(params, vec_offs, M, D1, gap, two_parts, partial,
+                                               nchunks);
+        count_launch();
+        return;
+    }
+    const size_t smem = sizeof(float) * M * gram_sub(M) + sizeof(double) * npairs * gram_parts(npairs);
     cudaFuncSetAttribute(gram_partial_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     gram_partial_k<<<nchunks, 256, smem, s>>>(params, vec_offs, M, D1, gap, two_parts, partial,
                                              nchunks);
     count_launch();
 }
 
-// sim[a][b] = dot/(norm_a*norm_b) (merging.hpp:55-82); zero norm -> 0
+// sim[a][b] = dot/(norm_a*norm_b) (merging.hpp:55-82); zero norm -> 0. One warp per pair:
+// the block partials of the pair and of both diagonals, lane-strided then a butterfly
+// (fixed order, identical bits on every lane).
 __global__ void gram_finish_k(const double* __restrict__ partial, int M, int nchunks,
                               double* __restrict__ sim) {
-    __shared__ double g[64 * 65 / 2 + 64];
     const int npairs = M * (M + 1) / 2;
-    for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
-        double s = 0.0;
-        for (int c = 0; c < nchunks; ++c) s += partial[static_cast<int64_t>(c) * npairs + p];
-        g[p] = s;
+    const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (p >= npairs) return;
+    int a = 0, rem = p;
+    while (rem >= M - a) {
+        rem -= M - a;
+        ++a;
     }
-    __syncthreads();
-    for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
-        int a = 0, rem = p;
-        while (rem >= M - a) {
-            rem -= M - a;
-            ++a;
-        }
-        const int b = a + rem;
-        auto diag = [&](int j) {
-            int idx = 0;
-            for (int i = 0; i < j; ++i) idx += M - i;
-            return g[idx];
-        };
-        const double na = sqrt(diag(a)), nb = sqrt(diag(b));
+    const int b = a + rem;
+    auto diag_idx = [&](int j) {
+        int idx = 0;
+        for (int i = 0; i < j; ++i) idx += M - i;
+        return idx;
+    };
+    const int da = diag_idx(a), db = diag_idx(b);
+    double sp = 0.0, sa = 0.0, sb = 0.0;
+    for (int c = lane; c < nchunks; c += 32) {
+        const double* row = partial + static_cast<int64_t>(c) * npairs;
+        sp += row[p];
+        sa += row[da];
+        sb += row[db];
+    }
+    sp = warp_sum_d(sp);
+    sa = warp_sum_d(sa);
+    sb = warp_sum_d(sb);
+    if (lane == 0) {
+        const double na = sqrt(sa), nb = sqrt(sb);
         double v = 0.0;
-        if (na > 0.0 && nb > 0.0) v = g[p] / (na * nb);
+        if (na > 0.0 && nb > 0.0) v = sp / (na * nb);
         sim[a * M + b] = v;
         sim[b * M + a] = v;
     }
 }
 
 void gram_finish(const double* partial, int M, int nchunks, double* sim, cudaStream_t s) {
-    gram_finish_k<<<1, 256, 0, s>>>(partial, M, nchunks, sim);
+    const int npairs = M * (M + 1) / 2;
+    gram_finish_k<<<static_cast<unsigned>((npairs + 7) / 8), 256, 0, s>>>(partial, M, nchunks, sim);
     count_launch();
 }
 
-// In place, simultaneous: thread i reads element i of every expert before writing any
-// (merging.hpp:106-135: phi_j <- float(phi_j + alpha/|Q|*sum_p (phi_p - phi_j)) in fp64).
-template <int MAXM>
+// merge_experts (merging.hpp:97-136): w_j += coef_j * sum_q (w_peer_q - w_j), all experts
+// from the same pre-merge snapshot (element i of every expert staged in smem), in fp64.
+// VEC elements per thread (float4 for M <= 16).
+template <int VEC>
 __global__ void __launch_bounds__(256) merge_apply_k(float* __restrict__ params,
                                                      const int64_t* __restrict__ expert_offs,
                                                      int M, int64_t per,
                                                      const int32_t* __restrict__ peers, int K,
                                                      const double* __restrict__ coef,
                                                      double* __restrict__ disp_partial) {
+    using V = typename std::conditional<VEC == 4, float4, float>::type;
     __shared__ int32_t sp[64 * 64];
     __shared__ double sc[64];
     __shared__ int64_t so[64];
     __shared__ double red[256];
-    extern __shared__ float snap[];  // [M][256]: element i of every expert, per thread
+    extern __shared__ __align__(16) unsigned char snap_raw[];
+    V* snap = reinterpret_cast<V*>(snap_raw);  // [M][256]
     for (int i = threadIdx.x; i < M * K; i += blockDim.x) sp[i] = peers[i];
     for (int i = threadIdx.x; i < M; i += blockDim.x) {
         sc[i] = coef[i];
@@ -1407,35 +1540,52 @@ __global__ void __launch_bounds__(256) merge_apply_k(float* __restrict__ params,
     __syncthreads();
     double disp = 0.0;
     const int tid = threadIdx.x;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + tid; i < per;
+    const int64_t nv = per / VEC;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + tid; i < nv;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        for (int j = 0; j < M; ++j) snap[j * 256 + tid] = params[so[j] + i];
+        for (int j = 0; j < M; ++j)
+            snap[j * 256 + tid] = *reinterpret_cast<const V*>(params + so[j] + i * VEC);
         for (int j = 0; j < M; ++j) {
-            const double self = static_cast<double>(snap[j * 256 + tid]);
-            double acc = 0.0;
-            for (int q = 0; q < K; ++q)
-                acc = __dadd_rn(acc, __dsub_rn(static_cast<double>(snap[sp[j * K + q] * 256 + tid]), self));
-            const double delta = __dmul_rn(sc[j], acc);
-            disp += delta * delta;
-            params[so[j] + i] = __double2float_rn(__dadd_rn(self, delta));
+            const float* self4 = reinterpret_cast<const float*>(&snap[j * 256 + tid]);
+            float outv[VEC];
+#pragma unroll
+            for (int c = 0; c < VEC; ++c) {
+                const double self = static_cast<double>(self4[c]);
+                double acc = 0.0;
+                for (int q = 0; q < K; ++q) {
+                    const float* pv = reinterpret_cast<const float*>(&snap[sp[j * K + q] * 256 + tid]);
+                    acc = __dadd_rn(acc, __dsub_rn(static_cast<double>(pv[c]), self));
+                }
+                const double delta = __dmul_rn(sc[j], acc);
+                disp += delta * delta;
+                outv[c] = __double2float_rn(__dadd_rn(self, delta));
+            }
+            *reinterpret_cast<V*>(params + so[j] + i * VEC) = *reinterpret_cast<const V*>(outv);
         }
     }
     red[tid] = disp;
     __syncthreads();
     if (tid == 0) {
-        double s = 0.0;
-        for (int i = 0; i < (int)blockDim.x; ++i) s += red[i];
-        disp_partial[blockIdx.x] = s;
+        double s2 = 0.0;
+        for (int i = 0; i < (int)blockDim.x; ++i) s2 += red[i];
+        disp_partial[blockIdx.x] = s2;
     }
 }
 
 void merge_apply(float* params, const int64_t* expert_offs, int M, int64_t per,
                  const int32_t* peers, int K, const double* coef, double* disp_partial,
                  int nblocks, cudaStream_t s) {
-    const size_t smem = sizeof(float) * M * 256;
-    cudaFuncSetAttribute(merge_apply_k<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    merge_apply_k<64><<<nblocks, 256, smem, s>>>(params, expert_offs, M, per, peers, K, coef,
-                                                 disp_partial);
+    if (M <= 16 && per % 4 == 0) {
+        const size_t smem = sizeof(float4) * M * 256;
+        cudaFuncSetAttribute(merge_apply_k<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        merge_apply_k<4><<<nblocks, 256, smem, s>>>(params, expert_offs, M, per, peers, K, coef,
+                                                     disp_partial);
+    } else {
+        const size_t smem = sizeof(float) * M * 256;
+        cudaFuncSetAttribute(merge_apply_k<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        merge_apply_k<1><<<nblocks, 256, smem, s>>>(params, expert_offs, M, per, peers, K, coef,
+                                                     disp_partial);
+    }
     count_launch();
 }
 
