@@ -1516,8 +1516,9 @@ void gram_finish(const double* partial, int M, int nchunks, double* sim, cudaStr
 }
 
 // merge_experts (merging.hpp:97-136): w_j += coef_j * sum_q (w_peer_q - w_j), all experts
-// from the same pre-merge snapshot (element i of every expert staged in smem), in fp64.
-// VEC elements per thread (float4 for M <= 16).
+// from the same pre-merge snapshot, in fp64. Each thread snapshots element i of every expert
+// into its own smem column (peers are data-dependent indices), converted to double once:
+// 2 elements per thread for M <= 16 (double2 columns), else 1.
 template <int VEC>
 __global__ void __launch_bounds__(256) merge_apply_k(float* __restrict__ params,
                                                      const int64_t* __restrict__ expert_offs,
@@ -1525,13 +1526,12 @@ __global__ void __launch_bounds__(256) merge_apply_k(float* __restrict__ params,
                                                      const int32_t* __restrict__ peers, int K,
                                                      const double* __restrict__ coef,
                                                      double* __restrict__ disp_partial) {
-    using V = typename std::conditional<VEC == 4, float4, float>::type;
+    using F = typename std::conditional<VEC == 2, float2, float>::type;
     __shared__ int32_t sp[64 * 64];
     __shared__ double sc[64];
     __shared__ int64_t so[64];
     __shared__ double red[256];
-    extern __shared__ __align__(16) unsigned char snap_raw[];
-    V* snap = reinterpret_cast<V*>(snap_raw);  // [M][256]
+    extern __shared__ __align__(16) double snap[];  // [M][256][VEC]
     for (int i = threadIdx.x; i < M * K; i += blockDim.x) sp[i] = peers[i];
     for (int i = threadIdx.x; i < M; i += blockDim.x) {
         sc[i] = coef[i];
@@ -1543,24 +1543,94 @@ __global__ void __launch_bounds__(256) merge_apply_k(float* __restrict__ params,
     const int64_t nv = per / VEC;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + tid; i < nv;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        for (int j = 0; j < M; ++j)
-            snap[j * 256 + tid] = *reinterpret_cast<const V*>(params + so[j] + i * VEC);
+        constexpr int JU = VEC == 2 ? 16 : 8;  // loads in flight per batch
+        for (int j0 = 0; j0 < M; j0 += JU) {
+            F x[JU];
+#pragma unroll
+            for (int u = 0; u < JU; ++u)
+                if (j0 + u < M) x[u] = *reinterpret_cast<const F*>(params + so[j0 + u] + i * VEC);
+#pragma unroll
+            for (int u = 0; u < JU; ++u) {
+                if (j0 + u >= M) break;
+                const float* xf = reinterpret_cast<const float*>(&x[u]);
+#pragma unroll
+                for (int c = 0; c < VEC; ++c)
+                    snap[((j0 + u) * 256 + tid) * VEC + c] = static_cast<double>(xf[c]);
+            }
+        }
         for (int j = 0; j < M; ++j) {
-            const float* self4 = reinterpret_cast<const float*>(&snap[j * 256 + tid]);
             float outv[VEC];
 #pragma unroll
             for (int c = 0; c < VEC; ++c) {
-                const double self = static_cast<double>(self4[c]);
+                const double self = snap[(j * 256 + tid) * VEC + c];
                 double acc = 0.0;
-                for (int q = 0; q < K; ++q) {
-                    const float* pv = reinterpret_cast<const float*>(&snap[sp[j * K + q] * 256 + tid]);
-                    acc = __dadd_rn(acc, __dsub_rn(static_cast<double>(pv[c]), self));
-                }
+                for (int q = 0; q < K; ++q)
+                    acc = __dadd_rn(acc, __dsub_rn(snap[(sp[j * K + q] * 256 + tid) * VEC + c], self));
                 const double delta = __dmul_rn(sc[j], acc);
                 disp += delta * delta;
                 outv[c] = __double2float_rn(__dadd_rn(self, delta));
             }
-            *reinterpret_cast<V*>(params + so[j] + i * VEC) = *reinterpret_cast<const V*>(outv);
+            *reinterpret_cast<F*>(params + so[j] + i * VEC) = *reinterpret_cast<const F*>(outv);
+        }
+    }
+    red[tid] = disp;
+    __syncthreads();
+    if (tid == 0) {
+        double s2 = 0.0;
+        for (int i = 0; i < (int)blockDim.x; ++i) s2 += red[i];
+        disp_partial[blockIdx.x] = s2;
+    }
+}
+
+// M <= 16, K <= 8: two elements per thread as double2 snapshot columns, the peers' column
+// offsets precomputed per block, the peer loop unrolled (same fp64 operations and order)
+__global__ void __launch_bounds__(256) merge_apply_small_k(float* __restrict__ params,
+                                                           const int64_t* __restrict__ expert_offs,
+                                                           int M, int64_t per,
+                                                           const int32_t* __restrict__ peers, int K,
+                                                           const double* __restrict__ coef,
+                                                           double* __restrict__ disp_partial) {
+    __shared__ int32_t spo[16 * 8];  // peer column offset (peer * 256)
+    __shared__ double sc[16];
+    __shared__ int64_t so[16];
+    __shared__ double red[256];
+    extern __shared__ __align__(16) double2 snap2[];  // [M][256]
+    for (int i = threadIdx.x; i < M * K; i += blockDim.x) spo[(i / K) * 8 + i % K] = peers[i] * 256;
+    for (int i = threadIdx.x; i < M; i += blockDim.x) {
+        sc[i] = coef[i];
+        so[i] = expert_offs[i];
+    }
+    __syncthreads();
+    double disp = 0.0;
+    const int tid = threadIdx.x;
+    const int64_t nv = per / 2;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + tid; i < nv;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        float2 x[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (j < M) x[j] = *reinterpret_cast<const float2*>(params + so[j] + 2 * i);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (j < M) snap2[j * 256 + tid] = make_double2(x[j].x, x[j].y);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            if (j >= M) break;
+            const double2 self = snap2[j * 256 + tid];
+            double ax = 0.0, ay = 0.0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (q >= K) break;
+                const double2 pv = snap2[spo[j * 8 + q] + tid];
+                ax = __dadd_rn(ax, __dsub_rn(pv.x, self.x));
+                ay = __dadd_rn(ay, __dsub_rn(pv.y, self.y));
+            }
+            const double dx = __dmul_rn(sc[j], ax), dy = __dmul_rn(sc[j], ay);
+            disp += dx * dx;
+            disp += dy * dy;
+            *reinterpret_cast<float2*>(params + so[j] + 2 * i) =
+                make_float2(__double2float_rn(__dadd_rn(self.x, dx)),
+                            __double2float_rn(__dadd_rn(self.y, dy)));
         }
     }
     red[tid] = disp;
@@ -1575,13 +1645,18 @@ __global__ void __launch_bounds__(256) merge_apply_k(float* __restrict__ params,
 void merge_apply(float* params, const int64_t* expert_offs, int M, int64_t per,
                  const int32_t* peers, int K, const double* coef, double* disp_partial,
                  int nblocks, cudaStream_t s) {
-    if (M <= 16 && per % 4 == 0) {
-        const size_t smem = sizeof(float4) * M * 256;
-        cudaFuncSetAttribute(merge_apply_k<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        merge_apply_k<4><<<nblocks, 256, smem, s>>>(params, expert_offs, M, per, peers, K, coef,
+    if (M <= 16 && K <= 8 && per % 2 == 0) {
+        const size_t smem = sizeof(double2) * M * 256;
+        cudaFuncSetAttribute(merge_apply_small_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        merge_apply_small_k<<<nblocks, 256, smem, s>>>(params, expert_offs, M, per, peers, K, coef,
+                                                       disp_partial);
+    } else if (M <= 16 && per % 2 == 0) {
+        const size_t smem = sizeof(double) * 2 * M * 256;
+        cudaFuncSetAttribute(merge_apply_k<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        merge_apply_k<2><<<nblocks, 256, smem, s>>>(params, expert_offs, M, per, peers, K, coef,
                                                      disp_partial);
     } else {
-        const size_t smem = sizeof(float) * M * 256;
+        const size_t smem = sizeof(double) * M * 256;
         cudaFuncSetAttribute(merge_apply_k<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         merge_apply_k<1><<<nblocks, 256, smem, s>>>(params, expert_offs, M, per, peers, K, coef,
                                                      disp_partial);
