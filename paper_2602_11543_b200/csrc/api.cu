@@ -154,6 +154,9 @@ struct spes_ctx {
     cudaEvent_t ev_fork[5] = {}, ev_ready[5] = {};  // side-stream hand-offs within a step
     std::vector<int64_t> layer_lo, layer_hi;  // owned experts' compact range per layer
     ncclComm_t comm = nullptr;
+    // peers' parameter vectors mapped over NVLink (CUDA IPC), for the owner-set means
+    std::vector<float*> peer_params;
+    bool p2p_tried = false, p2p_ok = false;
     int64_t launches = 0;
 
     // ownership
@@ -1101,6 +1104,8 @@ void spes_destroy(spes_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    for (float* p : c->peer_params)
+        if (p) cudaIpcCloseMemHandle(p);
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->h_tokens) cudaFreeHost(c->h_tokens);
     if (c->h_losses) cudaFreeHost(c->h_losses);
@@ -1644,6 +1649,62 @@ spes_status spes_outer_sync(spes_ctx* c, int32_t kind, double lr, double momentu
 }
 
 // ---- sync (Server::aggregate, protocol.cpp:197-251) ----
+// Map every peer's parameter vector (collective, once): IPC handles travel by an NCCL
+// all-gather; a second all-gather of the per-rank outcome keeps the choice between the
+// NVLink peer-read path and the NCCL send/recv path identical on all ranks.
+static void open_peer_params(spes_ctx* c) {
+    if (c->p2p_tried) return;
+    c->p2p_tried = true;
+    const int N = c->n_nodes, me = c->node;
+    if (const char* e = std::getenv("SPES_SYNC_P2P"))
+        if (std::atoi(e) == 0) return;  // all ranks see the same environment
+    struct Rec {
+        cudaIpcMemHandle_t h;
+        int32_t ok;
+        int32_t pad[15];
+    };
+    Rec mine{};
+    mine.ok = cudaIpcGetMemHandle(&mine.h, c->params) == cudaSuccess ? 1 : 0;
+    cudaGetLastError();
+    Rec* d = nullptr;
+    ck(cudaMalloc(&d, sizeof(Rec) * N), "cudaMalloc");
+    ck(cudaMemcpy(d + me, &mine, sizeof(Rec), cudaMemcpyHostToDevice), "H2D");
+    ckn(ncclAllGather(d + me, d, sizeof(Rec), ncclUint8, c->comm, c->stream), "allgather ipc");
+    std::vector<Rec> all(N);
+    ck(cudaMemcpyAsync(all.data(), d, sizeof(Rec) * N, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    int32_t ok = 1;
+    std::vector<float*> peers(N, nullptr);
+    for (int n = 0; n < N; ++n) {
+        if (!all[n].ok) ok = 0;
+        if (n == me || !ok) continue;
+        void* p = nullptr;
+        if (cudaIpcOpenMemHandle(&p, all[n].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            ok = 0;
+            continue;
+        }
+        peers[n] = static_cast<float*>(p);
+    }
+    // agree: every rank must have opened every peer
+    int32_t* flags = reinterpret_cast<int32_t*>(d);
+    ck(cudaMemcpy(flags + me, &ok, 4, cudaMemcpyHostToDevice), "H2D");
+    ckn(ncclAllGather(flags + me, flags, 1, ncclInt32, c->comm, c->stream), "allgather ok");
+    std::vector<int32_t> oks(N);
+    ck(cudaMemcpyAsync(oks.data(), flags, 4 * N, cudaMemcpyDeviceToHost, c->stream), "D2H");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    cudaFree(d);
+    bool all_ok = true;
+    for (int32_t v : oks) all_ok = all_ok && v;
+    if (!all_ok) {
+        for (float* p : peers)
+            if (p) cudaIpcCloseMemHandle(p);
+        return;
+    }
+    c->peer_params = peers;
+    c->p2p_ok = true;
+}
+
 spes_status spes_sync(spes_ctx* c, spes_sync_stats* stats) {
     return guard([&] {
         ck(cudaSetDevice(c->device), "cudaSetDevice");
@@ -1665,8 +1726,12 @@ spes_status spes_sync(spes_ctx* c, spes_sync_stats* stats) {
             const int64_t psi = L.psi();
             if (!c->psi_stage) c->psi_stage = c->scratch.alloc<float>(psi * N);
             // psi: every node's copy, then fp64 node-order mean (protocol.cpp:238-243)
-            ckn(ncclAllGather(c->params, c->psi_stage, psi, ncclFloat, c->comm, st), "allgather psi");
-            spes_k::owner_mean_strided(c->psi_stage, N, psi, psi, c->params, st);
+            {
+                Prof pp(c, "sync_psi");
+                ckn(ncclAllGather(c->params, c->psi_stage, psi, ncclFloat, c->comm, st),
+                    "allgather psi");
+                spes_k::owner_mean_strided(c->psi_stage, N, psi, psi, c->params, st);
+            }
             psi_in = 4.0 * psi * (N - 1);
             // experts: primary owner per expert
             std::vector<int> primary;
@@ -1674,46 +1739,66 @@ spes_status spes_sync(spes_ctx* c, spes_sync_stats* stats) {
             sync_plan(L.M, N, c->owners, primary, balanced);
             const int s_bal = balanced ? L.M / N : 0;
             const int64_t per = L.per_expert();
-            // staging for co-owner copies received by this primary
+            open_peer_params(c);
+            // staging for co-owner copies received by this primary (NCCL path only)
             int64_t need = 0;
             for (int e = 0; e < L.M; ++e)
                 if (primary[e] == me) need += static_cast<int64_t>(c->owners[e].size() - 1) * per * L.L;
-            if (need > c->expert_stage_cap) {
+            if (!c->p2p_ok && need > c->expert_stage_cap) {
                 c->expert_stage = c->scratch.alloc<float>(need);
                 c->expert_stage_cap = need;
             }
             std::map<std::pair<int, int>, float*> slot;  // (expert*L + l, owner) -> staging
             int64_t q = 0;
-            ckn(ncclGroupStart(), "group");
-            for (int l = 0; l < L.L; ++l)
-                for (int e = 0; e < L.M; ++e) {
-                    const auto& O = c->owners[e];
-                    if (O.size() < 2) continue;
-                    float* mine = c->params + L.off_expert(l, e);
-                    if (primary[e] == me) {
-                        for (int o : O) {
-                            if (o == me) continue;
-                            float* dst = c->expert_stage + q;
-                            q += per;
-                            slot[{e * L.L + l, o}] = dst;
-                            ckn(ncclRecv(dst, per, ncclFloat, o, c->comm, st), "recv");
-                            exp_in += 4.0 * per;
+            // phase timers (profiled rounds only)
+            auto ph = std::make_unique<Prof>(c, "sync_to_primary");
+            if (!c->p2p_ok) {  // co-owner copies to the primary over NCCL
+                ckn(ncclGroupStart(), "group");
+                for (int l = 0; l < L.L; ++l)
+                    for (int e = 0; e < L.M; ++e) {
+                        const auto& O = c->owners[e];
+                        if (O.size() < 2) continue;
+                        float* mine = c->params + L.off_expert(l, e);
+                        if (primary[e] == me) {
+                            for (int o : O) {
+                                if (o == me) continue;
+                                float* dst = c->expert_stage + q;
+                                q += per;
+                                slot[{e * L.L + l, o}] = dst;
+                                ckn(ncclRecv(dst, per, ncclFloat, o, c->comm, st), "recv");
+                            }
+                        } else if (std::find(O.begin(), O.end(), me) != O.end()) {
+                            ckn(ncclSend(mine, per, ncclFloat, primary[e], c->comm, st), "send");
                         }
-                    } else if (std::find(O.begin(), O.end(), me) != O.end()) {
-                        ckn(ncclSend(mine, per, ncclFloat, primary[e], c->comm, st), "send");
                     }
-                }
-            ckn(ncclGroupEnd(), "group end");
-            // owner-set mean at the primary, owners in ascending node order
+                ckn(ncclGroupEnd(), "group end");
+            }
+            ph.reset();
+            ph = std::make_unique<Prof>(c, "sync_owner_mean");
+            // owner-set mean at the primary, owners in ascending node order; with peer
+            // mappings the co-owners' copies are read in place over NVLink (their local
+            // rounds are done: every rank has passed the psi all-gather above, and no rank
+            // overwrites its copy before the expert all-gather below, which needs this
+            // primary's mean first)
             for (int l = 0; l < L.L; ++l)
                 for (int e = 0; e < L.M; ++e) {
                     const auto& O = c->owners[e];
                     if (O.size() < 2 || primary[e] != me) continue;
                     std::vector<const float*> srcs;
                     float* mine = c->params + L.off_expert(l, e);
-                    for (int o : O) srcs.push_back(o == me ? mine : slot[{e * L.L + l, o}]);
+                    for (int o : O) {
+                        if (o == me)
+                            srcs.push_back(mine);
+                        else if (c->p2p_ok)
+                            srcs.push_back(c->peer_params[o] + L.off_expert(l, e));
+                        else
+                            srcs.push_back(slot[{e * L.L + l, o}]);
+                        if (o != me) exp_in += 4.0 * per;
+                    }
                     spes_k::owner_mean(srcs.data(), static_cast<int>(srcs.size()), per, mine, st);
                 }
+            ph.reset();
+            ph = std::make_unique<Prof>(c, "sync_gather");
             // every node receives every expert from its primary
             if (balanced) {
                 for (int l = 0; l < L.L; ++l) {
@@ -1734,7 +1819,10 @@ spes_status spes_sync(spes_ctx* c, spes_sync_stats* stats) {
             int64_t mine_primary = 0;
             for (int e = 0; e < L.M; ++e) mine_primary += primary[e] == me;
             exp_in += 4.0 * per * L.L * (L.M - mine_primary);
+            ph.reset();
+            ph = std::make_unique<Prof>(c, "sync_refresh_shadows");
             refresh_shadows_all(c);
+            ph.reset();
         }
         cudaEventRecord(e1, st);
         ck(cudaStreamSynchronize(st), "sync");

@@ -1273,11 +1273,45 @@ __global__ void owner_mean_list_k(SrcList L, int n_src, int64_t n, float* __rest
     }
 }
 
+// float4 columns, every source's load in flight before the fp64 sums (the sources may be
+// peer GPUs' memory read over NVLink); same per-element operations as owner_mean_list_k
+__global__ void owner_mean_list4_k(SrcList L, int n_src, int64_t n4, float* __restrict__ out) {
+    const double inv = 1.0 / static_cast<double>(n_src);
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        float4 v[16];
+#pragma unroll
+        for (int s = 0; s < 16; ++s)
+            if (s < n_src) v[s] = reinterpret_cast<const float4*>(L.p[s])[i];
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+            if (s >= n_src) break;
+            a0 = __dadd_rn(a0, static_cast<double>(v[s].x));
+            a1 = __dadd_rn(a1, static_cast<double>(v[s].y));
+            a2 = __dadd_rn(a2, static_cast<double>(v[s].z));
+            a3 = __dadd_rn(a3, static_cast<double>(v[s].w));
+        }
+        reinterpret_cast<float4*>(out)[i] =
+            make_float4(__double2float_rn(__dmul_rn(a0, inv)), __double2float_rn(__dmul_rn(a1, inv)),
+                        __double2float_rn(__dmul_rn(a2, inv)), __double2float_rn(__dmul_rn(a3, inv)));
+    }
+}
+
 void owner_mean(const float* const* srcs, int n_src, int64_t n, float* out, cudaStream_t s) {
     SrcList L{};
-    for (int i = 0; i < n_src && i < 16; ++i) L.p[i] = srcs[i];
-    const int blocks = static_cast<int>(std::min<int64_t>(cdiv(n, 256), 148 * 16));
-    owner_mean_list_k<<<blocks, 256, 0, s>>>(L, n_src, n, out);
+    bool aligned = n % 4 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0;
+    for (int i = 0; i < n_src && i < 16; ++i) {
+        L.p[i] = srcs[i];
+        aligned = aligned && reinterpret_cast<uintptr_t>(srcs[i]) % 16 == 0;
+    }
+    if (aligned) {
+        const int blocks = static_cast<int>(std::min<int64_t>(cdiv(n / 4, 256), 148 * 8));
+        owner_mean_list4_k<<<blocks, 256, 0, s>>>(L, n_src, n / 4, out);
+    } else {
+        const int blocks = static_cast<int>(std::min<int64_t>(cdiv(n, 256), 148 * 16));
+        owner_mean_list_k<<<blocks, 256, 0, s>>>(L, n_src, n, out);
+    }
     count_launch();
 }
 

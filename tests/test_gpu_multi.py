@@ -28,8 +28,10 @@ def _n_gpus():
         return 0
 
 
-def _rank(rank, world, nccl_id, owned, params, tokens, q):
+def _rank(rank, world, nccl_id, owned, params, tokens, q, p2p=True):
     try:
+        import os
+        os.environ["SPES_SYNC_P2P"] = "1" if p2p else "0"  # read when the first sync runs
         cfg = model_cfg(**CFG)
         node = spes.Node(cfg, rank, world, rank, nccl_id)
         node.set_ownership(owned)
@@ -46,9 +48,12 @@ def _rank(rank, world, nccl_id, owned, params, tokens, q):
         q.put((rank, None, None, None, None, repr(e)))
 
 
-@pytest.mark.parametrize("world,layout", [(2, "replicated"), (2, "partition"), (4, "replicated"),
-                                          (4, "partition")])
-def test_nccl_sync_matches_oracle(world, layout):
+@pytest.mark.parametrize("world,layout,p2p", [(2, "replicated", True), (2, "partition", True),
+                                              (4, "replicated", True), (4, "partition", True),
+                                              (2, "replicated", False), (4, "replicated", False)])
+def test_nccl_sync_matches_oracle(world, layout, p2p):
+    """p2p: the primaries read co-owner copies in place over NVLink (CUDA IPC mappings);
+    otherwise the copies travel by NCCL send/recv. Same bits either way."""
     if _n_gpus() < world:
         pytest.skip(f"needs {world} GPUs")
     cfg = model_cfg(**CFG)
@@ -60,7 +65,7 @@ def test_nccl_sync_matches_oracle(world, layout):
     nccl_id = spes.nccl_unique_id()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_rank, args=(r, world, nccl_id, owned, params, tokens, q))
+    procs = [ctx.Process(target=_rank, args=(r, world, nccl_id, owned, params, tokens, q, p2p))
              for r in range(world)]
     for p in procs:
         p.start()
