@@ -291,7 +291,7 @@ def reference_arm(args):
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -456,15 +456,29 @@ def our_arm(args):
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {e}"}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     node.close()
     return 0
 
 
+_JSON_OUT = None
+
+
+def emit(line):
+    """The bench's one JSON line, on the real stdout."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
     os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
-    # NCCL's own log lines ("NCCL version ...") go to stderr: stdout carries only the JSON line
-    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    # stdout carries only the JSON line: native libraries' prints (e.g. NCCL's "NCCL
+    # version" banner) are sent to stderr by pointing fd 1 at fd 2
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     args = parse()
     if args.impl == "reference":
         return reference_arm(args)
