@@ -157,6 +157,10 @@ struct spes_ctx {
     // peers' parameter vectors mapped over NVLink (CUDA IPC), for the owner-set means
     std::vector<float*> peer_params;
     bool p2p_tried = false, p2p_ok = false;
+    int32_t* barrier_buf = nullptr;
+    std::vector<spes_k::PullTask> pull_host;
+    spes_k::PullTask* pull_dev = nullptr;
+    int pull_cap = 0;
     int64_t launches = 0;
 
     // ownership
@@ -1778,8 +1782,9 @@ spes_status spes_sync(spes_ctx* c, spes_sync_stats* stats) {
             // owner-set mean at the primary, owners in ascending node order; with peer
             // mappings the co-owners' copies are read in place over NVLink (their local
             // rounds are done: every rank has passed the psi all-gather above, and no rank
-            // overwrites its copy before the expert all-gather below, which needs this
-            // primary's mean first)
+            // overwrites its copy before the barrier below) and the primary also writes the
+            // expert's bf16 operand copy from the mean
+            const spes_k::Shadows shd = shadows_of(c);
             for (int l = 0; l < L.L; ++l)
                 for (int e = 0; e < L.M; ++e) {
                     const auto& O = c->owners[e];
@@ -1795,12 +1800,43 @@ spes_status spes_sync(spes_ctx* c, spes_sync_stats* stats) {
                             srcs.push_back(slot[{e * L.L + l, o}]);
                         if (o != me) exp_in += 4.0 * per;
                     }
-                    spes_k::owner_mean(srcs.data(), static_cast<int>(srcs.size()), per, mine, st);
+                    spes_k::owner_mean(srcs.data(), static_cast<int>(srcs.size()), per, mine, st,
+                                       c->p2p_ok ? &shd : nullptr, l * L.M + e);
                 }
             ph.reset();
             ph = std::make_unique<Prof>(c, "sync_gather");
             // every node receives every expert from its primary
-            if (balanced) {
+            if (c->p2p_ok) {
+                // pulled over NVLink between two barriers: every primary's mean is final
+                // before any pull, and no rank moves on (its next local round rewrites the
+                // experts it owns) before every pull is done. The pull also writes the
+                // operand copies, so only the head's needs a refresh below.
+                if (!c->barrier_buf) c->barrier_buf = c->persistent.alloc<int32_t>(1);
+                ckn(ncclAllReduce(c->barrier_buf, c->barrier_buf, 1, ncclInt32, ncclSum, c->comm, st),
+                    "barrier");
+                c->pull_host.clear();
+                for (int l = 0; l < L.L; ++l)
+                    for (int e = 0; e < L.M; ++e)
+                        if (primary[e] >= 0 && primary[e] != me) {
+                            const int64_t off = L.off_expert(l, e);
+                            c->pull_host.push_back(
+                                {c->peer_params[primary[e]] + off, c->params + off, l * L.M + e, 0});
+                            exp_in += 4.0 * per;
+                        }
+                const int nt = static_cast<int>(c->pull_host.size());
+                if (nt > c->pull_cap) {
+                    c->pull_dev = c->persistent.alloc<spes_k::PullTask>(nt);
+                    c->pull_cap = nt;
+                }
+                if (nt > 0) {
+                    ck(cudaMemcpyAsync(c->pull_dev, c->pull_host.data(), sizeof(spes_k::PullTask) * nt,
+                                       cudaMemcpyHostToDevice, st),
+                       "pull tasks");
+                    spes_k::expert_pull(c->pull_dev, nt, per, shd, st);
+                }
+                ckn(ncclAllReduce(c->barrier_buf, c->barrier_buf, 1, ncclInt32, ncclSum, c->comm, st),
+                    "barrier");
+            } else if (balanced) {
                 for (int l = 0; l < L.L; ++l) {
                     float* base = c->params + L.off_expert(l, 0);
                     const int64_t cnt = per * s_bal;
@@ -1816,12 +1852,18 @@ spes_status spes_sync(spes_ctx* c, spes_sync_stats* stats) {
                     }
                 ckn(ncclGroupEnd(), "group end");
             }
-            int64_t mine_primary = 0;
-            for (int e = 0; e < L.M; ++e) mine_primary += primary[e] == me;
-            exp_in += 4.0 * per * L.L * (L.M - mine_primary);
+            if (!c->p2p_ok) {
+                int64_t mine_primary = 0;
+                for (int e = 0; e < L.M; ++e) mine_primary += primary[e] == me;
+                exp_in += 4.0 * per * L.L * (L.M - mine_primary);
+            }
             ph.reset();
             ph = std::make_unique<Prof>(c, "sync_refresh_shadows");
-            refresh_shadows_all(c);
+            if (c->p2p_ok)  // expert copies were written by the means and the pulls
+                spes_k::refresh_shadows(c->params, c->all_segs, c->n_all_segs, L.V * L.d,
+                                        shd, st);  // the head leads the refresh table
+            else
+                refresh_shadows_all(c);
             ph.reset();
         }
         cudaEventRecord(e1, st);
@@ -2088,6 +2130,12 @@ spes_status spes_debug_read(spes_ctx* c, const char* name, int32_t layer, void* 
                     "debug_read: the final hidden state is kept only as the bf16 head operand");
             src = c->h[layer];
             sz = 4 * T * d;
+        } else if (n == "w1" || n == "w2") {  // a layer's bf16 expert operand copies
+            if (layer < 0 || layer >= L.L) throw std::out_of_range("debug_read: bad layer");
+            const int64_t per_slot = n == "w1" ? L.d * 2 * L.f : L.f * L.d;
+            const bf16* base = n == "w1" ? c->w1 : c->w2;
+            src = base + per_slot * L.M * layer;
+            sz = 2 * per_slot * L.M;
         } else if (n == "normed") {
             throw std::invalid_argument(
                 "debug_read: normed is not stored on the training path (recomputed in "

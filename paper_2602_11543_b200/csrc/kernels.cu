@@ -11,6 +11,7 @@
 
 #include <algorithm>
 
+#include <stdexcept>
 #include <type_traits>
 
 #include "common.cuh"
@@ -1275,7 +1276,8 @@ __global__ void owner_mean_list_k(SrcList L, int n_src, int64_t n, float* __rest
 
 // float4 columns, every source's load in flight before the fp64 sums (the sources may be
 // peer GPUs' memory read over NVLink); same per-element operations as owner_mean_list_k
-__global__ void owner_mean_list4_k(SrcList L, int n_src, int64_t n4, float* __restrict__ out) {
+__global__ void owner_mean_list4_k(SrcList L, int n_src, int64_t n4, float* __restrict__ out,
+                                   Shadows sh, int slot) {
     const double inv = 1.0 / static_cast<double>(n_src);
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -1292,13 +1294,21 @@ __global__ void owner_mean_list4_k(SrcList L, int n_src, int64_t n4, float* __re
             a2 = __dadd_rn(a2, static_cast<double>(v[s].z));
             a3 = __dadd_rn(a3, static_cast<double>(v[s].w));
         }
-        reinterpret_cast<float4*>(out)[i] =
+        const float4 r =
             make_float4(__double2float_rn(__dmul_rn(a0, inv)), __double2float_rn(__dmul_rn(a1, inv)),
                         __double2float_rn(__dmul_rn(a2, inv)), __double2float_rn(__dmul_rn(a3, inv)));
+        reinterpret_cast<float4*>(out)[i] = r;
+        if (slot >= 0) {  // the expert's bf16 GEMM operand copy, from the same values
+            AdamSeg sg{};
+            sg.kind = 1;
+            sg.slot = slot;
+            write_shadow4(sg, 4 * i, r, sh);
+        }
     }
 }
 
-void owner_mean(const float* const* srcs, int n_src, int64_t n, float* out, cudaStream_t s) {
+void owner_mean(const float* const* srcs, int n_src, int64_t n, float* out, cudaStream_t s,
+                const Shadows* sh, int slot) {
     SrcList L{};
     bool aligned = n % 4 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0;
     for (int i = 0; i < n_src && i < 16; ++i) {
@@ -1307,11 +1317,53 @@ void owner_mean(const float* const* srcs, int n_src, int64_t n, float* out, cuda
     }
     if (aligned) {
         const int blocks = static_cast<int>(std::min<int64_t>(cdiv(n / 4, 256), 148 * 8));
-        owner_mean_list4_k<<<blocks, 256, 0, s>>>(L, n_src, n / 4, out);
+        owner_mean_list4_k<<<blocks, 256, 0, s>>>(L, n_src, n / 4, out, sh ? *sh : Shadows{},
+                                                   sh ? slot : -1);
     } else {
+        if (sh) throw std::logic_error("owner_mean: operand refresh needs 16-byte aligned rows");
         const int blocks = static_cast<int>(std::min<int64_t>(cdiv(n, 256), 148 * 16));
         owner_mean_list_k<<<blocks, 256, 0, s>>>(L, n_src, n, out);
     }
+    count_launch();
+}
+
+// expert pulls of the sparse sync: every task copies one expert (per floats) from its
+// primary owner's parameters (a peer GPU, read over NVLink) into this node's parameters and
+// writes its bf16 GEMM operand copy from the same values
+__global__ void expert_pull_k(const PullTask* __restrict__ tasks, int64_t n4, Shadows sh) {
+    const PullTask t = tasks[blockIdx.y];
+    AdamSeg sg{};
+    sg.kind = 1;
+    sg.slot = t.slot;
+    const float4* src = reinterpret_cast<const float4*>(t.src);
+    float4* dst = reinterpret_cast<float4*>(t.dst);
+    constexpr int U = 4;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * U;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * U + threadIdx.x; base < n4;
+         base += stride) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = base + static_cast<int64_t>(u) * blockDim.x;
+            if (i < n4) v[u] = src[i];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = base + static_cast<int64_t>(u) * blockDim.x;
+            if (i < n4) {
+                dst[i] = v[u];
+                write_shadow4(sg, 4 * i, v[u], sh);
+            }
+        }
+    }
+}
+
+void expert_pull(const PullTask* tasks, int ntasks, int64_t per, Shadows sh, cudaStream_t s) {
+    if (ntasks <= 0) return;
+    const int64_t n4 = per / 4;
+    const int bx = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>(cdiv(n4, 256 * 4), (148 * 8 + ntasks - 1) / ntasks)));
+    expert_pull_k<<<dim3(bx, ntasks), 256, 0, s>>>(tasks, n4, sh);
     count_launch();
 }
 

@@ -145,6 +145,18 @@ struct Shadows {
     bf16* headB;
     int64_t d, f;
 };
+// out = fp64 mean of the sources in order (the sources may be peer GPUs' memory); with sh,
+// also the bf16 operand copy of expert slot `slot` (out is that expert's parameter block)
+void owner_mean(const float* const* srcs, int n_src, int64_t n, float* out, cudaStream_t s,
+                const Shadows* sh = nullptr, int slot = -1);
+// one expert (per floats) from a peer's parameters into ours, plus its bf16 operand copy
+struct PullTask {
+    const float* src;
+    float* dst;
+    int32_t slot;
+    int32_t pad;
+};
+void expert_pull(const PullTask* tasks, int ntasks, int64_t per, Shadows sh, cudaStream_t s);
 // MaskedAdamW step over the first `total` compact scalars; also writes the refreshed
 // bf16 copies. No update when *loss_total is non-finite (loss_total may be null).
 using spes_dev::AdamScalars;
@@ -171,7 +183,6 @@ void corpus_gather(const int32_t* corpus, const int64_t* rows, int64_t B, int64_
 // go to theta and out
 void outer_step(float* theta, const float* recv, int N, int64_t n, int64_t ld, int kind, double lr,
                 double momentum, double* buf, float* out, cudaStream_t s);
-void owner_mean(const float* const* srcs, int n_src, int64_t n, float* out, cudaStream_t s);
 void owner_mean_strided(const float* x, int n_src, int64_t stride, int64_t n, float* out,
                         cudaStream_t s);
 void gram_partials(const float* params, const int64_t* vec_offs, int M, int64_t D1,

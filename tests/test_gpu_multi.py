@@ -40,6 +40,16 @@ def _rank(rank, world, nccl_id, owned, params, tokens, q, p2p=True):
         pre = node.read_params()
         st = node.sync()
         post = node.read_params()
+        # the bf16 GEMM operand copies the sync left must equal a fresh refresh from fp32
+        d, f, M = cfg.hidden, cfg.intermediate, cfg.experts_total
+        def copies():
+            return [node.debug(w, l, np.uint16, None, M * n)
+                    for l in range(cfg.layers) for w, n in (("w1", 2 * d * f), ("w2", d * f))]
+        synced = copies()
+        node.load_params(post)  # rewrites every copy from the fp32 parameters
+        fresh = copies()
+        if not all(np.array_equal(a, b) for a, b in zip(synced, fresh)):
+            raise AssertionError("operand copies after sync differ from a refresh")
         ev, peers = node.merge_model(merge_sched(**SCHED), 0)
         merged = node.read_params()
         node.close()
