@@ -796,9 +796,9 @@ void forward_backward(spes_ctx* c) {
         {
             PROF("router_bwd");
             need(2);  // glog (and, earlier on the side stream, the loss scalars)
-            spes_k::normed_grad(hsrc(l), hmap(l), P + L.off_norm(l), P + L.off_router(l), Y.inv_rms,
+            spes_k::normed_grad(hsrc(l), hmap(l), P + L.off_norm(l), P + L.off_router(l),
                                 Y.slot_row, c->dxp, T, d, M, k, c->glog, c->gnormed, c->dot_part,
-                                nullptr, st);
+                                st);
         }
         {
             PROF("norm_router_grads");  // + rmsnorm backward into gh

@@ -697,7 +697,8 @@ constexpr int NRG_TC = kNormRouterChunks;
 constexpr int NG_QT_RMS = 128;  // columns per normed_grad tile = dot partials per token (d / 128)
 constexpr int NRG_EG = 16;
 // With `gh` non-null the z = 0 blocks also apply the rmsnorm backward to their columns
-// (rmsnorm_bwd_k's formula and dot order): h.grad += (gy*g)*inv - coef*x, so h and gnormed
+// (kernels.hpp:130-152; the dot from normed_grad's slab partials, summed in slab order):
+// h.grad += (gy*g)*inv - coef*x, so h and gnormed
 // are streamed once for both.
 __global__ void __launch_bounds__(256) norm_router_partial_k(
     const float* __restrict__ h, const int32_t* __restrict__ hrow,
@@ -1025,11 +1026,6 @@ void embed_grad_apply(const int32_t* inputs, const float* gh0, int64_t T, int64_
     count_launch();
 }
 
-void embed_grad(const int32_t* inputs, const float* gh0, int64_t T, int64_t d, int64_t V,
-                float* g_emb, int32_t* scratch, cudaStream_t s) {
-    embed_grad_plan(inputs, T, V, scratch, s);
-    embed_grad_apply(inputs, gh0, T, d, V, g_emb, scratch, s);
-}
 
 // ============================ device corpus batches ============================
 // batch row b = corpus row rows[b] (S+1 tokens), make_batch (corpus.cpp:81-87)

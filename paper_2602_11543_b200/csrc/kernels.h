@@ -101,37 +101,28 @@ void losses_reduce(const float* diff, const float* lse_head, const float* lse_r,
 void combine_backward(const float* gh, const float* y, const int32_t* row_token,
                       const float* row_w, const int32_t* R_total_dev, int64_t R_cap, int64_t d,
                       bf16* dyw, float* gw_part, cudaStream_t s);
-void router_backward(const float* h, const int32_t* hrow, const float* gain, const float* router,
-                     const float* probs,
-                     const float* lse_r, const float* inv_rms, const float* denom,
-                     const int32_t* topk_idx, const int32_t* slot_row, const float* gw_part,
-                     const float* dxp, const float* lb_coeff, int64_t T, int64_t d, int M, int k,
-                     int renorm, float g_lbsum, float g_s, float* glog, float* gnormed,
-                     float* dot_part, float* gh, cudaStream_t s);  // gh null: rmsnorm bwd deferred
-// router_backward's two halves: the per-token scalar chain (-> glog; needs only the
-// forward's routing and the gate-weight gradients) and the normed gradient (needs dX)
+// Router backward in two halves: the per-token scalar chain (-> glog; needs only the
+// forward's routing and the gate-weight gradients) and the normed gradient (needs dX; its
+// per-slab rmsnorm dot partials go to dot_part for norm_router_grads)
 void router_scalar_backward(const float* probs, const float* lse_r, const float* denom,
                             const int32_t* topk_idx, const int32_t* slot_row, const float* gw_row,
                             const float* lb_coeff, int64_t T, int M, int k, int renorm,
                             float g_lbsum, float g_s, float* glog, cudaStream_t s);
 void normed_grad(const float* h, const int32_t* hrow, const float* gain, const float* router,
-                 const float* inv_rms, const int32_t* slot_row, const float* dxp, int64_t T,
-                 int64_t d, int M, int k, const float* glog, float* gnormed, float* dot_part,
-                 float* gh, cudaStream_t s);
+                 const int32_t* slot_row, const float* dxp, int64_t T, int64_t d, int M, int k,
+                 const float* glog, float* gnormed, float* dot_part, cudaStream_t s);
 // token chunks of norm_router_grads ((d/128) x 37 blocks = whole waves of 2 per SM); its
 // partial buffer holds kNormRouterChunks * d * (M + 1) floats
 constexpr int kNormRouterChunks = 37;
 // normed is recomputed exactly from h, inv_rms and the gain (not stored in forward)
-// gh non-null: also applies the rmsnorm backward (router_backward then skips it)
+// gh non-null: also applies the rmsnorm backward (dot from normed_grad's dot_part)
 void norm_router_grads(const float* h, const int32_t* hrow, const float* gain, const float* gnormed,
                        const float* glog, const float* inv_rms, int64_t T, int64_t d, int M,
                        float* partial, float* g_gain, float* g_router, const float* dot_part,
                        float* gh, cudaStream_t s);
-// scratch: 2V + 1 + T int32 (fast path for V <= 1024; nullptr => generic kernel)
-void embed_grad(const int32_t* inputs, const float* gh0, int64_t T, int64_t d, int64_t V,
-                float* g_emb, int32_t* scratch, cudaStream_t s);
-// the same in two halves: the token bucketing by vocabulary id (needs only the inputs;
-// false => no fast path, embed_grad_apply does everything) and the gradient sums
+// embedding gradient in two halves: the token bucketing by vocabulary id (needs only the
+// inputs; scratch: 2V + 1 + T int32; false => no fast path (V > 1024 or no scratch), and
+// embed_grad_apply does everything) and the gradient sums
 bool embed_grad_plan(const int32_t* inputs, int64_t T, int64_t V, int32_t* scratch, cudaStream_t s);
 void embed_grad_apply(const int32_t* inputs, const float* gh0, int64_t T, int64_t d, int64_t V,
                       float* g_emb, int32_t* scratch, cudaStream_t s);

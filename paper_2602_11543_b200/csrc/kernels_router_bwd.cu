@@ -4,14 +4,15 @@
 //   logits.grad = (0 + gl*p_j) [moe_z logsumexp] + p_j*(gprobs_j - dot) [softmax bwd]
 //   normed.grad = dX of selected experts (desc.) + glog . R^T [matmul_nt_acc]
 //   h.grad     += rmsnorm backward (kernels.hpp:130-152)
-// Three kernels, each streaming its operands once:
+// Two kernels here, each streaming its operands once:
 //   router_scalar_bwd_k : thread per token, the M-wide scalar chain  -> glog [T x M]
 //   normed_grad_k       : 32-token x 128-column tiles; per element the dX sum (descending
 //                         experts) then the sequential-e router product; per-tile partial
 //                         of sum_q (gy*g)*x for the rmsnorm dot
-//   rmsnorm_bwd_k       : warp per token, h.grad += (gy*g)*inv - coef*x
-// Every element keeps the reference's own accumulation order; only the rmsnorm dot
-// (a sum over d) is a fixed-order tree.
+// The rmsnorm backward itself (h.grad += (gy*g)*inv - coef*x) runs inside
+// norm_router_partial_k (kernels.cu), which streams h and gnormed for the gain and router
+// gradients anyway. Every element keeps the reference's own accumulation order; only the
+// rmsnorm dot (a sum over d) is a fixed-order tree.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -162,37 +163,6 @@ __global__ void __launch_bounds__(256) normed_grad_k(
     }
 }
 
-__global__ void __launch_bounds__(256) rmsnorm_bwd_k(const float* __restrict__ h,
-                                                     const int32_t* __restrict__ hrow,
-                                                     const float* __restrict__ gain,
-                                                     const float* __restrict__ inv_rms,
-                                                     const float* __restrict__ gnormed,
-                                                     const float* __restrict__ dot_part, int T,
-                                                     int d, float* __restrict__ gh) {
-    const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (t >= T) return;
-    const int np = d / NG_QT;
-    float dot2 = 0.f;
-    for (int i = 0; i < np; ++i) dot2 += dot_part[static_cast<int64_t>(t) * np + i];
-    const float inv = inv_rms[t];
-    const float coef = fdiv(fmul(fmul(fmul(dot2, inv), inv), inv), static_cast<float>(d));
-    const float* xr = h + (hrow ? static_cast<int64_t>(hrow[t]) : static_cast<int64_t>(t)) * d;
-    const float* gy = gnormed + static_cast<int64_t>(t) * d;
-    float* ghr = gh + static_cast<int64_t>(t) * d;
-    for (int q0 = lane * 4; q0 < d; q0 += 128) {
-        const float4 a = __ldg(reinterpret_cast<const float4*>(gy + q0));
-        const float4 xv = __ldg(reinterpret_cast<const float4*>(xr + q0));
-        const float4 gv = __ldg(reinterpret_cast<const float4*>(gain + q0));
-        float4 o = *reinterpret_cast<const float4*>(ghr + q0);
-        o.x = fadd(o.x, fsub(fmul(fmul(a.x, gv.x), inv), fmul(coef, xv.x)));
-        o.y = fadd(o.y, fsub(fmul(fmul(a.y, gv.y), inv), fmul(coef, xv.y)));
-        o.z = fadd(o.z, fsub(fmul(fmul(a.z, gv.z), inv), fmul(coef, xv.z)));
-        o.w = fadd(o.w, fsub(fmul(fmul(a.w, gv.w), inv), fmul(coef, xv.w)));
-        *reinterpret_cast<float4*>(ghr + q0) = o;
-    }
-}
-
 void router_scalar_backward(const float* probs, const float* lse_r, const float* denom,
                             const int32_t* topk_idx, const int32_t* slot_row, const float* gw_row,
                             const float* lb_coeff, int64_t T, int M, int k, int renorm,
@@ -208,9 +178,8 @@ void router_scalar_backward(const float* probs, const float* lse_r, const float*
 }
 
 void normed_grad(const float* h, const int32_t* hrow, const float* gain, const float* router,
-                 const float* inv_rms, const int32_t* slot_row, const float* dxp, int64_t T,
-                 int64_t d, int M, int k, const float* glog, float* gnormed, float* dot_part,
-                 float* gh, cudaStream_t s) {
+                 const int32_t* slot_row, const float* dxp, int64_t T, int64_t d, int M, int k,
+                 const float* glog, float* gnormed, float* dot_part, cudaStream_t s) {
     const dim3 g2(static_cast<unsigned>((T + NG_TT - 1) / NG_TT), static_cast<unsigned>(d / NG_QT));
     auto f = M <= 8    ? normed_grad_k<8>
              : M <= 16 ? normed_grad_k<16>
@@ -219,24 +188,6 @@ void normed_grad(const float* h, const int32_t* hrow, const float* gain, const f
     f<<<g2, 256, 0, s>>>(h, hrow, gain, router, glog, slot_row, dxp, (int)T, (int)d, M, k, gnormed,
                          dot_part);
     count_launch();
-    if (gh) {
-        const unsigned g3 = static_cast<unsigned>((T + 7) / 8);
-        rmsnorm_bwd_k<<<g3, 256, 0, s>>>(h, hrow, gain, inv_rms, gnormed, dot_part, (int)T, (int)d, gh);
-        count_launch();
-    }
-}
-
-void router_backward(const float* h, const int32_t* hrow, const float* gain, const float* router,
-                     const float* probs,
-                     const float* lse_r, const float* inv_rms, const float* denom,
-                     const int32_t* topk_idx, const int32_t* slot_row, const float* gw_row,
-                     const float* dxp, const float* lb_coeff, int64_t T, int64_t d, int M, int k,
-                     int renorm, float g_lbsum, float g_s, float* glog, float* gnormed,
-                     float* dot_part, float* gh, cudaStream_t s) {
-    router_scalar_backward(probs, lse_r, denom, topk_idx, slot_row, gw_row, lb_coeff, T, M, k,
-                           renorm, g_lbsum, g_s, glog, s);
-    normed_grad(h, hrow, gain, router, inv_rms, slot_row, dxp, T, d, M, k, glog, gnormed, dot_part,
-                gh, s);
 }
 
 }  // namespace spes_k
