@@ -215,6 +215,19 @@ def adamw_roofline(fam, node, hbm_peak):
                     "reaches ~6.1 TB/s on this GPU (tools/stream_bench.cu)"}
 
 
+def sync_roofline(st, N):
+    """The last round's sparse sync on this rank: inbound bytes (psi copies + expert copies
+    read over NVLink / received over NCCL) over its device time, against the 900 GB/s per
+    direction NVLink 5 gives each B200."""
+    if not st or N < 2 or not st.get("ms"):
+        return None
+    b = float(st["psi_bytes_in"]) + float(st["expert_bytes_in"])
+    gbs = b / (st["ms"] / 1e3) / 1e9
+    return {"bound": "nvlink", "ms": st["ms"], "bytes_in": b, "achieved": gbs, "peak": 900.0,
+            "unit": "GB/s", "frac": gbs / 900.0,
+            "note": "rank 0; ms includes the owner means, barriers and operand-copy writes"}
+
+
 def ncu_traffic():
     """dram bytes per launch of the grouped GEMM from the committed ncu --set full summary."""
     try:
@@ -329,6 +342,7 @@ def our_arm(args):
     stream = torch.cuda.ExternalStream(node.stream(), device=f"cuda:{local}")
 
     round_no = [0]
+    last_sync = [None]
 
     def spes_round(host=False):
         node.round_begin()
@@ -337,7 +351,7 @@ def our_arm(args):
                 node.local_step(toks_host[h], opt)  # H2D tokens + D2H losses every step
             else:
                 node.local_step_device(ptrs[h], B, S, opt)
-        node.sync()
+        last_sync[0] = node.sync()
         if merge:
             node.merge_model(sched, round_no[0])
         round_no[0] += 1
@@ -441,6 +455,7 @@ def our_arm(args):
                                f"{args.prof_rounds} profiled round(s) right after the timed "
                                "region (the timed region itself runs unprofiled)"},
         "roofline_hbm": adamw_roofline(fam, node, hbm),
+        "sync": sync_roofline(last_sync[0], N),
         "kernels_ms": {k: round(v[0], 4) for k, v in fam.items()},
         "clocks": clocks,
     }
