@@ -969,34 +969,42 @@ __global__ void __launch_bounds__(64) embed_grad_sum_k(const int32_t* __restrict
                                                        const int32_t* __restrict__ list,
                                                        const float* __restrict__ gh0, int64_t d,
                                                        float* __restrict__ g_emb) {
+    // this id's token list staged in smem once (coalesced), then EU rows in flight per pass
+    constexpr int LCAP = 1024, EU = 16;
+    __shared__ int32_t sl[LCAP];
     const int v = blockIdx.x;
     const int64_t q = (static_cast<int64_t>(blockIdx.y) * 64 + threadIdx.x) * 4;
-    if (q >= d) return;
     const int32_t i0 = off[v], i1 = off[v + 1];
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    int32_t i = i0;
-    constexpr int EU = 16;  // rows in flight
-    for (; i + EU <= i1; i += EU) {
-        float4 g[EU];
+    for (int32_t c0 = i0; c0 < i1; c0 += LCAP) {
+        const int32_t c1 = min(i1, c0 + LCAP);
+        __syncthreads();
+        for (int32_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) sl[i - c0] = list[i];
+        __syncthreads();
+        if (q >= d) continue;
+        int32_t i = c0;
+        for (; i + EU <= c1; i += EU) {
+            float4 g[EU];
 #pragma unroll
-        for (int u = 0; u < EU; ++u)
-            g[u] = __ldg(reinterpret_cast<const float4*>(gh0 + static_cast<int64_t>(list[i + u]) * d + q));
+            for (int u = 0; u < EU; ++u)
+                g[u] = __ldg(reinterpret_cast<const float4*>(gh0 + static_cast<int64_t>(sl[i - c0 + u]) * d + q));
 #pragma unroll
-        for (int u = 0; u < EU; ++u) {
-            acc.x = fadd(acc.x, g[u].x);
-            acc.y = fadd(acc.y, g[u].y);
-            acc.z = fadd(acc.z, g[u].z);
-            acc.w = fadd(acc.w, g[u].w);
+            for (int u = 0; u < EU; ++u) {
+                acc.x = fadd(acc.x, g[u].x);
+                acc.y = fadd(acc.y, g[u].y);
+                acc.z = fadd(acc.z, g[u].z);
+                acc.w = fadd(acc.w, g[u].w);
+            }
+        }
+        for (; i < c1; ++i) {
+            const float4 g = __ldg(reinterpret_cast<const float4*>(gh0 + static_cast<int64_t>(sl[i - c0]) * d + q));
+            acc.x = fadd(acc.x, g.x);
+            acc.y = fadd(acc.y, g.y);
+            acc.z = fadd(acc.z, g.z);
+            acc.w = fadd(acc.w, g.w);
         }
     }
-    for (; i < i1; ++i) {
-        const float4 g = __ldg(reinterpret_cast<const float4*>(gh0 + static_cast<int64_t>(list[i]) * d + q));
-        acc.x = fadd(acc.x, g.x);
-        acc.y = fadd(acc.y, g.y);
-        acc.z = fadd(acc.z, g.z);
-        acc.w = fadd(acc.w, g.w);
-    }
-    *reinterpret_cast<float4*>(g_emb + static_cast<int64_t>(v) * d + q) = acc;
+    if (q < d) *reinterpret_cast<float4*>(g_emb + static_cast<int64_t>(v) * d + q) = acc;
 }
 
 bool embed_grad_plan(const int32_t* inputs, int64_t T, int64_t V, int32_t* scratch,
