@@ -48,11 +48,30 @@ __global__ void embed_gather_k(const float* __restrict__ emb, const int32_t* __r
     for (int64_t q = threadIdx.x; q < d / 4; q += blockDim.x) dst[q] = __ldg(src + q);
 }
 
+// inputs / targets only (layer 0 reads emb[inputs] in place): a thread per token
+__global__ void split_tokens_k(const int32_t* __restrict__ tokens, int64_t T, int64_t S, int64_t V,
+                               int32_t* __restrict__ inputs, int32_t* __restrict__ targets,
+                               int32_t* err) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    const int64_t b = t / S, s = t % S;
+    const int32_t tin = tokens[b * (S + 1) + s], tout = tokens[b * (S + 1) + s + 1];
+    const bool bad = tin < 0 || tin >= V || tout < 0 || tout >= V;
+    inputs[t] = bad ? 0 : tin;
+    targets[t] = bad ? 0 : tout;
+    if (bad) atomicExch(err, 1);
+}
+
 void embed_gather(const float* emb, const int32_t* tokens, int64_t B, int64_t S, int64_t d,
                   int64_t V, float* h, int32_t* inputs, int32_t* targets, int32_t* err,
                   cudaStream_t s) {
-    embed_gather_k<<<static_cast<unsigned>(B * S), 128, 0, s>>>(emb, tokens, S, d, V, h, inputs,
-                                                                targets, err);
+    if (!h) {
+        split_tokens_k<<<static_cast<unsigned>(cdiv(B * S, 256)), 256, 0, s>>>(
+            tokens, B * S, S, V, inputs, targets, err);
+    } else {
+        embed_gather_k<<<static_cast<unsigned>(B * S), 128, 0, s>>>(emb, tokens, S, d, V, h,
+                                                                    inputs, targets, err);
+    }
     count_launch();
 }
 
