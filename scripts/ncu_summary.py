@@ -2,7 +2,7 @@
 
   python scripts/ncu_summary.py launches gpurun_out/launches.csv profiles/r01/ncu_launches_step.txt profiles/ncu_gemm_summary.json
       ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv
-      launch list -> the last local step's launches (embed_gather_k .. the step's last
+      launch list -> the last local step's launches (split_tokens_k .. the step's last
       adamw_k), per-launch time / share / DRAM bytes, and the expert-GEMM DRAM bytes that
       bench.py reports as roofline.traffic
   python scripts/ncu_summary.py full gpurun_out/prof.ncu-rep profiles/r01/ncu_full_top_kernels.txt
@@ -35,9 +35,12 @@ def launches(csv_path, out_txt, out_json, cmd):
                      "Gbyte": 1e9, "GB": 1e9}[unit]
             e[r["Metric Name"]] = v * scale
     seq = [by_id[i] for i in sorted(by_id)]
-    starts = [i for i, e in enumerate(seq) if "embed_gather_k" in e["name"]]
+    # a step starts with the token split (layer 0 reads the embedding in place) or the
+    # embedding gather
+    starts = [i for i, e in enumerate(seq)
+              if "split_tokens_k" in e["name"] or "embed_gather_k" in e["name"]]
     if not starts:
-        sys.exit("no embed_gather_k launch in the list")
+        sys.exit("no split_tokens_k / embed_gather_k launch in the list")
     s0 = starts[-1]
     ends = [i for i in range(s0, len(seq)) if "adamw_k" in seq[i]["name"]]
     step = seq[s0:ends[-1] + 1] if ends else seq[s0:]
