@@ -267,7 +267,12 @@ spes_status spes_read_checkpoint(spes_ctx* ctx, const char* path, uint64_t* roun
 /* Counters: optimizer-state scalars (2(|psi|+|Phi_i|)), gradient scalars, step count. */
 spes_status spes_counts(spes_ctx* ctx, int64_t* opt_state_scalars, int64_t* grad_scalars,
                         int64_t* adam_step);
-/* Read a named device buffer of the last step (see DESIGN.md §debug names). */
+/* Read a named device buffer of the last step into host (bytes >= the buffer's size):
+ *   "h" (layer l's input; layer 0 rebuilt from the current embedding), "logits", "probs",
+ *   "topk_idx", "topk_w", "counts", "pad_off", "row_token", "slot_row", "perm", "y",
+ *   "grad_h0" (gradient w.r.t. the layer-0 input), "head_logits" (V != 256 only),
+ *   "w1" / "w2" (layer l's bf16 expert operand copies: [M][d][2f] gate|up interleaved in
+ *   128-column blocks, [M][f][d]). Unknown names: invalid_argument. */
 spes_status spes_debug_read(spes_ctx* ctx, const char* name, int32_t layer, void* host,
                             int64_t bytes);
 /* Gradient of the last step, full parameter layout (zeros for frozen blocks). Needs the
