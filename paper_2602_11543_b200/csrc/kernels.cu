@@ -719,13 +719,37 @@ constexpr int NRG_EG = 16;
 // (kernels.hpp:130-152; the dot from normed_grad's slab partials, summed in slab order):
 // h.grad += (gy*g)*inv - coef*x, so h and gnormed
 // are streamed once for both.
+// Operand streaming: each thread prefetches its own tokens' x / gnormed / gh float4s through a
+// per-thread cp.async ring (NRG_S stages: a token's three rows are one commit group), so the
+// loads of the next NRG_S - 1 tokens are in flight while this one is processed; the 64-token
+// batch's glog, dot partials and inv_rms are staged one batch ahead (4-byte cp.async, double
+// buffered). Only the issuing thread reads a ring slot, so the ring needs no barrier; the
+// batch staging needs one per batch. Arithmetic and its order are those of the plain loop.
+constexpr int NRG_S = 4;
+constexpr int NRG_NP_SMEM = 32;  // dot partials per token staged in smem (d <= 4096)
+__device__ __forceinline__ void cp_async16_nr(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async4_nr(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_nr() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+
 __global__ void __launch_bounds__(256) norm_router_partial_k(
     const float* __restrict__ h, const int32_t* __restrict__ hrow,
     const float* __restrict__ gain, const float* __restrict__ gnormed,
     const float* __restrict__ glog, const float* __restrict__ inv_rms, int T, int d, int M,
     float* __restrict__ partial, const float* __restrict__ dot_part, float* __restrict__ gh) {
-    __shared__ __align__(16) float sgl[64][NRG_EG];
-    __shared__ float scoef[64];
+    extern __shared__ __align__(16) float4 ring[];  // [NRG_S][3][256]
+    __shared__ __align__(16) float sgl[2][64][NRG_EG];
+    __shared__ float sinv[2][64];
+    __shared__ float sdot[2][64 * NRG_NP_SMEM];  // larger d reads dot_part directly
     __shared__ float red[32][4][NRG_EG + 1];
     const int ph = threadIdx.x >> 5, tx = threadIdx.x & 31;
     const int q = blockIdx.x * 128 + 4 * tx;
@@ -733,8 +757,13 @@ __global__ void __launch_bounds__(256) norm_router_partial_k(
     const int e0 = blockIdx.z * NRG_EG;
     const int ne = min(NRG_EG, M - e0);
     const bool do_gain = blockIdx.z == 0;
+    const bool do_rms = gh != nullptr && do_gain;
+    const int np = d / NG_QT_RMS;
+    const bool dot_smem = np <= NRG_NP_SMEM;
     const int per = (T + NRG_TC - 1) / NRG_TC;
     const int t0 = chunk * per, t1 = min(T, t0 + per);
+    const int nbatch = t1 > t0 ? (t1 - t0 + 63) / 64 : 0;
+    const int nseq = nbatch * 8;  // this thread's token slots: batch s/8, token ph + 8*(s%8)
     float gg[4] = {0.f, 0.f, 0.f, 0.f};
     float gr[4][NRG_EG];
 #pragma unroll
@@ -742,23 +771,81 @@ __global__ void __launch_bounds__(256) norm_router_partial_k(
 #pragma unroll
         for (int e = 0; e < NRG_EG; ++e) gr[j][e] = 0.f;
     const float4 gq = __ldg(reinterpret_cast<const float4*>(gain + q));
-    for (int tb = t0; tb < t1; tb += 64) {
-        __syncthreads();
+
+    auto slot_token = [&](int s) { return t0 + 64 * (s >> 3) + ph + 8 * (s & 7); };
+    // h row of slot s (the embedding row when layer 0 reads it in place)
+    auto slot_row = [&](int s) {
+        const int t = slot_token(s);
+        return (hrow && s < nseq && t < t1) ? __ldg(hrow + t) : t;
+    };
+    auto issue = [&](int s, int xr) {
+        if (s < nseq) {
+            const int t = slot_token(s);
+            if (t < t1) {
+                float4* st = ring + (s % NRG_S) * 3 * 256;
+                const int64_t o = static_cast<int64_t>(t) * d + q;
+                const int64_t xo = static_cast<int64_t>(xr) * d + q;
+                cp_async16_nr(st + threadIdx.x, h + xo);
+                if (do_gain) cp_async16_nr(st + 256 + threadIdx.x, gnormed + o);
+                if (do_rms) cp_async16_nr(st + 512 + threadIdx.x, gh + o);
+            }
+        }
+        cp_async_commit_nr();
+    };
+    auto stage_batch = [&](int b) {  // glog / inv_rms / dot partials of batch b
+        if (b >= nbatch) return;
+        const int tb = t0 + 64 * b, buf = b & 1;
         for (int i = threadIdx.x; i < 64 * NRG_EG; i += blockDim.x) {
             const int tt = i / NRG_EG, e = i % NRG_EG;
-            sgl[tt][e] = (tb + tt < t1 && e < ne) ? glog[static_cast<int64_t>(tb + tt) * M + e0 + e] : 0.f;
+            if (tb + tt < t1 && e < ne)
+                cp_async4_nr(&sgl[buf][tt][e], glog + static_cast<int64_t>(tb + tt) * M + e0 + e);
+            else
+                sgl[buf][tt][e] = 0.f;
         }
-        if (gh && do_gain && threadIdx.x < 64 && tb + threadIdx.x < t1) {
-            const int t = tb + threadIdx.x;
-            const int np = d / NG_QT_RMS;
-            float dot2 = 0.f;
-            for (int i = 0; i < np; ++i) dot2 += dot_part[static_cast<int64_t>(t) * np + i];
-            const float inv = inv_rms[t];
-            scoef[threadIdx.x] = fdiv(fmul(fmul(fmul(dot2, inv), inv), inv), static_cast<float>(d));
-        }
+        if (threadIdx.x < 64 && tb + threadIdx.x < t1) cp_async4_nr(&sinv[buf][threadIdx.x], inv_rms + tb + threadIdx.x);
+        if (do_rms && dot_smem)
+            for (int i = threadIdx.x; i < 64 * np; i += blockDim.x)
+                if (tb + i / np < t1)
+                    cp_async4_nr(&sdot[buf][i], dot_part + static_cast<int64_t>(tb) * np + i);
+    };
+
+    stage_batch(0);
+    cp_async_commit_nr();
+#pragma unroll
+    for (int s = 0; s < NRG_S - 1; ++s) issue(s, slot_row(s));
+    int xr_next = slot_row(NRG_S - 1);  // row index loaded one slot ahead of its issue
+    for (int b = 0; b < nbatch; ++b) {
+        // batch b's staging went out with slot 8b - 8 + NRG_S - 1 (batch 0's is the first
+        // group); all but the newest NRG_S - 1 groups complete covers it
+        asm volatile("cp.async.wait_group %0;" ::"n"(NRG_S - 1) : "memory");
         __syncthreads();
-        // two tokens per iteration (tt, tt + 8): both tokens' loads are in flight together
-        auto process = [&](int tt, const float4& xv, const float4& gv, float4 ov, float iv) {
+        stage_batch(b + 1);  // buffer (b+1)&1 was last read in batch b - 1
+        const int buf = b & 1;
+        const int tb = t0 + 64 * b;
+        // lane l < 8 forms the rmsnorm coefficient of this warp's token ph + 8l; the token
+        // loop picks it up by shuffle
+        float lane_coef = 0.f;
+        if (do_rms && tx < 8 && tb + ph + 8 * tx < t1) {
+            const int tt = ph + 8 * tx;
+            float dot2 = 0.f;
+            if (dot_smem)
+                for (int i = 0; i < np; ++i) dot2 += sdot[buf][tt * np + i];
+            else
+                for (int i = 0; i < np; ++i) dot2 += dot_part[static_cast<int64_t>(tb + tt) * np + i];
+            const float iv = sinv[buf][tt];
+            lane_coef = fdiv(fmul(fmul(fmul(dot2, iv), iv), iv), static_cast<float>(d));
+        }
+#pragma unroll 1
+        for (int j = 0; j < 8; ++j) {
+            const int s = 8 * b + j;
+            issue(s + NRG_S - 1, xr_next);  // batch b+1's staging rides in the j == 0 group
+            xr_next = slot_row(s + NRG_S);
+            asm volatile("cp.async.wait_group %0;" ::"n"(NRG_S - 1) : "memory");
+            const int tt = ph + 8 * j;
+            if (tb + tt >= t1) continue;
+            const float4* st = ring + (s % NRG_S) * 3 * 256;
+            const float4 xv = st[threadIdx.x];
+            const float iv = sinv[buf][tt];
             // normed exactly as the forward formed it: (x * inv) * g
             float4 nv;
             nv.x = fmul(fmul(xv.x, iv), gq.x);
@@ -766,8 +853,10 @@ __global__ void __launch_bounds__(256) norm_router_partial_k(
             nv.z = fmul(fmul(xv.z, iv), gq.z);
             nv.w = fmul(fmul(xv.w, iv), gq.w);
             if (do_gain) {
-                if (gh) {  // rmsnorm backward (kernels.hpp:130-152)
-                    const float coef = scoef[tt];
+                const float4 gv = st[256 + threadIdx.x];
+                if (do_rms) {  // rmsnorm backward (kernels.hpp:130-152)
+                    const float coef = __shfl_sync(0xffffffffu, lane_coef, j);
+                    float4 ov = st[512 + threadIdx.x];
                     ov.x = fadd(ov.x, fsub(fmul(fmul(gv.x, gq.x), iv), fmul(coef, xv.x)));
                     ov.y = fadd(ov.y, fsub(fmul(fmul(gv.y, gq.y), iv), fmul(coef, xv.y)));
                     ov.z = fadd(ov.z, fsub(fmul(fmul(gv.z, gq.z), iv), fmul(coef, xv.z)));
@@ -782,39 +871,16 @@ __global__ void __launch_bounds__(256) norm_router_partial_k(
             const float n[4] = {nv.x, nv.y, nv.z, nv.w};
 #pragma unroll
             for (int e4 = 0; e4 < NRG_EG; e4 += 4) {
-                const float4 g4 = *reinterpret_cast<const float4*>(&sgl[tt][e4]);
+                const float4 g4 = *reinterpret_cast<const float4*>(&sgl[buf][tt][e4]);
                 const float g[4] = {g4.x, g4.y, g4.z, g4.w};
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
+                for (int jj = 0; jj < 4; ++jj)
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) gr[j][e4 + u] += n[j] * g[u];
+                    for (int u = 0; u < 4; ++u) gr[jj][e4 + u] += n[jj] * g[u];
             }
-        };
-        const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int tt = ph; tt < 64 && tb + tt < t1; tt += 16) {
-            const int tt2 = tt + 8;
-            const bool v2 = tt2 < 64 && tb + tt2 < t1;
-            const int64_t o1 = static_cast<int64_t>(tb + tt) * d + q;
-            const int64_t o2 = static_cast<int64_t>(tb + (v2 ? tt2 : tt)) * d + q;
-            const int64_t xo1 = hrow ? static_cast<int64_t>(hrow[tb + tt]) * d + q : o1;
-            const int64_t xo2 = hrow ? static_cast<int64_t>(hrow[tb + (v2 ? tt2 : tt)]) * d + q : o2;
-            const float4 x1 = __ldg(reinterpret_cast<const float4*>(h + xo1));
-            const float4 x2 = __ldg(reinterpret_cast<const float4*>(h + xo2));
-            const float i1 = __ldg(inv_rms + tb + tt);
-            const float i2 = __ldg(inv_rms + tb + (v2 ? tt2 : tt));
-            float4 g1 = z4, g2 = z4, h1 = z4, h2 = z4;
-            if (do_gain) {
-                g1 = __ldg(reinterpret_cast<const float4*>(gnormed + o1));
-                g2 = __ldg(reinterpret_cast<const float4*>(gnormed + o2));
-                if (gh) {
-                    h1 = *reinterpret_cast<const float4*>(gh + o1);
-                    h2 = *reinterpret_cast<const float4*>(gh + o2);
-                }
-            }
-            process(tt, x1, g1, h1, i1);
-            if (v2) process(tt2, x2, g2, h2, i2);
         }
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     // combine the 8 warps in warp order (fixed), then write this chunk's partial
     for (int w = 0; w < 8; ++w) {
         __syncthreads();
@@ -861,7 +927,13 @@ void norm_router_grads(const float* h, const int32_t* hrow, const float* gain, c
                        float* partial, float* g_gain, float* g_router, const float* dot_part,
                        float* gh, cudaStream_t s) {
     dim3 grid(static_cast<unsigned>(d / 128), NRG_TC, static_cast<unsigned>((M + NRG_EG - 1) / NRG_EG));
-    norm_router_partial_k<<<grid, 256, 0, s>>>(h, hrow, gain, gnormed, glog, inv_rms, (int)T, (int)d, M,
+    constexpr int ring_bytes = NRG_S * 3 * 256 * 16;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(norm_router_partial_k, cudaFuncAttributeMaxDynamicSharedMemorySize, ring_bytes);
+        attr_set = true;
+    }
+    norm_router_partial_k<<<grid, 256, ring_bytes, s>>>(h, hrow, gain, gnormed, glog, inv_rms, (int)T, (int)d, M,
                                                partial, dot_part, gh);
     const int64_t n = d * (M + 1);
     norm_router_finish_k<<<static_cast<unsigned>(cdiv(n, 256)), 256, 0, s>>>(partial, (int)d, M,

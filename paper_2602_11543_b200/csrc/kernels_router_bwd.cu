@@ -86,21 +86,37 @@ __global__ void __launch_bounds__(256) normed_grad_k(
     const float* __restrict__ glog, const int32_t* __restrict__ slot_row,
     const float* __restrict__ dxp, int T, int d, int M, int k, float* __restrict__ gnormed,
     float* __restrict__ dot_part) {
-    __shared__ __align__(16) float sRT[MAXM][NG_QT];  // router tile, transposed: [e][q]
+    // router tile, transposed: [e][q]; pitch NG_QT + 4 makes the staging stores 2-way
+    // instead of 16-way bank conflicts (float4 reads stay aligned and conflict-free)
+    __shared__ __align__(16) float sRT[MAXM][NG_QT + 4];
     __shared__ float sG[NG_TT][MAXM];
     __shared__ int32_t sRow[NG_TT][8];
     const int t0 = blockIdx.x * NG_TT, q0 = blockIdx.y * NG_QT;
-    for (int i = threadIdx.x; i < NG_QT * M; i += blockDim.x) {
-        const int qq = i / M, e = i % M;
-        sRT[e][qq] = __ldg(R + static_cast<int64_t>(q0 + qq) * M + e);
-    }
-    for (int i = threadIdx.x; i < NG_TT * M; i += blockDim.x) {
-        const int tt = i / M, e = i % M;
-        sG[tt][e] = (t0 + tt < T) ? glog[static_cast<int64_t>(t0 + tt) * M + e] : 0.f;
-    }
-    for (int i = threadIdx.x; i < NG_TT * k; i += blockDim.x) {
-        const int tt = i / k, s = i % k;
-        sRow[tt][s] = (t0 + tt < T) ? slot_row[static_cast<int64_t>(t0 + tt) * k + s] : 0;
+    // the tile's router rows [q0, q0 + 128) x M and glog rows [t0, t0 + 32) x M are contiguous;
+    // power-of-two M and k (every shipped config) index them by shifts, not integer division
+    if ((M & (M - 1)) == 0 && (k & (k - 1)) == 0) {
+        const int lm = __ffs(M) - 1, lk = __ffs(k) - 1;
+        const float* Rt = R + static_cast<int64_t>(q0) * M;
+        for (int i = threadIdx.x; i < NG_QT * M; i += blockDim.x) sRT[i & (M - 1)][i >> lm] = __ldg(Rt + i);
+        const float* Gt = glog + static_cast<int64_t>(t0) * M;
+        for (int i = threadIdx.x; i < NG_TT * M; i += blockDim.x)
+            sG[i >> lm][i & (M - 1)] = (t0 + (i >> lm) < T) ? Gt[i] : 0.f;
+        const int32_t* St = slot_row + static_cast<int64_t>(t0) * k;
+        for (int i = threadIdx.x; i < NG_TT * k; i += blockDim.x)
+            sRow[i >> lk][i & (k - 1)] = (t0 + (i >> lk) < T) ? St[i] : 0;
+    } else {
+        for (int i = threadIdx.x; i < NG_QT * M; i += blockDim.x) {
+            const int qq = i / M, e = i % M;
+            sRT[e][qq] = __ldg(R + static_cast<int64_t>(q0 + qq) * M + e);
+        }
+        for (int i = threadIdx.x; i < NG_TT * M; i += blockDim.x) {
+            const int tt = i / M, e = i % M;
+            sG[tt][e] = (t0 + tt < T) ? glog[static_cast<int64_t>(t0 + tt) * M + e] : 0.f;
+        }
+        for (int i = threadIdx.x; i < NG_TT * k; i += blockDim.x) {
+            const int tt = i / k, s = i % k;
+            sRow[tt][s] = (t0 + tt < T) ? slot_row[static_cast<int64_t>(t0 + tt) * k + s] : 0;
+        }
     }
     __syncthreads();
     const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
@@ -137,16 +153,14 @@ __global__ void __launch_bounds__(256) normed_grad_k(
         if (t >= T) break;
         // expert dX rows in descending expert order (select_rows backward, j descending)
         float a[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int s = 7; s >= 0; --s) {
-            if (s < k) {
-                const float4 v = __ldg(reinterpret_cast<const float4*>(
-                    dxp + static_cast<int64_t>(sRow[tt][s]) * d + q0 + 4 * tx));
-                a[0] = fadd(a[0], v.x);
-                a[1] = fadd(a[1], v.y);
-                a[2] = fadd(a[2], v.z);
-                a[3] = fadd(a[3], v.w);
-            }
+        const float* dxc = dxp + q0 + 4 * tx;
+#pragma unroll 2
+        for (int s = k - 1; s >= 0; --s) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(dxc + static_cast<int64_t>(sRow[tt][s]) * d));
+            a[0] = fadd(a[0], v.x);
+            a[1] = fadd(a[1], v.y);
+            a[2] = fadd(a[2], v.z);
+            a[3] = fadd(a[3], v.w);
         }
         const int64_t xr_t = hrow ? static_cast<int64_t>(hrow[t]) : t;
         const float4 xv = __ldg(reinterpret_cast<const float4*>(h + xr_t * d + q0 + 4 * tx));
