@@ -134,11 +134,11 @@ __global__ void route_scan_k(int32_t* __restrict__ chunk_counts, int nchunks, in
     __shared__ int32_t s_nt[6][64];
     __shared__ GemmGroup s_g[6][64];
     const int64_t d = gb.d, f = gb.f;
-    if (j < M) {
-        const int e = j;
+    if (j < 6 * M) {  // thread (g, e) builds expert e's group of GEMM g
+        const int g = j / M, e = j % M;
         const int32_t mt = (s_off[e + 1] - s_off[e]) / gb.tile_rows;
         const int64_t goff = gb.grad_off_layer ? gb.grad_off_layer[e] : -1;
-        for (int g = 0; g < 6; ++g) {
+        {
             GemmGroup G{};
             G.bk0 = 0;
             G.out_row0 = s_off[e];
@@ -228,12 +228,12 @@ __global__ void route_scan_k(int32_t* __restrict__ chunk_counts, int nchunks, in
         tiles[j] = acc;
     }
     __syncthreads();
-    if (j < M)
-        for (int g = 0; g < 6; ++g) {
-            GemmGroup G = s_g[g][j];
-            G.tile_start = s_nt[g][j];
-            groups[g * M + j] = G;
-        }
+    if (j < 6 * M) {
+        const int g = j / M, e = j % M;
+        GemmGroup G = s_g[g][e];
+        G.tile_start = s_nt[g][e];
+        groups[g * M + e] = G;
+    }
 }
 
 // Stable scatter: rows of expert j in ascending token order (model.hpp:314-318).
@@ -296,7 +296,8 @@ void route_plan(const int32_t* topk_idx, const float* topk_w, int64_t T, int M, 
     if (scan_smem > 16 * 1024)
         cudaFuncSetAttribute(route_scan_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(scan_smem));
-    route_scan_k<<<1, 64, scan_smem, s>>>(
+    const int scan_threads = std::max(64, (6 * M + 31) / 32 * 32);  // one per (GEMM, expert)
+    route_scan_k<<<1, scan_threads, scan_smem, s>>>(
         p.chunk_counts, nchunks, (int)T, M, k, p.counts, p.pad_off,
                                   p.lb_coeff, p.groups, p.tiles, gb);
     cudaMemsetAsync(p.row_token, 0xFF, sizeof(int32_t) * R_cap, s);
