@@ -246,6 +246,13 @@ def test_local_step_cfg4_shapes(gpu):
     _check_step(model_cfg(**CFG4), B=1, S=256, owned=list(range(16)), seed=35)
 
 
+def test_local_step_non_pow2_experts(gpu):
+    # M = 6, k = 3: the integer-division staging paths of the router / norm-gradient kernels
+    # (every shipped config has power-of-two M and k, which index by shifts)
+    _check_step(model_cfg(vocab=256, hidden=128, intermediate=256, layers=2, experts_total=6,
+                          experts_active=3), B=2, S=80, owned=[1, 4, 5], seed=45)
+
+
 def test_local_step_ragged_T(gpu):
     # T not a multiple of 128, an owned expert that may receive no tokens
     _check_step(model_cfg(**CFG1), B=3, S=37, owned=[0, 7], seed=40)
