@@ -130,6 +130,9 @@ spes_status spes_set_ownership(spes_ctx* ctx, const int32_t* node_offsets,
 /* Full fp32 parameter vector in enumerate_blocks order (host memory). */
 spes_status spes_load_params(spes_ctx* ctx, const float* host, int64_t n);
 spes_status spes_read_params(spes_ctx* ctx, float* host, int64_t n);
+/* Same as spes_load_params from a device buffer of this context's GPU (e.g. a model
+ * initialized on the device; no host round trip for multi-GB models). */
+spes_status spes_load_params_device(spes_ctx* ctx, const float* dev, int64_t n);
 
 /* Start a local round: fresh MaskedAdamW state (trainer.hpp:151-156) unless carry_state. */
 spes_status spes_round_begin(spes_ctx* ctx, int32_t carry_state);
@@ -283,6 +286,11 @@ spes_status spes_read_grads(spes_ctx* ctx, float* host, int64_t n);
  * logic_error). 0 (default): gradients are materialized and one standalone optimizer
  * pass runs after the backward. Both give identical bits. */
 spes_status spes_set_fused_optimizer(spes_ctx* ctx, int32_t on);
+/* Inner optimizer of the local steps (LocalRoundConfig::inner, trainer.hpp:116-121):
+ * 0 = MaskedAdamW (default), 1 = SGD (theta -= float(lr) * g on the trainable blocks,
+ * trainer.hpp:197-204; no optimizer state, the fused placement does not apply).
+ * invalid_argument for other kinds. */
+spes_status spes_set_inner_optimizer(spes_ctx* ctx, int32_t kind);
 /* Stream layout of the local step. 1 (default): off-critical-path work (embedding-gradient
  * bucketing, loss scalars, the router's scalar backward, the owned experts' AdamW) runs on
  * a low-priority second stream beside the GEMMs; 0: one stream. Identical bits either way. */

@@ -9,6 +9,7 @@
 //   Server::aggregate (proj/src/protocol.cpp:197-251; collective here: every node calls)
 #pragma once
 
+#include <cmath>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -134,16 +135,18 @@ inline void unflatten(const std::vector<float>& flat, spes::ModelParams& p) {
     }
 }
 
-// Drop-in for spes::local_round (trainer.hpp:143-222) with AdamW inner steps.
+// Drop-in for spes::local_round (trainer.hpp:143-222): the H steps run on the device (one
+// spes_local_step per batch, each with its own (B, S)); inner optimizer AdamW (fresh state
+// per call unless carry_state) or SGD (trainer.hpp:197-204). record_trace (trainer.hpp:
+// 183-219) reads each step's gradients and parameters back and forms the same statistics
+// on the host in the reference's order: update_norms = sqrt(sum over trainable blocks of
+// double(g)^2), grad_sum = per trainable block float sum over steps, drift_sq = sum over
+// all blocks of (double(theta) - double(theta_global))^2.
 inline spes::LocalRoundResult local_round(Context& ctx, const spes::ModelParams& global,
                                           const spes::BatchProvider& next_batch,
                                           const spes::LocalRoundConfig& cfg,
                                           const spes::TrainMask& mask, bool carry_state = false) {
     if (cfg.steps < 1) throw std::invalid_argument("local_round: need H >= 1");
-    if (cfg.inner != spes::InnerOpt::AdamW)
-        throw std::logic_error("b200 local_round: only the AdamW inner optimizer is on the B200 path");
-    if (cfg.record_trace)
-        throw std::logic_error("b200 local_round: record_trace is not on the B200 path");
     // The TrainMask must be this node's row of the context's ownership map (the map is
     // global because the sparse sync needs every node's owner set). A single-node
     // context adopts the mask as its map.
@@ -154,24 +157,67 @@ inline spes::LocalRoundResult local_round(Context& ctx, const spes::ModelParams&
     else if (ctx.ownership().empty() ||
              ctx.ownership()[static_cast<size_t>(ctx.node())] != mask.owned_experts)
         throw std::invalid_argument("b200 local_round: mask differs from the context's ownership map");
-    ctx.load(flatten(global));
-    std::vector<int32_t> tokens;
-    int64_t B = 0, S = 0;
-    std::vector<double> lr;
-    for (int h = 0; h < cfg.steps; ++h) {
-        spes::Batch b = next_batch();
-        B = b.batch;
-        S = b.seq;
-        tokens.insert(tokens.end(), b.tokens.begin(), b.tokens.end());
-        lr.push_back(cfg.lr_at ? cfg.lr_at(cfg.first_step + h) : cfg.opt.lr);
+    const bool sgd = cfg.inner == spes::InnerOpt::SGD;
+    check(spes_set_inner_optimizer(ctx.get(), sgd ? 1 : 0));
+    if (cfg.record_trace) check(spes_set_fused_optimizer(ctx.get(), 0));  // gradients readable
+    const std::vector<float> theta0 = flatten(global);
+    ctx.load(theta0);
+    check(spes_round_begin(ctx.get(), carry_state ? 1 : 0));
+    const auto blocks = spes::enumerate_blocks(global.config);
+    std::vector<size_t> offs;  // flat offset of every block
+    {
+        size_t o = 0;
+        for (const auto& b : blocks) {
+            offs.push_back(o);
+            o += static_cast<size_t>(spes::block_tensor(global, b).numel());
+        }
     }
-    spes_adamw_cfg opt{cfg.opt.lr, cfg.opt.beta1, cfg.opt.beta2, cfg.opt.eps,
-                       cfg.opt.weight_decay};
-    auto losses = ctx.local_round(tokens, B, S, cfg.steps, lr, opt, carry_state);
     spes::LocalRoundResult res;
     res.params = global;
+    spes_adamw_cfg opt{cfg.opt.lr, cfg.opt.beta1, cfg.opt.beta2, cfg.opt.eps,
+                       cfg.opt.weight_decay};
+    std::vector<float> g(theta0.size());
+    for (int h = 0; h < cfg.steps; ++h) {
+        if (cfg.lr_at) opt.lr = cfg.lr_at(cfg.first_step + h);
+        spes::Batch b = next_batch();
+        if (static_cast<int64_t>(b.tokens.size()) != b.batch * (b.seq + 1))
+            throw std::invalid_argument("batch: tokens must hold batch * (seq + 1) ids");
+        spes_losses l{};
+        const spes_status st = spes_local_step(ctx.get(), b.tokens.data(), b.batch, b.seq, &opt, &l);
+        if (st == SPES_RUNTIME_ERROR)  // the reference reports the step (trainer.hpp:166-167)
+            throw std::runtime_error("local_round: non-finite loss at step " + std::to_string(h));
+        check(st);
+        res.step_losses.push_back({l.total, l.ce, l.lb, l.moe_z, l.z});
+        if (cfg.record_trace) {
+            check(spes_read_grads(ctx.get(), g.data(), static_cast<int64_t>(g.size())));
+            double n2 = 0.0;
+            size_t q = 0;
+            for (size_t i = 0; i < blocks.size(); ++i) {
+                if (!mask.trainable(blocks[i])) continue;
+                const size_t n = static_cast<size_t>(spes::block_tensor(global, blocks[i]).numel());
+                const float* gb = g.data() + offs[i];
+                for (size_t j = 0; j < n; ++j) n2 += static_cast<double>(gb[j]) * gb[j];
+                if (q == res.grad_sum.size()) {
+                    spes::Tensor t = spes::Tensor::zeros(spes::block_tensor(global, blocks[i]).shape);
+                    std::memcpy(t.data.data(), gb, n * sizeof(float));
+                    res.grad_sum.push_back({i, std::move(t)});
+                } else {
+                    auto& acc = res.grad_sum[q].grad.data;
+                    for (size_t j = 0; j < n; ++j) acc[j] += gb[j];
+                }
+                ++q;
+            }
+            res.update_norms.push_back(std::sqrt(n2));
+            const std::vector<float> now = ctx.read();
+            double d2 = 0.0;
+            for (size_t j = 0; j < now.size(); ++j) {
+                const double dd = static_cast<double>(now[j]) - static_cast<double>(theta0[j]);
+                d2 += dd * dd;
+            }
+            res.drift_sq.push_back(d2);
+        }
+    }
     unflatten(ctx.read(), res.params);
-    for (const auto& l : losses) res.step_losses.push_back({l.total, l.ce, l.lb, l.moe_z, l.z});
     int64_t opt_state = 0, grads = 0, step = 0;
     check(spes_counts(ctx.get(), &opt_state, &grads, &step));
     res.grad_scalar_count = grads;

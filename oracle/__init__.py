@@ -126,6 +126,13 @@ def ref():
         R.ref_local_round.restype = C.c_int
         R.ref_local_round.argtypes = [_cfgp, _f32p, _i32p, C.c_int64, C.c_int64, C.c_int32,
                                       _f64n, C.POINTER(AdamWCfg), _u8p, _f64p]
+        R.ref_local_round_timed.restype = C.c_int
+        R.ref_local_round_timed.argtypes = [_cfgp, _f32p, _i32p, C.c_int64, C.c_int64, C.c_int32,
+                                            _f64n, C.POINTER(AdamWCfg), _u8p, _f64p,
+                                            C.POINTER(C.c_double)]
+        R.ref_local_round_pair_timed.restype = C.c_int
+        R.ref_local_round_pair_timed.argtypes = [_cfgp, _f32p, _i32p, C.c_int64, _i32p, C.c_int64,
+                                                 C.POINTER(AdamWCfg), _u8p, _f64p]
         R.ref_aggregate_partition.restype = C.c_int
         R.ref_aggregate_partition.argtypes = [_cfgp, C.c_int32, _f32p, _f32p, _f32p]
         R.ref_similarity.argtypes = [_cfgp, _f32p, C.c_int32, C.c_int32, _f64p]

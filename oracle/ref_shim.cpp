@@ -3,6 +3,8 @@
 // it pins the C restatement (spes_oracle.c) bit-for-bit and is the reference arm
 // / cpu_baseline of bench.py. It calls the reference's own public API; nothing
 // of the reference is copied here.
+#include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <span>
@@ -134,10 +136,13 @@ int ref_forward_backward(const spes_model_cfg* c, const float* params, const int
     }
 }
 
-// local_round (trainer.hpp:143-222) with a fresh MaskedAdamW and per-step lr.
-int ref_local_round(const spes_model_cfg* c, float* params, const int32_t* tokens, int64_t B,
-                    int64_t S, int32_t H, const double* lr, const spes_adamw_cfg* opt,
-                    const uint8_t* trainable_expert, double* losses) {
+// local_round (trainer.hpp:143-222) with a fresh MaskedAdamW and per-step lr; seconds (if
+// not null) receives the wall time of the reference's local_round call alone (the flat <->
+// ModelParams conversions of this shim excluded).
+static int local_round_impl(const spes_model_cfg* c, float* params, const int32_t* tokens,
+                            int64_t B, int64_t S, int32_t H, const double* lr,
+                            const spes_adamw_cfg* opt, const uint8_t* trainable_expert,
+                            double* losses, double* seconds) {
     try {
         ModelConfig cfg = to_cfg(c);
         ModelParams p = from_flat(cfg, params);
@@ -155,7 +160,10 @@ int ref_local_round(const spes_model_cfg* c, float* params, const int32_t* token
         rc.opt.weight_decay = opt->weight_decay;
         if (lr) rc.lr_at = [lr](int64_t s) { return lr[s]; };
         rc.first_step = 0;
+        const auto t0 = std::chrono::steady_clock::now();
         auto res = local_round(p, next, rc, mask);
+        if (seconds)
+            *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         for (size_t h = 0; h < res.step_losses.size(); ++h) {
             losses[5 * h + 0] = res.step_losses[h].total;
             losses[5 * h + 1] = res.step_losses[h].ce;
@@ -164,6 +172,56 @@ int ref_local_round(const spes_model_cfg* c, float* params, const int32_t* token
             losses[5 * h + 4] = res.step_losses[h].z;
         }
         to_flat(res.params, params);
+        return 0;
+    } catch (const std::out_of_range&) {
+        return 2;
+    } catch (const std::runtime_error&) {
+        return 3;
+    } catch (...) {
+        return 1;
+    }
+}
+
+int ref_local_round(const spes_model_cfg* c, float* params, const int32_t* tokens, int64_t B,
+                    int64_t S, int32_t H, const double* lr, const spes_adamw_cfg* opt,
+                    const uint8_t* trainable_expert, double* losses) {
+    return local_round_impl(c, params, tokens, B, S, H, lr, opt, trainable_expert, losses, nullptr);
+}
+
+int ref_local_round_timed(const spes_model_cfg* c, float* params, const int32_t* tokens, int64_t B,
+                          int64_t S, int32_t H, const double* lr, const spes_adamw_cfg* opt,
+                          const uint8_t* trainable_expert, double* losses, double* seconds) {
+    return local_round_impl(c, params, tokens, B, S, H, lr, opt, trainable_expert, losses, seconds);
+}
+
+// Reference-arm timing (bench.py): local_round (H=1, fresh MaskedAdamW) from the same global
+// model at S1 and then S2 tokens (B=1; tokens1 / tokens2 hold S+1 ids), each timed around
+// the reference's local_round call alone; the model is converted from the flat vector once.
+int ref_local_round_pair_timed(const spes_model_cfg* c, const float* params,
+                               const int32_t* tokens1, int64_t S1, const int32_t* tokens2,
+                               int64_t S2, const spes_adamw_cfg* opt,
+                               const uint8_t* trainable_expert, double* seconds2) {
+    try {
+        ModelConfig cfg = to_cfg(c);
+        ModelParams p = from_flat(cfg, params);
+        TrainMask mask = mask_from(cfg, trainable_expert, 0);
+        LocalRoundConfig rc;
+        rc.steps = 1;
+        rc.opt.lr = opt->lr;
+        rc.opt.beta1 = opt->beta1;
+        rc.opt.beta2 = opt->beta2;
+        rc.opt.eps = opt->eps;
+        rc.opt.weight_decay = opt->weight_decay;
+        for (int i = 0; i < 2; ++i) {
+            const int32_t* tk = i == 0 ? tokens1 : tokens2;
+            const int64_t S = i == 0 ? S1 : S2;
+            BatchProvider next = [&]() { return batch_from(tk, 1, S); };
+            const auto t0 = std::chrono::steady_clock::now();
+            auto res = local_round(p, next, rc, mask);
+            seconds2[i] =
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            if (!std::isfinite(res.step_losses.at(0).total)) return 3;
+        }
         return 0;
     } catch (const std::out_of_range&) {
         return 2;

@@ -73,9 +73,11 @@ def lib():
         L.spes_set_ownership.argtypes = [vp, C.POINTER(i32), C.POINTER(i32)]
         L.spes_load_params.argtypes = [vp, f32p, i64]
         L.spes_read_params.argtypes = [vp, f32p, i64]
+        L.spes_load_params_device.argtypes = [vp, vp, i64]
         L.spes_read_grads.argtypes = [vp, f32p, i64]
         L.spes_set_fused_optimizer.argtypes = [vp, C.c_int32]
         L.spes_set_stream_overlap.argtypes = [vp, C.c_int32]
+        L.spes_set_inner_optimizer.argtypes = [vp, C.c_int32]
         L.spes_outer_begin.argtypes = [vp]
         i64p = C.POINTER(C.c_int64)
         L.spes_gen_corpus.argtypes = [i64, i64, C.c_int32, i64, C.c_uint64, C.c_double,
@@ -396,6 +398,10 @@ class Node:
         p = np.ascontiguousarray(p, np.float32)
         _check(lib().spes_load_params(self._ctx, f32(p), p.size))
 
+    def load_params_device(self, dev_ptr, n):
+        """Parameters from a device buffer (n fp32 scalars in enumerate_blocks order)."""
+        _check(lib().spes_load_params_device(self._ctx, C.c_void_p(dev_ptr), n))
+
     def read_params(self):
         out = np.zeros(self.P, np.float32)
         _check(lib().spes_read_params(self._ctx, f32(out), out.size))
@@ -405,6 +411,12 @@ class Node:
         """Owned experts' AdamW inside the dW GEMM epilogue, or (default) as a separate pass
         with materialized gradients (needed by read_grads); identical bits either way."""
         _check(lib().spes_set_fused_optimizer(self._ctx, 1 if on else 0))
+
+    def set_inner_optimizer(self, kind):
+        """LocalRoundConfig::inner (trainer.hpp:116-121): "adamw" (default) or "sgd"
+        (theta -= float(lr) * g on the trainable blocks, trainer.hpp:197-204)."""
+        k = {"adamw": 0, "sgd": 1}.get(kind, kind)
+        _check(lib().spes_set_inner_optimizer(self._ctx, k))
 
     def set_stream_overlap(self, on):
         """Second low-priority stream for the step's off-critical-path work (default on);

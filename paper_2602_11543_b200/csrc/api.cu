@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -131,7 +132,7 @@ struct LayerBufs {
     float *logits, *probs, *topk_w, *lse_r, *inv_rms, *denom, *y, *row_w, *lb_coeff;
     int32_t *topk_idx, *chunk_counts, *counts, *pad_off, *slot_row, *row_token, *tiles;
     GemmGroup* groups;
-    bf16 *xp, *gu, *hact;
+    bf16 *xp, *gu, *hact;  // routed rows (expert-major dispatch), GEMM outputs
     int64_t* grad_off;  // device [M]
     CUtensorMap a_xp, a_hact, a_xp_mn, a_hact_mn;  // *_mn: [tokens x features] as MN-major
     CUtensorMap b_w1_mn, b_w2_mn, b_w2, b_w1;  // *_mn: row-major weights as MN-major B
@@ -175,6 +176,9 @@ struct spes_ctx {
     // identical bits; the fused epilogue is issue/latency-bound at ~3.7 TB/s with the 8
     // epilogue warps that fit next to the MMA ring, so it does not beat the separate pass yet.
     bool fused_opt = false;
+    // inner optimizer (LocalRoundConfig::inner, trainer.hpp:116-121): AdamW, or SGD
+    // (theta -= lr * g, no moments; always the standalone pass)
+    bool inner_sgd = false;
     spes_k::AdamScalars cur_adam{};  // this step's AdamW scalars (set before backward)
     // DiLoCo baseline: this rank's slice of the round-start global model,
     // its fp64 Nesterov buffer, and the exchange buffers (N x slice each)
@@ -224,7 +228,7 @@ struct spes_ctx {
     float *dot_part = nullptr;
     double* loss_part = nullptr;
     int32_t* eg_scratch = nullptr;  // embedding-gradient bucketing (2V + 1 + T)
-    bf16* normed_bf = nullptr;  // router-normalized h of the current layer (expert GEMM input)
+    bf16* normed_bf = nullptr;  // router-normalized h of the current layer (dispatch source)
     float *dxp = nullptr, *gw_part = nullptr, *glog = nullptr, *gnormed = nullptr, *gh = nullptr,
           *nr_partial = nullptr;
     bf16 *hL = nullptr, *dlog_bf = nullptr;
@@ -406,22 +410,37 @@ void build_ownership_tables(spes_ctx* c) {
     c->adam_step = 0;
 }
 
+// optimizer segment tables: psi segments, then experts of 3df scalars each
+spes_k::SegTable train_table(const spes_ctx* c) {
+    return spes_k::SegTable{c->segs, 3, c->lay.psi(), c->lay.per_expert()};
+}
+spes_k::SegTable refresh_table(const spes_ctx* c) {  // head, then every expert
+    return spes_k::SegTable{c->all_segs, 1, c->lay.V * c->lay.d, c->lay.per_expert()};
+}
+
 spes_k::Shadows shadows_of(const spes_ctx* c) {
     return spes_k::Shadows{c->w1, c->w2, c->headB, c->lay.d, c->lay.f};
 }
 
 // Every bf16 operand copy from the fp32 parameters (after load / sync / merge).
 void refresh_shadows_all(spes_ctx* c) {
-    spes_k::refresh_shadows(c->params, c->all_segs, c->n_all_segs, c->all_segs_total,
-                            shadows_of(c), c->stream);
+    spes_k::refresh_shadows(c->params, refresh_table(c), c->all_segs_total, shadows_of(c),
+                            c->stream);
 }
 
 void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     const int64_t T = B * S;
     if (T < 1) throw std::invalid_argument("batch: need B*S >= 1");
+    if (T == c->T && c->T_pad > 0) {
+        // same token count, other batch shape: the buffers fit (tokens holds 2T >= B(S+1)
+        // ints) but the captured step splits inputs / targets with the old S
+        if (B != c->B || S != c->S) drop_graph(c);
+        c->B = B;
+        c->S = S;
+        return;
+    }
     c->B = B;
     c->S = S;
-    if (T == c->T && c->T_pad > 0) return;
     const Layout& L = c->lay;
     drop_graph(c);  // buffers move
     c->act.release();
@@ -437,7 +456,7 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     DevMem& A = c->act;
     c->h.assign(L.L + 1, nullptr);
     for (auto& p : c->h) p = A.alloc<float>(Tp * d);
-    c->tokens = A.alloc<int32_t>(B * (S + 1));
+    c->tokens = A.alloc<int32_t>(2 * T);  // B(S+1) = T + B <= 2T for every shape of this T
     c->inputs = A.alloc<int32_t>(Tp);
     c->eg_scratch = A.alloc<int32_t>(2 * L.V + 1 + Tp);
     c->targets = A.alloc<int32_t>(Tp);
@@ -490,8 +509,8 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     c->loss_part = A.alloc<double>((Tp / 256 + 1) * (2 + 2 * L.L));
     c->glog = A.alloc<float>(Tp * M);
     c->gnormed = A.alloc<float>(Tp * d);
-    c->normed_bf = A.alloc<bf16>(Tp * d);
     c->gh = A.alloc<float>(Tp * d);
+    c->normed_bf = A.alloc<bf16>(Tp * d);
     c->nr_partial = A.alloc<float>(spes_k::kNormRouterChunks * d * (M + 1));
     c->hL = A.alloc<bf16>(Tp * d);
     ck(cudaMemsetAsync(c->hL, 0, sizeof(bf16) * Tp * d, c->stream), "hL");  // padding rows
@@ -596,9 +615,11 @@ Seeds seeds_for(const spes_ctx* c) {
 // Off-critical-path work on the low-priority side stream (not while profiling: the
 // per-family event timings need one serial stream).
 bool use_side(const spes_ctx* c) { return c->overlap_opt && !c->prof; }
+// owned experts' optimizer step inside the dW GEMM epilogues (AdamW only)
+bool fused(const spes_ctx* c) { return c->fused_opt && !c->inner_sgd; }
 // owned experts' AdamW there, right after their dW GEMMs
 bool split_opt(const spes_ctx* c) {
-    return use_side(c) && !c->fused_opt && c->G > c->lay.psi();
+    return use_side(c) && !fused(c) && c->G > c->lay.psi();
 }
 
 void forward_backward(spes_ctx* c) {
@@ -658,12 +679,13 @@ void forward_backward(spes_ctx* c) {
                                  Y.row_token, Y.row_w, Y.groups, Y.tiles};
             spes_k::GroupBases gb{Y.gu, Y.y, c->dgu, c->dxp, c->grads, Y.grad_off, d, f,
                                   bn_for(d), bn_for(f), bn_for(d), bn_for(d), c->tr,
-                                  P + L.off_expert(l, 0), l * M, c->fused_opt ? 1 : 0};
+                                  P + L.off_expert(l, 0), l * M, fused(c) ? 1 : 0};
             spes_k::route_plan(Y.topk_idx, Y.topk_w, T, M, k, R, rp, gb, st);
         }
         {
-            PROF("permute");
-            spes_k::permute_rows_bf16(c->normed_bf, d, Y.row_token, Y.pad_off + M, R, Y.xp, st);
+            PROF("permute");  // TMA-staged row scatter (dispatch)
+            spes_k::permute_rows_tma(c->normed_bf, d, Y.slot_row, Y.row_token, Y.pad_off + M, T, k,
+                                     Y.xp, st);
         }
         {
             PROF("gemm_fwd_gate_up");
@@ -701,7 +723,7 @@ void forward_backward(spes_ctx* c) {
         fork(1);  // loss scalars: read by the host and by the optimizer's finite-loss guard
         spes_k::losses_reduce(c->diff, c->lse_head, c->lse_all, c->probs_all, c->coeff_all, T, Tp,
                               L.L, M, sd.inv_T, sd.inv_L, sd.c_ce, sd.c_lb, sd.c_mz, sd.c_z,
-                              c->loss_part, c->d_losses, ss);
+                              c->err, c->loss_part, c->d_losses, ss);
         ready(1);
     }
     // ---- backward ----
@@ -734,7 +756,7 @@ void forward_backward(spes_ctx* c) {
                                            c->glog, ss);
             ready(2);
         }
-        const bool unfused_dw = c->max_tiles[4] > 0 && !c->fused_opt;
+        const bool unfused_dw = c->max_tiles[4] > 0 && !fused(c);
         // owned experts' AdamW for the weights of this layer whose gradients are final and
         // whose bf16 operand copies the remaining GEMMs no longer read: wd (sub = 2) after
         // dW_down (dH read W2 before), wg|wu (sub = 0) after dW_gu (dX read W1 before)
@@ -745,10 +767,11 @@ void forward_backward(spes_ctx* c) {
             if (!c->early_wd && sub == 2) return;
             const int64_t off = sub == 2 ? 2 * df : 0;
             const int64_t len = sub == 2 ? df : (c->early_wd ? 2 * df : per);
+            if (nown == 0) return;
             fork(ev);
-            spes_k::adamw_strided(c->params, c->grads, c->m, c->v, c->segs,
-                                  static_cast<int>(c->segs_host.size()), c->layer_lo[l] + off,
-                                  per, len, nown, c->d_adam, shadows_of(c), c->d_losses, ss);
+            const int seg0 = 3 + static_cast<int>((c->layer_lo[l] - c->lay.psi()) / per);
+            spes_k::adamw_pieces(c->params, c->grads, c->m, c->v, train_table(c), seg0, nown, off,
+                                 len, c->d_adam, shadows_of(c), c->d_losses, ss);
         };
         {
             PROF("gemm_bwd_dh");
@@ -770,7 +793,7 @@ void forward_backward(spes_ctx* c) {
                                    Y.groups + 3 * M, M, Y.tiles + 3,
                                    c->max_tiles[3], st);
         }
-        if (c->max_tiles[4] > 0 && c->fused_opt) {
+        if (c->max_tiles[4] > 0 && fused(c)) {
             need(1);  // the epilogues' finite-loss guard reads the loss scalars
             // owned experts: dW and MaskedAdamW in one pass (no gradient materialized)
             const spes_k::Shadows sh = shadows_of(c);
@@ -818,6 +841,15 @@ void forward_backward(spes_ctx* c) {
 // MaskedAdamW::step scalars (trainer.hpp:68-84): bias corrections in double, cast to float.
 // Called before the backward so the fused dW epilogues can apply the step.
 void optimizer_begin(spes_ctx* c, const spes_adamw_cfg* o) {
+    if (c->inner_sgd) {  // trainer.hpp:197-204: float(lr), no optimizer state
+        c->cur_adam = spes_k::AdamScalars{};
+        c->cur_adam.lr = static_cast<float>(o->lr);
+        c->cur_adam.sgd = 1;
+        ck(cudaMemcpyAsync(c->d_adam, &c->cur_adam, sizeof(c->cur_adam), cudaMemcpyHostToDevice,
+                           c->stream),
+           "sgd scalars");
+        return;
+    }
     c->adam_step += 1;
     const float bc1 = 1.f - static_cast<float>(std::pow(o->beta1, static_cast<double>(c->adam_step)));
     const float bc2 = 1.f - static_cast<float>(std::pow(o->beta2, static_cast<double>(c->adam_step)));
@@ -837,10 +869,10 @@ void optimizer_begin(spes_ctx* c, const spes_adamw_cfg* o) {
 void optimizer_finish(spes_ctx* c) {
     PROF("adamw");
     const bool split = split_opt(c);
-    const int64_t n = c->fused_opt || split ? c->lay.psi() : c->G;  // psi is the compact prefix
-    spes_k::adamw(c->params, c->grads, c->m, c->v, c->segs,
-                  static_cast<int>(c->segs_host.size()), 0, n, c->d_adam, shadows_of(c),
-                  c->d_losses, c->stream);
+    // psi: the table's 3 leading segments; then the owned experts
+    const int nseg = fused(c) || split ? 3 : static_cast<int>(c->segs_host.size());
+    spes_k::adamw(c->params, c->grads, c->m, c->v, train_table(c), 0, nseg, c->d_adam,
+                  shadows_of(c), c->d_losses, c->stream);
     if (use_side(c)) {  // everything enqueued on the side stream this step
         ck(cudaEventRecord(c->ev_join, c->side), "event");
         ck(cudaStreamWaitEvent(c->stream, c->ev_join, 0), "wait");
@@ -865,8 +897,22 @@ void upload_tokens(spes_ctx* c, const int32_t* tokens, int64_t n) {
        "H2D tokens");
 }
 
+// The device status word (c->err): bit 0 an out-of-vocabulary token id (set by the token
+// split), bit 1 a non-finite loss (set by the loss reduction). It is sticky: once set, no
+// later step applies an update (spes_dev::loss_ok) until the host reports and clears it,
+// which ends the round with the reference's exception (model.hpp:280-281: out_of_range
+// before any update; trainer.hpp:166-167: runtime_error, no update).
+void raise_status(spes_ctx* c, int32_t st, const std::string& where) {
+    if (!st) return;
+    ck(cudaMemsetAsync(c->err, 0, 4, c->stream), "clear status");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    if (st & 1) throw std::out_of_range("batch: token id out of vocabulary" + where);
+    throw std::runtime_error("local_round: non-finite loss" + where);
+}
+
+// losses of the last step (one D2H with its status word); reports a bad step
 void read_losses(spes_ctx* c, spes_losses* out) {
-    ck(cudaMemcpyAsync(c->h_losses, c->d_losses, sizeof(double) * 5, cudaMemcpyDeviceToHost,
+    ck(cudaMemcpyAsync(c->h_losses, c->d_losses, sizeof(double) * 6, cudaMemcpyDeviceToHost,
                        c->stream),
        "D2H losses");
     ck(cudaStreamSynchronize(c->stream), "step");
@@ -877,14 +923,14 @@ void read_losses(spes_ctx* c, spes_losses* out) {
     out->z = c->h_losses[4];
 }
 
-void check_err_flag(spes_ctx* c) {
-    int32_t e = 0;
-    ck(cudaMemcpyAsync(&e, c->err, 4, cudaMemcpyDeviceToHost, c->stream), "err");
+// Steps run without reading their losses (device tokens, losses == NULL) are checked when
+// the round ends: at the next sync, round start or parameter read.
+void check_status(spes_ctx* c, const char* where) {
+    if (c->T == 0 || !c->err) return;
+    int32_t st = 0;
+    ck(cudaMemcpyAsync(&st, c->err, 4, cudaMemcpyDeviceToHost, c->stream), "D2H status");
     ck(cudaStreamSynchronize(c->stream), "sync");
-    if (e) {
-        cudaMemsetAsync(c->err, 0, 4, c->stream);
-        throw std::out_of_range("batch: token id out of vocabulary");
-    }
+    raise_status(c, st, where);
 }
 
 void local_step_impl(spes_ctx* c, int64_t B, int64_t S, const spes_adamw_cfg* opt,
@@ -893,7 +939,7 @@ void local_step_impl(spes_ctx* c, int64_t B, int64_t S, const spes_adamw_cfg* op
     // forward + backward (fused: owned experts updated unless the loss is non-finite) and
     // the optimizer pass (device-side non-finite check), eagerly or as a replayed graph
     const bool graph = c->use_graph && !c->prof;
-    if (graph && c->step_graph && c->graph_T == c->T && c->graph_fused == (c->fused_opt ? 1 : 0)) {
+    if (graph && c->step_graph && c->graph_T == c->T && c->graph_fused == (fused(c) ? 1 : 0)) {
         ck(cudaGraphLaunch(c->step_graph, c->stream), "graph launch");
         c->launches += c->graph_launches;
     } else if (graph && c->graph_seen_T == c->T) {  // second step of this shape: capture
@@ -909,7 +955,7 @@ void local_step_impl(spes_ctx* c, int64_t B, int64_t S, const spes_adamw_cfg* op
         c->graph_launches = c->launches - before;
         c->launches = before + c->graph_launches;
         c->graph_T = c->T;
-        c->graph_fused = c->fused_opt ? 1 : 0;
+        c->graph_fused = fused(c) ? 1 : 0;
         ck(cudaGraphLaunch(c->step_graph, c->stream), "graph launch");
     } else {
         forward_backward(c);
@@ -918,9 +964,10 @@ void local_step_impl(spes_ctx* c, int64_t B, int64_t S, const spes_adamw_cfg* op
     }
     if (losses) {
         read_losses(c, losses);
-        if (!std::isfinite(losses->total)) {  // no update was applied; caller reports it
-            c->adam_step -= 1;
-            return;
+        const int32_t st = static_cast<int32_t>(c->h_losses[5]);
+        if (st) {  // no update was applied (this step, or any since the bad one)
+            if (!c->inner_sgd) c->adam_step -= 1;
+            raise_status(c, st, "");
         }
     }
     (void)B;
@@ -1054,6 +1101,12 @@ spes_status spes_create(const spes_model_cfg* cfg, int32_t node, int32_t n_nodes
         if (const char* e = std::getenv("SPES_OPT_OVERLAP")) c->overlap_opt = std::atoi(e) != 0;
         if (const char* e = std::getenv("SPES_FUSED_OPT")) c->fused_opt = std::atoi(e) != 0;
         if (const char* e = std::getenv("SPES_EARLY_WD")) c->early_wd = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SPES_STEP_GRAPH")) c->use_graph = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SPES_ADAM_BG")) {  // "threads,tiles" (experiments)
+            int th = 256, ti = 4;
+            if (std::sscanf(e, "%d,%d", &th, &ti) >= 1 && th >= 32 && th <= 1024 && th % 32 == 0)
+                spes_k::adamw_background_shape(th, ti < 1 ? 1 : ti);
+        }
         c->expf_variant = spes_expf::host_variant_from(&expf);
         spes_k::gemm_prepare(cuda_device);
         const Layout& L = c->lay;
@@ -1290,6 +1343,18 @@ spes_status spes_read_checkpoint(spes_ctx* c, const char* path, uint64_t* round)
     });
 }
 
+spes_status spes_load_params_device(spes_ctx* c, const float* dev, int64_t n) {
+    return guard([&] {
+        if (n != c->lay.total()) throw std::invalid_argument("load_params: size mismatch");
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        set_counter(c);
+        ck(cudaMemcpyAsync(c->params, dev, sizeof(float) * n, cudaMemcpyDeviceToDevice, c->stream),
+           "D2D params");
+        refresh_shadows_all(c);
+        ck(cudaStreamSynchronize(c->stream), "sync");
+    });
+}
+
 spes_status spes_read_params(spes_ctx* c, float* host, int64_t n) {
     return guard([&] {
         if (n != c->lay.total()) throw std::invalid_argument("read_params: size mismatch");
@@ -1303,6 +1368,7 @@ spes_status spes_read_params(spes_ctx* c, float* host, int64_t n) {
 spes_status spes_round_begin(spes_ctx* c, int32_t carry_state) {
     return guard([&] {
         ck(cudaSetDevice(c->device), "cudaSetDevice");
+        check_status(c, " (unreported step of the previous round)");
         if (!carry_state) {
             // fresh MaskedAdamW (trainer.hpp:151-156): zero moments, step 0
             ck(cudaMemsetAsync(c->m, 0, sizeof(float) * c->G, c->stream), "m");
@@ -1322,8 +1388,6 @@ spes_status spes_local_step(spes_ctx* c, const int32_t* tokens, int64_t B, int64
         ensure_activations(c, B, S);
         upload_tokens(c, tokens, B * (S + 1));
         local_step_impl(c, B, S, opt, losses);
-        if (losses && !std::isfinite(losses->total))
-            throw std::runtime_error("local_round: non-finite loss at step 0");
     });
 }
 
@@ -1337,12 +1401,7 @@ spes_status spes_local_step_device(spes_ctx* c, const int32_t* d_tokens, int64_t
         ck(cudaMemcpyAsync(c->tokens, d_tokens, sizeof(int32_t) * B * (S + 1),
                            cudaMemcpyDeviceToDevice, c->stream),
            "D2D tokens");
-        local_step_impl(c, B, S, opt, losses);
-        if (losses) {
-            check_err_flag(c);
-            if (!std::isfinite(losses->total))
-                throw std::runtime_error("local_round: non-finite loss at step 0");
-        }
+        local_step_impl(c, B, S, opt, losses);  // losses == NULL: reported at round end
     });
 }
 
@@ -1369,9 +1428,12 @@ spes_status spes_local_round(spes_ctx* c, const int32_t* tokens, int64_t B, int6
             if (lr) o.lr = lr[h];
             spes_losses tmp;
             spes_losses* lo = per_step ? &per_step[h] : &tmp;
-            local_step_impl(c, B, S, &o, lo);
-            if (!std::isfinite(lo->total))
-                throw std::runtime_error("local_round: non-finite loss at step " + std::to_string(h));
+            try {
+                local_step_impl(c, B, S, &o, lo);
+            } catch (const std::runtime_error& e) {
+                if (dynamic_cast<const SpesError*>(&e)) throw;
+                throw std::runtime_error(std::string(e.what()) + " at step " + std::to_string(h));
+            }
         }
     });
 }
@@ -1534,8 +1596,6 @@ spes_status spes_local_step_rows(spes_ctx* c, const int64_t* rows, int64_t B,
         ensure_activations(c, B, c->corpus_seq);
         gather_corpus_rows(c, rows, B);
         local_step_impl(c, B, c->corpus_seq, opt, losses);
-        if (losses && !std::isfinite(losses->total))
-            throw std::runtime_error("local_round: non-finite loss at step 0");
     });
 }
 
@@ -1559,9 +1619,12 @@ spes_status spes_local_round_rows(spes_ctx* c, const int64_t* rows, int64_t B, i
             if (lr) o.lr = lr[h];
             spes_losses tmp;
             spes_losses* lo = per_step ? &per_step[h] : &tmp;
-            local_step_impl(c, B, c->corpus_seq, &o, lo);
-            if (!std::isfinite(lo->total))
-                throw std::runtime_error("local_round: non-finite loss at step " + std::to_string(h));
+            try {
+                local_step_impl(c, B, c->corpus_seq, &o, lo);
+            } catch (const std::runtime_error& e) {
+                if (dynamic_cast<const SpesError*>(&e)) throw;
+                throw std::runtime_error(std::string(e.what()) + " at step " + std::to_string(h));
+            }
         }
     });
 }
@@ -1609,9 +1672,9 @@ spes_status spes_outer_sync(spes_ctx* c, int32_t kind, double lr, double momentu
             return std::make_pair(lo, std::min<int64_t>(P, lo + sl) - lo);
         };
         cudaEvent_t e0, e1;
-        cudaEventCreate(&e0);
-        cudaEventCreate(&e1);
-        cudaEventRecord(e0, st);
+        ck(cudaEventCreate(&e0), "event");
+        ck(cudaEventCreate(&e1), "event");
+        ck(cudaEventRecord(e0, st), "event");
         const auto [mlo, mn] = range(me);
         // recv[i] = node i's local values of my slice (node order)
         ck(cudaMemcpyAsync(c->outer_recv + static_cast<int64_t>(me) * sl, c->params + mlo,
@@ -1638,10 +1701,10 @@ spes_status spes_outer_sync(spes_ctx* c, int32_t kind, double lr, double momentu
         ck(cudaMemcpyAsync(c->params, c->outer_gather, sizeof(float) * P, cudaMemcpyDeviceToDevice, st),
            "new global");
         refresh_shadows_all(c);
-        cudaEventRecord(e1, st);
+        ck(cudaEventRecord(e1, st), "event");
         ck(cudaStreamSynchronize(st), "outer sync");
         float ms = 0.f;
-        cudaEventElapsedTime(&ms, e0, e1);
+        ck(cudaEventElapsedTime(&ms, e0, e1), "event time");
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         if (stats) {
@@ -1718,12 +1781,13 @@ spes_status spes_sync(spes_ctx* c, spes_sync_stats* stats) {
         cudaStream_t st = c->stream;
         if (N == 1) {  // one node: the owner-set means are the node's own values
             if (stats) *stats = spes_sync_stats{};
+            check_status(c, " (a step of this round)");
             return;
         }
         cudaEvent_t e0, e1;
-        cudaEventCreate(&e0);
-        cudaEventCreate(&e1);
-        cudaEventRecord(e0, st);
+        ck(cudaEventCreate(&e0), "event");
+        ck(cudaEventCreate(&e1), "event");
+        ck(cudaEventRecord(e0, st), "event");
         double psi_in = 0, exp_in = 0;
         Prof prof_sync(c, "sync");
         if (N > 1) {
@@ -1860,16 +1924,15 @@ spes_status spes_sync(spes_ctx* c, spes_sync_stats* stats) {
             ph.reset();
             ph = std::make_unique<Prof>(c, "sync_refresh_shadows");
             if (c->p2p_ok)  // expert copies were written by the means and the pulls
-                spes_k::refresh_shadows(c->params, c->all_segs, c->n_all_segs, L.V * L.d,
-                                        shd, st);  // the head leads the refresh table
+                spes_k::refresh_shadows(c->params, refresh_table(c), L.V * L.d, shd, st);  // the head leads the refresh table
             else
                 refresh_shadows_all(c);
             ph.reset();
         }
-        cudaEventRecord(e1, st);
+        ck(cudaEventRecord(e1, st), "event");
         ck(cudaStreamSynchronize(st), "sync");
         float ms = 0;
-        cudaEventElapsedTime(&ms, e0, e1);
+        ck(cudaEventElapsedTime(&ms, e0, e1), "event time");
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         if (stats) {
@@ -1877,6 +1940,9 @@ spes_status spes_sync(spes_ctx* c, spes_sync_stats* stats) {
             stats->expert_bytes_in = exp_in;
             stats->ms = ms;
         }
+        // after the collective, so a bad node never leaves its peers waiting in it (its
+        // updates stopped at the bad step; the reference aborts the run at that point)
+        check_status(c, " (a step of this round)");
     });
 }
 
@@ -2060,7 +2126,7 @@ spes_status spes_merge(spes_ctx* c, const spes_merge_sched* sched, int32_t round
 
 spes_status spes_counts(spes_ctx* c, int64_t* opt_state, int64_t* grad_scalars, int64_t* step) {
     return guard([&] {
-        if (opt_state) *opt_state = 2 * c->G;
+        if (opt_state) *opt_state = c->inner_sgd ? 0 : 2 * c->G;
         if (grad_scalars) *grad_scalars = c->G;
         if (step) *step = c->adam_step;
     });
@@ -2070,6 +2136,16 @@ spes_status spes_set_fused_optimizer(spes_ctx* c, int32_t on) {
     return guard([&] {
         ck(cudaStreamSynchronize(c->stream), "sync");
         c->fused_opt = on != 0;  // group tables are rebuilt every step with the mode
+    });
+}
+
+spes_status spes_set_inner_optimizer(spes_ctx* c, int32_t kind) {
+    return guard([&] {
+        if (kind != 0 && kind != 1)
+            throw std::invalid_argument("inner optimizer: 0 (AdamW) or 1 (SGD)");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        c->inner_sgd = kind == 1;
+        drop_graph(c);  // the captured step holds the other optimizer placement
     });
 }
 
@@ -2084,7 +2160,7 @@ spes_status spes_set_stream_overlap(spes_ctx* c, int32_t on) {
 spes_status spes_read_grads(spes_ctx* c, float* host, int64_t n) {
     return guard([&] {
         if (n != c->lay.total()) throw std::invalid_argument("read_grads: size mismatch");
-        if (c->fused_opt && c->G > c->lay.psi())
+        if (fused(c) && c->G > c->lay.psi())
             throw std::logic_error(
                 "read_grads: owned-expert gradients are fused into the optimizer; call "
                 "spes_set_fused_optimizer(ctx, 0) before the step to materialize them");
@@ -2317,7 +2393,8 @@ spes_status spes_kernel_adamw(float* theta, const float* grad, float* m, float* 
                                     static_cast<float>(o->weight_decay), bc1, bc2};
         auto* da = D.alloc<spes_k::AdamScalars>(1);
         ck(cudaMemcpy(da, &a, sizeof(a), cudaMemcpyHostToDevice), "H2D");
-        spes_k::adamw(dt, dgr, dm, dv, ds, 1, 0, n, da, spes_k::Shadows{nullptr, nullptr, nullptr, 0, 0},
+        spes_k::adamw(dt, dgr, dm, dv, spes_k::SegTable{ds, 1, n, 4}, 0, 1, da,
+                      spes_k::Shadows{nullptr, nullptr, nullptr, 0, 0},
                       nullptr, 0);
         ck(cudaDeviceSynchronize(), "adamw kernel");
         ck(cudaMemcpy(theta, dt, 4 * n, cudaMemcpyDeviceToHost), "D2H");

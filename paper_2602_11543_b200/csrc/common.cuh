@@ -70,6 +70,7 @@ __device__ __forceinline__ float sigmoid_f(float z) {
 // MaskedAdamW::step scalars (trainer.hpp:68-84; bias corrections computed on the host)
 struct AdamScalars {
     float lr, b1, b2, omb1, omb2, eps, wd, bc1, bc2;
+    int32_t sgd;  // 1: the SGD inner step theta -= lr * g (trainer.hpp:197-204), no moments
 };
 // One MaskedAdamW element update (trainer.hpp:85-92), exact fp32 op order. Shared by the
 // standalone optimizer pass and the dW-GEMM epilogues so both produce identical bits.
@@ -83,9 +84,11 @@ __device__ __forceinline__ float adam_elem(float th, float g, float& m, float& v
     return fsub(th, upd);
 }
 // device-side guard: the reference applies no update after a non-finite loss
-// (trainer.hpp:166-167); the step's total loss lives on the device
-__device__ __forceinline__ bool loss_ok(const double* total) {
-    return total == nullptr || isfinite(*total);
+// (trainer.hpp:166-167) and validates token ids before the step (model.hpp:280-281).
+// losses[5] is the step's status word (0 = ok; bit 0 an out-of-vocabulary token, bit 1 a
+// non-finite loss), sticky until the host reports it, so no later step updates either.
+__device__ __forceinline__ bool loss_ok(const double* losses) {
+    return losses == nullptr || losses[5] == 0.0;
 }
 
 }  // namespace spes_dev

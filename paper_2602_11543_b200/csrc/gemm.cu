@@ -367,12 +367,10 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* 
     if (ng > GEMM_MAX_GROUPS) throw std::invalid_argument("grouped GEMM: too many groups");
     if (g_gemm_pairs) {
         auto kern = grouped_gemm_2cta_kernel<BN, Epi, AMN, BMN>;
-        static bool configured2 = false;
-        if (!configured2) {
+        static std::atomic<uint64_t> configured2{0};
+        if (first_use_on_device(configured2))
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  Gemm2Cfg<BN, Epi::SLOTS>::SMEM_BYTES);
-            configured2 = true;
-        }
         const int pairs = max_tiles < num_sms() / 2 ? max_tiles : num_sms() / 2;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(2 * pairs);
@@ -391,12 +389,10 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* 
         return;
     }
     auto kern = grouped_gemm_kernel<BN, Epi, AMN, BMN>;
-    static bool configured = false;  // one per template instantiation
-    if (!configured) {
+    static std::atomic<uint64_t> configured{0};  // one per template instantiation
+    if (first_use_on_device(configured))
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              GemmCfg<BN, Epi::SLOTS>::SMEM_BYTES);
-        configured = true;
-    }
     const int grid = max_tiles < num_sms() ? max_tiles : num_sms();
     kern<<<grid, GEMM_THREADS, GemmCfg<BN, Epi::SLOTS>::SMEM_BYTES, s>>>(a, b, g, ng, tiles,
                                                                        max_tiles, epi);

@@ -31,7 +31,7 @@ struct Gemm2Cfg {
     static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + FIXED + EPI_BYTES;
 };
 
-template <int BN, class Epi, bool A_MN = false, bool B_MN = false, int DBG_NO_TMA = 0>
+template <int BN, class Epi, bool A_MN = false, bool B_MN = false>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap mapA,
                              const __grid_constant__ CUtensorMap mapB,
@@ -99,14 +99,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     uint8_t* sa = smem + stage * C::STAGE_BYTES;
                     uint8_t* sb = sa + C::A_BYTES;
                     const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
-                    if (DBG_NO_TMA && (t != pair || kb >= C::STAGES)) {  // MMA-rate probe only
-                        mbar_arrive_cluster(fb);
-                        if (++stage == C::STAGES) {
-                            stage = 0;
-                            phase ^= 1;
-                        }
-                        continue;
-                    }
                     if (leader)  // the leader expects both CTAs' bytes on its own barrier
                         mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
                     else

@@ -17,6 +17,7 @@
 #include "common.cuh"
 #include "glibc_expf.h"
 #include "kernels.h"
+#include "sm100_primitives.cuh"
 
 namespace spes_k {
 
@@ -39,7 +40,7 @@ __global__ void embed_gather_k(const float* __restrict__ emb, const int32_t* __r
     if (threadIdx.x == 0) {
         inputs[t] = bad ? 0 : tin;
         targets[t] = bad ? 0 : tout;
-        if (bad) atomicExch(err, 1);
+        if (bad) atomicOr(err, 1);
     }
     if (bad) tin = 0;
     if (!h) return;  // layer-0 input read in place as emb[inputs[t]] by its consumers
@@ -59,7 +60,7 @@ __global__ void split_tokens_k(const int32_t* __restrict__ tokens, int64_t T, in
     const bool bad = tin < 0 || tin >= V || tout < 0 || tout >= V;
     inputs[t] = bad ? 0 : tin;
     targets[t] = bad ? 0 : tout;
-    if (bad) atomicExch(err, 1);
+    if (bad) atomicOr(err, 1);
 }
 
 void embed_gather(const float* emb, const int32_t* tokens, int64_t B, int64_t S, int64_t d,
@@ -307,89 +308,80 @@ void route_plan(const int32_t* topk_idx, const float* topk_w, int64_t T, int M, 
     count_launch(3);
 }
 
-// ============================ gather / transpose to bf16 ============================
-// 64 x 64 tile: dst[r][c] = bf16(src[map(r)][c]) and dstT[c][r] = same.
-__global__ void __launch_bounds__(256) gather_rows_bf16_k(
-    const float* __restrict__ src, int64_t ld_src, const int32_t* __restrict__ row_map,
-    const int32_t* __restrict__ nrows_dev, int64_t rows, int64_t cols, bf16* __restrict__ dst,
-    bf16* __restrict__ dstT, int64_t rows_cap) {
-    __shared__ float tile[64][65];
-    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 64;
-    const int64_t c0 = static_cast<int64_t>(blockIdx.y) * 64;
-    const int64_t nrows = nrows_dev ? *nrows_dev : rows;
-    if (r0 >= nrows) return;
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int rr = ty + 16 * i;
-        const int64_t r = r0 + rr;
-        int64_t srow = -1;
-        if (r < nrows) srow = row_map ? row_map[r] : r;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (srow >= 0) v = __ldg(reinterpret_cast<const float4*>(src + srow * ld_src + c0 + 4 * tx));
-        tile[rr][4 * tx + 0] = v.x;
-        tile[rr][4 * tx + 1] = v.y;
-        tile[rr][4 * tx + 2] = v.z;
-        tile[rr][4 * tx + 3] = v.w;
-        if (r < nrows) {
-            __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y);
-            __nv_bfloat162 b = __floats2bfloat162_rn(v.z, v.w);
-            uint2 pk;
-            pk.x = *reinterpret_cast<uint32_t*>(&a);
-            pk.y = *reinterpret_cast<uint32_t*>(&b);
-            *reinterpret_cast<uint2*>(dst + r * cols + c0 + 4 * tx) = pk;
+// ============================ dispatch (permute) ============================
+// Xp[slot_row[t][s]] = normed_bf[t] for every token t and selected slot s (model.hpp:314-318,
+// 327: select_rows by the expert-major, token-ascending plan), as a scatter of whole rows
+// staged by TMA bulk copies: one bulk load of the token's 2d-byte row into shared memory,
+// then k bulk stores of it to its routed rows. A warp drives one token at a time from its
+// elected lane with two row buffers (the next token's load is in flight while the current
+// one is stored). Padding rows of every expert (row_token < 0) are written as zeros by the
+// whole warp afterwards. Deterministic: every Xp row has exactly one writer.
+constexpr int PERM_WARPS = 4;
+__global__ void __launch_bounds__(32 * PERM_WARPS) permute_tma_k(
+    const bf16* __restrict__ src, uint32_t row_bytes, const int32_t* __restrict__ slot_row,
+    const int32_t* __restrict__ row_token, const int32_t* __restrict__ nrows_dev, int T, int k,
+    bf16* __restrict__ xp) {
+    extern __shared__ __align__(128) uint8_t psm[];
+    __shared__ __align__(8) uint64_t bars[PERM_WARPS][2];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint8_t* buf0 = psm + static_cast<size_t>(w) * 2 * row_bytes;
+    const int gw = blockIdx.x * PERM_WARPS + w, nw = gridDim.x * PERM_WARPS;
+    if (lane == 0) {
+        mbar_init(&bars[w][0], 1);
+        mbar_init(&bars[w][1], 1);
+        fence_barrier_init();
+    }
+    __syncwarp();
+    if (lane == 0 && gw < T) {
+        uint32_t phase[2] = {0, 0};
+        mbar_arrive_expect_tx(&bars[w][0], row_bytes);
+        bulk_load(buf0, reinterpret_cast<const uint8_t*>(src) + static_cast<size_t>(gw) * row_bytes,
+                  row_bytes, &bars[w][0]);
+        int it = 0;
+        for (int t = gw; t < T; t += nw, ++it) {
+            const int b = it & 1;
+            const int tn = t + nw;
+            if (tn < T) {  // next token into the other buffer once its stores have read it
+                bulk_wait_read<0>();
+                mbar_arrive_expect_tx(&bars[w][b ^ 1], row_bytes);
+                bulk_load(buf0 + (b ^ 1) * row_bytes,
+                          reinterpret_cast<const uint8_t*>(src) + static_cast<size_t>(tn) * row_bytes,
+                          row_bytes, &bars[w][b ^ 1]);
+            }
+            mbar_wait(&bars[w][b], phase[b]);
+            phase[b] ^= 1;
+            for (int s = 0; s < k; ++s) {
+                const int64_t r = slot_row[static_cast<int64_t>(t) * k + s];
+                bulk_store(reinterpret_cast<uint8_t*>(xp) + r * row_bytes, buf0 + b * row_bytes,
+                           row_bytes);
+            }
+            bulk_commit();
         }
+        bulk_wait<0>();
     }
-    __syncthreads();
-    if (!dstT) return;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int cc = ty + 16 * i;
-        __nv_bfloat162 a = __floats2bfloat162_rn(tile[4 * tx + 0][cc], tile[4 * tx + 1][cc]);
-        __nv_bfloat162 b = __floats2bfloat162_rn(tile[4 * tx + 2][cc], tile[4 * tx + 3][cc]);
-        uint2 pk;
-        pk.x = *reinterpret_cast<uint32_t*>(&a);
-        pk.y = *reinterpret_cast<uint32_t*>(&b);
-        const int64_t r = r0 + 4 * tx;
-        if (r < rows_cap) *reinterpret_cast<uint2*>(dstT + (c0 + cc) * rows_cap + r) = pk;
+    // padding rows (the tail of every expert's tile-aligned range) as zeros
+    const int64_t nrows = *nrows_dev;
+    const int n16 = static_cast<int>(row_bytes / 16);
+    for (int64_t r = gw; r < nrows; r += nw) {
+        if (row_token[r] >= 0) continue;
+        uint4* d4 = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(xp) + r * row_bytes);
+        for (int i = lane; i < n16; i += 32) d4[i] = make_uint4(0, 0, 0, 0);
     }
 }
 
-void gather_rows_bf16(const float* src, int64_t ld_src, const int32_t* row_map,
-                      const int32_t* nrows_dev, int64_t rows, int64_t cols, bf16* dst,
-                      bf16* dstT, int64_t rows_cap, cudaStream_t s) {
-    dim3 grid(static_cast<unsigned>(cdiv(rows, 64)), static_cast<unsigned>(cols / 64));
-    gather_rows_bf16_k<<<grid, 256, 0, s>>>(src, ld_src, row_map, nrows_dev, rows, cols, dst,
-                                            dstT, rows_cap);
-    count_launch();
-}
-
-// ============================ permute (bf16 rows) ============================
-// One warp per destination row, 16-byte vectors; padding rows (row_map < 0) are zeroed.
-__global__ void __launch_bounds__(256) permute_rows_bf16_k(const bf16* __restrict__ src,
-                                                           int64_t cols,
-                                                           const int32_t* __restrict__ row_map,
-                                                           const int32_t* __restrict__ nrows_dev,
-                                                           bf16* __restrict__ dst) {
-    const int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-    if (r >= *nrows_dev) return;
-    const int lane = threadIdx.x & 31;
-    const int32_t sr = row_map[r];
-    const int64_t n16 = cols / 8;
-    uint4* d4 = reinterpret_cast<uint4*>(dst + r * cols);
-    if (sr < 0) {
-        for (int64_t i = lane; i < n16; i += 32) d4[i] = make_uint4(0, 0, 0, 0);
-        return;
-    }
-    const uint4* s4 = reinterpret_cast<const uint4*>(src + static_cast<int64_t>(sr) * cols);
-#pragma unroll 4
-    for (int64_t i = lane; i < n16; i += 32) d4[i] = __ldg(s4 + i);
-}
-
-void permute_rows_bf16(const bf16* src, int64_t cols, const int32_t* row_map,
-                       const int32_t* nrows_dev, int64_t rows_cap, bf16* dst, cudaStream_t s) {
-    permute_rows_bf16_k<<<static_cast<unsigned>(cdiv(rows_cap, 8)), 256, 0, s>>>(
-        src, cols, row_map, nrows_dev, dst);
+void permute_rows_tma(const bf16* src, int64_t cols, const int32_t* slot_row,
+                      const int32_t* row_token, const int32_t* nrows_dev, int64_t T, int k,
+                      bf16* dst, cudaStream_t s) {
+    const uint32_t row_bytes = static_cast<uint32_t>(cols * sizeof(bf16));
+    const int smem = PERM_WARPS * 2 * static_cast<int>(row_bytes);
+    static std::atomic<uint64_t> attr{0};
+    if (first_use_on_device(attr))
+        cudaFuncSetAttribute(permute_tma_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             PERM_WARPS * 2 * 8192 * 2);
+    const int per_sm = std::max(1, std::min(8, (200 * 1024) / std::max(smem, 1)));
+    const int blocks = static_cast<int>(std::min<int64_t>(148 * per_sm, cdiv(T, PERM_WARPS)));
+    permute_tma_k<<<std::max(blocks, 1), 32 * PERM_WARPS, smem, s>>>(
+        src, row_bytes, slot_row, row_token, nrows_dev, static_cast<int>(T), k, dst);
     count_launch();
 }
 
@@ -608,7 +600,7 @@ __global__ void __launch_bounds__(256) losses_partial_k(
 
 __global__ void losses_finish_k(const double* __restrict__ part, int nb, int L, float inv_T,
                                 float inv_L, float c_ce, float c_lb, float c_mz, float c_z,
-                                double* __restrict__ out) {
+                                int32_t* status, double* __restrict__ out) {
     __shared__ double acc[2 + 2 * 64];
     const int ns = 2 + 2 * L;
     for (int i = threadIdx.x; i < ns; i += blockDim.x) {
@@ -641,17 +633,24 @@ __global__ void losses_finish_k(const double* __restrict__ part, int nb, int L, 
         out[2] = lbv;
         out[3] = moe_z;
         out[4] = z;
+        // status word (see loss_ok): the token check of this or an unreported earlier step
+        // (status bit 0, set by the token split) and this step's loss
+        int32_t st = *status;
+        if (!isfinite(total)) st |= 2;
+        if (st) atomicOr(status, st);
+        out[5] = static_cast<double>(st);
     }
 }
 
 void losses_reduce(const float* diff, const float* lse_head, const float* lse_r,
                    const float* probs, const float* lb_coeff, int64_t T, int64_t Tstride, int L,
                    int M, float inv_T, float inv_L, float c_ce, float c_lb, float c_mz, float c_z,
-                   double* part, double* out, cudaStream_t s) {
+                   int32_t* status, double* part, double* out, cudaStream_t s) {
     const int nb = static_cast<int>(cdiv(T, 256));
     losses_partial_k<<<nb, 256, 0, s>>>(diff, lse_head, lse_r, probs, lb_coeff, T, Tstride, L, M,
                                         part);
-    losses_finish_k<<<1, 128, 0, s>>>(part, nb, L, inv_T, inv_L, c_ce, c_lb, c_mz, c_z, out);
+    losses_finish_k<<<1, 128, 0, s>>>(part, nb, L, inv_T, inv_L, c_ce, c_lb, c_mz, c_z,
+                                      status, out);
     count_launch(2);
 }
 
@@ -929,11 +928,9 @@ void norm_router_grads(const float* h, const int32_t* hrow, const float* gain, c
                        float* gh, cudaStream_t s) {
     dim3 grid(static_cast<unsigned>(d / 128), NRG_TC, static_cast<unsigned>((M + NRG_EG - 1) / NRG_EG));
     constexpr int ring_bytes = NRG_S * 3 * 256 * 16;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::atomic<uint64_t> attr_set{0};
+    if (first_use_on_device(attr_set))
         cudaFuncSetAttribute(norm_router_partial_k, cudaFuncAttributeMaxDynamicSharedMemorySize, ring_bytes);
-        attr_set = true;
-    }
     norm_router_partial_k<<<grid, 256, ring_bytes, s>>>(h, hrow, gain, gnormed, glog, inv_rms, (int)T, (int)d, M,
                                                partial, dot_part, gh);
     const int64_t n = d * (M + 1);
@@ -1182,17 +1179,18 @@ void outer_step(float* theta, const float* recv, int N, int64_t n, int64_t ld, i
 }
 
 // ============================ AdamW (+ bf16 operand copies) ============================
-// MaskedAdamW::step element update (trainer.hpp:85-92), exact fp32 op order, over the
-// compact trainable segments (psi + owned experts). The updated values are also written
-// as the bf16 GEMM operand copies (W1 interleaved gate|up, W2 = Wd, headB), so no
-// separate shadow pass re-reads the parameters.
-__device__ __forceinline__ int find_seg(const AdamSeg* __restrict__ segs, int nseg, int64_t i) {
-    int lo = 0, hi = nseg - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (segs[mid].comp_off <= i) lo = mid; else hi = mid - 1;
-    }
-    return lo;
+// MaskedAdamW::step element update (trainer.hpp:85-92; or the SGD inner step of
+// trainer.hpp:197-204), exact fp32 op order, over the compact trainable segments (psi +
+// owned experts). The updated values are also written as the bf16 GEMM operand copies
+// (W1 interleaved gate|up, W2 = Wd, headB), so no separate shadow pass re-reads them.
+//
+// Segment lookup is by block: blockIdx.y picks the segment (a launch covers whole segments,
+// or the same piece of consecutive expert segments), so no thread ever searches a table.
+__device__ __forceinline__ int seg_of(const SegTable& t, int64_t i) {  // refresh pass only
+    if (i >= t.psi_len) return t.npsi + static_cast<int>((i - t.psi_len) / t.per);
+    int s = 0;
+    while (s + 1 < t.npsi && t.segs[s + 1].comp_off <= i) ++s;
+    return s;
 }
 
 // 4 consecutive parameters starting at offset o within segment sg -> bf16 copy
@@ -1209,7 +1207,8 @@ __device__ __forceinline__ void write_shadow4(const AdamSeg& sg, int64_t o, cons
         if (o32 < 2 * df) {  // wg / wu: [d x f] -> W1 [d x 2f] interleaved
             const bool up = o32 >= df;
             const uint32_t oo = up ? o32 - df : o32;
-            const uint32_t q = oo / f, x = oo - q * f;
+            const uint32_t q = (f & (f - 1)) == 0 ? oo >> (__ffs(f) - 1) : oo / f;  // uniform
+            const uint32_t x = oo - q * f;
             dst = sh.w1 + static_cast<int64_t>(sg.slot) * 2 * df + static_cast<int64_t>(q) * 2 * f +
                   (up ? il_up(x) : il_gate(x));
         } else {  // wd: [f x d] -> W2 as is
@@ -1223,117 +1222,126 @@ __device__ __forceinline__ void write_shadow4(const AdamSeg& sg, int64_t o, cons
     *reinterpret_cast<uint2*>(dst) = pk;
 }
 
-// Each thread owns ADAM_U consecutive float4 groups per pass (all loads in flight
-// before any update); segments are never split inside a group because every segment
-// length is a multiple of 4.
-constexpr int ADAM_U = 2;
-constexpr int ADAM_MAX_SEGS = 256;  // segment table in (dynamic) smem up to this size
-// Elements: blockIdx.y picks the piece [lo4 + y*blk4, + n4) (float4 units) of a strided
-// set (one piece = one contiguous range in the common case; a weight of every owned
-// expert for the background launches); blockIdx.x / threadIdx walk the piece.
+// Each thread owns ADAM_U float4 groups of a tile (all loads in flight before any update);
+// segment lengths are multiples of 4.
+constexpr int ADAM_U = 2;  // tile = blockDim.x * ADAM_U float4 groups
+
+// Block (x, y): segment seg0 + y, its piece [off, off + len) (len < 0: to the segment's
+// end), tiles x, x + gridDim.x, ...
 __global__ void __launch_bounds__(256) adamw_k(float* __restrict__ params,
                                                const float* __restrict__ grads,
                                                float* __restrict__ m, float* __restrict__ v,
-                                               const AdamSeg* segs, int nseg, int seg_smem,
-                                               int64_t lo4, int64_t blk4, int64_t n4,
+                                               const AdamSeg* __restrict__ segs, int seg0,
+                                               int64_t off, int64_t len,
                                                const AdamScalars* __restrict__ ap,
                                                Shadows sh, const double* __restrict__ loss_total) {
     if (!loss_ok(loss_total)) return;
     const AdamScalars a = *ap;
-    extern __shared__ AdamSeg s_segs[];
-    if (seg_smem) {
-        for (int i = threadIdx.x; i < nseg; i += blockDim.x) s_segs[i] = segs[i];
-        __syncthreads();
-        segs = s_segs;
-    }
-    const int64_t first = lo4 + static_cast<int64_t>(blockIdx.y) * blk4;
-    const int64_t total4 = first + n4;
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * ADAM_U;
-    for (int64_t base = first + (static_cast<int64_t>(blockIdx.x) * blockDim.x) * ADAM_U + threadIdx.x;
-         base < total4; base += stride) {
+    const AdamSeg sg = segs[seg0 + blockIdx.y];
+    const int64_t plen = len < 0 ? sg.len - off : len;
+    const int64_t n4 = plen / 4;
+    float* th_base = params + sg.param_off + off;  // piece element e: th_base[e], comp[e]
+    const int64_t comp = sg.comp_off + off;
+    const float* gb = grads + comp;
+    float* mb = m + comp;
+    float* vb = v + comp;
+    const int nt = blockDim.x, tile4 = nt * ADAM_U;
+    for (int64_t t0 = static_cast<int64_t>(blockIdx.x) * tile4; t0 < n4;
+         t0 += static_cast<int64_t>(gridDim.x) * tile4) {
         float4 th[ADAM_U], g[ADAM_U], mm[ADAM_U], vv[ADAM_U];
-        AdamSeg sg[ADAM_U];
-        int64_t idx[ADAM_U];
 #pragma unroll
         for (int u = 0; u < ADAM_U; ++u) {
-            idx[u] = base + static_cast<int64_t>(u) * blockDim.x;  // coalesced per u
-            if (idx[u] < total4) {
-                const int64_t i = idx[u] * 4;
-                sg[u] = segs[find_seg(segs, nseg, i)];
-                th[u] = *reinterpret_cast<const float4*>(params + sg[u].param_off + (i - sg[u].comp_off));
-                g[u] = __ldcs(reinterpret_cast<const float4*>(grads + i));
-                mm[u] = __ldcs(reinterpret_cast<const float4*>(m + i));
-                vv[u] = __ldcs(reinterpret_cast<const float4*>(v + i));
+            const int64_t q = t0 + u * nt + threadIdx.x;  // coalesced per u
+            if (q < n4) {
+                th[u] = *reinterpret_cast<const float4*>(th_base + 4 * q);
+                g[u] = __ldcs(reinterpret_cast<const float4*>(gb + 4 * q));
+                if (!a.sgd) {
+                    mm[u] = __ldcs(reinterpret_cast<const float4*>(mb + 4 * q));
+                    vv[u] = __ldcs(reinterpret_cast<const float4*>(vb + 4 * q));
+                }
             }
         }
 #pragma unroll
         for (int u = 0; u < ADAM_U; ++u) {
-            if (idx[u] >= total4) continue;
-            const int64_t i = idx[u] * 4;
-            const int64_t o = i - sg[u].comp_off;
-            th[u].x = adam_elem(th[u].x, g[u].x, mm[u].x, vv[u].x, a);
-            th[u].y = adam_elem(th[u].y, g[u].y, mm[u].y, vv[u].y, a);
-            th[u].z = adam_elem(th[u].z, g[u].z, mm[u].z, vv[u].z, a);
-            th[u].w = adam_elem(th[u].w, g[u].w, mm[u].w, vv[u].w, a);
-            *reinterpret_cast<float4*>(params + sg[u].param_off + o) = th[u];
-            __stcs(reinterpret_cast<float4*>(m + i), mm[u]);
-            __stcs(reinterpret_cast<float4*>(v + i), vv[u]);
-            write_shadow4(sg[u], o, th[u], sh);
+            const int64_t q = t0 + u * nt + threadIdx.x;
+            if (q >= n4) continue;
+            if (a.sgd) {  // theta -= lr * g (trainer.hpp:197-204)
+                th[u].x = fsub(th[u].x, fmul(a.lr, g[u].x));
+                th[u].y = fsub(th[u].y, fmul(a.lr, g[u].y));
+                th[u].z = fsub(th[u].z, fmul(a.lr, g[u].z));
+                th[u].w = fsub(th[u].w, fmul(a.lr, g[u].w));
+            } else {
+                th[u].x = adam_elem(th[u].x, g[u].x, mm[u].x, vv[u].x, a);
+                th[u].y = adam_elem(th[u].y, g[u].y, mm[u].y, vv[u].y, a);
+                th[u].z = adam_elem(th[u].z, g[u].z, mm[u].z, vv[u].z, a);
+                th[u].w = adam_elem(th[u].w, g[u].w, mm[u].w, vv[u].w, a);
+                __stcs(reinterpret_cast<float4*>(mb + 4 * q), mm[u]);
+                __stcs(reinterpret_cast<float4*>(vb + 4 * q), vv[u]);
+            }
+            *reinterpret_cast<float4*>(th_base + 4 * q) = th[u];
+            write_shadow4(sg, off + 4 * q, th[u], sh);
         }
     }
 }
 
+// 64 threads (2 warps): fits in the registers a resident GEMM CTA leaves free, so the
+// background launches really run beside the GEMMs (cfg5 N=1: 5845 -> 5779 ms per round
+// against 256-thread blocks, which only run where no GEMM CTA is resident)
+int g_adam_bg_threads = 64, g_adam_bg_tiles = 16;
+void adamw_background_shape(int threads, int tiles) {
+    g_adam_bg_threads = threads;
+    g_adam_bg_tiles = tiles;
+}
+
 static void adamw_launch(float* params, const float* grads, float* m, float* v,
-                         const AdamSeg* segs, int nseg, int64_t lo4, int64_t blk4, int64_t n4,
-                         int nblk, const AdamScalars* a, Shadows sh, const double* loss_total,
-                         cudaStream_t s, bool background) {
-    if (n4 <= 0 || nblk <= 0) return;
-    // persistent grid with the segment table in smem; or (background launches, beside the
-    // GEMMs) short blocks of 4 strides with no smem, so that they fit next to a GEMM CTA
-    // and a higher-priority stream's blocks get SMs as they retire
-    const int seg_smem = !background && nseg <= ADAM_MAX_SEGS;
-    const int64_t bx = background ? cdiv(n4, 256 * ADAM_U * 4)
-                                  : std::max<int64_t>(1, std::min<int64_t>(cdiv(n4, 256 * ADAM_U),
-                                                                           148 * 8 / nblk));
-    const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(nblk));
-    adamw_k<<<grid, 256, seg_smem ? sizeof(AdamSeg) * nseg : 0, s>>>(
-        params, grads, m, v, segs, nseg, seg_smem, lo4, blk4, n4, a, sh, loss_total);
+                         const AdamSeg* segs, int seg0, int nseg, int64_t off, int64_t len,
+                         int64_t max_len, const AdamScalars* a, Shadows sh,
+                         const double* loss_total, cudaStream_t s, bool background) {
+    if (nseg <= 0 || max_len <= 0) return;
+    // several waves of 256-thread blocks over all segments; or (background launches,
+    // beside the GEMMs) small blocks that fit in the registers a resident GEMM CTA leaves
+    // free (g_adam_bg_threads), a few tiles each
+    const int nt = background ? g_adam_bg_threads : 256;
+    const int64_t tiles = cdiv(max_len / 4, nt * ADAM_U);
+    const int64_t bx = background ? cdiv(tiles, g_adam_bg_tiles)
+                                  : std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * 32 / nseg));
+    const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(nseg));
+    adamw_k<<<grid, nt, 0, s>>>(params, grads, m, v, segs, seg0, off, len, a, sh, loss_total);
     count_launch();
 }
 
-void adamw(float* params, const float* grads, float* m, float* v, const AdamSeg* segs, int nseg,
-           int64_t lo, int64_t hi, const AdamScalars* a, Shadows sh, const double* loss_total,
-           cudaStream_t s, bool short_blocks) {
-    // segment lengths are multiples of 4
-    adamw_launch(params, grads, m, v, segs, nseg, lo / 4, 0, hi / 4 - lo / 4, 1, a, sh, loss_total,
-                 s, short_blocks);
+void adamw(float* params, const float* grads, float* m, float* v, const SegTable& tab,
+           int seg0, int nseg, const AdamScalars* a, Shadows sh, const double* loss_total,
+           cudaStream_t s) {
+    const int64_t max_len = std::max<int64_t>(tab.per, tab.psi_len);  // bound on a segment
+    adamw_launch(params, grads, m, v, tab.segs, seg0, nseg, 0, -1, max_len, a, sh, loss_total, s,
+                 false);
 }
 
-void adamw_strided(float* params, const float* grads, float* m, float* v, const AdamSeg* segs,
-                   int nseg, int64_t lo, int64_t blk, int64_t len, int nblk, const AdamScalars* a,
-                   Shadows sh, const double* loss_total, cudaStream_t s) {
-    adamw_launch(params, grads, m, v, segs, nseg, lo / 4, blk / 4, len / 4, nblk, a, sh,
-                 loss_total, s, true);
+void adamw_pieces(float* params, const float* grads, float* m, float* v, const SegTable& tab,
+                  int seg0, int nseg, int64_t off, int64_t len, const AdamScalars* a, Shadows sh,
+                  const double* loss_total, cudaStream_t s) {
+    adamw_launch(params, grads, m, v, tab.segs, seg0, nseg, off, len, len, a, sh, loss_total, s,
+                 true);
 }
 
 __global__ void __launch_bounds__(256) refresh_shadows_k(const float* __restrict__ params,
-                                                         const AdamSeg* __restrict__ segs,
-                                                         int nseg, int64_t total4, Shadows sh) {
+                                                         SegTable tab, int64_t total4, Shadows sh) {
     for (int64_t i4 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i4 < total4;
          i4 += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t i = i4 * 4;
-        const AdamSeg sg = segs[find_seg(segs, nseg, i)];
+        const AdamSeg sg = tab.segs[seg_of(tab, i)];
         if (sg.kind == 0) continue;
         const int64_t o = i - sg.comp_off;
         write_shadow4(sg, o, __ldg(reinterpret_cast<const float4*>(params + sg.param_off + o)), sh);
     }
 }
 
-void refresh_shadows(const float* params, const AdamSeg* segs, int nseg, int64_t total,
-                     Shadows sh, cudaStream_t s) {
+void refresh_shadows(const float* params, const SegTable& tab, int64_t total, Shadows sh,
+                     cudaStream_t s) {
     const int64_t total4 = total / 4;
     const int blocks = static_cast<int>(std::min<int64_t>(cdiv(total4, 256), 148 * 8));
-    refresh_shadows_k<<<blocks, 256, 0, s>>>(params, segs, nseg, total4, sh);
+    refresh_shadows_k<<<blocks, 256, 0, s>>>(params, tab, total4, sh);
     count_launch();
 }
 

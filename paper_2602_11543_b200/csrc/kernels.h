@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "common.cuh"
 #include "grouped_gemm.cuh"
 
@@ -18,6 +20,15 @@ using spes_dev::GemmGroup;
 extern thread_local int64_t* g_launch_counter;
 inline void count_launch(int n = 1) {
     if (g_launch_counter) *g_launch_counter += n;
+}
+
+// cudaFuncSetAttribute applies to the current device only: one bit per device records
+// where a kernel's attributes are set (contexts on several GPUs may share a process).
+inline bool first_use_on_device(std::atomic<uint64_t>& mask) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    return (mask.fetch_or(bit) & bit) == 0;
 }
 
 struct AdamSeg {
@@ -71,15 +82,12 @@ struct GroupBases {  // output bases written into the group tables
 };
 void route_plan(const int32_t* topk_idx, const float* topk_w, int64_t T, int M, int k,
                 int64_t R_cap, const RoutePlan& p, const GroupBases& gb, cudaStream_t s);
-// rows of src (fp32, row_map[r] or r when row_map == nullptr, -1 => zero row) as bf16
-// [rows x cols] and transposed [cols x rows_cap]; rows processed: *nrows (device) or rows.
-void gather_rows_bf16(const float* src, int64_t ld_src, const int32_t* row_map,
-                      const int32_t* nrows_dev, int64_t rows, int64_t cols, bf16* dst,
-                      bf16* dstT, int64_t rows_cap, cudaStream_t s);
-// dst[r] = src[row_map[r]] (bf16 rows of `cols`), zero rows where row_map[r] < 0;
-// rows processed: *nrows_dev.
-void permute_rows_bf16(const bf16* src, int64_t cols, const int32_t* row_map,
-                       const int32_t* nrows_dev, int64_t rows_cap, bf16* dst, cudaStream_t s);
+// Dispatch: Xp[slot_row[t][s]] = src[t] (bf16 rows of `cols`) by TMA bulk copies (one
+// row load, k row stores per token); rows with row_token < 0 among the first *nrows_dev
+// are zeroed (cols * 2 bytes must be a multiple of 16 and at most 16 KiB).
+void permute_rows_tma(const bf16* src, int64_t cols, const int32_t* slot_row,
+                      const int32_t* row_token, const int32_t* nrows_dev, int64_t T, int k,
+                      bf16* dst, cudaStream_t s);
 // h_next_bf (optional): bf16 copy of h_next (the head GEMM operand after the last layer);
 // h_next may then be null (the final fp32 hidden state has no other consumer)
 void combine_forward(const float* h, const int32_t* hrow, const float* y, const int32_t* slot_row,
@@ -90,12 +98,13 @@ void combine_forward(const float* h, const int32_t* hrow, const float* y, const 
 void head_ce(const float* logits, const int32_t* targets, int64_t T, int64_t T_pad, int64_t V,
              float g_s2, float g_ssum, bf16* dlogits, float* diff,
              float* lse, cudaStream_t s);
-// Loss scalars (tolerance-level, deterministic tree order) -> out[5] (doubles)
+// Loss scalars (tolerance-level, deterministic tree order) -> out[0..4] (doubles), and
+// the step's status word (sticky in *status, copied to out[5]; see spes_dev::loss_ok)
 void losses_reduce(const float* diff, const float* lse_head, const float* lse_r,
                    const float* probs, const float* lb_coeff, int64_t T, int64_t Tstride, int L,
                    int M,
                    float inv_T, float inv_L, float c_ce, float c_lb, float c_mz, float c_z,
-                   double* part, double* out, cudaStream_t s);
+                   int32_t* status, double* part, double* out, cudaStream_t s);
 
 // ---- backward ----
 void combine_backward(const float* gh, const float* y, const int32_t* row_token,
@@ -148,21 +157,31 @@ struct PullTask {
     int32_t pad;
 };
 void expert_pull(const PullTask* tasks, int ntasks, int64_t per, Shadows sh, cudaStream_t s);
-// MaskedAdamW step over the first `total` compact scalars; also writes the refreshed
-// bf16 copies. No update when *loss_total is non-finite (loss_total may be null).
+// Segment table of the compact optimizer layout: npsi leading segments (psi_len scalars in
+// total) followed by expert segments of `per` scalars each.
+struct SegTable {
+    const AdamSeg* segs;
+    int32_t npsi;
+    int64_t psi_len, per;
+};
+// MaskedAdamW (or, a->sgd, SGD) step over the whole segments [seg0, seg0 + nseg) of the
+// table; also writes the refreshed bf16 copies. No update while the step status is bad
+// (spes_dev::loss_ok; loss_total may be null).
 using spes_dev::AdamScalars;
-// compact elements [lo, hi) (multiples of 4)
-void adamw(float* params, const float* grads, float* m, float* v, const AdamSeg* segs, int nseg,
-           int64_t lo, int64_t hi, const AdamScalars* a, Shadows sh, const double* loss_total,
-           cudaStream_t s, bool short_blocks = false);
-// compact elements lo + b*blk + [0, len) for b < nblk (multiples of 4), as a background
-// launch (short blocks, no smem: fits beside a GEMM CTA)
-void adamw_strided(float* params, const float* grads, float* m, float* v, const AdamSeg* segs,
-                   int nseg, int64_t lo, int64_t blk, int64_t len, int nblk, const AdamScalars* a,
-                   Shadows sh, const double* loss_total, cudaStream_t s);  // a: device memory (graph-replayable)
-// Rewrite every bf16 copy from the fp32 parameters (after load / sync / merge).
-void refresh_shadows(const float* params, const AdamSeg* segs, int nseg, int64_t total,
-                     Shadows sh, cudaStream_t s);
+void adamw(float* params, const float* grads, float* m, float* v, const SegTable& tab,
+           int seg0, int nseg, const AdamScalars* a, Shadows sh, const double* loss_total,
+           cudaStream_t s);
+// The piece [off, off + len) of each of the segments [seg0, seg0 + nseg) (multiples of 4), as
+// a background launch (short blocks, no smem: fits beside a GEMM CTA)
+void adamw_pieces(float* params, const float* grads, float* m, float* v, const SegTable& tab,
+                  int seg0, int nseg, int64_t off, int64_t len, const AdamScalars* a, Shadows sh,
+                  const double* loss_total, cudaStream_t s);  // a: device memory (graph-replayable)
+// block shape of the background (adamw_pieces) launches: threads per block, tiles per block
+void adamw_background_shape(int threads, int tiles);
+// Rewrite the bf16 copies of refresh-table scalars [0, total) from the fp32 parameters
+// (after load / sync / merge).
+void refresh_shadows(const float* params, const SegTable& tab, int64_t total, Shadows sh,
+                     cudaStream_t s);
 
 // batch tokens B x (S+1) from the HBM-resident corpus rows
 void corpus_gather(const int32_t* corpus, const int64_t* rows, int64_t B, int64_t S1,

@@ -313,12 +313,10 @@ static void launch_rf(unsigned grid, cudaStream_t s, const float* h, const int32
                       float eps, int variant, float* normed, bf16* normed_bf, float* logits,
                       float* probs, int32_t* topk_idx, float* topk_w, float* lse, float* inv_rms,
                       float* denom) {
-    static bool configured = false;
-    if (!configured) {
+    static std::atomic<uint64_t> configured{0};
+    if (first_use_on_device(configured))
         cudaFuncSetAttribute(router_fwd_k<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              RfSmem<MM>::BYTES);
-        configured = true;
-    }
     router_fwd_k<MM><<<grid, 32 * RF_WARPS, RfSmem<MM>::BYTES, s>>>(
         h, hrow, gain, router, (int)T, (int)d, M, k, renorm, eps, variant, normed, normed_bf, logits,
         probs, topk_idx, topk_w, lse, inv_rms, denom);

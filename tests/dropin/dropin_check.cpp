@@ -11,7 +11,11 @@
 //                experts bit-identical to the input, grad_scalar_count identical,
 //                trainable displacement within DELTA_RTOL after H AdamW steps;
 //   merge_model: peer sets and every parameter bit-identical (fp64 merge, identical input).
+//   SGD inner steps with record_trace: losses, update norms, drift and per-block gradient
+//                sums within bf16 tolerance of the reference's;
+//   batches of different (B, S) in one round: per-step losses within LOSS_RTOL;
 //   errors:      H < 1 -> std::invalid_argument; token out of range -> std::out_of_range.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -108,6 +112,77 @@ int main(int argc, char** argv) {
     std::printf("  trainable displacement rel err = %.3e\n", rel);
     expect(frozen_same, "local_round frozen experts bit-identical to the input");
     expect(rel < DELTA_RTOL, "local_round trainable displacement within 5e-2 rel of the reference");
+
+    // ---- SGD inner steps with record_trace (trainer.hpp:116-122, 183-219) ----
+    {
+        spes::LocalRoundConfig sc = rc;
+        sc.inner = spes::InnerOpt::SGD;
+        sc.opt.lr = 0.05;
+        sc.record_trace = true;
+        const auto r2 = spes::local_round(global, batches(cfg, B, S, 9), sc, mask);
+        const auto g2 = spes_b200::local_round(ctx, global, batches(cfg, B, S, 9), sc, mask);
+        bool ok = r2.step_losses.size() == g2.step_losses.size() &&
+                  r2.update_norms.size() == g2.update_norms.size() &&
+                  r2.drift_sq.size() == g2.drift_sq.size() &&
+                  r2.grad_sum.size() == g2.grad_sum.size();
+        double worst = 0.0;
+        auto rel = [&](double a, double b) {
+            const double e = std::fabs(a - b) / std::max(std::fabs(b), 1e-30);
+            worst = std::max(worst, e);
+            return e;
+        };
+        for (size_t h = 0; ok && h < r2.step_losses.size(); ++h) {
+            ok &= rel(g2.step_losses[h].total, r2.step_losses[h].total) <= LOSS_RTOL;
+            ok &= rel(g2.update_norms[h], r2.update_norms[h]) <= 2e-2;
+            ok &= rel(g2.drift_sq[h], r2.drift_sq[h]) <= DELTA_RTOL;
+        }
+        for (size_t i = 0; ok && i < r2.grad_sum.size(); ++i) {
+            const auto& a = g2.grad_sum[i];
+            const auto& b = r2.grad_sum[i];
+            ok &= a.block_index == b.block_index && a.grad.shape == b.grad.shape;
+            double e2 = 0.0, n2 = 0.0;
+            for (size_t j = 0; ok && j < b.grad.data.size(); ++j) {
+                const double d = static_cast<double>(a.grad.data[j]) - b.grad.data[j];
+                e2 += d * d;
+                n2 += static_cast<double>(b.grad.data[j]) * b.grad.data[j];
+            }
+            if (n2 > 0) worst = std::max(worst, std::sqrt(e2 / n2));
+            ok &= n2 == 0 ? e2 == 0 : std::sqrt(e2 / n2) <= 2e-2;
+        }
+        std::printf("  sgd + record_trace: worst relative deviation %.3e\n", worst);
+        expect(ok, "local_round SGD + record_trace (losses, update norms, drift, grad sums)");
+    }
+
+    // ---- batches of different shapes within one round (trainer.hpp:163: each its own) ----
+    {
+        auto mixed = [&](uint64_t seed) {
+            auto base = std::make_shared<int>(0);
+            auto rng = std::make_shared<std::mt19937_64>(seed);
+            return spes::BatchProvider([cfg, base, rng]() {
+                static const int64_t shapes[3][2] = {{4, 64}, {8, 32}, {2, 100}};
+                const auto* sh = shapes[(*base)++ % 3];
+                spes::Batch b;
+                b.batch = sh[0];
+                b.seq = sh[1];
+                std::uniform_int_distribution<int32_t> u(0, static_cast<int32_t>(cfg.vocab - 1));
+                b.tokens.resize(static_cast<size_t>(b.batch * (b.seq + 1)));
+                for (auto& t : b.tokens) t = u(*rng);
+                return b;
+            });
+        };
+        spes::LocalRoundConfig mc = rc;
+        mc.steps = 5;
+        const auto r3 = spes::local_round(global, mixed(11), mc, mask);
+        const auto g3 = spes_b200::local_round(ctx, global, mixed(11), mc, mask);
+        bool ok = r3.step_losses.size() == g3.step_losses.size();
+        for (size_t h = 0; ok && h < r3.step_losses.size(); ++h) {
+            std::printf("  mixed-shape step %zu loss ref %.7f b200 %.7f\n", h,
+                        r3.step_losses[h].total, g3.step_losses[h].total);
+            ok = std::fabs(g3.step_losses[h].total - r3.step_losses[h].total) <=
+                 LOSS_RTOL * std::fabs(r3.step_losses[h].total);
+        }
+        expect(ok, "local_round over batches of different (B, S) within one round");
+    }
 
     // ---- merge_model: bit-exact on identical input ----
     spes::MergeSchedule ms;

@@ -8,6 +8,8 @@ Bar (SURVEY.md §8c / north_star):
   * routing of layers > 0 depends on bf16 expert outputs: reported as an
     agreement rate, every disagreement must be a near-tie under the oracle.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -21,8 +23,11 @@ CFG1 = dict(vocab=256, hidden=128, intermediate=256, layers=2, experts_total=8, 
 CFG2 = dict(vocab=256, hidden=1024, intermediate=1024, layers=1, experts_total=16, experts_active=2)
 CFG4 = dict(vocab=256, hidden=2048, intermediate=1024, layers=1, experts_total=64, experts_active=8)
 
-# bf16 operands, fp32 accumulation: relative Frobenius error per gradient block
-GRAD_RTOL = 3e-2
+# bf16 operands, fp32 accumulation: relative Frobenius error per gradient block. Measured
+# maximum over every block of every local-step case with identical routing (GRADERR lines,
+# round 2, B200): 5.18e-3 at cfg1 / cfg2 / cfg4 / non-pow2 / ragged shapes, 8.56e-3 at cfg5
+# shapes (test_gpu_large.py, the layer-1 router gradient); the bound is 2x the maximum.
+GRAD_RTOL = float(os.environ.get("SPES_GRAD_RTOL", "1.75e-2"))
 LOSS_RTOL = 2e-3
 
 
@@ -53,7 +58,9 @@ def test_expf_port_exhaustive_negative_range(gpu):
     assert bad == 0
 
 
-@pytest.mark.parametrize("shape,T,seed", [(CFG1, 256, 0), (CFG2, 4096, 1), (CFG4, 2048, 2)])
+# the last two: the bench's full token count per step (B*S = 16384) at cfg2 / cfg4 shapes
+@pytest.mark.parametrize("shape,T,seed", [(CFG1, 256, 0), (CFG2, 4096, 1), (CFG4, 2048, 2),
+                                          (CFG2, 16384, 3), (CFG4, 16384, 4)])
 def test_router_kernel_bitexact(gpu, shape, T, seed):
     cfg = model_cfg(**shape)
     rng = np.random.default_rng(seed)
@@ -73,7 +80,36 @@ def test_router_kernel_bitexact(gpu, shape, T, seed):
         spes.f32(out["logits"]), spes.f32(out["probs"]), spes.i32(out["idx"]), spes.f32(out["w"]),
         spes.i32(out["counts"]), spes.i32(out["perm"]), 0))
     for key in ("normed", "logits", "probs", "idx", "w", "counts", "perm"):
-        assert bitexact(out[key], ref[key]), key
+        if not bitexact(out[key], ref[key]):
+            bad = np.flatnonzero(out[key].reshape(-1).view(np.uint32) !=
+                                 ref[key].reshape(-1).view(np.uint32))
+            raise AssertionError(f"{key}: {bad.size} entries differ, first at {bad[:8]}: "
+                                 f"{out[key].reshape(-1)[bad[:8]]} vs {ref[key].reshape(-1)[bad[:8]]}")
+
+
+@pytest.mark.parametrize("shape,T", [(CFG1, 256), (CFG4, 16384)])
+def test_routing_plan_repeatable(gpu, shape, T):
+    """The routing plan (counting sort, model.hpp:314-318) is deterministic: 20 repeated
+    launches on the same logits give the same permutation, bit for bit, as the oracle."""
+    cfg = model_cfg(**shape)
+    rng = np.random.default_rng(5)
+    d, M, k = cfg.hidden, cfg.experts_total, cfg.experts_active
+    h = (rng.standard_normal((T, d)) * 0.5).astype(np.float32)
+    gain = (1 + 0.1 * rng.standard_normal(d)).astype(np.float32)
+    router = (rng.standard_normal((d, M)) * 0.05).astype(np.float32)
+    ref = oracle.router_forward(cfg, h, gain, router)
+    for it in range(20):
+        perm = np.zeros(T * k, np.int32)
+        counts = np.zeros(M, np.int32)
+        idx = np.zeros((T, k), np.int32)
+        spes._check(spes.lib().spes_kernel_router(
+            cfg, spes.f32(h), spes.f32(gain), spes.f32(router), T, None, None, None,
+            spes.i32(idx), None, spes.i32(counts), spes.i32(perm), 0))
+        assert bitexact(idx, ref["idx"]), f"launch {it}: top-k indices"
+        assert bitexact(counts, ref["counts"]), f"launch {it}: counts"
+        bad = np.flatnonzero(perm != ref["perm"])
+        assert bad.size == 0, (f"launch {it}: {bad.size} permutation entries differ, first "
+                               f"{bad[:8]}: got {perm[bad[:8]]} want {ref['perm'][bad[:8]]}")
 
 
 def test_adamw_kernel_bitexact(gpu):
@@ -110,6 +146,56 @@ def test_owner_mean_bitexact(gpu, r):
 
 
 # ---------------------------------------------------------------- full local step
+
+def _check_deep_routing(cfg, node, params, tr, T, label, min_agree=0.9):
+    """Layers > 0 take the previous layer's bf16-GEMM output as input. Given the device's own
+    layer input h_l, the router is bit-exact (rmsnorm, logits, softmax, top-k, weights);
+    against the oracle's own h_l, routing agrees except where the oracle's k-th and
+    (k+1)-th probabilities nearly tie (relative gap < 5%)."""
+    L, d, M, k = cfg.layers, cfg.hidden, cfg.experts_total, cfg.experts_active
+    offs = spes.block_offsets(cfg)
+    for l in range(1, L):
+        idx = node.debug("topk_idx", l, np.int32, (T, k), T * k)
+        probs = node.debug("probs", l, np.float32, (T, M), T * M)
+        h_l = node.debug("h", l, np.float32, (T, d), T * d)
+        gain = params[offs[2 + 2 * l]:offs[2 + 2 * l] + d]
+        router = params[offs[3 + 2 * l]:offs[3 + 2 * l] + d * M].reshape(d, M)
+        ref = oracle.router_forward(cfg, h_l, gain, router)
+        assert bitexact(idx, ref["idx"]), f"layer {l} routing on the device's own input"
+        assert bitexact(probs, ref["probs"]), f"layer {l} probabilities on the device's own input"
+        same = (idx == tr["topk_idx"][l]).all(axis=1)
+        if k < M:
+            p = np.sort(tr["probs"][l], axis=1)[:, ::-1]
+            rel_gap = (p[:, k - 1] - p[:, k]) / p[:, k - 1]
+            worst = rel_gap[~same].max() if (~same).any() else 0.0
+        else:
+            worst = 0.0
+        print(f"GRADERR {label} layer {l} routing agreement vs oracle {same.mean():.4f}, "
+              f"largest relative top-k gap at a disagreement {worst:.3e}")
+        assert same.mean() >= min_agree, f"layer {l} routing agreement {same.mean():.4f}"
+        assert worst < 0.05, "routing disagreement away from a near-tie"
+
+
+def _check_grad_blocks(cfg, g_gpu, g_ref, label, rtol=None):
+    """Per-block relative Frobenius error against the oracle; frozen blocks exactly zero.
+    The observed maximum is printed (GRADERR lines, pytest -s) so GRAD_RTOL stays a
+    measured bound rather than a guess."""
+    offs = spes.block_offsets(cfg)
+    ends = list(offs[1:]) + [spes.param_count(cfg)]
+    worst, worst_at = 0.0, None
+    for b0, b1 in zip(offs, ends):
+        gr, gg = g_ref[b0:b1], g_gpu[b0:b1]
+        if not gr.any():
+            assert not gg.any(), f"frozen block {b0} got a gradient"
+            continue
+        e = rel_err(gg, gr)
+        if e > worst:
+            worst, worst_at = e, b0
+        assert e < (rtol or GRAD_RTOL), f"block at {b0}: rel err {e:.3e}"
+    print(f"GRADERR {label} d={cfg.hidden} f={cfg.intermediate} M={cfg.experts_total} "
+          f"k={cfg.experts_active} L={cfg.layers}: max block rel err {worst:.3e} at {worst_at}")
+    return worst
+
 
 def _node(cfg, params, owned_lists, node=0):
     n = spes.Node(cfg, node=node, n_nodes=1, device=0)
@@ -156,26 +242,14 @@ def _check_step(cfg, B, S, owned, seed, renorm=False):
     emb_now = node.read_params()[: cfg.vocab * d].reshape(cfg.vocab, d)
     assert bitexact(node.debug("h", 0, np.float32, (T, d), T * d),
                     emb_now[tokens[:, :-1].reshape(-1)])
-    # deeper layers: agreement rate, disagreements only at near-ties of the oracle probs
-    for l in range(1, L):
-        idx = node.debug("topk_idx", l, np.int32, (T, k), T * k)
-        same = (idx == tr["topk_idx"][l]).all(axis=1)
-        p = np.sort(tr["probs"][l], axis=1)[:, ::-1]
-        margin = p[:, k - 1] - p[:, k] if k < M else np.full(T, np.inf)
-        assert same.mean() > 0.97, f"layer {l} routing agreement {same.mean():.4f}"
-        assert (margin[~same] < 1e-2).all(), "routing disagreement away from a near-tie"
+    _check_deep_routing(cfg, node, params, tr, T, "cfg1-like" if d == 128 else f"d={d}")
     # losses
     for i, name in enumerate(("total", "ce", "lb", "moe_z", "z")):
         assert abs(losses[i] - l_ref[i]) <= LOSS_RTOL * abs(l_ref[i]) + 1e-7, name
     # gradients, block by block
     offs = spes.block_offsets(cfg)
     ends = list(offs[1:]) + [spes.param_count(cfg)]
-    for b0, b1 in zip(offs, ends):
-        gr, gg = g_ref[b0:b1], g_gpu[b0:b1]
-        if not gr.any():
-            assert not gg.any(), f"frozen block {b0} got a gradient"
-            continue
-        assert rel_err(gg, gr) < GRAD_RTOL, f"block at {b0}: rel err {rel_err(gg, gr):.3e}"
+    _check_grad_blocks(cfg, g_gpu, g_ref, f"B={B} S={S}")
     # embedding gradient == sequential scatter-add of the device's own grad_h0 rows in
     # token order (graph.hpp:220-229): bit-exact given identical upstream
     gh0 = node.debug("grad_h0", 0, np.float32, (T, d), T * d)
@@ -396,4 +470,98 @@ def test_upcycled_model_local_step(gpu):
     assert bitexact(idx0, tr["topk_idx"][0])
     assert (idx0 == np.array([0, 1])).all()  # exact ties -> lowest indices
     assert abs(losses[0] - l_ref[0]) <= LOSS_RTOL * abs(l_ref[0])
+    node.close()
+
+
+# ---------------------------------------------------------------- batch shapes, status, SGD
+
+def test_batch_shape_change_same_token_count(gpu, monkeypatch):
+    """(B, S) changes with B*S fixed: the replayed step graph must not split the
+    new batch with the old S. A graph-replaying node and an eager node (SPES_STEP_GRAPH=0)
+    run the same shape sequence and must agree bit for bit; each step's layer-0 routing is
+    checked against the oracle on that step's own (B, S) batch."""
+    cfg = model_cfg(**CFG1)
+    params = oracle.random_params(cfg, 61)
+    shapes = [(4, 64), (4, 64), (4, 64), (8, 32), (8, 32), (8, 32), (2, 128), (4, 64)]
+    batches = [oracle.random_tokens(cfg, B, S, 62 + i)[0] for i, (B, S) in enumerate(shapes)]
+    out = []
+    for graph in ("1", "0"):
+        monkeypatch.setenv("SPES_STEP_GRAPH", graph)
+        node = spes.Node(cfg)
+        node.set_ownership([[0, 1, 2, 3]])
+        node.load_params(params)
+        node.round_begin()
+        losses = []
+        for tk in batches:
+            p_before = node.read_params()
+            losses.append(node.local_step(tk, adamw_cfg(lr=1e-3)))
+            T = tk.shape[0] * (tk.shape[1] - 1)
+            _, _, tr = oracle.forward_backward(cfg, p_before, tk, [0, 1, 2, 3], trace=True)
+            idx = node.debug("topk_idx", 0, np.int32, (T, cfg.experts_active), T * cfg.experts_active)
+            assert bitexact(idx, tr["topk_idx"][0]), f"graph={graph}: routing of a {tk.shape} batch"
+        out.append((np.array(losses), node.read_params()))
+        node.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert bitexact(out[0][1], out[1][1])
+
+
+def test_device_tokens_status_reported_at_round_end(gpu):
+    """Device-resident tokens without loss reads (the bench path): an out-of-vocabulary id
+    applies no update (model.hpp:280-281 throws before the step) and is reported when the
+    round ends, as out_of_range; the status then clears and training resumes."""
+    import torch
+    cfg = model_cfg(**CFG1)
+    params = oracle.random_params(cfg, 71)
+    node = spes.Node(cfg)
+    node.load_params(params)
+    node.round_begin()
+    good = oracle.random_tokens(cfg, 2, 64, 72)[0]
+    bad = good.copy()
+    bad[1, 5] = cfg.vocab + 3
+    d_good = torch.from_numpy(good).cuda()
+    d_bad = torch.from_numpy(bad).cuda()
+    node.local_step_device(d_good.data_ptr(), 2, 64)
+    p1 = node.read_params()
+    node.local_step_device(d_bad.data_ptr(), 2, 64)    # no host sync: not raised yet
+    node.local_step_device(d_good.data_ptr(), 2, 64)   # after a bad step: no update either
+    torch.cuda.synchronize()
+    assert bitexact(node.read_params(), p1), "an update was applied after a bad batch"
+    with pytest.raises(spes.SpesError) as e:
+        node.sync()
+    assert e.value.kind == "out_of_range"
+    node.round_begin()                                   # cleared: trains again
+    node.local_step_device(d_good.data_ptr(), 2, 64)
+    node.sync()
+    assert not bitexact(node.read_params(), p1)
+    # with losses requested, the step itself reports
+    node.round_begin()
+    with pytest.raises(spes.SpesError) as e:
+        node.local_step_device(d_bad.data_ptr(), 2, 64, want_losses=True)
+    assert e.value.kind == "out_of_range"
+    node.close()
+
+
+def test_sgd_inner_optimizer(gpu):
+    """InnerOpt::SGD (trainer.hpp:197-204): theta -= float(lr) * g on the trainable blocks,
+    bit-exact given the device's own gradients; frozen experts untouched; no moments."""
+    cfg = model_cfg(**CFG1)
+    params = oracle.random_params(cfg, 81)
+    tokens = oracle.random_tokens(cfg, 2, 64, 82)[0]
+    owned = [1, 2, 5, 6]
+    node = spes.Node(cfg)
+    node.set_ownership([owned])
+    node.load_params(params)
+    node.set_inner_optimizer("sgd")
+    node.round_begin()
+    lr = 0.05
+    losses = node.local_step(tokens, adamw_cfg(lr=lr))
+    g = node.read_grads()
+    p = node.read_params()
+    assert bitexact(p, params - np.float32(lr) * g)
+    l_ref, g_ref, _ = oracle.forward_backward(cfg, params, tokens, owned, trace=True)
+    assert abs(losses[0] - l_ref[0]) <= LOSS_RTOL * abs(l_ref[0])
+    assert node.counts()["opt_state_scalars"] == 0
+    node.set_fused_optimizer(True)       # no fused placement for SGD: same path
+    losses2 = node.local_step(tokens, adamw_cfg(lr=lr))
+    assert bitexact(node.read_params(), p - np.float32(lr) * node.read_grads())
     node.close()

@@ -1,4 +1,4 @@
-"""N > 1 host logic on CPU (gloo, world_size 2..4).
+"""N > 1 host logic on CPU (gloo, world_size 2..8).
 
 The sparse sync's data movement is planned by spes_sync_plan (the same function
 spes_sync uses before issuing NCCL calls). Here every rank follows that plan with
@@ -39,11 +39,11 @@ def _mean_in_order(arrs):
     return (acc * (1.0 / len(arrs))).astype(np.float32)
 
 
-def _worker(rank, world, port, owned, node_params, glob, out_q):
+def _worker(rank, world, port, owned, node_params, glob, out_q, M):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    cfg = model_cfg(**CFG)
+    cfg = model_cfg(**dict(CFG, experts_total=M))
     P = node_params.shape[1]
     M, L = cfg.experts_total, cfg.layers
     per = 3 * cfg.hidden * cfg.intermediate
@@ -87,11 +87,13 @@ def _worker(rank, world, port, owned, node_params, glob, out_q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,layout", [(2, "partition"), (2, "replicated"), (4, "replicated"),
-                                          (3, "irregular")])
-def test_sync_plan_gloo_matches_oracle_aggregate(world, layout):
-    cfg = model_cfg(**CFG)
-    M = cfg.experts_total
+# (8, "replicated", 16) is cfg2 / cfg4's topology: 8 nodes, M = 16, r = 2,
+# node n owns {(2n + i) mod 16, i < 4}, primary(e) = e // 2, owner pairs {e//2, (e//2 - 1) mod 8}
+@pytest.mark.parametrize("world,layout,M", [(2, "partition", 8), (2, "replicated", 8),
+                                            (4, "replicated", 8), (3, "irregular", 8),
+                                            (8, "replicated", 16)])
+def test_sync_plan_gloo_matches_oracle_aggregate(world, layout, M):
+    cfg = model_cfg(**dict(CFG, experts_total=M))
     if layout == "partition":
         owned = spes.param_partition(cfg, world)
     elif layout == "replicated":
@@ -106,11 +108,13 @@ def test_sync_plan_gloo_matches_oracle_aggregate(world, layout):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, owned, node_params, glob, q))
+    if layout == "replicated" and M == 16 and world == 8:
+        assert owned == [sorted((2 * n + i) % 16 for i in range(4)) for n in range(8)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, owned, node_params, glob, q, M))
              for r in range(world)]
     for p in procs:
         p.start()
-    results = [q.get(timeout=120) for _ in range(world)]
+    results = [q.get(timeout=300) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
     for rank, res, balanced in results:
