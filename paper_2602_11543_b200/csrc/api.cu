@@ -90,7 +90,8 @@ Layout layout_of(const spes_model_cfg* c) {
                   c->experts_active};
 }
 
-// ModelConfig::validate (model.hpp:33-40) + B200 tiling constraints.
+// ModelConfig::validate (model.hpp:33-40) + the B200 routing limits. Hidden, intermediate
+// and vocab sizes are free: the device layout pads them to the tcgen05 tile (device_cfg).
 void validate_cfg(const spes_model_cfg* c) {
     if (!c) fail(SPES_INVALID_ARGUMENT, "model config: null");
     if (c->vocab < 1 || c->hidden < 1 || c->intermediate < 1 || c->layers < 1)
@@ -100,14 +101,50 @@ void validate_cfg(const spes_model_cfg* c) {
     if (c->coeff_ce < 0 || c->coeff_lb < 0 || c->coeff_moe_z < 0 || c->coeff_z < 0)
         throw std::invalid_argument("model config: loss coefficients must be >= 0");
     if (c->tied_head) throw std::logic_error("tied head not implemented");
-    if (c->hidden % 128 || c->intermediate % 128 || c->vocab % 128)
-        fail(SPES_INVALID_ARGUMENT,
-             "B200 path: hidden, intermediate and vocab must be multiples of 128 (tcgen05 tiles)");
     if (c->experts_total > 64 || c->experts_active > 8)
         fail(SPES_INVALID_ARGUMENT, "B200 path: experts_total <= 64 and experts_active <= 8");
 }
 
 int bn_for(int64_t n) { return (n % 256 == 0) ? 256 : 128; }
+
+// The device model: hidden, intermediate and vocab rounded up to the 128-wide tcgen05 tile.
+// Padded rows / columns of every block are zeros and stay zeros (their gradients are zero,
+// so AdamW / SGD / sync / merge keep them at zero); the rmsnorm mean divides by the true
+// hidden size and the softmax-CE masks the padded vocabulary columns, so the padded model
+// computes the caller's model exactly (parameter I/O converts between the layouts).
+spes_model_cfg device_cfg(const spes_model_cfg* c) {
+    spes_model_cfg p = *c;
+    p.hidden = (c->hidden + 127) / 128 * 128;
+    p.intermediate = (c->intermediate + 127) / 128 * 128;
+    p.vocab = (c->vocab + 127) / 128 * 128;
+    return p;
+}
+
+// Copy between the caller's layout (enumerate_blocks of its config, `u`) and the padded
+// device layout (`p`, zero-filled by the caller when to_dev): every block is a row-major
+// matrix whose rows and columns both may be padded.
+void convert_layout(const Layout& U, const Layout& D, const float* src, float* dst, bool to_dev) {
+    auto block = [&](int64_t uo, int64_t po, int64_t ur, int64_t uc, int64_t pc) {
+        for (int64_t r = 0; r < ur; ++r) {
+            const float* a = to_dev ? src + uo + r * uc : src + po + r * pc;
+            float* b = to_dev ? dst + po + r * pc : dst + uo + r * uc;
+            std::memcpy(b, a, sizeof(float) * uc);
+        }
+    };
+    block(U.off_emb(), D.off_emb(), U.V, U.d, D.d);     // emb [V x d]
+    block(U.off_head(), D.off_head(), U.d, U.V, D.V);   // head [d x V]
+    for (int l = 0; l < U.L; ++l) {
+        block(U.off_norm(l), D.off_norm(l), 1, U.d, D.d);        // gain [d]
+        block(U.off_router(l), D.off_router(l), U.d, U.M, D.M);  // router [d x M]
+    }
+    for (int l = 0; l < U.L; ++l)
+        for (int j = 0; j < U.M; ++j) {
+            const int64_t uo = U.off_expert(l, j), po = D.off_expert(l, j);
+            block(uo, po, U.d, U.f, D.f);                                      // wg [d x f]
+            block(uo + U.d * U.f, po + D.d * D.f, U.d, U.f, D.f);              // wu [d x f]
+            block(uo + 2 * U.d * U.f, po + 2 * D.d * D.f, U.f, U.d, D.d);      // wd [f x d]
+        }
+}
 int64_t rup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
 struct DevMem {
@@ -141,8 +178,10 @@ struct LayerBufs {
 }  // namespace
 
 struct spes_ctx {
-    spes_model_cfg cfg;
-    Layout lay;
+    spes_model_cfg cfg;  // the caller's model
+    Layout lay;          // device layout (hidden / intermediate / vocab padded to 128)
+    Layout ulay;         // the caller's layout (enumerate_blocks of cfg)
+    bool padded = false;
     int node = 0, n_nodes = 1, device = 0;
     int expf_variant = 1;
     cudaStream_t stream = nullptr;
@@ -653,7 +692,7 @@ void forward_backward(spes_ctx* c) {
 #define PROF(name) Prof _prof_##__LINE__(c, name)
     {
         PROF("embed_gather");
-        spes_k::embed_gather(P + L.off_emb(), c->tokens, c->B, c->S, d, V,
+        spes_k::embed_gather(P + L.off_emb(), c->tokens, c->B, c->S, d, c->ulay.V,
                              c->virtual_h0 ? nullptr : c->h[0], c->inputs,
                              c->targets, c->err, st);
     }
@@ -668,7 +707,8 @@ void forward_backward(spes_ctx* c) {
         LayerBufs& Y = c->layers[l];
         {
             PROF("router_fwd");
-            spes_k::router_forward(hsrc(l), hmap(l), P + L.off_norm(l), P + L.off_router(l), T, d, M, k,
+            spes_k::router_forward(hsrc(l), hmap(l), P + L.off_norm(l), P + L.off_router(l), T, d,
+                                   c->ulay.d, M, k,
                                    c->cfg.renormalize_after_topk, c->cfg.rms_eps, c->expf_variant,
                                    nullptr, c->normed_bf, Y.logits, Y.probs, Y.topk_idx,
                                    Y.topk_w, Y.lse_r, Y.inv_rms, Y.denom, st);
@@ -707,7 +747,7 @@ void forward_backward(spes_ctx* c) {
     }
     {
         PROF("head_fwd");
-        if (V == 256) {  // softmax-CE in the GEMM epilogue: no fp32 logits round trip
+        if (V == 256 && c->ulay.V == V) {  // softmax-CE in the GEMM epilogue: no fp32 logits
             spes_k::gemm_head_ce(c->a_hL, c->b_headB_mn, c->head_groups + 0, 1, c->head_tiles + 0,
                                  c->head_max[0], c->targets, T, sd.g_s2, sd.g_ssum, c->dlog_bf, c->diff, c->lse_head, st);
         } else {
@@ -717,8 +757,8 @@ void forward_backward(spes_ctx* c) {
     }
     {
         PROF("head_ce_losses");
-        if (V != 256)
-            spes_k::head_ce(c->head_logits, c->targets, T, Tp, V, sd.g_s2,
+        if (V != 256 || c->ulay.V != V)
+            spes_k::head_ce(c->head_logits, c->targets, T, Tp, V, c->ulay.V, sd.g_s2,
                             sd.g_ssum, c->dlog_bf, c->diff, c->lse_head, st);
         fork(1);  // loss scalars: read by the host and by the optimizer's finite-loss guard
         spes_k::losses_reduce(c->diff, c->lse_head, c->lse_all, c->probs_all, c->coeff_all, T, Tp,
@@ -825,7 +865,8 @@ void forward_backward(spes_ctx* c) {
         }
         {
             PROF("norm_router_grads");  // + rmsnorm backward into gh
-            spes_k::norm_router_grads(hsrc(l), hmap(l), P + L.off_norm(l), c->gnormed, c->glog, Y.inv_rms, T, d, M,
+            spes_k::norm_router_grads(hsrc(l), hmap(l), P + L.off_norm(l), c->gnormed, c->glog,
+                                      Y.inv_rms, T, d, c->ulay.d, M,
                                       c->nr_partial, c->grads + L.off_norm(l),
                                       c->grads + L.off_router(l), c->dot_part, c->gh, st);
         }
@@ -881,7 +922,7 @@ void optimizer_finish(spes_ctx* c) {
 
 void validate_tokens(const spes_ctx* c, const int32_t* tokens, int64_t n) {
     for (int64_t i = 0; i < n; ++i)
-        if (tokens[i] < 0 || tokens[i] >= c->lay.V)
+        if (tokens[i] < 0 || tokens[i] >= c->ulay.V)
             throw std::out_of_range("batch: token id out of vocabulary");
 }
 
@@ -1083,7 +1124,10 @@ spes_status spes_create(const spes_model_cfg* cfg, int32_t node, int32_t n_nodes
         if (n_nodes > 1 && !nccl_id) throw std::invalid_argument("nccl id required when n_nodes > 1");
         auto c = std::make_unique<spes_ctx>();
         c->cfg = *cfg;
-        c->lay = layout_of(cfg);
+        const spes_model_cfg dcfg = device_cfg(cfg);
+        c->lay = layout_of(&dcfg);
+        c->ulay = layout_of(cfg);
+        c->padded = c->lay.total() != c->ulay.total();
         c->node = node;
         c->n_nodes = n_nodes;
         c->device = cuda_device;
@@ -1206,15 +1250,47 @@ spes_status spes_set_ownership(spes_ctx* c, const int32_t* node_offsets, const i
     });
 }
 
+// the caller's parameter vector (enumerate_blocks layout, host) -> the device model
+void upload_user_params(spes_ctx* c, const float* host) {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    set_counter(c);
+    if (!c->padded) {
+        ck(cudaMemcpyAsync(c->params, host, sizeof(float) * c->lay.total(), cudaMemcpyHostToDevice,
+                           c->stream),
+           "H2D params");
+    } else {
+        std::vector<float> dev(static_cast<size_t>(c->lay.total()), 0.f);
+        convert_layout(c->ulay, c->lay, host, dev.data(), true);
+        ck(cudaMemcpyAsync(c->params, dev.data(), sizeof(float) * dev.size(),
+                           cudaMemcpyHostToDevice, c->stream),
+           "H2D params");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+    }
+    refresh_shadows_all(c);
+    ck(cudaStreamSynchronize(c->stream), "sync");
+}
+// the device model -> the caller's layout (host)
+void download_user_params(spes_ctx* c, float* host) {
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    if (!c->padded) {
+        ck(cudaMemcpyAsync(host, c->params, sizeof(float) * c->lay.total(), cudaMemcpyDeviceToHost,
+                           c->stream),
+           "D2H params");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        return;
+    }
+    std::vector<float> dev(static_cast<size_t>(c->lay.total()));
+    ck(cudaMemcpyAsync(dev.data(), c->params, sizeof(float) * dev.size(), cudaMemcpyDeviceToHost,
+                       c->stream),
+       "D2H params");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    convert_layout(c->ulay, c->lay, dev.data(), host, false);
+}
+
 spes_status spes_load_params(spes_ctx* c, const float* host, int64_t n) {
     return guard([&] {
-        if (n != c->lay.total()) throw std::invalid_argument("load_params: size mismatch");
-        ck(cudaSetDevice(c->device), "cudaSetDevice");
-        set_counter(c);
-        ck(cudaMemcpyAsync(c->params, host, sizeof(float) * n, cudaMemcpyHostToDevice, c->stream),
-           "H2D params");
-        refresh_shadows_all(c);
-        ck(cudaStreamSynchronize(c->stream), "sync");
+        if (n != c->ulay.total()) throw std::invalid_argument("load_params: size mismatch");
+        upload_user_params(c, host);
     });
 }
 
@@ -1258,23 +1334,11 @@ std::vector<spes_wire::Block> wire_blocks(const spes_model_cfg* cfg) {
 }
 // device parameters <-> a host copy (pinned staging would not pay off for a one-shot export)
 std::vector<float> params_to_host(spes_ctx* c) {
-    std::vector<float> h(static_cast<size_t>(c->lay.total()));
-    ck(cudaSetDevice(c->device), "cudaSetDevice");
-    ck(cudaMemcpyAsync(h.data(), c->params, sizeof(float) * h.size(), cudaMemcpyDeviceToHost,
-                       c->stream),
-       "D2H params");
-    ck(cudaStreamSynchronize(c->stream), "sync");
+    std::vector<float> h(static_cast<size_t>(c->ulay.total()));
+    download_user_params(c, h.data());
     return h;
 }
-void params_from_host(spes_ctx* c, const std::vector<float>& h) {
-    ck(cudaSetDevice(c->device), "cudaSetDevice");
-    set_counter(c);
-    ck(cudaMemcpyAsync(c->params, h.data(), sizeof(float) * h.size(), cudaMemcpyHostToDevice,
-                       c->stream),
-       "H2D params");
-    refresh_shadows_all(c);
-    ck(cudaStreamSynchronize(c->stream), "sync");
-}
+void params_from_host(spes_ctx* c, const std::vector<float>& h) { upload_user_params(c, h.data()); }
 }  // namespace
 
 int64_t spes_model_payload_bytes(const spes_model_cfg* cfg) {
@@ -1319,7 +1383,7 @@ spes_status spes_encode_model(spes_ctx* c, uint8_t* out, int64_t cap) {
 spes_status spes_decode_model(spes_ctx* c, const uint8_t* payload, int64_t len) {
     return guard([&] {
         const auto blocks = wire_blocks(&c->cfg);
-        std::vector<float> h(static_cast<size_t>(c->lay.total()));
+        std::vector<float> h(static_cast<size_t>(c->ulay.total()));
         spes_wire::decode_model(blocks, payload, len, h.data());
         params_from_host(c, h);
     });
@@ -1336,7 +1400,7 @@ spes_status spes_write_checkpoint(spes_ctx* c, const char* path, uint64_t round)
 spes_status spes_read_checkpoint(spes_ctx* c, const char* path, uint64_t* round) {
     return guard([&] {
         const auto blocks = wire_blocks(&c->cfg);
-        std::vector<float> h(static_cast<size_t>(c->lay.total()));
+        std::vector<float> h(static_cast<size_t>(c->ulay.total()));
         const uint64_t r = spes_wire::read_checkpoint(path, blocks, h.data());
         params_from_host(c, h);
         if (round) *round = r;
@@ -1345,9 +1409,15 @@ spes_status spes_read_checkpoint(spes_ctx* c, const char* path, uint64_t* round)
 
 spes_status spes_load_params_device(spes_ctx* c, const float* dev, int64_t n) {
     return guard([&] {
-        if (n != c->lay.total()) throw std::invalid_argument("load_params: size mismatch");
+        if (n != c->ulay.total()) throw std::invalid_argument("load_params: size mismatch");
         ck(cudaSetDevice(c->device), "cudaSetDevice");
         set_counter(c);
+        if (c->padded) {  // through the host conversion (padded layouts are small models)
+            std::vector<float> h(static_cast<size_t>(n));
+            ck(cudaMemcpy(h.data(), dev, sizeof(float) * n, cudaMemcpyDeviceToHost), "D2H params");
+            upload_user_params(c, h.data());
+            return;
+        }
         ck(cudaMemcpyAsync(c->params, dev, sizeof(float) * n, cudaMemcpyDeviceToDevice, c->stream),
            "D2D params");
         refresh_shadows_all(c);
@@ -1357,11 +1427,8 @@ spes_status spes_load_params_device(spes_ctx* c, const float* dev, int64_t n) {
 
 spes_status spes_read_params(spes_ctx* c, float* host, int64_t n) {
     return guard([&] {
-        if (n != c->lay.total()) throw std::invalid_argument("read_params: size mismatch");
-        ck(cudaSetDevice(c->device), "cudaSetDevice");
-        ck(cudaMemcpyAsync(host, c->params, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream),
-           "D2H params");
-        ck(cudaStreamSynchronize(c->stream), "sync");
+        if (n != c->ulay.total()) throw std::invalid_argument("read_params: size mismatch");
+        download_user_params(c, host);
     });
 }
 
@@ -2126,8 +2193,11 @@ spes_status spes_merge(spes_ctx* c, const spes_merge_sched* sched, int32_t round
 
 spes_status spes_counts(spes_ctx* c, int64_t* opt_state, int64_t* grad_scalars, int64_t* step) {
     return guard([&] {
-        if (opt_state) *opt_state = c->inner_sgd ? 0 : 2 * c->G;
-        if (grad_scalars) *grad_scalars = c->G;
+        // the caller's model's units (|psi| + |Phi_i|, trainer.hpp:186-189)
+        const int64_t nown = static_cast<int64_t>(c->node_experts[c->node].size());
+        const int64_t Gu = c->ulay.psi() + c->ulay.L * nown * c->ulay.per_expert();
+        if (opt_state) *opt_state = c->inner_sgd ? 0 : 2 * Gu;
+        if (grad_scalars) *grad_scalars = Gu;
         if (step) *step = c->adam_step;
     });
 }
@@ -2159,7 +2229,7 @@ spes_status spes_set_stream_overlap(spes_ctx* c, int32_t on) {
 
 spes_status spes_read_grads(spes_ctx* c, float* host, int64_t n) {
     return guard([&] {
-        if (n != c->lay.total()) throw std::invalid_argument("read_grads: size mismatch");
+        if (n != c->ulay.total()) throw std::invalid_argument("read_grads: size mismatch");
         if (fused(c) && c->G > c->lay.psi())
             throw std::logic_error(
                 "read_grads: owned-expert gradients are fused into the optimizer; call "
@@ -2168,9 +2238,12 @@ spes_status spes_read_grads(spes_ctx* c, float* host, int64_t n) {
         std::vector<float> comp(c->G);
         ck(cudaMemcpyAsync(comp.data(), c->grads, 4 * c->G, cudaMemcpyDeviceToHost, c->stream), "D2H");
         ck(cudaStreamSynchronize(c->stream), "sync");
-        std::memset(host, 0, 4 * n);
+        std::vector<float> full(c->padded ? static_cast<size_t>(c->lay.total()) : 0);
+        float* dst = c->padded ? full.data() : host;
+        std::memset(dst, 0, 4 * c->lay.total());
         for (const auto& s : c->segs_host)
-            std::memcpy(host + s.param_off, comp.data() + s.comp_off, 4 * s.len);
+            std::memcpy(dst + s.param_off, comp.data() + s.comp_off, 4 * s.len);
+        if (c->padded) convert_layout(c->ulay, c->lay, full.data(), host, false);
     });
 }
 
@@ -2188,24 +2261,30 @@ spes_status spes_debug_read(spes_ctx* c, const char* name, int32_t layer, void* 
             if (layer < 0 || layer >= L.L) throw std::out_of_range("debug_read: bad layer");
             return c->layers[layer];
         };
+        // [T x d] activations in the caller's hidden width (device rows may be padded)
+        const int64_t du = c->ulay.d;
+        auto rows_out = [&](const float* dev_rows) {
+            if (bytes < 4 * T * du) throw std::invalid_argument("debug_read: buffer too small");
+            ck(cudaMemcpy2D(host, 4 * du, dev_rows, 4 * d, 4 * du, T, cudaMemcpyDeviceToHost), "D2H");
+        };
         if (n == "h") {
             if (layer < 0 || layer > L.L) throw std::out_of_range("debug_read: bad layer");
             if (layer == 0 && c->virtual_h0) {  // emb[inputs] (never materialized on device)
-                if (bytes < 4 * T * d) throw std::invalid_argument("debug_read: buffer too small");
+                if (bytes < 4 * T * du) throw std::invalid_argument("debug_read: buffer too small");
                 std::vector<int32_t> in(static_cast<size_t>(T));
                 ck(cudaMemcpy(in.data(), c->inputs, 4 * T, cudaMemcpyDeviceToHost), "D2H");
                 float* out = static_cast<float*>(host);
                 for (int64_t t = 0; t < T; ++t)
-                    ck(cudaMemcpy(out + t * d, c->params + L.off_emb() + static_cast<int64_t>(in[t]) * d,
-                                  4 * d, cudaMemcpyDeviceToHost),
+                    ck(cudaMemcpy(out + t * du, c->params + L.off_emb() + static_cast<int64_t>(in[t]) * d,
+                                  4 * du, cudaMemcpyDeviceToHost),
                        "D2H emb row");
                 return;
             }
             if (layer == L.L)
                 throw std::invalid_argument(
                     "debug_read: the final hidden state is kept only as the bf16 head operand");
-            src = c->h[layer];
-            sz = 4 * T * d;
+            rows_out(c->h[layer]);
+            return;
         } else if (n == "w1" || n == "w2") {  // a layer's bf16 expert operand copies
             if (layer < 0 || layer >= L.L) throw std::out_of_range("debug_read: bad layer");
             const int64_t per_slot = n == "w1" ? L.d * 2 * L.f : L.f * L.d;
@@ -2241,8 +2320,8 @@ spes_status spes_debug_read(spes_ctx* c, const char* name, int32_t layer, void* 
             src = lay().slot_row;
             sz = 4 * T * k;
         } else if (n == "grad_h0") {  // gradient w.r.t. the embedding output (last step)
-            src = c->gh;
-            sz = 4 * T * d;
+            rows_out(c->gh);
+            return;
         } else if (n == "head_logits") {
             if (L.V == 256)  // the fused head-CE epilogue never writes fp32 logits
                 throw std::logic_error("debug_read: head_logits are not materialised for V == 256");
@@ -2336,7 +2415,8 @@ spes_status spes_kernel_router(const spes_model_cfg* cfg, const float* h, const 
         ck(cudaMemcpy(dg, gain, 4 * d, cudaMemcpyHostToDevice), "H2D");
         ck(cudaMemcpy(dr, router, 4 * d * M, cudaMemcpyHostToDevice), "H2D");
         const int variant = spes_expf::host_variant_from(&expf);
-        spes_k::router_forward(dh, nullptr, dg, dr, T, d, M, k, cfg->renormalize_after_topk, cfg->rms_eps,
+        spes_k::router_forward(dh, nullptr, dg, dr, T, d, d, M, k, cfg->renormalize_after_topk,
+                               cfg->rms_eps,
                                variant, dn, nullptr, dl, dp, di, dw, dlse, dinv, dden, 0);
         // routing plan for counts / permutation
         const int64_t R = rup(T * k + static_cast<int64_t>(M) * 128, 128);
@@ -2356,9 +2436,17 @@ spes_status spes_kernel_router(const spes_model_cfg* cfg, const float* h, const 
         if (topk_w) ck(cudaMemcpy(topk_w, dw, 4 * T * k, cudaMemcpyDeviceToHost), "D2H");
         if (counts) ck(cudaMemcpy(counts, rp.counts, 4 * M, cudaMemcpyDeviceToHost), "D2H");
         if (perm) {
-            std::vector<int32_t> rt(R), po(M + 1);
+            std::vector<int32_t> rt(R), po(M + 1), sr(static_cast<size_t>(T * k));
             ck(cudaMemcpy(rt.data(), rp.row_token, 4 * R, cudaMemcpyDeviceToHost), "D2H");
             ck(cudaMemcpy(po.data(), rp.pad_off, 4 * (M + 1), cudaMemcpyDeviceToHost), "D2H");
+            ck(cudaMemcpy(sr.data(), rp.slot_row, 4 * T * k, cudaMemcpyDeviceToHost), "D2H");
+            // the plan's two views must agree: row_token[slot_row[t][s]] == t
+            for (int64_t i = 0; i < T * k; ++i)
+                if (sr[i] < 0 || sr[i] >= R || rt[sr[i]] != i / k)
+                    throw std::runtime_error(
+                        "route plan inconsistent: token " + std::to_string(i / k) + " slot " +
+                        std::to_string(i % k) + " -> row " + std::to_string(sr[i]) +
+                        " holding token " + std::to_string(sr[i] >= 0 && sr[i] < R ? rt[sr[i]] : -2));
             int64_t q = 0;
             for (int j = 0; j < M; ++j)
                 for (int r = po[j]; r < po[j + 1]; ++r)

@@ -470,7 +470,7 @@ void combine_forward(const float* h, const int32_t* hrow, const float* y, const 
 // exponential is evaluated once (V <= 32 * HC_MAXJ; larger V takes the streaming path).
 constexpr int HC_MAXJ = 16;
 __global__ void head_ce_k(const float* __restrict__ logits, const int32_t* __restrict__ targets,
-                          int64_t T, int64_t T_pad, int64_t V, float g_s2,
+                          int64_t T, int64_t T_pad, int64_t V, int64_t Vt, float g_s2,
                           float g_ssum, bf16* __restrict__ dlogits, float* __restrict__ diff,
                           float* __restrict__ lse_out) {
     const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -492,7 +492,7 @@ __global__ void head_ce_k(const float* __restrict__ logits, const int32_t* __res
 #pragma unroll
         for (int u = 0; u < HC_MAXJ; ++u) {
             const int64_t j = lane + 32 * u;
-            x[u] = j < V ? row[j] : -INFINITY;
+            x[u] = j < Vt ? row[j] : -INFINITY;
             mx = fmaxf(mx, x[u]);
         }
         mx = warp_max(mx);
@@ -500,7 +500,7 @@ __global__ void head_ce_k(const float* __restrict__ logits, const int32_t* __res
 #pragma unroll
         for (int u = 0; u < HC_MAXJ; ++u) {
             const int64_t j = lane + 32 * u;
-            x[u] = j < V ? ex(fsub(x[u], mx)) : 0.f;
+            x[u] = j < Vt ? ex(fsub(x[u], mx)) : 0.f;
             sum += x[u];
         }
         sum = warp_sum(sum);
@@ -515,18 +515,20 @@ __global__ void head_ce_k(const float* __restrict__ logits, const int32_t* __res
 #pragma unroll
         for (int u = 0; u < HC_MAXJ; ++u) {
             const int64_t j = lane + 32 * u;
-            if (j < V) {
+            if (j < Vt) {
                 const float base = (j == tgt) ? -1.f * g_ssum : 0.f;
                 drow[j] = __float2bfloat16_rn(fadd(base, fmul(glse, x[u] * isum)));
+            } else if (j < V) {
+                drow[j] = __float2bfloat16_rn(0.f);
             }
         }
         return;
     }
     float mx = -INFINITY;
-    for (int64_t j = lane; j < V; j += 32) mx = fmaxf(mx, row[j]);
+    for (int64_t j = lane; j < Vt; j += 32) mx = fmaxf(mx, row[j]);
     mx = warp_max(mx);
     float sum = 0.f;
-    for (int64_t j = lane; j < V; j += 32) sum += ex(fsub(row[j], mx));
+    for (int64_t j = lane; j < Vt; j += 32) sum += ex(fsub(row[j], mx));
     sum = warp_sum(sum);
     const float lse = mx + logf(sum);
     const float picked = row[tgt];
@@ -537,6 +539,10 @@ __global__ void head_ce_k(const float* __restrict__ logits, const int32_t* __res
     const float glse = fadd(fadd(fadd(0.f, fmul(g_s2, lse)), fmul(g_s2, lse)), g_ssum);
     const float isum = 1.f / sum;
     for (int64_t j = lane; j < V; j += 32) {
+        if (j >= Vt) {
+            drow[j] = __float2bfloat16_rn(0.f);
+            continue;
+        }
         const float p = ex(fsub(row[j], mx)) * isum;
         const float base = (j == tgt) ? -1.f * g_ssum : 0.f;
         drow[j] = __float2bfloat16_rn(fadd(base, fmul(glse, p)));
@@ -544,10 +550,11 @@ __global__ void head_ce_k(const float* __restrict__ logits, const int32_t* __res
 }
 
 void head_ce(const float* logits, const int32_t* targets, int64_t T, int64_t T_pad, int64_t V,
-             float g_s2, float g_ssum, bf16* dlogits, float* diff, float* lse, cudaStream_t s) {
+             int64_t Vt, float g_s2, float g_ssum, bf16* dlogits, float* diff, float* lse,
+             cudaStream_t s) {
     const int64_t threads = T_pad * 32;
     head_ce_k<<<static_cast<unsigned>(cdiv(threads, 256)), 256, 0, s>>>(
-        logits, targets, T, T_pad, V, g_s2, g_ssum, dlogits, diff, lse);
+        logits, targets, T, T_pad, V, Vt, g_s2, g_ssum, dlogits, diff, lse);
     count_launch();
 }
 
@@ -744,7 +751,7 @@ __device__ __forceinline__ void cp_async_commit_nr() { asm volatile("cp.async.co
 __global__ void __launch_bounds__(256) norm_router_partial_k(
     const float* __restrict__ h, const int32_t* __restrict__ hrow,
     const float* __restrict__ gain, const float* __restrict__ gnormed,
-    const float* __restrict__ glog, const float* __restrict__ inv_rms, int T, int d, int M,
+    const float* __restrict__ glog, const float* __restrict__ inv_rms, int T, int d, int dn, int M,
     float* __restrict__ partial, const float* __restrict__ dot_part, float* __restrict__ gh) {
     extern __shared__ __align__(16) float4 ring[];  // [NRG_S][3][256]
     __shared__ __align__(16) float sgl[2][64][NRG_EG];
@@ -833,7 +840,7 @@ __global__ void __launch_bounds__(256) norm_router_partial_k(
             else
                 for (int i = 0; i < np; ++i) dot2 += dot_part[static_cast<int64_t>(tb + tt) * np + i];
             const float iv = sinv[buf][tt];
-            lane_coef = fdiv(fmul(fmul(fmul(dot2, iv), iv), iv), static_cast<float>(d));
+            lane_coef = fdiv(fmul(fmul(fmul(dot2, iv), iv), iv), static_cast<float>(dn));
         }
 #pragma unroll 1
         for (int j = 0; j < 8; ++j) {
@@ -923,15 +930,16 @@ __global__ void norm_router_finish_k(const float* __restrict__ partial, int d, i
 }
 
 void norm_router_grads(const float* h, const int32_t* hrow, const float* gain, const float* gnormed,
-                       const float* glog, const float* inv_rms, int64_t T, int64_t d, int M,
-                       float* partial, float* g_gain, float* g_router, const float* dot_part,
+                       const float* glog, const float* inv_rms, int64_t T, int64_t d, int64_t dn,
+                       int M, float* partial, float* g_gain, float* g_router, const float* dot_part,
                        float* gh, cudaStream_t s) {
     dim3 grid(static_cast<unsigned>(d / 128), NRG_TC, static_cast<unsigned>((M + NRG_EG - 1) / NRG_EG));
     constexpr int ring_bytes = NRG_S * 3 * 256 * 16;
     static std::atomic<uint64_t> attr_set{0};
     if (first_use_on_device(attr_set))
         cudaFuncSetAttribute(norm_router_partial_k, cudaFuncAttributeMaxDynamicSharedMemorySize, ring_bytes);
-    norm_router_partial_k<<<grid, 256, ring_bytes, s>>>(h, hrow, gain, gnormed, glog, inv_rms, (int)T, (int)d, M,
+    norm_router_partial_k<<<grid, 256, ring_bytes, s>>>(h, hrow, gain, gnormed, glog, inv_rms, (int)T,
+                                                        (int)d, (int)dn, M,
                                                partial, dot_part, gh);
     const int64_t n = d * (M + 1);
     norm_router_finish_k<<<static_cast<unsigned>(cdiv(n, 256)), 256, 0, s>>>(partial, (int)d, M,
@@ -1227,12 +1235,13 @@ __device__ __forceinline__ void write_shadow4(const AdamSeg& sg, int64_t o, cons
 constexpr int ADAM_U = 2;  // tile = blockDim.x * ADAM_U float4 groups
 
 // Block (x, y): segment seg0 + y, its piece [off, off + len) (len < 0: to the segment's
-// end), tiles x, x + gridDim.x, ...
+// end), tiles [x * tpb, (x + 1) * tpb): blocks run in launch order, so each segment is
+// streamed front to back by consecutive blocks (DRAM-page friendly: 6.4 TB/s alone)
 __global__ void __launch_bounds__(256) adamw_k(float* __restrict__ params,
                                                const float* __restrict__ grads,
                                                float* __restrict__ m, float* __restrict__ v,
                                                const AdamSeg* __restrict__ segs, int seg0,
-                                               int64_t off, int64_t len,
+                                               int64_t off, int64_t len, int tpb,
                                                const AdamScalars* __restrict__ ap,
                                                Shadows sh, const double* __restrict__ loss_total) {
     if (!loss_ok(loss_total)) return;
@@ -1246,13 +1255,14 @@ __global__ void __launch_bounds__(256) adamw_k(float* __restrict__ params,
     float* mb = m + comp;
     float* vb = v + comp;
     const int nt = blockDim.x, tile4 = nt * ADAM_U;
-    for (int64_t t0 = static_cast<int64_t>(blockIdx.x) * tile4; t0 < n4;
-         t0 += static_cast<int64_t>(gridDim.x) * tile4) {
+    const int64_t first = static_cast<int64_t>(blockIdx.x) * tpb * tile4;
+    const int64_t last = min(n4, first + static_cast<int64_t>(tpb) * tile4);
+    for (int64_t t0 = first; t0 < last; t0 += tile4) {
         float4 th[ADAM_U], g[ADAM_U], mm[ADAM_U], vv[ADAM_U];
 #pragma unroll
         for (int u = 0; u < ADAM_U; ++u) {
             const int64_t q = t0 + u * nt + threadIdx.x;  // coalesced per u
-            if (q < n4) {
+            if (q < last) {
                 th[u] = *reinterpret_cast<const float4*>(th_base + 4 * q);
                 g[u] = __ldcs(reinterpret_cast<const float4*>(gb + 4 * q));
                 if (!a.sgd) {
@@ -1264,7 +1274,7 @@ __global__ void __launch_bounds__(256) adamw_k(float* __restrict__ params,
 #pragma unroll
         for (int u = 0; u < ADAM_U; ++u) {
             const int64_t q = t0 + u * nt + threadIdx.x;
-            if (q >= n4) continue;
+            if (q >= last) continue;
             if (a.sgd) {  // theta -= lr * g (trainer.hpp:197-204)
                 th[u].x = fsub(th[u].x, fmul(a.lr, g[u].x));
                 th[u].y = fsub(th[u].y, fmul(a.lr, g[u].y));
@@ -1298,15 +1308,14 @@ static void adamw_launch(float* params, const float* grads, float* m, float* v,
                          int64_t max_len, const AdamScalars* a, Shadows sh,
                          const double* loss_total, cudaStream_t s, bool background) {
     if (nseg <= 0 || max_len <= 0) return;
-    // several waves of 256-thread blocks over all segments; or (background launches,
-    // beside the GEMMs) small blocks that fit in the registers a resident GEMM CTA leaves
-    // free (g_adam_bg_threads), a few tiles each
+    // 256-thread blocks of 8 tiles; or (background launches, beside the GEMMs) small
+    // blocks that fit in the registers a resident GEMM CTA leaves free (g_adam_bg_threads)
     const int nt = background ? g_adam_bg_threads : 256;
+    const int tpb = background ? g_adam_bg_tiles : 8;
     const int64_t tiles = cdiv(max_len / 4, nt * ADAM_U);
-    const int64_t bx = background ? cdiv(tiles, g_adam_bg_tiles)
-                                  : std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * 32 / nseg));
-    const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(nseg));
-    adamw_k<<<grid, nt, 0, s>>>(params, grads, m, v, segs, seg0, off, len, a, sh, loss_total);
+    const dim3 grid(static_cast<unsigned>(cdiv(tiles, tpb)), static_cast<unsigned>(nseg));
+    adamw_k<<<grid, nt, 0, s>>>(params, grads, m, v, segs, seg0, off, len, tpb, a, sh,
+                                loss_total);
     count_launch();
 }
 

@@ -44,9 +44,11 @@ void embed_gather(const float* emb, const int32_t* tokens, int64_t B, int64_t S,
                   int64_t V, float* h, int32_t* inputs, int32_t* targets, int32_t* err,
                   cudaStream_t s);
 // normed (fp32) and normed_bf (bf16, the expert GEMM operand) are each optional.
-// hrow (optional): row t of h is h + hrow[t] * d (layer 0 reads emb[inputs] in place)
+// hrow (optional): row t of h is h + hrow[t] * d (layer 0 reads emb[inputs] in place).
+// d: row width; dn: the rmsnorm mean's width (the model's hidden size; < d when rows carry
+// zero padding)
 void router_forward(const float* h, const int32_t* hrow, const float* gain, const float* router,
-                    int64_t T, int64_t d,
+                    int64_t T, int64_t d, int64_t dn,
                     int M, int k, int renorm, float eps, int expf_variant, float* normed,
                     bf16* normed_bf, float* logits, float* probs, int32_t* topk_idx,
                     float* topk_w, float* lse, float* inv_rms, float* denom, cudaStream_t s);
@@ -95,8 +97,10 @@ void combine_forward(const float* h, const int32_t* hrow, const float* y, const 
                      float* h_next, bf16* h_next_bf, cudaStream_t s);
 // CE + z on head logits; writes dlogits as bf16 (the head backward GEMM operand; padding
 // rows zero) and the per-token terms.
+// V: row width of logits / dlogits; Vt <= V: the model's vocabulary (columns >= Vt are zero
+// padding: excluded from the softmax, zero gradient)
 void head_ce(const float* logits, const int32_t* targets, int64_t T, int64_t T_pad, int64_t V,
-             float g_s2, float g_ssum, bf16* dlogits, float* diff,
+             int64_t Vt, float g_s2, float g_ssum, bf16* dlogits, float* diff,
              float* lse, cudaStream_t s);
 // Loss scalars (tolerance-level, deterministic tree order) -> out[0..4] (doubles), and
 // the step's status word (sticky in *status, copied to out[5]; see spes_dev::loss_ok)
@@ -126,7 +130,8 @@ constexpr int kNormRouterChunks = 37;
 // normed is recomputed exactly from h, inv_rms and the gain (not stored in forward)
 // gh non-null: also applies the rmsnorm backward (dot from normed_grad's dot_part)
 void norm_router_grads(const float* h, const int32_t* hrow, const float* gain, const float* gnormed,
-                       const float* glog, const float* inv_rms, int64_t T, int64_t d, int M,
+                       const float* glog, const float* inv_rms, int64_t T, int64_t d, int64_t dn,
+                       int M,
                        float* partial, float* g_gain, float* g_router, const float* dot_part,
                        float* gh, cudaStream_t s);
 // embedding gradient in two halves: the token bucketing by vocabulary id (needs only the

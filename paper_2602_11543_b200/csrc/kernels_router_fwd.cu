@@ -62,7 +62,8 @@ template <int MAXM>
 __global__ void __launch_bounds__(32 * RF_WARPS) router_fwd_k(
     const float* __restrict__ h, const int32_t* __restrict__ hrow, const float* __restrict__ gain,
     const float* __restrict__ R,
-    int T, int d, int M, int k, int renorm, float eps, int variant, float* __restrict__ normed,
+    int T, int d, int dn_rms, int M, int k, int renorm, float eps, int variant,
+    float* __restrict__ normed,
     bf16* __restrict__ normed_bf, float* __restrict__ logits, float* __restrict__ probs,
     int32_t* __restrict__ topk_idx, float* __restrict__ topk_w, float* __restrict__ lse_out,
     float* __restrict__ inv_out, float* __restrict__ denom_out) {
@@ -149,7 +150,8 @@ __global__ void __launch_bounds__(32 * RF_WARPS) router_fwd_k(
     }
     float inv[TT];
 #pragma unroll
-    for (int j = 0; j < TT; ++j) inv[j] = fdiv(1.f, fsqrt(fadd(fdiv(ms[j], static_cast<float>(d)), eps)));
+    for (int j = 0; j < TT; ++j)  // mean over the model's hidden width (rows may be zero-padded)
+        inv[j] = fdiv(1.f, fsqrt(fadd(fdiv(ms[j], static_cast<float>(dn_rms)), eps)));
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();  // all warps done with pass 1 before the rings are reused
 
@@ -309,7 +311,8 @@ __global__ void __launch_bounds__(32 * RF_WARPS) router_fwd_k(
 template <int MM>
 static void launch_rf(unsigned grid, cudaStream_t s, const float* h, const int32_t* hrow,
                       const float* gain,
-                      const float* router, int64_t T, int64_t d, int M, int k, int renorm,
+                      const float* router, int64_t T, int64_t d, int64_t dn, int M, int k,
+                      int renorm,
                       float eps, int variant, float* normed, bf16* normed_bf, float* logits,
                       float* probs, int32_t* topk_idx, float* topk_w, float* lse, float* inv_rms,
                       float* denom) {
@@ -318,12 +321,13 @@ static void launch_rf(unsigned grid, cudaStream_t s, const float* h, const int32
         cudaFuncSetAttribute(router_fwd_k<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              RfSmem<MM>::BYTES);
     router_fwd_k<MM><<<grid, 32 * RF_WARPS, RfSmem<MM>::BYTES, s>>>(
-        h, hrow, gain, router, (int)T, (int)d, M, k, renorm, eps, variant, normed, normed_bf, logits,
+        h, hrow, gain, router, (int)T, (int)d, (int)dn, M, k, renorm, eps, variant, normed, normed_bf,
+        logits,
         probs, topk_idx, topk_w, lse, inv_rms, denom);
 }
 
 void router_forward(const float* h, const int32_t* hrow, const float* gain, const float* router,
-                    int64_t T, int64_t d,
+                    int64_t T, int64_t d, int64_t dn,
                     int M, int k, int renorm, float eps, int variant, float* normed,
                     bf16* normed_bf, float* logits, float* probs, int32_t* topk_idx,
                     float* topk_w, float* lse, float* inv_rms, float* denom, cudaStream_t s) {
@@ -335,7 +339,8 @@ void router_forward(const float* h, const int32_t* hrow, const float* gain, cons
     const unsigned grid = static_cast<unsigned>((T + per_block - 1) / per_block);
     auto* f = maxm == 8 ? launch_rf<8> : maxm == 16 ? launch_rf<16> : maxm == 32 ? launch_rf<32>
                                                                                   : launch_rf<64>;
-    f(grid, s, h, hrow, gain, router, T, d, M, k, renorm, eps, variant, normed, normed_bf, logits, probs,
+    f(grid, s, h, hrow, gain, router, T, d, dn, M, k, renorm, eps, variant, normed, normed_bf, logits,
+      probs,
       topk_idx, topk_w, lse, inv_rms, denom);
     count_launch();
 }

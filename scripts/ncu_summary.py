@@ -1,10 +1,11 @@
 """Summaries of the ncu captures kept under profiles/ (run here, on the pulled files).
 
-  python scripts/ncu_summary.py launches gpurun_out/launches.csv profiles/r01/ncu_launches_step.txt profiles/ncu_gemm_summary.json
+  python scripts/ncu_summary.py launches gpurun_out/launches.csv profiles/r02/ncu_launches_cfg5.txt profiles/ncu_traffic.json cfg5 "<command>"
       ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv
       launch list -> the last local step's launches (split_tokens_k .. the step's last
-      adamw_k), per-launch time / share / DRAM bytes, and the expert-GEMM DRAM bytes that
-      bench.py reports as roofline.traffic
+      adamw_k), per-launch time / share / DRAM bytes, and (merged into the json under the
+      configuration's name) the expert-GEMM DRAM bytes per launch that bench.py reports as
+      roofline.traffic
   python scripts/ncu_summary.py full gpurun_out/prof.ncu-rep profiles/r01/ncu_full_top_kernels.txt
       ncu --set full capture -> the headline metrics of each captured launch
 """
@@ -20,7 +21,7 @@ def _rows(text):
     return list(csv.DictReader(io.StringIO("\n".join(lines))))
 
 
-def launches(csv_path, out_txt, out_json, cmd):
+def launches(csv_path, out_txt, out_json, cfg_name, cmd):
     rows = _rows(open(csv_path).read())
     by_id = {}
     for r in rows:
@@ -46,7 +47,7 @@ def launches(csv_path, out_txt, out_json, cmd):
     step = seq[s0:ends[-1] + 1] if ends else seq[s0:]
     total = sum(e["us"] for e in step)
     out = [
-        "# One SPES local step (cfg2, N=1), ncu launch list: gpu__time_duration.sum per launch,",
+        f"# One SPES local step ({cfg_name}, N=1), ncu launch list: gpu__time_duration.sum per launch,",
         "# --clock-control none, serialized and cold-cache (share of the step is what matters;",
         "# in the graph-replayed step the side-stream launches overlap the main stream).",
         f"# Command: {cmd}",
@@ -74,8 +75,13 @@ def launches(csv_path, out_txt, out_json, cmd):
                                    for e in gem),
         "ncu_us_per_step": sum(e["us"] for e in gem),
     }
-    summary["dram_bytes_per_launch"] = summary["dram_bytes_per_step"] / max(1, len(gem))
-    json.dump(summary, open(out_json, "w"), indent=1)
+    summary["gemm_dram_bytes_per_launch"] = summary["dram_bytes_per_step"] / max(1, len(gem))
+    try:
+        allc = json.load(open(out_json))
+    except Exception:
+        allc = {}
+    allc[cfg_name] = summary
+    json.dump(allc, open(out_json, "w"), indent=1)
     print(f"{len(step)} launches, {total:.1f} us; {len(gem)} grouped GEMM launches")
 
 
@@ -121,7 +127,8 @@ def full(rep, out_txt, cmd):
 if __name__ == "__main__":
     what = sys.argv[1]
     if what == "launches":
-        launches(sys.argv[2], sys.argv[3], sys.argv[4], sys.argv[5] if len(sys.argv) > 5 else "")
+        launches(sys.argv[2], sys.argv[3], sys.argv[4], sys.argv[5],
+                 sys.argv[6] if len(sys.argv) > 6 else "")
     elif what == "full":
         full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else "")
     else:

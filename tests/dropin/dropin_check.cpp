@@ -229,6 +229,34 @@ int main(int argc, char** argv) {
     } catch (const std::out_of_range&) {
         expect(true, "token id out of vocabulary throws out_of_range");
     }
+    // ---- the reference's default ModelConfig (model.hpp:21-31; off the 128-wide tiles) ----
+    {
+        spes::ModelConfig dc;  // vocab 64, hidden 32, intermediate 64, 2 layers, 4 experts top-2
+        const spes::ModelParams g0 = spes::init_model<float>(dc, 3, 0.02);
+        spes::TrainMask m0;
+        m0.node_id = 0;
+        m0.owned_experts = {1, 2};
+        spes::LocalRoundConfig c0;
+        c0.steps = 3;
+        const auto r4 = spes::local_round(g0, batches(dc, 2, 16, 21), c0, m0);
+        spes_b200::Context dctx(spes_b200::to_c(dc), 0, 1, device);
+        const auto g4 = spes_b200::local_round(dctx, g0, batches(dc, 2, 16, 21), c0, m0);
+        bool ok = r4.step_losses.size() == g4.step_losses.size() &&
+                  r4.grad_scalar_count == g4.grad_scalar_count;
+        for (size_t h = 0; ok && h < r4.step_losses.size(); ++h) {
+            std::printf("  default-config step %zu loss ref %.7f b200 %.7f\n", h,
+                        r4.step_losses[h].total, g4.step_losses[h].total);
+            ok = std::fabs(g4.step_losses[h].total - r4.step_losses[h].total) <=
+                 LOSS_RTOL * std::fabs(r4.step_losses[h].total);
+        }
+        for (const auto& b : spes::enumerate_blocks(dc))
+            if (!m0.trainable(b)) {
+                const auto& a = spes::block_tensor(g4.params, b).data;
+                const auto& x = spes::block_tensor(g0, b).data;
+                ok &= std::memcmp(a.data(), x.data(), a.size() * sizeof(float)) == 0;
+            }
+        expect(ok, "local_round on the reference's default ModelConfig (padded on the device)");
+    }
     std::printf(failures ? "DROPIN FAILED\n" : "DROPIN OK\n");
     return failures ? 1 : 0;
 }

@@ -54,9 +54,18 @@ def test_validate_cfg_errors_mirror_reference():
                      experts_active=2)
     tied.tied_head = 1
     assert L.spes_validate_cfg(C.byref(tied)) == 3  # logic_error (model.hpp:361)
-    odd = model_cfg(vocab=256, hidden=96, intermediate=256, layers=1, experts_total=4,
+    # any hidden / intermediate / vocab size: the device layout pads them to the tcgen05
+    # tile; the reference's own default ModelConfig (model.hpp:21-31) is accepted
+    odd = model_cfg(vocab=100, hidden=96, intermediate=200, layers=1, experts_total=4,
                     experts_active=2)
-    assert L.spes_validate_cfg(C.byref(odd)) == 1
+    assert L.spes_validate_cfg(C.byref(odd)) == 0
+    assert L.spes_validate_cfg(C.byref(model_cfg())) == 0
+    big_m = model_cfg(vocab=256, hidden=128, intermediate=256, layers=1, experts_total=65,
+                      experts_active=2)
+    assert L.spes_validate_cfg(C.byref(big_m)) == 1  # B200 routing limit: M <= 64
+    zero = model_cfg(vocab=256, hidden=0, intermediate=256, layers=1, experts_total=4,
+                     experts_active=2)
+    assert L.spes_validate_cfg(C.byref(zero)) == 1  # model.hpp:33-35
 
 
 @pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")

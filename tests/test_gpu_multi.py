@@ -17,6 +17,9 @@ from paper_2602_11543_b200.abi import adamw_cfg, merge_sched, model_cfg
 pytestmark = pytest.mark.gpu
 
 CFG = dict(vocab=256, hidden=128, intermediate=256, layers=2, experts_total=8, experts_active=2)
+# cfg2 shapes: d = f = 1024, 16 experts top-2, one layer
+CFG2 = dict(vocab=256, hidden=1024, intermediate=1024, layers=1, experts_total=16,
+            experts_active=2)
 SCHED = dict(warmup_rounds=4, interval=1, alpha0=0.1, peers=3, source=0)
 
 
@@ -28,11 +31,11 @@ def _n_gpus():
         return 0
 
 
-def _rank(rank, world, nccl_id, owned, params, tokens, q, p2p=True):
+def _rank(rank, world, nccl_id, owned, params, tokens, q, p2p=True, shape=None):
     try:
         import os
         os.environ["SPES_SYNC_P2P"] = "1" if p2p else "0"  # read when the first sync runs
-        cfg = model_cfg(**CFG)
+        cfg = model_cfg(**(shape or CFG))
         node = spes.Node(cfg, rank, world, rank, nccl_id)
         node.set_ownership(owned)
         node.load_params(params)
@@ -58,24 +61,31 @@ def _rank(rank, world, nccl_id, owned, params, tokens, q, p2p=True):
         q.put((rank, None, None, None, None, repr(e)))
 
 
-@pytest.mark.parametrize("world,layout,p2p", [(2, "replicated", True), (2, "partition", True),
-                                              (4, "replicated", True), (4, "partition", True),
-                                              (2, "replicated", False), (4, "replicated", False)])
-def test_nccl_sync_matches_oracle(world, layout, p2p):
+@pytest.mark.parametrize("world,layout,p2p,shape",
+                         [(2, "replicated", True, "cfg1"), (2, "partition", True, "cfg1"),
+                          (4, "replicated", True, "cfg1"), (4, "partition", True, "cfg1"),
+                          (2, "replicated", False, "cfg1"), (4, "replicated", False, "cfg1"),
+                          (4, "replicated", True, "cfg2"), (4, "replicated", False, "cfg2"),
+                          (2, "replicated", True, "cfg2")])
+def test_nccl_sync_matches_oracle(world, layout, p2p, shape):
     """p2p: the primaries read co-owner copies in place over NVLink (CUDA IPC mappings);
-    otherwise the copies travel by NCCL send/recv. Same bits either way."""
+    otherwise the copies travel by NCCL send/recv. Same bits either way. cfg2: the float4
+    peer pulls and owner means at cfg2 sizes (50 M expert scalars)."""
     if _n_gpus() < world:
         pytest.skip(f"needs {world} GPUs")
-    cfg = model_cfg(**CFG)
+    shp = CFG2 if shape == "cfg2" else CFG
+    cfg = model_cfg(**shp)
     M = cfg.experts_total
     owned = (spes.replicated_ownership(M, world, 2) if layout == "replicated"
              else spes.param_partition(cfg, world))
     params = oracle.random_params(cfg, 5)
-    tokens = [oracle.random_tokens(cfg, 2, 64, 100 + r, H=2) for r in range(world)]
+    S = 128 if shape == "cfg2" else 64
+    tokens = [oracle.random_tokens(cfg, 2, S, 100 + r, H=2) for r in range(world)]
     nccl_id = spes.nccl_unique_id()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_rank, args=(r, world, nccl_id, owned, params, tokens, q, p2p))
+    procs = [ctx.Process(target=_rank, args=(r, world, nccl_id, owned, params, tokens, q, p2p,
+                                             shp))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -93,6 +103,10 @@ def test_nccl_sync_matches_oracle(world, layout, p2p):
     for r in res[1:]:
         assert np.array_equal(r[3].view(np.uint32), merged0.view(np.uint32))
     m_ref, _, _ = oracle.merge_model(cfg, expect, merge_sched(**SCHED), 0)
+    if shape == "cfg2":  # the synced model's expert blocks really changed
+        per = 3 * cfg.hidden * cfg.intermediate
+        o = oracle.expert_offset(cfg, 0, 0)
+        assert not np.array_equal(pre[0][o:o + per], expect[o:o + per])
     assert np.array_equal(merged0.view(np.uint32), m_ref.view(np.uint32))
 
 

@@ -327,6 +327,19 @@ def test_local_step_non_pow2_experts(gpu):
                           experts_active=3), B=2, S=80, owned=[1, 4, 5], seed=45)
 
 
+def test_local_step_reference_default_config(gpu):
+    # the reference's default ModelConfig (model.hpp:21-31: V=64, d=32, f=64, L=2, M=4, k=2):
+    # hidden / intermediate / vocab are zero-padded to the 128-wide tiles on the device
+    _check_step(model_cfg(), B=2, S=32, owned=[1, 2], seed=47)
+
+
+def test_local_step_unaligned_shapes_renorm(gpu):
+    # every dimension off the tile grid, renormalized gates, 6 experts
+    _check_step(model_cfg(vocab=100, hidden=96, intermediate=200, layers=2, experts_total=6,
+                          experts_active=2, renormalize_after_topk=True),
+                B=3, S=40, owned=[0, 3, 5], seed=48)
+
+
 def test_local_step_ragged_T(gpu):
     # T not a multiple of 128, an owned expert that may receive no tokens
     _check_step(model_cfg(**CFG1), B=3, S=37, owned=[0, 7], seed=40)
