@@ -482,15 +482,18 @@ def our_arm(args):
     value = tokens / (ms / 1e3)
 
     # ---- e2e: public API with host tokens and losses read back every step ----
-    ke = args.e2e_steps or max(1, min(args.steps, 3))
-    dist.barrier()
-    torch.cuda.synchronize(local)
-    t0 = time.perf_counter()
-    for _ in range(ke):
-        spes_round(host=True)
-    torch.cuda.synchronize(local)
-    t_e2e = dist.max(time.perf_counter() - t0)
-    e2e_value = N * H * B * S * ke / t_e2e
+    # (--e2e-steps 0 skips it: sweeps only)
+    ke = max(1, min(args.steps, 3)) if args.e2e_steps is None else args.e2e_steps
+    e2e_value = None
+    if ke > 0:
+        dist.barrier()
+        torch.cuda.synchronize(local)
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            spes_round(host=True)
+        torch.cuda.synchronize(local)
+        t_e2e = dist.max(time.perf_counter() - t0)
+        e2e_value = N * H * B * S * ke / t_e2e
 
     # ---- rooflines from the profiled round: the grouped tcgen05 GEMM (dominant kernel)
     # and every HBM-bound family ----

@@ -197,10 +197,19 @@ struct spes_ctx {
     // peers' parameter vectors mapped over NVLink (CUDA IPC), for the owner-set means
     std::vector<float*> peer_params;
     bool p2p_tried = false, p2p_ok = false;
+    // fused expert exchange (sync_exchange): per-layer "means done" flags of this node
+    // (exported by IPC with the parameters), the peers' flags, the cached task list
+    uint32_t* sync_flags = nullptr;
+    std::vector<uint32_t*> peer_flags;
+    uint32_t** peer_flags_dev = nullptr;
+    uint32_t sync_epoch = 0;
+    spes_k::SyncTask* sync_tasks = nullptr;
+    int n_sync_tasks = -1;  // -1: task list to (re)build
+    int sync_max_src = 1;
+    int* sync_ctr = nullptr;
+    int* sync_layer_total = nullptr;
+    double sync_mean_bytes = 0, sync_pull_bytes = 0;
     int32_t* barrier_buf = nullptr;
-    std::vector<spes_k::PullTask> pull_host;
-    spes_k::PullTask* pull_dev = nullptr;
-    int pull_cap = 0;
     int64_t launches = 0;
 
     // ownership
@@ -1146,10 +1155,11 @@ spes_status spes_create(const spes_model_cfg* cfg, int32_t node, int32_t n_nodes
         if (const char* e = std::getenv("SPES_FUSED_OPT")) c->fused_opt = std::atoi(e) != 0;
         if (const char* e = std::getenv("SPES_EARLY_WD")) c->early_wd = std::atoi(e) != 0;
         if (const char* e = std::getenv("SPES_STEP_GRAPH")) c->use_graph = std::atoi(e) != 0;
-        if (const char* e = std::getenv("SPES_ADAM_BG")) {  // "threads,tiles" (experiments)
-            int th = 256, ti = 4;
-            if (std::sscanf(e, "%d,%d", &th, &ti) >= 1 && th >= 32 && th <= 1024 && th % 32 == 0)
-                spes_k::adamw_background_shape(th, ti < 1 ? 1 : ti);
+        if (const char* e = std::getenv("SPES_ADAM_BG")) {  // "threads,tiles,per_sm,u"
+            int th = 64, ti = 16, ps = 0, u = 2;
+            if (std::sscanf(e, "%d,%d,%d,%d", &th, &ti, &ps, &u) >= 1 && th >= 32 && th <= 256 &&
+                th % 32 == 0)
+                spes_k::adamw_background_shape(th, ti < 1 ? 1 : ti, ps < 0 ? 0 : ps, u);
         }
         c->expf_variant = spes_expf::host_variant_from(&expf);
         spes_k::gemm_prepare(cuda_device);
@@ -1207,6 +1217,8 @@ void spes_destroy(spes_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (float* p : c->peer_params)
         if (p) cudaIpcCloseMemHandle(p);
+    for (size_t n = 0; n < c->peer_flags.size(); ++n)
+        if (c->peer_flags[n] && static_cast<int>(n) != c->node) cudaIpcCloseMemHandle(c->peer_flags[n]);
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->h_tokens) cudaFreeHost(c->h_tokens);
     if (c->h_losses) cudaFreeHost(c->h_losses);
@@ -1223,6 +1235,7 @@ void spes_destroy(spes_ctx* c) {
     }
     if (c->corpus) cudaFree(c->corpus);
     if (c->d_rows) cudaFree(c->d_rows);
+    if (c->sync_tasks) cudaFree(c->sync_tasks);
     delete c;
 }
 
@@ -1244,6 +1257,7 @@ spes_status spes_set_ownership(spes_ctx* c, const int32_t* node_offsets, const i
         ck(cudaStreamSynchronize(c->stream), "sync");
         c->node_experts = ne;
         build_ownership_tables(c);
+        c->n_sync_tasks = -1;  // the exchange plan follows the ownership map
         // activation buffers embed grad offsets / tile bounds: rebuild on next step
         c->act.release();
         c->T = c->T_pad = 0;
@@ -1793,12 +1807,16 @@ static void open_peer_params(spes_ctx* c) {
     if (const char* e = std::getenv("SPES_SYNC_P2P"))
         if (std::atoi(e) == 0) return;  // all ranks see the same environment
     struct Rec {
-        cudaIpcMemHandle_t h;
+        cudaIpcMemHandle_t h, hf;
         int32_t ok;
         int32_t pad[15];
     };
+    if (!c->sync_flags) c->sync_flags = c->persistent.alloc<uint32_t>(c->lay.L);
     Rec mine{};
-    mine.ok = cudaIpcGetMemHandle(&mine.h, c->params) == cudaSuccess ? 1 : 0;
+    mine.ok = cudaIpcGetMemHandle(&mine.h, c->params) == cudaSuccess &&
+                      cudaIpcGetMemHandle(&mine.hf, c->sync_flags) == cudaSuccess
+                  ? 1
+                  : 0;
     cudaGetLastError();
     Rec* d = nullptr;
     ck(cudaMalloc(&d, sizeof(Rec) * N), "cudaMalloc");
@@ -1809,16 +1827,22 @@ static void open_peer_params(spes_ctx* c) {
     ck(cudaStreamSynchronize(c->stream), "sync");
     int32_t ok = 1;
     std::vector<float*> peers(N, nullptr);
+    std::vector<uint32_t*> pflags(N, nullptr);
+    pflags[me] = c->sync_flags;
     for (int n = 0; n < N; ++n) {
         if (!all[n].ok) ok = 0;
         if (n == me || !ok) continue;
         void* p = nullptr;
-        if (cudaIpcOpenMemHandle(&p, all[n].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        void* pf = nullptr;
+        if (cudaIpcOpenMemHandle(&p, all[n].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+            cudaIpcOpenMemHandle(&pf, all[n].hf, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
             cudaGetLastError();
+            if (p) cudaIpcCloseMemHandle(p);
             ok = 0;
             continue;
         }
         peers[n] = static_cast<float*>(p);
+        pflags[n] = static_cast<uint32_t*>(pf);
     }
     // agree: every rank must have opened every peer
     int32_t* flags = reinterpret_cast<int32_t*>(d);
@@ -1831,12 +1855,99 @@ static void open_peer_params(spes_ctx* c) {
     bool all_ok = true;
     for (int32_t v : oks) all_ok = all_ok && v;
     if (!all_ok) {
-        for (float* p : peers)
-            if (p) cudaIpcCloseMemHandle(p);
+        for (int n = 0; n < N; ++n) {
+            if (n == me) continue;
+            if (peers[n]) cudaIpcCloseMemHandle(peers[n]);
+            if (pflags[n]) cudaIpcCloseMemHandle(pflags[n]);
+        }
         return;
     }
     c->peer_params = peers;
+    c->peer_flags = pflags;
+    c->peer_flags_dev = c->persistent.alloc<uint32_t*>(N);
+    ck(cudaMemcpy(c->peer_flags_dev, pflags.data(), sizeof(uint32_t*) * N, cudaMemcpyHostToDevice),
+       "peer flags");
     c->p2p_ok = true;
+}
+
+// Task list of the fused expert exchange (kernels.cu sync_exchange_k): chunks of 128 Ki
+// scalars of every owner-set mean this node is primary for (owners ascending; copies of
+// co-owners read from their mapped parameters) and of every expert it pulls from a
+// primary. Built once per ownership map (pointers do not move).
+static void build_sync_tasks(spes_ctx* c, const std::vector<int>& primary) {
+    const Layout& L = c->lay;
+    const int me = c->node;
+    int lg = 17, order = 1;  // chunk = 2^lg scalars; order 1: layers interleaved
+    if (const char* e = std::getenv("SPES_SYNC_CHUNK")) lg = std::max(12, std::min(24, std::atoi(e)));
+    if (const char* e = std::getenv("SPES_SYNC_ORDER")) order = std::atoi(e);
+    const int64_t per = L.per_expert(), chunk = int64_t(1) << lg;
+    std::vector<std::vector<spes_k::SyncTask>> means(L.L), pulls(L.L);
+    std::vector<int> layer_total(L.L, 0);
+    c->sync_mean_bytes = c->sync_pull_bytes = 0;
+    c->sync_max_src = 1;
+    for (int l = 0; l < L.L; ++l)
+        for (int e = 0; e < L.M; ++e) {
+            const auto& O = c->owners[e];
+            const int64_t off = L.off_expert(l, e);
+            const bool mean = O.size() >= 2 && primary[e] == me;
+            const bool pull = primary[e] >= 0 && primary[e] != me;
+            if (!mean && !pull) continue;
+            if (mean && static_cast<int>(O.size()) > spes_k::SYNC_MAX_SRC)
+                throw std::invalid_argument("sync: more than 8 owners of one expert");
+            for (int64_t o0 = 0; o0 < per; o0 += chunk) {
+                spes_k::SyncTask t{};
+                t.dst = c->params + off + o0;
+                t.off = o0;
+                t.n4 = std::min(chunk, per - o0) / 4;
+                t.slot = l * L.M + e;
+                t.layer = l;
+                if (mean) {
+                    t.nsrc = static_cast<int32_t>(O.size());
+                    t.primary = -1;
+                    for (size_t q = 0; q < O.size(); ++q)
+                        t.src[q] = (O[q] == me ? c->params : c->peer_params[O[q]]) + off + o0;
+                    means[l].push_back(t);
+                    layer_total[l] += 1;
+                } else {
+                    t.nsrc = 0;
+                    t.primary = primary[e];
+                    t.src[0] = c->peer_params[primary[e]] + off + o0;
+                    pulls[l].push_back(t);
+                }
+            }
+            if (mean) c->sync_mean_bytes += 4.0 * per * (O.size() - 1);
+            if (mean) c->sync_max_src = std::max(c->sync_max_src, static_cast<int>(O.size()));
+            if (pull) c->sync_pull_bytes += 4.0 * per;
+        }
+    // queue order: means of layers 0 and 1, pulls of layer 0, means of layer 2, pulls of
+    // layer 1, ...: a layer's pulls come after every node's means of that layer have had a
+    // head start, and the means of later layers still overlap them
+    std::vector<spes_k::SyncTask> q;
+    if (order == 1) {
+        for (int l = 0; l <= L.L; ++l) {
+            if (l < L.L) q.insert(q.end(), means[l].begin(), means[l].end());
+            if (l >= 1) q.insert(q.end(), pulls[l - 1].begin(), pulls[l - 1].end());
+        }
+    } else {  // every mean first, then every pull
+        for (int l = 0; l < L.L; ++l) q.insert(q.end(), means[l].begin(), means[l].end());
+        for (int l = 0; l < L.L; ++l) q.insert(q.end(), pulls[l].begin(), pulls[l].end());
+    }
+    const int n = static_cast<int>(q.size());
+    const auto& means_q = q;
+    if (c->sync_tasks) cudaFree(c->sync_tasks);
+    ck(cudaMalloc(&c->sync_tasks, sizeof(spes_k::SyncTask) * std::max(n, 1)), "sync tasks");
+    if (n > 0)
+        ck(cudaMemcpy(c->sync_tasks, means_q.data(), sizeof(spes_k::SyncTask) * n,
+                      cudaMemcpyHostToDevice),
+           "sync tasks");
+    if (!c->sync_ctr) {
+        c->sync_ctr = c->persistent.alloc<int>(1 + L.L);
+        c->sync_layer_total = c->persistent.alloc<int>(L.L);
+    }
+    ck(cudaMemcpy(c->sync_layer_total, layer_total.data(), sizeof(int) * L.L,
+                  cudaMemcpyHostToDevice),
+       "layer totals");
+    c->n_sync_tasks = n;
 }
 
 spes_status spes_sync(spes_ctx* c, spes_sync_stats* stats) {
@@ -1909,64 +2020,47 @@ spes_status spes_sync(spes_ctx* c, spes_sync_stats* stats) {
                 ckn(ncclGroupEnd(), "group end");
             }
             ph.reset();
-            ph = std::make_unique<Prof>(c, "sync_owner_mean");
-            // owner-set mean at the primary, owners in ascending node order; with peer
-            // mappings the co-owners' copies are read in place over NVLink (their local
-            // rounds are done: every rank has passed the psi all-gather above, and no rank
-            // overwrites its copy before the barrier below) and the primary also writes the
-            // expert's bf16 operand copy from the mean
             const spes_k::Shadows shd = shadows_of(c);
-            for (int l = 0; l < L.L; ++l)
-                for (int e = 0; e < L.M; ++e) {
-                    const auto& O = c->owners[e];
-                    if (O.size() < 2 || primary[e] != me) continue;
-                    std::vector<const float*> srcs;
-                    float* mine = c->params + L.off_expert(l, e);
-                    for (int o : O) {
-                        if (o == me)
-                            srcs.push_back(mine);
-                        else if (c->p2p_ok)
-                            srcs.push_back(c->peer_params[o] + L.off_expert(l, e));
-                        else
-                            srcs.push_back(slot[{e * L.L + l, o}]);
-                        if (o != me) exp_in += 4.0 * per;
-                    }
-                    spes_k::owner_mean(srcs.data(), static_cast<int>(srcs.size()), per, mine, st,
-                                       c->p2p_ok ? &shd : nullptr, l * L.M + e);
-                }
-            ph.reset();
-            ph = std::make_unique<Prof>(c, "sync_gather");
-            // every node receives every expert from its primary
             if (c->p2p_ok) {
-                // pulled over NVLink between two barriers: every primary's mean is final
-                // before any pull, and no rank moves on (its next local round rewrites the
-                // experts it owns) before every pull is done. The pull also writes the
-                // operand copies, so only the head's needs a refresh below.
+                // one persistent kernel: owner-set means at the primary (co-owners' copies
+                // read in place over NVLink; their local rounds are done, every rank has
+                // passed the psi all-gather above) and pulls from the primaries, a layer's
+                // pulls gated by its primary's per-layer flag, so means and pulls overlap
+                // across layers and nodes. Both write the experts' bf16 operand copies. The
+                // barrier after it keeps every rank from starting its next local round (which
+                // rewrites the experts it owns) before every pull from it is done.
+                ph = std::make_unique<Prof>(c, "sync_exchange");
+                if (c->n_sync_tasks < 0) build_sync_tasks(c, primary);
+                exp_in += c->sync_mean_bytes + c->sync_pull_bytes;
+                c->sync_epoch += 1;
+                spes_k::sync_exchange(c->sync_tasks, c->n_sync_tasks, c->sync_max_src, c->sync_ctr,
+                                      c->sync_layer_total, L.L, c->sync_flags, c->peer_flags_dev,
+                                      c->sync_epoch, shd, st);
                 if (!c->barrier_buf) c->barrier_buf = c->persistent.alloc<int32_t>(1);
                 ckn(ncclAllReduce(c->barrier_buf, c->barrier_buf, 1, ncclInt32, ncclSum, c->comm, st),
                     "barrier");
-                c->pull_host.clear();
+            } else {
+                ph = std::make_unique<Prof>(c, "sync_owner_mean");
+                // owner-set mean at the primary from the staged copies, owners ascending
                 for (int l = 0; l < L.L; ++l)
-                    for (int e = 0; e < L.M; ++e)
-                        if (primary[e] >= 0 && primary[e] != me) {
-                            const int64_t off = L.off_expert(l, e);
-                            c->pull_host.push_back(
-                                {c->peer_params[primary[e]] + off, c->params + off, l * L.M + e, 0});
-                            exp_in += 4.0 * per;
+                    for (int e = 0; e < L.M; ++e) {
+                        const auto& O = c->owners[e];
+                        if (O.size() < 2 || primary[e] != me) continue;
+                        std::vector<const float*> srcs;
+                        float* mine = c->params + L.off_expert(l, e);
+                        for (int o : O) {
+                            srcs.push_back(o == me ? mine : slot[{e * L.L + l, o}]);
+                            if (o != me) exp_in += 4.0 * per;
                         }
-                const int nt = static_cast<int>(c->pull_host.size());
-                if (nt > c->pull_cap) {
-                    c->pull_dev = c->persistent.alloc<spes_k::PullTask>(nt);
-                    c->pull_cap = nt;
-                }
-                if (nt > 0) {
-                    ck(cudaMemcpyAsync(c->pull_dev, c->pull_host.data(), sizeof(spes_k::PullTask) * nt,
-                                       cudaMemcpyHostToDevice, st),
-                       "pull tasks");
-                    spes_k::expert_pull(c->pull_dev, nt, per, shd, st);
-                }
-                ckn(ncclAllReduce(c->barrier_buf, c->barrier_buf, 1, ncclInt32, ncclSum, c->comm, st),
-                    "barrier");
+                        spes_k::owner_mean(srcs.data(), static_cast<int>(srcs.size()), per, mine,
+                                           st, nullptr, l * L.M + e);
+                    }
+                ph.reset();
+                ph = std::make_unique<Prof>(c, "sync_gather");
+            }
+            // NCCL path: every node receives every expert from its primary
+            if (c->p2p_ok) {
+                // done by the exchange above
             } else if (balanced) {
                 for (int l = 0; l < L.L; ++l) {
                     float* base = c->params + L.off_expert(l, 0);

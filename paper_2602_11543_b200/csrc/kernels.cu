@@ -1232,11 +1232,13 @@ __device__ __forceinline__ void write_shadow4(const AdamSeg& sg, int64_t o, cons
 
 // Each thread owns ADAM_U float4 groups of a tile (all loads in flight before any update);
 // segment lengths are multiples of 4.
-constexpr int ADAM_U = 2;  // tile = blockDim.x * ADAM_U float4 groups
-
 // Block (x, y): segment seg0 + y, its piece [off, off + len) (len < 0: to the segment's
-// end), tiles [x * tpb, (x + 1) * tpb): blocks run in launch order, so each segment is
-// streamed front to back by consecutive blocks (DRAM-page friendly: 6.4 TB/s alone)
+// end), in chunks of tpb tiles of blockDim.x * U float4 groups: chunks x, x + gridDim.x, ...
+// The standalone pass launches one chunk per block, so consecutive blocks stream each
+// segment front to back (DRAM-page friendly); the background pass launches a few blocks
+// per SM that walk their piece (so they never hold more registers than a resident GEMM
+// CTA leaves free, and keep more bytes in flight per thread with U = 4).
+template <int U>
 __global__ void __launch_bounds__(256) adamw_k(float* __restrict__ params,
                                                const float* __restrict__ grads,
                                                float* __restrict__ m, float* __restrict__ v,
@@ -1254,53 +1256,60 @@ __global__ void __launch_bounds__(256) adamw_k(float* __restrict__ params,
     const float* gb = grads + comp;
     float* mb = m + comp;
     float* vb = v + comp;
-    const int nt = blockDim.x, tile4 = nt * ADAM_U;
-    const int64_t first = static_cast<int64_t>(blockIdx.x) * tpb * tile4;
-    const int64_t last = min(n4, first + static_cast<int64_t>(tpb) * tile4);
-    for (int64_t t0 = first; t0 < last; t0 += tile4) {
-        float4 th[ADAM_U], g[ADAM_U], mm[ADAM_U], vv[ADAM_U];
+    const int nt = blockDim.x, tile4 = nt * U;
+    const int64_t chunk4 = static_cast<int64_t>(tpb) * tile4;
+    for (int64_t first = static_cast<int64_t>(blockIdx.x) * chunk4; first < n4;
+         first += static_cast<int64_t>(gridDim.x) * chunk4) {
+        const int64_t last = min(n4, first + chunk4);
+        for (int64_t t0 = first; t0 < last; t0 += tile4) {
+            float4 th[U], g[U], mm[U], vv[U];
 #pragma unroll
-        for (int u = 0; u < ADAM_U; ++u) {
-            const int64_t q = t0 + u * nt + threadIdx.x;  // coalesced per u
-            if (q < last) {
-                th[u] = *reinterpret_cast<const float4*>(th_base + 4 * q);
-                g[u] = __ldcs(reinterpret_cast<const float4*>(gb + 4 * q));
-                if (!a.sgd) {
-                    mm[u] = __ldcs(reinterpret_cast<const float4*>(mb + 4 * q));
-                    vv[u] = __ldcs(reinterpret_cast<const float4*>(vb + 4 * q));
+            for (int u = 0; u < U; ++u) {
+                const int64_t q = t0 + u * nt + threadIdx.x;  // coalesced per u
+                if (q < last) {
+                    th[u] = *reinterpret_cast<const float4*>(th_base + 4 * q);
+                    g[u] = __ldcs(reinterpret_cast<const float4*>(gb + 4 * q));
+                    if (!a.sgd) {
+                        mm[u] = __ldcs(reinterpret_cast<const float4*>(mb + 4 * q));
+                        vv[u] = __ldcs(reinterpret_cast<const float4*>(vb + 4 * q));
+                    }
                 }
             }
-        }
 #pragma unroll
-        for (int u = 0; u < ADAM_U; ++u) {
-            const int64_t q = t0 + u * nt + threadIdx.x;
-            if (q >= last) continue;
-            if (a.sgd) {  // theta -= lr * g (trainer.hpp:197-204)
-                th[u].x = fsub(th[u].x, fmul(a.lr, g[u].x));
-                th[u].y = fsub(th[u].y, fmul(a.lr, g[u].y));
-                th[u].z = fsub(th[u].z, fmul(a.lr, g[u].z));
-                th[u].w = fsub(th[u].w, fmul(a.lr, g[u].w));
-            } else {
-                th[u].x = adam_elem(th[u].x, g[u].x, mm[u].x, vv[u].x, a);
-                th[u].y = adam_elem(th[u].y, g[u].y, mm[u].y, vv[u].y, a);
-                th[u].z = adam_elem(th[u].z, g[u].z, mm[u].z, vv[u].z, a);
-                th[u].w = adam_elem(th[u].w, g[u].w, mm[u].w, vv[u].w, a);
-                __stcs(reinterpret_cast<float4*>(mb + 4 * q), mm[u]);
-                __stcs(reinterpret_cast<float4*>(vb + 4 * q), vv[u]);
+            for (int u = 0; u < U; ++u) {
+                const int64_t q = t0 + u * nt + threadIdx.x;
+                if (q >= last) continue;
+                if (a.sgd) {  // theta -= lr * g (trainer.hpp:197-204)
+                    th[u].x = fsub(th[u].x, fmul(a.lr, g[u].x));
+                    th[u].y = fsub(th[u].y, fmul(a.lr, g[u].y));
+                    th[u].z = fsub(th[u].z, fmul(a.lr, g[u].z));
+                    th[u].w = fsub(th[u].w, fmul(a.lr, g[u].w));
+                } else {
+                    th[u].x = adam_elem(th[u].x, g[u].x, mm[u].x, vv[u].x, a);
+                    th[u].y = adam_elem(th[u].y, g[u].y, mm[u].y, vv[u].y, a);
+                    th[u].z = adam_elem(th[u].z, g[u].z, mm[u].z, vv[u].z, a);
+                    th[u].w = adam_elem(th[u].w, g[u].w, mm[u].w, vv[u].w, a);
+                    __stcs(reinterpret_cast<float4*>(mb + 4 * q), mm[u]);
+                    __stcs(reinterpret_cast<float4*>(vb + 4 * q), vv[u]);
+                }
+                *reinterpret_cast<float4*>(th_base + 4 * q) = th[u];
+                write_shadow4(sg, off + 4 * q, th[u], sh);
             }
-            *reinterpret_cast<float4*>(th_base + 4 * q) = th[u];
-            write_shadow4(sg, off + 4 * q, th[u], sh);
         }
     }
 }
 
+// Background (side-stream) launch shape: threads per block, tiles per chunk, blocks per SM
+// over the whole launch (0: one chunk per block), float4 groups per thread (2 or 4).
 // 64 threads (2 warps): fits in the registers a resident GEMM CTA leaves free, so the
 // background launches really run beside the GEMMs (cfg5 N=1: 5845 -> 5779 ms per round
 // against 256-thread blocks, which only run where no GEMM CTA is resident)
-int g_adam_bg_threads = 64, g_adam_bg_tiles = 16;
-void adamw_background_shape(int threads, int tiles) {
+int g_adam_bg_threads = 64, g_adam_bg_tiles = 16, g_adam_bg_per_sm = 0, g_adam_bg_u = 2;
+void adamw_background_shape(int threads, int tiles, int per_sm, int u) {
     g_adam_bg_threads = threads;
     g_adam_bg_tiles = tiles;
+    g_adam_bg_per_sm = per_sm;
+    g_adam_bg_u = u == 4 ? 4 : 2;
 }
 
 static void adamw_launch(float* params, const float* grads, float* m, float* v,
@@ -1308,14 +1317,21 @@ static void adamw_launch(float* params, const float* grads, float* m, float* v,
                          int64_t max_len, const AdamScalars* a, Shadows sh,
                          const double* loss_total, cudaStream_t s, bool background) {
     if (nseg <= 0 || max_len <= 0) return;
-    // 256-thread blocks of 8 tiles; or (background launches, beside the GEMMs) small
-    // blocks that fit in the registers a resident GEMM CTA leaves free (g_adam_bg_threads)
+    // 256-thread blocks, one chunk of 8 tiles each; or the background shape above
     const int nt = background ? g_adam_bg_threads : 256;
     const int tpb = background ? g_adam_bg_tiles : 8;
-    const int64_t tiles = cdiv(max_len / 4, nt * ADAM_U);
-    const dim3 grid(static_cast<unsigned>(cdiv(tiles, tpb)), static_cast<unsigned>(nseg));
-    adamw_k<<<grid, nt, 0, s>>>(params, grads, m, v, segs, seg0, off, len, tpb, a, sh,
-                                loss_total);
+    const int U = background ? g_adam_bg_u : 2;
+    const int64_t chunks = cdiv(cdiv(max_len / 4, nt * U), tpb);
+    int64_t bx = chunks;
+    if (background && g_adam_bg_per_sm > 0)
+        bx = std::max<int64_t>(1, std::min<int64_t>(chunks, 148 * g_adam_bg_per_sm / nseg));
+    const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(nseg));
+    if (U == 4)
+        adamw_k<4><<<grid, nt, 0, s>>>(params, grads, m, v, segs, seg0, off, len, tpb, a, sh,
+                                       loss_total);
+    else
+        adamw_k<2><<<grid, nt, 0, s>>>(params, grads, m, v, segs, seg0, off, len, tpb, a, sh,
+                                       loss_total);
     count_launch();
 }
 
@@ -1440,45 +1456,114 @@ void owner_mean(const float* const* srcs, int n_src, int64_t n, float* out, cuda
     count_launch();
 }
 
-// expert pulls of the sparse sync: every task copies one expert (per floats) from its
-// primary owner's parameters (a peer GPU, read over NVLink) into this node's parameters and
-// writes its bf16 GEMM operand copy from the same values
-__global__ void expert_pull_k(const PullTask* __restrict__ tasks, int64_t n4, Shadows sh) {
-    const PullTask t = tasks[blockIdx.y];
-    AdamSeg sg{};
-    sg.kind = 1;
-    sg.slot = t.slot;
-    const float4* src = reinterpret_cast<const float4*>(t.src);
-    float4* dst = reinterpret_cast<float4*>(t.dst);
-    constexpr int U = 4;
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * U;
-    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * U + threadIdx.x; base < n4;
-         base += stride) {
-        float4 v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t i = base + static_cast<int64_t>(u) * blockDim.x;
-            if (i < n4) v[u] = src[i];
+// ---- the fused expert exchange of the sparse sync (one persistent kernel) ----
+// Tasks are chunks of experts: first every owner-set mean this node is primary for (its
+// co-owners' copies read in place over NVLink, fp64 sum in ascending node order,
+// protocol.cpp:238-243), then every expert chunk it pulls from that expert's primary. Blocks
+// claim tasks from a device counter in that order. When the last mean chunk of a layer is
+// done, the node publishes flags[layer] = epoch (release, system scope); a pull chunk of a
+// layer first waits until its primary's flag for the layer reaches the epoch (acquire). So a
+// layer's pulls overlap the remaining means, here and on every peer, with no host barrier
+// between the phases. No deadlock: a block only waits on a pull after every mean task of
+// this node has been claimed by a running block, and peers progress independently.
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int NS>  // sources per mean, at most
+__global__ void __launch_bounds__(256) sync_exchange_k(const SyncTask* __restrict__ tasks,
+                                                       int ntasks, int* __restrict__ ctr,
+                                                       const int* __restrict__ layer_total, int L,
+                                                       uint32_t* flags, uint32_t* const* peer_flags,
+                                                       uint32_t epoch, Shadows sh) {
+    __shared__ int s_task;
+    if (blockIdx.x == 0 && threadIdx.x < L && layer_total[threadIdx.x] == 0)
+        st_release_sys(flags + threadIdx.x, epoch);  // nothing to average in this layer
+    for (;;) {
+        if (threadIdx.x == 0) s_task = atomicAdd(ctr, 1);
+        __syncthreads();
+        const int ti = s_task;
+        __syncthreads();
+        if (ti >= ntasks) break;
+        const SyncTask t = tasks[ti];
+        if (t.nsrc == 0) {  // a pull: wait for the primary's means of this layer
+            if (threadIdx.x == 0)
+                while (ld_acquire_sys(peer_flags[t.primary] + t.layer) < epoch) __nanosleep(256);
+            __syncthreads();
+            (void)ld_acquire_sys(peer_flags[t.primary] + t.layer);
         }
+        AdamSeg sg{};
+        sg.kind = 1;
+        sg.slot = t.slot;
+        const int nsrc = t.nsrc == 0 ? 1 : t.nsrc;
+        const double inv = 1.0 / static_cast<double>(nsrc);
+        float4* dst = reinterpret_cast<float4*>(t.dst);
+        constexpr int XU = 4;  // float4 groups per thread in flight, per source
+        for (int64_t i0 = threadIdx.x; i0 < t.n4; i0 += XU * blockDim.x) {
+            float4 v[NS][XU];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t i = base + static_cast<int64_t>(u) * blockDim.x;
-            if (i < n4) {
-                dst[i] = v[u];
-                write_shadow4(sg, 4 * i, v[u], sh);
+            for (int s2 = 0; s2 < NS; ++s2)
+                if (s2 < nsrc)
+#pragma unroll
+                    for (int u = 0; u < XU; ++u) {
+                        const int64_t i = i0 + u * blockDim.x;
+                        if (i < t.n4) v[s2][u] = reinterpret_cast<const float4*>(t.src[s2])[i];
+                    }
+#pragma unroll
+            for (int u = 0; u < XU; ++u) {
+                const int64_t i = i0 + u * blockDim.x;
+                if (i >= t.n4) break;
+                float4 r = v[0][u];
+                if (t.nsrc > 0) {  // owner-set mean, nodes ascending (a unique owner: copy)
+                    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+                    for (int s2 = 0; s2 < NS; ++s2) {
+                        if (s2 >= nsrc) break;
+                        a0 = __dadd_rn(a0, static_cast<double>(v[s2][u].x));
+                        a1 = __dadd_rn(a1, static_cast<double>(v[s2][u].y));
+                        a2 = __dadd_rn(a2, static_cast<double>(v[s2][u].z));
+                        a3 = __dadd_rn(a3, static_cast<double>(v[s2][u].w));
+                    }
+                    r = make_float4(__double2float_rn(__dmul_rn(a0, inv)),
+                                    __double2float_rn(__dmul_rn(a1, inv)),
+                                    __double2float_rn(__dmul_rn(a2, inv)),
+                                    __double2float_rn(__dmul_rn(a3, inv)));
+                }
+                dst[i] = r;
+                write_shadow4(sg, t.off + 4 * i, r, sh);
+            }
+        }
+        if (t.nsrc > 0) {  // mean chunk done: the layer's flag once all its chunks are
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                if (atomicAdd(ctr + 1 + t.layer, 1) + 1 == layer_total[t.layer]) {
+                    __threadfence_system();
+                    st_release_sys(flags + t.layer, epoch);
+                }
             }
         }
     }
 }
 
-void expert_pull(const PullTask* tasks, int ntasks, int64_t per, Shadows sh, cudaStream_t s) {
-    if (ntasks <= 0) return;
-    const int64_t n4 = per / 4;
-    const int bx = static_cast<int>(std::max<int64_t>(
-        1, std::min<int64_t>(cdiv(n4, 256 * 4), (148 * 8 + ntasks - 1) / ntasks)));
-    expert_pull_k<<<dim3(bx, ntasks), 256, 0, s>>>(tasks, n4, sh);
+void sync_exchange(const SyncTask* tasks, int ntasks, int max_src, int* ctr,
+                   const int* layer_total, int L, uint32_t* flags, uint32_t* const* peer_flags,
+                   uint32_t epoch, Shadows sh, cudaStream_t s) {
+    cudaMemsetAsync(ctr, 0, sizeof(int) * (1 + L), s);
+    if (max_src <= 2)
+        sync_exchange_k<2><<<148 * 4, 256, 0, s>>>(tasks, ntasks, ctr, layer_total, L, flags,
+                                                   peer_flags, epoch, sh);
+    else
+        sync_exchange_k<SYNC_MAX_SRC><<<148 * 2, 256, 0, s>>>(tasks, ntasks, ctr, layer_total, L,
+                                                              flags, peer_flags, epoch, sh);
     count_launch();
 }
+
 
 // ============================ merge: Gram + apply ============================
 // Projection vector of expert j: D1 floats at vec_offs[j] (+ a second D1 run at

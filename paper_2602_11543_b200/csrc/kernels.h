@@ -155,13 +155,24 @@ struct Shadows {
 void owner_mean(const float* const* srcs, int n_src, int64_t n, float* out, cudaStream_t s,
                 const Shadows* sh = nullptr, int slot = -1);
 // one expert (per floats) from a peer's parameters into ours, plus its bf16 operand copy
-struct PullTask {
-    const float* src;
+// Fused expert exchange of the sparse sync (kernels.cu): owner-set means (nsrc >= 1 sources
+// in ascending node order) then pulls from the primaries (nsrc == 0, src[0] = the primary's
+// copy), gated per layer by the primaries' flags (flags / peer_flags: one uint32 per layer
+// and node, IPC-mapped; epoch increases per sync). ctr: 1 + L ints (reset here).
+constexpr int SYNC_MAX_SRC = 8;
+struct SyncTask {
+    const float* src[SYNC_MAX_SRC];
     float* dst;
-    int32_t slot;
-    int32_t pad;
+    int64_t off;   // element offset of the chunk within its expert (bf16 copy addressing)
+    int64_t n4;    // float4 groups in the chunk
+    int32_t nsrc;  // owners averaged; 0 = a pull
+    int32_t slot;  // expert slot (layer * M + j)
+    int32_t layer;
+    int32_t primary;
 };
-void expert_pull(const PullTask* tasks, int ntasks, int64_t per, Shadows sh, cudaStream_t s);
+void sync_exchange(const SyncTask* tasks, int ntasks, int max_src, int* ctr,
+                   const int* layer_total, int L, uint32_t* flags, uint32_t* const* peer_flags,
+                   uint32_t epoch, Shadows sh, cudaStream_t s);
 // Segment table of the compact optimizer layout: npsi leading segments (psi_len scalars in
 // total) followed by expert segments of `per` scalars each.
 struct SegTable {
@@ -181,8 +192,9 @@ void adamw(float* params, const float* grads, float* m, float* v, const SegTable
 void adamw_pieces(float* params, const float* grads, float* m, float* v, const SegTable& tab,
                   int seg0, int nseg, int64_t off, int64_t len, const AdamScalars* a, Shadows sh,
                   const double* loss_total, cudaStream_t s);  // a: device memory (graph-replayable)
-// block shape of the background (adamw_pieces) launches: threads per block, tiles per block
-void adamw_background_shape(int threads, int tiles);
+// shape of the background (adamw_pieces) launches: threads per block, tiles per chunk,
+// blocks per SM over the launch (0: one chunk per block), float4 groups per thread (2 / 4)
+void adamw_background_shape(int threads, int tiles, int per_sm, int u);
 // Rewrite the bf16 copies of refresh-table scalars [0, total) from the fp32 parameters
 // (after load / sync / merge).
 void refresh_shadows(const float* params, const SegTable& tab, int64_t total, Shadows sh,
