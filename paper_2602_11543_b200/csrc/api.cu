@@ -224,6 +224,11 @@ struct spes_ctx {
     // identical bits; the fused epilogue is issue/latency-bound at ~3.7 TB/s with the 8
     // epilogue warps that fit next to the MMA ring, so it does not beat the separate pass yet.
     bool fused_opt = false;
+    // dSwiGLU factor rows staged by TMA (SPES_DSWIGLU_TMA=0: off). Only for d <= 1024: the
+    // staging ring leaves room for 3 operand stages instead of 5, which costs more than it
+    // gains once the dH GEMM's K = d is long (cfg2 d=1024: dH 640 -> 712 TFLOP/s; cfg5
+    // d=4096: 1140 -> 984)
+    bool staged_dswiglu = true;
     // inner optimizer (LocalRoundConfig::inner, trainer.hpp:116-121): AdamW, or SGD
     // (theta -= lr * g, no moments; always the standalone pass)
     bool inner_sgd = false;
@@ -284,6 +289,7 @@ struct spes_ctx {
     float *lse_all = nullptr, *probs_all = nullptr, *coeff_all = nullptr;
     double* d_losses = nullptr;
     GemmGroup* head_groups = nullptr;  // [2 + head_split]: fwd, dX, dW K-splits
+    CUtensorMap* gu_maps = nullptr;    // [L] per layer's GU as {64 x 128} boxes (device memory)
     int32_t* head_tiles = nullptr;     // [3]
     int head_max[3] = {0, 0, 0};
     int head_split = 1;
@@ -548,6 +554,14 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
                                 bn_for(f) / bdiv);
         Y.b_w1 = make_tmap_bf16(c->w1 + static_cast<int64_t>(l) * M * d * 2 * f, M * d, 2 * f,
                                 bn_for(d) / bdiv);
+    }
+    {  // the dSwiGLU epilogue stages its factor rows from GU by TMA: maps in device memory
+        std::vector<CUtensorMap> gm(L.L);
+        for (int l = 0; l < L.L; ++l)
+            gm[l] = spes_host::make_tmap_bf16(c->layers[l].gu, R, 2 * f, 128);
+        c->gu_maps = A.alloc<CUtensorMap>(L.L);
+        ck(cudaMemcpy(c->gu_maps, gm.data(), sizeof(CUtensorMap) * L.L, cudaMemcpyHostToDevice),
+           "gu maps");
     }
     c->dyw = A.alloc<bf16>(R * d);
     c->dgu = A.alloc<bf16>(R * 2 * f);
@@ -825,7 +839,8 @@ void forward_backward(spes_ctx* c) {
         {
             PROF("gemm_bwd_dh");
             spes_k::gemm_dswiglu(bn_for(f), c->a_dyw, Y.b_w2, Y.groups + 2 * M, M, Y.tiles + 2,
-                                 c->max_tiles[2], Y.gu, f, st);
+                                 c->max_tiles[2], Y.gu, f,
+                                 c->staged_dswiglu && d <= 1024 ? c->gu_maps + l : nullptr, st);
         }
         if (unfused_dw) {
             {
@@ -1155,6 +1170,7 @@ spes_status spes_create(const spes_model_cfg* cfg, int32_t node, int32_t n_nodes
         if (const char* e = std::getenv("SPES_FUSED_OPT")) c->fused_opt = std::atoi(e) != 0;
         if (const char* e = std::getenv("SPES_EARLY_WD")) c->early_wd = std::atoi(e) != 0;
         if (const char* e = std::getenv("SPES_STEP_GRAPH")) c->use_graph = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SPES_DSWIGLU_TMA")) c->staged_dswiglu = std::atoi(e) != 0;
         if (const char* e = std::getenv("SPES_ADAM_BG")) {  // "threads,tiles,per_sm,u"
             int th = 64, ti = 16, ps = 0, u = 2;
             if (std::sscanf(e, "%d,%d,%d,%d", &th, &ti, &ps, &u) >= 1 && th >= 32 && th <= 256 &&
@@ -1870,14 +1886,17 @@ static void open_peer_params(spes_ctx* c) {
     c->p2p_ok = true;
 }
 
-// Task list of the fused expert exchange (kernels.cu sync_exchange_k): chunks of 128 Ki
-// scalars of every owner-set mean this node is primary for (owners ascending; copies of
+// Task list of the fused expert exchange (kernels.cu sync_exchange_k): chunks of every
+// owner-set mean this node is primary for (owners ascending; copies of
 // co-owners read from their mapped parameters) and of every expert it pulls from a
 // primary. Built once per ownership map (pointers do not move).
 static void build_sync_tasks(spes_ctx* c, const std::vector<int>& primary) {
     const Layout& L = c->lay;
     const int me = c->node;
-    int lg = 17, order = 1;  // chunk = 2^lg scalars; order 1: layers interleaved
+    // chunk = 2^lg scalars: about 32 chunks per expert within [64 Ki, 1 Mi] (cfg2: 128 Ki,
+    // cfg5: 512 Ki; 2^17..2^20 measured within 3% at cfg5 N=4); order 1: layers interleaved
+    int lg = 16, order = 1;
+    while (lg < 20 && (int64_t(1) << (lg + 1)) * 32 <= c->lay.per_expert()) ++lg;
     if (const char* e = std::getenv("SPES_SYNC_CHUNK")) lg = std::max(12, std::min(24, std::atoi(e)));
     if (const char* e = std::getenv("SPES_SYNC_ORDER")) order = std::atoi(e);
     const int64_t per = L.per_expert(), chunk = int64_t(1) << lg;
@@ -1919,6 +1938,25 @@ static void build_sync_tasks(spes_ctx* c, const std::vector<int>& primary) {
             if (mean) c->sync_max_src = std::max(c->sync_max_src, static_cast<int>(O.size()));
             if (pull) c->sync_pull_bytes += 4.0 * per;
         }
+    // a layer's pulls round-robin over the primaries, starting after this node: every node
+    // pulls from every primary at the same time instead of all nodes draining one primary's
+    // NVLink egress after another (the (layer, expert) order made the primaries hot spots)
+    for (int l = 0; l < L.L; ++l) {
+        const int N = c->n_nodes;
+        std::vector<std::vector<spes_k::SyncTask>> byp(N);
+        for (const auto& t : pulls[l]) byp[(t.primary - me - 1 + 2 * N) % N].push_back(t);
+        std::vector<spes_k::SyncTask> rr;
+        for (size_t i = 0;; ++i) {
+            bool any = false;
+            for (int p = 0; p < N; ++p)
+                if (i < byp[p].size()) {
+                    rr.push_back(byp[p][i]);
+                    any = true;
+                }
+            if (!any) break;
+        }
+        pulls[l].swap(rr);
+    }
     // queue order: means of layers 0 and 1, pulls of layer 0, means of layer 2, pulls of
     // layer 1, ...: a layer's pulls come after every node's means of that layer have had a
     // head start, and the means of later layers still overlap them

@@ -143,6 +143,59 @@ struct EpiDSwiGLU {
     }
 };
 
+// The same dSwiGLU with the saved factor rows staged by TMA (pair kernel, BN = 256): the
+// kernel's warp 3 loads each 64-column piece of the tile's A (gate slots) and B (up slots)
+// factor rows (2 x 128 rows x 128 B, 128B-swizzled) into a double-buffered ring as soon as
+// the tile is scheduled, so the loads overlap the MMAs instead of stalling the epilogue.
+// Per piece, the two warps of a TMEM lane quarter read the same 64 accumulator columns:
+// half 0 forms dG = dH * A, half 1 dU = dH * B, each a whole 128-byte row per store.
+struct EpiDSwiGLUStaged {
+    static constexpr int SLOTS = 1;
+    static constexpr int PIECES = 4;                  // 256 columns / 64
+    static constexpr int STAGED_BYTES = 2 * 2 * 16384;  // 2 buffers x (A piece + B piece)
+    const CUtensorMap* fmap;                          // GU [rows x 2f], {64 x 128} boxes
+    __device__ void prefetch(const GemmGroup&, int, int, int, int) const {}
+    __device__ void stage_load(const GemmGroup& g, int mt, int nt, int pc, uint8_t* dst,
+                               uint64_t* bar) const {
+        const int row = static_cast<int>(g.out_row0) + mt * GEMM_BM;
+        const int64_t x0 = static_cast<int64_t>(nt) * 256 + pc * 64;
+        tma_load_2d(fmap, bar, dst, static_cast<int32_t>(il_gate(x0)), row);
+        tma_load_2d(fmap, bar, dst + 16384, static_cast<int32_t>(il_up(x0)), row);
+    }
+    __device__ void operator()(const GemmGroup& g, int mt, int nt, int r, uint32_t taddr,
+                               bool empty, int half, EpiOut& out, StageCtx& sc) const {
+        const int64_t row = g.out_row0 + static_cast<int64_t>(mt) * GEMM_BM + r;
+        bf16* dgurow = static_cast<bf16*>(g.out0) + row * g.ldo;
+        const int lane = r & 31;
+#pragma unroll 1
+        for (int pc = 0; pc < PIECES; ++pc) {
+            const int b = sc.cnt & 1;
+            mbar_wait(&sc.full[b], (sc.cnt >> 1) & 1);
+            ++sc.cnt;
+            // this thread's factor row (128 B, 16-byte chunks swizzled by row % 8)
+            const uint8_t* frow = sc.buf[b] + half * 16384 + r * 128;
+            const int64_t x0 = static_cast<int64_t>(nt) * 256 + pc * 64;
+            uint4 pk[8];
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+                float dh[32], fa[32];
+                uint4 fr[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    fr[j] = *reinterpret_cast<const uint4*>(frow + (((4 * s2 + j) ^ (r & 7)) << 4));
+                unpack_bf16x32(fr, fa);
+                acc_load32(taddr + pc * 64 + 32 * s2, empty, dh);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) dh[i] = dh[i] * fa[i];
+                pack_bf16x32(dh, *reinterpret_cast<uint4(*)[4]>(&pk[4 * s2]));
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sc.empty[b]);  // the piece's smem is no longer read
+            out.put<8>(dgurow + (half ? il_up(x0) : il_gate(x0)), pk);
+        }
+    }
+};
+
 struct EpiGradW1 {
     static constexpr int SLOTS = 1;
     __device__ void prefetch(const GemmGroup&, int, int, int, int) const {}
@@ -370,12 +423,12 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* 
         static std::atomic<uint64_t> configured2{0};
         if (first_use_on_device(configured2))
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Gemm2Cfg<BN, Epi::SLOTS>::SMEM_BYTES);
+                                 Gemm2Cfg<BN, Epi::SLOTS, EpiStaged<Epi>::bytes>::SMEM_BYTES);
         const int pairs = max_tiles < num_sms() / 2 ? max_tiles : num_sms() / 2;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(2 * pairs);
         cfg.blockDim = dim3(GEMM_THREADS);
-        cfg.dynamicSmemBytes = Gemm2Cfg<BN, Epi::SLOTS>::SMEM_BYTES;
+        cfg.dynamicSmemBytes = Gemm2Cfg<BN, Epi::SLOTS, EpiStaged<Epi>::bytes>::SMEM_BYTES;
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -388,15 +441,19 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* 
         count_launch();
         return;
     }
-    auto kern = grouped_gemm_kernel<BN, Epi, AMN, BMN>;
-    static std::atomic<uint64_t> configured{0};  // one per template instantiation
-    if (first_use_on_device(configured))
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             GemmCfg<BN, Epi::SLOTS>::SMEM_BYTES);
-    const int grid = max_tiles < num_sms() ? max_tiles : num_sms();
-    kern<<<grid, GEMM_THREADS, GemmCfg<BN, Epi::SLOTS>::SMEM_BYTES, s>>>(a, b, g, ng, tiles,
-                                                                       max_tiles, epi);
-    count_launch();
+    if constexpr (EpiStaged<Epi>::bytes > 0) {
+        throw std::logic_error("grouped GEMM: staged epilogues need the cta_group::2 kernel");
+    } else {
+        auto kern = grouped_gemm_kernel<BN, Epi, AMN, BMN>;
+        static std::atomic<uint64_t> configured{0};  // one per template instantiation
+        if (first_use_on_device(configured))
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 GemmCfg<BN, Epi::SLOTS>::SMEM_BYTES);
+        const int grid = max_tiles < num_sms() ? max_tiles : num_sms();
+        kern<<<grid, GEMM_THREADS, GemmCfg<BN, Epi::SLOTS>::SMEM_BYTES, s>>>(a, b, g, ng, tiles,
+                                                                           max_tiles, epi);
+        count_launch();
+    }
 }
 
 void gemm_prepare(int device) {
@@ -446,8 +503,10 @@ void gemm_head_ce(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g
 
 void gemm_dswiglu(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
                   const int32_t* tiles, int max_tiles, const bf16* gu, int64_t f,
-                  cudaStream_t s) {
-    if (bn == 256)
+                  const CUtensorMap* gu_map, cudaStream_t s) {
+    if (bn == 256 && g_gemm_pairs && gu_map)  // factor rows staged by TMA
+        launch<256, false, false>(a, b, g, ng, tiles, max_tiles, EpiDSwiGLUStaged{gu_map}, s);
+    else if (bn == 256)
         launch<256, false, false>(a, b, g, ng, tiles, max_tiles, EpiDSwiGLU<256>{gu, f}, s);
     else
         launch<128, false, false>(a, b, g, ng, tiles, max_tiles, EpiDSwiGLU<128>{gu, f}, s);

@@ -155,6 +155,26 @@ struct GemmGroup {
     int32_t _pad;
 };
 
+// Epilogues may stage an input tile through shared memory by TMA (StagedEpi below): they
+// declare STAGED_BYTES (two buffers' worth, each 1024-byte aligned halves) and the pair
+// kernel's warp 3 loads each piece ahead of the epilogue.
+template <class E, class = void>
+struct EpiStaged {
+    static constexpr int bytes = 0;
+};
+template <class E>
+struct EpiStaged<E, decltype(void(E::STAGED_BYTES))> {
+    static constexpr int bytes = E::STAGED_BYTES;
+};
+// the epilogue side of the staging ring: buffer b holds a piece; full[b] completes when its
+// TMA bytes landed, empty[b] when all 8 epilogue warps of the CTA have used it
+struct StageCtx {
+    uint8_t* buf[2];
+    uint64_t* full;
+    uint64_t* empty;
+    uint32_t cnt;  // pieces consumed so far by this warp (same sequence in every warp)
+};
+
 template <int BN, int SLOTS = 1>
 struct GemmCfg {
     static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;

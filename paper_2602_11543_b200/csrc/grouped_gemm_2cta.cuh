@@ -16,14 +16,15 @@
 
 namespace spes_dev {
 
-template <int BN, int SLOTS = 1>
+template <int BN, int SLOTS = 1, int STAGED = 0>
 struct Gemm2Cfg {
     static constexpr int BNH = BN / 2;
     static constexpr int A_BYTES = GEMM_BM * GEMM_BK * 2;
     static constexpr int B_BYTES = BNH * GEMM_BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int FIXED = 1024 + 256 + GEMM_TABLE_BYTES;
-    static constexpr int EPI_BYTES = epi_stage_bytes(SLOTS);
+    // staged epilogue input (1024-aligned after the epilogue staging slots)
+    static constexpr int EPI_BYTES = (epi_stage_bytes(SLOTS) + 1023) / 1024 * 1024 + STAGED;
     static constexpr int FIT = (GEMM_SMEM_MAX - FIXED - EPI_BYTES) / STAGE_BYTES;
     static constexpr int STAGES = FIT > 6 ? 6 : FIT;
     static_assert(STAGES >= 2, "smem ring too shallow");
@@ -37,7 +38,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                              const __grid_constant__ CUtensorMap mapB,
                              const GemmGroup* __restrict__ groups, int num_groups,
                              const int* __restrict__ total_tiles_ptr, int max_tiles, Epi epi) {
-    using C = Gemm2Cfg<BN, Epi::SLOTS>;
+    constexpr int STAGED = EpiStaged<Epi>::bytes;
+    using C = Gemm2Cfg<BN, Epi::SLOTS, STAGED>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -50,6 +52,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int* s_ts = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(bars) + 256);
     int* s_nkb = s_ts + GEMM_MAX_GROUPS;
     uint8_t* s_epi = reinterpret_cast<uint8_t*>(bars) + 256 + GEMM_TABLE_BYTES;
+    // staged epilogue input: two buffers after the 1024-aligned end of the staging slots
+    uint64_t* sfull = tempty + 2 + 1;   // past tmem_slot's 8 bytes
+    uint64_t* sempty = sfull + 2;
+    uint8_t* s_stage = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(s_epi + epi_stage_bytes(Epi::SLOTS)) + 1023) &
+        ~static_cast<uintptr_t>(1023));
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -70,6 +78,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 16);  // 8 epilogue warps x 2 CTAs (leader's copy used)
         }
+        if constexpr (STAGED > 0)
+            for (int b = 0; b < 2; ++b) {
+                mbar_init(&sfull[b], 1);   // this CTA's warp 3 (expect_tx)
+                mbar_init(&sempty[b], 8);  // this CTA's 8 epilogue warps
+            }
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc_pair(tmem_slot, C::TMEM_COLS);
@@ -168,11 +181,31 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 }
             }
         }
+    } else if (warp == 3) {
+        if constexpr (STAGED > 0) {  // the epilogue's input pieces, ahead of the epilogue
+            if (lane == 0) {
+                uint32_t cnt = 0;
+                for (int t = pair; t < total; t += npairs) {
+                    const int gi = find_group(s_ts, num_groups, t);
+                    const GemmGroup& g = groups[gi];
+                    const int local = t - g.tile_start;
+                    const int mt = local / g.n_tiles, nt = local % g.n_tiles;
+                    for (int pc = 0; pc < Epi::PIECES; ++pc, ++cnt) {
+                        const int b = cnt & 1;
+                        mbar_wait(&sempty[b], ((cnt >> 1) & 1) ^ 1);
+                        mbar_arrive_expect_tx(&sfull[b], STAGED / 2);
+                        epi.stage_load(g, 2 * mt + static_cast<int>(rank), nt, pc,
+                                       s_stage + b * (STAGED / 2), &sfull[b]);
+                    }
+                }
+            }
+        }
     } else if (warp >= 4) {
         const int q = warp & 3;
         const int half = (warp - 4) >> 2;
         const int r = q * 32 + lane;
         EpiOut out{s_epi + (warp - 4) * Epi::SLOTS * EPI_SLOT_BYTES, lane};
+        StageCtx sc{{s_stage, s_stage + STAGED / 2}, sfull, sempty, 0};
         int it = 0;
         for (int t = pair; t < total; t += npairs, ++it) {
             const int gi = find_group(s_ts, num_groups, t);
@@ -191,7 +224,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
-            epi(g, 2 * mt + static_cast<int>(rank), nt, r, taddr, g.k_len == 0, half, out);
+            if constexpr (STAGED > 0)
+                epi(g, 2 * mt + static_cast<int>(rank), nt, r, taddr, g.k_len == 0, half, out, sc);
+            else
+                epi(g, 2 * mt + static_cast<int>(rank), nt, r, taddr, g.k_len == 0, half, out);
             tc_fence_before();
             __syncwarp();
             // relaxed remote arrive: only the (already waited) TMEM reads need ordering

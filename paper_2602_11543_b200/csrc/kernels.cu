@@ -1476,7 +1476,7 @@ __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
 }
 
 template <int NS>  // sources per mean, at most
-__global__ void __launch_bounds__(256) sync_exchange_k(const SyncTask* __restrict__ tasks,
+__global__ void __launch_bounds__(256, NS <= 2 ? 3 : 1) sync_exchange_k(const SyncTask* __restrict__ tasks,
                                                        int ntasks, int* __restrict__ ctr,
                                                        const int* __restrict__ layer_total, int L,
                                                        uint32_t* flags, uint32_t* const* peer_flags,
@@ -1490,7 +1490,7 @@ __global__ void __launch_bounds__(256) sync_exchange_k(const SyncTask* __restric
         const int ti = s_task;
         __syncthreads();
         if (ti >= ntasks) break;
-        const SyncTask t = tasks[ti];
+        const SyncTask& t = tasks[ti];  // fields read as needed (L1-resident)
         if (t.nsrc == 0) {  // a pull: wait for the primary's means of this layer
             if (threadIdx.x == 0)
                 while (ld_acquire_sys(peer_flags[t.primary] + t.layer) < epoch) __nanosleep(256);
@@ -1503,6 +1503,27 @@ __global__ void __launch_bounds__(256) sync_exchange_k(const SyncTask* __restric
         const int nsrc = t.nsrc == 0 ? 1 : t.nsrc;
         const double inv = 1.0 / static_cast<double>(nsrc);
         float4* dst = reinterpret_cast<float4*>(t.dst);
+        if (t.nsrc == 0) {  // a pull: a plain copy with 8 float4 per thread in flight
+            constexpr int PU = 8;
+            const float4* src = reinterpret_cast<const float4*>(t.src[0]);
+            for (int64_t i0 = threadIdx.x; i0 < t.n4; i0 += PU * blockDim.x) {
+                float4 v[PU];
+#pragma unroll
+                for (int u = 0; u < PU; ++u) {
+                    const int64_t i = i0 + u * blockDim.x;
+                    if (i < t.n4) v[u] = src[i];
+                }
+#pragma unroll
+                for (int u = 0; u < PU; ++u) {
+                    const int64_t i = i0 + u * blockDim.x;
+                    if (i < t.n4) {
+                        dst[i] = v[u];
+                        write_shadow4(sg, t.off + 4 * i, v[u], sh);
+                    }
+                }
+            }
+            continue;
+        }
         constexpr int XU = 4;  // float4 groups per thread in flight, per source
         for (int64_t i0 = threadIdx.x; i0 < t.n4; i0 += XU * blockDim.x) {
             float4 v[NS][XU];
@@ -1556,7 +1577,7 @@ void sync_exchange(const SyncTask* tasks, int ntasks, int max_src, int* ctr,
                    uint32_t epoch, Shadows sh, cudaStream_t s) {
     cudaMemsetAsync(ctr, 0, sizeof(int) * (1 + L), s);
     if (max_src <= 2)
-        sync_exchange_k<2><<<148 * 4, 256, 0, s>>>(tasks, ntasks, ctr, layer_total, L, flags,
+        sync_exchange_k<2><<<148 * 3, 256, 0, s>>>(tasks, ntasks, ctr, layer_total, L, flags,
                                                    peer_flags, epoch, sh);
     else
         sync_exchange_k<SYNC_MAX_SRC><<<148 * 2, 256, 0, s>>>(tasks, ntasks, ctr, layer_total, L,

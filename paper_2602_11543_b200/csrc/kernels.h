@@ -228,9 +228,11 @@ enum class GemmMajor { KK, KMN, MNMN };
 void gemm_store_f32(int bn, GemmMajor mj, const CUtensorMap& a, const CUtensorMap& b,
                     const GemmGroup* g, int ng, const int32_t* tiles, int max_tiles,
                     cudaStream_t s);
+// gu_map (optional, device memory): the GU buffer as {64 x 128}-box tensor map; with it the
+// pair kernel stages the factor rows by TMA (EpiDSwiGLUStaged)
 void gemm_dswiglu(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
                   const int32_t* tiles, int max_tiles, const bf16* gu, int64_t f,
-                  cudaStream_t s);
+                  const CUtensorMap* gu_map, cudaStream_t s);
 // head forward (V == 256) with softmax-CE fused into the epilogue: writes bf16 dlogits
 // ([T_pad x 256], padding rows zero), the per-token CE term and lse (head_ce semantics)
 void gemm_head_ce(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
