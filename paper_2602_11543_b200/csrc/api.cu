@@ -224,10 +224,10 @@ struct spes_ctx {
     // identical bits; the fused epilogue is issue/latency-bound at ~3.7 TB/s with the 8
     // epilogue warps that fit next to the MMA ring, so it does not beat the separate pass yet.
     bool fused_opt = false;
-    // dSwiGLU factor rows staged by TMA (SPES_DSWIGLU_TMA=0: off). Only for d <= 1024: the
-    // staging ring leaves room for 3 operand stages instead of 5, which costs more than it
-    // gains once the dH GEMM's K = d is long (cfg2 d=1024: dH 640 -> 712 TFLOP/s; cfg5
-    // d=4096: 1140 -> 984)
+    // dSwiGLU factor rows staged by TMA (SPES_DSWIGLU_TMA=0: off). One staging buffer
+    // leaves room for 4 operand stages instead of 5 (two buffers: 3). Only for d <= 2048:
+    // at cfg2 (d = 1024) dH goes 641 -> 774 TFLOP/s (two buffers: 719), at cfg5 (d = 4096,
+    // long K) the shallower ring costs more than the epilogue gains (1140 -> 984)
     bool staged_dswiglu = true;
     // inner optimizer (LocalRoundConfig::inner, trainer.hpp:116-121): AdamW, or SGD
     // (theta -= lr * g, no moments; always the standalone pass)
@@ -840,7 +840,7 @@ void forward_backward(spes_ctx* c) {
             PROF("gemm_bwd_dh");
             spes_k::gemm_dswiglu(bn_for(f), c->a_dyw, Y.b_w2, Y.groups + 2 * M, M, Y.tiles + 2,
                                  c->max_tiles[2], Y.gu, f,
-                                 c->staged_dswiglu && d <= 1024 ? c->gu_maps + l : nullptr, st);
+                                 c->staged_dswiglu && d <= 2048 ? c->gu_maps + l : nullptr, st);
         }
         if (unfused_dw) {
             {
@@ -1170,7 +1170,10 @@ spes_status spes_create(const spes_model_cfg* cfg, int32_t node, int32_t n_nodes
         if (const char* e = std::getenv("SPES_FUSED_OPT")) c->fused_opt = std::atoi(e) != 0;
         if (const char* e = std::getenv("SPES_EARLY_WD")) c->early_wd = std::atoi(e) != 0;
         if (const char* e = std::getenv("SPES_STEP_GRAPH")) c->use_graph = std::atoi(e) != 0;
-        if (const char* e = std::getenv("SPES_DSWIGLU_TMA")) c->staged_dswiglu = std::atoi(e) != 0;
+        if (const char* e = std::getenv("SPES_DSWIGLU_TMA")) {  // 0 off, 1 / 2 staging buffers
+            c->staged_dswiglu = std::atoi(e) != 0;
+            if (c->staged_dswiglu) spes_k::gemm_dswiglu_buffers(std::atoi(e));
+        }
         if (const char* e = std::getenv("SPES_ADAM_BG")) {  // "threads,tiles,per_sm,u"
             int th = 64, ti = 16, ps = 0, u = 2;
             if (std::sscanf(e, "%d,%d,%d,%d", &th, &ti, &ps, &u) >= 1 && th >= 32 && th <= 256 &&
@@ -2582,7 +2585,18 @@ spes_status spes_kernel_router(const spes_model_cfg* cfg, const float* h, const 
             int64_t q = 0;
             for (int j = 0; j < M; ++j)
                 for (int r = po[j]; r < po[j + 1]; ++r)
-                    if (rt[r] >= 0) perm[q++] = rt[r];
+                    if (rt[r] >= 0) {
+                        if (q >= T * k || (q > 0 && r > po[j] && rt[r - 1] >= rt[r] && rt[r - 1] >= 0))
+                            throw std::runtime_error(
+                                "route plan: row " + std::to_string(r) + " of expert " +
+                                std::to_string(j) + " holds token " + std::to_string(rt[r]) +
+                                " after " + std::to_string(r > 0 ? rt[r - 1] : -9) + " (entry " +
+                                std::to_string(q) + " of " + std::to_string(T * k) + ")");
+                        perm[q++] = rt[r];
+                    }
+            if (q != T * k)
+                throw std::runtime_error("route plan: " + std::to_string(q) + " routed rows, expected " +
+                                         std::to_string(T * k));
         }
     });
 }

@@ -149,10 +149,12 @@ struct EpiDSwiGLU {
 // the tile is scheduled, so the loads overlap the MMAs instead of stalling the epilogue.
 // Per piece, the two warps of a TMEM lane quarter read the same 64 accumulator columns:
 // half 0 forms dG = dH * A, half 1 dU = dH * B, each a whole 128-byte row per store.
+template <int NB>  // staging buffers (1: room for 4 operand stages, 2: 3 stages)
 struct EpiDSwiGLUStaged {
     static constexpr int SLOTS = 1;
-    static constexpr int PIECES = 4;                  // 256 columns / 64
-    static constexpr int STAGED_BYTES = 2 * 2 * 16384;  // 2 buffers x (A piece + B piece)
+    static constexpr int PIECES = 4;  // 256 columns / 64
+    static constexpr int STAGE_BUFS = NB;
+    static constexpr int STAGED_BYTES = NB * 2 * 16384;  // NB x (A piece + B piece)
     const CUtensorMap* fmap;                          // GU [rows x 2f], {64 x 128} boxes
     __device__ void prefetch(const GemmGroup&, int, int, int, int) const {}
     __device__ void stage_load(const GemmGroup& g, int mt, int nt, int pc, uint8_t* dst,
@@ -169,11 +171,11 @@ struct EpiDSwiGLUStaged {
         const int lane = r & 31;
 #pragma unroll 1
         for (int pc = 0; pc < PIECES; ++pc) {
-            const int b = sc.cnt & 1;
-            mbar_wait(&sc.full[b], (sc.cnt >> 1) & 1);
+            const int b = sc.cnt % NB;
+            mbar_wait(&sc.full[b], (sc.cnt / NB) & 1);
             ++sc.cnt;
             // this thread's factor row (128 B, 16-byte chunks swizzled by row % 8)
-            const uint8_t* frow = sc.buf[b] + half * 16384 + r * 128;
+            const uint8_t* frow = sc.base + b * 32768 + half * 16384 + r * 128;
             const int64_t x0 = static_cast<int64_t>(nt) * 256 + pc * 64;
             uint4 pk[8];
 #pragma unroll
@@ -501,11 +503,18 @@ void gemm_head_ce(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g
                              EpiHeadCE{targets, T, g_s2, g_ssum, dlog, diff, lse}, s);
 }
 
+int g_dswiglu_bufs = 1;
+void gemm_dswiglu_buffers(int n) { g_dswiglu_bufs = n == 2 ? 2 : 1; }
+
 void gemm_dswiglu(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
                   const int32_t* tiles, int max_tiles, const bf16* gu, int64_t f,
                   const CUtensorMap* gu_map, cudaStream_t s) {
-    if (bn == 256 && g_gemm_pairs && gu_map)  // factor rows staged by TMA
-        launch<256, false, false>(a, b, g, ng, tiles, max_tiles, EpiDSwiGLUStaged{gu_map}, s);
+    if (bn == 256 && g_gemm_pairs && gu_map) {  // factor rows staged by TMA
+        if (g_dswiglu_bufs == 2)
+            launch<256, false, false>(a, b, g, ng, tiles, max_tiles, EpiDSwiGLUStaged<2>{gu_map}, s);
+        else
+            launch<256, false, false>(a, b, g, ng, tiles, max_tiles, EpiDSwiGLUStaged<1>{gu_map}, s);
+    }
     else if (bn == 256)
         launch<256, false, false>(a, b, g, ng, tiles, max_tiles, EpiDSwiGLU<256>{gu, f}, s);
     else

@@ -166,10 +166,11 @@ template <class E>
 struct EpiStaged<E, decltype(void(E::STAGED_BYTES))> {
     static constexpr int bytes = E::STAGED_BYTES;
 };
-// the epilogue side of the staging ring: buffer b holds a piece; full[b] completes when its
-// TMA bytes landed, empty[b] when all 8 epilogue warps of the CTA have used it
+// the epilogue side of the staging ring (Epi::STAGE_BUFS buffers of STAGED_BYTES /
+// STAGE_BUFS bytes): buffer b holds a piece; full[b] completes when its TMA bytes landed,
+// empty[b] when all 8 epilogue warps of the CTA have used it
 struct StageCtx {
-    uint8_t* buf[2];
+    uint8_t* base;
     uint64_t* full;
     uint64_t* empty;
     uint32_t cnt;  // pieces consumed so far by this warp (same sequence in every warp)

@@ -190,12 +190,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     const GemmGroup& g = groups[gi];
                     const int local = t - g.tile_start;
                     const int mt = local / g.n_tiles, nt = local % g.n_tiles;
+                    constexpr int NB = Epi::STAGE_BUFS, PB = STAGED / NB;
                     for (int pc = 0; pc < Epi::PIECES; ++pc, ++cnt) {
-                        const int b = cnt & 1;
-                        mbar_wait(&sempty[b], ((cnt >> 1) & 1) ^ 1);
-                        mbar_arrive_expect_tx(&sfull[b], STAGED / 2);
-                        epi.stage_load(g, 2 * mt + static_cast<int>(rank), nt, pc,
-                                       s_stage + b * (STAGED / 2), &sfull[b]);
+                        const int b = cnt % NB;
+                        mbar_wait(&sempty[b], ((cnt / NB) & 1) ^ 1);
+                        mbar_arrive_expect_tx(&sfull[b], PB);
+                        epi.stage_load(g, 2 * mt + static_cast<int>(rank), nt, pc, s_stage + b * PB,
+                                       &sfull[b]);
                     }
                 }
             }
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int half = (warp - 4) >> 2;
         const int r = q * 32 + lane;
         EpiOut out{s_epi + (warp - 4) * Epi::SLOTS * EPI_SLOT_BYTES, lane};
-        StageCtx sc{{s_stage, s_stage + STAGED / 2}, sfull, sempty, 0};
+        StageCtx sc{s_stage, sfull, sempty, 0};
         int it = 0;
         for (int t = pair; t < total; t += npairs, ++it) {
             const int gi = find_group(s_ts, num_groups, t);

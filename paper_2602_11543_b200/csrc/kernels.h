@@ -228,6 +228,8 @@ enum class GemmMajor { KK, KMN, MNMN };
 void gemm_store_f32(int bn, GemmMajor mj, const CUtensorMap& a, const CUtensorMap& b,
                     const GemmGroup* g, int ng, const int32_t* tiles, int max_tiles,
                     cudaStream_t s);
+// staging buffers of the TMA-staged dSwiGLU epilogue (1 or 2; experiments)
+void gemm_dswiglu_buffers(int n);
 // gu_map (optional, device memory): the GU buffer as {64 x 128}-box tensor map; with it the
 // pair kernel stages the factor rows by TMA (EpiDSwiGLUStaged)
 void gemm_dswiglu(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,

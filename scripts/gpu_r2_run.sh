@@ -1,15 +1,15 @@
-O=gpurun_out/ncu_dsw
+# N=1 evidence set: the driver's default bench (cfg5, with cpu_baseline), the reference arm,
+# the other BASELINE configurations, and the GPU test suite
+O=gpurun_out/ev2
 mkdir -p $O
-CMD="python bench.py --config cfg2 --steps 1 --warmup 2 --H 2 --prof-rounds 0 --e2e-steps 0 --no-cpu-baseline"
-timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:EpiDSwiGLU" -s 2 -c 1 -o $O/dsw $CMD > $O/ncu.log 2>&1; echo rc=$?
-ncu -i $O/dsw.ncu-rep --page details --csv 2>/dev/null | grep -E "Duration|Tensor|Issue Slots Busy|Warp Cycles Per Issued|Stall|DRAM Throughput|Compute \(SM\)|Memory Throughput" | head -40 > $O/details.txt
-ncu -i $O/dsw.ncu-rep --page raw --csv 2>/dev/null > $O/raw.csv
-python - <<'PY'
-import csv,io
-rows=list(csv.reader(io.StringIO(open('gpurun_out/ncu_dsw/raw.csv').read())))
-hdr,units,data=rows[0],rows[1],rows[2:]
-d=dict(zip(hdr,data[0]))
-for k in sorted(d):
-    if any(x in k for x in ['smsp__pcsamp_warps_issue_stalled','tc_cycles_active','gpu__time_duration.sum','dram__bytes_read.sum','dram__bytes_write.sum','issue_active.avg.pct','smsp__average_warp']):
-        print(k, d[k])
-PY
+timeout 900 python bench.py > $O/bench_default.json 2> $O/bench_default.err; echo default rc=$?
+timeout 900 python bench.py --impl reference > $O/bench_reference.json 2> $O/bench_reference.err; echo ref rc=$?
+for c in cfg2 cfg3 cfg4; do
+timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > $O/bench_${c}_n1.json 2> $O/bench_${c}_n1.err; echo $c rc=$?
+done
+SPES_DSWIGLU_TMA=0 timeout 600 python bench.py --config cfg4 --steps 10 --warmup 3 --e2e-steps 0 --no-cpu-baseline > $O/bench_cfg4_n1_unstaged.json 2> $O/bench_cfg4_n1_unstaged.err
+grep -h gemm_bwd_dh $O/bench_cfg4_n1.err $O/bench_cfg4_n1_unstaged.err
+timeout 1500 python -m pytest tests -m gpu -q -s -p no:cacheprovider 2>&1 | grep -E "GRADERR|passed|failed|Error|error|^E |FAIL" | tail -40 > $O/pytest_gpu.txt
+for f in $O/*.json; do python -c "
+import json;d=json.load(open('$f'));print('$f',d.get('value'),d.get('ms_per_step'),(d.get('e2e') or {}).get('value'),(d.get('cpu_baseline') or {}).get('value'))"; done
+tail -3 $O/pytest_gpu.txt
