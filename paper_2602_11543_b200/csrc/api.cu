@@ -233,6 +233,7 @@ struct spes_ctx {
     // (theta -= lr * g, no moments; always the standalone pass)
     bool inner_sgd = false;
     spes_k::AdamScalars cur_adam{};  // this step's AdamW scalars (set before backward)
+    spes_k::AdamMaps* adam_maps = nullptr;  // [L] TMA views for the staged fused optimizer
     // DiLoCo baseline: this rank's slice of the round-start global model,
     // its fp64 Nesterov buffer, and the exchange buffers (N x slice each)
     // device corpus: sequences x (S+1) tokens resident in HBM
@@ -462,6 +463,29 @@ void build_ownership_tables(spes_ctx* c) {
                   cudaMemcpyHostToDevice),
        "grad_off");
     c->adam_step = 0;
+    // TMA views of every layer's expert parameters and owned experts' moments (fused
+    // optimizer, pair kernel): rows of f (wg / wu) and of d (wd) floats
+    {
+        std::vector<spes_k::AdamMaps> am(L.L);
+        for (int l = 0; l < L.L; ++l) {
+            const float* th = c->params + L.off_expert(l, 0);
+            const int64_t nown = (c->layer_hi[l] - c->layer_lo[l]) / L.per_expert();
+            const int64_t rows_m = std::max<int64_t>(1, 3 * nown);
+            using spes_host::make_tmap_f32;
+            am[l].th_f = make_tmap_f32(th, 3 * L.d * L.M, L.f, 32, 128);
+            am[l].th_d = make_tmap_f32(th, 3 * L.f * L.M, L.d, 32, 128);
+            am[l].m_f = make_tmap_f32(c->m + c->layer_lo[l], rows_m * L.d, L.f, 32, 128);
+            am[l].v_f = make_tmap_f32(c->v + c->layer_lo[l], rows_m * L.d, L.f, 32, 128);
+            am[l].m_d = make_tmap_f32(c->m + c->layer_lo[l], rows_m * L.f, L.d, 32, 128);
+            am[l].v_d = make_tmap_f32(c->v + c->layer_lo[l], rows_m * L.f, L.d, 32, 128);
+            am[l].th_base = th;
+            am[l].mv_base = c->layer_lo[l];
+        }
+        if (!c->adam_maps) c->adam_maps = c->persistent.alloc<spes_k::AdamMaps>(std::max(1, L.L));
+        ck(cudaMemcpy(c->adam_maps, am.data(), sizeof(spes_k::AdamMaps) * L.L,
+                      cudaMemcpyHostToDevice),
+           "adam maps");
+    }
 }
 
 // optimizer segment tables: psi segments, then experts of 3df scalars each
@@ -806,8 +830,13 @@ void forward_backward(spes_ctx* c) {
         LayerBufs& Y = c->layers[l];
         {
             PROF("combine_bwd");
+            // token-ordered rows once the upstream gradient (T x d fp32) outgrows L2's
+            // reach (cfg5: 0.69 -> 0.80 of HBM); expert-major rows otherwise (cfg2: 0.74
+            // token-ordered 0.62)
+            const bool tok_order = 4 * T * d > (int64_t(64) << 20);
             spes_k::combine_backward(c->gh, Y.y, Y.row_token, Y.row_w, Y.pad_off + M, R, d, c->dyw,
-                                     c->gw_part, st);
+                                     c->gw_part, st, tok_order ? Y.slot_row : nullptr, Y.topk_w,
+                                     T, k);
         }
         {  // the router's per-token scalar chain only needs the gate-weight gradients: it
            // runs beside the expert GEMMs
@@ -865,12 +894,12 @@ void forward_backward(spes_ctx* c) {
             {
                 PROF("gemm_bwd_dw_gate_up+adamw");
                 spes_k::gemm_adamw_w1(Y.a_xp_mn, c->b_dgu_mn, Y.groups + 4 * M, M, Y.tiles + 4,
-                                      c->max_tiles[4], ae, st);
+                                      c->max_tiles[4], ae, st, c->adam_maps, M);
             }
             {
                 PROF("gemm_bwd_dw_down+adamw");
                 spes_k::gemm_adamw_w2(bn_for(d), Y.a_hact_mn, c->b_dyw_mn, Y.groups + 5 * M, M,
-                                      Y.tiles + 5, c->max_tiles[5], ae, st);
+                                      Y.tiles + 5, c->max_tiles[5], ae, st, c->adam_maps, M);
             }
         } else if (unfused_dw) {
             {
@@ -2006,6 +2035,11 @@ spes_status spes_sync(spes_ctx* c, spes_sync_stats* stats) {
         cudaEvent_t e0, e1;
         ck(cudaEventCreate(&e0), "event");
         ck(cudaEventCreate(&e1), "event");
+        // the reported time starts once every node has arrived (a one-word all-reduce), so it
+        // measures the exchange itself, not this node waiting for slower nodes' local rounds
+        if (!c->barrier_buf) c->barrier_buf = c->persistent.alloc<int32_t>(1);
+        ckn(ncclAllReduce(c->barrier_buf, c->barrier_buf, 1, ncclInt32, ncclSum, c->comm, st),
+            "barrier");
         ck(cudaEventRecord(e0, st), "event");
         double psi_in = 0, exp_in = 0;
         Prof prof_sync(c, "sync");

@@ -309,6 +309,152 @@ struct EpiAdamW2 {
     }
 };
 
+// ---- MaskedAdamW fused into the dW epilogue, operands staged by TMA ------------------
+// KIND 1: dW of gate||up (tile columns [0,128) -> wg, [128,256) -> wu); KIND 2: dW of down.
+// The kernel's warp 3 loads each 32-column piece of the tile's theta, m and v (3 x 128 rows
+// x 128 B, 128B-swizzled) into a double-buffered smem ring ahead of the epilogue; every
+// epilogue warp updates its 32 rows x 16 columns in place from the TMEM gradients (the same
+// adam_elem as the standalone pass: bit-identical), writes the bf16 operand copy, and once
+// all 8 warps are done one thread writes the three tiles back by TMA stores and frees the
+// buffer when they have read it. No gradient is materialized and no thread waits on a
+// global load.
+template <int KIND, int BN>
+struct EpiAdamStaged {
+    static constexpr int SLOTS = 0;
+    static constexpr int PIECES = BN / 32;
+    static constexpr int STAGE_BUFS = 2;
+    static constexpr int STAGED_BYTES = 2 * 3 * 16384;
+    static constexpr int STAGE_ARRIVALS = 1;  // the thread that issued the write-back
+    AdamEpi p;
+    const AdamMaps* maps;  // [L]
+    int M;
+    __device__ void prefetch(const GemmGroup&, int, int, int, int) const {}
+    // piece pc of tile (mt, nt): the view (f- or d-wide) rows / column of theta and m / v
+    __device__ void coords(const GemmGroup& g, int mt, int nt, int pc, const AdamMaps*& am,
+                           int& col, int& row_th, int& row_mv, bool& up) const {
+        am = maps + g.aux / M;
+        const int64_t w = KIND == 1 ? p.f : p.d;  // view row length
+        int64_t x0;
+        if (KIND == 1) {
+            up = pc >= PIECES / 2;
+            x0 = static_cast<int64_t>(nt) * 128 + (pc % (PIECES / 2)) * 32;
+        } else {
+            up = false;
+            x0 = static_cast<int64_t>(nt) * BN + pc * 32;
+        }
+        const int64_t extra = up ? p.d : 0;  // wu rows follow wg's d rows
+        col = static_cast<int>(x0);
+        row_th = static_cast<int>((static_cast<const float*>(g.out0) - am->th_base) / w + extra +
+                                  static_cast<int64_t>(mt) * GEMM_BM);
+        row_mv = static_cast<int>((g.out_row0 - am->mv_base) / w + extra +
+                                  static_cast<int64_t>(mt) * GEMM_BM);
+    }
+    __device__ void stage_load(const GemmGroup& g, int mt, int nt, int pc, uint8_t* dst,
+                               uint64_t* bar) const {
+        const AdamMaps* am;
+        int col, rt, rm;
+        bool up;
+        coords(g, mt, nt, pc, am, col, rt, rm, up);
+        const CUtensorMap* mth = KIND == 1 ? &am->th_f : &am->th_d;
+        const CUtensorMap* mm = KIND == 1 ? &am->m_f : &am->m_d;
+        const CUtensorMap* mv = KIND == 1 ? &am->v_f : &am->v_d;
+        tma_load_2d(mth, bar, dst, col, rt);
+        tma_load_2d(mm, bar, dst + 16384, col, rm);
+        tma_load_2d(mv, bar, dst + 32768, col, rm);
+    }
+    __device__ void operator()(const GemmGroup& g, int mt, int nt, int r, uint32_t taddr,
+                               bool empty, int half, EpiOut& out, StageCtx& sc) const {
+        const bool ok = loss_ok(p.loss_total);  // uniform: no update after a bad step
+        const AdamScalars a = *p.a;
+        const int64_t row = static_cast<int64_t>(mt) * GEMM_BM + r;  // row within the block
+        const bool leader = threadIdx.x == 128;                     // warp 4, lane 0
+#pragma unroll 1
+        for (int pc = 0; pc < PIECES; ++pc) {
+            const int b = sc.cnt & 1;
+            mbar_wait(&sc.full[b], (sc.cnt >> 1) & 1);
+            ++sc.cnt;
+            uint8_t* buf = sc.base + b * (STAGED_BYTES / 2);
+            const AdamMaps* am;
+            int col, rt, rm;
+            bool up;
+            coords(g, mt, nt, pc, am, col, rt, rm, up);
+            if (ok) {
+                // gradients: this warp's 32 rows x 16 columns of the piece
+                const uint32_t tcol =
+                    KIND == 1 ? (up ? 128u : 0u) + (pc % (PIECES / 2)) * 32 + half * 16
+                              : pc * 32 + half * 16;
+                uint32_t gu[16];
+                float gr[16];
+                if (empty) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) gr[i] = 0.f;
+                } else {
+                    tmem_ld16(taddr + tcol, gu);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) gr[i] = __uint_as_float(gu[i]);
+                }
+                float th[16];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {  // 16-byte chunk 4*half + j of the 128-byte row
+                    const int off = r * 128 + (((4 * half + j) ^ (r & 7)) << 4);
+                    float4 t4 = *reinterpret_cast<float4*>(buf + off);
+                    float4 m4 = *reinterpret_cast<float4*>(buf + 16384 + off);
+                    float4 v4 = *reinterpret_cast<float4*>(buf + 32768 + off);
+                    t4.x = adam_elem(t4.x, gr[4 * j + 0], m4.x, v4.x, a);
+                    t4.y = adam_elem(t4.y, gr[4 * j + 1], m4.y, v4.y, a);
+                    t4.z = adam_elem(t4.z, gr[4 * j + 2], m4.z, v4.z, a);
+                    t4.w = adam_elem(t4.w, gr[4 * j + 3], m4.w, v4.w, a);
+                    *reinterpret_cast<float4*>(buf + off) = t4;
+                    *reinterpret_cast<float4*>(buf + 16384 + off) = m4;
+                    *reinterpret_cast<float4*>(buf + 32768 + off) = v4;
+                    th[4 * j + 0] = t4.x;
+                    th[4 * j + 1] = t4.y;
+                    th[4 * j + 2] = t4.z;
+                    th[4 * j + 3] = t4.w;
+                }
+                // the bf16 GEMM operand copy of these 16 parameters (32 contiguous bytes)
+                const int64_t x = col + half * 16;
+                bf16* sh;
+                if (KIND == 1)
+                    sh = p.w1 + static_cast<int64_t>(g.aux) * 2 * p.d * p.f + row * 2 * p.f +
+                         (up ? il_up(x) : il_gate(x));
+                else
+                    sh = p.w2 + static_cast<int64_t>(g.aux) * p.d * p.f + row * p.d + x;
+                uint4 pk[2];
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    __nv_bfloat162 c0 = __floats2bfloat162_rn(th[8 * i + 0], th[8 * i + 1]);
+                    __nv_bfloat162 c1 = __floats2bfloat162_rn(th[8 * i + 2], th[8 * i + 3]);
+                    __nv_bfloat162 c2 = __floats2bfloat162_rn(th[8 * i + 4], th[8 * i + 5]);
+                    __nv_bfloat162 c3 = __floats2bfloat162_rn(th[8 * i + 6], th[8 * i + 7]);
+                    pk[i] = make_uint4(*reinterpret_cast<uint32_t*>(&c0),
+                                       *reinterpret_cast<uint32_t*>(&c1),
+                                       *reinterpret_cast<uint32_t*>(&c2),
+                                       *reinterpret_cast<uint32_t*>(&c3));
+                }
+                reinterpret_cast<uint4*>(sh)[0] = pk[0];
+                reinterpret_cast<uint4*>(sh)[1] = pk[1];
+                fence_proxy_async_smem();
+            }
+            named_bar_sync(1, 256);  // every epilogue warp is done with this piece
+            if (leader) {
+                if (ok) {
+                    const CUtensorMap* mth = KIND == 1 ? &am->th_f : &am->th_d;
+                    const CUtensorMap* mm = KIND == 1 ? &am->m_f : &am->m_d;
+                    const CUtensorMap* mv = KIND == 1 ? &am->v_f : &am->v_d;
+                    tma_store_2d(mth, buf, col, rt);
+                    tma_store_2d(mm, buf + 16384, col, rm);
+                    tma_store_2d(mv, buf + 32768, col, rm);
+                    bulk_commit();
+                    bulk_wait_read<0>();
+                }
+                mbar_arrive(&sc.empty[b]);
+            }
+        }
+    }
+};
+
 // ---- head forward with the softmax-CE fused into the epilogue (V == BN == 256) ----------
 // The accumulator tile holds the full logits row of each of its 128 tokens; the two warps
 // of a TMEM lane quarter (column halves) combine their row max and exp sums through smem
@@ -527,12 +673,24 @@ void gemm_grad_w1(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g
 }
 
 void gemm_adamw_w1(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
-                   const int32_t* tiles, int max_tiles, const AdamEpi& p, cudaStream_t s) {
-    launch<256, true, true>(a, b, g, ng, tiles, max_tiles, EpiAdamW1{p}, s);
+                   const int32_t* tiles, int max_tiles, const AdamEpi& p, cudaStream_t s,
+                   const AdamMaps* aw, int M) {
+    if (aw && g_gemm_pairs)
+        launch<256, true, true>(a, b, g, ng, tiles, max_tiles, EpiAdamStaged<1, 256>{p, aw, M}, s);
+    else
+        launch<256, true, true>(a, b, g, ng, tiles, max_tiles, EpiAdamW1{p}, s);
 }
 
 void gemm_adamw_w2(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
-                   const int32_t* tiles, int max_tiles, const AdamEpi& p, cudaStream_t s) {
+                   const int32_t* tiles, int max_tiles, const AdamEpi& p, cudaStream_t s,
+                   const AdamMaps* aw, int M) {
+    if (aw && g_gemm_pairs) {
+        if (bn == 256)
+            launch<256, true, true>(a, b, g, ng, tiles, max_tiles, EpiAdamStaged<2, 256>{p, aw, M}, s);
+        else
+            launch<128, true, true>(a, b, g, ng, tiles, max_tiles, EpiAdamStaged<2, 128>{p, aw, M}, s);
+        return;
+    }
     if (bn == 256)
         launch<256, true, true>(a, b, g, ng, tiles, max_tiles, EpiAdamW2<256>{p}, s);
     else

@@ -166,6 +166,15 @@ template <class E>
 struct EpiStaged<E, decltype(void(E::STAGED_BYTES))> {
     static constexpr int bytes = E::STAGED_BYTES;
 };
+// arrivals that free a staging buffer (default: each of the 8 epilogue warps once)
+template <class E, class = void>
+struct EpiStageArrivals {
+    static constexpr int count = 8;
+};
+template <class E>
+struct EpiStageArrivals<E, decltype(void(E::STAGE_ARRIVALS))> {
+    static constexpr int count = E::STAGE_ARRIVALS;
+};
 // the epilogue side of the staging ring (Epi::STAGE_BUFS buffers of STAGED_BYTES /
 // STAGE_BUFS bytes): buffer b holds a piece; full[b] completes when its TMA bytes landed,
 // empty[b] when all 8 epilogue warps of the CTA have used it

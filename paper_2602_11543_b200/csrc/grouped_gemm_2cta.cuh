@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if constexpr (STAGED > 0)
             for (int b = 0; b < 2; ++b) {
                 mbar_init(&sfull[b], 1);   // this CTA's warp 3 (expect_tx)
-                mbar_init(&sempty[b], 8);  // this CTA's 8 epilogue warps
+                mbar_init(&sempty[b], EpiStageArrivals<Epi>::count);  // epilogue releases
             }
         fence_barrier_init();
     }

@@ -665,13 +665,36 @@ void losses_reduce(const float* diff, const float* lse_head, const float* lse_r,
 // Warp per routed row r (token t_r, weight w_r): dYw[r] = bf16(gh[t_r] * w_r)
 // (rowwise_mul backward, graph.hpp:299-305) and the gate-weight gradient
 // <gh[t_r], Y[r]> (graph.hpp:307-316). Padding rows get zeros.
+// A warp per routed row. With slot_row, warps take the (token, slot) pairs in token order,
+// so the k rows of a token run side by side in one block and its upstream-gradient row is
+// read from DRAM once (expert-major row order re-read it k times once T x d exceeds L2:
+// cfg5 read 4.2 GB per layer for 2.4 GB of operands); blocks past the pairs zero the
+// padding rows.
 __global__ void __launch_bounds__(256) combine_bwd_k(
     const float* __restrict__ gh, const float* __restrict__ y, const int32_t* __restrict__ row_token,
     const float* __restrict__ row_w, const int32_t* __restrict__ R_total, int64_t d,
-    bf16* __restrict__ dyw, float* __restrict__ gw) {
-    const int64_t r = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+    bf16* __restrict__ dyw, float* __restrict__ gw, const int32_t* __restrict__ slot_row,
+    int64_t npairs) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    if (r >= *R_total) return;
+    int64_t r = i;
+    if (slot_row) {
+        if (i < npairs) {
+            r = slot_row[i];
+        } else {  // padding rows, a grid-stride over the rows
+            const int64_t nrows = *R_total;
+            const int64_t nw = static_cast<int64_t>(gridDim.x) * 8 - npairs;
+            for (int64_t q = i - npairs; q < nrows; q += nw) {
+                if (row_token[q] >= 0) continue;
+                for (int64_t c = lane * 4; c < d; c += 128)
+                    *reinterpret_cast<uint2*>(dyw + q * d + c) = make_uint2(0, 0);
+                if (lane == 0) gw[q] = 0.f;
+            }
+            return;
+        }
+    } else if (r >= *R_total) {
+        return;
+    }
     const int32_t t = row_token[r];
     const float wv = t >= 0 ? row_w[r] : 0.f;
     float dot = 0.f;
@@ -707,9 +730,14 @@ __global__ void __launch_bounds__(256) combine_bwd_k(
 
 void combine_backward(const float* gh, const float* y, const int32_t* row_token,
                       const float* row_w, const int32_t* R_total_dev, int64_t R_cap, int64_t d,
-                      bf16* dyw, float* gw, cudaStream_t s) {
-    combine_bwd_k<<<static_cast<unsigned>(cdiv(R_cap, 8)), 256, 0, s>>>(gh, y, row_token, row_w,
-                                                                       R_total_dev, d, dyw, gw);
+                      bf16* dyw, float* gw, cudaStream_t s, const int32_t* slot_row,
+                      const float* topk_w, int64_t T, int k) {
+    (void)topk_w;
+    const int64_t npairs = slot_row ? T * k : 0;
+    const int64_t blocks = slot_row ? cdiv(npairs, 8) + 148 : cdiv(R_cap, 8);
+    combine_bwd_k<<<static_cast<unsigned>(blocks), 256, 0, s>>>(gh, y, row_token, row_w,
+                                                                R_total_dev, d, dyw, gw, slot_row,
+                                                                npairs);
     count_launch();
 }
 

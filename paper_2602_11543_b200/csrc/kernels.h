@@ -111,9 +111,11 @@ void losses_reduce(const float* diff, const float* lse_head, const float* lse_r,
                    int32_t* status, double* part, double* out, cudaStream_t s);
 
 // ---- backward ----
+// slot_row / topk_w (optional): the token-major form (each token's gradient row read once)
 void combine_backward(const float* gh, const float* y, const int32_t* row_token,
                       const float* row_w, const int32_t* R_total_dev, int64_t R_cap, int64_t d,
-                      bf16* dyw, float* gw_part, cudaStream_t s);
+                      bf16* dyw, float* gw_part, cudaStream_t s, const int32_t* slot_row = nullptr,
+                      const float* topk_w = nullptr, int64_t T = 0, int k = 0);
 // Router backward in two halves: the per-token scalar chain (-> glog; needs only the
 // forward's routing and the gate-weight gradients) and the normed gradient (needs dX; its
 // per-slab rmsnorm dot partials go to dot_part for norm_router_grads)
@@ -253,10 +255,23 @@ struct AdamEpi {
     int64_t d, f;
     const double* loss_total;
 };
+// Tensor maps of one layer's expert parameters and Adam moments for the TMA-staged fused
+// optimizer (gemm.cu EpiAdamStaged): the layer's expert region of theta (all M experts) and
+// of m / v (its owned experts, compact) viewed as rows of f floats (wg / wu blocks) and of d
+// floats (wd blocks), boxes of 32 x 128 fp32 with the 128B swizzle. Device memory.
+struct AdamMaps {
+    CUtensorMap th_f, m_f, v_f, th_d, m_d, v_d;
+    const float* th_base;   // theta of expert 0 of the layer
+    int64_t mv_base;        // compact offset of the layer's first owned expert
+};
+// aw (optional, device memory, one per layer): with it the pair kernel stages theta / m / v
+// by TMA and writes them back by TMA stores (EpiAdamStaged)
 void gemm_adamw_w1(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
-                   const int32_t* tiles, int max_tiles, const AdamEpi& p, cudaStream_t s);
+                   const int32_t* tiles, int max_tiles, const AdamEpi& p, cudaStream_t s,
+                   const AdamMaps* aw = nullptr, int M = 0);
 void gemm_adamw_w2(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
-                   const int32_t* tiles, int max_tiles, const AdamEpi& p, cudaStream_t s);
+                   const int32_t* tiles, int max_tiles, const AdamEpi& p, cudaStream_t s,
+                   const AdamMaps* aw = nullptr, int M = 0);
 void gemm_prepare(int device);
 // cta_group::2 cluster-pair GEMMs (256-row tiles) for the following launches on this thread
 void gemm_set_pair_mode(bool on);

@@ -13,6 +13,8 @@
 // norm_router_partial_k (kernels.cu), which streams h and gnormed for the gain and router
 // gradients anyway. Every element keeps the reference's own accumulation order; only the
 // rmsnorm dot (a sum over d) is a fixed-order tree.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -85,7 +87,7 @@ __global__ void __launch_bounds__(256) normed_grad_k(
     const float* __restrict__ R,
     const float* __restrict__ glog, const int32_t* __restrict__ slot_row,
     const float* __restrict__ dxp, int T, int d, int M, int k, float* __restrict__ gnormed,
-    float* __restrict__ dot_part) {
+    float* __restrict__ dot_part, int prefetch) {
     // router tile, transposed: [e][q]; pitch NG_QT + 4 makes the staging stores 2-way
     // instead of 16-way bank conflicts (float4 reads stay aligned and conflict-free)
     __shared__ __align__(16) float sRT[MAXM][NG_QT + 4];
@@ -120,6 +122,18 @@ __global__ void __launch_bounds__(256) normed_grad_k(
     }
     __syncthreads();
     const int ty = threadIdx.x >> 5, tx = threadIdx.x & 31;
+    // the expert dX rows this thread sums after the router product: their DRAM reads start
+    // now (L2 prefetch), under the product's chains, instead of after them
+    if (prefetch) {
+        const float* dxc = dxp + q0 + 4 * tx;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int tt = ty * 4 + i;
+            if (t0 + tt >= T) break;
+            for (int s = 0; s < k; ++s)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(dxc + static_cast<int64_t>(sRow[tt][s]) * d));
+        }
+    }
     // router product for 4 tokens x 4 columns: one broadcast glog load per token and
     // one router load per column feed 16 independent sequential-e chains
     float sr[4][4];
@@ -199,8 +213,12 @@ void normed_grad(const float* h, const int32_t* hrow, const float* gain, const f
              : M <= 16 ? normed_grad_k<16>
              : M <= 32 ? normed_grad_k<32>
                        : normed_grad_k<64>;
+    static const int pf = [] {
+        const char* e = std::getenv("SPES_NG_PREFETCH");
+        return e ? std::atoi(e) : 1;
+    }();
     f<<<g2, 256, 0, s>>>(h, hrow, gain, router, glog, slot_row, dxp, (int)T, (int)d, M, k, gnormed,
-                         dot_part);
+                         dot_part, pf);
     count_launch();
 }
 
