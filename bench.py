@@ -255,6 +255,10 @@ def gemm_rooflines(fam, cfg, counts, owned, T, peak, steps):
     fl = {"gemm_fwd_gate_up": 4 * R * d * f, "gemm_fwd_down": 2 * R * d * f,
           "gemm_bwd_dh": 2 * R * d * f, "gemm_bwd_dx": 4 * R * d * f,
           "gemm_bwd_dw_gate_up": 4 * R_own * d * f, "gemm_bwd_dw_down": 2 * R_own * d * f}
+    # the fused placement (SPES_FUSED_OPT=1) times the dW GEMMs with their MaskedAdamW
+    for k_ in list(fl):
+        if k_ + "+adamw" in fam:
+            fl[k_ + "+adamw"] = fl[k_]
     out = {}
     for k_, x in fl.items():
         if k_ not in fam:
@@ -276,7 +280,9 @@ def sync_roofline(st, N):
     gbs = b / (st["ms"] / 1e3) / 1e9
     return {"bound": "nvlink", "ms": st["ms"], "bytes_in": b, "achieved": gbs, "peak": 900.0,
             "unit": "GB/s", "frac": gbs / 900.0,
-            "note": "rank 0; ms includes the owner means, barriers and operand-copy writes"}
+            "note": "rank 0; ms runs from the moment every node has arrived (waiting for slower "
+                    "nodes' local rounds excluded) and includes the owner means, pulls, barrier "
+                    "and operand-copy writes"}
 
 
 def ncu_traffic(cfg_name):

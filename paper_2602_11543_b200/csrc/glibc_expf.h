@@ -10,6 +10,10 @@
 // (ifunc __expf_fma) on CPUs with FMA+AVX2, so both evaluation orders are
 // provided and the host's is detected at runtime; tests check the device port
 // exhaustively against host expf over [-104, 0].
+//
+// Attribution: the 2^(i/32) table, the polynomial coefficients and the evaluation scheme
+// are those of ARM optimized-routines' expf (Copyright (c) 2017-2018, Arm Limited; MIT /
+// Apache-2.0 WITH LLVM-exception) as shipped in the GNU C Library (LGPL-2.1-or-later).
 #pragma once
 
 #include <stdint.h>

@@ -7,12 +7,13 @@
 // Two kernels here, each streaming its operands once:
 //   router_scalar_bwd_k : thread per token, the M-wide scalar chain  -> glog [T x M]
 //   normed_grad_k       : 32-token x 128-column tiles; per element the dX sum (descending
-//                         experts) then the sequential-e router product; per-tile partial
-//                         of sum_q (gy*g)*x for the rmsnorm dot
+//                         experts) then the router product over e ascending (fused
+//                         multiply-adds: a gradient, tolerance-level); per-tile partial of
+//                         sum_q (gy*g)*x for the rmsnorm dot
 // The rmsnorm backward itself (h.grad += (gy*g)*inv - coef*x) runs inside
 // norm_router_partial_k (kernels.cu), which streams h and gnormed for the gain and router
-// gradients anyway. Every element keeps the reference's own accumulation order; only the
-// rmsnorm dot (a sum over d) is a fixed-order tree.
+// gradients anyway. Every element keeps the reference's accumulation order (the router
+// product with FMA); the rmsnorm dot (a sum over d) is a fixed-order tree.
 #include <cstdlib>
 
 #include "common.cuh"
@@ -149,14 +150,11 @@ __global__ void __launch_bounds__(256) normed_grad_k(
         for (int i = 0; i < 4; ++i) g[i] = sG[ty * 4 + i][e];
         const float4 r4 = *reinterpret_cast<const float4*>(&sRT[e][4 * tx]);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const float2 gi = make_float2(g[i], g[i]);
-            const float2 p01 = fmul2(gi, make_float2(r4.x, r4.y));
-            const float2 p23 = fmul2(gi, make_float2(r4.z, r4.w));
-            sr[i][0] = fadd(sr[i][0], p01.x);
-            sr[i][1] = fadd(sr[i][1], p01.y);
-            sr[i][2] = fadd(sr[i][2], p23.x);
-            sr[i][3] = fadd(sr[i][3], p23.y);
+        for (int i = 0; i < 4; ++i) {  // fused multiply-adds (a gradient: tolerance-level)
+            sr[i][0] = fmaf(g[i], r4.x, sr[i][0]);
+            sr[i][1] = fmaf(g[i], r4.y, sr[i][1]);
+            sr[i][2] = fmaf(g[i], r4.z, sr[i][2]);
+            sr[i][3] = fmaf(g[i], r4.w, sr[i][3]);
         }
     }
     const float4 gq = __ldg(reinterpret_cast<const float4*>(gain + q0 + 4 * tx));
