@@ -552,6 +552,9 @@ int num_sms() {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
         if (g_num_sms <= 0) g_num_sms = 148;
+        // experiments: persistent GEMM grids over fewer SMs (the rest left to the side stream)
+        if (const char* e = std::getenv("SPES_GEMM_SMS"))
+            g_num_sms = std::max(2, std::min(g_num_sms, std::atoi(e)));
     }
     return g_num_sms;
 }

@@ -749,7 +749,6 @@ void combine_backward(const float* gh, const float* y, const int32_t* row_token,
 // each thread keeps 4 columns x 16 experts of router-gradient partials in registers.
 constexpr int NRG_TC = kNormRouterChunks;
 constexpr int NG_QT_RMS = 128;  // columns per normed_grad tile = dot partials per token (d / 128)
-constexpr int NRG_EG = 16;
 // With `gh` non-null the z = 0 blocks also apply the rmsnorm backward to their columns
 // (kernels.hpp:130-152; the dot from normed_grad's slab partials, summed in slab order):
 // h.grad += (gy*g)*inv - coef*x, so h and gnormed
@@ -776,16 +775,22 @@ __device__ __forceinline__ void cp_async4_nr(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_commit_nr() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 
+template <int NRG_EG>
 __global__ void __launch_bounds__(256) norm_router_partial_k(
     const float* __restrict__ h, const int32_t* __restrict__ hrow,
     const float* __restrict__ gain, const float* __restrict__ gnormed,
     const float* __restrict__ glog, const float* __restrict__ inv_rms, int T, int d, int dn, int M,
     float* __restrict__ partial, const float* __restrict__ dot_part, float* __restrict__ gh) {
     extern __shared__ __align__(16) float4 ring[];  // [NRG_S][3][256]
-    __shared__ __align__(16) float sgl[2][64][NRG_EG];
+    // glog and dot-partial staging during the token loop; the final warp reduction reuses
+    // the same bytes (static shared memory stays under 48 KB at 32 experts per block)
+    constexpr int SGL = 2 * 64 * NRG_EG, SDOT = 2 * 64 * NRG_NP_SMEM, RED = 32 * 4 * (NRG_EG + 1);
+    constexpr int RAW = (SGL + SDOT) > RED ? SGL + SDOT : RED;
+    __shared__ __align__(16) float sraw[RAW];
     __shared__ float sinv[2][64];
-    __shared__ float sdot[2][64 * NRG_NP_SMEM];  // larger d reads dot_part directly
-    __shared__ float red[32][4][NRG_EG + 1];
+    float(*sgl)[64][NRG_EG] = reinterpret_cast<float(*)[64][NRG_EG]>(sraw);
+    float(*sdot)[64 * NRG_NP_SMEM] = reinterpret_cast<float(*)[64 * NRG_NP_SMEM]>(sraw + SGL);
+    float(*red)[4][NRG_EG + 1] = reinterpret_cast<float(*)[4][NRG_EG + 1]>(sraw);
     const int ph = threadIdx.x >> 5, tx = threadIdx.x & 31;
     const int q = blockIdx.x * 128 + 4 * tx;
     const int chunk = blockIdx.y;
@@ -916,6 +921,7 @@ __global__ void __launch_bounds__(256) norm_router_partial_k(
         }
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();  // the staging bytes become the reduction buffer
     // combine the 8 warps in warp order (fixed), then write this chunk's partial
     for (int w = 0; w < 8; ++w) {
         __syncthreads();
@@ -957,18 +963,30 @@ __global__ void norm_router_finish_k(const float* __restrict__ partial, int d, i
         g_router[static_cast<int64_t>(q) * M + (c - 1)] = s;
 }
 
+// 32 experts per block (SPES_NRG_WIDE=1) measured slower at cfg5 (225 vs 177 ms per round:
+// 184 registers, one block per SM), so 16 is the default
+static const int g_nrg_wide = [] {
+    const char* e = std::getenv("SPES_NRG_WIDE");
+    return e ? std::atoi(e) : 0;
+}();
 void norm_router_grads(const float* h, const int32_t* hrow, const float* gain, const float* gnormed,
                        const float* glog, const float* inv_rms, int64_t T, int64_t d, int64_t dn,
                        int M, float* partial, float* g_gain, float* g_router, const float* dot_part,
                        float* gh, cudaStream_t s) {
-    dim3 grid(static_cast<unsigned>(d / 128), NRG_TC, static_cast<unsigned>((M + NRG_EG - 1) / NRG_EG));
+    // 32 experts per block for M > 16: h streamed and normed rebuilt M/32 times, not M/16
+    const int eg = (M > 16 && g_nrg_wide) ? 32 : 16;
+    dim3 grid(static_cast<unsigned>(d / 128), NRG_TC, static_cast<unsigned>((M + eg - 1) / eg));
     constexpr int ring_bytes = NRG_S * 3 * 256 * 16;
     static std::atomic<uint64_t> attr_set{0};
-    if (first_use_on_device(attr_set))
-        cudaFuncSetAttribute(norm_router_partial_k, cudaFuncAttributeMaxDynamicSharedMemorySize, ring_bytes);
-    norm_router_partial_k<<<grid, 256, ring_bytes, s>>>(h, hrow, gain, gnormed, glog, inv_rms, (int)T,
-                                                        (int)d, (int)dn, M,
-                                               partial, dot_part, gh);
+    if (first_use_on_device(attr_set)) {
+        cudaFuncSetAttribute(norm_router_partial_k<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             ring_bytes);
+        cudaFuncSetAttribute(norm_router_partial_k<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             ring_bytes);
+    }
+    auto kern = eg == 32 ? norm_router_partial_k<32> : norm_router_partial_k<16>;
+    kern<<<grid, 256, ring_bytes, s>>>(h, hrow, gain, gnormed, glog, inv_rms, (int)T, (int)d,
+                                       (int)dn, M, partial, dot_part, gh);
     const int64_t n = d * (M + 1);
     norm_router_finish_k<<<static_cast<unsigned>(cdiv(n, 256)), 256, 0, s>>>(partial, (int)d, M,
                                                                             g_gain, g_router);
