@@ -368,7 +368,9 @@ def reference_arm(args):
     rank, world, local = dist_env()
     if rank != 0:
         return 0
-    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+    # all host cores for the one process that runs (torchrun sets OMP_NUM_THREADS=1 for its
+    # ranks; the reference's OpenMP runtime reads it when oracle/_ref is first loaded)
+    os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
     vals = []
     # a CPU sample needs no more than one warm-up (page-in); each step is one bounded sample
     warm = min(args.warmup, 1)

@@ -1,9 +1,11 @@
-for cfg in "17 1" "20 1" "20 0"; do set -- $cfg
-SPES_SYNC_CHUNK=$1 SPES_SYNC_ORDER=$2 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 4 --config cfg5 --H 1 --steps 3 --warmup 2 --e2e-steps 0 --prof-rounds 0 --no-cpu-baseline > gpurun_out/r2_m6_$1_$2.json 2> gpurun_out/r2_m6_$1_$2.err
-python -c "
-import json;d=json.load(open('gpurun_out/r2_m6_$1_$2.json'));print('chunk $1 order $2',d['value'],d['ms_per_step'],d['sync']['ms'],d['sync']['frac'])"
+O=gpurun_out/ev3m
+mkdir -p $O
+timeout 1200 python -m pytest tests/test_gpu_multi.py -m gpu -q -p no:cacheprovider 2>&1 | tail -5 > $O/pytest_gpu_multi.txt
+cat $O/pytest_gpu_multi.txt
+for N in 2 4; do
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2951$N bench.py --gpus $N --steps 3 --warmup 3 > $O/bench_cfg5_n$N.json 2> $O/bench_cfg5_n$N.err
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2952$N bench.py --gpus $N --impl reference --steps 2 --warmup 1 > $O/bench_reference_n$N.json 2> $O/bench_reference_n$N.err
 done
-timeout 900 python -m pytest tests/test_gpu_multi.py -m gpu -q -p no:cacheprovider 2>&1 | tail -3
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29513 bench.py --gpus 4 --config cfg2 --steps 10 --warmup 3 --e2e-steps 0 --prof-rounds 0 --no-cpu-baseline > gpurun_out/r2_m6_cfg2_n4.json 2> gpurun_out/r2_m6_cfg2_n4.err
-python -c "
-import json;d=json.load(open('gpurun_out/r2_m6_cfg2_n4.json'));print('cfg2 n4',d['value'],d['ms_per_step'],d['sync']['ms'],d['sync']['frac'])"
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 4 --config cfg2 --steps 10 --warmup 3 > $O/bench_cfg2_n4.json 2> $O/bench_cfg2_n4.err
+for f in $O/*.json; do python -c "
+import json;d=json.load(open('$f'));print('$f',d.get('value'),d.get('ms_per_step'),(d.get('e2e') or {}).get('value'),(d.get('sync') or {}).get('ms'),(d.get('sync') or {}).get('frac'))" 2>/dev/null; done

@@ -1,7 +1,8 @@
 """Synthetic corpus and batch streams against the UNMODIFIED reference's
 gen_corpus / shard_corpus / make_batch_provider (proj/src/corpus.cpp via oracle/_ref), and
 the device-resident corpus path: a local round over corpus rows equals the same round over
-host-uploaded tokens bit for bit."""
+host-uploaded tokens bit for bit, and the reference's own batches trained by the oracle
+within the loss tolerance."""
 import numpy as np
 import pytest
 
@@ -77,6 +78,16 @@ def test_device_corpus_round_equals_host_tokens():
         lb = b.local_round(tok[rows], adamw_cfg())
         assert np.array_equal(la, lb)
         assert np.array_equal(a.read_params().view(np.uint32), b.read_params().view(np.uint32))
+        # against the reference itself: its own provider's batches (make_batch_provider over
+        # its gen_corpus, via oracle/_ref) trained by the CPU oracle's local_round
+        if oracle.ref_available():
+            ref_b = np.zeros((3, 4, c["seq"] + 1), np.int32)
+            oracle.ref().ref_batches(c["vocab"], c["seq"], c["sources"], c["sequences"],
+                                     c["seed"], np.arange(c["sequences"], dtype=np.int64),
+                                     c["sequences"], 4, 3, 3, ref_b)
+            assert np.array_equal(ref_b, tok[rows])  # the device gathered the same batches
+            _, l_ref = oracle.local_round(cfg, params, ref_b, [0, 1, 2, 3], adamw_cfg())
+            assert np.allclose(la[:, 0], l_ref[:, 0], rtol=5e-3)
         with pytest.raises(spes.SpesError) as e:
             a.local_step_rows(np.array([c["sequences"]]))
         assert e.value.kind == "out_of_range"
