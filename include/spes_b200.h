@@ -196,6 +196,14 @@ spes_status spes_batch_stream_next(spes_batch_stream* s, int64_t* rows);
 void spes_batch_stream_destroy(spes_batch_stream* s);
 /* corpus -> HBM (token ids validated once) */
 spes_status spes_corpus_load(spes_ctx* ctx, const int32_t* tokens, int64_t sequences, int64_t seq);
+/* gen_corpus (corpus.cpp:49-79) generated straight into this context's HBM corpus: the
+ * Markov sources are built on the host (make_source's rejection-sampled normals), then the
+ * device replays the engine and samples every sequence's chain; the same tokens as
+ * spes_gen_corpus bit for bit. vocab <= the model's vocabulary. tokens_out (sequences x
+ * (seq+1)) and source_id_out (sequences) may be NULL. */
+spes_status spes_corpus_generate(spes_ctx* ctx, int64_t vocab, int64_t seq, int32_t sources,
+                                 int64_t sequences, uint64_t seed, double skew,
+                                 int32_t* tokens_out, int32_t* source_id_out);
 /* local step / round over corpus rows (rows: B, resp. H x B indices) */
 spes_status spes_local_step_rows(spes_ctx* ctx, const int64_t* rows, int64_t B,
                                  const spes_adamw_cfg* opt, spes_losses* losses);

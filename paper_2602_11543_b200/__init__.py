@@ -89,6 +89,8 @@ def lib():
         L.spes_batch_stream_destroy.argtypes = [vp]
         L.spes_batch_stream_destroy.restype = None
         L.spes_corpus_load.argtypes = [vp, C.POINTER(C.c_int32), i64, i64]
+        L.spes_corpus_generate.argtypes = [vp, i64, i64, C.c_int32, i64, C.c_uint64, C.c_double,
+                                           C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
         L.spes_local_step_rows.argtypes = [vp, i64p, i64, C.POINTER(AdamWCfg), C.POINTER(Losses)]
         L.spes_local_round_rows.argtypes = [vp, i64p, i64, C.c_int32, C.POINTER(C.c_double),
                                             C.POINTER(AdamWCfg), C.c_int32, C.POINTER(Losses)]
@@ -427,6 +429,16 @@ class Node:
         """Upload a corpus [sequences, S+1] to HBM once (token ids validated here)."""
         tokens = np.ascontiguousarray(tokens, np.int32)
         _check(lib().spes_corpus_load(self._ctx, i32(tokens), tokens.shape[0], tokens.shape[1] - 1))
+
+    def corpus_generate(self, vocab, seq, sources, sequences, seed, skew=0.0, fetch=True):
+        """gen_corpus (corpus.cpp:49-79) generated on the device into this node's HBM corpus;
+        returns (tokens [sequences, seq+1], source_id) when fetch, else None."""
+        tok = np.zeros((sequences, seq + 1), np.int32) if fetch else None
+        sid = np.zeros(sequences, np.int32) if fetch else None
+        _check(lib().spes_corpus_generate(self._ctx, vocab, seq, sources, sequences, seed, skew,
+                                          i32(tok) if fetch else None,
+                                          i32(sid) if fetch else None))
+        return (tok, sid) if fetch else None
 
     def local_step_rows(self, rows, opt=None):
         rows = np.ascontiguousarray(rows, np.int64)

@@ -224,10 +224,10 @@ struct spes_ctx {
     // identical bits; the fused epilogue is issue/latency-bound at ~3.7 TB/s with the 8
     // epilogue warps that fit next to the MMA ring, so it does not beat the separate pass yet.
     bool fused_opt = false;
-    // dSwiGLU factor rows staged by TMA (SPES_DSWIGLU_TMA=0: off). One staging buffer
-    // leaves room for 4 operand stages instead of 5 (two buffers: 3). Only for d <= 2048:
-    // at cfg2 (d = 1024) dH goes 641 -> 774 TFLOP/s (two buffers: 719), at cfg5 (d = 4096,
-    // long K) the shallower ring costs more than the epilogue gains (1140 -> 984)
+    // dSwiGLU factor rows staged by TMA (SPES_DSWIGLU_TMA=0: off; default variant 4: 32-column
+    // pieces written back in place, 3 buffers, 5 operand stages; dH cfg2 641 -> 831 TFLOP/s,
+    // cfg5 1112 -> 1182). Variants 1 / 2 (64-column pieces through the transpose slots) cost
+    // operand stages and are only used for d <= 2048
     bool staged_dswiglu = true;
     // inner optimizer (LocalRoundConfig::inner, trainer.hpp:116-121): AdamW, or SGD
     // (theta -= lr * g, no moments; always the standalone pass)
@@ -291,6 +291,7 @@ struct spes_ctx {
     double* d_losses = nullptr;
     GemmGroup* head_groups = nullptr;  // [2 + head_split]: fwd, dX, dW K-splits
     CUtensorMap* gu_maps = nullptr;    // [L] per layer's GU as {64 x 128} boxes (device memory)
+    CUtensorMap* dsw_maps = nullptr;   // [L][2] GU {32 x 128} + dGU {32 x 32}, 64B swizzle
     int32_t* head_tiles = nullptr;     // [3]
     int head_max[3] = {0, 0, 0};
     int head_split = 1;
@@ -589,6 +590,17 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     }
     c->dyw = A.alloc<bf16>(R * d);
     c->dgu = A.alloc<bf16>(R * 2 * f);
+    {  // the in-place variant: 32-column factor pieces and the dGU stores
+        std::vector<CUtensorMap> dm(2 * L.L);
+        for (int l = 0; l < L.L; ++l) {
+            dm[2 * l] = spes_host::make_tmap_bf16_sw64(c->layers[l].gu, R, 2 * f, 128);
+            dm[2 * l + 1] = spes_host::make_tmap_bf16_sw64(c->dgu, R, 2 * f, 32);
+        }
+        c->dsw_maps = A.alloc<CUtensorMap>(2 * L.L);
+        ck(cudaMemcpy(c->dsw_maps, dm.data(), sizeof(CUtensorMap) * 2 * L.L,
+                      cudaMemcpyHostToDevice),
+           "dswiglu maps");
+    }
     c->dxp = A.alloc<float>(R * d);
     c->gw_part = A.alloc<float>(R);
     c->dot_part = A.alloc<float>(Tp * (d / 128));
@@ -869,7 +881,8 @@ void forward_backward(spes_ctx* c) {
             PROF("gemm_bwd_dh");
             spes_k::gemm_dswiglu(bn_for(f), c->a_dyw, Y.b_w2, Y.groups + 2 * M, M, Y.tiles + 2,
                                  c->max_tiles[2], Y.gu, f,
-                                 c->staged_dswiglu && d <= 2048 ? c->gu_maps + l : nullptr, st);
+                                 c->staged_dswiglu && d <= 2048 ? c->gu_maps + l : nullptr,
+                                 c->staged_dswiglu ? c->dsw_maps + 2 * l : nullptr, st);
         }
         if (unfused_dw) {
             {
@@ -1199,7 +1212,7 @@ spes_status spes_create(const spes_model_cfg* cfg, int32_t node, int32_t n_nodes
         if (const char* e = std::getenv("SPES_FUSED_OPT")) c->fused_opt = std::atoi(e) != 0;
         if (const char* e = std::getenv("SPES_EARLY_WD")) c->early_wd = std::atoi(e) != 0;
         if (const char* e = std::getenv("SPES_STEP_GRAPH")) c->use_graph = std::atoi(e) != 0;
-        if (const char* e = std::getenv("SPES_DSWIGLU_TMA")) {  // 0 off, 1 / 2 staging buffers
+        if (const char* e = std::getenv("SPES_DSWIGLU_TMA")) {  // 0 off, else the variant (1-4)
             c->staged_dswiglu = std::atoi(e) != 0;
             if (c->staged_dswiglu) spes_k::gemm_dswiglu_buffers(std::atoi(e));
         }
@@ -1644,6 +1657,9 @@ void shard_corpus(const int32_t* source_id, int64_t n, int nodes, int by_source,
 BatchStream* stream_create(const int64_t* shard, int64_t n, int64_t batch, uint64_t seed);
 void stream_next(BatchStream* s, int64_t* rows);
 void stream_destroy(BatchStream* s);
+void prepare_device_corpus(int64_t vocab, int64_t seq, int sources, int64_t sequences,
+                           uint64_t seed, double skew, std::vector<double>& cum,
+                           uint64_t* state, int* pos);
 }
 }
 struct spes_batch_stream {
@@ -1693,6 +1709,60 @@ spes_status spes_corpus_load(spes_ctx* c, const int32_t* tokens, int64_t sequenc
         ck(cudaMemcpy(c->corpus, tokens, sizeof(int32_t) * sequences * (seq + 1),
                       cudaMemcpyHostToDevice),
            "corpus H2D");
+        c->corpus_rows = sequences;
+        c->corpus_seq = seq;
+    });
+}
+
+spes_status spes_corpus_generate(spes_ctx* c, int64_t vocab, int64_t seq, int32_t sources,
+                                 int64_t sequences, uint64_t seed, double skew,
+                                 int32_t* tokens_out, int32_t* source_id_out) {
+    return guard([&] {
+        if (vocab > c->ulay.V)
+            throw std::invalid_argument("corpus: vocabulary larger than the model's");
+        std::vector<double> cum;
+        uint64_t state[312];
+        int pos = 0;
+        spes_corpus::prepare_device_corpus(vocab, seq, sources, sequences, seed, skew, cum, state,
+                                           &pos);
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        const int64_t n = sequences * (seq + 1);
+        if (c->corpus) cudaFree(c->corpus);
+        c->corpus = nullptr;
+        c->corpus_rows = 0;
+        ck(cudaMalloc(&c->corpus, sizeof(int32_t) * n), "corpus alloc");
+        double *d_cum = nullptr, *d_u = nullptr;
+        uint64_t* d_state = nullptr;
+        auto release = [&] {
+            cudaFree(d_cum);
+            cudaFree(d_u);
+            cudaFree(d_state);
+        };
+        try {
+            ck(cudaMalloc(&d_cum, sizeof(double) * cum.size()), "corpus tables");
+            ck(cudaMalloc(&d_u, sizeof(double) * n), "corpus draws");
+            ck(cudaMalloc(&d_state, sizeof(state)), "engine state");
+            ck(cudaMemcpyAsync(d_cum, cum.data(), sizeof(double) * cum.size(),
+                               cudaMemcpyHostToDevice, c->stream),
+               "H2D tables");
+            ck(cudaMemcpyAsync(d_state, state, sizeof(state), cudaMemcpyHostToDevice, c->stream),
+               "H2D state");
+            spes_k::corpus_draws(d_state, pos, n, d_u, c->stream);
+            spes_k::corpus_chains(d_cum, d_u, sequences, seq, static_cast<int>(vocab), sources,
+                                  c->corpus, c->stream);
+            ck(cudaGetLastError(), "corpus kernels");
+            if (tokens_out)
+                ck(cudaMemcpyAsync(tokens_out, c->corpus, sizeof(int32_t) * n,
+                                   cudaMemcpyDeviceToHost, c->stream),
+                   "D2H corpus");
+            ck(cudaStreamSynchronize(c->stream), "corpus generation");
+        } catch (...) {
+            release();
+            throw;
+        }
+        release();
+        if (source_id_out)
+            for (int64_t r = 0; r < sequences; ++r) source_id_out[r] = static_cast<int32_t>(r % sources);
         c->corpus_rows = sequences;
         c->corpus_seq = seq;
     });
@@ -2333,8 +2403,11 @@ spes_status spes_merge(spes_ctx* c, const spes_merge_sched* sched, int32_t round
                 ck(cudaMemcpyAsync(c->layer_expert_offs, hp->eo, 8 * M, cudaMemcpyHostToDevice,
                                    c->stream),
                    "eo");
+                // the merged experts' bf16 operand copies are written from the same values
+                // (no refresh pass over the experts afterwards)
+                const spes_k::Shadows shm = shadows_of(c);
                 spes_k::merge_apply(c->params, c->layer_expert_offs, M, L.per_expert(), c->peers_dev,
-                                    K, c->coef, c->disp_partial, nblocks, c->stream);
+                                    K, c->coef, c->disp_partial, nblocks, c->stream, &shm, l * M);
                 ck(cudaMemcpyAsync(hp->disp, c->disp_partial, 8 * nblocks, cudaMemcpyDeviceToHost,
                                    c->stream),
                    "disp");
@@ -2350,10 +2423,6 @@ spes_status spes_merge(spes_ctx* c, const spes_merge_sched* sched, int32_t round
             }
             if (peers_out)
                 std::memcpy(peers_out + static_cast<size_t>(l) * M * K, peers.data(), 4 * M * K);
-        }
-        {
-            Prof prof(c, "merge_refresh_shadows");
-            refresh_shadows_all(c);
         }
         ck(cudaStreamSynchronize(c->stream), "sync");
         if (n_events) *n_events = L.L;
@@ -2422,7 +2491,8 @@ spes_status spes_debug_read(spes_ctx* c, const char* name, int32_t layer, void* 
         ck(cudaSetDevice(c->device), "cudaSetDevice");
         const Layout& L = c->lay;
         const std::string n(name);
-        if (c->T == 0) throw std::logic_error("debug_read: no step has run");
+        if (c->T == 0 && n != "w1" && n != "w2")
+            throw std::logic_error("debug_read: no step has run");
         const int64_t T = c->T, d = L.d, M = L.M, k = L.k;
         const void* src = nullptr;
         int64_t sz = 0;

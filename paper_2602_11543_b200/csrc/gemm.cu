@@ -198,6 +198,65 @@ struct EpiDSwiGLUStaged {
     }
 };
 
+// dSwiGLU with the factor pieces staged by TMA and the products written back IN PLACE:
+// 32-column pieces (2 x 128 rows x 64 B, 64B-swizzled) in NB ring buffers; each thread
+// overwrites its factor row with its dG (half 0) / dU (half 1) row and the warp's lane 0
+// stores its 32 x 32 box by TMA. No epilogue transpose slots, so NB = 3 buffers (48 KB)
+// still leave 5 operand stages; a buffer is released once its store has read it (one piece
+// later, so the wait never stalls the piece in hand).
+template <int NB>
+struct EpiDSwiGLUInPlace {
+    static constexpr int SLOTS = 0;
+    static constexpr int PIECES = 8;  // 256 columns / 32
+    static constexpr int STAGE_BUFS = NB;
+    static constexpr int STAGED_BYTES = NB * 2 * 8192;
+    const CUtensorMap* fmap;  // GU [rows x 2f], {32 x 128} boxes, 64B swizzle
+    const CUtensorMap* omap;  // dGU [rows x 2f], {32 x 32} boxes, 64B swizzle
+    __device__ void prefetch(const GemmGroup&, int, int, int, int) const {}
+    __device__ void stage_load(const GemmGroup& g, int mt, int nt, int pc, uint8_t* dst,
+                               uint64_t* bar) const {
+        const int row = static_cast<int>(g.out_row0) + mt * GEMM_BM;
+        const int64_t x0 = static_cast<int64_t>(nt) * 256 + pc * 32;
+        tma_load_2d(fmap, bar, dst, static_cast<int32_t>(il_gate(x0)), row);
+        tma_load_2d(fmap, bar, dst + 8192, static_cast<int32_t>(il_up(x0)), row);
+    }
+    __device__ void operator()(const GemmGroup& g, int mt, int nt, int r, uint32_t taddr,
+                               bool empty, int half, EpiOut&, StageCtx& sc) const {
+        const int lane = r & 31, q = r >> 5;
+        const int orow = static_cast<int>(g.out_row0) + mt * GEMM_BM + q * 32;
+        const int sw = (r >> 1) & 3;  // 64B swizzle: 16-byte chunk c sits at c ^ ((r/2)%4)
+#pragma unroll 1
+        for (int pc = 0; pc < PIECES; ++pc) {
+            const int b = sc.cnt % NB;
+            mbar_wait(&sc.full[b], (sc.cnt / NB) & 1);
+            ++sc.cnt;
+            uint8_t* piece = sc.base + b * 16384 + half * 8192;
+            uint8_t* frow = piece + r * 64;
+            float dh[32], fa[32];
+            uint4 fr[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) fr[j] = *reinterpret_cast<const uint4*>(frow + ((j ^ sw) << 4));
+            unpack_bf16x32(fr, fa);
+            acc_load32(taddr + pc * 32, empty, dh);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) dh[i] = dh[i] * fa[i];
+            pack_bf16x32(dh, fr);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) *reinterpret_cast<uint4*>(frow + ((j ^ sw) << 4)) = fr[j];
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                const int64_t x0 = static_cast<int64_t>(nt) * 256 + pc * 32;
+                tma_store_2d(omap, piece + q * 2048,
+                             static_cast<int32_t>(half ? il_up(x0) : il_gate(x0)), orow);
+                bulk_commit();
+                bulk_wait_read<1>();  // the previous piece's store has read its buffer
+                if (sc.cnt >= 2) mbar_arrive(&sc.empty[(sc.cnt - 2) % NB]);
+            }
+        }
+    }
+};
+
 struct EpiGradW1 {
     static constexpr int SLOTS = 1;
     __device__ void prefetch(const GemmGroup&, int, int, int, int) const {}
@@ -652,13 +711,22 @@ void gemm_head_ce(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g
                              EpiHeadCE{targets, T, g_s2, g_ssum, dlog, diff, lse}, s);
 }
 
-int g_dswiglu_bufs = 1;
-void gemm_dswiglu_buffers(int n) { g_dswiglu_bufs = n == 2 ? 2 : 1; }
+// 1 / 2: 64-column pieces through the transpose slots with 1 / 2 staging buffers;
+// 3 / 4: 32-column pieces written back in place, 2 / 3 buffers
+int g_dswiglu_bufs = 4;
+void gemm_dswiglu_buffers(int n) { g_dswiglu_bufs = n >= 1 && n <= 4 ? n : 4; }
 
 void gemm_dswiglu(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
                   const int32_t* tiles, int max_tiles, const bf16* gu, int64_t f,
-                  const CUtensorMap* gu_map, cudaStream_t s) {
-    if (bn == 256 && g_gemm_pairs && gu_map) {  // factor rows staged by TMA
+                  const CUtensorMap* gu_map, const CUtensorMap* inplace_maps, cudaStream_t s) {
+    if (bn == 256 && g_gemm_pairs && inplace_maps && g_dswiglu_bufs >= 3) {
+        if (g_dswiglu_bufs == 3)
+            launch<256, false, false>(a, b, g, ng, tiles, max_tiles,
+                                      EpiDSwiGLUInPlace<2>{inplace_maps, inplace_maps + 1}, s);
+        else
+            launch<256, false, false>(a, b, g, ng, tiles, max_tiles,
+                                      EpiDSwiGLUInPlace<3>{inplace_maps, inplace_maps + 1}, s);
+    } else if (bn == 256 && g_gemm_pairs && gu_map) {  // factor rows staged by TMA
         if (g_dswiglu_bufs == 2)
             launch<256, false, false>(a, b, g, ng, tiles, max_tiles, EpiDSwiGLUStaged<2>{gu_map}, s);
         else

@@ -53,8 +53,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int* s_nkb = s_ts + GEMM_MAX_GROUPS;
     uint8_t* s_epi = reinterpret_cast<uint8_t*>(bars) + 256 + GEMM_TABLE_BYTES;
     // staged epilogue input: two buffers after the 1024-aligned end of the staging slots
-    uint64_t* sfull = tempty + 2 + 1;   // past tmem_slot's 8 bytes
-    uint64_t* sempty = sfull + 2;
+    uint64_t* sfull = tempty + 2 + 1;   // past tmem_slot's 8 bytes; up to 4 buffers
+    uint64_t* sempty = sfull + 4;
     uint8_t* s_stage = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(s_epi + epi_stage_bytes(Epi::SLOTS)) + 1023) &
         ~static_cast<uintptr_t>(1023));
@@ -78,11 +78,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 16);  // 8 epilogue warps x 2 CTAs (leader's copy used)
         }
-        if constexpr (STAGED > 0)
-            for (int b = 0; b < 2; ++b) {
+        if constexpr (STAGED > 0) {
+            static_assert(Epi::STAGE_BUFS <= 4, "staging barriers: up to 4 buffers");
+            for (int b = 0; b < Epi::STAGE_BUFS; ++b) {
                 mbar_init(&sfull[b], 1);   // this CTA's warp 3 (expect_tx)
                 mbar_init(&sempty[b], EpiStageArrivals<Epi>::count);  // epilogue releases
             }
+        }
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc_pair(tmem_slot, C::TMEM_COLS);

@@ -1870,13 +1870,38 @@ void gram_finish(const double* partial, int M, int nchunks, double* sim, cudaStr
 // from the same pre-merge snapshot, in fp64. Each thread snapshots element i of every expert
 // into its own smem column (peers are data-dependent indices), converted to double once:
 // 2 elements per thread for M <= 16 (double2 columns), else 1.
+// VEC (1 or 2) consecutive parameters at offset o (even for VEC = 2) of expert slot `slot`
+// -> its bf16 operand copy (a pair never straddles a 128-column block of W1)
+template <int VEC>
+__device__ __forceinline__ void write_shadow_n(int slot, int64_t o, const float* v,
+                                               const Shadows& sh) {
+    const uint32_t df = static_cast<uint32_t>(sh.d * sh.f), f = static_cast<uint32_t>(sh.f);
+    const uint32_t o32 = static_cast<uint32_t>(o);
+    bf16* dst;
+    if (o32 < 2 * df) {
+        const bool up = o32 >= df;
+        const uint32_t oo = up ? o32 - df : o32;
+        const uint32_t q = (f & (f - 1)) == 0 ? oo >> (__ffs(f) - 1) : oo / f;
+        const uint32_t x = oo - q * f;
+        dst = sh.w1 + static_cast<int64_t>(slot) * 2 * df + static_cast<int64_t>(q) * 2 * f +
+              (up ? il_up(x) : il_gate(x));
+    } else {
+        dst = sh.w2 + static_cast<int64_t>(slot) * df + (o32 - 2 * df);
+    }
+    if (VEC == 2)
+        *reinterpret_cast<__nv_bfloat162*>(dst) = __floats2bfloat162_rn(v[0], v[1]);
+    else
+        *dst = __float2bfloat16_rn(v[0]);
+}
+
 template <int VEC>
 __global__ void __launch_bounds__(256) merge_apply_k(float* __restrict__ params,
                                                      const int64_t* __restrict__ expert_offs,
                                                      int M, int64_t per,
                                                      const int32_t* __restrict__ peers, int K,
                                                      const double* __restrict__ coef,
-                                                     double* __restrict__ disp_partial) {
+                                                     double* __restrict__ disp_partial, Shadows sh,
+                                                     int slot0) {
     using F = typename std::conditional<VEC == 2, float2, float>::type;
     __shared__ int32_t sp[64 * 64];
     __shared__ double sc[64];
@@ -1922,6 +1947,7 @@ __global__ void __launch_bounds__(256) merge_apply_k(float* __restrict__ params,
                 outv[c] = __double2float_rn(__dadd_rn(self, delta));
             }
             *reinterpret_cast<F*>(params + so[j] + i * VEC) = *reinterpret_cast<const F*>(outv);
+            if (slot0 >= 0) write_shadow_n<VEC>(slot0 + j, i * VEC, outv, sh);
         }
     }
     red[tid] = disp;
@@ -1940,7 +1966,8 @@ __global__ void __launch_bounds__(256) merge_apply_small_k(float* __restrict__ p
                                                            int M, int64_t per,
                                                            const int32_t* __restrict__ peers, int K,
                                                            const double* __restrict__ coef,
-                                                           double* __restrict__ disp_partial) {
+                                                           double* __restrict__ disp_partial,
+                                                           Shadows sh, int slot0) {
     __shared__ int32_t spo[16 * 8];  // peer column offset (peer * 256)
     __shared__ double sc[16];
     __shared__ int64_t so[16];
@@ -1979,9 +2006,10 @@ __global__ void __launch_bounds__(256) merge_apply_small_k(float* __restrict__ p
             const double dx = __dmul_rn(sc[j], ax), dy = __dmul_rn(sc[j], ay);
             disp += dx * dx;
             disp += dy * dy;
-            *reinterpret_cast<float2*>(params + so[j] + 2 * i) =
-                make_float2(__double2float_rn(__dadd_rn(self.x, dx)),
-                            __double2float_rn(__dadd_rn(self.y, dy)));
+            const float outv[2] = {__double2float_rn(__dadd_rn(self.x, dx)),
+                                   __double2float_rn(__dadd_rn(self.y, dy))};
+            *reinterpret_cast<float2*>(params + so[j] + 2 * i) = make_float2(outv[0], outv[1]);
+            if (slot0 >= 0) write_shadow_n<2>(slot0 + j, 2 * i, outv, sh);
         }
     }
     red[tid] = disp;
@@ -1995,22 +2023,24 @@ __global__ void __launch_bounds__(256) merge_apply_small_k(float* __restrict__ p
 
 void merge_apply(float* params, const int64_t* expert_offs, int M, int64_t per,
                  const int32_t* peers, int K, const double* coef, double* disp_partial,
-                 int nblocks, cudaStream_t s) {
+                 int nblocks, cudaStream_t s, const Shadows* sh, int slot0) {
+    const Shadows shv = sh ? *sh : Shadows{};
+    if (!sh) slot0 = -1;
     if (M <= 16 && K <= 8 && per % 2 == 0) {
         const size_t smem = sizeof(double2) * M * 256;
         cudaFuncSetAttribute(merge_apply_small_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         merge_apply_small_k<<<nblocks, 256, smem, s>>>(params, expert_offs, M, per, peers, K, coef,
-                                                       disp_partial);
+                                                       disp_partial, shv, slot0);
     } else if (M <= 16 && per % 2 == 0) {
         const size_t smem = sizeof(double) * 2 * M * 256;
         cudaFuncSetAttribute(merge_apply_k<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         merge_apply_k<2><<<nblocks, 256, smem, s>>>(params, expert_offs, M, per, peers, K, coef,
-                                                     disp_partial);
+                                                     disp_partial, shv, slot0);
     } else {
         const size_t smem = sizeof(double) * M * 256;
         cudaFuncSetAttribute(merge_apply_k<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         merge_apply_k<1><<<nblocks, 256, smem, s>>>(params, expert_offs, M, per, peers, K, coef,
-                                                     disp_partial);
+                                                     disp_partial, shv, slot0);
     }
     count_launch();
 }

@@ -205,6 +205,12 @@ void refresh_shadows(const float* params, const SegTable& tab, int64_t total, Sh
 // batch tokens B x (S+1) from the HBM-resident corpus rows
 void corpus_gather(const int32_t* corpus, const int64_t* rows, int64_t B, int64_t S1,
                    int32_t* tokens, cudaStream_t s);
+// device corpus generation (corpus_dev.cu): n uniform doubles from the std::mt19937_64
+// state (312 words, next position pos), then one Markov chain per sequence over the
+// sources' prefix-sum tables cum [C][V+1][V]
+void corpus_draws(const uint64_t* state, int pos, int64_t n, double* out, cudaStream_t s);
+void corpus_chains(const double* cum, const double* u, int64_t sequences, int64_t seq, int V,
+                   int C, int32_t* tokens, cudaStream_t s);
 
 // ---- sync / merge ----
 // DiLoCo outer step over this rank's slice (theta, n scalars): recv = the N nodes' local
@@ -219,7 +225,7 @@ void gram_partials(const float* params, const int64_t* vec_offs, int M, int64_t 
 void gram_finish(const double* partial, int M, int nchunks, double* sim, cudaStream_t s);
 void merge_apply(float* params, const int64_t* expert_offs, int M, int64_t per,
                  const int32_t* peers, int K, const double* coef, double* disp_partial,
-                 int nblocks, cudaStream_t s);
+                 int nblocks, cudaStream_t s, const Shadows* sh = nullptr, int slot0 = -1);
 
 // ---- GEMMs (gemm.cu) ----
 void gemm_swiglu(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
@@ -230,13 +236,16 @@ enum class GemmMajor { KK, KMN, MNMN };
 void gemm_store_f32(int bn, GemmMajor mj, const CUtensorMap& a, const CUtensorMap& b,
                     const GemmGroup* g, int ng, const int32_t* tiles, int max_tiles,
                     cudaStream_t s);
-// staging buffers of the TMA-staged dSwiGLU epilogue (1 or 2; experiments)
+// variant of the TMA-staged dSwiGLU epilogue: 1 / 2 = 64-column pieces with 1 / 2 staging
+// buffers, 3 / 4 = 32-column pieces written back in place with 2 / 3 buffers (default 4)
 void gemm_dswiglu_buffers(int n);
 // gu_map (optional, device memory): the GU buffer as {64 x 128}-box tensor map; with it the
-// pair kernel stages the factor rows by TMA (EpiDSwiGLUStaged)
+// pair kernel stages the factor rows by TMA (EpiDSwiGLUStaged). inplace_maps (optional,
+// device memory, two maps): GU as {32 x 128} and dGU as {32 x 32} boxes, 64B swizzle
+// (EpiDSwiGLUInPlace, preferred when given)
 void gemm_dswiglu(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
                   const int32_t* tiles, int max_tiles, const bf16* gu, int64_t f,
-                  const CUtensorMap* gu_map, cudaStream_t s);
+                  const CUtensorMap* gu_map, const CUtensorMap* inplace_maps, cudaStream_t s);
 // head forward (V == 256) with softmax-CE fused into the epilogue: writes bf16 dlogits
 // ([T_pad x 256], padding rows zero), the per-token CE term and lse (head_ce semantics)
 void gemm_head_ce(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,

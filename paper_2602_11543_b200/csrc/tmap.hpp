@@ -45,6 +45,26 @@ inline CUtensorMap make_tmap_bf16(const void* base, uint64_t rows, uint64_t cols
     return m;
 }
 
+// Row-major [rows x cols] bf16 matrix as {32 x box_rows} tiles with the 64-byte swizzle
+// (16-byte chunk c of row r at c ^ ((r / 2) % 4)): the dSwiGLU epilogue's factor pieces
+// and its in-place product stores.
+inline CUtensorMap make_tmap_bf16_sw64(const void* base, uint64_t rows, uint64_t cols,
+                                       uint32_t box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 2};
+    cuuint32_t box[2] = {32, box_rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = tmap_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
+                                dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw std::runtime_error("cuTensorMapEncodeTiled (bf16, 64B swizzle) failed (" +
+                                 std::to_string(r) + ")");
+    return m;
+}
+
 // Row-major [rows x cols] fp32 matrix as {box_cols x box_rows} tiles, 128B swizzle
 // (box_cols * 4 <= 128).
 inline CUtensorMap make_tmap_f32(const void* base, uint64_t rows, uint64_t cols, uint32_t box_cols,

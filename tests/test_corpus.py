@@ -94,3 +94,37 @@ def test_device_corpus_round_equals_host_tokens():
     finally:
         a.close()
         b.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("vocab,seq,sources,sequences,skew", [
+    (256, 64, 4, 96, 0.0),     # the CORPUS shape above
+    (200, 33, 3, 50, 1.5),     # vocabulary below the model's, skewed bands, ragged sizes
+    (256, 1023, 1, 300, 0.0),  # one source, 307k draws (about a thousand engine refills)
+])
+def test_device_corpus_generation_bitexact(vocab, seq, sources, sequences, skew):
+    """spes_corpus_generate (corpus_dev.cu): the engine replayed and the chains sampled on
+    the device equal the host transcription and the reference's own gen_corpus."""
+    cfg = model_cfg(vocab=256, hidden=128, intermediate=256, layers=2, experts_total=8,
+                    experts_active=2)
+    node = spes.Node(cfg, 0, 1, 0)
+    try:
+        tok, sid = node.corpus_generate(vocab, seq, sources, sequences, 23, skew)
+        ht, hs = spes.gen_corpus(vocab, seq, sources, sequences, 23, skew)
+        assert np.array_equal(tok, ht) and np.array_equal(sid, hs)
+        if oracle.ref_available():
+            rt = np.zeros_like(tok)
+            rs = np.zeros_like(sid)
+            assert oracle.ref().ref_gen_corpus(vocab, seq, sources, sequences, 23, skew, rt,
+                                               rs) == 0
+            assert np.array_equal(tok, rt)
+        # the generated corpus is the node's HBM corpus: steps over its rows run
+        node.set_ownership([[0, 1, 2, 3]])
+        node.load_params(oracle.random_params(cfg, 5))
+        la = node.local_round_rows(np.array([[0, sequences - 1]]), adamw_cfg())
+        assert np.isfinite(la).all()
+        with pytest.raises(spes.SpesError) as e:
+            node.corpus_generate(cfg.vocab + 1, 8, 1, 2, 1)
+        assert e.value.kind == "invalid_argument"
+    finally:
+        node.close()

@@ -14,7 +14,7 @@ import oracle
 import paper_2602_11543_b200 as spes
 from paper_2602_11543_b200.abi import adamw_cfg, merge_sched, model_cfg
 from test_gpu_parity import (CFG2, CFG4, GRAD_RTOL, LOSS_RTOL, _check_deep_routing,
-                             _check_grad_blocks, bitexact)
+                             _check_grad_blocks, _check_operand_copies, bitexact)
 
 pytestmark = pytest.mark.gpu
 
@@ -128,6 +128,7 @@ def test_merge_bitexact_large(gpu, shape, peers, source):
     p_ref, ev_ref, peers_ref = oracle.merge_model(cfg, params, sched, 1)
     assert (peers_gpu == peers_ref).all()
     assert bitexact(node.read_params(), p_ref)
+    _check_operand_copies(node, cfg)
     for a, b in zip(ev_gpu, ev_ref):
         assert a[:3] == b[:3]
         assert abs(a[3] - b[3]) <= 1e-9 * abs(b[3])

@@ -404,6 +404,17 @@ def test_stream_overlap_identical_bits(gpu, shape, owned, B, S):
 
 # ---------------------------------------------------------------- merge warm-up
 
+def _check_operand_copies(node, cfg):
+    """The bf16 GEMM operand copies the merge wrote equal a fresh refresh from fp32."""
+    d, f, M = cfg.hidden, cfg.intermediate, cfg.experts_total
+    def copies():
+        return [node.debug(w, l, np.uint16, None, M * n)
+                for l in range(cfg.layers) for w, n in (("w1", 2 * d * f), ("w2", d * f))]
+    merged = copies()
+    node.load_params(node.read_params())  # rewrites every copy from the fp32 parameters
+    assert all(np.array_equal(a, b) for a, b in zip(merged, copies())), "operand copies"
+
+
 def test_merge_bitexact_vs_oracle(gpu):
     cfg = model_cfg(**CFG1)
     params = oracle.random_params(cfg, 13, std=0.05)
@@ -417,6 +428,7 @@ def test_merge_bitexact_vs_oracle(gpu):
     p_ref, ev_ref, peers_ref = oracle.merge_model(cfg, params, sched, 0)
     assert (peers_gpu == peers_ref).all()
     assert bitexact(node.read_params(), p_ref)
+    _check_operand_copies(node, cfg)
     for a, b in zip(ev_gpu, ev_ref):
         assert a[0] == b[0] and a[1] == b[1] and a[2] == b[2]
         assert abs(a[3] - b[3]) <= 1e-9 * abs(b[3])
