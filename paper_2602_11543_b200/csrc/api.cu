@@ -170,6 +170,8 @@ struct LayerBufs {
     int32_t *topk_idx, *chunk_counts, *counts, *pad_off, *slot_row, *row_token, *tiles;
     GemmGroup* groups;
     bf16 *xp, *gu, *hact;  // routed rows (expert-major dispatch), GEMM outputs
+    bf16* normed_bf;       // router-normalized h (dispatch source; router-gradient operand)
+    CUtensorMap a_normed_mn;  // normed_bf [tokens x d] as the MN-major A of g_router
     int64_t* grad_off;  // device [M]
     CUtensorMap a_xp, a_hact, a_xp_mn, a_hact_mn;  // *_mn: [tokens x features] as MN-major
     CUtensorMap b_w1_mn, b_w2_mn, b_w2, b_w1;  // *_mn: row-major weights as MN-major B
@@ -282,7 +284,16 @@ struct spes_ctx {
     float *dot_part = nullptr;
     double* loss_part = nullptr;
     int32_t* eg_scratch = nullptr;  // embedding-gradient bucketing (2V + 1 + T)
-    bf16* normed_bf = nullptr;  // router-normalized h of the current layer (dispatch source)
+    // router weight gradient on the tensor cores (g_router = normed^T glog, MN-major pair
+    // GEMM over the tokens, split K, then summed in split order into the gradient); set
+    // at creation (M > 16)
+    bool router_tc = false;
+    bf16* glog_bf = nullptr;  // [T_pad x 128] bf16 glog, experts zero-padded to 128 columns
+    CUtensorMap b_glog_mn;
+    float* rg_part = nullptr;  // [rg_split][d][128]
+    GemmGroup* rg_groups = nullptr;
+    int32_t* rg_tiles = nullptr;
+    int rg_split = 1, rg_max = 0;
     float *dxp = nullptr, *gw_part = nullptr, *glog = nullptr, *gnormed = nullptr, *gh = nullptr,
           *nr_partial = nullptr;
     bf16 *hL = nullptr, *dlog_bf = nullptr;
@@ -567,8 +578,12 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
         Y.gu = A.alloc<bf16>(R * 2 * f);
         Y.hact = A.alloc<bf16>(R * f);
         Y.y = A.alloc<float>(R * d);
+        Y.normed_bf = A.alloc<bf16>(Tp * d);
+        // padding rows stay zero (finite operands for the router-gradient GEMM)
+        ck(cudaMemsetAsync(Y.normed_bf, 0, sizeof(bf16) * Tp * d, c->stream), "normed_bf");
         Y.grad_off = c->grad_off_dev + static_cast<int64_t>(l) * M;
         using spes_host::make_tmap_bf16;
+        Y.a_normed_mn = make_tmap_bf16(Y.normed_bf, Tp, d, 64);
         Y.a_xp = make_tmap_bf16(Y.xp, R, d, 128);
         Y.a_hact = make_tmap_bf16(Y.hact, R, f, 128);
         Y.a_xp_mn = make_tmap_bf16(Y.xp, R, d, 64);
@@ -608,7 +623,36 @@ void ensure_activations(spes_ctx* c, int64_t B, int64_t S) {
     c->glog = A.alloc<float>(Tp * M);
     c->gnormed = A.alloc<float>(Tp * d);
     c->gh = A.alloc<float>(Tp * d);
-    c->normed_bf = A.alloc<bf16>(Tp * d);
+    c->glog_bf = A.alloc<bf16>(Tp * 128);
+    ck(cudaMemsetAsync(c->glog_bf, 0, sizeof(bf16) * Tp * 128, c->stream), "glog_bf");
+    c->b_glog_mn = spes_host::make_tmap_bf16(c->glog_bf, Tp, 128, 64);
+    {  // g_router: (d / tr) output tiles of 256 x 128, K (tokens) split to cover the SMs
+        const int64_t tiles = d / tr;
+        int64_t ns = std::max<int64_t>(1, (2 * 148 / bdiv + tiles - 1) / tiles);
+        while (ns > 1 && (Tp % (64 * ns) != 0 || Tp / ns < 512)) --ns;
+        c->rg_split = static_cast<int>(ns);
+        c->rg_part = A.alloc<float>(ns * d * 128);
+        c->rg_groups = A.alloc<GemmGroup>(ns);
+        c->rg_tiles = A.alloc<int32_t>(1);
+        std::vector<GemmGroup> rg(ns);
+        int32_t ts = 0;
+        for (int64_t sp = 0; sp < ns; ++sp) {
+            GemmGroup& g = rg[sp];
+            g.k0 = static_cast<int32_t>(sp * (Tp / ns));
+            g.bk0 = g.k0;
+            g.k_len = static_cast<int32_t>(Tp / ns);
+            g.m_tiles = static_cast<int32_t>(d / tr);
+            g.n_tiles = 1;
+            g.out0 = c->rg_part + sp * d * 128;
+            g.ldo = 128;
+            g.tile_start = ts;
+            ts += g.m_tiles;
+        }
+        c->rg_max = ts;
+        ck(cudaMemcpy(c->rg_groups, rg.data(), sizeof(GemmGroup) * ns, cudaMemcpyHostToDevice),
+           "router-gradient groups");
+        ck(cudaMemcpy(c->rg_tiles, &ts, sizeof(ts), cudaMemcpyHostToDevice), "router-gradient tiles");
+    }
     c->nr_partial = A.alloc<float>(spes_k::kNormRouterChunks * d * (M + 1));
     c->hL = A.alloc<bf16>(Tp * d);
     ck(cudaMemsetAsync(c->hL, 0, sizeof(bf16) * Tp * d, c->stream), "hL");  // padding rows
@@ -769,7 +813,7 @@ void forward_backward(spes_ctx* c) {
             spes_k::router_forward(hsrc(l), hmap(l), P + L.off_norm(l), P + L.off_router(l), T, d,
                                    c->ulay.d, M, k,
                                    c->cfg.renormalize_after_topk, c->cfg.rms_eps, c->expf_variant,
-                                   nullptr, c->normed_bf, Y.logits, Y.probs, Y.topk_idx,
+                                   nullptr, Y.normed_bf, Y.logits, Y.probs, Y.topk_idx,
                                    Y.topk_w, Y.lse_r, Y.inv_rms, Y.denom, st);
         }
         {
@@ -783,7 +827,7 @@ void forward_backward(spes_ctx* c) {
         }
         {
             PROF("permute");  // TMA-staged row scatter (dispatch)
-            spes_k::permute_rows_tma(c->normed_bf, d, Y.slot_row, Y.row_token, Y.pad_off + M, T, k,
+            spes_k::permute_rows_tma(Y.normed_bf, d, Y.slot_row, Y.row_token, Y.pad_off + M, T, k,
                                      Y.xp, st);
         }
         {
@@ -857,7 +901,7 @@ void forward_backward(spes_ctx* c) {
             spes_k::router_scalar_backward(Y.probs, Y.lse_r, Y.denom, Y.topk_idx, Y.slot_row,
                                            c->gw_part, Y.lb_coeff, T, M, k,
                                            c->cfg.renormalize_after_topk, sd.g_lbsum, sd.g_s,
-                                           c->glog, ss);
+                                           c->glog, c->router_tc ? c->glog_bf : nullptr, ss);
             ready(2);
         }
         const bool unfused_dw = c->max_tiles[4] > 0 && !fused(c);
@@ -932,9 +976,16 @@ void forward_backward(spes_ctx* c) {
         {
             PROF("norm_router_grads");  // + rmsnorm backward into gh
             spes_k::norm_router_grads(hsrc(l), hmap(l), P + L.off_norm(l), c->gnormed, c->glog,
-                                      Y.inv_rms, T, d, c->ulay.d, M,
+                                      Y.inv_rms, T, d, c->ulay.d, c->router_tc ? 0 : M,
                                       c->nr_partial, c->grads + L.off_norm(l),
                                       c->grads + L.off_router(l), c->dot_part, c->gh, st);
+        }
+        if (c->router_tc) {
+            PROF("router_grad_gemm");  // g_router = normed^T glog (bf16 operands, fp32 sums)
+            spes_k::gemm_store_f32(128, spes_k::GemmMajor::MNMN, Y.a_normed_mn, c->b_glog_mn,
+                                   c->rg_groups, c->rg_split, c->rg_tiles, c->rg_max, st);
+            spes_k::router_grad_reduce(c->rg_part, c->rg_split, d, M, c->grads + L.off_router(l),
+                                       st);
         }
     }
     {
@@ -1212,6 +1263,11 @@ spes_status spes_create(const spes_model_cfg* cfg, int32_t node, int32_t n_nodes
         if (const char* e = std::getenv("SPES_FUSED_OPT")) c->fused_opt = std::atoi(e) != 0;
         if (const char* e = std::getenv("SPES_EARLY_WD")) c->early_wd = std::atoi(e) != 0;
         if (const char* e = std::getenv("SPES_STEP_GRAPH")) c->use_graph = std::atoi(e) != 0;
+        // the CUDA-core kernel re-streams h once per 16 experts: above 16 the tensor-core
+        // GEMM wins (cfg5 norm+router gradients 182 -> 66 ms per round), at 16 it does not
+        // (cfg2 3.2 -> 4.1 ms)
+        c->router_tc = c->lay.M > 16;
+        if (const char* e = std::getenv("SPES_ROUTER_TC")) c->router_tc = std::atoi(e) != 0;
         if (const char* e = std::getenv("SPES_DSWIGLU_TMA")) {  // 0 off, else the variant (1-4)
             c->staged_dswiglu = std::atoi(e) != 0;
             if (c->staged_dswiglu) spes_k::gemm_dswiglu_buffers(std::atoi(e));

@@ -835,7 +835,7 @@ __global__ void __launch_bounds__(256) norm_router_partial_k(
     auto stage_batch = [&](int b) {  // glog / inv_rms / dot partials of batch b
         if (b >= nbatch) return;
         const int tb = t0 + 64 * b, buf = b & 1;
-        for (int i = threadIdx.x; i < 64 * NRG_EG; i += blockDim.x) {
+        for (int i = threadIdx.x; ne > 0 && i < 64 * NRG_EG; i += blockDim.x) {
             const int tt = i / NRG_EG, e = i % NRG_EG;
             if (tb + tt < t1 && e < ne)
                 cp_async4_nr(&sgl[buf][tt][e], glog + static_cast<int64_t>(tb + tt) * M + e0 + e);
@@ -908,6 +908,7 @@ __global__ void __launch_bounds__(256) norm_router_partial_k(
                 gg[2] += (gv.z * xv.z) * iv;
                 gg[3] += (gv.w * xv.w) * iv;
             }
+            if (ne <= 0) continue;  // gain / rmsnorm only (router gradient on the tensor cores)
             const float n[4] = {nv.x, nv.y, nv.z, nv.w};
 #pragma unroll
             for (int e4 = 0; e4 < NRG_EG; e4 += 4) {
@@ -975,7 +976,8 @@ void norm_router_grads(const float* h, const int32_t* hrow, const float* gain, c
                        float* gh, cudaStream_t s) {
     // 32 experts per block for M > 16: h streamed and normed rebuilt M/32 times, not M/16
     const int eg = (M > 16 && g_nrg_wide) ? 32 : 16;
-    dim3 grid(static_cast<unsigned>(d / 128), NRG_TC, static_cast<unsigned>((M + eg - 1) / eg));
+    dim3 grid(static_cast<unsigned>(d / 128), NRG_TC,
+              static_cast<unsigned>(M > 0 ? (M + eg - 1) / eg : 1));
     constexpr int ring_bytes = NRG_S * 3 * 256 * 16;
     static std::atomic<uint64_t> attr_set{0};
     if (first_use_on_device(attr_set)) {
@@ -2073,6 +2075,23 @@ __global__ void splitk_reduce_k(const float4* __restrict__ part, int nsplit, int
         }
         out[i] = a;
     }
+}
+
+__global__ void router_grad_reduce_k(const float* __restrict__ part, int nsplit, int64_t d, int M,
+                                     float* __restrict__ out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= d * M) return;
+    const int64_t q = i / M, e = i % M;
+    float a = 0.f;
+    for (int sp = 0; sp < nsplit; ++sp) a += __ldg(part + (sp * d + q) * 128 + e);
+    out[i] = a;
+}
+
+void router_grad_reduce(const float* part, int nsplit, int64_t d, int M, float* out,
+                        cudaStream_t s) {
+    router_grad_reduce_k<<<static_cast<unsigned>(cdiv(d * M, 256)), 256, 0, s>>>(part, nsplit, d,
+                                                                                M, out);
+    count_launch();
 }
 
 void splitk_reduce(const float* part, int nsplit, int64_t n, float* out, cudaStream_t s) {

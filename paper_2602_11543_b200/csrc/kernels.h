@@ -122,7 +122,8 @@ void combine_backward(const float* gh, const float* y, const int32_t* row_token,
 void router_scalar_backward(const float* probs, const float* lse_r, const float* denom,
                             const int32_t* topk_idx, const int32_t* slot_row, const float* gw_row,
                             const float* lb_coeff, int64_t T, int M, int k, int renorm,
-                            float g_lbsum, float g_s, float* glog, cudaStream_t s);
+                            float g_lbsum, float g_s, float* glog, bf16* glog_bf,
+                            cudaStream_t s);
 void normed_grad(const float* h, const int32_t* hrow, const float* gain, const float* router,
                  const int32_t* slot_row, const float* dxp, int64_t T, int64_t d, int M, int k,
                  const float* glog, float* gnormed, float* dot_part, cudaStream_t s);
@@ -131,6 +132,8 @@ void normed_grad(const float* h, const int32_t* hrow, const float* gain, const f
 constexpr int kNormRouterChunks = 37;
 // normed is recomputed exactly from h, inv_rms and the gain (not stored in forward)
 // gh non-null: also applies the rmsnorm backward (dot from normed_grad's dot_part)
+// M = 0: gain gradient and rmsnorm backward only (the router gradient runs on the tensor
+// cores, router_grad_reduce)
 void norm_router_grads(const float* h, const int32_t* hrow, const float* gain, const float* gnormed,
                        const float* glog, const float* inv_rms, int64_t T, int64_t d, int64_t dn,
                        int M,
@@ -288,6 +291,9 @@ int num_sms();
 
 // out[i] = sum over splits in order of part[s*n + i]   (deterministic split-K combine)
 void splitk_reduce(const float* part, int nsplit, int64_t n, float* out, cudaStream_t s);
+// g_router [d x M] = sum over splits (in order) of part [nsplit][d][128] (columns < M)
+void router_grad_reduce(const float* part, int nsplit, int64_t d, int M, float* out,
+                        cudaStream_t s);
 
 // expf port checks
 void expf_port_device(const float* x, float* y, int64_t n, int variant, cudaStream_t s);

@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(128) router_scalar_bwd_k(
     const float* __restrict__ denom, const int32_t* __restrict__ topk_idx,
     const int32_t* __restrict__ slot_row, const float* __restrict__ gw_row,
     const float* __restrict__ lb_coeff, int T, int M, int k, int renorm, float g_lbsum, float g_s,
-    float* __restrict__ glog) {
+    float* __restrict__ glog, bf16* __restrict__ glog_bf) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= T) return;
     float p[MAXM], gp[MAXM];
@@ -73,9 +73,18 @@ __global__ void __launch_bounds__(128) router_scalar_bwd_k(
     for (int e = 0; e < MAXM; ++e)
         if (e < M) dot = fadd(dot, fmul(gp[e], p[e]));
     float* grow = glog + static_cast<int64_t>(t) * M;
+    float gv[MAXM];
 #pragma unroll
-    for (int e = 0; e < MAXM; ++e)
-        if (e < M) grow[e] = fadd(fadd(0.f, fmul(gl, p[e])), fmul(p[e], fsub(gp[e], dot)));
+    for (int e = 0; e < MAXM; ++e) {
+        gv[e] = e < M ? fadd(fadd(0.f, fmul(gl, p[e])), fmul(p[e], fsub(gp[e], dot))) : 0.f;
+        if (e < M) grow[e] = gv[e];
+    }
+    if (glog_bf) {  // the router-gradient GEMM operand: [T_pad x 128], columns >= M stay zero
+        __nv_bfloat162* brow = reinterpret_cast<__nv_bfloat162*>(glog_bf + static_cast<int64_t>(t) * 128);
+#pragma unroll
+        for (int e = 0; e < MAXM; e += 2)
+            if (e < M) brow[e / 2] = __floats2bfloat162_rn(gv[e], e + 1 < M ? gv[e + 1] : 0.f);
+    }
 }
 
 constexpr int NG_TT = 32;   // tokens per tile
@@ -192,14 +201,15 @@ __global__ void __launch_bounds__(256) normed_grad_k(
 void router_scalar_backward(const float* probs, const float* lse_r, const float* denom,
                             const int32_t* topk_idx, const int32_t* slot_row, const float* gw_row,
                             const float* lb_coeff, int64_t T, int M, int k, int renorm,
-                            float g_lbsum, float g_s, float* glog, cudaStream_t s) {
+                            float g_lbsum, float g_s, float* glog, bf16* glog_bf,
+                            cudaStream_t s) {
     const unsigned g1 = static_cast<unsigned>((T + 127) / 128);
     auto f = M <= 8    ? router_scalar_bwd_k<8>
              : M <= 16 ? router_scalar_bwd_k<16>
              : M <= 32 ? router_scalar_bwd_k<32>
                        : router_scalar_bwd_k<64>;
     f<<<g1, 128, 0, s>>>(probs, lse_r, denom, topk_idx, slot_row, gw_row, lb_coeff, (int)T, M, k,
-                         renorm, g_lbsum, g_s, glog);
+                         renorm, g_lbsum, g_s, glog, glog_bf);
     count_launch();
 }
 

@@ -1,11 +1,10 @@
-O=gpurun_out/m11
+O=gpurun_out/m14
 mkdir -p $O
-for v in 1 2 3; do
-SPES_RF_SHAPE=$v timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_large.py -m gpu -q -p no:cacheprovider -x -k "rout or local_step_cfg1 or cfg5" 2>&1 | tail -2 > $O/pytest_v$v.txt
-echo "shape $v: $(tail -1 $O/pytest_v$v.txt)"
-for c in cfg5 cfg2; do
-SPES_RF_SHAPE=$v timeout 600 python bench.py --config $c --steps 3 --warmup 3 --e2e-steps 0 --no-cpu-baseline > $O/bench_${c}_v$v.json 2> $O/bench_${c}_v$v.err
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -s -p no:cacheprovider -k "router_gradient_paths" 2>&1 | grep -E "GRADERR|passed|failed|Error|^E " | tail -20 > $O/pytest.txt
+cat $O/pytest.txt
+for c in cfg4; do for tc in 0 1; do
+SPES_ROUTER_TC=$tc timeout 600 python bench.py --config $c --steps 5 --warmup 3 --e2e-steps 0 --no-cpu-baseline > $O/bench_${c}_tc$tc.json 2> $O/bench_${c}_tc$tc.err
 python -c "
-import json;d=json.load(open('$O/bench_${c}_v$v.json'));print('$c v$v',d['value'],d['ms_per_step'])"
-grep -E "router_fwd" $O/bench_${c}_v$v.err
+import json;d=json.load(open('$O/bench_${c}_tc$tc.json'));print('$c tc$tc',d['value'],d['ms_per_step'])"
+grep -E "norm_router|router_grad" $O/bench_${c}_tc$tc.err
 done; done

@@ -8,6 +8,7 @@ Bar (SURVEY.md §8c / north_star):
   * routing of layers > 0 depends on bf16 expert outputs: reported as an
     agreement rate, every disagreement must be a near-tie under the oracle.
 """
+import ctypes as C
 import os
 
 import numpy as np
@@ -343,6 +344,36 @@ def test_local_step_unaligned_shapes_renorm(gpu):
 def test_local_step_ragged_T(gpu):
     # T not a multiple of 128, an owned expert that may receive no tokens
     _check_step(model_cfg(**CFG1), B=3, S=37, owned=[0, 7], seed=40)
+
+
+@pytest.mark.parametrize("shape", ["cfg1", "cfg4"])
+def test_router_gradient_paths(gpu, monkeypatch, shape):
+    """Both router-gradient paths (SPES_ROUTER_TC: the tensor-core normed^T glog GEMM, the
+    default above 16 experts, and the CUDA-core partial kernel) against the oracle; the
+    gain gradient and the rest of the step do not depend on the path (identical bits)."""
+    cfg = model_cfg(**(CFG1 if shape == "cfg1" else CFG4))
+    B, S, owned = (4, 64, [0, 1, 2, 3]) if shape == "cfg1" else (1, 256, list(range(16)))
+    params = oracle.random_params(cfg, 57)
+    tokens = oracle.random_tokens(cfg, B, S, 58)[0]
+    grads = {}
+    for tc in ("0", "1"):
+        monkeypatch.setenv("SPES_ROUTER_TC", tc)
+        node = spes.Node(cfg, 0, 1, 0)
+        node.set_ownership([owned])
+        node.load_params(params)
+        node.set_fused_optimizer(False)
+        node.round_begin()
+        node.local_step(tokens, adamw_cfg(lr=1e-3))
+        grads[tc] = node.read_grads()
+        node.close()
+    _, g_ref, _ = oracle.forward_backward(cfg, params, tokens, owned, trace=True)
+    for tc, g in grads.items():
+        _check_grad_blocks(cfg, g, g_ref, f"{shape} router_tc={tc}")
+    keep = np.ones(grads["0"].size, bool)
+    for l in range(cfg.layers):  # router block of layer l: d x M after its norm gain
+        r0 = oracle.lib().oracle_off_router(C.byref(cfg), l)
+        keep[r0:r0 + cfg.hidden * cfg.experts_total] = False
+    assert bitexact(grads["0"][keep], grads["1"][keep]), "non-router gradients differ by path"
 
 
 def test_local_round_and_errors(gpu):
