@@ -347,7 +347,19 @@ struct spes_ctx {
 
 namespace {
 
-void set_counter(spes_ctx* c) { spes_k::g_launch_counter = &c->launches; }
+// Kernel launches are counted into the calling context for the duration of one API call.
+// The thread-local pointer is restored when the call returns, so it never outlives the
+// call: a destroyed context must not be written through by a later kernel-level call (that
+// dangling increment once corrupted unrelated host memory between tests).
+struct CounterScope {
+    int64_t* prev;
+    explicit CounterScope(spes_ctx* c) : prev(spes_k::g_launch_counter) {
+        spes_k::g_launch_counter = &c->launches;
+    }
+    ~CounterScope() { spes_k::g_launch_counter = prev; }
+    CounterScope(const CounterScope&) = delete;
+    CounterScope& operator=(const CounterScope&) = delete;
+};
 
 void drop_graph(spes_ctx* c) {
     if (c->step_graph) cudaGraphExecDestroy(c->step_graph);
@@ -1249,7 +1261,7 @@ spes_status spes_create(const spes_model_cfg* cfg, int32_t node, int32_t n_nodes
         c->n_nodes = n_nodes;
         c->device = cuda_device;
         ck(cudaSetDevice(cuda_device), "cudaSetDevice");
-        set_counter(c.get());
+        CounterScope counter_scope(c.get());
         int prio_lo = 0, prio_hi = 0;
         ck(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi), "priorities");
         ck(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi), "stream");
@@ -1359,7 +1371,7 @@ void spes_destroy(spes_ctx* c) {
 spes_status spes_set_ownership(spes_ctx* c, const int32_t* node_offsets, const int32_t* experts) {
     return guard([&] {
         ck(cudaSetDevice(c->device), "cudaSetDevice");
-        set_counter(c);
+        CounterScope counter_scope(c);
         std::vector<std::vector<int>> ne(c->n_nodes);
         for (int n = 0; n < c->n_nodes; ++n) {
             for (int q = node_offsets[n]; q < node_offsets[n + 1]; ++q) {
@@ -1384,7 +1396,7 @@ spes_status spes_set_ownership(spes_ctx* c, const int32_t* node_offsets, const i
 // the caller's parameter vector (enumerate_blocks layout, host) -> the device model
 void upload_user_params(spes_ctx* c, const float* host) {
     ck(cudaSetDevice(c->device), "cudaSetDevice");
-    set_counter(c);
+    CounterScope counter_scope(c);
     if (!c->padded) {
         ck(cudaMemcpyAsync(c->params, host, sizeof(float) * c->lay.total(), cudaMemcpyHostToDevice,
                            c->stream),
@@ -1542,7 +1554,7 @@ spes_status spes_load_params_device(spes_ctx* c, const float* dev, int64_t n) {
     return guard([&] {
         if (n != c->ulay.total()) throw std::invalid_argument("load_params: size mismatch");
         ck(cudaSetDevice(c->device), "cudaSetDevice");
-        set_counter(c);
+        CounterScope counter_scope(c);
         if (c->padded) {  // through the host conversion (padded layouts are small models)
             std::vector<float> h(static_cast<size_t>(n));
             ck(cudaMemcpy(h.data(), dev, sizeof(float) * n, cudaMemcpyDeviceToHost), "D2H params");
@@ -1580,7 +1592,7 @@ spes_status spes_local_step(spes_ctx* c, const int32_t* tokens, int64_t B, int64
                             const spes_adamw_cfg* opt, spes_losses* losses) {
     return guard([&] {
         ck(cudaSetDevice(c->device), "cudaSetDevice");
-        set_counter(c);
+        CounterScope counter_scope(c);
         if (B < 1 || S < 1) throw std::invalid_argument("batch: need B, S >= 1");
         validate_tokens(c, tokens, B * (S + 1));
         ensure_activations(c, B, S);
@@ -1593,7 +1605,7 @@ spes_status spes_local_step_device(spes_ctx* c, const int32_t* d_tokens, int64_t
                                    const spes_adamw_cfg* opt, spes_losses* losses) {
     return guard([&] {
         ck(cudaSetDevice(c->device), "cudaSetDevice");
-        set_counter(c);
+        CounterScope counter_scope(c);
         if (B < 1 || S < 1) throw std::invalid_argument("batch: need B, S >= 1");
         ensure_activations(c, B, S);
         ck(cudaMemcpyAsync(c->tokens, d_tokens, sizeof(int32_t) * B * (S + 1),
@@ -1608,7 +1620,7 @@ spes_status spes_local_round(spes_ctx* c, const int32_t* tokens, int64_t B, int6
                              spes_losses* per_step) {
     return guard([&] {
         ck(cudaSetDevice(c->device), "cudaSetDevice");
-        set_counter(c);
+        CounterScope counter_scope(c);
         if (H < 1) throw std::invalid_argument("local_round: need H >= 1");
         if (B < 1 || S < 1) throw std::invalid_argument("batch: need B, S >= 1");
         const int64_t per = B * (S + 1);
@@ -1846,7 +1858,7 @@ spes_status spes_local_step_rows(spes_ctx* c, const int64_t* rows, int64_t B,
                                  const spes_adamw_cfg* opt, spes_losses* losses) {
     return guard([&] {
         ck(cudaSetDevice(c->device), "cudaSetDevice");
-        set_counter(c);
+        CounterScope counter_scope(c);
         if (B < 1) throw std::invalid_argument("batch: need B >= 1");
         ensure_activations(c, B, c->corpus_seq);
         gather_corpus_rows(c, rows, B);
@@ -1859,7 +1871,7 @@ spes_status spes_local_round_rows(spes_ctx* c, const int64_t* rows, int64_t B, i
                                   spes_losses* per_step) {
     return guard([&] {
         ck(cudaSetDevice(c->device), "cudaSetDevice");
-        set_counter(c);
+        CounterScope counter_scope(c);
         if (H < 1) throw std::invalid_argument("local_round: need H >= 1");
         if (B < 1) throw std::invalid_argument("batch: need B >= 1");
         if (!carry_state) {
@@ -1918,7 +1930,7 @@ spes_status spes_outer_sync(spes_ctx* c, int32_t kind, double lr, double momentu
             throw std::logic_error("outer_sync: call spes_outer_begin on the round-start model first");
         if (kind != 0 && kind != 1) throw std::invalid_argument("outer_sync: kind is 0 (SGD) or 1 (Nesterov)");
         ck(cudaSetDevice(c->device), "cudaSetDevice");
-        set_counter(c);
+        CounterScope counter_scope(c);
         cudaStream_t st = c->stream;
         const int64_t P = c->lay.total(), sl = c->outer_slice;
         const int N = c->n_nodes, me = c->node;
@@ -2149,7 +2161,7 @@ static void build_sync_tasks(spes_ctx* c, const std::vector<int>& primary) {
 spes_status spes_sync(spes_ctx* c, spes_sync_stats* stats) {
     return guard([&] {
         ck(cudaSetDevice(c->device), "cudaSetDevice");
-        set_counter(c);
+        CounterScope counter_scope(c);
         const Layout& L = c->lay;
         const int N = c->n_nodes, me = c->node;
         cudaStream_t st = c->stream;
@@ -2394,7 +2406,7 @@ bool near_tie_at_boundary(const double* sim_row, int M, int j, int K) {
 spes_status spes_similarity(spes_ctx* c, int32_t layer, int32_t source, double* sim_out) {
     return guard([&] {
         ck(cudaSetDevice(c->device), "cudaSetDevice");
-        set_counter(c);
+        CounterScope counter_scope(c);
         if (c->lay.M < 2) throw std::invalid_argument("similarity_matrix: need M >= 2");
         if (layer < 0 || layer >= c->lay.L) throw std::out_of_range("similarity: bad layer");
         layer_sims(c, layer, source);
@@ -2407,7 +2419,7 @@ spes_status spes_merge(spes_ctx* c, const spes_merge_sched* sched, int32_t round
                        spes_merge_event* events, int32_t* peers_out, int32_t* n_events) {
     return guard([&] {
         ck(cudaSetDevice(c->device), "cudaSetDevice");
-        set_counter(c);
+        CounterScope counter_scope(c);
         if (n_events) *n_events = 0;
         if (!spes_merge_at(sched, round0)) return;
         double alpha = 0.0;

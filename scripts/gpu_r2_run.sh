@@ -1,10 +1,13 @@
-O=gpurun_out/m14
+O=gpurun_out/m18
 mkdir -p $O
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -s -p no:cacheprovider -k "router_gradient_paths" 2>&1 | grep -E "GRADERR|passed|failed|Error|^E " | tail -20 > $O/pytest.txt
-cat $O/pytest.txt
-for c in cfg4; do for tc in 0 1; do
-SPES_ROUTER_TC=$tc timeout 600 python bench.py --config $c --steps 5 --warmup 3 --e2e-steps 0 --no-cpu-baseline > $O/bench_${c}_tc$tc.json 2> $O/bench_${c}_tc$tc.err
-python -c "
-import json;d=json.load(open('$O/bench_${c}_tc$tc.json'));print('$c tc$tc',d['value'],d['ms_per_step'])"
-grep -E "norm_router|router_grad" $O/bench_${c}_tc$tc.err
-done; done
+run() {  # name env...
+  n=$1; shift
+  env "$@" timeout 600 python bench.py --steps 3 --warmup 3 --e2e-steps 0 --no-cpu-baseline --prof-rounds 0 > $O/bench_$n.json 2> $O/bench_$n.err
+  python -c "
+import json;d=json.load(open('$O/bench_$n.json'));print('$n',d['value'],d['ms_per_step'],d['clocks']['sm_mhz'])"
+}
+run carve1 SPES_SIDE_CARVEOUT=1
+run carve0 SPES_SIDE_CARVEOUT=0
+run nooverlap SPES_OPT_OVERLAP=0
+run carve1b SPES_SIDE_CARVEOUT=1
+run carve1_bg256 SPES_SIDE_CARVEOUT=1 SPES_ADAM_BG=256,8,0,2
