@@ -254,7 +254,10 @@ def gemm_rooflines(fam, cfg, counts, owned, T, peak, steps):
     R_own = float(sum(np.asarray(c)[list(owned)].sum() for c in counts))
     fl = {"gemm_fwd_gate_up": 4 * R * d * f, "gemm_fwd_down": 2 * R * d * f,
           "gemm_bwd_dh": 2 * R * d * f, "gemm_bwd_dx": 4 * R * d * f,
-          "gemm_bwd_dw_gate_up": 4 * R_own * d * f, "gemm_bwd_dw_down": 2 * R_own * d * f}
+          "gemm_bwd_dw_gate_up": 4 * R_own * d * f, "gemm_bwd_dw_down": 2 * R_own * d * f,
+          # router weight gradient normed^T glog (tensor cores above 16 experts): 2 T d M per
+          # layer of algorithmic work (the device pads M to 128 columns)
+          "router_grad_gemm": 2.0 * T * d * cfg.experts_total * cfg.layers}
     # the fused placement (SPES_FUSED_OPT=1) times the dW GEMMs with their MaskedAdamW
     for k_ in list(fl):
         if k_ + "+adamw" in fam:

@@ -91,8 +91,8 @@ constexpr int NG_TT = 32;   // tokens per tile
 constexpr int NG_QT = 128;  // columns per tile
 
 // grid (T/32, d/128), 256 threads: thread (ty, tx) -> tokens 4ty..4ty+3, columns 4tx..4tx+3
-template <int MAXM>
-__global__ void __launch_bounds__(256) normed_grad_k(
+template <int MAXM, bool ALLK>
+__global__ void __launch_bounds__(256, ALLK ? 4 : 1) normed_grad_k(
     const float* __restrict__ h, const int32_t* __restrict__ hrow, const float* __restrict__ gain,
     const float* __restrict__ R,
     const float* __restrict__ glog, const int32_t* __restrict__ slot_row,
@@ -175,13 +175,30 @@ __global__ void __launch_bounds__(256) normed_grad_k(
         // expert dX rows in descending expert order (select_rows backward, j descending)
         float a[4] = {0.f, 0.f, 0.f, 0.f};
         const float* dxc = dxp + q0 + 4 * tx;
+        if constexpr (ALLK) {  // all k row pieces in flight at once (k <= 8), summed descending
+            float4 v[8];
+#pragma unroll
+            for (int s = 0; s < 8; ++s)
+                if (s < k)
+                    v[s] = __ldg(reinterpret_cast<const float4*>(dxc + static_cast<int64_t>(sRow[tt][s]) * d));
+#pragma unroll
+            for (int s = 7; s >= 0; --s) {
+                if (s < k) {
+                    a[0] = fadd(a[0], v[s].x);
+                    a[1] = fadd(a[1], v[s].y);
+                    a[2] = fadd(a[2], v[s].z);
+                    a[3] = fadd(a[3], v[s].w);
+                }
+            }
+        } else {
 #pragma unroll 2
-        for (int s = k - 1; s >= 0; --s) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(dxc + static_cast<int64_t>(sRow[tt][s]) * d));
-            a[0] = fadd(a[0], v.x);
-            a[1] = fadd(a[1], v.y);
-            a[2] = fadd(a[2], v.z);
-            a[3] = fadd(a[3], v.w);
+            for (int s = k - 1; s >= 0; --s) {
+                const float4 v = __ldg(reinterpret_cast<const float4*>(dxc + static_cast<int64_t>(sRow[tt][s]) * d));
+                a[0] = fadd(a[0], v.x);
+                a[1] = fadd(a[1], v.y);
+                a[2] = fadd(a[2], v.z);
+                a[3] = fadd(a[3], v.w);
+            }
         }
         const int64_t xr_t = hrow ? static_cast<int64_t>(hrow[t]) : t;
         const float4 xv = __ldg(reinterpret_cast<const float4*>(h + xr_t * d + q0 + 4 * tx));
@@ -217,10 +234,18 @@ void normed_grad(const float* h, const int32_t* hrow, const float* gain, const f
                  const int32_t* slot_row, const float* dxp, int64_t T, int64_t d, int M, int k,
                  const float* glog, float* gnormed, float* dot_part, cudaStream_t s) {
     const dim3 g2(static_cast<unsigned>((T + NG_TT - 1) / NG_TT), static_cast<unsigned>(d / NG_QT));
-    auto f = M <= 8    ? normed_grad_k<8>
-             : M <= 16 ? normed_grad_k<16>
-             : M <= 32 ? normed_grad_k<32>
-                       : normed_grad_k<64>;
+    // all k expert pieces in flight (64 registers, 4 blocks per SM) for k > 4: cfg5 router
+    // backward 218 -> 210 ms per round; at k = 2 (cfg2) the 2-deep loop is faster (4.4 vs
+    // 4.7 ms). SPES_NG_ALLK=0/1 overrides.
+    static const int allk_env = [] {
+        const char* e = std::getenv("SPES_NG_ALLK");
+        return e ? std::atoi(e) : -1;
+    }();
+    const bool allk = allk_env >= 0 ? allk_env != 0 : k > 4;
+    auto f = M <= 8    ? (allk ? normed_grad_k<8, true> : normed_grad_k<8, false>)
+             : M <= 16 ? (allk ? normed_grad_k<16, true> : normed_grad_k<16, false>)
+             : M <= 32 ? (allk ? normed_grad_k<32, true> : normed_grad_k<32, false>)
+                       : (allk ? normed_grad_k<64, true> : normed_grad_k<64, false>);
     static const int pf = [] {
         const char* e = std::getenv("SPES_NG_PREFETCH");
         return e ? std::atoi(e) : 1;

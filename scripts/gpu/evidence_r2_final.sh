@@ -1,7 +1,7 @@
 # Round-2 evidence set on one B200: the GPU test suite, the driver's default bench (cfg5,
 # with cpu_baseline), the reference arm, the other configurations at N=1, and the ncu
 # launch lists of a cfg5 and a cfg2 step (per-launch time and DRAM bytes -> roofline.traffic)
-O=gpurun_out/ev4
+O=gpurun_out/ev5
 mkdir -p $O
 timeout 1500 python -m pytest tests -m gpu -q -s -p no:cacheprovider 2>&1 | grep -E "GRADERR|passed|failed|Error|error|^E |FAIL|PASS" | tail -60 > $O/pytest_gpu.txt
 timeout 900 python bench.py > $O/bench_default.json 2> $O/bench_default.err; echo default rc=$?
@@ -20,3 +20,9 @@ import json;d=json.load(open('$f'));print('$f',d.get('value'),d.get('ms_per_step
 tail -3 $O/pytest_gpu.txt
 # the smoke the driver runs
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1; tail -1 $O/smoke.txt
+# ncu --set full of the top kernel families of one cfg5 step (summarised on the box)
+C=cfg5
+CMD="python bench.py --config $C --steps 1 --warmup 2 --H 2 --prof-rounds 0 --e2e-steps 1 --no-cpu-baseline"
+timeout 1800 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:adamw_k|grouped_gemm_2cta_kernel|router_fwd_k|normed_grad_k|norm_router_partial_k|combine_bwd_k|combine_fwd_k|permute_tma_k|router_scalar_bwd_k" -s 140 -c 44 -o $O/full $CMD > $O/ncu_full.log 2>&1; echo full rc=$?
+python scripts/ncu_summary.py full $O/full.ncu-rep $O/ncu_full_$C.txt "$CMD"
+find $O -name '*.ncu-rep' -size +40M -delete

@@ -66,6 +66,13 @@ def launches(csv_path, out_txt, out_json, cfg_name, cmd):
     cb = [i for i, e in enumerate(step) if "combine_bwd_k" in e["name"]]
     if hf and cb:
         head = set(range(hf[0], cb[0]))
+    # ... and the router weight-gradient GEMM (the first grouped GEMM after each
+    # norm_router_finish_k, above 16 experts)
+    for i, e in enumerate(step):
+        if "norm_router_finish_k" in e["name"]:
+            j = next((j for j in range(i + 1, len(step)) if "grouped_gemm" in step[j]["name"]), None)
+            if j is not None and "EpiStoreF32<128>, 1, 1" in step[j]["name"]:
+                head.add(j)
     gem = [e for i, e in enumerate(step) if "grouped_gemm" in e["name"] and i not in head]
     summary = {
         "source": f"{out_txt} ({cmd})",
@@ -116,8 +123,9 @@ def full(rep, out_txt, cmd):
             if m in d:
                 out.append("   %-64s %14s %s" % (m, d[m], u.get(m, "")))
                 if m.startswith("dram__bytes"):
+                    unit = u.get(m, "Mbyte").strip().strip('"')
                     tb += float(d[m].replace(",", "")) * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1,
-                                                          "Gbyte": 1e3}.get(u.get(m, "Mbyte"), 1)
+                                                          "Gbyte": 1e3}.get(unit, 1)
         out.append("   traffic_MB %.1f" % tb)
         out.append("")
     open(out_txt, "w").write("\n".join(out) + "\n")
