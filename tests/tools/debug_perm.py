@@ -1,6 +1,6 @@
-"""Reproduce the intermittent permutation mismatch of spes_kernel_router (debug aid)."""
+"""Reproduce the (now fixed, profiles/r02/flake_fix) intermittent permutation mismatch of spes_kernel_router."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import oracle
 import paper_2602_11543_b200 as spes
