@@ -376,6 +376,28 @@ def test_router_gradient_paths(gpu, monkeypatch, shape):
     assert bitexact(grads["0"][keep], grads["1"][keep]), "non-router gradients differ by path"
 
 
+def test_dswiglu_epilogue_variants_identical_bits(gpu, monkeypatch):
+    """Every dSwiGLU epilogue (SPES_DSWIGLU_TMA: 0 direct loads, 1 TMA-staged 64-column
+    pieces, 3 / 4 TMA-staged 32-column pieces written back in place by TMA) computes the same
+    per-element products: identical gradients, bit for bit (cfg2 shapes: pair tiles)."""
+    cfg = model_cfg(**CFG2)
+    params = oracle.random_params(cfg, 71)
+    tokens = oracle.random_tokens(cfg, 1, 384, 72)[0]
+    grads = {}
+    for v in ("0", "1", "3", "4"):
+        monkeypatch.setenv("SPES_DSWIGLU_TMA", v)
+        node = spes.Node(cfg, 0, 1, 0)
+        node.set_ownership([[0, 1, 2, 3]])
+        node.load_params(params)
+        node.set_fused_optimizer(False)
+        node.round_begin()
+        node.local_step(tokens, adamw_cfg(lr=1e-3))
+        grads[v] = node.read_grads()
+        node.close()
+    for v in ("1", "3", "4"):
+        assert bitexact(grads[v], grads["0"]), f"variant {v} differs from the direct epilogue"
+
+
 def test_local_round_and_errors(gpu):
     cfg = model_cfg(**CFG1)
     params = oracle.random_params(cfg, 3)
