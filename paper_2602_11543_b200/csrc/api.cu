@@ -226,11 +226,12 @@ struct spes_ctx {
     // identical bits; the fused epilogue is issue/latency-bound at ~3.7 TB/s with the 8
     // epilogue warps that fit next to the MMA ring, so it does not beat the separate pass yet.
     bool fused_opt = false;
-    // dSwiGLU factor rows staged by TMA (SPES_DSWIGLU_TMA=0: off; default variant 4: 32-column
-    // pieces written back in place, 3 buffers, 5 operand stages; dH cfg2 641 -> 831 TFLOP/s,
-    // cfg5 1112 -> 1182). Variants 1 / 2 (64-column pieces through the transpose slots) cost
-    // operand stages and are only used for d <= 2048
-    bool staged_dswiglu = true;
+    // dSwiGLU epilogue of this context (SPES_DSWIGLU_TMA at creation; gemm_dswiglu): 4 =
+    // 32-column pieces staged by TMA and written back in place, 3 buffers, 5 operand stages
+    // (dH cfg2 641 -> 831 TFLOP/s, cfg5 1112 -> 1182); 0 direct loads; 1 / 2 64-column pieces
+    // through the transpose slots (cost operand stages; only used for d <= 2048); 3 in place
+    // with 2 buffers
+    int dswiglu_variant = 4;
     // inner optimizer (LocalRoundConfig::inner, trainer.hpp:116-121): AdamW, or SGD
     // (theta -= lr * g, no moments; always the standalone pass)
     bool inner_sgd = false;
@@ -937,8 +938,8 @@ void forward_backward(spes_ctx* c) {
             PROF("gemm_bwd_dh");
             spes_k::gemm_dswiglu(bn_for(f), c->a_dyw, Y.b_w2, Y.groups + 2 * M, M, Y.tiles + 2,
                                  c->max_tiles[2], Y.gu, f,
-                                 c->staged_dswiglu && d <= 2048 ? c->gu_maps + l : nullptr,
-                                 c->staged_dswiglu ? c->dsw_maps + 2 * l : nullptr, st);
+                                 d <= 2048 ? c->gu_maps + l : nullptr, c->dsw_maps + 2 * l,
+                                 c->dswiglu_variant, st);
         }
         if (unfused_dw) {
             {
@@ -1280,10 +1281,8 @@ spes_status spes_create(const spes_model_cfg* cfg, int32_t node, int32_t n_nodes
         // (cfg2 3.2 -> 4.1 ms)
         c->router_tc = c->lay.M > 16;
         if (const char* e = std::getenv("SPES_ROUTER_TC")) c->router_tc = std::atoi(e) != 0;
-        if (const char* e = std::getenv("SPES_DSWIGLU_TMA")) {  // 0 off, else the variant (1-4)
-            c->staged_dswiglu = std::atoi(e) != 0;
-            if (c->staged_dswiglu) spes_k::gemm_dswiglu_buffers(std::atoi(e));
-        }
+        if (const char* e = std::getenv("SPES_DSWIGLU_TMA"))  // 0 direct, else the variant (1-4)
+            c->dswiglu_variant = std::max(0, std::min(4, std::atoi(e)));
         if (const char* e = std::getenv("SPES_ADAM_BG")) {  // "threads,tiles,per_sm,u"
             int th = 64, ti = 16, ps = 0, u = 2;
             if (std::sscanf(e, "%d,%d,%d,%d", &th, &ti, &ps, &u) >= 1 && th >= 32 && th <= 256 &&

@@ -711,23 +711,21 @@ void gemm_head_ce(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g
                              EpiHeadCE{targets, T, g_s2, g_ssum, dlog, diff, lse}, s);
 }
 
-// 1 / 2: 64-column pieces through the transpose slots with 1 / 2 staging buffers;
-// 3 / 4: 32-column pieces written back in place, 2 / 3 buffers
-int g_dswiglu_bufs = 4;
-void gemm_dswiglu_buffers(int n) { g_dswiglu_bufs = n >= 1 && n <= 4 ? n : 4; }
-
+// variant 1 / 2: 64-column pieces through the transpose slots with 1 / 2 staging buffers;
+// 3 / 4: 32-column pieces written back in place, 2 / 3 buffers (the maps decide which apply)
 void gemm_dswiglu(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
                   const int32_t* tiles, int max_tiles, const bf16* gu, int64_t f,
-                  const CUtensorMap* gu_map, const CUtensorMap* inplace_maps, cudaStream_t s) {
-    if (bn == 256 && g_gemm_pairs && inplace_maps && g_dswiglu_bufs >= 3) {
-        if (g_dswiglu_bufs == 3)
+                  const CUtensorMap* gu_map, const CUtensorMap* inplace_maps, int variant,
+                  cudaStream_t s) {
+    if (bn == 256 && g_gemm_pairs && inplace_maps && variant >= 3) {
+        if (variant == 3)
             launch<256, false, false>(a, b, g, ng, tiles, max_tiles,
                                       EpiDSwiGLUInPlace<2>{inplace_maps, inplace_maps + 1}, s);
         else
             launch<256, false, false>(a, b, g, ng, tiles, max_tiles,
                                       EpiDSwiGLUInPlace<3>{inplace_maps, inplace_maps + 1}, s);
-    } else if (bn == 256 && g_gemm_pairs && gu_map) {  // factor rows staged by TMA
-        if (g_dswiglu_bufs == 2)
+    } else if (bn == 256 && g_gemm_pairs && gu_map && variant >= 1) {  // staged by TMA
+        if (variant == 2)
             launch<256, false, false>(a, b, g, ng, tiles, max_tiles, EpiDSwiGLUStaged<2>{gu_map}, s);
         else
             launch<256, false, false>(a, b, g, ng, tiles, max_tiles, EpiDSwiGLUStaged<1>{gu_map}, s);

@@ -239,16 +239,15 @@ enum class GemmMajor { KK, KMN, MNMN };
 void gemm_store_f32(int bn, GemmMajor mj, const CUtensorMap& a, const CUtensorMap& b,
                     const GemmGroup* g, int ng, const int32_t* tiles, int max_tiles,
                     cudaStream_t s);
-// variant of the TMA-staged dSwiGLU epilogue: 1 / 2 = 64-column pieces with 1 / 2 staging
-// buffers, 3 / 4 = 32-column pieces written back in place with 2 / 3 buffers (default 4)
-void gemm_dswiglu_buffers(int n);
-// gu_map (optional, device memory): the GU buffer as {64 x 128}-box tensor map; with it the
-// pair kernel stages the factor rows by TMA (EpiDSwiGLUStaged). inplace_maps (optional,
-// device memory, two maps): GU as {32 x 128} and dGU as {32 x 32} boxes, 64B swizzle
-// (EpiDSwiGLUInPlace, preferred when given)
+// dSwiGLU epilogue variant: 0 direct loads; 1 / 2 TMA-staged 64-column pieces through the
+// transpose slots with 1 / 2 buffers (needs gu_map: the GU buffer as {64 x 128}-box tensor
+// map in device memory); 3 / 4 TMA-staged 32-column pieces written back in place by TMA with
+// 2 / 3 buffers (needs inplace_maps: GU as {32 x 128} and dGU as {32 x 32} boxes, 64B
+// swizzle, device memory). Pair tiles (BN = 256) only; otherwise the direct epilogue.
 void gemm_dswiglu(int bn, const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,
                   const int32_t* tiles, int max_tiles, const bf16* gu, int64_t f,
-                  const CUtensorMap* gu_map, const CUtensorMap* inplace_maps, cudaStream_t s);
+                  const CUtensorMap* gu_map, const CUtensorMap* inplace_maps, int variant,
+                  cudaStream_t s);
 // head forward (V == 256) with softmax-CE fused into the epilogue: writes bf16 dlogits
 // ([T_pad x 256], padding rows zero), the per-token CE term and lse (head_ce semantics)
 void gemm_head_ce(const CUtensorMap& a, const CUtensorMap& b, const GemmGroup* g, int ng,

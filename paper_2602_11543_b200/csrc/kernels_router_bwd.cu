@@ -237,11 +237,8 @@ void normed_grad(const float* h, const int32_t* hrow, const float* gain, const f
     // all k expert pieces in flight (64 registers, 4 blocks per SM) for k > 4: cfg5 router
     // backward 218 -> 210 ms per round; at k = 2 (cfg2) the 2-deep loop is faster (4.4 vs
     // 4.7 ms). SPES_NG_ALLK=0/1 overrides.
-    static const int allk_env = [] {
-        const char* e = std::getenv("SPES_NG_ALLK");
-        return e ? std::atoi(e) : -1;
-    }();
-    const bool allk = allk_env >= 0 ? allk_env != 0 : k > 4;
+    const char* allk_env = std::getenv("SPES_NG_ALLK");  // read per launch (graph-captured)
+    const bool allk = allk_env ? std::atoi(allk_env) != 0 : k > 4;
     auto f = M <= 8    ? (allk ? normed_grad_k<8, true> : normed_grad_k<8, false>)
              : M <= 16 ? (allk ? normed_grad_k<16, true> : normed_grad_k<16, false>)
              : M <= 32 ? (allk ? normed_grad_k<32, true> : normed_grad_k<32, false>)

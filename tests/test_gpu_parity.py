@@ -398,6 +398,26 @@ def test_dswiglu_epilogue_variants_identical_bits(gpu, monkeypatch):
         assert bitexact(grads[v], grads["0"]), f"variant {v} differs from the direct epilogue"
 
 
+def test_normed_grad_load_depth_identical_bits(gpu, monkeypatch):
+    """normed_grad_k with all k expert pieces in flight (SPES_NG_ALLK=1, the default for
+    k > 4) and with the 2-deep loop sum in the same descending order: identical gradients."""
+    cfg = model_cfg(**CFG4)
+    params = oracle.random_params(cfg, 73)
+    tokens = oracle.random_tokens(cfg, 1, 256, 74)[0]
+    grads = {}
+    for v in ("0", "1"):
+        monkeypatch.setenv("SPES_NG_ALLK", v)
+        node = spes.Node(cfg, 0, 1, 0)
+        node.set_ownership([list(range(16))])
+        node.load_params(params)
+        node.set_fused_optimizer(False)
+        node.round_begin()
+        node.local_step(tokens, adamw_cfg(lr=1e-3))
+        grads[v] = node.read_grads()
+        node.close()
+    assert bitexact(grads["0"], grads["1"])
+
+
 def test_local_round_and_errors(gpu):
     cfg = model_cfg(**CFG1)
     params = oracle.random_params(cfg, 3)
