@@ -1,8 +1,7 @@
-O=gpurun_out/m26
+O=gpurun_out/m31
 mkdir -p $O
-for rep in 1 2 3; do for v in 0 1; do
-SPES_ADAM_TAIL_FG=$v timeout 600 python bench.py --steps 3 --warmup 3 --e2e-steps 0 --no-cpu-baseline --prof-rounds 0 > $O/bench_cfg5_t${v}_$rep.json 2> $O/bench_cfg5_t${v}_$rep.err
-python -c "
-import json;d=json.load(open('$O/bench_cfg5_t${v}_$rep.json'));print('cfg5 tail_fg=$v rep$rep',round(d['value']),round(d['ms_per_step'],2),d['clocks']['sm_mhz'])"
-done; done
-SPES_ADAM_TAIL_FG=1 timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -p no:cacheprovider -k "overlap or local_step_cfg1" 2>&1 | tail -1
+C=cfg5
+CMD="python bench.py --config $C --steps 1 --warmup 2 --H 2 --prof-rounds 0 --e2e-steps 1 --no-cpu-baseline"
+timeout 1500 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:EpiGradW1|normed_grad_k|norm_router_partial_k|EpiStoreF32<128>|EpiDSwiGLUInPlace" -s 20 -c 10 -o $O/full $CMD > $O/ncu_full.log 2>&1; echo full rc=$?
+python scripts/ncu_summary.py full $O/full.ncu-rep $O/ncu_full_cfg5_bwd.txt "$CMD"
+find $O -name '*.ncu-rep' -size +40M -delete
