@@ -1343,6 +1343,8 @@ void spes_destroy(spes_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->side) cudaStreamSynchronize(c->side);  // normally joined into stream at step end
+    if (spes_k::g_launch_counter == &c->launches) spes_k::g_launch_counter = nullptr;
     for (float* p : c->peer_params)
         if (p) cudaIpcCloseMemHandle(p);
     for (size_t n = 0; n < c->peer_flags.size(); ++n)
